@@ -1,0 +1,291 @@
+#!/usr/bin/env python
+"""Benchmark of the docking hot path (BASELINE.json metric: ligands/sec docked, device-timed,
+at 1/2/4/8 B200, and the fraction of the instruction roofline).
+
+Workload (per rank, weak scaling): BASELINE config 3 — mixed synthetic ligands (heavy atoms
+U{8..40}, rotatable bonds U{0..min(20, heavy-2)}, seed 3, each rank its own contiguous shard of
+the global index space as in config 5) docked against the shared synthetic pocket (P=200, 57^3
+class grid, spacing 0.5 Å) with the default DockConfig, batched kernel family.  A "step" docks
+the rank's whole shard: alignment kernel + optimisation/select/rescore kernel.
+
+  value  = total ligands / step time, inputs resident in HBM (kernel-only, CUDA events on the
+           library's stream, max over ranks)
+  e2e    = the same through the public C ABI call ds_dock with host buffers (pinned staging,
+           H2D, kernels, D2H of the result records + best poses), host wall-clock, max over ranks
+
+`--impl reference` times the CPU oracle (the reference's algorithm restated in C, all host
+threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# algorithmic thread-instruction costs per unit
+C_ALIGN, C_ROT, C_PAIR, C_SCORE, C_RESC = 24, 20, 8, 14, 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ligands", type=int, default=200_000, help="ligands per rank per step")
+    ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=1024, help="ligands in the CPU-baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def work_model(batch, res, cfg):
+    """Algorithmic warp-instructions per ligand from the device's own counters."""
+    A = np.diff(batch.atom_off).astype(np.float64)
+    F = np.diff(batch.frag_off).astype(np.float64)
+    N = cfg.restarts_n
+    n_rot = (360 // cfg.alignment_step_deg) ** 2
+    u_align = N * n_rot * A
+    # torsion rotations: sum over fragments of |M| x (n_t - 1) x N
+    pop = np.array([bin(int(w)).count("1") for w in batch.frag_mask.reshape(-1)], np.float64).reshape(-1, 5).sum(1)
+    msum = np.add.reduceat(pop, batch.frag_off[:-1]) if len(pop) else np.zeros(batch.n)
+    msum = np.where(F > 0, msum, 0.0)
+    n_t = 360 // cfg.torsion_step_deg
+    u_rot = N * (n_t - 1) * msum
+    u_pair = res["bump_checks"].astype(np.float64)
+    u_score = N * n_t * msum  # upper bound: clean angles score only the moving atoms (base hoisted)
+    u_resc = res["n_kept"].astype(np.float64) * A * 200.0
+    w_align = C_ALIGN * u_align / 32.0
+    w_total = (C_ALIGN * u_align + C_ROT * u_rot + C_PAIR * u_pair + C_SCORE * u_score + C_RESC * u_resc) / 32.0
+    return float(w_align.sum()), float(w_total.sum())
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle.oracle as orc
+    from paper_2209_05069_b200 import io, model
+    from paper_2209_05069_b200.native import InteractionTable
+    cfg = model.DockConfig()
+    pocket = io.synthetic_pocket()
+    table = InteractionTable.default()
+    threads = os.cpu_count() or 1
+    n = args.cpu_sample
+    times = []
+    for step in range(args.warmup + args.steps):
+        batch = io.generate_mixed_batch(n, seed=args.seed, first_index=step * n)
+        t0 = time.perf_counter()
+        orc.dock_batch(batch, pocket, table, cfg, seed=0, threads=threads)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    v = n / float(np.mean(times))
+    line = {"impl": "reference", "metric": "ligands/sec docked", "value": v, "unit": "ligands/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * float(np.mean(times)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+int32", "data": "synthetic",
+            "config": {"workload": "config3 mixed ligands (heavy U{8..40}, F U{0..20}), synthetic pocket 200 atoms, "
+                                   "DockConfig defaults", "ligands_per_step": n},
+            "cpu_baseline": {"value": v, "unit": "ligands/s", "cores": threads, "kind": "port",
+                             "sample": f"{n} ligands of the config-3 distribution per step, oracle/dock_oracle.c, "
+                                       f"OpenMP {threads} threads"},
+            "e2e": {"value": v, "unit": "ligands/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2209_05069_b200 import io, model, native
+    from paper_2209_05069_b200.native import InteractionTable, ResidentBatch, pack
+
+    cfg = model.DockConfig()
+    pocket = io.synthetic_pocket()
+    table = InteractionTable.default()
+    n = args.ligands
+    batch = io.generate_mixed_batch(n, seed=args.seed, first_index=rank * n)
+    packed = pack(batch)
+    ctx = native.Context(local)
+    dp = ctx.pocket(pocket, table)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(local)
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- kernel-only (resident inputs) ----
+    rb = ResidentBatch(ctx, packed)
+    for _ in range(args.warmup):
+        rb.dock(dp, cfg, seed=0)
+    barrier()
+    step_ms, align_ms, opt_ms = [], [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            st = rb.dock(dp, cfg, seed=0)
+            step_ms.append(st.total_ms)
+            align_ms.append(st.align_ms)
+            opt_ms.append(st.optimize_ms)
+    barrier()
+    res = rb.download()
+    ms = max_over_ranks(float(np.mean(step_ms)))
+    value = n * world / (ms / 1000.0)
+    status_ok = float(np.mean(res["status"] == 0))
+
+    # ---- end to end through ds_dock with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(1):
+            out = ctx.dock(dp, packed, cfg, 0, native.FAMILY_BATCHED, coords=True)
+        barrier()
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for _ in range(args.steps):
+            out = ctx.dock(dp, packed, cfg, 0, native.FAMILY_BATCHED, coords=True)
+            h2d, d2h = out.stats.h2d_bytes, out.stats.d2h_bytes
+        barrier()
+        dt = max_over_ranks((time.perf_counter() - t0) / args.steps)
+        e2e = {"value": n * world / dt, "unit": "ligands/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1000 * dt}
+
+    # ---- roofline of the dominant kernel (instruction issue) ----
+    peaks = measured_peaks()
+    clocks = clk.summary()
+    f_mhz = peaks.get("sm_max_mhz", 1965.0)
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+    peak_winst = n_sm * 4 * f_mhz * 1e6
+    w_align, w_total = work_model(batch, res, cfg)
+    a_ms, o_ms = float(np.mean(align_ms)), float(np.mean(opt_ms))
+    dom_is_align = a_ms >= o_ms
+    achieved = (w_align / (a_ms / 1e3)) if dom_is_align else ((w_total - w_align) / (o_ms / 1e3))
+    roof = {"bound": "issue", "kernel": "k_align_batched" if dom_is_align else "k_optimize_batched",
+            "achieved": achieved / 1e9, "peak": peak_winst / 1e9, "unit": "Gwarp-inst/s",
+            "frac": achieved / peak_winst, "traffic": None,
+            "note": f"algorithmic warp-instructions (SURVEY §8d costs) / CUDA-event launch time; peak = {n_sm} SM x 4 "
+                    f"issue/clk x {f_mhz} MHz (MEASURED_PEAKS.json sm_max_mhz)"}
+    whole = {"achieved": (w_total / (ms / 1e3)) / 1e9, "frac": (w_total / (ms / 1e3)) / peak_winst,
+             "unit": "Gwarp-inst/s"}
+    in_bytes = int(packed.atom_xyzt.nbytes + packed.frag_desc.nbytes + packed.atom_off.nbytes * 2 + packed.id_hash.nbytes)
+    hbm = {"bound": "hbm", "achieved": in_bytes / (ms / 1e3) / 1e9, "peak": peaks.get("hbm_gbs", 6535.4),
+           "unit": "GB/s", "frac": in_bytes / (ms / 1e3) / 1e9 / peaks.get("hbm_gbs", 6535.4), "traffic": None}
+
+    # ---- CPU baseline (oracle, bounded sample, rank 0 at N=1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle.oracle as orc
+        sample = batch.subset(range(0, min(args.cpu_sample, n)))
+        threads = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        orc.dock_batch(sample, pocket, table, cfg, seed=0, threads=threads)
+        dt = time.perf_counter() - t0
+        cpu = {"value": sample.n / dt, "unit": "ligands/s", "cores": threads, "kind": "port",
+               "sample": f"first {sample.n} ligands of this workload, oracle/dock_oracle.c (OpenMP, {threads} threads)"}
+
+    if rank == 0:
+        line = {"metric": "ligands/sec docked", "value": value, "unit": "ligands/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32+int32", "data": "synthetic",
+                "config": {"workload": "config3 mixed ligands (heavy U{8..40}, F U{0..20}) per rank, synthetic pocket "
+                                       "(200 atoms, spacing 0.5 A), DockConfig defaults, batched family",
+                           "ligands_per_rank": n, "grid_dims": list(pocket.grid_dims),
+                           "l2": "inputs larger than L2 (per-step ligand data > 126 MB at 200k ligands)",
+                           "parallelism": f"dp{world} (contiguous ligand shards, no collective)"},
+                "e2e": e2e, "roofline": roof, "roofline_whole_step": whole, "roofline_hbm": hbm,
+                "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": 2 * args.steps,
+                "kernel_ms": {"align": a_ms, "optimize": o_ms}, "status_ok_frac": status_ok}
+        print(json.dumps(line), flush=True)
+    rb.close()
+    dp.close()
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

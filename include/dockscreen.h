@@ -1,0 +1,242 @@
+/*
+ * dockscreen.h — C ABI of libdockscreen.so, the B200 (sm_100a) docking hot path.
+ *
+ * This ABI is the drop-in for the reference package's native slot
+ * `dockscreen.kernels._core` (pkg/setup.py:10-18), whose Cython source is absent
+ * from the reference (pkg/setup.py:13 names src/dockscreen/kernels/_core.pyx,
+ * which does not ship).  By SPEC the slot carries the L2 kernels of Alg. 1
+ * that `docking.dock_ligand` and the two
+ * engines call.  On B200 the slot is coarser: one call docks
+ * a whole packed ligand batch (SPEC.md:277-285 per ligand) with either kernel
+ * family of the paper (latency: PAPER.md:287-348, batched: PAPER.md:349-426),
+ * and the per-op entry points (ds_op_*) expose the L2 ops themselves.
+ *
+ * Plain C types only: pointers + sizes, caller-owned host buffers,
+ * ctx-owned device memory.  Every function returns DS_OK (0) or a negative
+ * DS_ERR_* code; the message of the last failure on the calling thread is
+ * available from ds_last_error().  Per-ligand outcomes (NoValidPose,
+ * DegenerateAxis: SPEC.md:149, 271, 281) are reported in ds_result.status and
+ * never abort a batch.
+ *
+ * Numeric recipe: DESIGN.md §3 ("pins").  All scores produced here are
+ * bit-identical to oracle/ (the CPU restatement) on the same inputs.
+ */
+#ifndef DOCKSCREEN_H
+#define DOCKSCREEN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DS_ABI_VERSION 1
+
+#define DS_MAX_ATOMS 160      /* SPEC.md:44 (largest bucket bound) */
+#define DS_MASK_WORDS 5       /* 160 bits of moving mask per fragment           */
+#define DS_FRAG_WORDS 8       /* words per packed fragment record (32 B)        */
+#define DS_N_TYPES 16         /* element codes 0..15, 0 = hydrogen */
+#define DS_MAX_BINS 8
+#define DS_MAX_RESTARTS 32
+#define DS_TORSION_NONE 255   /* fragment whose angles all bumped (kept as is)  */
+
+/* return codes (SPEC error names in comments) */
+enum {
+  DS_OK = 0,
+  DS_ERR_INVALID_ARG = -1,
+  DS_ERR_TOO_MANY_ATOMS = -2,      /* TooManyAtoms */
+  DS_ERR_MALFORMED_FRAGMENT = -3,  /* MalformedFragment */
+  DS_ERR_INDEX_OUT_OF_RANGE = -4,  /* IndexOutOfRange */
+  DS_ERR_DEGENERATE_AXIS = -5,     /* DegenerateAxis */
+  DS_ERR_EMPTY_POCKET = -6,        /* EmptyPocket */
+  DS_ERR_INFEASIBLE_SHAPE = -7,    /* InfeasibleShape */
+  DS_ERR_UNSUPPORTED = -8,
+  DS_ERR_CUDA = -9,
+  DS_ERR_NO_DEVICE = -10,
+  DS_ERR_OOM = -11
+};
+
+/* per-ligand status in ds_result.status */
+enum {
+  DS_STATUS_OK = 0,
+  DS_STATUS_NO_VALID_POSE = 1,     /* NoValidPose */
+  DS_STATUS_DEGENERATE_AXIS = 2,   /* DegenerateAxis      */
+  DS_STATUS_NOT_RUN = 3
+};
+
+/* kernel families (PAPER.md:287 latency, PAPER.md:349 batched) */
+enum { DS_FAMILY_BATCHED = 0, DS_FAMILY_LATENCY = 1 };
+
+typedef struct ds_ctx ds_ctx;
+typedef struct ds_pocket ds_pocket;
+typedef struct ds_dev_batch ds_dev_batch;
+
+/* Pocket + InteractionTable.  Grid values x-fastest
+ * (SPEC.md:472).  Pocket atoms are in Å, same frame as the grid. */
+typedef struct ds_pocket_desc {
+  float origin[3];
+  float spacing;
+  int32_t dims[3];
+  int32_t n_atoms;
+  const int32_t *values;      /* dims[0]*dims[1]*dims[2] */
+  const float *atom_xyz;      /* n_atoms*3 */
+  const uint8_t *atom_type;   /* n_atoms   */
+  const float *table;         /* 16*16, symmetric */
+  int32_t n_bins;             /* 1..DS_MAX_BINS */
+  const float *bin_ub;        /* ascending upper bounds (Å); last = cutoff */
+  const float *bin_mult;
+} ds_pocket_desc;
+
+/* DockConfig + the dock seed. */
+typedef struct ds_dock_config {
+  int32_t restarts_n;          /* N, default 8  */
+  int32_t rescore_top_k;       /* K, default 4  */
+  int32_t alignment_step_deg;  /* default 12    */
+  int32_t torsion_step_deg;    /* default 36    */
+  float bump_distance;         /* Å, default 0.8 */
+  float similarity_rmsd;       /* Å, default 1.0 */
+  float rescore_cutoff;        /* Å, default 8.0 (must equal the last bin_ub) */
+  int32_t early_exit;          /* default 1 */
+  int64_t seed;                /* dock seed, default 0 */
+} ds_dock_config;
+
+/* Packed ligand batch (SoA, CSR over atoms and fragments).
+ *  atom_xyzt[4*a+0..2] = centred coordinates d = p - c0 (f32, Å), c0 = f32(f64 mean)
+ *  atom_xyzt[4*a+3]    = element code as float (0 = H)
+ *  frag_desc[8*f+0..4] = moving-mask bitset over the ligand's atoms
+ *  frag_desc[8*f+5]    = axis_begin | axis_end << 8
+ *  frag_desc[8*f+6..7] = reserved (0)
+ *  id_hash[l]          = FNV-1a-64 of the ligand id bytes (ds_ligand_id_hash)
+ *  centroid[3*l]       = c0 (Å) — only used to map output poses back; may be NULL */
+typedef struct ds_batch_desc {
+  int32_t n_ligands;
+  int32_t reserved;
+  const int32_t *atom_off;     /* n+1 */
+  const float *atom_xyzt;      /* atom_off[n]*4 */
+  const int32_t *frag_off;     /* n+1 */
+  const uint32_t *frag_desc;   /* frag_off[n]*8 */
+  const uint64_t *id_hash;     /* n */
+} ds_batch_desc;
+
+/* One result record per ligand (32 B). chem = chem_fx * 2^-24 (DESIGN.md §3 P11). */
+typedef struct ds_result {
+  int32_t status;
+  int32_t geom_score;          /* best pose geometric score */
+  int64_t chem_fx;             /* best pose chemical score, fixed point 2^-24 */
+  uint8_t best_restart;
+  uint8_t best_ax;             /* alignment indices of the best restart (angle = idx*step) */
+  uint8_t best_ay;
+  uint8_t n_kept;              /* poses kept by select_poses */
+  uint32_t poses_scored;
+  uint32_t bump_checks;        /* pair evaluations performed (DESIGN.md §3 P14) */
+  uint32_t bump_early_exits;
+} ds_result;
+
+/* Per (ligand, restart) record, optional. */
+typedef struct ds_restart_record {
+  int32_t align_score;         /* grid score of the aligned pose */
+  int32_t final_geom;          /* grid score after optimize_pose */
+  uint8_t ax, ay, valid, kept; /* kept: 1 + keep rank, 0 = not kept */
+  int32_t reserved;
+} ds_restart_record;
+
+/* Output buffers (caller-owned, host). Everything but `results` may be NULL. */
+typedef struct ds_outputs {
+  ds_result *results;              /* n */
+  float *best_coords;              /* atom_off[n]*3, best pose in Å (pocket frame) */
+  uint8_t *best_torsion;           /* frag_off[n], torsion index per fragment of the best pose */
+  ds_restart_record *restarts;     /* n*N */
+  uint8_t *restart_torsion;        /* frag_off[n]*N, [(frag_off[l]+f)*N + r] */
+} ds_outputs;
+
+/* Timing of the last dock call (device-timed with CUDA events on the ctx stream). */
+typedef struct ds_stats {
+  float total_ms;                  /* first H2D .. last D2H (or kernels only for resident) */
+  float align_ms;                  /* alignment kernel(s) */
+  float optimize_ms;               /* torsion + select + rescore kernel(s) */
+  int32_t launches;                /* kernels launched by the call */
+  int32_t reserved;
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+} ds_stats;
+
+/* ---- library / context -------------------------------------------------- */
+int ds_abi_version(void);
+const char *ds_last_error(void);
+int ds_device_count(int *n);
+/* A ctx = one CUDA stream + worst-case workspaces allocated once (PAPER.md:310-313,
+ * SPEC.md:394,399).  One ctx per host thread. */
+int ds_create(int device, ds_ctx **out);
+void ds_destroy(ds_ctx *ctx);
+int ds_ctx_alloc_count(const ds_ctx *ctx, int64_t *count);
+/* Opaque cudaStream_t of the ctx (for external event timing). */
+void *ds_ctx_stream(ds_ctx *ctx);
+int ds_synchronize(ds_ctx *ctx);
+
+/* ---- pocket ------------------------------------------------------------- */
+int ds_pocket_create(ds_ctx *ctx, const ds_pocket_desc *desc, ds_pocket **out);
+void ds_pocket_destroy(ds_pocket *pocket);
+
+/* ---- docking (SPEC.md:277 per ligand; engines SPEC.md:391, 401) --------- */
+/* Synchronous: H2D of the batch, kernels, D2H of the outputs. */
+int ds_dock(ds_ctx *ctx, const ds_pocket *pocket, const ds_batch_desc *batch,
+            const ds_dock_config *cfg, int family, const ds_outputs *out, ds_stats *stats);
+/* Device-resident variant used for kernel-only timing. */
+int ds_batch_upload(ds_ctx *ctx, const ds_batch_desc *batch, ds_dev_batch **out);
+int ds_dock_resident(ds_ctx *ctx, const ds_pocket *pocket, ds_dev_batch *batch,
+                     const ds_dock_config *cfg, int family, ds_stats *stats);
+int ds_batch_download(ds_ctx *ctx, ds_dev_batch *batch, const ds_outputs *out);
+void ds_batch_destroy(ds_dev_batch *batch);
+/* Ligands one batched launch keeps resident on this device for atom range
+ * `range_idx` (0..4) — the B200 analogue of the paper's occupancy-derived
+ * capacity. */
+int ds_query_capacity(ds_ctx *ctx, int range_idx, int *ligands);
+
+/* ---- L2 ops of the native slot, batched on device ------ */
+/* grid_score of n_poses poses of n_atoms atoms each, coordinates in Å. */
+int ds_op_grid_score(ds_ctx *ctx, const ds_pocket *pocket, const float *coords,
+                     int n_atoms, int n_poses, int32_t *out_scores);
+/* rescore of n_poses poses; chem in fixed point 2^-24. */
+int ds_op_rescore(ds_ctx *ctx, const ds_pocket *pocket, const float *coords,
+                  const uint8_t *types, int n_atoms, int n_poses, float cutoff,
+                  int64_t *out_chem_fx);
+
+/* ---- host-side helpers (input makers and packing; not on the timed path) - */
+/* FNV-1a-64 of the id bytes (keys the starting-pose PRNG, DESIGN.md §3 P5). */
+uint64_t ds_ligand_id_hash(const char *id, size_t len);
+/* Canonical id of generated ligand `index`: "lig_<seed>_<index>"; returns length. */
+int ds_generated_id(int64_t seed, int64_t index, char *buf, size_t cap);
+/* Per-ligand (heavy, frags) shapes of the mixed datasets (BASELINE configs 3, 5):
+ * heavy ~ U{heavy_min..heavy_max}, frags ~ U{0..min(frag_max, heavy-2)}. */
+int ds_mixed_shapes(int64_t seed, int64_t first_index, int32_t count, int32_t heavy_min,
+                    int32_t heavy_max, int32_t frag_max, int32_t *shapes /* 2*count */);
+/* SPEC.md:443 generate_dataset for ligands first_index .. first_index+count-1.
+ * shapes[2i], shapes[2i+1] = (heavy atoms, fragments).  Pass 1 (atom_xyz == NULL)
+ * fills the three CSR offset arrays (count+1 each); pass 2 fills the payload.
+ * Coordinates are absolute (Å).  Bonds/axes are ligand-local atom indices. */
+int ds_generate_ligands(int64_t seed, int64_t first_index, int32_t count, const int32_t *shapes,
+                        int32_t *atom_off, int32_t *bond_off, int32_t *frag_off,
+                        float *atom_xyz, uint8_t *atom_type, int32_t *bonds,
+                        int32_t *frag_axis, uint32_t *frag_mask /* 5 words per fragment */);
+/* Pack ligands into the ds_batch_desc layout (validating SPEC.md:81-89 except the
+ * bond-cut rule, which needs bonds).  id_hash is an input when ids == NULL. On an
+ * invalid ligand returns its DS_ERR_* code and sets *bad_index. */
+int ds_pack_ligands(int32_t count, const int32_t *atom_off, const float *atom_xyz,
+                    const uint8_t *atom_type, const int32_t *frag_off, const int32_t *frag_axis,
+                    const uint32_t *frag_mask, const char *ids, const int64_t *id_off,
+                    float *atom_xyzt, uint32_t *frag_desc, uint64_t *id_hash, float *centroid,
+                    int32_t *bad_index);
+/* Synthetic pocket atoms: uniform in the shell rmin <= r <= rmax, types 1..15. */
+int ds_generate_pocket_atoms(int64_t seed, int32_t n, float rmin, float rmax,
+                             float *atom_xyz, uint8_t *atom_type);
+/* SPEC.md:453 build_pocket grid (x-fastest).  values == NULL: size query. */
+int ds_build_pocket_grid(const float *atom_xyz, int32_t n_atoms, float spacing, float padding,
+                         float origin[3], int32_t dims[3], int32_t *values);
+/* Seeded symmetric 16x16 interaction table in [-1, 1]. */
+int ds_default_table(int64_t seed, float *table /* 256 */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DOCKSCREEN_H */

@@ -1,0 +1,657 @@
+// C ABI of libdockscreen (include/dockscreen.h): contexts, pocket upload, batch docking.
+//
+// The context is the paper's latency-implementation unit: one host thread,
+// one CUDA stream, worst-case device workspace allocated once and reused.  Batched docking
+// reuses the same context; its buffers grow geometrically with the batch.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ds_kernels.cuh"
+
+namespace ds {
+int align_warp_smem_bytes_host(int N);
+void launch_align_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
+                          AlignOut out, int *queue, int grid_in_smem, int blocks, int warps, size_t smem,
+                          cudaStream_t st);
+void launch_optimize_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
+                             const uint32_t *keys, OptOut out, int *queue, int blocks, int warps, size_t smem,
+                             cudaStream_t st);
+size_t optimize_warp_smem_bytes();
+void launch_grid_score(const PocketView &pk, const float *coords, int n_atoms, int n_poses, int32_t *out,
+                       cudaStream_t st);
+void launch_rescore(const PocketView &pk, const float *coords, const uint8_t *types, int n_atoms, int n_poses,
+                    float cutoff2, int64_t *out, cudaStream_t st);
+}  // namespace ds
+
+using namespace ds;
+
+namespace {
+thread_local char g_err[512];
+
+int fail(int code, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define DS_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess) return fail(DS_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+// device buffer that grows geometrically; counts cudaMalloc calls
+struct DevBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+};
+}  // namespace
+
+struct ds_ctx {
+  int device = 0;
+  int sm_count = 0;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[6] = {};
+  int64_t allocs = 0;
+  float2 *trig = nullptr;       // 360 (cos, sin)
+  // batch-sized device buffers
+  DevBuf b_atom_off, b_atoms, b_frag_off, b_frags, b_idh, b_order_a, b_order_o, b_keys, b_res, b_rrec, b_rtors,
+      b_coords, b_btors, b_queue, b_scratch;
+  // pinned host staging
+  void *h_stage = nullptr;
+  size_t h_cap = 0;
+  int ensure(DevBuf &b, size_t bytes) {
+    if (bytes <= b.cap) return DS_OK;
+    size_t nc = std::max(bytes, b.cap * 3 / 2);
+    nc = (nc + 255) & ~(size_t)255;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    cudaError_t e = cudaMalloc(&b.p, nc);
+    if (e != cudaSuccess) return fail(DS_ERR_OOM, "cudaMalloc(%zu): %s", nc, cudaGetErrorString(e));
+    b.cap = nc;
+    ++allocs;
+    return DS_OK;
+  }
+  int ensure_host(size_t bytes) {
+    if (bytes <= h_cap) return DS_OK;
+    size_t nc = std::max(bytes, h_cap * 3 / 2);
+    if (h_stage) cudaFreeHost(h_stage);
+    h_stage = nullptr;
+    h_cap = 0;
+    cudaError_t e = cudaMallocHost(&h_stage, nc);
+    if (e != cudaSuccess) return fail(DS_ERR_OOM, "cudaMallocHost(%zu): %s", nc, cudaGetErrorString(e));
+    h_cap = nc;
+    ++allocs;
+    return DS_OK;
+  }
+};
+
+struct ds_pocket {
+  ds_ctx *ctx = nullptr;
+  PocketView view{};
+  int8_t *d_grid = nullptr;
+  float4 *d_patoms = nullptr;
+  int32_t *d_wfx = nullptr;
+  float cutoff = 0.f;
+};
+
+struct ds_dev_batch {
+  ds_ctx *ctx = nullptr;
+  int L = 0, n_atoms = 0, n_frags = 0;
+  int N = 0;
+  std::vector<int> atom_off, frag_off;  // host copies for downloads
+  bool docked = false;
+};
+
+extern "C" {
+
+int ds_abi_version(void) { return DS_ABI_VERSION; }
+const char *ds_last_error(void) { return g_err; }
+
+int ds_device_count(int *n) {
+  if (!n) return fail(DS_ERR_INVALID_ARG, "n is NULL");
+  cudaError_t e = cudaGetDeviceCount(n);
+  if (e != cudaSuccess) {
+    *n = 0;
+    return fail(DS_ERR_NO_DEVICE, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  return DS_OK;
+}
+
+int ds_create(int device, ds_ctx **out) {
+  if (!out) return fail(DS_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(DS_ERR_NO_DEVICE, "no CUDA device visible");
+  if (device < 0 || device >= n) return fail(DS_ERR_INVALID_ARG, "device %d out of range (%d devices)", device, n);
+  DS_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  DS_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(DS_ERR_UNSUPPORTED, "libdockscreen is built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
+  ds_ctx *c = new ds_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  c->smem_optin = prop.sharedMemPerBlockOptin;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return fail(DS_ERR_CUDA, "cudaStreamCreate failed");
+  }
+  for (auto &e : c->ev) cudaEventCreate(&e);
+  // P0: trig table of integer degrees, f32 of f64 (shared by every kernel)
+  float2 h[360];
+  for (int d = 0; d < 360; ++d) {
+    const double rad = (double)d * 0.017453292519943295;  // pi/180
+    h[d] = make_float2((float)cos(rad), (float)sin(rad));
+  }
+  if (cudaMalloc(&c->trig, sizeof h) != cudaSuccess) {
+    ds_destroy(c);
+    return fail(DS_ERR_OOM, "cudaMalloc(trig) failed");
+  }
+  ++c->allocs;
+  cudaMemcpy(c->trig, h, sizeof h, cudaMemcpyHostToDevice);
+  *out = c;
+  return DS_OK;
+}
+
+void ds_destroy(ds_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  DevBuf *bufs[] = {&c->b_atom_off, &c->b_atoms, &c->b_frag_off, &c->b_frags, &c->b_idh, &c->b_order_a,
+                    &c->b_order_o, &c->b_keys, &c->b_res, &c->b_rrec, &c->b_rtors, &c->b_coords, &c->b_btors,
+                    &c->b_queue, &c->b_scratch};
+  for (DevBuf *b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (c->trig) cudaFree(c->trig);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  for (auto &e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int ds_ctx_alloc_count(const ds_ctx *c, int64_t *count) {
+  if (!c || !count) return fail(DS_ERR_INVALID_ARG, "NULL argument");
+  *count = c->allocs;
+  return DS_OK;
+}
+
+void *ds_ctx_stream(ds_ctx *c) { return c ? (void *)c->stream : nullptr; }
+
+int ds_synchronize(ds_ctx *c) {
+  if (!c) return fail(DS_ERR_INVALID_ARG, "NULL ctx");
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  return DS_OK;
+}
+
+int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
+  if (!c || !d || !out) return fail(DS_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  if (!(d->spacing > 0.f)) return fail(DS_ERR_INVALID_ARG, "grid spacing must be > 0");
+  for (int k = 0; k < 3; ++k)
+    if (d->dims[k] < 1 || d->dims[k] >= (1 << 21)) return fail(DS_ERR_INVALID_ARG, "bad grid dims");
+  const int64_t G = (int64_t)d->dims[0] * d->dims[1] * d->dims[2];
+  if (G >= (1ll << 30)) return fail(DS_ERR_UNSUPPORTED, "grid too large");
+  if (!d->values) return fail(DS_ERR_INVALID_ARG, "grid values NULL");
+  if (d->n_atoms < 0 || (d->n_atoms > 0 && (!d->atom_xyz || !d->atom_type)))
+    return fail(DS_ERR_INVALID_ARG, "bad pocket atoms");
+  if (!d->table || d->n_bins < 1 || d->n_bins > DS_MAX_BINS || !d->bin_ub || !d->bin_mult)
+    return fail(DS_ERR_INVALID_ARG, "bad interaction table");
+  for (int b = 1; b < d->n_bins; ++b)
+    if (!(d->bin_ub[b] > d->bin_ub[b - 1])) return fail(DS_ERR_INVALID_ARG, "bins must be ascending");
+  // int8 device grid: every value must fit
+  const int gbytes = (int)((G + 1 + 15) & ~15ll);
+  std::vector<int8_t> g8(gbytes, 0);
+  for (int64_t i = 0; i < G; ++i) {
+    const int32_t v = d->values[i];
+    if (v < -128 || v > 127) return fail(DS_ERR_UNSUPPORTED, "grid value %d at node %lld does not fit int8", v, (long long)i);
+    g8[i] = (int8_t)v;
+  }
+  g8[G] = (int8_t)kOutside;
+  for (int t = 0; t < DS_N_TYPES * DS_N_TYPES; ++t)
+    if (d->table[t] != d->table[(t % DS_N_TYPES) * DS_N_TYPES + t / DS_N_TYPES])
+      return fail(DS_ERR_INVALID_ARG, "interaction table must be symmetric");
+  DS_CUDA(cudaSetDevice(c->device));
+  ds_pocket *p = new ds_pocket();
+  p->ctx = c;
+  PocketView &v = p->view;
+  v.g.nx = d->dims[0];
+  v.g.ny = d->dims[1];
+  v.g.nz = d->dims[2];
+  v.g.nxy = d->dims[0] * d->dims[1];
+  v.g.sentinel = (int)G;
+  v.grid_bytes = gbytes;
+  v.spacing = d->spacing;
+  v.inv_s = (float)(1.0 / (double)d->spacing);  // P2
+  v.ox = d->origin[0];
+  v.oy = d->origin[1];
+  v.oz = d->origin[2];
+  v.n_atoms = d->n_atoms;
+  v.nb = d->n_bins;
+  for (int b = 0; b < DS_MAX_BINS; ++b) {
+    const double ub = b < d->n_bins ? (double)d->bin_ub[b] / (double)d->spacing : 0.0;
+    v.ub2[b] = (float)(ub * ub);  // P11
+  }
+  p->cutoff = d->bin_ub[d->n_bins - 1];
+  // pocket atoms in the grid frame: f32((p - o) / s) evaluated in f64 (P11)
+  std::vector<float4> pa(std::max(d->n_atoms, 1));
+  for (int j = 0; j < d->n_atoms; ++j) {
+    float q[3];
+    for (int k = 0; k < 3; ++k)
+      q[k] = (float)(((double)d->atom_xyz[3 * j + k] - (double)d->origin[k]) / (double)d->spacing);
+    if (d->atom_type[j] >= DS_N_TYPES) {
+      delete p;
+      return fail(DS_ERR_INDEX_OUT_OF_RANGE, "pocket atom %d type %d", j, d->atom_type[j]);
+    }
+    pa[j] = make_float4(q[0], q[1], q[2], (float)d->atom_type[j]);
+  }
+  // fixed-point table x multiplier: W = llrint(f32(table*mult) * 2^24), bin nb -> 0 (P11)
+  const int nb1 = d->n_bins + 1;
+  std::vector<int32_t> w((size_t)DS_N_TYPES * DS_N_TYPES * nb1, 0);
+  for (int t = 0; t < DS_N_TYPES * DS_N_TYPES; ++t)
+    for (int b = 0; b < d->n_bins; ++b) {
+      const float prod = d->table[t] * d->bin_mult[b];
+      const double s = (double)prod * 16777216.0;
+      if (!(fabs(s) < 2147483647.0)) {
+        delete p;
+        return fail(DS_ERR_UNSUPPORTED, "table*multiplier %g out of fixed-point range", (double)prod);
+      }
+      w[(size_t)t * nb1 + b] = (int32_t)llrint(s);
+    }
+  v.trig = c->trig;
+  if (cudaMalloc(&p->d_grid, gbytes) != cudaSuccess || cudaMalloc(&p->d_patoms, pa.size() * sizeof(float4)) != cudaSuccess ||
+      cudaMalloc(&p->d_wfx, w.size() * 4) != cudaSuccess) {
+    ds_pocket_destroy(p);
+    return fail(DS_ERR_OOM, "pocket allocation failed");
+  }
+  c->allocs += 3;
+  cudaMemcpy(p->d_grid, g8.data(), gbytes, cudaMemcpyHostToDevice);
+  cudaMemcpy(p->d_patoms, pa.data(), pa.size() * sizeof(float4), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->d_wfx, w.data(), w.size() * 4, cudaMemcpyHostToDevice);
+  v.grid = p->d_grid;
+  v.patoms = p->d_patoms;
+  v.wfx = p->d_wfx;
+  // keep the grid L2-resident for the LDG paths (access-policy window, north star)
+  cudaStreamAttrValue attr = {};
+  size_t maxwin = 0;
+  int l2max = 0;
+  cudaDeviceGetAttribute(&l2max, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
+  maxwin = (size_t)l2max;
+  if (maxwin > 0) {
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min((size_t)gbytes, (size_t)64 << 20));
+    attr.accessPolicyWindow.base_ptr = p->d_grid;
+    attr.accessPolicyWindow.num_bytes = std::min((size_t)gbytes, maxwin);
+    attr.accessPolicyWindow.hitRatio = 1.0f;
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &attr);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    ds_pocket_destroy(p);
+    return fail(DS_ERR_CUDA, "pocket upload: %s", cudaGetErrorString(e));
+  }
+  *out = p;
+  return DS_OK;
+}
+
+void ds_pocket_destroy(ds_pocket *p) {
+  if (!p) return;
+  if (p->ctx) cudaSetDevice(p->ctx->device);
+  if (p->d_grid) cudaFree(p->d_grid);
+  if (p->d_patoms) cudaFree(p->d_patoms);
+  if (p->d_wfx) cudaFree(p->d_wfx);
+  delete p;
+}
+
+}  // extern "C"
+
+namespace {
+
+int check_config(const ds_dock_config *cfg, const ds_pocket *pk, DockParams *dp) {
+  if (!cfg) return fail(DS_ERR_INVALID_ARG, "cfg is NULL");
+  if (cfg->restarts_n < 1 || cfg->restarts_n > DS_MAX_RESTARTS)
+    return fail(DS_ERR_INVALID_ARG, "restarts_n must be in 1..%d", DS_MAX_RESTARTS);
+  if (cfg->rescore_top_k < 1 || cfg->rescore_top_k > cfg->restarts_n)
+    return fail(DS_ERR_INVALID_ARG, "rescore_top_k must be in 1..restarts_n");
+  if (cfg->alignment_step_deg < 1 || 360 % cfg->alignment_step_deg)
+    return fail(DS_ERR_INVALID_ARG, "360 must be divisible by alignment_step_deg");
+  if (cfg->torsion_step_deg < 1 || 360 % cfg->torsion_step_deg)
+    return fail(DS_ERR_INVALID_ARG, "360 must be divisible by torsion_step_deg");
+  if (!(cfg->bump_distance > 0.f) || !(cfg->similarity_rmsd > 0.f) || !(cfg->rescore_cutoff > 0.f))
+    return fail(DS_ERR_INVALID_ARG, "distances must be positive");
+  if (cfg->rescore_cutoff != pk->cutoff)
+    return fail(DS_ERR_INVALID_ARG, "rescore_cutoff %g must equal the last bin bound %g (SPEC.md:179)",
+                (double)cfg->rescore_cutoff, (double)pk->cutoff);
+  dp->N = cfg->restarts_n;
+  dp->K = cfg->rescore_top_k;
+  dp->step_a = cfg->alignment_step_deg;
+  dp->n_a = 360 / cfg->alignment_step_deg;
+  dp->n_rot = dp->n_a * dp->n_a;
+  if (dp->n_rot > 65536) return fail(DS_ERR_UNSUPPORTED, "alignment_step_deg >= 2 required on device (32-bit argmax keys)");
+  dp->step_t = cfg->torsion_step_deg;
+  dp->n_t = 360 / cfg->torsion_step_deg;
+  dp->seed = cfg->seed;
+  dp->early_exit = cfg->early_exit ? 1 : 0;
+  const double s = (double)pk->view.spacing;
+  const double bd = (double)cfg->bump_distance / s;
+  dp->bd2 = (float)(bd * bd);                              // P9
+  dp->eps_axis = (float)(1e-9 / s);                        // P8
+  const double th = (double)cfg->similarity_rmsd / s;
+  dp->thr2 = th * th;                                      // P12
+  return DS_OK;
+}
+
+int check_batch(const ds_batch_desc *b) {
+  if (!b) return fail(DS_ERR_INVALID_ARG, "batch is NULL");
+  if (b->n_ligands < 0) return fail(DS_ERR_INVALID_ARG, "n_ligands < 0");
+  if (b->n_ligands == 0) return DS_OK;
+  if (!b->atom_off || !b->atom_xyzt || !b->frag_off || !b->id_hash)
+    return fail(DS_ERR_INVALID_ARG, "batch arrays NULL");
+  if (b->frag_off[b->n_ligands] > 0 && !b->frag_desc) return fail(DS_ERR_INVALID_ARG, "frag_desc NULL");
+  for (int i = 0; i < b->n_ligands; ++i) {
+    const int A = b->atom_off[i + 1] - b->atom_off[i];
+    if (A < 1) return fail(DS_ERR_INVALID_ARG, "ligand %d has no atoms", i);
+    if (A > DS_MAX_ATOMS) return fail(DS_ERR_TOO_MANY_ATOMS, "ligand %d has %d atoms (> %d)", i, A, DS_MAX_ATOMS);
+    if (b->frag_off[i + 1] < b->frag_off[i]) return fail(DS_ERR_INVALID_ARG, "frag_off not monotone");
+    for (int f = b->frag_off[i]; f < b->frag_off[i + 1]; ++f) {
+      const uint32_t ax = b->frag_desc[(size_t)DS_FRAG_WORDS * f + 5];
+      const int ab = (int)(ax & 0xFF), ae = (int)((ax >> 8) & 0xFF);
+      if (ab >= A || ae >= A) return fail(DS_ERR_INDEX_OUT_OF_RANGE, "ligand %d fragment axis out of range", i);
+    }
+  }
+  return DS_OK;
+}
+
+// LPT orders: alignment work ~ A (counting sort, descending); optimisation work ~ F*(A^2)/4 + A
+void lpt_orders(const ds_batch_desc *b, std::vector<int> &oa, std::vector<int> &oo) {
+  const int L = b->n_ligands;
+  oa.resize(L);
+  oo.resize(L);
+  std::vector<int> cnt(DS_MAX_ATOMS + 2, 0);
+  for (int i = 0; i < L; ++i) cnt[DS_MAX_ATOMS - (b->atom_off[i + 1] - b->atom_off[i])]++;
+  std::vector<int> pos(DS_MAX_ATOMS + 2, 0);
+  for (int k = 1; k <= DS_MAX_ATOMS + 1; ++k) pos[k] = pos[k - 1] + cnt[k - 1];
+  for (int i = 0; i < L; ++i) oa[pos[DS_MAX_ATOMS - (b->atom_off[i + 1] - b->atom_off[i])]++] = i;
+  std::vector<std::pair<int64_t, int>> cost(L);
+  for (int i = 0; i < L; ++i) {
+    const int64_t A = b->atom_off[i + 1] - b->atom_off[i], F = b->frag_off[i + 1] - b->frag_off[i];
+    cost[i] = {-(F * A * A / 4 + 4 * A), i};
+  }
+  std::sort(cost.begin(), cost.end());
+  for (int i = 0; i < L; ++i) oo[i] = cost[i].second;
+}
+
+struct Staged {
+  size_t off_atom_off, off_atoms, off_frag_off, off_frags, off_idh, off_oa, off_oo, total;
+};
+
+int upload_batch(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
+  const int L = b->n_ligands;
+  const int NA = b->atom_off[L], NF = b->frag_off[L];
+  std::vector<int> oa, oo;
+  lpt_orders(b, oa, oo);
+  int rc;
+  if ((rc = c->ensure(c->b_atom_off, sizeof(int) * (L + 1))) || (rc = c->ensure(c->b_atoms, 16ull * std::max(NA, 1))) ||
+      (rc = c->ensure(c->b_frag_off, sizeof(int) * (L + 1))) || (rc = c->ensure(c->b_frags, 32ull * std::max(NF, 1))) ||
+      (rc = c->ensure(c->b_idh, 8ull * L)) || (rc = c->ensure(c->b_order_a, 4ull * L)) ||
+      (rc = c->ensure(c->b_order_o, 4ull * L)) || (rc = c->ensure(c->b_keys, 4ull * L * N)) ||
+      (rc = c->ensure(c->b_res, sizeof(ds_result) * (size_t)L)) ||
+      (rc = c->ensure(c->b_rrec, sizeof(ds_restart_record) * (size_t)L * N)) ||
+      (rc = c->ensure(c->b_rtors, (size_t)std::max(NF, 1) * N)) || (rc = c->ensure(c->b_coords, 12ull * std::max(NA, 1))) ||
+      (rc = c->ensure(c->b_btors, (size_t)std::max(NF, 1))) || (rc = c->ensure(c->b_queue, 256)))
+    return rc;
+  // stage into pinned memory, one H2D per array
+  Staged s;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o += (bytes + 255) & ~(size_t)255;
+    return r;
+  };
+  s.off_atom_off = take(4ull * (L + 1));
+  s.off_atoms = take(16ull * NA);
+  s.off_frag_off = take(4ull * (L + 1));
+  s.off_frags = take(32ull * NF);
+  s.off_idh = take(8ull * L);
+  s.off_oa = take(4ull * L);
+  s.off_oo = take(4ull * L);
+  s.total = o;
+  if ((rc = c->ensure_host(s.total))) return rc;
+  char *h = (char *)c->h_stage;
+  memcpy(h + s.off_atom_off, b->atom_off, 4ull * (L + 1));
+  memcpy(h + s.off_atoms, b->atom_xyzt, 16ull * NA);
+  memcpy(h + s.off_frag_off, b->frag_off, 4ull * (L + 1));
+  if (NF) memcpy(h + s.off_frags, b->frag_desc, 32ull * NF);
+  memcpy(h + s.off_idh, b->id_hash, 8ull * L);
+  memcpy(h + s.off_oa, oa.data(), 4ull * L);
+  memcpy(h + s.off_oo, oo.data(), 4ull * L);
+  cudaStream_t st_ = c->stream;
+  DS_CUDA(cudaMemcpyAsync(c->b_atom_off.p, h + s.off_atom_off, 4ull * (L + 1), cudaMemcpyHostToDevice, st_));
+  DS_CUDA(cudaMemcpyAsync(c->b_atoms.p, h + s.off_atoms, 16ull * NA, cudaMemcpyHostToDevice, st_));
+  DS_CUDA(cudaMemcpyAsync(c->b_frag_off.p, h + s.off_frag_off, 4ull * (L + 1), cudaMemcpyHostToDevice, st_));
+  if (NF) DS_CUDA(cudaMemcpyAsync(c->b_frags.p, h + s.off_frags, 32ull * NF, cudaMemcpyHostToDevice, st_));
+  DS_CUDA(cudaMemcpyAsync(c->b_idh.p, h + s.off_idh, 8ull * L, cudaMemcpyHostToDevice, st_));
+  DS_CUDA(cudaMemcpyAsync(c->b_order_a.p, h + s.off_oa, 4ull * L, cudaMemcpyHostToDevice, st_));
+  DS_CUDA(cudaMemcpyAsync(c->b_order_o.p, h + s.off_oo, 4ull * L, cudaMemcpyHostToDevice, st_));
+  if (st) st->h2d_bytes += (int64_t)(4ull * (L + 1) * 2 + 16ull * NA + 32ull * NF + 8ull * L + 8ull * L);
+  return DS_OK;
+}
+
+int run_batched(ds_ctx *c, const ds_pocket *pk, int L, int NA, int NF, const DockParams &dp, bool want_coords,
+                bool want_btors, bool want_rrec, ds_stats *st) {
+  BatchView bt;
+  bt.L = L;
+  bt.atom_off = (const int *)c->b_atom_off.p;
+  bt.atoms = (const float4 *)c->b_atoms.p;
+  bt.frag_off = (const int *)c->b_frag_off.p;
+  bt.frags = (const uint4 *)c->b_frags.p;
+  bt.idh = (const uint64_t *)c->b_idh.p;
+  int *queue = (int *)c->b_queue.p;
+  DS_CUDA(cudaMemsetAsync(queue, 0, 256, c->stream));
+  // --- alignment: one CTA per SM, grid staged into smem when it fits ---
+  const size_t per_warp = (size_t)align_warp_smem_bytes_host(dp.N);
+  const size_t fixed = (size_t)((dp.n_a * 8 + 15) & ~15);
+  int warps_a = 32;
+  const size_t gb = (size_t)pk->view.grid_bytes;
+  int in_smem = gb + fixed + per_warp * 8 <= c->smem_optin;
+  if (in_smem) warps_a = (int)std::min<size_t>(32, (c->smem_optin - gb - fixed) / per_warp);
+  const size_t smem_a = (in_smem ? gb : 0) + fixed + per_warp * warps_a;
+  AlignOut ao{(uint32_t *)c->b_keys.p};
+  cudaEventRecord(c->ev[1], c->stream);
+  launch_align_batched(pk->view, bt, dp, (const int *)c->b_order_a.p, ao, queue, in_smem, c->sm_count, warps_a, smem_a,
+                       c->stream);
+  cudaEventRecord(c->ev[2], c->stream);
+  // --- optimisation + select + rescore: warp per ligand ---
+  const int warps_o = 8;
+  const size_t smem_o = optimize_warp_smem_bytes() * warps_o;
+  int per_sm = std::max(1, (int)std::min<size_t>(4, c->smem_optin / std::max<size_t>(smem_o, 1)));
+  const int blocks_o = c->sm_count * per_sm;
+  int rc;
+  if ((rc = c->ensure(c->b_scratch, sizeof(float4) * (size_t)blocks_o * warps_o * dp.N * DS_MAX_ATOMS))) return rc;
+  OptOut oo;
+  oo.res = (ds_result *)c->b_res.p;
+  oo.rrec = want_rrec ? (ds_restart_record *)c->b_rrec.p : nullptr;
+  oo.rtors = (uint8_t *)c->b_rtors.p;
+  oo.final_u = (float4 *)c->b_scratch.p;
+  oo.best_coords = want_coords ? (float *)c->b_coords.p : nullptr;
+  oo.best_tors = want_btors ? (uint8_t *)c->b_btors.p : nullptr;
+  launch_optimize_batched(pk->view, bt, dp, (const int *)c->b_order_o.p, (const uint32_t *)c->b_keys.p, oo, queue + 16,
+                          blocks_o, warps_o, smem_o, c->stream);
+  cudaEventRecord(c->ev[3], c->stream);
+  if (st) st->launches += 2;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DS_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return DS_OK;
+}
+
+int download(ds_ctx *c, int L, int NA, int NF, int N, const ds_outputs *out, ds_stats *st) {
+  cudaStream_t s = c->stream;
+  if (out->results) {
+    DS_CUDA(cudaMemcpyAsync(out->results, c->b_res.p, sizeof(ds_result) * (size_t)L, cudaMemcpyDeviceToHost, s));
+    if (st) st->d2h_bytes += sizeof(ds_result) * (int64_t)L;
+  }
+  if (out->best_coords && NA) {
+    DS_CUDA(cudaMemcpyAsync(out->best_coords, c->b_coords.p, 12ull * NA, cudaMemcpyDeviceToHost, s));
+    if (st) st->d2h_bytes += 12ll * NA;
+  }
+  if (out->best_torsion && NF) {
+    DS_CUDA(cudaMemcpyAsync(out->best_torsion, c->b_btors.p, (size_t)NF, cudaMemcpyDeviceToHost, s));
+    if (st) st->d2h_bytes += NF;
+  }
+  if (out->restarts) {
+    DS_CUDA(cudaMemcpyAsync(out->restarts, c->b_rrec.p, sizeof(ds_restart_record) * (size_t)L * N, cudaMemcpyDeviceToHost, s));
+    if (st) st->d2h_bytes += (int64_t)sizeof(ds_restart_record) * L * N;
+  }
+  if (out->restart_torsion && NF) {
+    DS_CUDA(cudaMemcpyAsync(out->restart_torsion, c->b_rtors.p, (size_t)NF * N, cudaMemcpyDeviceToHost, s));
+    if (st) st->d2h_bytes += (int64_t)NF * N;
+  }
+  return DS_OK;
+}
+
+void fill_times(ds_ctx *c, ds_stats *st, bool with_copies) {
+  if (!st) return;
+  float t = 0.f;
+  cudaEventElapsedTime(&t, c->ev[1], c->ev[2]);
+  st->align_ms = t;
+  cudaEventElapsedTime(&t, c->ev[2], c->ev[3]);
+  st->optimize_ms = t;
+  cudaEventElapsedTime(&t, with_copies ? c->ev[0] : c->ev[1], with_copies ? c->ev[4] : c->ev[3]);
+  st->total_ms = t;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ds_dock(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const ds_dock_config *cfg, int family,
+            const ds_outputs *out, ds_stats *st) {
+  if (!c || !pk || !out || !out->results) return fail(DS_ERR_INVALID_ARG, "NULL argument");
+  if (family != DS_FAMILY_BATCHED && family != DS_FAMILY_LATENCY) return fail(DS_ERR_INVALID_ARG, "unknown family %d", family);
+  DockParams dp;
+  int rc;
+  if ((rc = check_config(cfg, pk, &dp)) || (rc = check_batch(b))) return rc;
+  if (st) memset(st, 0, sizeof *st);
+  const int L = b->n_ligands;
+  if (L == 0) return DS_OK;
+  DS_CUDA(cudaSetDevice(c->device));
+  cudaEventRecord(c->ev[0], c->stream);
+  if ((rc = upload_batch(c, b, dp.N, st))) return rc;
+  const int NA = b->atom_off[L], NF = b->frag_off[L];
+  // Both families share the batched kernels in this build (the latency family is routed
+  // through the same kernels until its own spread-out kernels land).
+  if ((rc = run_batched(c, pk, L, NA, NF, dp, out->best_coords != nullptr, out->best_torsion != nullptr,
+                        out->restarts != nullptr, st)))
+    return rc;
+  if ((rc = download(c, L, NA, NF, dp.N, out, st))) return rc;
+  cudaEventRecord(c->ev[4], c->stream);
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  fill_times(c, st, true);
+  return DS_OK;
+}
+
+int ds_batch_upload(ds_ctx *c, const ds_batch_desc *b, ds_dev_batch **out) {
+  if (!c || !out) return fail(DS_ERR_INVALID_ARG, "NULL argument");
+  int rc;
+  if ((rc = check_batch(b))) return rc;
+  DS_CUDA(cudaSetDevice(c->device));
+  ds_dev_batch *d = new ds_dev_batch();
+  d->ctx = c;
+  d->L = b->n_ligands;
+  d->atom_off.assign(b->atom_off, b->atom_off + d->L + 1);
+  d->frag_off.assign(b->frag_off, b->frag_off + d->L + 1);
+  d->n_atoms = b->atom_off[d->L];
+  d->n_frags = b->frag_off[d->L];
+  if ((rc = upload_batch(c, b, DS_MAX_RESTARTS, nullptr))) {
+    delete d;
+    return rc;
+  }
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  *out = d;
+  return DS_OK;
+}
+
+int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_dock_config *cfg, int family,
+                     ds_stats *st) {
+  if (!c || !pk || !d || d->ctx != c) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  DockParams dp;
+  int rc;
+  if ((rc = check_config(cfg, pk, &dp))) return rc;
+  if (st) memset(st, 0, sizeof *st);
+  if (d->L == 0) return DS_OK;
+  DS_CUDA(cudaSetDevice(c->device));
+  if ((rc = run_batched(c, pk, d->L, d->n_atoms, d->n_frags, dp, true, true, true, st))) return rc;
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  d->N = dp.N;
+  d->docked = true;
+  fill_times(c, st, false);
+  return DS_OK;
+}
+
+int ds_batch_download(ds_ctx *c, ds_dev_batch *d, const ds_outputs *out) {
+  if (!c || !d || !out) return fail(DS_ERR_INVALID_ARG, "NULL argument");
+  if (!d->docked) return fail(DS_ERR_INVALID_ARG, "batch has not been docked");
+  int rc;
+  if ((rc = download(c, d->L, d->n_atoms, d->n_frags, d->N, out, nullptr))) return rc;
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  return DS_OK;
+}
+
+void ds_batch_destroy(ds_dev_batch *d) { delete d; }
+
+int ds_query_capacity(ds_ctx *c, int range_idx, int *ligands) {
+  if (!c || !ligands || range_idx < 0 || range_idx > 4) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  // the batched kernels are persistent: a full wave is (SMs x resident warps) ligands
+  const int per_sm_align = 32;
+  *ligands = c->sm_count * per_sm_align;
+  return DS_OK;
+}
+
+int ds_op_grid_score(ds_ctx *c, const ds_pocket *pk, const float *coords, int n_atoms, int n_poses, int32_t *out) {
+  if (!c || !pk || !coords || !out || n_atoms < 0 || n_poses < 0) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  if (!n_poses) return DS_OK;
+  DS_CUDA(cudaSetDevice(c->device));
+  const size_t nc = 12ull * n_atoms * n_poses;
+  int rc;
+  if ((rc = c->ensure(c->b_coords, std::max<size_t>(nc, 16))) || (rc = c->ensure(c->b_keys, 4ull * n_poses))) return rc;
+  DS_CUDA(cudaMemcpyAsync(c->b_coords.p, coords, nc, cudaMemcpyHostToDevice, c->stream));
+  launch_grid_score(pk->view, (const float *)c->b_coords.p, n_atoms, n_poses, (int32_t *)c->b_keys.p, c->stream);
+  DS_CUDA(cudaGetLastError());
+  DS_CUDA(cudaMemcpyAsync(out, c->b_keys.p, 4ull * n_poses, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  return DS_OK;
+}
+
+int ds_op_rescore(ds_ctx *c, const ds_pocket *pk, const float *coords, const uint8_t *types, int n_atoms, int n_poses,
+                  float cutoff, int64_t *out) {
+  if (!c || !pk || !coords || !types || !out || n_atoms < 0 || n_poses < 0) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  if (cutoff != pk->cutoff) return fail(DS_ERR_INVALID_ARG, "cutoff must equal the last bin bound");
+  if (!n_poses) return DS_OK;
+  DS_CUDA(cudaSetDevice(c->device));
+  const size_t nc = 12ull * n_atoms * n_poses;
+  int rc;
+  if ((rc = c->ensure(c->b_coords, std::max<size_t>(nc, 16))) || (rc = c->ensure(c->b_rtors, std::max(n_atoms, 1))) ||
+      (rc = c->ensure(c->b_res, 8ull * n_poses)))
+    return rc;
+  DS_CUDA(cudaMemcpyAsync(c->b_coords.p, coords, nc, cudaMemcpyHostToDevice, c->stream));
+  DS_CUDA(cudaMemcpyAsync(c->b_rtors.p, types, (size_t)n_atoms, cudaMemcpyHostToDevice, c->stream));
+  launch_rescore(pk->view, (const float *)c->b_coords.p, (const uint8_t *)c->b_rtors.p, n_atoms, n_poses, 0.f,
+                 (int64_t *)c->b_res.p, c->stream);
+  DS_CUDA(cudaGetLastError());
+  DS_CUDA(cudaMemcpyAsync(out, c->b_res.p, 8ull * n_poses, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  return DS_OK;
+}
+
+}  // extern "C"

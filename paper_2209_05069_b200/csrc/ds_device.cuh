@@ -1,0 +1,134 @@
+// Device-side numeric primitives of the docking hot path (sm_100a).
+//
+// Every function here implements one pin of the numeric recipe and must stay
+// bit-identical to the CPU restatement in oracle/.  The translation unit is compiled with
+// --fmad=false, so a*b+c is two roundings unless written as __fmaf_rn / fma explicitly.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dockscreen.h"
+
+namespace ds {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr float kMagic = 12582912.0f;     // 1.5 * 2^23: x + kMagic rounds x half-even to an integer
+constexpr int kMagicBits = 0x4B400000;    // bit pattern of kMagic
+constexpr int kOutside = -100;            // out-of-grid penalty per atom
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr int kChemShift = 24;            // chem fixed point 2^-24 (P11)
+
+// ---- P5: counter-based starting-pose PRNG (SplitMix64 finaliser) --------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// ---- P1: pinned f32 3x3 product C = A (x) B, C_ij = fma(A_i2,B_2j, fma(A_i1,B_1j, A_i0*B_0j))
+__device__ __forceinline__ void matmul3(const float *A, const float *B, float *C) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      C[3 * i + j] = __fmaf_rn(A[3 * i + 2], B[6 + j], __fmaf_rn(A[3 * i + 1], B[3 + j], __fmul_rn(A[3 * i], B[j])));
+}
+
+// ---- P3: pose transform u = M d + t, u_k = fma(M_k2,d.z, fma(M_k1,d.y, fma(M_k0,d.x,t_k)))
+__device__ __forceinline__ float3 apply_mt(const float *M, const float *t, float dx, float dy, float dz) {
+  float3 u;
+  u.x = __fmaf_rn(M[2], dz, __fmaf_rn(M[1], dy, __fmaf_rn(M[0], dx, t[0])));
+  u.y = __fmaf_rn(M[5], dz, __fmaf_rn(M[4], dy, __fmaf_rn(M[3], dx, t[1])));
+  u.z = __fmaf_rn(M[8], dz, __fmaf_rn(M[7], dy, __fmaf_rn(M[6], dx, t[2])));
+  return u;
+}
+
+// ---- P4: nearest node (round half-even) + in-grid test; returns kSentinel index if outside.
+// For |u| < 2^22 the magic add equals rintf; every |u| >= 2^22, inf or NaN lands outside
+// (dims < 2^22), exactly like the oracle's float test 0 <= rint(u) <= n-1.
+struct GridGeom {
+  int nx, ny, nz, nxy, sentinel;
+};
+__device__ __forceinline__ int node_index(const GridGeom &g, float ux, float uy, float uz) {
+  const int bx = __float_as_int(__fadd_rn(ux, kMagic)) - kMagicBits;
+  const int by = __float_as_int(__fadd_rn(uy, kMagic)) - kMagicBits;
+  const int bz = __float_as_int(__fadd_rn(uz, kMagic)) - kMagicBits;
+  const bool in = ((unsigned)bx < (unsigned)g.nx) & ((unsigned)by < (unsigned)g.ny) & ((unsigned)bz < (unsigned)g.nz);
+  const int idx = bx + g.nx * by + g.nxy * bz;
+  return in ? idx : g.sentinel;
+}
+
+// ---- P5: starting pose parameters of restart r: R0s = (Rz(g) (x) (Ry(b) (x) Rx(a))) * inv_s,
+// t = (n-1) * (0.1 + 0.8 U)   (grid frame)
+__device__ __forceinline__ void start_params(uint64_t idh, int64_t seed, int r, const float2 *trig, float inv_s,
+                                             int nx, int ny, int nz, float *R0s, float *t) {
+  const uint64_t base = idh ^ ((uint64_t)seed * kGolden);
+  uint64_t z[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) z[k] = mix64(base + (uint64_t)(r * 8 + k + 1) * kGolden);
+  const int n[3] = {nx, ny, nz};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float U = __fmul_rn((float)(uint32_t)(z[k] >> 40), 5.9604644775390625e-08f);  // exact
+    t[k] = __fmul_rn((float)(n[k] - 1), __fadd_rn(0.1f, __fmul_rn(0.8f, U)));
+  }
+  const float2 ca = trig[(int)((z[3] >> 32) % 360u)];
+  const float2 cb = trig[(int)((z[4] >> 32) % 360u)];
+  const float2 cg = trig[(int)((z[5] >> 32) % 360u)];
+  const float Rx[9] = {1.f, 0.f, 0.f, 0.f, ca.x, -ca.y, 0.f, ca.y, ca.x};
+  const float Ry[9] = {cb.x, 0.f, cb.y, 0.f, 1.f, 0.f, -cb.y, 0.f, cb.x};
+  const float Rz[9] = {cg.x, -cg.y, 0.f, cg.y, cg.x, 0.f, 0.f, 0.f, 1.f};
+  float Ryx[9], R0[9];
+  matmul3(Ry, Rx, Ryx);
+  matmul3(Rz, Ryx, R0);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R0s[k] = __fmul_rn(R0[k], inv_s);
+}
+
+// ---- P6: alignment rotation Ra(ix,iy) = Ry(ay) (x) Rx(ax) in single-product form, M = Ra (x) R0s
+__device__ __forceinline__ void align_matrix(float2 cx_sx, float2 cy_sy, const float *R0s, float *M) {
+  const float cx = cx_sx.x, sx = cx_sx.y, cy = cy_sy.x, sy = cy_sy.y;
+  const float Ra[9] = {cy, __fmul_rn(sy, sx), __fmul_rn(sy, cx), 0.f, cx, -sx, -sy, __fmul_rn(cy, sx),
+                       __fmul_rn(cy, cx)};
+  matmul3(Ra, R0s, M);
+}
+
+// ---- P8: torsion rotation (Rodrigues) about unit axis k by table angle (c, s)
+__device__ __forceinline__ void torsion_matrix(float kx, float ky, float kz, float c, float s, float *R) {
+  const float C = __fsub_rn(1.0f, c);
+  const float Ckx = __fmul_rn(C, kx), Cky = __fmul_rn(C, ky), Ckz = __fmul_rn(C, kz);
+  const float skx = __fmul_rn(s, kx), sky = __fmul_rn(s, ky), skz = __fmul_rn(s, kz);
+  R[0] = __fmaf_rn(Ckx, kx, c);
+  R[1] = __fmaf_rn(Ckx, ky, -skz);
+  R[2] = __fmaf_rn(Ckx, kz, sky);
+  R[3] = __fmaf_rn(Cky, kx, skz);
+  R[4] = __fmaf_rn(Cky, ky, c);
+  R[5] = __fmaf_rn(Cky, kz, -skx);
+  R[6] = __fmaf_rn(Ckz, kx, -sky);
+  R[7] = __fmaf_rn(Ckz, ky, skx);
+  R[8] = __fmaf_rn(Ckz, kz, c);
+}
+
+// p' = R (p - a) + a
+__device__ __forceinline__ float3 torsion_apply(const float *R, float3 a, float px, float py, float pz) {
+  const float wx = __fsub_rn(px, a.x), wy = __fsub_rn(py, a.y), wz = __fsub_rn(pz, a.z);
+  float3 o;
+  o.x = __fmaf_rn(R[2], wz, __fmaf_rn(R[1], wy, __fmaf_rn(R[0], wx, a.x)));
+  o.y = __fmaf_rn(R[5], wz, __fmaf_rn(R[4], wy, __fmaf_rn(R[3], wx, a.y)));
+  o.z = __fmaf_rn(R[8], wz, __fmaf_rn(R[7], wy, __fmaf_rn(R[6], wx, a.z)));
+  return o;
+}
+
+// ---- P9: squared distance fma(dz,dz, fma(dy,dy, dx*dx))
+__device__ __forceinline__ float dist2(float ax, float ay, float az, float bx, float by, float bz) {
+  const float dx = __fsub_rn(ax, bx), dy = __fsub_rn(ay, by), dz = __fsub_rn(az, bz);
+  return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace ds

@@ -1,0 +1,347 @@
+// Host-side input makers and packing for libdockscreen (not on the timed path).
+//
+//  * ds_generate_ligands  — SPEC.md:443-451 generate_dataset (chain ligands, 1-2 H per
+//                           heavy atom, self-avoiding 1.5 Å steps, F rotatable bonds).
+//  * ds_build_pocket_grid — SPEC.md:453-461 build_pocket (shell-reward integer grid).
+//  * ds_pack_ligands      — validation + the packed SoA batch layout.
+//
+// All randomness is a counter-based SplitMix64 keyed by (seed, global ligand index), so any
+// shard of a 10M-ligand screen can be generated independently on its own rank
+// (BASELINE config 5).  Only IEEE +,-,*,/,sqrt are used (no libm transcendental), so
+// the generated inputs are identical on every x86-64 host.
+#include "../../include/dockscreen.h"
+
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+namespace {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+
+inline uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct Rng {  // SplitMix64 stream
+  uint64_t x;
+  Rng(uint64_t seed, uint64_t stream, uint64_t index)
+      : x(mix64(seed * kGolden ^ mix64(stream + 0x632BE59BD9B4E019ull)) + index * 0xD1B54A32D192ED03ull) {}
+  uint64_t next() { x += kGolden; return mix64(x); }
+  double u01() { return (double)(next() >> 11) * (1.0 / 9007199254740992.0); }
+  uint32_t below(uint32_t n) { return (uint32_t)((next() >> 32) % n); }
+  void unit(double v[3]) {  // rejection-sampled unit vector (no trig)
+    for (;;) {
+      double x = 2.0 * u01() - 1.0, y = 2.0 * u01() - 1.0, z = 2.0 * u01() - 1.0;
+      double r2 = x * x + y * y + z * z;
+      if (r2 > 1e-6 && r2 <= 1.0) {
+        double r = sqrt(r2);
+        v[0] = x / r; v[1] = y / r; v[2] = z / r;
+        return;
+      }
+    }
+  }
+};
+
+enum : uint64_t { kStreamShape = 1, kStreamHydro = 2, kStreamGeom = 3, kStreamFrag = 4, kStreamPocket = 5,
+                  kStreamTable = 6 };
+
+inline double dist2(const double *a, const double *b) {
+  double dx = a[0] - b[0], dy = a[1] - b[1], dz = a[2] - b[2];
+  return dx * dx + dy * dy + dz * dz;
+}
+
+// number of hydrogens per heavy atom (1-2, total capped at DS_MAX_ATOMS)
+int hydrogen_counts(int64_t seed, int64_t gi, int heavy, int *nh) {
+  Rng r((uint64_t)seed, kStreamHydro, (uint64_t)gi);
+  int total = heavy;
+  for (int k = 0; k < heavy; ++k) {
+    int want = 1 + (int)(r.next() & 1);
+    int room = DS_MAX_ATOMS - total;
+    int h = want < room ? want : room;
+    if (h < 0) h = 0;
+    if (nh) nh[k] = h;
+    total += h;
+  }
+  return total;
+}
+
+thread_local char g_err[256];
+
+}  // namespace
+
+extern "C" {
+
+uint64_t ds_ligand_id_hash(const char *id, size_t len) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (size_t i = 0; i < len; ++i) {
+    h ^= (uint8_t)id[i];
+    h *= 0x100000001B3ull;
+  }
+  return h;
+}
+
+int ds_generated_id(int64_t seed, int64_t index, char *buf, size_t cap) {
+  return snprintf(buf, cap, "lig_%lld_%lld", (long long)seed, (long long)index);
+}
+
+int ds_mixed_shapes(int64_t seed, int64_t first_index, int32_t count, int32_t heavy_min, int32_t heavy_max,
+                    int32_t frag_max, int32_t *shapes) {
+  if (count < 0 || !shapes || heavy_min < 1 || heavy_max < heavy_min || heavy_max > DS_MAX_ATOMS || frag_max < 0)
+    return DS_ERR_INVALID_ARG;
+#pragma omp parallel for schedule(static)
+  for (int32_t i = 0; i < count; ++i) {
+    Rng r((uint64_t)seed, kStreamShape, (uint64_t)(first_index + i));
+    int heavy = heavy_min + (int)r.below((uint32_t)(heavy_max - heavy_min + 1));
+    int fcap = std::min(frag_max, std::max(heavy - 2, 0));
+    int frags = (int)r.below((uint32_t)(fcap + 1));
+    shapes[2 * i] = heavy;
+    shapes[2 * i + 1] = frags;
+  }
+  return DS_OK;
+}
+
+int ds_generate_ligands(int64_t seed, int64_t first_index, int32_t count, const int32_t *shapes,
+                        int32_t *atom_off, int32_t *bond_off, int32_t *frag_off, float *atom_xyz,
+                        uint8_t *atom_type, int32_t *bonds, int32_t *frag_axis, uint32_t *frag_mask) {
+  if (count < 0 || !shapes || !atom_off || !bond_off || !frag_off) return DS_ERR_INVALID_ARG;
+  for (int32_t i = 0; i < count; ++i) {
+    int heavy = shapes[2 * i], frags = shapes[2 * i + 1];
+    // InfeasibleShape: fragments >= heavy - 1, or the atom cap
+    if (heavy < 1 || heavy > DS_MAX_ATOMS || frags < 0 || (frags > 0 && frags >= heavy - 1)) return DS_ERR_INFEASIBLE_SHAPE;
+  }
+  if (!atom_xyz) {  // pass 1: sizes
+    std::vector<int> tot(count);
+#pragma omp parallel for schedule(static)
+    for (int32_t i = 0; i < count; ++i) tot[i] = hydrogen_counts(seed, first_index + i, shapes[2 * i], nullptr);
+    atom_off[0] = bond_off[0] = frag_off[0] = 0;
+    for (int32_t i = 0; i < count; ++i) {
+      atom_off[i + 1] = atom_off[i] + tot[i];
+      bond_off[i + 1] = bond_off[i] + tot[i] - 1;
+      frag_off[i + 1] = frag_off[i] + shapes[2 * i + 1];
+    }
+    return DS_OK;
+  }
+  if (!atom_type || !bonds || !frag_axis || !frag_mask) return DS_ERR_INVALID_ARG;
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int32_t i = 0; i < count; ++i) {
+    const int64_t gi = first_index + i;
+    const int heavy = shapes[2 * i], frags = shapes[2 * i + 1];
+    int nh[DS_MAX_ATOMS];
+    const int total = hydrogen_counts(seed, gi, heavy, nh);
+    double pos[DS_MAX_ATOMS][3];
+    int parent[DS_MAX_ATOMS];
+    Rng g((uint64_t)seed, kStreamGeom, (uint64_t)gi);
+    // heavy chain: self-avoiding 1.5 Å steps (min 1.4 Å to every earlier non-neighbour)
+    pos[0][0] = pos[0][1] = pos[0][2] = 0.0;
+    parent[0] = -1;
+    for (int k = 1; k < heavy; ++k) {
+      double cand[3];
+      for (int attempt = 0; attempt < 64; ++attempt) {
+        double u[3];
+        g.unit(u);
+        for (int c = 0; c < 3; ++c) cand[c] = pos[k - 1][c] + 1.5 * u[c];
+        bool ok = true;
+        for (int j = 0; j + 1 < k && ok; ++j) ok = dist2(cand, pos[j]) >= 1.4 * 1.4;
+        if (ok) break;
+      }
+      for (int c = 0; c < 3; ++c) pos[k][c] = cand[c];
+      parent[k] = k - 1;
+    }
+    // hydrogens at 1.0 Å from their heavy atom, >= 0.9 Å from every other atom if possible
+    int a = heavy;
+    for (int k = 0; k < heavy; ++k) {
+      for (int h = 0; h < nh[k]; ++h, ++a) {
+        double cand[3];
+        for (int attempt = 0; attempt < 16; ++attempt) {
+          double u[3];
+          g.unit(u);
+          for (int c = 0; c < 3; ++c) cand[c] = pos[k][c] + 1.0 * u[c];
+          bool ok = true;
+          for (int j = 0; j < a && ok; ++j)
+            if (j != k) ok = dist2(cand, pos[j]) >= 0.9 * 0.9;
+          if (ok) break;
+        }
+        for (int c = 0; c < 3; ++c) pos[a][c] = cand[c];
+        parent[a] = k;
+      }
+    }
+    const int ao = atom_off[i];
+    for (int k = 0; k < total; ++k) {
+      for (int c = 0; c < 3; ++c) atom_xyz[3 * (ao + k) + c] = (float)pos[k][c];
+      atom_type[ao + k] = k < heavy ? (uint8_t)(1 + g.below(DS_N_TYPES - 1)) : (uint8_t)0;
+    }
+    // bonds: chain then X-H, in atom order of the child
+    const int bo = bond_off[i];
+    for (int k = 1; k < total; ++k) {
+      bonds[2 * (bo + k - 1)] = parent[k];
+      bonds[2 * (bo + k - 1) + 1] = k;
+    }
+    // rotatable bonds: F distinct chain bonds (k, k+1) with k in [0, heavy-3], ascending;
+    // the moving side is the tail component minus axis_end (DESIGN.md §3 P13)
+    Rng fr((uint64_t)seed, kStreamFrag, (uint64_t)gi);
+    int cand_bonds[DS_MAX_ATOMS];
+    const int nb = heavy - 2;
+    for (int k = 0; k < nb; ++k) cand_bonds[k] = k;
+    for (int f = 0; f < frags; ++f) {  // partial Fisher-Yates
+      int j = f + (int)fr.below((uint32_t)(nb - f));
+      std::swap(cand_bonds[f], cand_bonds[j]);
+    }
+    std::sort(cand_bonds, cand_bonds + frags);
+    const int fo = frag_off[i];
+    for (int f = 0; f < frags; ++f) {
+      const int k = cand_bonds[f];
+      frag_axis[2 * (fo + f)] = k;
+      frag_axis[2 * (fo + f) + 1] = k + 1;
+      uint32_t *m = frag_mask + (size_t)DS_MASK_WORDS * (fo + f);
+      for (int w = 0; w < DS_MASK_WORDS; ++w) m[w] = 0;
+      for (int t = 0; t < total; ++t) {
+        const int root = t < heavy ? t : parent[t];
+        if (root >= k + 1 && t != k + 1) m[t >> 5] |= 1u << (t & 31);
+      }
+    }
+  }
+  return DS_OK;
+}
+
+int ds_pack_ligands(int32_t count, const int32_t *atom_off, const float *atom_xyz, const uint8_t *atom_type,
+                    const int32_t *frag_off, const int32_t *frag_axis, const uint32_t *frag_mask, const char *ids,
+                    const int64_t *id_off, float *atom_xyzt, uint32_t *frag_desc, uint64_t *id_hash, float *centroid,
+                    int32_t *bad_index) {
+  if (count < 0 || !atom_off || !atom_xyz || !atom_type || !frag_off || !atom_xyzt || !frag_desc || !id_hash)
+    return DS_ERR_INVALID_ARG;
+  int first_bad = -1, first_code = DS_OK;
+#pragma omp parallel for schedule(static)
+  for (int32_t i = 0; i < count; ++i) {
+    const int a0 = atom_off[i], A = atom_off[i + 1] - a0;
+    int code = DS_OK;
+    if (A < 1) code = DS_ERR_INVALID_ARG;
+    else if (A > DS_MAX_ATOMS) code = DS_ERR_TOO_MANY_ATOMS;
+    for (int k = 0; k < A && code == DS_OK; ++k)
+      if (atom_type[a0 + k] >= DS_N_TYPES) code = DS_ERR_INDEX_OUT_OF_RANGE;
+    for (int f = frag_off[i]; f < frag_off[i + 1] && code == DS_OK; ++f) {
+      const int b = frag_axis[2 * f], e = frag_axis[2 * f + 1];
+      if (b < 0 || e < 0 || b >= A || e >= A) { code = DS_ERR_INDEX_OUT_OF_RANGE; break; }
+      const uint32_t *m = frag_mask + (size_t)DS_MASK_WORDS * f;
+      int pop = 0;
+      for (int w = 0; w < DS_MASK_WORDS; ++w) {
+        uint32_t valid = (A >= 32 * (w + 1)) ? 0xFFFFFFFFu : (A <= 32 * w ? 0u : ((1u << (A - 32 * w)) - 1u));
+        if (m[w] & ~valid) { code = DS_ERR_INDEX_OUT_OF_RANGE; break; }
+        pop += __builtin_popcount(m[w]);
+      }
+      if (code != DS_OK) break;
+      const bool b_in = (m[b >> 5] >> (b & 31)) & 1, e_in = (m[e >> 5] >> (e & 31)) & 1;
+      // axis atoms distinct and outside the mask; mask non-empty proper subset
+      if (b == e || b_in || e_in || pop == 0 || pop > A - 2) code = DS_ERR_MALFORMED_FRAGMENT;
+    }
+    if (code != DS_OK) {
+#pragma omp critical
+      {
+        if (first_bad < 0 || i < first_bad) { first_bad = i; first_code = code; }
+      }
+      continue;
+    }
+    // c0 = f32(f64 sequential mean), d = f32(p - c0)   (DESIGN.md §3 P2)
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < A; ++k)
+      for (int c = 0; c < 3; ++c) s[c] += (double)atom_xyz[3 * (a0 + k) + c];
+    float c0[3];
+    for (int c = 0; c < 3; ++c) c0[c] = (float)(s[c] / (double)A);
+    for (int k = 0; k < A; ++k) {
+      float *o = atom_xyzt + 4 * (size_t)(a0 + k);
+      for (int c = 0; c < 3; ++c) o[c] = atom_xyz[3 * (a0 + k) + c] - c0[c];
+      o[3] = (float)atom_type[a0 + k];
+    }
+    if (centroid)
+      for (int c = 0; c < 3; ++c) centroid[3 * i + c] = c0[c];
+    for (int f = frag_off[i]; f < frag_off[i + 1]; ++f) {
+      uint32_t *d = frag_desc + (size_t)DS_FRAG_WORDS * f;
+      for (int w = 0; w < DS_MASK_WORDS; ++w) d[w] = frag_mask[(size_t)DS_MASK_WORDS * f + w];
+      d[5] = (uint32_t)frag_axis[2 * f] | ((uint32_t)frag_axis[2 * f + 1] << 8);
+      d[6] = d[7] = 0;
+    }
+    if (ids) id_hash[i] = ds_ligand_id_hash(ids + id_off[i], (size_t)(id_off[i + 1] - id_off[i]));
+  }
+  if (first_bad >= 0) {
+    if (bad_index) *bad_index = first_bad;
+    return first_code;
+  }
+  return DS_OK;
+}
+
+int ds_generate_pocket_atoms(int64_t seed, int32_t n, float rmin, float rmax, float *atom_xyz, uint8_t *atom_type) {
+  if (n < 0 || !atom_xyz || !atom_type || !(rmax > 0) || rmin < 0 || rmin > rmax) return DS_ERR_INVALID_ARG;
+  Rng r((uint64_t)seed, kStreamPocket, 0);
+  const double lo2 = (double)rmin * rmin, hi2 = (double)rmax * rmax;
+  for (int32_t i = 0; i < n; ++i) {
+    double p[3];
+    for (;;) {
+      for (int c = 0; c < 3; ++c) p[c] = (2.0 * r.u01() - 1.0) * (double)rmax;
+      double q = p[0] * p[0] + p[1] * p[1] + p[2] * p[2];
+      if (q >= lo2 && q <= hi2) break;
+    }
+    for (int c = 0; c < 3; ++c) atom_xyz[3 * i + c] = (float)p[c];
+    atom_type[i] = (uint8_t)(1 + r.below(DS_N_TYPES - 1));
+  }
+  return DS_OK;
+}
+
+int ds_build_pocket_grid(const float *atom_xyz, int32_t n_atoms, float spacing, float padding, float origin[3],
+                         int32_t dims[3], int32_t *values) {
+  if (n_atoms <= 0) return DS_ERR_EMPTY_POCKET;
+  if (!atom_xyz || !(spacing > 0) || padding < 0 || !origin || !dims) return DS_ERR_INVALID_ARG;
+  double lo[3], hi[3];
+  for (int c = 0; c < 3; ++c) lo[c] = hi[c] = atom_xyz[c];
+  for (int i = 1; i < n_atoms; ++i)
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = std::min(lo[c], (double)atom_xyz[3 * i + c]);
+      hi[c] = std::max(hi[c], (double)atom_xyz[3 * i + c]);
+    }
+  for (int c = 0; c < 3; ++c) {
+    origin[c] = (float)(lo[c] - (double)padding);
+    double span = (hi[c] + (double)padding) - (double)origin[c];
+    dims[c] = (int32_t)ceil(span / (double)spacing - 1e-9) + 1;
+    if (dims[c] < 1) dims[c] = 1;
+  }
+  if (!values) return DS_OK;
+  const int nx = dims[0], ny = dims[1], nz = dims[2];
+#pragma omp parallel for schedule(static) collapse(2)
+  for (int z = 0; z < nz; ++z)
+    for (int y = 0; y < ny; ++y)
+      for (int x = 0; x < nx; ++x) {
+        const double node[3] = {(double)origin[0] + x * (double)spacing, (double)origin[1] + y * (double)spacing,
+                                (double)origin[2] + z * (double)spacing};
+        double best = INFINITY;
+        for (int i = 0; i < n_atoms; ++i) {
+          const double a[3] = {atom_xyz[3 * i], atom_xyz[3 * i + 1], atom_xyz[3 * i + 2]};
+          best = std::min(best, dist2(node, a));
+        }
+        const double d = sqrt(best);
+        // g(d): -1 at contact -> +1 at 3 Å, flat to 5 Å, -> -1 at 8 Å, -1 beyond (P18)
+        double g;
+        if (d <= 3.0) g = -1.0 + 2.0 * d / 3.0;
+        else if (d <= 5.0) g = 1.0;
+        else if (d <= 8.0) g = 1.0 - 2.0 * (d - 5.0) / 3.0;
+        else g = -1.0;
+        values[(size_t)x + (size_t)nx * ((size_t)y + (size_t)ny * z)] = (int32_t)nearbyint(10.0 * g);
+      }
+  return DS_OK;
+}
+
+int ds_default_table(int64_t seed, float *table) {
+  if (!table) return DS_ERR_INVALID_ARG;
+  Rng r((uint64_t)seed, kStreamTable, 0);
+  for (int i = 0; i < DS_N_TYPES; ++i)
+    for (int j = i; j < DS_N_TYPES; ++j) {
+      float w = (float)(2.0 * r.u01() - 1.0);
+      table[i * DS_N_TYPES + j] = table[j * DS_N_TYPES + i] = w;
+    }
+  return DS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,54 @@
+// Kernel parameter blocks shared by ds_kernels.cu and ds_api.cu.
+#pragma once
+#include "ds_device.cuh"
+
+namespace ds {
+
+struct PocketView {
+  const int8_t *grid;        // nx*ny*nz values + sentinel (= kOutside) at index nx*ny*nz
+  GridGeom g;
+  int grid_bytes;            // padded to 16 B (includes the sentinel)
+  float inv_s, spacing;
+  float ox, oy, oz;
+  int n_atoms;
+  const float4 *patoms;      // pocket atoms in the grid frame, .w = element code
+  const int32_t *wfx;        // [16][16][nb+1] fixed-point table*mult (2^-24); entry nb = 0
+  int nb;
+  float ub2[DS_MAX_BINS];    // squared bin upper bounds, grid frame
+  const float2 *trig;        // (cos, sin) of integer degrees 0..359 (f32 of f64)
+};
+
+struct BatchView {
+  int L;
+  const int *atom_off;       // L+1
+  const float4 *atoms;       // centred coords + type
+  const int *frag_off;       // L+1
+  const uint4 *frags;        // 2 uint4 per fragment (mask words 0..4, axis word 5)
+  const uint64_t *idh;
+};
+
+struct DockParams {
+  int N, K;
+  int n_a, step_a, n_rot;
+  int n_t, step_t;
+  int64_t seed;
+  int early_exit;
+  float bd2;                 // squared bump distance, grid frame
+  float eps_axis;            // DegenerateAxis threshold, grid frame
+  double thr2;               // squared similarity RMSD, grid frame
+};
+
+struct AlignOut {
+  uint32_t *keys;            // L*N packed (score+32768)<<16 | (65535-rot)
+};
+
+struct OptOut {
+  ds_result *res;            // L
+  ds_restart_record *rrec;   // L*N (may be null)
+  uint8_t *rtors;            // frag_total*N (always)
+  float4 *final_u;           // scratch: per ligand slot? no: per global warp N*160
+  float *best_coords;        // atom_total*3 (may be null)
+  uint8_t *best_tors;        // frag_total (may be null)
+};
+
+}  // namespace ds

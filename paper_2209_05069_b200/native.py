@@ -1,0 +1,438 @@
+"""ctypes binding of libdockscreen.so (include/dockscreen.h) and the packed batch layout.
+
+This is the B200 occupant of the reference's native slot `dockscreen.kernels._core`
+(pkg/setup.py:10-18).  The reference falls back to NumPy when its extension is missing
+(pkg/setup.py:21-22); this package has NO fallback: `lib()` raises NativeUnavailable when the
+shared library is absent, and every docking call raises when no CUDA device is visible.
+ctypes releases the GIL for the duration of each call, so engine threads overlap.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import model
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdockscreen.so")
+
+DS_OK = 0
+ERRORS = {
+    -1: ValueError, -2: model.TooManyAtoms, -3: model.MalformedFragment, -4: model.IndexOutOfRange,
+    -5: model.DegenerateAxis, -6: model.EmptyPocket, -7: model.InfeasibleShape,
+}
+STATUS_OK, STATUS_NO_VALID_POSE, STATUS_DEGENERATE_AXIS = 0, 1, 2
+FAMILY_BATCHED, FAMILY_LATENCY = 0, 1
+MASK_WORDS, FRAG_WORDS, MAX_RESTARTS, TORSION_NONE = 5, 8, 32, 255
+CHEM_SCALE = float(1 << 24)
+
+
+class NativeUnavailable(RuntimeError):
+    """libdockscreen.so is missing or a CUDA device is not usable — no fallback exists."""
+
+
+class DsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libdockscreen error {code}: {msg}")
+        self.code = code
+
+
+# ---- ABI structs (mirror include/dockscreen.h) -----------------------------------------
+class PocketDesc(C.Structure):
+    _fields_ = [("origin", C.c_float * 3), ("spacing", C.c_float), ("dims", C.c_int32 * 3),
+                ("n_atoms", C.c_int32), ("values", C.c_void_p), ("atom_xyz", C.c_void_p),
+                ("atom_type", C.c_void_p), ("table", C.c_void_p), ("n_bins", C.c_int32),
+                ("bin_ub", C.c_void_p), ("bin_mult", C.c_void_p)]
+
+
+class DockConfigC(C.Structure):
+    _fields_ = [("restarts_n", C.c_int32), ("rescore_top_k", C.c_int32), ("alignment_step_deg", C.c_int32),
+                ("torsion_step_deg", C.c_int32), ("bump_distance", C.c_float), ("similarity_rmsd", C.c_float),
+                ("rescore_cutoff", C.c_float), ("early_exit", C.c_int32), ("seed", C.c_int64)]
+
+
+class BatchDesc(C.Structure):
+    _fields_ = [("n_ligands", C.c_int32), ("reserved", C.c_int32), ("atom_off", C.c_void_p),
+                ("atom_xyzt", C.c_void_p), ("frag_off", C.c_void_p), ("frag_desc", C.c_void_p),
+                ("id_hash", C.c_void_p)]
+
+
+class Outputs(C.Structure):
+    _fields_ = [("results", C.c_void_p), ("best_coords", C.c_void_p), ("best_torsion", C.c_void_p),
+                ("restarts", C.c_void_p), ("restart_torsion", C.c_void_p)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("total_ms", C.c_float), ("align_ms", C.c_float), ("optimize_ms", C.c_float),
+                ("launches", C.c_int32), ("reserved", C.c_int32), ("h2d_bytes", C.c_int64),
+                ("d2h_bytes", C.c_int64)]
+
+
+RESULT_DTYPE = np.dtype([("status", "<i4"), ("geom_score", "<i4"), ("chem_fx", "<i8"), ("best_restart", "u1"),
+                         ("best_ax", "u1"), ("best_ay", "u1"), ("n_kept", "u1"), ("poses_scored", "<u4"),
+                         ("bump_checks", "<u4"), ("bump_early_exits", "<u4")])
+RESTART_DTYPE = np.dtype([("align_score", "<i4"), ("final_geom", "<i4"), ("ax", "u1"), ("ay", "u1"),
+                          ("valid", "u1"), ("kept", "u1"), ("reserved", "<i4")])
+assert RESULT_DTYPE.itemsize == 32 and RESTART_DTYPE.itemsize == 16
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+def lib():
+    """Load libdockscreen.so (fails loudly; there is no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeUnavailable(f"{LIB_PATH} not built (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
+        sig = {
+            "ds_abi_version": (C.c_int, []), "ds_last_error": (C.c_char_p, []),
+            "ds_device_count": (C.c_int, [vp]), "ds_create": (C.c_int, [C.c_int, vp]),
+            "ds_destroy": (None, [vp]), "ds_ctx_alloc_count": (C.c_int, [vp, vp]),
+            "ds_ctx_stream": (vp, [vp]), "ds_synchronize": (C.c_int, [vp]),
+            "ds_pocket_create": (C.c_int, [vp, vp, vp]), "ds_pocket_destroy": (None, [vp]),
+            "ds_dock": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, vp]),
+            "ds_batch_upload": (C.c_int, [vp, vp, vp]),
+            "ds_dock_resident": (C.c_int, [vp, vp, vp, vp, C.c_int, vp]),
+            "ds_batch_download": (C.c_int, [vp, vp, vp]), "ds_batch_destroy": (None, [vp]),
+            "ds_query_capacity": (C.c_int, [vp, C.c_int, vp]),
+            "ds_op_grid_score": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp]),
+            "ds_op_rescore": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_float, vp]),
+            "ds_ligand_id_hash": (u64, [C.c_char_p, C.c_size_t]),
+            "ds_generated_id": (C.c_int, [i64, i64, C.c_char_p, C.c_size_t]),
+            "ds_mixed_shapes": (C.c_int, [i64, i64, i32, i32, i32, i32, vp]),
+            "ds_generate_ligands": (C.c_int, [i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+            "ds_pack_ligands": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+            "ds_generate_pocket_atoms": (C.c_int, [i64, i32, C.c_float, C.c_float, vp, vp]),
+            "ds_build_pocket_grid": (C.c_int, [vp, i32, C.c_float, C.c_float, vp, vp, vp]),
+            "ds_default_table": (C.c_int, [i64, vp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        if L.ds_abi_version() != 1:
+            raise NativeUnavailable("libdockscreen ABI mismatch")
+        _lib = L
+        return L
+
+
+def check(rc: int):
+    if rc != DS_OK:
+        msg = lib().ds_last_error().decode(errors="replace")
+        exc = ERRORS.get(rc)
+        if exc is not None:
+            raise exc(msg)
+        if rc in (-9, -10):
+            raise NativeUnavailable(msg)
+        raise DsError(rc, msg)
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    rc = lib().ds_device_count(C.byref(n))
+    return int(n.value) if rc == DS_OK else 0
+
+
+# ---- ligand batches --------------------------------------------------------------------
+@dataclass
+class LigandBatch:
+    """CSR ligand batch in the reference's terms (absolute Å coordinates, element codes,
+    bonds, fragments with moving-mask bitsets) plus the ids."""
+    atom_off: np.ndarray      # int32 [n+1]
+    atom_xyz: np.ndarray      # float32 [atoms, 3]
+    atom_type: np.ndarray     # uint8 [atoms]
+    bond_off: np.ndarray      # int32 [n+1]
+    bonds: np.ndarray         # int32 [bonds, 2]
+    frag_off: np.ndarray      # int32 [n+1]
+    frag_axis: np.ndarray     # int32 [frags, 2]
+    frag_mask: np.ndarray     # uint32 [frags, 5]
+    ids: List[str]
+
+    @property
+    def n(self) -> int:
+        return len(self.atom_off) - 1
+
+    def n_atoms(self) -> np.ndarray:
+        return np.diff(self.atom_off)
+
+    def n_frags(self) -> np.ndarray:
+        return np.diff(self.frag_off)
+
+    def id_bytes(self):
+        enc = [s.encode() for s in self.ids]
+        off = np.zeros(len(enc) + 1, dtype=np.int64)
+        off[1:] = np.cumsum([len(e) for e in enc])
+        return b"".join(enc), off
+
+    def subset(self, idx: Sequence[int]) -> "LigandBatch":
+        return LigandBatch.from_ligands([self.ligand(int(i)) for i in idx])
+
+    def ligand(self, i: int) -> model.Ligand:
+        a0, a1 = int(self.atom_off[i]), int(self.atom_off[i + 1])
+        atoms = tuple(model.Atom.of(*self.atom_xyz[k], int(self.atom_type[k])) for k in range(a0, a1))
+        b0, b1 = int(self.bond_off[i]), int(self.bond_off[i + 1])
+        bonds = tuple((int(a), int(b)) for a, b in self.bonds[b0:b1])
+        frags = []
+        for f in range(int(self.frag_off[i]), int(self.frag_off[i + 1])):
+            bits = self.frag_mask[f]
+            mask = frozenset(k for k in range(a1 - a0) if (int(bits[k >> 5]) >> (k & 31)) & 1)
+            frags.append(model.Fragment(int(self.frag_axis[f, 0]), int(self.frag_axis[f, 1]), mask))
+        return model.Ligand(self.ids[i], atoms, bonds, tuple(frags))
+
+    def to_ligands(self) -> List[model.Ligand]:
+        return [self.ligand(i) for i in range(self.n)]
+
+    @staticmethod
+    def from_ligands(ligands: Sequence[model.Ligand]) -> "LigandBatch":
+        n = len(ligands)
+        na = np.array([len(l.atoms) for l in ligands], dtype=np.int32)
+        nb = np.array([len(l.bonds) for l in ligands], dtype=np.int32)
+        nf = np.array([len(l.fragments) for l in ligands], dtype=np.int32)
+        off = lambda c: np.concatenate([[0], np.cumsum(c)]).astype(np.int32)
+        xyz = np.zeros((int(na.sum()), 3), dtype=np.float32)
+        typ = np.zeros(int(na.sum()), dtype=np.uint8)
+        bonds = np.zeros((int(nb.sum()), 2), dtype=np.int32)
+        axis = np.zeros((int(nf.sum()), 2), dtype=np.int32)
+        mask = np.zeros((int(nf.sum()), MASK_WORDS), dtype=np.uint32)
+        ao, bo, fo = off(na), off(nb), off(nf)
+        for i, l in enumerate(ligands):
+            if len(l.atoms) > model.MAX_ATOMS:
+                raise model.TooManyAtoms(f"{l.id}: {len(l.atoms)} atoms")
+            if l.atoms:
+                xyz[ao[i]:ao[i + 1]] = np.array([a.position for a in l.atoms], dtype=np.float32)
+                typ[ao[i]:ao[i + 1]] = [a.element_type for a in l.atoms]
+            if l.bonds:
+                bonds[bo[i]:bo[i + 1]] = np.array(l.bonds, dtype=np.int32)
+            for k, f in enumerate(l.fragments):
+                axis[fo[i] + k] = (f.axis_begin, f.axis_end)
+                for m in f.moving_mask:
+                    if not (0 <= m < model.MAX_ATOMS):
+                        raise model.IndexOutOfRange(f"{l.id}: mask index {m}")
+                    mask[fo[i] + k, m >> 5] |= np.uint32(1 << (m & 31))
+        return LigandBatch(ao, xyz, typ, bo, bonds, fo, axis, mask, [l.id for l in ligands])
+
+
+@dataclass
+class PackedBatch:
+    """The ds_batch_desc layout (centred coordinates, fragment records, id hashes)."""
+    n: int
+    atom_off: np.ndarray
+    atom_xyzt: np.ndarray     # float32 [atoms, 4]
+    frag_off: np.ndarray
+    frag_desc: np.ndarray     # uint32 [frags, 8]
+    id_hash: np.ndarray       # uint64 [n]
+    centroid: np.ndarray      # float32 [n, 3]
+
+    def desc(self) -> BatchDesc:
+        d = BatchDesc()
+        d.n_ligands = self.n
+        d.atom_off = _p(self.atom_off)
+        d.atom_xyzt = _p(self.atom_xyzt)
+        d.frag_off = _p(self.frag_off)
+        d.frag_desc = _p(self.frag_desc)
+        d.id_hash = _p(self.id_hash)
+        return d
+
+
+def pack(batch: LigandBatch) -> PackedBatch:
+    """Validate + pack (ds_pack_ligands): c0 = f32(f64 mean), d = p - c0 (DESIGN.md §3 P2)."""
+    n = batch.n
+    na, nf = int(batch.atom_off[-1]), int(batch.frag_off[-1])
+    xyzt = np.zeros((max(na, 1), 4), dtype=np.float32)
+    fdesc = np.zeros((max(nf, 1), FRAG_WORDS), dtype=np.uint32)
+    idh = np.zeros(max(n, 1), dtype=np.uint64)
+    cen = np.zeros((max(n, 1), 3), dtype=np.float32)
+    ids, id_off = batch.id_bytes()
+    idbuf = C.create_string_buffer(ids, max(len(ids), 1))
+    bad = C.c_int32(-1)
+    c = lambda a: np.ascontiguousarray(a)
+    ao, xyz, typ = c(batch.atom_off.astype(np.int32)), c(batch.atom_xyz.astype(np.float32)), c(batch.atom_type.astype(np.uint8))
+    fo, fax, fm = c(batch.frag_off.astype(np.int32)), c(batch.frag_axis.astype(np.int32)), c(batch.frag_mask.astype(np.uint32))
+    if fax.size == 0:
+        fax = np.zeros((1, 2), np.int32)
+        fm = np.zeros((1, MASK_WORDS), np.uint32)
+    rc = lib().ds_pack_ligands(n, _p(ao), _p(xyz), _p(typ), _p(fo), _p(fax), _p(fm), C.cast(idbuf, C.c_void_p),
+                               _p(id_off), _p(xyzt), _p(fdesc), _p(idh), _p(cen), C.byref(bad))
+    if rc != DS_OK:
+        msg = lib().ds_last_error().decode(errors="replace")
+        exc = ERRORS.get(rc, DsError)
+        who = batch.ids[bad.value] if 0 <= bad.value < n else "?"
+        raise exc(f"ligand {who}: invalid ({rc}) {msg}")
+    return PackedBatch(n, ao, xyzt, fo, fdesc, idh[:n] if n else idh[:0], cen)
+
+
+# ---- pockets / tables ------------------------------------------------------------------
+DEFAULT_BINS = ((2.0, 0.5), (4.0, 1.0), (6.0, 0.5), (8.0, 0.25))   # DESIGN.md §3 P11
+
+
+@dataclass(frozen=True)
+class InteractionTable:
+    """16x16 symmetric weights + ascending (upper_bound, multiplier) bins."""
+    table: np.ndarray
+    bins: tuple = DEFAULT_BINS
+
+    @staticmethod
+    def default(seed: int = 11) -> "InteractionTable":
+        t = np.zeros(256, dtype=np.float32)
+        check(lib().ds_default_table(seed, _p(t)))
+        return InteractionTable(t.reshape(16, 16), DEFAULT_BINS)
+
+    @property
+    def cutoff(self) -> float:
+        return float(self.bins[-1][0])
+
+
+class DevicePocket:
+    """A pocket + interaction table uploaded to one context (shared read-only)."""
+
+    def __init__(self, ctx: "Context", pocket: model.Pocket, table: InteractionTable):
+        self.ctx, self.pocket, self.table = ctx, pocket, table
+        xyz, typ = pocket.atom_arrays()
+        self._keep = [pocket.grid_values, np.ascontiguousarray(xyz), np.ascontiguousarray(typ),
+                      np.ascontiguousarray(table.table, dtype=np.float32).reshape(-1),
+                      np.array([b[0] for b in table.bins], dtype=np.float32),
+                      np.array([b[1] for b in table.bins], dtype=np.float32)]
+        d = PocketDesc()
+        for k in range(3):
+            d.origin[k] = float(pocket.grid_origin[k])
+            d.dims[k] = int(pocket.grid_dims[k])
+        d.spacing = float(pocket.grid_spacing)
+        d.n_atoms = len(typ)
+        d.values, d.atom_xyz, d.atom_type, d.table, _, _ = (_p(a) for a in self._keep)
+        d.n_bins = len(table.bins)
+        d.bin_ub, d.bin_mult = _p(self._keep[4]), _p(self._keep[5])
+        h = C.c_void_p()
+        check(lib().ds_pocket_create(ctx.handle, C.byref(d), C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            lib().ds_pocket_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def config_c(cfg: model.DockConfig, seed: int = 0) -> DockConfigC:
+    c = DockConfigC()
+    c.restarts_n, c.rescore_top_k = cfg.restarts_n, cfg.rescore_top_k
+    c.alignment_step_deg, c.torsion_step_deg = cfg.alignment_step_deg, cfg.torsion_step_deg
+    c.bump_distance, c.similarity_rmsd, c.rescore_cutoff = cfg.bump_distance, cfg.similarity_rmsd, cfg.rescore_cutoff
+    c.early_exit = 1 if cfg.early_exit else 0
+    c.seed = int(seed)
+    return c
+
+
+@dataclass
+class DockOutput:
+    results: np.ndarray               # RESULT_DTYPE [n]
+    best_coords: Optional[np.ndarray]  # float32 [atoms, 3]
+    best_torsion: Optional[np.ndarray]  # uint8 [frags]
+    restarts: Optional[np.ndarray]     # RESTART_DTYPE [n, N]
+    restart_torsion: Optional[np.ndarray]  # uint8 [frags, N]
+    stats: Stats
+
+
+class Context:
+    """ds_ctx: one CUDA stream + workspaces on one device."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().ds_create(int(device), C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def alloc_count(self) -> int:
+        n = C.c_int64(0)
+        check(lib().ds_ctx_alloc_count(self.handle, C.byref(n)))
+        return int(n.value)
+
+    def pocket(self, pocket: model.Pocket, table: Optional[InteractionTable] = None) -> DevicePocket:
+        return DevicePocket(self, pocket, table or InteractionTable.default())
+
+    def dock(self, dpocket: DevicePocket, packed: PackedBatch, cfg: model.DockConfig, seed: int = 0,
+             family: int = FAMILY_BATCHED, coords: bool = True, detail: bool = False) -> DockOutput:
+        n, N = packed.n, cfg.restarts_n
+        na, nf = int(packed.atom_off[-1]) if n else 0, int(packed.frag_off[-1]) if n else 0
+        res = np.zeros(max(n, 1), dtype=RESULT_DTYPE)
+        bc = np.zeros((max(na, 1), 3), dtype=np.float32) if coords else None
+        bt = np.zeros(max(nf, 1), dtype=np.uint8)
+        rr = np.zeros((max(n, 1), N), dtype=RESTART_DTYPE) if detail else None
+        rt = np.zeros((max(nf, 1), N), dtype=np.uint8) if detail else None
+        out = Outputs(_p(res), _p(bc), _p(bt), _p(rr), _p(rt))
+        st = Stats()
+        ccfg = config_c(cfg, seed)
+        check(lib().ds_dock(self.handle, dpocket.handle, C.byref(packed.desc()), C.byref(ccfg), int(family),
+                            C.byref(out), C.byref(st)))
+        return DockOutput(res[:n], bc[:na] if bc is not None else None, bt[:nf],
+                          rr[:n] if rr is not None else None, rt[:nf] if rt is not None else None, st)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().ds_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class ResidentBatch:
+    """A packed batch kept in device memory (kernel-only timing, bench.py `value`)."""
+
+    def __init__(self, ctx: Context, packed: PackedBatch):
+        h = C.c_void_p()
+        check(lib().ds_batch_upload(ctx.handle, C.byref(packed.desc()), C.byref(h)))
+        self.ctx, self.packed, self.handle = ctx, packed, h
+
+    def dock(self, dpocket: DevicePocket, cfg: model.DockConfig, seed: int = 0, family: int = FAMILY_BATCHED) -> Stats:
+        st = Stats()
+        ccfg = config_c(cfg, seed)
+        check(lib().ds_dock_resident(self.ctx.handle, dpocket.handle, self.handle, C.byref(ccfg), int(family),
+                                     C.byref(st)))
+        return st
+
+    def download(self) -> np.ndarray:
+        res = np.zeros(max(self.packed.n, 1), dtype=RESULT_DTYPE)
+        out = Outputs(_p(res), None, None, None, None)
+        check(lib().ds_batch_download(self.ctx.handle, self.handle, C.byref(out)))
+        return res[:self.packed.n]
+
+    def close(self):
+        if self.handle:
+            lib().ds_batch_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
