@@ -23,6 +23,8 @@ void launch_optimize_batched(const PocketView &pk, const BatchView &bt, const Do
                              const uint32_t *keys, OptOut out, int *queue, int blocks, int warps, size_t smem,
                              cudaStream_t st);
 size_t optimize_warp_smem_bytes();
+size_t optimize_cta_smem_bytes(int n_patoms, int nb);
+int optimize_blocks_per_sm(int warps, size_t smem);
 void launch_grid_score(const PocketView &pk, const float *coords, int n_atoms, int n_poses, int32_t *out,
                        cudaStream_t st);
 void launch_rescore(const PocketView &pk, const float *coords, const uint8_t *types, int n_atoms, int n_poses,
@@ -205,6 +207,7 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
   if (!d->values) return fail(DS_ERR_INVALID_ARG, "grid values NULL");
   if (d->n_atoms < 0 || (d->n_atoms > 0 && (!d->atom_xyz || !d->atom_type)))
     return fail(DS_ERR_INVALID_ARG, "bad pocket atoms");
+  if (d->n_atoms > 4096) return fail(DS_ERR_UNSUPPORTED, "at most 4096 pocket atoms (staged in shared memory)");
   if (!d->table || d->n_bins < 1 || d->n_bins > DS_MAX_BINS || !d->bin_ub || !d->bin_mult)
     return fail(DS_ERR_INVALID_ARG, "bad interaction table");
   for (int b = 1; b < d->n_bins; ++b)
@@ -472,10 +475,10 @@ int run_batched(ds_ctx *c, const ds_pocket *pk, int L, int NA, int NF, const Doc
   launch_align_batched(pk->view, bt, dp, (const int *)c->b_order_a.p, ao, queue, in_smem, c->sm_count, warps_a, smem_a,
                        c->stream);
   cudaEventRecord(c->ev[2], c->stream);
-  // --- optimisation + select + rescore: warp per ligand ---
+  // --- optimisation + select + rescore: warp per ligand, persistent, occupancy-sized ---
   const int warps_o = 8;
-  const size_t smem_o = optimize_warp_smem_bytes() * warps_o;
-  int per_sm = std::max(1, (int)std::min<size_t>(4, c->smem_optin / std::max<size_t>(smem_o, 1)));
+  const size_t smem_o = optimize_cta_smem_bytes(pk->view.n_atoms, pk->view.nb) + optimize_warp_smem_bytes() * warps_o;
+  const int per_sm = std::max(1, optimize_blocks_per_sm(warps_o, smem_o));
   const int blocks_o = c->sm_count * per_sm;
   int rc;
   if ((rc = c->ensure(c->b_scratch, sizeof(float4) * (size_t)blocks_o * warps_o * dp.N * DS_MAX_ATOMS))) return rc;

@@ -2,29 +2,36 @@
 // SPEC.md:257-285) — batched family, one warp per ligand.
 //
 // Per restart the warp rebuilds the aligned pose from the packed argmax key of the alignment
-// kernel, then walks the fragments in list order.  Per fragment it compacts the moving set M and
-// the bump-relevant complement C' (= not M, not an axis atom) into shared memory with ballots, and
-// for every torsion angle rotates M, runs the M x C' bump scan in lexicographic pair order in
-// rounds of 32 with a warp-uniform early exit (__any_sync — the zero-cost exit that makes the
-// batched shape win), and scores clean angles as base + sum over M (the
-// non-moving atoms' grid values do not change with the angle).  The best clean angle is
-// committed before the next fragment.  Then select_poses (heavy-atom RMSD,
-// f64, lanes over pose pairs) and an integer fixed-point rescore (order-free, exact).
+// kernel, then walks the fragments in list order (they are stateful).  Per
+// fragment it compacts the moving set M and the bump-relevant complement C' (not M, not an axis
+// atom) into shared memory with ballots, and then sweeps ALL torsion angles at once: lanes own
+// (angle, moving atom) slots, rotate their atom in registers, and scan C' broadcast from shared
+// memory (one LDS.128 per complement atom per warp).  A bump retires every lane of that angle at
+// the next chunk boundary (__ballot_sync + __match_any_sync) — the early exit costs one vote per
+// chunk, which is why the batched shape wins.  Clean angles are scored as
+// base + sum over M (the non-moving atoms' grid values do not depend on the angle) with exact
+// integer shared-memory adds, and the best clean angle (ties -> smallest) is committed.
+// Then select_poses (heavy-atom RMSD in f64, lanes over pose pairs) and an integer fixed-point
+// rescore (order-free, exact) with the pocket atoms and the weight table staged in shared memory.
 #include "ds_kernels.cuh"
 
 namespace ds {
 
 constexpr int kMaxA = DS_MAX_ATOMS;
+constexpr int kChunk = 8;            // complement atoms between early-exit votes
 
 struct OptWarpSmem {
   float4 u[kMaxA];       // committed pose of the current restart (grid frame), .w = type
-  float4 wk[kMaxA];      // [0, nM): moving atoms at the current angle; [kMaxA-1-c]: complement atom c
+  float4 cmp[kMaxA + kChunk];  // compacted complement C' of the current fragment (+ far sentinels)
   uint8_t mlist[kMaxA];  // moving atom indices in ascending order
+  int ascore[32];        // per-angle sums over M (current angle block)
+  unsigned abump;        // bumped-angle bits (current angle block)
+  unsigned pad[3];
   int geom[DS_MAX_RESTARTS];
   int valid[DS_MAX_RESTARTS];
   unsigned dis[DS_MAX_RESTARTS];   // dissimilarity bitsets (select_poses)
   int ord[DS_MAX_RESTARTS];
-  long long chem[DS_MAX_RESTARTS];
+  int kept[DS_MAX_RESTARTS];
 };
 
 __device__ __forceinline__ int grid_val(const PocketView &pk, int idx) { return (int)__ldg(pk.grid + idx); }
@@ -37,13 +44,73 @@ __device__ __forceinline__ long long warp_sum64(long long v) {
   return v;
 }
 
+// rotated position of a moving atom for torsion angle index k (k == 0: identity, P8)
+__device__ __forceinline__ float3 torsion_pos(const PocketView &pk, int step_t, int k, float kx, float ky, float kz,
+                                              float3 a, float4 p) {
+  if (k == 0) return make_float3(p.x, p.y, p.z);
+  const float2 cs = pk.trig[k * step_t];
+  float R[9];
+  torsion_matrix(kx, ky, kz, cs.x, cs.y, R);
+  return torsion_apply(R, a, p.x, p.y, p.z);
+}
+
+// rescore sum of one pose against all pocket atoms (P11).  Lanes own pocket atoms (staged in
+// smem with .w = the integer row offset tj*(nb+1)); ligand atoms are broadcast from S.u.
+template <int NB>
+__device__ __forceinline__ long long rescore_pose(const OptWarpSmem &S, int A, const float4 *pat, int P,
+                                                  const int32_t *wfx, int nb, const float *ub2) {
+  long long acc = 0;
+  const int nb1 = NB > 0 ? NB + 1 : nb + 1;
+  float u[DS_MAX_BINS];
+#pragma unroll
+  for (int q = 0; q < DS_MAX_BINS; ++q) u[q] = ub2[q];
+  for (int j0 = 0; j0 < P; j0 += 32) {
+    const int j = j0 + (threadIdx.x & 31);
+    // past-the-end lanes use a far sentinel: its bin is nb, whose weight is 0
+    const float4 y = j < P ? pat[j] : make_float4(1e19f, 1e19f, 1e19f, 0.f);
+    const int32_t *wcol = wfx + __float_as_int(y.w);
+    for (int i = 0; i < A; ++i) {
+      const float4 x = S.u[i];
+      const int row = (int)x.w * DS_N_TYPES * nb1;
+      const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
+      int b = 0;
+      if (NB > 0) {
+#pragma unroll
+        for (int q = 0; q < NB; ++q) b += !(d2 < u[q]);
+      } else {
+        for (int q = 0; q < nb; ++q) b += !(d2 < u[q]);
+      }
+      acc += wcol[row + b];
+    }
+  }
+  return acc;
+}
+
 __global__ void __launch_bounds__(256)
     k_optimize_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
                        OptOut out, int *queue) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  OptWarpSmem &S = reinterpret_cast<OptWarpSmem *>(smem)[warp];
-  const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // per-CTA: pocket atoms + fixed-point weights + bin bounds, then the per-warp scratch
+  const int nb1 = pk.nb + 1;
+  float4 *s_pat = reinterpret_cast<float4 *>(smem);
+  int32_t *s_w = reinterpret_cast<int32_t *>(s_pat + pk.n_atoms);
+  const int wsz = DS_N_TYPES * DS_N_TYPES * nb1;
+  float *s_ub2 = reinterpret_cast<float *>(s_w + wsz);
+  size_t fixed = (size_t)pk.n_atoms * 16 + (size_t)wsz * 4 + DS_MAX_BINS * 4;
+  fixed = (fixed + 15) & ~(size_t)15;
+  OptWarpSmem &S = reinterpret_cast<OptWarpSmem *>(smem + fixed)[warp];
+  for (int j = threadIdx.x; j < pk.n_atoms; j += blockDim.x) {
+    float4 y = __ldg(pk.patoms + j);
+    y.w = __int_as_float((int)y.w * nb1);  // row offset of the pocket atom's type in the weight table
+    s_pat[j] = y;
+  }
+  for (int j = threadIdx.x; j < wsz; j += blockDim.x) s_w[j] = __ldg(pk.wfx + j);
+  if (threadIdx.x < DS_MAX_BINS) s_ub2[threadIdx.x] = pk.ub2[threadIdx.x];
+  __syncthreads();
+  const float4 *pat = s_pat;
+
+  const int gwarp = blockIdx.x * nwarps + warp;
   float4 *scr = out.final_u + (size_t)gwarp * dp.N * kMaxA;  // final poses of the N restarts
   const GridGeom g = pk.g;
   const unsigned lt = lanemask_lt();
@@ -69,13 +136,15 @@ __global__ void __launch_bounds__(256)
       const int rot = 65535 - (int)(key & 0xFFFFu);
       const int align_score = (int)(key >> 16) - 32768;
       const int ix = rot / dp.n_a, iy = rot - ix * dp.n_a;
-      float R0s[9], T[3], M[9];
-      start_params(idh, dp.seed, r, pk.trig, pk.inv_s, g.nx, g.ny, g.nz, R0s, T);
-      align_matrix(pk.trig[ix * dp.step_a], pk.trig[iy * dp.step_a], R0s, M);
-      for (int i = lane; i < A; i += 32) {
-        const float4 d = __ldg(bt.atoms + a0 + i);
-        const float3 u = apply_mt(M, T, d.x, d.y, d.z);
-        S.u[i] = make_float4(u.x, u.y, u.z, d.w);
+      {
+        float R0s[9], T[3], M[9];
+        start_params(idh, dp.seed, r, pk.trig, pk.inv_s, g.nx, g.ny, g.nz, R0s, T);
+        align_matrix(pk.trig[ix * dp.step_a], pk.trig[iy * dp.step_a], R0s, M);
+        for (int i = lane; i < A; i += 32) {
+          const float4 d = __ldg(bt.atoms + a0 + i);
+          const float3 u = apply_mt(M, T, d.x, d.y, d.z);
+          S.u[i] = make_float4(u.x, u.y, u.z, d.w);
+        }
       }
       __syncwarp();
 
@@ -96,15 +165,16 @@ __global__ void __launch_bounds__(256)
           const bool cp = in && !mv && i != ab && i != ae;
           const unsigned bm = __ballot_sync(kFull, mv), bc = __ballot_sync(kFull, cp);
           if (mv) S.mlist[nM + __popc(bm & lt)] = (uint8_t)i;
-          if (cp) S.wk[kMaxA - 1 - (nC + __popc(bc & lt))] = S.u[i];
           if (in && !mv) {
             const float4 p = S.u[i];
+            if (cp) S.cmp[nC + __popc(bc & lt)] = p;
             base += grid_val(pk, node_index(g, p.x, p.y, p.z));
           }
           nM += __popc(bm);
           nC += __popc(bc);
         }
         base = warp_sum(base);
+        if (lane < kChunk) S.cmp[nC + lane] = make_float4(1e19f, 1e19f, 1e19f, 0.f);
         const float4 pa = S.u[ab], pb = S.u[ae];
         const float3 a3 = make_float3(pa.x, pa.y, pa.z);
         float kx = 0.f, ky = 0.f, kz = 0.f;
@@ -119,81 +189,74 @@ __global__ void __launch_bounds__(256)
           ky = __fdiv_rn(vy, len);
           kz = __fdiv_rn(vz, len);
         }
-        // per-lane start of the lexicographic pair enumeration p = lane + 32*round
-        const unsigned total = (unsigned)nM * (unsigned)nC;
-        int pi = 0, pj = 0, qstep = 0, rstep = 0;
-        if (nC > 0) {
-          pi = lane / nC;
-          pj = lane - pi * nC;
-          qstep = 32 / nC;
-          rstep = 32 - qstep * nC;
-        }
-        int best = INT_MIN, best_k = -1;
-        for (int k = 0; k < dp.n_t; ++k) {
-          float Rk[9];
-          if (k > 0) {
-            const float2 cs = pk.trig[k * dp.step_t];
-            torsion_matrix(kx, ky, kz, cs.x, cs.y, Rk);
-          }
-          for (int m = lane; m < nM; m += 32) {
-            const float4 p = S.u[S.mlist[m]];
-            if (k == 0) {
-              S.wk[m] = p;
-            } else {
-              const float3 q = torsion_apply(Rk, a3, p.x, p.y, p.z);
-              S.wk[m] = make_float4(q.x, q.y, q.z, p.w);
+        unsigned best_key = 0;  // (score + 32768) << 16 | (65535 - angle); 0 = no clean angle
+        for (int k0 = 0; k0 < dp.n_t; k0 += 32) {
+          const int nA = min(32, dp.n_t - k0);
+          if (lane < nA) S.ascore[lane] = 0;
+          if (lane == 0) S.abump = 0u;
+          __syncwarp();
+          const int nslot = nA * nM;
+          const int nMd = nM > 0 ? nM : 1;
+          int sa = lane / nMd, sm = lane - sa * nMd;    // slot = lane + 32 * round -> (angle, moving atom)
+          const int qa = 32 / nMd, qm = 32 - qa * nMd;
+          for (int s0 = 0; s0 < nslot; s0 += 32) {
+            const bool valid = s0 + lane < nslot;
+            // with early exit, angles bumped in an earlier round are retired; without, every pair runs
+            const bool pre = valid && !(dp.early_exit && ((S.abump >> sa) & 1u));
+            const unsigned act0 = __ballot_sync(kFull, pre);
+            if (act0) {
+              float3 q = make_float3(0.f, 0.f, 0.f);
+              if (pre) q = torsion_pos(pk, dp.step_t, k0 + sa, kx, ky, kz, a3, S.u[S.mlist[sm]]);
+              const unsigned same = __match_any_sync(kFull, valid ? sa : -1);
+              bool active = pre;
+              float mind = __int_as_float(0x7f800000);  // min squared distance seen (P9: bump iff < bd2)
+              for (int c = 0; c < nC; c += kChunk) {   // cmp[] is padded with far sentinels to kChunk
+                const unsigned am = __ballot_sync(kFull, active);
+                if (!am) break;
+                pairs_total += (unsigned)__popc(am) * (unsigned)min(kChunk, nC - c);
+#pragma unroll
+                for (int t = 0; t < kChunk; ++t) {
+                  const float4 y = S.cmp[c + t];
+                  mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+                }
+                if (dp.early_exit) {
+                  const unsigned hb = __ballot_sync(kFull, pre && mind < dp.bd2);
+                  active = active && !(hb & same);
+                }
+              }
+              const bool hit = pre && mind < dp.bd2;
+              const unsigned hb = __ballot_sync(kFull, hit);
+              if (hit) atomicOr(&S.abump, 1u << sa);
+              if (pre && !(hb & same)) {
+                const int v = grid_val(pk, node_index(g, q.x, q.y, q.z));
+                atomicAdd(&S.ascore[sa], v);
+              }
             }
+            sa += qa;
+            sm += qm;
+            if (sm >= nM) {
+              sm -= nM;
+              ++sa;
+            }
+            __syncwarp();
           }
           __syncwarp();
-          // bump scan (P9): exists i in M, j in C' with d2 < bd2
-          bool bumped = false;
-          {
-            int i = pi, j = pj;
-            bool hit = false;
-            for (unsigned b0 = 0; b0 < total; b0 += 32) {
-              const unsigned p = b0 + (unsigned)lane;
-              if (p < total) {
-                const float4 x = S.wk[i];
-                const float4 y = S.wk[kMaxA - 1 - j];
-                hit |= dist2(x.x, x.y, x.z, y.x, y.y, y.z) < dp.bd2;
-              }
-              pairs_total += min(32u, total - b0);
-              i += qstep;
-              j += rstep;
-              if (j >= nC) {
-                j -= nC;
-                ++i;
-              }
-              if (dp.early_exit && __any_sync(kFull, hit)) break;
-            }
-            bumped = __any_sync(kFull, hit);
-          }
-          ++evals;
-          if (!bumped) {
-            int sc = 0;
-            for (int m = lane; m < nM; m += 32) {
-              const float4 p = S.wk[m];
-              sc += grid_val(pk, node_index(g, p.x, p.y, p.z));
-            }
-            sc = base + warp_sum(sc);
-            if (sc > best) {
-              best = sc;
-              best_k = k;
-            }
-          } else if (dp.early_exit) {
-            ++early_exits;
-          }
+          unsigned kk = 0;
+          if (lane < nA && !((S.abump >> lane) & 1u))
+            kk = ((unsigned)(base + S.ascore[lane] + 32768) << 16) | (unsigned)(65535 - (k0 + lane));
+          const unsigned nb_bump = (unsigned)__popc(S.abump);
+          evals += (unsigned)nA;
+          if (dp.early_exit) early_exits += nb_bump;
+          best_key = max(best_key, __reduce_max_sync(kFull, kk));
           __syncwarp();
         }
+        const int best_k = best_key ? 65535 - (int)(best_key & 0xFFFFu) : -1;
         // commit the winner before the next fragment
         if (best_k > 0) {
-          const float2 cs = pk.trig[best_k * dp.step_t];
-          float Rk[9];
-          torsion_matrix(kx, ky, kz, cs.x, cs.y, Rk);
           for (int m = lane; m < nM; m += 32) {
             const int i = S.mlist[m];
             const float4 p = S.u[i];
-            const float3 q = torsion_apply(Rk, a3, p.x, p.y, p.z);
+            const float3 q = torsion_pos(pk, dp.step_t, best_k, kx, ky, kz, a3, p);
             S.u[i] = make_float4(q.x, q.y, q.z, p.w);
           }
         }
@@ -298,33 +361,27 @@ __global__ void __launch_bounds__(256)
     }
     __syncwarp();
     // greedy keep (warp-uniform)
-    int kept[DS_MAX_RESTARTS];
     int nk = 0;
     for (int o = 0; o < nvalid && nk < dp.K; ++o) {
       const int c = S.ord[o];
       bool ok = true;
-      for (int t = 0; t < nk; ++t) ok = ok && ((S.dis[c] >> kept[t]) & 1u);
-      if (ok) kept[nk++] = c;
+      for (int t = 0; t < nk; ++t) ok = ok && ((S.dis[c] >> S.kept[t]) & 1u);
+      if (ok) {
+        if (lane == 0) S.kept[nk] = c;
+        ++nk;
+        __syncwarp();
+      }
     }
     // ---- rescore kept poses (P11): exact fixed-point sum over (ligand atom, pocket atom) ----
     long long best_chem = 0;
     int best_r = -1;
     for (int t = 0; t < nk; ++t) {
-      const int r = kept[t];
-      long long acc = 0;
-      const float4 *ur = scr + (size_t)r * kMaxA;
-      for (int i = lane; i < A; i += 32) {
-        const float4 x = ur[i];
-        const int32_t *wrow = pk.wfx + (int)x.w * DS_N_TYPES * (pk.nb + 1);
-        for (int j = 0; j < pk.n_atoms; ++j) {
-          const float4 y = __ldg(pk.patoms + j);
-          const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
-          int b = 0;
-#pragma unroll
-          for (int q = 0; q < DS_MAX_BINS; ++q) b += (q < pk.nb) & !(d2 < pk.ub2[q]);
-          acc += __ldg(wrow + (int)y.w * (pk.nb + 1) + b);
-        }
-      }
+      const int r = S.kept[t];
+      __syncwarp();
+      for (int i = lane; i < A; i += 32) S.u[i] = scr[(size_t)r * kMaxA + i];
+      __syncwarp();
+      long long acc = pk.nb == 4 ? rescore_pose<4>(S, A, pat, pk.n_atoms, s_w, pk.nb, s_ub2)
+                                 : rescore_pose<0>(S, A, pat, pk.n_atoms, s_w, pk.nb, s_ub2);
       acc = warp_sum64(acc);
       if (best_r < 0 || acc > best_chem || (acc == best_chem && r < best_r)) {
         best_chem = acc;
@@ -359,12 +416,23 @@ __global__ void __launch_bounds__(256)
 }
 
 size_t optimize_warp_smem_bytes() { return sizeof(OptWarpSmem); }
+size_t optimize_cta_smem_bytes(int n_patoms, int nb) {
+  size_t fixed = (size_t)n_patoms * 16 + (size_t)DS_N_TYPES * DS_N_TYPES * (nb + 1) * 4 + DS_MAX_BINS * 4;
+  return (fixed + 15) & ~(size_t)15;
+}
 
 void launch_optimize_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                              const uint32_t *keys, OptOut out, int *queue, int blocks, int warps, size_t smem,
                              cudaStream_t st) {
   cudaFuncSetAttribute(k_optimize_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_optimize_batched<<<blocks, warps * 32, smem, st>>>(pk, bt, dp, order, keys, out, queue);
+}
+
+int optimize_blocks_per_sm(int warps, size_t smem) {
+  int n = 0;
+  cudaFuncSetAttribute(k_optimize_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_optimize_batched, warps * 32, smem);
+  return n;
 }
 
 }  // namespace ds
