@@ -103,18 +103,6 @@ static void mat3_mul(const float *A, const float *B, float *C) {
   memcpy(C, t, sizeof t);
 }
 
-/* P6: Ra(ax, ay) = Ry(ay) (x) Rx(ax) in single-product form */
-static void align_rotation(int ax_deg, int ay_deg, float Ra[9]) {
-  float cx = g_cos[ax_deg], sx = g_sin[ax_deg], cy = g_cos[ay_deg], sy = g_sin[ay_deg];
-  float r[9] = {cy, sy * sx, sy * cx, 0.f, cx, -sx, -sy, cy * sx, cy * cx};
-  memcpy(Ra, r, sizeof r);
-}
-
-/* P3: u = M d + t */
-static void transform_point(const float M[9], const float t[3], const float d[3], float u[3]) {
-  for (int k = 0; k < 3; ++k) u[k] = fmaf(M[3 * k + 2], d[2], fmaf(M[3 * k + 1], d[1], fmaf(M[3 * k], d[0], t[k])));
-}
-
 /* ---------------------------------------------------------------- P5: PRNG */
 static uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -213,13 +201,24 @@ static void starting_pose(const or_lig *L, const or_pk *k, int r, int64_t seed, 
   for (int q = 0; q < 9; ++q) R0s[q] = R0[q] * k->inv_s;
 }
 
-/* coordinates of the rigid pose (ix, iy) of a restart: (Ra (x) R0s) d + t */
+/* P6: coordinates of the rigid pose (ax, ay) of a restart, x rotation first then y (Alg. 1
+ * lines 4-6; apply_rigid of SPEC.md:135 about the centroid t, fresh from the starting pose,
+ * SPEC.md:303): R' = Rx(ax) (x) R0s, v = R' d, u = Ry(ay) v + t written out as
+ * u_x = fma(sy, v_z, fma(cy, v_x, t_x)), u_y = v_y + t_y, u_z = fma(cy, v_z, fma(-sy, v_x, t_z)). */
 static void rigid_pose(const or_lig *L, const float R0s[9], const float t[3], int ax_deg, int ay_deg,
                        float (*u)[3]) {
-  float Ra[9], M[9];
-  align_rotation(ax_deg, ay_deg, Ra);
-  mat3_mul(Ra, R0s, M);
-  for (int i = 0; i < L->A; ++i) transform_point(M, t, L->d[i], u[i]);
+  float Rx[9], Rp[9];
+  rot_x(ax_deg, Rx);
+  mat3_mul(Rx, R0s, Rp);
+  const float cy = g_cos[ay_deg], sy = g_sin[ay_deg];
+  for (int i = 0; i < L->A; ++i) {
+    const float *d = L->d[i];
+    float v[3];
+    for (int k = 0; k < 3; ++k) v[k] = fmaf(Rp[3 * k + 2], d[2], fmaf(Rp[3 * k + 1], d[1], Rp[3 * k] * d[0]));
+    u[i][0] = fmaf(sy, v[2], fmaf(cy, v[0], t[0]));
+    u[i][1] = v[1] + t[1];
+    u[i][2] = fmaf(cy, v[2], fmaf(-sy, v[0], t[2]));
+  }
 }
 
 /* SPEC.md:247 align: exhaustive (ix, iy) sweep, ties -> smallest (ax, ay) */

@@ -147,11 +147,14 @@ def starting_pose(L: Ligand, P: Pocket, r: int, seed: int):
 
 
 def rigid_coords(L, R0s, t, ax, ay):
-    cx, sx = trig(ax)
+    """Pose (ax, ay): u = Ry(ay) (Rx(ax) R0s d) + t, x rotation first (DESIGN.md §3 P6)."""
+    Rp = mat3_mul(rot_x(ax), R0s)
     cy, sy = trig(ay)
-    Ra = [cy, f32(sy * sx), f32(sy * cx), f32(0), cx, -sx, -sy, f32(cy * sx), f32(cy * cx)]
-    M = mat3_mul(Ra, R0s)
-    return [transform(M, t, d) for d in L.d]
+    out = []
+    for d in L.d:
+        v = [fmaf(Rp[3 * k + 2], d[2], fmaf(Rp[3 * k + 1], d[1], f32(Rp[3 * k] * d[0]))) for k in range(3)]
+        out.append([fmaf(sy, v[2], fmaf(cy, v[0], t[0])), f32(v[1] + t[1]), fmaf(cy, v[2], fmaf(-sy, v[0], t[2]))])
+    return out
 
 
 def align(L, P, R0s, t, step):

@@ -1,42 +1,87 @@
 // Alignment (Alg. 1 lines 3-9) — batched family.
 //
-// One persistent CTA per SM stages the int8 pocket grid into shared memory once (the B200
-// replacement for the paper's texture-cached pocket); each warp then pulls
-// ligands from an atomic queue (LPT order) and scores all N x n_a^2 rigid poses of its ligand.
-// Lanes own (restart, rotation) slots, R per lane, so every lane is busy for any atom count
-// (the paper's lanes-over-atoms mapping idles lanes when A % 32 != 0); atoms are
-// broadcast from a per-warp smem stage.  Output: one packed argmax key per (ligand, restart).
+// One persistent CTA per SM stages the int8 pocket grid (biased to uint8, with a one-node
+// out-of-grid halo) into shared memory once — the B200 replacement for the paper's
+// texture-cached pocket; each warp then pulls ligands from an atomic queue
+// (LPT order) and scores all N x n_a^2 rigid poses of its ligand.
+//
+// Work split: a lane owns a (restart, ax) unit and sweeps every atom of the ligand for ALL ay.
+// Because the pose is Ry(ay) (Rx(ax) (R0s d)) + t (DESIGN.md §3 P6), the inner vector
+// v = Rx(ax) R0s d and the whole y coordinate (clamp and row offset included) are shared by the
+// n_a values of ay, leaving 4 FFMA + a branch-free nearest-node lookup (2 FADD, 4 IMNMX, 1-2 IMAD,
+// 1 LDS.U8) + 1 add per (atom, ay).  For the default 12° step the 30 (cos, sin) pairs of ay are
+// __constant__ and the ay loop is fully unrolled, so they are FFMA constant-bank operands; the
+// 30 running scores are packed two per register as biased 16-bit sums.  Every lane is busy
+// whatever the atom count (the paper's lanes-over-atoms mapping idles lanes when A % 32 != 0,
+// PAPER.md:717).  Output: one packed argmax key per (ligand, restart):
+// (score + 32768) << 16 | (65535 - (ix * n_a + iy)).
 #include "ds_kernels.cuh"
 
 namespace ds {
 
-// dynamic smem layout: [grid bytes (16-aligned)] [trig_a float2[n_a]] [per warp: stage float4[32],
+__constant__ float4 c_trig_ay[360];  // (cos, sin, -sin, 0) of iy * step_a
+
+// dynamic smem layout: [grid bytes (16-aligned)] [trig_a float4[n_a]] [per warp: stage float4[32],
 // params float[N*12], keys u32[N]]
 __host__ __device__ inline int align_warp_smem_bytes(int N) { return 32 * 16 + ((N * 12 * 4 + N * 4 + 15) & ~15); }
 
-template <int R, bool kSmemGrid>
+__device__ __forceinline__ unsigned grid_u8(const uint8_t *grid, int idx, bool smem) {
+  return smem ? (unsigned)grid[idx] : (unsigned)__ldg(grid + idx);
+}
+
+// Accumulate the biased grid values of angles iy = iy0 .. iy0+G-1 for one atom's v into G/2
+// packed registers (low half: even k, high half: odd k).
+template <int G, bool kConst, bool kSmemGrid>
+__device__ __forceinline__ void unit_atom(const float3 v, const float *t, unsigned yk, const GridGeom &g,
+                                          const uint8_t *grid, const float4 *strig, int iy0, int n_a,
+                                          unsigned *acc) {
+#pragma unroll
+  for (int k = 0; k < G; k += 2) {
+    const float4 c0 = kConst ? c_trig_ay[k] : strig[min(iy0 + k, n_a - 1)];
+    const float4 c1 = kConst ? c_trig_ay[k + 1] : strig[min(iy0 + k + 1, n_a - 1)];
+    const float ux0 = __fmaf_rn(c0.y, v.z, __fmaf_rn(c0.x, v.x, t[0]));
+    const float uz0 = __fmaf_rn(c0.x, v.z, __fmaf_rn(c0.z, v.x, t[2]));
+    const float ux1 = __fmaf_rn(c1.y, v.z, __fmaf_rn(c1.x, v.x, t[0]));
+    const float uz1 = __fmaf_rn(c1.x, v.z, __fmaf_rn(c1.z, v.x, t[2]));
+    const int i0 = (int)(clamp_bits(ux0, g.nx) + g.NXY * clamp_bits(uz0, g.nz) + yk);
+    const int i1 = (int)(clamp_bits(ux1, g.nx) + g.NXY * clamp_bits(uz1, g.nz) + yk);
+    acc[k >> 1] += grid_u8(grid, i0, kSmemGrid) + (grid_u8(grid, i1, kSmemGrid) << 16);
+  }
+}
+
+// NA > 0: n_a == NA fixed (G == NA, one unit per (restart, ax)); NA == 0: runtime n_a, ay in chunks
+// of G with units ordered chunk-major so a warp round shares its chunk.
+template <int NA, int G, bool kSmemGrid>
 __global__ void __launch_bounds__(1024, 1)
     k_align_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, AlignOut out, int *queue) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr bool kConst = NA > 0;
+  static_assert(G % 2 == 0, "scores are packed in pairs");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n_a = kConst ? NA : dp.n_a;
   const int gbytes = kSmemGrid ? pk.grid_bytes : 0;
-  const int8_t *grid = pk.grid;
+  const uint8_t *grid = pk.grid;
   if (kSmemGrid) {
     const int4 *src = reinterpret_cast<const int4 *>(pk.grid);
     int4 *dst = reinterpret_cast<int4 *>(smem);
     for (int i = threadIdx.x; i < gbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-    grid = reinterpret_cast<const int8_t *>(smem);
+    grid = smem;
   }
-  float2 *strig = reinterpret_cast<float2 *>(smem + gbytes);
-  for (int i = threadIdx.x; i < dp.n_a; i += blockDim.x) strig[i] = pk.trig[i * dp.step_a];
-  unsigned char *wbase = smem + gbytes + ((dp.n_a * 8 + 15) & ~15) + warp * align_warp_smem_bytes(dp.N);
+  float4 *strig = reinterpret_cast<float4 *>(smem + gbytes);
+  for (int i = threadIdx.x; i < n_a; i += blockDim.x) {
+    const float2 cs = pk.trig[i * dp.step_a];
+    strig[i] = make_float4(cs.x, cs.y, -cs.y, 0.f);
+  }
+  unsigned char *wbase = smem + gbytes + n_a * 16 + warp * align_warp_smem_bytes(dp.N);
   float4 *stage = reinterpret_cast<float4 *>(wbase);
   float *prm = reinterpret_cast<float *>(wbase + 32 * 16);
   unsigned *keys = reinterpret_cast<unsigned *>(prm + dp.N * 12);
   __syncthreads();
 
   const GridGeom g = pk.g;
-  const int total = dp.N * dp.n_rot;
+  const int nch = kConst ? 1 : (n_a + G - 1) / G;   // ay chunks
+  const int per_h = dp.N * n_a;                        // units per chunk: (restart, ax)
+  const int total = nch * per_h;
   for (;;) {
     int item = 0;
     if (lane == 0) item = atomicAdd(queue, 1);
@@ -54,29 +99,29 @@ __global__ void __launch_bounds__(1024, 1)
     if (nchunk == 1) stage[lane] = lane < A ? __ldg(bt.atoms + a0 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
 
-    for (int base = 0; base < total; base += 32 * R) {
-      float M[R][9], T[R][3];
-      int score[R], rst[R], rot[R];
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        int s = base + j * 32 + lane;
-        s = s < total ? s : total - 1;
-        const int r = s / dp.n_rot;
-        const int q = s - r * dp.n_rot;
-        const int ix = q / dp.n_a;
-        const int iy = q - ix * dp.n_a;
-        rst[j] = r;
-        rot[j] = (base + j * 32 + lane) < total ? q : -1;
-        const float *P = prm + r * 12;
+    for (int base = 0; base < total; base += 32) {
+      const bool uvalid = base + lane < total;
+      const int unit = min(base + lane, total - 1);
+      const int h = kConst ? 0 : unit / per_h;
+      const int q = unit - h * per_h;
+      const int r = q / n_a;
+      const int ix = q - r * n_a;
+      const int iy0 = h * G;
+      const float *P = prm + r * 12;
+      float Rp[9], t[3];
+      {
         float R0s[9];
 #pragma unroll
         for (int k = 0; k < 9; ++k) R0s[k] = P[k];
-        align_matrix(strig[ix], strig[iy], R0s, M[j]);
-        T[j][0] = P[9];
-        T[j][1] = P[10];
-        T[j][2] = P[11];
-        score[j] = 0;
+        const float4 cx = strig[ix];
+        align_rx(make_float2(cx.x, cx.y), R0s, Rp);
+        t[0] = P[9];
+        t[1] = P[10];
+        t[2] = P[11];
       }
+      unsigned acc[G / 2];
+#pragma unroll
+      for (int k = 0; k < G / 2; ++k) acc[k] = 0u;
       for (int c = 0; c < nchunk; ++c) {
         if (nchunk > 1) {
           __syncwarp();
@@ -87,17 +132,20 @@ __global__ void __launch_bounds__(1024, 1)
         const int n = min(32, A - c * 32);
         for (int a = 0; a < n; ++a) {
           const float4 d = stage[a];
-#pragma unroll
-          for (int j = 0; j < R; ++j) {
-            const float3 u = apply_mt(M[j], T[j], d.x, d.y, d.z);
-            const int idx = node_index(g, u.x, u.y, u.z);
-            score[j] += kSmemGrid ? (int)grid[idx] : (int)__ldg(grid + idx);
-          }
+          const float3 v = align_v(Rp, d.x, d.y, d.z);
+          const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny) + g.K;  // u_y is shared by all ay
+          unit_atom<G, kConst, kSmemGrid>(v, t, yk, g, grid, strig, iy0, n_a, acc);
         }
       }
+      unsigned best = 0u;
+      const int bias = 128 * A;  // the device grid stores v + 128
 #pragma unroll
-      for (int j = 0; j < R; ++j)
-        if (rot[j] >= 0) atomicMax(&keys[rst[j]], ((unsigned)(score[j] + 32768) << 16) | (unsigned)(65535 - rot[j]));
+      for (int k = 0; k < G; ++k) {
+        const int iy = iy0 + k;
+        const int sc = (int)((acc[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) - bias;
+        if (iy < n_a) best = max(best, ((unsigned)(sc + 32768) << 16) | (unsigned)(65535 - (ix * n_a + iy)));
+      }
+      if (uvalid) atomicMax(&keys[r], best);
     }
     __syncwarp();
     for (int r = lane; r < dp.N; r += 32) out.keys[(size_t)lig * dp.N + r] = keys[r];
@@ -105,17 +153,102 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
+// ---- latency family: one ligand spread over the GPU -----------------------
+// Block (ligand, restart, atom chunk) = one warp; lane = ax.  Each lane scores its ax for every ay
+// over the chunk's atoms (grid read through L1 from the biased global copy) and adds the partial
+// sums into scores[(lig*N + r) * n_rot + ax*n_a + ay] with global atomics; the optimisation
+// kernel takes the argmax.  ACH atoms per block keeps ~A/ACH x N blocks in flight.
+template <int NA>
+__global__ void __launch_bounds__(32)
+    k_align_latency(PocketView pk, BatchView bt, DockParams dp, int ach, int nchunks, int *scores) {
+  constexpr bool kConst = NA > 0;
+  constexpr int G = kConst ? NA : 8;
+  const int lane = threadIdx.x;
+  const int lig = blockIdx.x / (dp.N * nchunks);
+  const int rem = blockIdx.x - lig * dp.N * nchunks;
+  const int r = rem / nchunks;
+  const int c = rem - r * nchunks;
+  const int a0 = bt.atom_off[lig];
+  const int A = bt.atom_off[lig + 1] - a0;
+  const int c0 = c * ach, c1 = min(A, c0 + ach);
+  if (c0 >= A) return;
+  __shared__ float4 strig[360];
+  const int n_a = kConst ? NA : dp.n_a;
+  for (int i = lane; i < n_a; i += 32) {
+    const float2 cs = pk.trig[i * dp.step_a];
+    strig[i] = make_float4(cs.x, cs.y, -cs.y, 0.f);
+  }
+  __syncwarp();
+  const GridGeom g = pk.g;
+  float R0s[9], t[3];
+  start_params(bt.idh[lig], dp.seed, r, pk.trig, pk.inv_s, g.nx, g.ny, g.nz, R0s, t);
+  int *sc = scores + ((size_t)lig * dp.N + r) * dp.n_rot;
+  for (int ix = lane; ix < n_a; ix += 32) {
+    float Rp[9];
+    const float4 cx = strig[ix];
+    align_rx(make_float2(cx.x, cx.y), R0s, Rp);
+    for (int iy0 = 0; iy0 < n_a; iy0 += G) {
+      unsigned acc[G / 2];
+#pragma unroll
+      for (int k = 0; k < G / 2; ++k) acc[k] = 0u;
+      for (int a = c0; a < c1; ++a) {
+        const float4 d = __ldg(bt.atoms + a0 + a);
+        const float3 v = align_v(Rp, d.x, d.y, d.z);
+        const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny) + g.K;
+        unit_atom<G, kConst, false>(v, t, yk, g, pk.grid, strig, iy0, n_a, acc);
+      }
+      const int bias = 128 * (c1 - c0);
+#pragma unroll
+      for (int k = 0; k < G; ++k)
+        if (iy0 + k < n_a) atomicAdd(sc + ix * n_a + iy0 + k, (int)((acc[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) - bias);
+    }
+  }
+}
+
+void launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
+                          cudaStream_t st) {
+  const int ach = 4;
+  const int nchunks = (max_atoms + ach - 1) / ach;
+  const int blocks = bt.L * dp.N * nchunks;
+  if (dp.n_a == 30) {
+    static float4 h[30];
+    for (int i = 0; i < 30; ++i) {
+      const double rad = (double)(i * dp.step_a) * 0.017453292519943295;
+      const float c = (float)cos(rad), s = (float)sin(rad);
+      h[i] = make_float4(c, s, -s, 0.f);
+    }
+    cudaMemcpyToSymbolAsync(c_trig_ay, h, sizeof h, 0, cudaMemcpyHostToDevice, st);
+    k_align_latency<30><<<blocks, 32, 0, st>>>(pk, bt, dp, ach, nchunks, scores);
+  } else {
+    k_align_latency<0><<<blocks, 32, 0, st>>>(pk, bt, dp, ach, nchunks, scores);
+  }
+}
+
 int align_warp_smem_bytes_host(int N) { return align_warp_smem_bytes(N); }
+
+template <int NA, int G, bool S>
+static void launch_t(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order, AlignOut out,
+                     int *queue, int blocks, int warps, size_t smem, cudaStream_t st) {
+  cudaFuncSetAttribute(k_align_batched<NA, G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_align_batched<NA, G, S><<<blocks, warps * 32, smem, st>>>(pk, bt, dp, order, out, queue);
+}
 
 void launch_align_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                           AlignOut out, int *queue, int grid_in_smem, int blocks, int warps, size_t smem,
                           cudaStream_t st) {
-  if (grid_in_smem) {
-    cudaFuncSetAttribute(k_align_batched<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_align_batched<2, true><<<blocks, warps * 32, smem, st>>>(pk, bt, dp, order, out, queue);
+  if (dp.n_a == 30) {  // default 12° step: all 30 ay per unit, constant-bank angles
+    static float4 h[30];  // same values as the ctx trig table (P0); identical for every caller
+    for (int i = 0; i < 30; ++i) {
+      const double rad = (double)(i * dp.step_a) * 0.017453292519943295;
+      const float c = (float)cos(rad), s = (float)sin(rad);
+      h[i] = make_float4(c, s, -s, 0.f);
+    }
+    cudaMemcpyToSymbolAsync(c_trig_ay, h, sizeof h, 0, cudaMemcpyHostToDevice, st);
+    if (grid_in_smem) launch_t<30, 30, true>(pk, bt, dp, order, out, queue, blocks, warps, smem, st);
+    else launch_t<30, 30, false>(pk, bt, dp, order, out, queue, blocks, warps, smem, st);
   } else {
-    cudaFuncSetAttribute(k_align_batched<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_align_batched<2, false><<<blocks, warps * 32, smem, st>>>(pk, bt, dp, order, out, queue);
+    if (grid_in_smem) launch_t<0, 8, true>(pk, bt, dp, order, out, queue, blocks, warps, smem, st);
+    else launch_t<0, 8, false>(pk, bt, dp, order, out, queue, blocks, warps, smem, st);
   }
 }
 

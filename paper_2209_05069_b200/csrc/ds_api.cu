@@ -101,7 +101,7 @@ struct ds_ctx {
 struct ds_pocket {
   ds_ctx *ctx = nullptr;
   PocketView view{};
-  int8_t *d_grid = nullptr;
+  uint8_t *d_grid = nullptr;
   float4 *d_patoms = nullptr;
   int32_t *d_wfx = nullptr;
   float cutoff = 0.f;
@@ -212,15 +212,18 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
     return fail(DS_ERR_INVALID_ARG, "bad interaction table");
   for (int b = 1; b < d->n_bins; ++b)
     if (!(d->bin_ub[b] > d->bin_ub[b - 1])) return fail(DS_ERR_INVALID_ARG, "bins must be ascending");
-  // int8 device grid: every value must fit
-  const int gbytes = (int)((G + 1 + 15) & ~15ll);
-  std::vector<int8_t> g8(gbytes, 0);
-  for (int64_t i = 0; i < G; ++i) {
-    const int32_t v = d->values[i];
-    if (v < -128 || v > 127) return fail(DS_ERR_UNSUPPORTED, "grid value %d at node %lld does not fit int8", v, (long long)i);
-    g8[i] = (int8_t)v;
-  }
-  g8[G] = (int8_t)kOutside;
+  // int8 device grid with a one-node halo of kOutside: every value must fit
+  const int64_t NX = d->dims[0] + 2, NY = d->dims[1] + 2, NZ = d->dims[2] + 2;
+  const int gbytes = (int)((NX * NY * NZ + 15) & ~15ll);
+  std::vector<uint8_t> g8(gbytes, (uint8_t)(kOutside + 128));  // stored biased by +128
+  for (int64_t z = 0; z < d->dims[2]; ++z)
+    for (int64_t y = 0; y < d->dims[1]; ++y)
+      for (int64_t x = 0; x < d->dims[0]; ++x) {
+        const int32_t val = d->values[x + d->dims[0] * (y + d->dims[1] * z)];
+        if (val < -128 || val > 127)
+          return fail(DS_ERR_UNSUPPORTED, "grid value %d does not fit int8", val);
+        g8[(x + 1) + NX * ((y + 1) + NY * (z + 1))] = (uint8_t)(val + 128);
+      }
   for (int t = 0; t < DS_N_TYPES * DS_N_TYPES; ++t)
     if (d->table[t] != d->table[(t % DS_N_TYPES) * DS_N_TYPES + t / DS_N_TYPES])
       return fail(DS_ERR_INVALID_ARG, "interaction table must be symmetric");
@@ -231,8 +234,9 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
   v.g.nx = d->dims[0];
   v.g.ny = d->dims[1];
   v.g.nz = d->dims[2];
-  v.g.nxy = d->dims[0] * d->dims[1];
-  v.g.sentinel = (int)G;
+  v.g.NX = (unsigned)NX;
+  v.g.NXY = (unsigned)(NX * NY);
+  v.g.K = (unsigned)(1 + NX + NX * NY) * (1u - (unsigned)kMagicBits);
   v.grid_bytes = gbytes;
   v.spacing = d->spacing;
   v.inv_s = (float)(1.0 / (double)d->spacing);  // P2
@@ -464,7 +468,7 @@ int run_batched(ds_ctx *c, const ds_pocket *pk, int L, int NA, int NF, const Doc
   DS_CUDA(cudaMemsetAsync(queue, 0, 256, c->stream));
   // --- alignment: one CTA per SM, grid staged into smem when it fits ---
   const size_t per_warp = (size_t)align_warp_smem_bytes_host(dp.N);
-  const size_t fixed = (size_t)((dp.n_a * 8 + 15) & ~15);
+  const size_t fixed = (size_t)dp.n_a * 16;
   int warps_a = 32;
   const size_t gb = (size_t)pk->view.grid_bytes;
   int in_smem = gb + fixed + per_warp * 8 <= c->smem_optin;

@@ -43,19 +43,22 @@ __device__ __forceinline__ float3 apply_mt(const float *M, const float *t, float
   return u;
 }
 
-// ---- P4: nearest node (round half-even) + in-grid test; returns kSentinel index if outside.
-// For |u| < 2^22 the magic add equals rintf; every |u| >= 2^22, inf or NaN lands outside
-// (dims < 2^22), exactly like the oracle's float test 0 <= rint(u) <= n-1.
+// ---- P4: nearest node (round half-even) + in-grid test, as an index into the PADDED grid.
+// The device grid carries a one-node halo holding kOutside, so the in-grid test becomes a clamp of
+// the magic-rounded bits to [kMagicBits - 1, kMagicBits + n] (two IMNMX per axis, no branch/select).
+// For |u| < 2^22 the magic add equals rintf; every |u| >= 2^22, inf or NaN clamps into the halo
+// (dims < 2^21), exactly like the oracle's float test 0 <= rint(u) <= n-1.
 struct GridGeom {
-  int nx, ny, nz, nxy, sentinel;
+  int nx, ny, nz;          // interior dims
+  unsigned NX, NXY;        // padded row / plane pitch: nx+2, (nx+2)(ny+2)
+  unsigned K;              // (1 + NX + NXY) * (1 - kMagicBits) mod 2^32
 };
+__device__ __forceinline__ unsigned clamp_bits(float u, int n) {
+  const int b = __float_as_int(__fadd_rn(u, kMagic));
+  return (unsigned)min(max(b, kMagicBits - 1), kMagicBits + n);
+}
 __device__ __forceinline__ int node_index(const GridGeom &g, float ux, float uy, float uz) {
-  const int bx = __float_as_int(__fadd_rn(ux, kMagic)) - kMagicBits;
-  const int by = __float_as_int(__fadd_rn(uy, kMagic)) - kMagicBits;
-  const int bz = __float_as_int(__fadd_rn(uz, kMagic)) - kMagicBits;
-  const bool in = ((unsigned)bx < (unsigned)g.nx) & ((unsigned)by < (unsigned)g.ny) & ((unsigned)bz < (unsigned)g.nz);
-  const int idx = bx + g.nx * by + g.nxy * bz;
-  return in ? idx : g.sentinel;
+  return (int)(clamp_bits(ux, g.nx) + g.NX * clamp_bits(uy, g.ny) + g.NXY * clamp_bits(uz, g.nz) + g.K);
 }
 
 // ---- P5: starting pose parameters of restart r: R0s = (Rz(g) (x) (Ry(b) (x) Rx(a))) * inv_s,
@@ -85,12 +88,27 @@ __device__ __forceinline__ void start_params(uint64_t idh, int64_t seed, int r, 
   for (int k = 0; k < 9; ++k) R0s[k] = __fmul_rn(R0[k], inv_s);
 }
 
-// ---- P6: alignment rotation Ra(ix,iy) = Ry(ay) (x) Rx(ax) in single-product form, M = Ra (x) R0s
-__device__ __forceinline__ void align_matrix(float2 cx_sx, float2 cy_sy, const float *R0s, float *M) {
-  const float cx = cx_sx.x, sx = cx_sx.y, cy = cy_sy.x, sy = cy_sy.y;
-  const float Ra[9] = {cy, __fmul_rn(sy, sx), __fmul_rn(sy, cx), 0.f, cx, -sx, -sy, __fmul_rn(cy, sx),
-                       __fmul_rn(cy, cx)};
-  matmul3(Ra, R0s, M);
+// ---- P6: alignment pose (ix, iy) of a restart, x rotation first then y (Alg. 1 lines 4-6):
+//   R' = Rx(ax) (x) R0s,  v = R' d  (v_k = fma(R'_k2,d.z, fma(R'_k1,d.y, R'_k0*d.x)))
+//   u_x = fma(sy, v_z, fma(cy, v_x, t_x)),  u_y = v_y + t_y,  u_z = fma(cy, v_z, fma(-sy, v_x, t_z))
+// i.e. u = Ry(ay) (Rx(ax) (R0s d)) + t; u_y does not depend on ay.
+__device__ __forceinline__ void align_rx(float2 cx_sx, const float *R0s, float *Rp) {
+  const float Rx[9] = {1.f, 0.f, 0.f, 0.f, cx_sx.x, -cx_sx.y, 0.f, cx_sx.y, cx_sx.x};
+  matmul3(Rx, R0s, Rp);
+}
+__device__ __forceinline__ float3 align_v(const float *Rp, float dx, float dy, float dz) {
+  float3 v;
+  v.x = __fmaf_rn(Rp[2], dz, __fmaf_rn(Rp[1], dy, __fmul_rn(Rp[0], dx)));
+  v.y = __fmaf_rn(Rp[5], dz, __fmaf_rn(Rp[4], dy, __fmul_rn(Rp[3], dx)));
+  v.z = __fmaf_rn(Rp[8], dz, __fmaf_rn(Rp[7], dy, __fmul_rn(Rp[6], dx)));
+  return v;
+}
+__device__ __forceinline__ float3 align_u(float3 v, float cy, float sy, const float *t) {
+  float3 u;
+  u.x = __fmaf_rn(sy, v.z, __fmaf_rn(cy, v.x, t[0]));
+  u.y = __fadd_rn(v.y, t[1]);
+  u.z = __fmaf_rn(cy, v.z, __fmaf_rn(-sy, v.x, t[2]));
+  return u;
 }
 
 // ---- P8: torsion rotation (Rodrigues) about unit axis k by table angle (c, s)

@@ -5,9 +5,9 @@
 namespace ds {
 
 struct PocketView {
-  const int8_t *grid;        // nx*ny*nz values + sentinel (= kOutside) at index nx*ny*nz
+  const uint8_t *grid;       // (nx+2)(ny+2)(nz+2) values + 128 (uint8), x-fastest, halo = kOutside
   GridGeom g;
-  int grid_bytes;            // padded to 16 B (includes the sentinel)
+  int grid_bytes;            // rounded up to 16 B
   float inv_s, spacing;
   float ox, oy, oz;
   int n_atoms;

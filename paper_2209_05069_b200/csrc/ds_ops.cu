@@ -17,7 +17,7 @@ __global__ void k_grid_score(PocketView pk, const float *coords, int n_atoms, in
     const float *q = coords + 3 * ((size_t)pose * n_atoms + i);
     const int idx = node_index(pk.g, to_grid(q[0], pk.inv_s, offx), to_grid(q[1], pk.inv_s, offy),
                                to_grid(q[2], pk.inv_s, offz));
-    s += (int)__ldg(pk.grid + idx);
+    s += (int)__ldg(pk.grid + idx) - 128;  // device grid is stored biased by +128
   }
   s = (int)__reduce_add_sync(kFull, (unsigned)s);
   if (lane == 0) out[pose] = s;

@@ -34,7 +34,7 @@ struct OptWarpSmem {
   int kept[DS_MAX_RESTARTS];
 };
 
-__device__ __forceinline__ int grid_val(const PocketView &pk, int idx) { return (int)__ldg(pk.grid + idx); }
+__device__ __forceinline__ int grid_val(const PocketView &pk, int idx) { return (int)__ldg(pk.grid + idx) - 128; }
 
 __device__ __forceinline__ int warp_sum(int v) { return (int)__reduce_add_sync(kFull, (unsigned)v); }
 
@@ -137,12 +137,13 @@ __global__ void __launch_bounds__(256)
       const int align_score = (int)(key >> 16) - 32768;
       const int ix = rot / dp.n_a, iy = rot - ix * dp.n_a;
       {
-        float R0s[9], T[3], M[9];
+        float R0s[9], T[3], Rp[9];
         start_params(idh, dp.seed, r, pk.trig, pk.inv_s, g.nx, g.ny, g.nz, R0s, T);
-        align_matrix(pk.trig[ix * dp.step_a], pk.trig[iy * dp.step_a], R0s, M);
+        align_rx(pk.trig[ix * dp.step_a], R0s, Rp);
+        const float2 cy = pk.trig[iy * dp.step_a];
         for (int i = lane; i < A; i += 32) {
           const float4 d = __ldg(bt.atoms + a0 + i);
-          const float3 u = apply_mt(M, T, d.x, d.y, d.z);
+          const float3 u = align_u(align_v(Rp, d.x, d.y, d.z), cy.x, cy.y, T);
           S.u[i] = make_float4(u.x, u.y, u.z, d.w);
         }
       }
