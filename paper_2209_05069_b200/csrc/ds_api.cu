@@ -25,6 +25,11 @@ void launch_optimize_batched(const PocketView &pk, const BatchView &bt, const Do
 size_t optimize_warp_smem_bytes();
 size_t optimize_cta_smem_bytes(int n_patoms, int nb);
 int optimize_blocks_per_sm(int warps, size_t smem);
+void launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
+                          cudaStream_t st);
+size_t latency_rec_bytes();
+void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *scores,
+                             OptOut out, void *recs, int *done, cudaStream_t st);
 void launch_grid_score(const PocketView &pk, const float *coords, int n_atoms, int n_poses, int32_t *out,
                        cudaStream_t st);
 void launch_rescore(const PocketView &pk, const float *coords, const uint8_t *types, int n_atoms, int n_poses,
@@ -67,7 +72,7 @@ struct ds_ctx {
   float2 *trig = nullptr;       // 360 (cos, sin)
   // batch-sized device buffers
   DevBuf b_atom_off, b_atoms, b_frag_off, b_frags, b_idh, b_order_a, b_order_o, b_keys, b_res, b_rrec, b_rtors,
-      b_coords, b_btors, b_queue, b_scratch;
+      b_coords, b_btors, b_queue, b_scratch, b_lat_scores, b_lat_recs, b_lat_done;
   // pinned host staging
   void *h_stage = nullptr;
   size_t h_cap = 0;
@@ -171,7 +176,7 @@ void ds_destroy(ds_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   DevBuf *bufs[] = {&c->b_atom_off, &c->b_atoms, &c->b_frag_off, &c->b_frags, &c->b_idh, &c->b_order_a,
                     &c->b_order_o, &c->b_keys, &c->b_res, &c->b_rrec, &c->b_rtors, &c->b_coords, &c->b_btors,
-                    &c->b_queue, &c->b_scratch};
+                    &c->b_queue, &c->b_scratch, &c->b_lat_scores, &c->b_lat_recs, &c->b_lat_done};
   for (DevBuf *b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->trig) cudaFree(c->trig);
@@ -502,6 +507,51 @@ int run_batched(ds_ctx *c, const ds_pocket *pk, int L, int NA, int NF, const Doc
   return DS_OK;
 }
 
+// Latency family: alignment spread over (ligand, restart, atom chunk) warps, then one CTA per
+// (ligand, restart) for the torsion sweep; the ligand's last CTA selects and rescores.
+int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const DockParams &dp, bool want_coords,
+                bool want_btors, bool want_rrec, ds_stats *st) {
+  BatchView bt;
+  bt.L = L;
+  bt.atom_off = (const int *)c->b_atom_off.p;
+  bt.atoms = (const float4 *)c->b_atoms.p;
+  bt.frag_off = (const int *)c->b_frag_off.p;
+  bt.frags = (const uint4 *)c->b_frags.p;
+  bt.idh = (const uint64_t *)c->b_idh.p;
+  int rc;
+  const size_t nsc = (size_t)L * dp.N * dp.n_rot;
+  if ((rc = c->ensure(c->b_lat_scores, 4 * nsc)) || (rc = c->ensure(c->b_lat_recs, latency_rec_bytes() * (size_t)L * dp.N)) ||
+      (rc = c->ensure(c->b_lat_done, 4ull * L)) ||
+      (rc = c->ensure(c->b_scratch, sizeof(float4) * (size_t)L * dp.N * DS_MAX_ATOMS)))
+    return rc;
+  DS_CUDA(cudaMemsetAsync(c->b_lat_scores.p, 0, 4 * nsc, c->stream));
+  DS_CUDA(cudaMemsetAsync(c->b_lat_done.p, 0, 4ull * L, c->stream));
+  cudaEventRecord(c->ev[1], c->stream);
+  launch_align_latency(pk->view, bt, dp, max_atoms, (int *)c->b_lat_scores.p, c->stream);
+  cudaEventRecord(c->ev[2], c->stream);
+  OptOut oo;
+  oo.res = (ds_result *)c->b_res.p;
+  oo.rrec = want_rrec ? (ds_restart_record *)c->b_rrec.p : nullptr;
+  oo.rtors = (uint8_t *)c->b_rtors.p;
+  oo.final_u = (float4 *)c->b_scratch.p;
+  oo.best_coords = want_coords ? (float *)c->b_coords.p : nullptr;
+  oo.best_tors = want_btors ? (uint8_t *)c->b_btors.p : nullptr;
+  launch_optimize_latency(pk->view, bt, dp, (const int *)c->b_lat_scores.p, oo, c->b_lat_recs.p,
+                          (int *)c->b_lat_done.p, c->stream);
+  cudaEventRecord(c->ev[3], c->stream);
+  if (st) st->launches += 2;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DS_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return DS_OK;
+}
+
+int run_family(ds_ctx *c, const ds_pocket *pk, int family, int L, int NA, int NF, int max_atoms, const DockParams &dp,
+               bool want_coords, bool want_btors, bool want_rrec, ds_stats *st) {
+  if (family == DS_FAMILY_LATENCY)
+    return run_latency(c, pk, L, max_atoms, dp, want_coords, want_btors, want_rrec, st);
+  return run_batched(c, pk, L, NA, NF, dp, want_coords, want_btors, want_rrec, st);
+}
+
 int download(ds_ctx *c, int L, int NA, int NF, int N, const ds_outputs *out, ds_stats *st) {
   cudaStream_t s = c->stream;
   if (out->results) {
@@ -556,10 +606,10 @@ int ds_dock(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const ds_doc
   cudaEventRecord(c->ev[0], c->stream);
   if ((rc = upload_batch(c, b, dp.N, st))) return rc;
   const int NA = b->atom_off[L], NF = b->frag_off[L];
-  // Both families share the batched kernels in this build (the latency family is routed
-  // through the same kernels until its own spread-out kernels land).
-  if ((rc = run_batched(c, pk, L, NA, NF, dp, out->best_coords != nullptr, out->best_torsion != nullptr,
-                        out->restarts != nullptr, st)))
+  int max_atoms = 0;
+  for (int i = 0; i < L; ++i) max_atoms = std::max(max_atoms, b->atom_off[i + 1] - b->atom_off[i]);
+  if ((rc = run_family(c, pk, family, L, NA, NF, max_atoms, dp, out->best_coords != nullptr,
+                       out->best_torsion != nullptr, out->restarts != nullptr, st)))
     return rc;
   if ((rc = download(c, L, NA, NF, dp.N, out, st))) return rc;
   cudaEventRecord(c->ev[4], c->stream);
@@ -598,7 +648,9 @@ int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_d
   if (st) memset(st, 0, sizeof *st);
   if (d->L == 0) return DS_OK;
   DS_CUDA(cudaSetDevice(c->device));
-  if ((rc = run_batched(c, pk, d->L, d->n_atoms, d->n_frags, dp, true, true, true, st))) return rc;
+  int max_atoms = 0;
+  for (int i = 0; i < d->L; ++i) max_atoms = std::max(max_atoms, d->atom_off[i + 1] - d->atom_off[i]);
+  if ((rc = run_family(c, pk, family, d->L, d->n_atoms, d->n_frags, max_atoms, dp, true, true, true, st))) return rc;
   DS_CUDA(cudaStreamSynchronize(c->stream));
   d->N = dp.N;
   d->docked = true;

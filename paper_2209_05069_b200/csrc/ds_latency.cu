@@ -1,0 +1,406 @@
+// Latency kernel family: one ligand is spread over the whole GPU.
+//
+//  k_align_latency    (ds_align.cu)  blocks = ligand x restart x atom chunk, lane = ax
+//  k_optimize_latency (this file)    one CTA per (ligand, restart) — the paper's "grid level =
+//                                    initial poses" — with every thread of the
+//                                    CTA on the (angle, moving atom) slots of a fragment; the CTA
+//                                    barrier is the paper's block-level synchronisation
+//                                    (PAPER.md:732-737).  The last CTA of a ligand to finish runs
+//                                    select_poses + rescore.
+// Numeric recipe identical to the batched family: results are bit-identical.
+#include "ds_kernels.cuh"
+
+namespace ds {
+
+constexpr int kLatThreads = 256;
+constexpr int kLatChunk = 8;
+
+struct LatRec {  // per (ligand, restart), read by the ligand's last CTA
+  int geom, valid, degen, align_score;
+  unsigned evals, pairs, exits, rot;
+};
+
+struct LatSmem {
+  float4 u[DS_MAX_ATOMS];
+  float4 cmp[DS_MAX_ATOMS + kLatChunk];
+  uint8_t mlist[DS_MAX_ATOMS];
+  int ascore[32];
+  unsigned abump;
+  unsigned key;
+  int nM, nC, base, degen, best_k, is_last;
+  float kx, ky, kz;
+  unsigned pairs;
+  int geom;
+  int ord[DS_MAX_RESTARTS], kept[DS_MAX_RESTARTS], nkept;
+  unsigned dis[DS_MAX_RESTARTS];
+  unsigned long long chem;
+  int heavy;
+};
+
+__device__ __forceinline__ int lat_grid_val(const PocketView &pk, int idx) { return (int)__ldg(pk.grid + idx) - 128; }
+
+__device__ __forceinline__ float3 lat_torsion_pos(const PocketView &pk, int step_t, int k, float kx, float ky, float kz,
+                                                  float3 a, float4 p) {
+  if (k == 0) return make_float3(p.x, p.y, p.z);
+  const float2 cs = pk.trig[k * step_t];
+  float R[9];
+  torsion_matrix(kx, ky, kz, cs.x, cs.y, R);
+  return torsion_apply(R, a, p.x, p.y, p.z);
+}
+
+__global__ void __launch_bounds__(kLatThreads)
+    k_optimize_latency(PocketView pk, BatchView bt, DockParams dp, const int *scores, OptOut out, LatRec *recs,
+                       int *done) {
+  __shared__ LatSmem S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lig = blockIdx.x / dp.N, r = blockIdx.x - lig * dp.N;
+  const int a0 = bt.atom_off[lig], A = bt.atom_off[lig + 1] - a0;
+  const int f0 = bt.frag_off[lig], F = bt.frag_off[lig + 1] - f0;
+  const GridGeom g = pk.g;
+  if (tid == 0) {
+    S.key = 0u;
+    S.pairs = 0u;
+    S.geom = 0;
+    S.degen = 0;
+    S.heavy = 0;
+  }
+  __syncthreads();
+  // ---- argmax of the alignment scores (ties -> smallest rotation index) ----
+  {
+    const int *sc = scores + ((size_t)lig * dp.N + r) * dp.n_rot;
+    unsigned best = 0u;
+    for (int q = tid; q < dp.n_rot; q += kLatThreads)
+      best = max(best, ((unsigned)(__ldcg(sc + q) + 32768) << 16) | (unsigned)(65535 - q));
+    best = __reduce_max_sync(kFull, best);
+    if (lane == 0) atomicMax(&S.key, best);
+  }
+  __syncthreads();
+  const unsigned key = S.key;
+  const int rot = 65535 - (int)(key & 0xFFFFu);
+  const int ix = rot / dp.n_a, iy = rot - ix * dp.n_a;
+  {
+    float R0s[9], T[3], Rp[9];
+    start_params(bt.idh[lig], dp.seed, r, pk.trig, pk.inv_s, g.nx, g.ny, g.nz, R0s, T);
+    align_rx(pk.trig[ix * dp.step_a], R0s, Rp);
+    const float2 cy = pk.trig[iy * dp.step_a];
+    for (int i = tid; i < A; i += kLatThreads) {
+      const float4 d = __ldg(bt.atoms + a0 + i);
+      const float3 u = align_u(align_v(Rp, d.x, d.y, d.z), cy.x, cy.y, T);
+      S.u[i] = make_float4(u.x, u.y, u.z, d.w);
+    }
+  }
+  __syncthreads();
+  unsigned evals = 0, exits = 0;
+  int all_bumped = 0;
+  for (int f = 0; f < F; ++f) {
+    // ---- compaction of M and C' (warp 0, ascending order), axis (thread 0) ----
+    if (warp == 0) {
+      const uint4 fa = __ldg(bt.frags + 2 * (size_t)(f0 + f));
+      const uint4 fb = __ldg(bt.frags + 2 * (size_t)(f0 + f) + 1);
+      const unsigned mw[5] = {fa.x, fa.y, fa.z, fa.w, fb.x};
+      const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
+      const unsigned lt = lanemask_lt();
+      int nM = 0, nC = 0, base = 0;
+#pragma unroll
+      for (int s = 0; s < 5; ++s) {
+        if (s * 32 >= A) break;
+        const int i = s * 32 + lane;
+        const bool in = i < A;
+        const bool mv = in && ((mw[s] >> lane) & 1u);
+        const bool cp = in && !mv && i != ab && i != ae;
+        const unsigned bm = __ballot_sync(kFull, mv), bc = __ballot_sync(kFull, cp);
+        if (mv) S.mlist[nM + __popc(bm & lt)] = (uint8_t)i;
+        if (in && !mv) {
+          const float4 p = S.u[i];
+          if (cp) S.cmp[nC + __popc(bc & lt)] = p;
+          base += lat_grid_val(pk, node_index(g, p.x, p.y, p.z));
+        }
+        nM += __popc(bm);
+        nC += __popc(bc);
+      }
+      base = (int)__reduce_add_sync(kFull, (unsigned)base);
+      if (lane < kLatChunk) S.cmp[nC + lane] = make_float4(1e19f, 1e19f, 1e19f, 0.f);
+      if (lane == 0) {
+        S.nM = nM;
+        S.nC = nC;
+        S.base = base;
+        S.abump = 0u;
+        const float4 pa = S.u[ab], pb = S.u[ae];
+        if (dp.n_t > 1) {
+          const float vx = __fsub_rn(pb.x, pa.x), vy = __fsub_rn(pb.y, pa.y), vz = __fsub_rn(pb.z, pa.z);
+          const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
+          if (!(len >= dp.eps_axis)) S.degen = 1;
+          S.kx = __fdiv_rn(vx, len);
+          S.ky = __fdiv_rn(vy, len);
+          S.kz = __fdiv_rn(vz, len);
+        }
+      }
+      S.ascore[lane] = 0;
+    }
+    __syncthreads();
+    if (S.degen) break;
+    const int nM = S.nM, nC = S.nC;
+    const uint4 fb = __ldg(bt.frags + 2 * (size_t)(f0 + f) + 1);
+    const float4 pa = S.u[fb.y & 0xFFu];
+    const float3 a3 = make_float3(pa.x, pa.y, pa.z);
+    const float kx = S.kx, ky = S.ky, kz = S.kz;
+    unsigned best_key = 0u;
+    for (int k0 = 0; k0 < dp.n_t; k0 += 32) {
+      const int nA = min(32, dp.n_t - k0);
+      if (k0 > 0) {
+        if (tid < 32) S.ascore[tid] = 0;
+        if (tid == 0) S.abump = 0u;
+        __syncthreads();
+      }
+      unsigned my_pairs = 0;
+      for (int s = tid; s < nA * nM; s += kLatThreads) {
+        const int a = s / nM, m = s - a * nM;
+        if (dp.early_exit && ((*(volatile unsigned *)&S.abump >> a) & 1u)) continue;
+        const float3 q = lat_torsion_pos(pk, dp.step_t, k0 + a, kx, ky, kz, a3, S.u[S.mlist[m]]);
+        float mind = __int_as_float(0x7f800000);
+        bool retired = false;
+        for (int c = 0; c < nC; c += kLatChunk) {
+          if (dp.early_exit && ((*(volatile unsigned *)&S.abump >> a) & 1u)) {
+            retired = true;
+            break;
+          }
+          my_pairs += (unsigned)min(kLatChunk, nC - c);
+#pragma unroll
+          for (int t = 0; t < kLatChunk; ++t) {
+            const float4 y = S.cmp[c + t];
+            mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+          }
+          if (dp.early_exit && mind < dp.bd2) break;
+        }
+        if (retired) continue;
+        if (mind < dp.bd2) atomicOr(&S.abump, 1u << a);
+        else atomicAdd(&S.ascore[a], lat_grid_val(pk, node_index(g, q.x, q.y, q.z)));
+      }
+      my_pairs = __reduce_add_sync(kFull, my_pairs);
+      if (lane == 0) atomicAdd(&S.pairs, my_pairs);
+      __syncthreads();
+      if (warp == 0) {
+        unsigned kk = 0;
+        if (lane < nA && !((S.abump >> lane) & 1u))
+          kk = ((unsigned)(S.base + S.ascore[lane] + 32768) << 16) | (unsigned)(65535 - (k0 + lane));
+        best_key = max(best_key, __reduce_max_sync(kFull, kk));
+      }
+      evals += (unsigned)nA;
+      if (dp.early_exit) exits += (unsigned)__popc(S.abump);
+      __syncthreads();
+    }
+    if (warp == 0 && lane == 0) {
+      const int bk = best_key ? 65535 - (int)(best_key & 0xFFFFu) : -1;
+      S.best_k = bk;
+      out.rtors[(size_t)(f0 + f) * dp.N + r] = bk < 0 ? (uint8_t)DS_TORSION_NONE : (uint8_t)bk;
+    }
+    __syncthreads();
+    const int best_k = S.best_k;
+    if (best_k > 0)
+      for (int m = tid; m < nM; m += kLatThreads) {
+        const int i = S.mlist[m];
+        const float4 p = S.u[i];
+        const float3 q = lat_torsion_pos(pk, dp.step_t, best_k, kx, ky, kz, a3, p);
+        S.u[i] = make_float4(q.x, q.y, q.z, p.w);
+      }
+    if (best_k < 0) ++all_bumped;
+    __syncthreads();
+  }
+  // ---- final pose, geometric score, per-restart record ----
+  const int degen = S.degen;
+  float4 *scr = out.final_u + ((size_t)lig * dp.N + r) * DS_MAX_ATOMS;
+  if (!degen) {
+    int sc = 0, hv = 0;
+    for (int i = tid; i < A; i += kLatThreads) {
+      const float4 p = S.u[i];
+      sc += lat_grid_val(pk, node_index(g, p.x, p.y, p.z));
+      hv += p.w != 0.f;
+      scr[i] = p;
+    }
+    sc = (int)__reduce_add_sync(kFull, (unsigned)sc);
+    hv = (int)__reduce_add_sync(kFull, (unsigned)hv);
+    if (lane == 0) {
+      atomicAdd(&S.geom, sc);
+      atomicAdd(&S.heavy, hv);
+    }
+  }
+  __syncthreads();
+  const int valid = !(F >= 1 && all_bumped == F);
+  if (tid == 0) {
+    LatRec rec;
+    rec.geom = S.geom;
+    rec.valid = valid;
+    rec.degen = degen;
+    rec.align_score = (int)(key >> 16) - 32768;
+    rec.evals = evals;
+    rec.pairs = S.pairs;
+    rec.exits = exits;
+    rec.rot = (unsigned)rot;
+    recs[(size_t)lig * dp.N + r] = rec;
+    if (out.rrec) {
+      ds_restart_record rr;
+      rr.align_score = rec.align_score;
+      rr.final_geom = rec.geom;
+      rr.ax = (uint8_t)ix;
+      rr.ay = (uint8_t)iy;
+      rr.valid = (uint8_t)valid;
+      rr.kept = 0;
+      rr.reserved = 0;
+      out.rrec[(size_t)lig * dp.N + r] = rr;
+    }
+    __threadfence();
+    S.is_last = atomicAdd(done + lig, 1) == dp.N - 1;
+  }
+  __syncthreads();
+  if (!S.is_last) return;
+  __threadfence();
+
+  // ---- the ligand's last CTA: select_poses + rescore (P11, P12) ----
+  const LatRec *lr = recs + (size_t)lig * dp.N;
+  __shared__ int s_geom[DS_MAX_RESTARTS], s_valid[DS_MAX_RESTARTS];
+  __shared__ unsigned s_cnt[4];
+  if (tid < dp.N) {
+    s_geom[tid] = __ldcg(&lr[tid].geom);
+    s_valid[tid] = __ldcg(&lr[tid].valid);
+    S.dis[tid] = 0u;
+  }
+  if (tid == 0) {
+    unsigned ev = 0, pr = 0, ex = 0, dg = 0;
+    for (int q = 0; q < dp.N; ++q) {
+      ev += __ldcg(&lr[q].evals);
+      pr += __ldcg(&lr[q].pairs);
+      ex += __ldcg(&lr[q].exits);
+      dg |= (unsigned)__ldcg(&lr[q].degen);
+    }
+    s_cnt[0] = ev;
+    s_cnt[1] = pr;
+    s_cnt[2] = ex;
+    s_cnt[3] = dg;
+    S.chem = 0ull;
+  }
+  __syncthreads();
+  ds_result res;
+  memset(&res, 0, sizeof res);
+  res.poses_scored = (unsigned)(dp.N * dp.n_rot) + s_cnt[0];
+  res.bump_checks = s_cnt[1];
+  res.bump_early_exits = s_cnt[2];
+  if (s_cnt[3]) {
+    res.status = DS_STATUS_DEGENERATE_AXIS;
+    if (tid == 0) out.res[lig] = res;
+    return;
+  }
+  int nvalid = 0;
+  for (int q = 0; q < dp.N; ++q) nvalid += s_valid[q];
+  if (nvalid == 0) {
+    res.status = DS_STATUS_NO_VALID_POSE;
+    if (tid == 0) out.res[lig] = res;
+    return;
+  }
+  if (tid < dp.N && s_valid[tid]) {
+    int rank = 0;
+    for (int q = 0; q < dp.N; ++q)
+      rank += s_valid[q] && (s_geom[q] > s_geom[tid] || (s_geom[q] == s_geom[tid] && q < tid));
+    S.ord[rank] = tid;
+  }
+  const float4 *base_scr = out.final_u + (size_t)lig * dp.N * DS_MAX_ATOMS;
+  const int heavy = S.heavy;
+  const int npairs = dp.N * (dp.N - 1) / 2;
+  for (int pidx = tid; pidx < npairs; pidx += kLatThreads) {
+    int p = 0, rem = pidx;
+    while (rem >= dp.N - 1 - p) {
+      rem -= dp.N - 1 - p;
+      ++p;
+    }
+    const int q = p + 1 + rem;
+    if (!s_valid[p] || !s_valid[q]) continue;
+    double sum = 0.0;
+    const float4 *up = base_scr + (size_t)p * DS_MAX_ATOMS, *uq = base_scr + (size_t)q * DS_MAX_ATOMS;
+    for (int i = 0; i < A; ++i) {
+      const float4 x = __ldcg(up + i), y = __ldcg(uq + i);
+      if (x.w == 0.f) continue;
+      const double dx = __dsub_rn((double)x.x, (double)y.x);
+      const double dy = __dsub_rn((double)x.y, (double)y.y);
+      const double dz = __dsub_rn((double)x.z, (double)y.z);
+      double t = __dmul_rn(dx, dx);
+      t = __dadd_rn(t, __dmul_rn(dy, dy));
+      t = __dadd_rn(t, __dmul_rn(dz, dz));
+      sum = __dadd_rn(sum, t);
+    }
+    if (heavy > 0 && sum >= __dmul_rn(dp.thr2, (double)heavy)) {
+      atomicOr(&S.dis[p], 1u << q);
+      atomicOr(&S.dis[q], 1u << p);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int nk = 0;
+    for (int o = 0; o < nvalid && nk < dp.K; ++o) {
+      const int c = S.ord[o];
+      bool ok = true;
+      for (int t = 0; t < nk; ++t) ok = ok && ((S.dis[c] >> S.kept[t]) & 1u);
+      if (ok) S.kept[nk++] = c;
+    }
+    S.nkept = nk;
+  }
+  __syncthreads();
+  const int nk = S.nkept;
+  const int nb1 = pk.nb + 1;
+  long long best_chem = 0;
+  int best_r = -1;
+  for (int t = 0; t < nk; ++t) {
+    const int rr = S.kept[t];
+    for (int i = tid; i < A; i += kLatThreads) S.u[i] = __ldcg(base_scr + (size_t)rr * DS_MAX_ATOMS + i);
+    if (tid == 0) S.chem = 0ull;
+    __syncthreads();
+    long long acc = 0;
+    for (int j = tid; j < pk.n_atoms; j += kLatThreads) {
+      const float4 y = __ldg(pk.patoms + j);
+      const int tj = (int)y.w * nb1;
+      for (int i = 0; i < A; ++i) {
+        const float4 x = S.u[i];
+        const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
+        int b = 0;
+        for (int q = 0; q < pk.nb; ++q) b += !(d2 < pk.ub2[q]);
+        acc += __ldg(pk.wfx + (int)x.w * DS_N_TYPES * nb1 + tj + b);
+      }
+    }
+    atomicAdd(&S.chem, (unsigned long long)acc);
+    __syncthreads();
+    const long long chem = (long long)S.chem;
+    if (best_r < 0 || chem > best_chem || (chem == best_chem && rr < best_r)) {
+      best_chem = chem;
+      best_r = rr;
+    }
+    if (tid == 0 && out.rrec) out.rrec[(size_t)lig * dp.N + rr].kept = (uint8_t)(t + 1);
+    __syncthreads();
+  }
+  const int brot = (int)__ldcg(&lr[best_r].rot);
+  res.status = DS_STATUS_OK;
+  res.geom_score = s_geom[best_r];
+  res.chem_fx = best_chem;
+  res.best_restart = (uint8_t)best_r;
+  res.best_ax = (uint8_t)(brot / dp.n_a);
+  res.best_ay = (uint8_t)(brot - (brot / dp.n_a) * dp.n_a);
+  res.n_kept = (uint8_t)nk;
+  if (tid == 0) out.res[lig] = res;
+  if (out.best_coords)
+    for (int i = tid; i < A; i += kLatThreads) {
+      const float4 x = __ldcg(base_scr + (size_t)best_r * DS_MAX_ATOMS + i);
+      float *o = out.best_coords + 3 * (size_t)(a0 + i);
+      o[0] = __fmaf_rn(x.x, pk.spacing, pk.ox);
+      o[1] = __fmaf_rn(x.y, pk.spacing, pk.oy);
+      o[2] = __fmaf_rn(x.z, pk.spacing, pk.oz);
+    }
+  if (out.best_tors)
+    for (int f = tid; f < F; f += kLatThreads)
+      out.best_tors[f0 + f] = __ldcg(out.rtors + (size_t)(f0 + f) * dp.N + best_r);
+}
+
+size_t latency_rec_bytes() { return sizeof(LatRec); }
+
+void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *scores,
+                             OptOut out, void *recs, int *done, cudaStream_t st) {
+  k_optimize_latency<<<bt.L * dp.N, kLatThreads, 0, st>>>(pk, bt, dp, scores, out, (LatRec *)recs, done);
+}
+
+}  // namespace ds

@@ -32,6 +32,62 @@ def test_batched_parity_mixed(gpu_ctx, synth_pocket, table):
     compare(batch, g, o, cfg)
 
 
+@pytest.mark.parametrize("shape", [(12, 5), (36, 20), (8, 0)])
+def test_latency_parity_shapes(gpu_ctx, synth_pocket, table, shape):
+    """Latency family (one ligand spread over the GPU) against the oracle, one ligand per call and
+    a small batch per call."""
+    cfg = model.DockConfig()
+    batch = io.generate_dataset_batch(shape[0], shape[1], 6, seed=2)
+    for i in range(2):
+        one = batch.subset([i])
+        g, o = _run(gpu_ctx, one, synth_pocket, table, cfg, family=FAMILY_LATENCY)
+        compare(one, g, o, cfg)
+    g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg, family=FAMILY_LATENCY)
+    compare(batch, g, o, cfg)
+
+
+def test_latency_parity_mixed_and_options(gpu_ctx, synth_pocket, table):
+    batch = io.generate_mixed_batch(40, seed=6)
+    for cfg in (model.DockConfig(), model.DockConfig(early_exit=False),
+                model.DockConfig(restarts_n=5, rescore_top_k=3, alignment_step_deg=20, torsion_step_deg=30)):
+        g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg, family=FAMILY_LATENCY)
+        compare(batch, g, o, cfg)
+        if not cfg.early_exit:
+            assert np.array_equal(g.results["bump_checks"].astype(np.int64), o.results["bump_checks"])
+
+
+def test_families_agree(gpu_ctx, synth_pocket, table):
+    """Engine equivalence on the device: both families, identical records."""
+    batch = io.generate_mixed_batch(100, seed=8)
+    cfg = model.DockConfig()
+    dp = gpu_ctx.pocket(synth_pocket, table)
+    a = gpu_ctx.dock(dp, pack(batch), cfg, 3, FAMILY_BATCHED, coords=True, detail=True)
+    b = gpu_ctx.dock(dp, pack(batch), cfg, 3, FAMILY_LATENCY, coords=True, detail=True)
+    for f in ("status", "geom_score", "chem_fx", "best_restart", "best_ax", "best_ay", "n_kept", "poses_scored",
+              "bump_early_exits"):
+        assert np.array_equal(a.results[f], b.results[f]), f
+    assert np.array_equal(a.best_coords, b.best_coords)
+    assert np.array_equal(a.restart_torsion, b.restart_torsion)
+
+
+def test_batched_options(gpu_ctx, synth_pocket, table):
+    """Non-default DockConfig on the batched family (generic alignment kernel path)."""
+    batch = io.generate_mixed_batch(60, seed=9)
+    for cfg in (model.DockConfig(restarts_n=5, rescore_top_k=3, alignment_step_deg=20, torsion_step_deg=30),
+                model.DockConfig(restarts_n=12, rescore_top_k=6, alignment_step_deg=10, similarity_rmsd=0.5)):
+        g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg, seed=4)
+        compare(batch, g, o, cfg)
+
+
+def test_l2_variant_pocket_global_grid(gpu_ctx, table):
+    """Spacing 0.375 Å (75^3-class grid, too large for shared memory): the LDG/L2 path."""
+    pocket = io.synthetic_pocket(spacing=0.375)
+    batch = io.generate_mixed_batch(60, seed=10)
+    cfg = model.DockConfig()
+    g, o = _run(gpu_ctx, batch, pocket, table, cfg)
+    compare(batch, g, o, cfg)
+
+
 def test_batched_parity_no_early_exit(gpu_ctx, synth_pocket, table):
     batch = io.generate_mixed_batch(64, seed=4)
     cfg = model.DockConfig(early_exit=False)
