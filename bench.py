@@ -184,7 +184,7 @@ def main():
     table = InteractionTable.default()
     n = args.ligands
     batch = io.generate_mixed_batch(n, seed=args.seed, first_index=rank * n)
-    packed = pack(batch)
+    packed = pack(batch, pinned=True)   # inputs in pinned host memory (e2e contract)
     ctx = native.Context(local)
     dp = ctx.pocket(pocket, table)
 
@@ -221,13 +221,14 @@ def main():
     # ---- end to end through ds_dock with host buffers ----
     e2e = None
     if not args.no_e2e:
+        bufs = native.OutputBuffers(packed, pinned=True)   # pinned result records + best poses
         for _ in range(1):
-            out = ctx.dock(dp, packed, cfg, 0, native.FAMILY_BATCHED, coords=True)
+            out = ctx.dock(dp, packed, cfg, 0, native.FAMILY_BATCHED, coords=True, buffers=bufs)
         barrier()
         t0 = time.perf_counter()
         h2d = d2h = 0
         for _ in range(args.steps):
-            out = ctx.dock(dp, packed, cfg, 0, native.FAMILY_BATCHED, coords=True)
+            out = ctx.dock(dp, packed, cfg, 0, native.FAMILY_BATCHED, coords=True, buffers=bufs)
             h2d, d2h = out.stats.h2d_bytes, out.stats.d2h_bytes
         barrier()
         dt = max_over_ranks((time.perf_counter() - t0) / args.steps)

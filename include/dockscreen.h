@@ -172,6 +172,10 @@ void ds_destroy(ds_ctx *ctx);
 int ds_ctx_alloc_count(const ds_ctx *ctx, int64_t *count);
 /* Opaque cudaStream_t of the ctx (for external event timing). */
 void *ds_ctx_stream(ds_ctx *ctx);
+/* Pinned (page-locked) host memory.  Batch arrays and output buffers placed here are
+ * DMA'd directly by ds_dock (no staging copy).  NULL on failure. */
+void *ds_host_alloc(size_t bytes);
+void ds_host_free(void *ptr);
 int ds_synchronize(ds_ctx *ctx);
 
 /* ---- pocket ------------------------------------------------------------- */

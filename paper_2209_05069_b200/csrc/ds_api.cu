@@ -195,6 +195,20 @@ int ds_ctx_alloc_count(const ds_ctx *c, int64_t *count) {
 
 void *ds_ctx_stream(ds_ctx *c) { return c ? (void *)c->stream : nullptr; }
 
+void *ds_host_alloc(size_t bytes) {
+  void *p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    fail(DS_ERR_OOM, "cudaHostAlloc(%zu) failed", bytes);
+    return nullptr;
+  }
+  return p;
+}
+
+void ds_host_free(void *p) {
+  if (p) cudaFreeHost(p);
+}
+
 int ds_synchronize(ds_ctx *c) {
   if (!c) return fail(DS_ERR_INVALID_ARG, "NULL ctx");
   DS_CUDA(cudaStreamSynchronize(c->stream));
@@ -361,6 +375,7 @@ int check_config(const ds_dock_config *cfg, const ds_pocket *pk, DockParams *dp)
   dp->eps_axis = (float)(1e-9 / s);                        // P8
   const double th = (double)cfg->similarity_rmsd / s;
   dp->thr2 = th * th;                                      // P12
+  dp->cull2 = (float)((bd + 0.02) * (bd + 0.02));          // conservative bump-candidate bound
   return DS_OK;
 }
 
@@ -390,23 +405,36 @@ void lpt_orders(const ds_batch_desc *b, std::vector<int> &oa, std::vector<int> &
   const int L = b->n_ligands;
   oa.resize(L);
   oo.resize(L);
-  std::vector<int> cnt(DS_MAX_ATOMS + 2, 0);
-  for (int i = 0; i < L; ++i) cnt[DS_MAX_ATOMS - (b->atom_off[i + 1] - b->atom_off[i])]++;
-  std::vector<int> pos(DS_MAX_ATOMS + 2, 0);
-  for (int k = 1; k <= DS_MAX_ATOMS + 1; ++k) pos[k] = pos[k - 1] + cnt[k - 1];
-  for (int i = 0; i < L; ++i) oa[pos[DS_MAX_ATOMS - (b->atom_off[i + 1] - b->atom_off[i])]++] = i;
-  std::vector<std::pair<int64_t, int>> cost(L);
-  for (int i = 0; i < L; ++i) {
-    const int64_t A = b->atom_off[i + 1] - b->atom_off[i], F = b->frag_off[i + 1] - b->frag_off[i];
-    cost[i] = {-(F * A * A / 4 + 4 * A), i};
-  }
-  std::sort(cost.begin(), cost.end());
-  for (int i = 0; i < L; ++i) oo[i] = cost[i].second;
+  // counting sorts, descending cost: alignment ~ A, optimisation ~ (F + 2) * A (torsion slots
+  // plus restart rebuild/rescore), both O(L)
+  auto csort = [&](std::vector<int> &out, int nkeys, auto key) {
+    std::vector<int> cnt(nkeys + 1, 0);
+    for (int i = 0; i < L; ++i) cnt[nkeys - 1 - key(i)]++;
+    int run = 0;
+    for (int k = 0; k < nkeys; ++k) {
+      const int t = cnt[k];
+      cnt[k] = run;
+      run += t;
+    }
+    for (int i = 0; i < L; ++i) out[cnt[nkeys - 1 - key(i)]++] = i;
+  };
+  csort(oa, DS_MAX_ATOMS + 1, [&](int i) { return b->atom_off[i + 1] - b->atom_off[i]; });
+  const int kmax = 4096;
+  csort(oo, kmax, [&](int i) {
+    const int A = b->atom_off[i + 1] - b->atom_off[i], F = b->frag_off[i + 1] - b->frag_off[i];
+    return std::min(kmax - 1, ((F + 2) * A) >> 3);
+  });
 }
 
-struct Staged {
-  size_t off_atom_off, off_atoms, off_frag_off, off_frags, off_idh, off_oa, off_oo, total;
-};
+bool is_pinned(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 
 int upload_batch(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
   const int L = b->n_ligands;
@@ -423,39 +451,36 @@ int upload_batch(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
       (rc = c->ensure(c->b_rtors, (size_t)std::max(NF, 1) * N)) || (rc = c->ensure(c->b_coords, 12ull * std::max(NA, 1))) ||
       (rc = c->ensure(c->b_btors, (size_t)std::max(NF, 1))) || (rc = c->ensure(c->b_queue, 256)))
     return rc;
-  // stage into pinned memory, one H2D per array
-  Staged s;
+  // One H2D per array.  Arrays already in pinned memory (ds_host_alloc) are DMA'd directly;
+  // pageable ones are first copied into the ctx's pinned staging buffer.
+  struct Arr {
+    void *dst;
+    const void *src;
+    size_t bytes;
+    bool pinned;
+    size_t off;
+  } arrs[7] = {{c->b_atom_off.p, b->atom_off, 4ull * (L + 1)},   {c->b_atoms.p, b->atom_xyzt, 16ull * NA},
+               {c->b_frag_off.p, b->frag_off, 4ull * (L + 1)},   {c->b_frags.p, b->frag_desc, 32ull * NF},
+               {c->b_idh.p, b->id_hash, 8ull * L},               {c->b_order_a.p, oa.data(), 4ull * L},
+               {c->b_order_o.p, oo.data(), 4ull * L}};
   size_t o = 0;
-  auto take = [&](size_t bytes) {
-    size_t r = o;
-    o += (bytes + 255) & ~(size_t)255;
-    return r;
-  };
-  s.off_atom_off = take(4ull * (L + 1));
-  s.off_atoms = take(16ull * NA);
-  s.off_frag_off = take(4ull * (L + 1));
-  s.off_frags = take(32ull * NF);
-  s.off_idh = take(8ull * L);
-  s.off_oa = take(4ull * L);
-  s.off_oo = take(4ull * L);
-  s.total = o;
-  if ((rc = c->ensure_host(s.total))) return rc;
+  for (int k = 0; k < 7; ++k) {
+    arrs[k].pinned = k < 5 && arrs[k].bytes >= (1u << 16) && is_pinned(arrs[k].src);
+    arrs[k].off = o;
+    if (!arrs[k].pinned) o += (arrs[k].bytes + 255) & ~(size_t)255;
+  }
+  if ((rc = c->ensure_host(std::max<size_t>(o, 256)))) return rc;
   char *h = (char *)c->h_stage;
-  memcpy(h + s.off_atom_off, b->atom_off, 4ull * (L + 1));
-  memcpy(h + s.off_atoms, b->atom_xyzt, 16ull * NA);
-  memcpy(h + s.off_frag_off, b->frag_off, 4ull * (L + 1));
-  if (NF) memcpy(h + s.off_frags, b->frag_desc, 32ull * NF);
-  memcpy(h + s.off_idh, b->id_hash, 8ull * L);
-  memcpy(h + s.off_oa, oa.data(), 4ull * L);
-  memcpy(h + s.off_oo, oo.data(), 4ull * L);
   cudaStream_t st_ = c->stream;
-  DS_CUDA(cudaMemcpyAsync(c->b_atom_off.p, h + s.off_atom_off, 4ull * (L + 1), cudaMemcpyHostToDevice, st_));
-  DS_CUDA(cudaMemcpyAsync(c->b_atoms.p, h + s.off_atoms, 16ull * NA, cudaMemcpyHostToDevice, st_));
-  DS_CUDA(cudaMemcpyAsync(c->b_frag_off.p, h + s.off_frag_off, 4ull * (L + 1), cudaMemcpyHostToDevice, st_));
-  if (NF) DS_CUDA(cudaMemcpyAsync(c->b_frags.p, h + s.off_frags, 32ull * NF, cudaMemcpyHostToDevice, st_));
-  DS_CUDA(cudaMemcpyAsync(c->b_idh.p, h + s.off_idh, 8ull * L, cudaMemcpyHostToDevice, st_));
-  DS_CUDA(cudaMemcpyAsync(c->b_order_a.p, h + s.off_oa, 4ull * L, cudaMemcpyHostToDevice, st_));
-  DS_CUDA(cudaMemcpyAsync(c->b_order_o.p, h + s.off_oo, 4ull * L, cudaMemcpyHostToDevice, st_));
+  for (int k = 0; k < 7; ++k) {
+    if (!arrs[k].bytes) continue;
+    const void *src = arrs[k].src;
+    if (!arrs[k].pinned) {
+      memcpy(h + arrs[k].off, src, arrs[k].bytes);
+      src = h + arrs[k].off;
+    }
+    DS_CUDA(cudaMemcpyAsync(arrs[k].dst, src, arrs[k].bytes, cudaMemcpyHostToDevice, st_));
+  }
   if (st) st->h2d_bytes += (int64_t)(4ull * (L + 1) * 2 + 16ull * NA + 32ull * NF + 8ull * L + 8ull * L);
   return DS_OK;
 }

@@ -36,6 +36,7 @@ struct DockParams {
   float bd2;                 // squared bump distance, grid frame
   float eps_axis;            // DegenerateAxis threshold, grid frame
   double thr2;               // squared similarity RMSD, grid frame
+  float cull2;               // squared bump-candidate bound (bump distance + 0.02 nodes), grid frame
 };
 
 struct AlignOut {

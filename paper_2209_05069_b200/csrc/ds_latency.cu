@@ -20,10 +20,15 @@ struct LatRec {  // per (ligand, restart), read by the ligand's last CTA
   unsigned evals, pairs, exits, rot;
 };
 
+constexpr int kLatCand = 8;
+
 struct LatSmem {
   float4 u[DS_MAX_ATOMS];
   float4 cmp[DS_MAX_ATOMS + kLatChunk];
+  float2 chr[DS_MAX_ATOMS];
   uint8_t mlist[DS_MAX_ATOMS];
+  uint8_t cl[DS_MAX_ATOMS][kLatCand];
+  uint8_t cn[DS_MAX_ATOMS];
   int ascore[32];
   unsigned abump;
   unsigned key;
@@ -38,6 +43,12 @@ struct LatSmem {
 };
 
 __device__ __forceinline__ int lat_grid_val(const PocketView &pk, int idx) { return (int)__ldg(pk.grid + idx) - 128; }
+
+__device__ __forceinline__ float2 lat_cyl(float4 p, float3 a, float kx, float ky, float kz) {
+  const float wx = p.x - a.x, wy = p.y - a.y, wz = p.z - a.z;
+  const float h = wx * kx + wy * ky + wz * kz;
+  return make_float2(h, sqrtf(fmaxf(wx * wx + wy * wy + wz * wz - h * h, 0.f)));
+}
 
 __device__ __forceinline__ float3 lat_torsion_pos(const PocketView &pk, int step_t, int k, float kx, float ky, float kz,
                                                   float3 a, float4 p) {
@@ -144,6 +155,23 @@ __global__ void __launch_bounds__(kLatThreads)
     const float4 pa = S.u[fb.y & 0xFFu];
     const float3 a3 = make_float3(pa.x, pa.y, pa.z);
     const float kx = S.kx, ky = S.ky, kz = S.kz;
+    // bump candidates per moving atom (cylindrical bound, see ds_optimize.cu)
+    for (int c = tid; c < nC; c += kLatThreads) S.chr[c] = lat_cyl(S.cmp[c], a3, kx, ky, kz);
+    __syncthreads();
+    for (int m = tid; m < nM; m += kLatThreads) {
+      const float2 hm = lat_cyl(S.u[S.mlist[m]], a3, kx, ky, kz);
+      int cnt = 0;
+      for (int c = 0; c < nC; ++c) {
+        const float2 hc = S.chr[c];
+        const float dh = hm.x - hc.x, dr = hm.y - hc.y;
+        if (dh * dh + dr * dr < dp.cull2) {
+          if (cnt < kLatCand) S.cl[m][cnt] = (uint8_t)c;
+          ++cnt;
+        }
+      }
+      S.cn[m] = (uint8_t)(cnt > kLatCand ? 255 : cnt);
+    }
+    __syncthreads();
     unsigned best_key = 0u;
     for (int k0 = 0; k0 < dp.n_t; k0 += 32) {
       const int nA = min(32, dp.n_t - k0);
@@ -158,21 +186,22 @@ __global__ void __launch_bounds__(kLatThreads)
         if (dp.early_exit && ((*(volatile unsigned *)&S.abump >> a) & 1u)) continue;
         const float3 q = lat_torsion_pos(pk, dp.step_t, k0 + a, kx, ky, kz, a3, S.u[S.mlist[m]]);
         float mind = __int_as_float(0x7f800000);
-        bool retired = false;
-        for (int c = 0; c < nC; c += kLatChunk) {
-          if (dp.early_exit && ((*(volatile unsigned *)&S.abump >> a) & 1u)) {
-            retired = true;
-            break;
-          }
-          my_pairs += (unsigned)min(kLatChunk, nC - c);
-#pragma unroll
-          for (int t = 0; t < kLatChunk; ++t) {
-            const float4 y = S.cmp[c + t];
+        my_pairs += (unsigned)nC;  // pairs resolved (P14)
+        const int cnt = S.cn[m];
+        if (cnt != 255) {
+          for (int t = 0; t < cnt; ++t) {
+            const float4 y = S.cmp[S.cl[m][t]];
             mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
           }
-          if (dp.early_exit && mind < dp.bd2) break;
+        } else {
+          for (int c = 0; c < nC; c += kLatChunk) {
+#pragma unroll
+            for (int t = 0; t < kLatChunk; ++t) {
+              const float4 y = S.cmp[c + t];
+              mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+            }
+          }
         }
-        if (retired) continue;
         if (mind < dp.bd2) atomicOr(&S.abump, 1u << a);
         else atomicAdd(&S.ascore[a], lat_grid_val(pk, node_index(g, q.x, q.y, q.z)));
       }

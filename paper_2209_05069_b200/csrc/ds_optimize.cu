@@ -3,30 +3,36 @@
 //
 // Per restart the warp rebuilds the aligned pose from the packed argmax key of the alignment
 // kernel, then walks the fragments in list order (they are stateful).  Per
-// fragment it compacts the moving set M and the bump-relevant complement C' (not M, not an axis
-// atom) into shared memory with ballots, and then sweeps ALL torsion angles at once: lanes own
-// (angle, moving atom) slots, rotate their atom in registers, and scan C' broadcast from shared
-// memory (one LDS.128 per complement atom per warp).  A bump retires every lane of that angle at
-// the next chunk boundary (__ballot_sync + __match_any_sync) — the early exit costs one vote per
-// chunk, which is why the batched shape wins.  Clean angles are scored as
-// base + sum over M (the non-moving atoms' grid values do not depend on the angle) with exact
-// integer shared-memory adds, and the best clean angle (ties -> smallest) is committed.
+// fragment:
+//  * ballots compact the moving set M and the bump-relevant complement C' (not M, not an axis atom);
+//  * bump candidates: a torsion keeps each moving atom on its circle about the axis, so (i, j)
+//    can only bump if the distance between i's circle and j — sqrt(dh^2 + dr^2) in cylindrical
+//    coordinates about the axis — is below the bump distance.  Pairs failing that bound (with a
+//    0.02-node margin that dwarfs f32 rounding) are resolved once per fragment instead of once per
+//    angle; the survivors (~1.5 % of pairs on the config-3 mix) form a CSR candidate list per
+//    moving atom and are checked exactly with P9 for every angle;
+//  * all torsion angles at once: lanes own (angle, moving atom) slots, rotate their atom in
+//    registers and test its candidates; a hit marks the angle bumped, clean slots add their grid
+//    value (exact integer smem adds) to base + sum over M (non-moving atoms do not change);
+//  * the best clean angle (ties -> smallest) is committed.
 // Then select_poses (heavy-atom RMSD in f64, lanes over pose pairs) and an integer fixed-point
-// rescore (order-free, exact) with the pocket atoms and the weight table staged in shared memory.
+// rescore (order-free, exact) with pocket atoms and weights staged in shared memory.
 #include "ds_kernels.cuh"
 
 namespace ds {
 
 constexpr int kMaxA = DS_MAX_ATOMS;
-constexpr int kChunk = 8;            // complement atoms between early-exit votes
+constexpr int kCand = 6;             // bump-candidate slots per moving atom (overflow: full scan)
 
 struct OptWarpSmem {
-  float4 u[kMaxA];       // committed pose of the current restart (grid frame), .w = type
-  float4 cmp[kMaxA + kChunk];  // compacted complement C' of the current fragment (+ far sentinels)
-  uint8_t mlist[kMaxA];  // moving atom indices in ascending order
-  int ascore[32];        // per-angle sums over M (current angle block)
-  unsigned abump;        // bumped-angle bits (current angle block)
-  unsigned pad[3];
+  float4 u[kMaxA];          // committed pose of the current restart (grid frame), .w = type
+  float2 chr[kMaxA];        // cylindrical (h, r) of the C' atoms about the fragment axis
+  uint8_t mlist[kMaxA];     // moving atom indices, ascending
+  uint8_t clist[kMaxA];     // complement atom indices, ascending
+  uint8_t cl[kMaxA][kCand]; // bump-candidate atom indices per moving atom
+  uint8_t cn[kMaxA];        // candidate count, 255 = overflow (scan all of C')
+  int ascore[32];           // per-angle sums over M (current angle block)
+  unsigned abump;           // bumped-angle bits (current angle block)
   int geom[DS_MAX_RESTARTS];
   int valid[DS_MAX_RESTARTS];
   unsigned dis[DS_MAX_RESTARTS];   // dissimilarity bitsets (select_poses)
@@ -44,6 +50,15 @@ __device__ __forceinline__ long long warp_sum64(long long v) {
   return v;
 }
 
+// cylindrical coordinates (h along the axis, r from it) of p about the axis through a along k;
+// only used for the conservative culling bound, so its rounding does not matter
+__device__ __forceinline__ float2 cyl_coords(float4 p, float3 a, float kx, float ky, float kz) {
+  const float wx = p.x - a.x, wy = p.y - a.y, wz = p.z - a.z;
+  const float h = wx * kx + wy * ky + wz * kz;
+  const float r2 = wx * wx + wy * wy + wz * wz - h * h;
+  return make_float2(h, sqrtf(fmaxf(r2, 0.f)));
+}
+
 // rotated position of a moving atom for torsion angle index k (k == 0: identity, P8)
 __device__ __forceinline__ float3 torsion_pos(const PocketView &pk, int step_t, int k, float kx, float ky, float kz,
                                               float3 a, float4 p) {
@@ -55,12 +70,13 @@ __device__ __forceinline__ float3 torsion_pos(const PocketView &pk, int step_t, 
 }
 
 // rescore sum of one pose against all pocket atoms (P11).  Lanes own pocket atoms (staged in
-// smem with .w = the integer row offset tj*(nb+1)); ligand atoms are broadcast from S.u.
+// smem with .w = the integer column offset tj*(nb+1)); ligand atoms are broadcast from S.u whose
+// .w holds the integer row offset ti*16*(nb+1).  Partial sums stay in int32 for <= 64 atoms
+// (|W| <= 2^24) before widening.
 template <int NB>
 __device__ __forceinline__ long long rescore_pose(const OptWarpSmem &S, int A, const float4 *pat, int P,
                                                   const int32_t *wfx, int nb, const float *ub2) {
   long long acc = 0;
-  const int nb1 = NB > 0 ? NB + 1 : nb + 1;
   float u[DS_MAX_BINS];
 #pragma unroll
   for (int q = 0; q < DS_MAX_BINS; ++q) u[q] = ub2[q];
@@ -69,24 +85,28 @@ __device__ __forceinline__ long long rescore_pose(const OptWarpSmem &S, int A, c
     // past-the-end lanes use a far sentinel: its bin is nb, whose weight is 0
     const float4 y = j < P ? pat[j] : make_float4(1e19f, 1e19f, 1e19f, 0.f);
     const int32_t *wcol = wfx + __float_as_int(y.w);
-    for (int i = 0; i < A; ++i) {
-      const float4 x = S.u[i];
-      const int row = (int)x.w * DS_N_TYPES * nb1;
-      const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
-      int b = 0;
-      if (NB > 0) {
+    for (int i0 = 0; i0 < A; i0 += 64) {
+      int part = 0;
+      const int i1 = min(A, i0 + 64);
+      for (int i = i0; i < i1; ++i) {
+        const float4 x = S.u[i];
+        const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
+        int b = __float_as_int(x.w);
+        if (NB > 0) {
 #pragma unroll
-        for (int q = 0; q < NB; ++q) b += !(d2 < u[q]);
-      } else {
-        for (int q = 0; q < nb; ++q) b += !(d2 < u[q]);
+          for (int q = 0; q < NB; ++q) b += !(d2 < u[q]);
+        } else {
+          for (int q = 0; q < nb; ++q) b += !(d2 < u[q]);
+        }
+        part += wcol[b];
       }
-      acc += wcol[row + b];
+      acc += part;
     }
   }
   return acc;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
     k_optimize_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
                        OptOut out, int *queue) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -102,13 +122,12 @@ __global__ void __launch_bounds__(256)
   OptWarpSmem &S = reinterpret_cast<OptWarpSmem *>(smem + fixed)[warp];
   for (int j = threadIdx.x; j < pk.n_atoms; j += blockDim.x) {
     float4 y = __ldg(pk.patoms + j);
-    y.w = __int_as_float((int)y.w * nb1);  // row offset of the pocket atom's type in the weight table
+    y.w = __int_as_float((int)y.w * nb1);  // column offset of the pocket atom's type in the weight table
     s_pat[j] = y;
   }
   for (int j = threadIdx.x; j < wsz; j += blockDim.x) s_w[j] = __ldg(pk.wfx + j);
   if (threadIdx.x < DS_MAX_BINS) s_ub2[threadIdx.x] = pk.ub2[threadIdx.x];
   __syncthreads();
-  const float4 *pat = s_pat;
 
   const int gwarp = blockIdx.x * nwarps + warp;
   float4 *scr = out.final_u + (size_t)gwarp * dp.N * kMaxA;  // final poses of the N restarts
@@ -166,16 +185,15 @@ __global__ void __launch_bounds__(256)
           const bool cp = in && !mv && i != ab && i != ae;
           const unsigned bm = __ballot_sync(kFull, mv), bc = __ballot_sync(kFull, cp);
           if (mv) S.mlist[nM + __popc(bm & lt)] = (uint8_t)i;
+          if (cp) S.clist[nC + __popc(bc & lt)] = (uint8_t)i;
           if (in && !mv) {
             const float4 p = S.u[i];
-            if (cp) S.cmp[nC + __popc(bc & lt)] = p;
             base += grid_val(pk, node_index(g, p.x, p.y, p.z));
           }
           nM += __popc(bm);
           nC += __popc(bc);
         }
         base = warp_sum(base);
-        if (lane < kChunk) S.cmp[nC + lane] = make_float4(1e19f, 1e19f, 1e19f, 0.f);
         const float4 pa = S.u[ab], pb = S.u[ae];
         const float3 a3 = make_float3(pa.x, pa.y, pa.z);
         float kx = 0.f, ky = 0.f, kz = 0.f;
@@ -189,6 +207,23 @@ __global__ void __launch_bounds__(256)
           kx = __fdiv_rn(vx, len);
           ky = __fdiv_rn(vy, len);
           kz = __fdiv_rn(vz, len);
+        }
+        __syncwarp();
+        // ---- bump candidates (CSR per moving atom) ----
+        for (int c = lane; c < nC; c += 32) S.chr[c] = cyl_coords(S.u[S.clist[c]], a3, kx, ky, kz);
+        __syncwarp();
+        for (int m = lane; m < nM; m += 32) {
+          const float2 hm = cyl_coords(S.u[S.mlist[m]], a3, kx, ky, kz);
+          int cnt = 0;
+          for (int c = 0; c < nC; ++c) {
+            const float2 hc = S.chr[c];
+            const float dh = hm.x - hc.x, dr = hm.y - hc.y;
+            if (dh * dh + dr * dr < dp.cull2) {
+              if (cnt < kCand) S.cl[m][cnt] = S.clist[c];
+              ++cnt;
+            }
+          }
+          S.cn[m] = (uint8_t)(cnt > kCand ? 255 : cnt);
         }
         unsigned best_key = 0;  // (score + 32768) << 16 | (65535 - angle); 0 = no clean angle
         for (int k0 = 0; k0 < dp.n_t; k0 += 32) {
@@ -206,31 +241,24 @@ __global__ void __launch_bounds__(256)
             const bool pre = valid && !(dp.early_exit && ((S.abump >> sa) & 1u));
             const unsigned act0 = __ballot_sync(kFull, pre);
             if (act0) {
-              float3 q = make_float3(0.f, 0.f, 0.f);
-              if (pre) q = torsion_pos(pk, dp.step_t, k0 + sa, kx, ky, kz, a3, S.u[S.mlist[sm]]);
-              const unsigned same = __match_any_sync(kFull, valid ? sa : -1);
-              bool active = pre;
-              float mind = __int_as_float(0x7f800000);  // min squared distance seen (P9: bump iff < bd2)
-              for (int c = 0; c < nC; c += kChunk) {   // cmp[] is padded with far sentinels to kChunk
-                const unsigned am = __ballot_sync(kFull, active);
-                if (!am) break;
-                pairs_total += (unsigned)__popc(am) * (unsigned)min(kChunk, nC - c);
-#pragma unroll
-                for (int t = 0; t < kChunk; ++t) {
-                  const float4 y = S.cmp[c + t];
-                  mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+              pairs_total += (unsigned)__popc(act0) * (unsigned)nC;  // pairs resolved (P14)
+              if (pre) {
+                const float3 q = torsion_pos(pk, dp.step_t, k0 + sa, kx, ky, kz, a3, S.u[S.mlist[sm]]);
+                float mind = __int_as_float(0x7f800000);  // min squared distance (P9: bump iff < bd2)
+                const int cnt = S.cn[sm];
+                if (cnt != 255) {
+                  for (int t = 0; t < cnt; ++t) {
+                    const float4 y = S.u[S.cl[sm][t]];
+                    mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+                  }
+                } else {
+                  for (int c = 0; c < nC; ++c) {
+                    const float4 y = S.u[S.clist[c]];
+                    mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+                  }
                 }
-                if (dp.early_exit) {
-                  const unsigned hb = __ballot_sync(kFull, pre && mind < dp.bd2);
-                  active = active && !(hb & same);
-                }
-              }
-              const bool hit = pre && mind < dp.bd2;
-              const unsigned hb = __ballot_sync(kFull, hit);
-              if (hit) atomicOr(&S.abump, 1u << sa);
-              if (pre && !(hb & same)) {
-                const int v = grid_val(pk, node_index(g, q.x, q.y, q.z));
-                atomicAdd(&S.ascore[sa], v);
+                if (mind < dp.bd2) atomicOr(&S.abump, 1u << sa);
+                else atomicAdd(&S.ascore[sa], grid_val(pk, node_index(g, q.x, q.y, q.z)));
               }
             }
             sa += qa;
@@ -241,13 +269,11 @@ __global__ void __launch_bounds__(256)
             }
             __syncwarp();
           }
-          __syncwarp();
           unsigned kk = 0;
           if (lane < nA && !((S.abump >> lane) & 1u))
             kk = ((unsigned)(base + S.ascore[lane] + 32768) << 16) | (unsigned)(65535 - (k0 + lane));
-          const unsigned nb_bump = (unsigned)__popc(S.abump);
           evals += (unsigned)nA;
-          if (dp.early_exit) early_exits += nb_bump;
+          if (dp.early_exit) early_exits += (unsigned)__popc(S.abump);
           best_key = max(best_key, __reduce_max_sync(kFull, kk));
           __syncwarp();
         }
@@ -379,10 +405,14 @@ __global__ void __launch_bounds__(256)
     for (int t = 0; t < nk; ++t) {
       const int r = S.kept[t];
       __syncwarp();
-      for (int i = lane; i < A; i += 32) S.u[i] = scr[(size_t)r * kMaxA + i];
+      for (int i = lane; i < A; i += 32) {
+        float4 x = scr[(size_t)r * kMaxA + i];
+        x.w = __int_as_float((int)x.w * DS_N_TYPES * nb1);  // row offset of the ligand atom's type
+        S.u[i] = x;
+      }
       __syncwarp();
-      long long acc = pk.nb == 4 ? rescore_pose<4>(S, A, pat, pk.n_atoms, s_w, pk.nb, s_ub2)
-                                 : rescore_pose<0>(S, A, pat, pk.n_atoms, s_w, pk.nb, s_ub2);
+      long long acc = pk.nb == 4 ? rescore_pose<4>(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2)
+                                 : rescore_pose<0>(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2);
       acc = warp_sum64(acc);
       if (best_r < 0 || acc > best_chem || (acc == best_chem && r < best_r)) {
         best_chem = acc;

@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import weakref
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
@@ -105,6 +106,7 @@ def lib():
             "ds_device_count": (C.c_int, [vp]), "ds_create": (C.c_int, [C.c_int, vp]),
             "ds_destroy": (None, [vp]), "ds_ctx_alloc_count": (C.c_int, [vp, vp]),
             "ds_ctx_stream": (vp, [vp]), "ds_synchronize": (C.c_int, [vp]),
+            "ds_host_alloc": (vp, [C.c_size_t]), "ds_host_free": (None, [vp]),
             "ds_pocket_create": (C.c_int, [vp, vp, vp]), "ds_pocket_destroy": (None, [vp]),
             "ds_dock": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, vp]),
             "ds_batch_upload": (C.c_int, [vp, vp, vp]),
@@ -130,6 +132,25 @@ def lib():
             raise NativeUnavailable("libdockscreen ABI mismatch")
         _lib = L
         return L
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """A numpy array in pinned host memory (ds_host_alloc); ds_dock DMAs such arrays directly."""
+    dtype = np.dtype(dtype)
+    count = int(np.prod(shape))
+    nbytes = max(count * dtype.itemsize, 1)
+    ptr = lib().ds_host_alloc(nbytes)
+    if not ptr:
+        raise MemoryError(f"ds_host_alloc({nbytes}) failed")
+    buf = (C.c_char * nbytes).from_address(ptr)
+    weakref.finalize(buf, lib().ds_host_free, ptr)
+    return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
+
+
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    out = pinned_empty(a.shape, a.dtype)
+    out[...] = a
+    return out
 
 
 def check(rc: int):
@@ -250,14 +271,16 @@ class PackedBatch:
         return d
 
 
-def pack(batch: LigandBatch) -> PackedBatch:
-    """Validate + pack (ds_pack_ligands): c0 = f32(f64 mean), d = p - c0 (DESIGN.md §3 P2)."""
+def pack(batch: LigandBatch, pinned: bool = False) -> PackedBatch:
+    """Validate + pack (ds_pack_ligands): c0 = f32(f64 mean), d = p - c0 (DESIGN.md §3 P2).
+    pinned=True places the packed arrays in page-locked memory (direct DMA by ds_dock)."""
     n = batch.n
     na, nf = int(batch.atom_off[-1]), int(batch.frag_off[-1])
-    xyzt = np.zeros((max(na, 1), 4), dtype=np.float32)
-    fdesc = np.zeros((max(nf, 1), FRAG_WORDS), dtype=np.uint32)
-    idh = np.zeros(max(n, 1), dtype=np.uint64)
-    cen = np.zeros((max(n, 1), 3), dtype=np.float32)
+    alloc = pinned_empty if pinned else (lambda s, d: np.empty(s, d))
+    xyzt = alloc((max(na, 1), 4), np.float32)
+    fdesc = alloc((max(nf, 1), FRAG_WORDS), np.uint32)
+    idh = alloc(max(n, 1), np.uint64)
+    cen = alloc((max(n, 1), 3), np.float32)
     ids, id_off = batch.id_bytes()
     idbuf = C.create_string_buffer(ids, max(len(ids), 1))
     bad = C.c_int32(-1)
@@ -274,6 +297,8 @@ def pack(batch: LigandBatch) -> PackedBatch:
         exc = ERRORS.get(rc, DsError)
         who = batch.ids[bad.value] if 0 <= bad.value < n else "?"
         raise exc(f"ligand {who}: invalid ({rc}) {msg}")
+    if pinned:
+        ao, fo = pinned_copy(ao), pinned_copy(fo)
     return PackedBatch(n, ao, xyzt, fo, fdesc, idh[:n] if n else idh[:0], cen)
 
 
@@ -353,6 +378,18 @@ class DockOutput:
     stats: Stats
 
 
+class OutputBuffers:
+    """Reusable (pinned by default) result buffers for repeated ds_dock calls on one batch shape."""
+
+    def __init__(self, packed: PackedBatch, pinned: bool = True):
+        alloc = pinned_empty if pinned else (lambda s, d: np.zeros(s, d))
+        n = packed.n
+        na, nf = int(packed.atom_off[-1]) if n else 0, int(packed.frag_off[-1]) if n else 0
+        self.results = alloc(max(n, 1), RESULT_DTYPE)
+        self.best_coords = alloc((max(na, 1), 3), np.float32)
+        self.best_torsion = alloc(max(nf, 1), np.uint8)
+
+
 class Context:
     """ds_ctx: one CUDA stream + workspaces on one device."""
 
@@ -371,12 +408,17 @@ class Context:
         return DevicePocket(self, pocket, table or InteractionTable.default())
 
     def dock(self, dpocket: DevicePocket, packed: PackedBatch, cfg: model.DockConfig, seed: int = 0,
-             family: int = FAMILY_BATCHED, coords: bool = True, detail: bool = False) -> DockOutput:
+             family: int = FAMILY_BATCHED, coords: bool = True, detail: bool = False,
+             buffers: Optional["OutputBuffers"] = None) -> DockOutput:
+        """ds_dock on host buffers.  `buffers` (e.g. pinned OutputBuffers) are reused if given."""
         n, N = packed.n, cfg.restarts_n
         na, nf = int(packed.atom_off[-1]) if n else 0, int(packed.frag_off[-1]) if n else 0
-        res = np.zeros(max(n, 1), dtype=RESULT_DTYPE)
-        bc = np.zeros((max(na, 1), 3), dtype=np.float32) if coords else None
-        bt = np.zeros(max(nf, 1), dtype=np.uint8)
+        if buffers is not None:
+            res, bc, bt = buffers.results, (buffers.best_coords if coords else None), buffers.best_torsion
+        else:
+            res = np.zeros(max(n, 1), dtype=RESULT_DTYPE)
+            bc = np.zeros((max(na, 1), 3), dtype=np.float32) if coords else None
+            bt = np.zeros(max(nf, 1), dtype=np.uint8)
         rr = np.zeros((max(n, 1), N), dtype=RESTART_DTYPE) if detail else None
         rt = np.zeros((max(nf, 1), N), dtype=np.uint8) if detail else None
         out = Outputs(_p(res), _p(bc), _p(bt), _p(rr), _p(rt))
