@@ -171,11 +171,13 @@ def main():
         run_reference(args, rank, world)
         return
     import torch
+    # one process per GPU; ranks beyond the visible device count share devices (plumbing tests only)
+    local = local % max(torch.cuda.device_count(), 1)
     dist = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl" if torch.cuda.device_count() >= world else "gloo")
     from paper_2209_05069_b200 import io, model, native
     from paper_2209_05069_b200.native import InteractionTable, ResidentBatch, pack
 
@@ -196,7 +198,8 @@ def main():
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

@@ -170,6 +170,10 @@ int ds_device_count(int *n);
 int ds_create(int device, ds_ctx **out);
 void ds_destroy(ds_ctx *ctx);
 int ds_ctx_alloc_count(const ds_ctx *ctx, int64_t *count);
+/* Allocate the worst-case workspace once ("allocate and deallocate that memory
+ * only once in the lifetime of the thread"): afterwards ds_dock on batches within these bounds
+ * (and the given restarts / alignment step) performs no device or pinned allocation. */
+int ds_ctx_reserve(ds_ctx *ctx, int max_ligands, int max_atoms, int max_frags, const ds_dock_config *cfg);
 /* Opaque cudaStream_t of the ctx (for external event timing). */
 void *ds_ctx_stream(ds_ctx *ctx);
 /* Pinned (page-locked) host memory.  Batch arrays and output buffers placed here are

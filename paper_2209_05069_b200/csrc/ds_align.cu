@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(1024, 1)
         for (int a = 0; a < n; ++a) {
           const float4 d = stage[a];
           const float3 v = align_v(Rp, d.x, d.y, d.z);
-          const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny) + g.K;  // u_y is shared by all ay
+          const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny);  // u_y is shared by all ay
           unit_atom<G, kConst, kSmemGrid>(v, t, yk, g, grid, strig, iy0, n_a, acc);
         }
       }
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(32)
       for (int a = c0; a < c1; ++a) {
         const float4 d = __ldg(bt.atoms + a0 + a);
         const float3 v = align_v(Rp, d.x, d.y, d.z);
-        const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny) + g.K;
+        const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny);
         unit_atom<G, kConst, false>(v, t, yk, g, pk.grid, strig, iy0, n_a, acc);
       }
       const int bias = 128 * (c1 - c0);

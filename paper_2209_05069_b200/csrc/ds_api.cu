@@ -255,7 +255,6 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
   v.g.nz = d->dims[2];
   v.g.NX = (unsigned)NX;
   v.g.NXY = (unsigned)(NX * NY);
-  v.g.K = (unsigned)(1 + NX + NX * NY) * (1u - (unsigned)kMagicBits);
   v.grid_bytes = gbytes;
   v.spacing = d->spacing;
   v.inv_s = (float)(1.0 / (double)d->spacing);  // P2
@@ -436,11 +435,8 @@ bool is_pinned(const void *p) {
 }
 
 
-int upload_batch(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
-  const int L = b->n_ligands;
-  const int NA = b->atom_off[L], NF = b->frag_off[L];
-  std::vector<int> oa, oo;
-  lpt_orders(b, oa, oo);
+// batch-sized device buffers (both families); grows geometrically, never shrinks
+int reserve_buffers(ds_ctx *c, int L, int NA, int NF, int N) {
   int rc;
   if ((rc = c->ensure(c->b_atom_off, sizeof(int) * (L + 1))) || (rc = c->ensure(c->b_atoms, 16ull * std::max(NA, 1))) ||
       (rc = c->ensure(c->b_frag_off, sizeof(int) * (L + 1))) || (rc = c->ensure(c->b_frags, 32ull * std::max(NF, 1))) ||
@@ -451,6 +447,16 @@ int upload_batch(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
       (rc = c->ensure(c->b_rtors, (size_t)std::max(NF, 1) * N)) || (rc = c->ensure(c->b_coords, 12ull * std::max(NA, 1))) ||
       (rc = c->ensure(c->b_btors, (size_t)std::max(NF, 1))) || (rc = c->ensure(c->b_queue, 256)))
     return rc;
+  return DS_OK;
+}
+
+int upload_batch(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
+  const int L = b->n_ligands;
+  const int NA = b->atom_off[L], NF = b->frag_off[L];
+  std::vector<int> oa, oo;
+  lpt_orders(b, oa, oo);
+  int rc;
+  if ((rc = reserve_buffers(c, L, NA, NF, N))) return rc;
   // One H2D per array.  Arrays already in pinned memory (ds_host_alloc) are DMA'd directly;
   // pageable ones are first copied into the ctx's pinned staging buffer.
   struct Arr {
@@ -640,6 +646,24 @@ int ds_dock(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const ds_doc
   cudaEventRecord(c->ev[4], c->stream);
   DS_CUDA(cudaStreamSynchronize(c->stream));
   fill_times(c, st, true);
+  return DS_OK;
+}
+
+int ds_ctx_reserve(ds_ctx *c, int max_ligands, int max_atoms, int max_frags, const ds_dock_config *cfg) {
+  if (!c || !cfg || max_ligands < 1 || max_atoms < 1 || max_frags < 0) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  if (cfg->restarts_n < 1 || cfg->restarts_n > DS_MAX_RESTARTS || cfg->alignment_step_deg < 1 ||
+      360 % cfg->alignment_step_deg)
+    return fail(DS_ERR_INVALID_ARG, "bad config");
+  DS_CUDA(cudaSetDevice(c->device));
+  const int N = cfg->restarts_n, na = 360 / cfg->alignment_step_deg;
+  const size_t L = (size_t)max_ligands;
+  int rc;
+  if ((rc = reserve_buffers(c, max_ligands, max_atoms, max_frags, DS_MAX_RESTARTS)) ||
+      (rc = c->ensure(c->b_lat_scores, 4 * L * N * na * na)) ||
+      (rc = c->ensure(c->b_lat_recs, latency_rec_bytes() * L * N)) || (rc = c->ensure(c->b_lat_done, 4 * L)) ||
+      (rc = c->ensure(c->b_scratch, sizeof(float4) * L * N * DS_MAX_ATOMS)) ||
+      (rc = c->ensure_host((size_t)max_atoms * 16 + (size_t)max_frags * 32 + L * 32 + 4096)))
+    return rc;
   return DS_OK;
 }
 

@@ -44,21 +44,22 @@ __device__ __forceinline__ float3 apply_mt(const float *M, const float *t, float
 }
 
 // ---- P4: nearest node (round half-even) + in-grid test, as an index into the PADDED grid.
-// The device grid carries a one-node halo holding kOutside, so the in-grid test becomes a clamp of
-// the magic-rounded bits to [kMagicBits - 1, kMagicBits + n] (two IMNMX per axis, no branch/select).
-// For |u| < 2^22 the magic add equals rintf; every |u| >= 2^22, inf or NaN clamps into the halo
-// (dims < 2^21), exactly like the oracle's float test 0 <= rint(u) <= n-1.
+// The device grid carries a one-node halo holding kOutside on every side, so the in-grid test is
+// one unsigned clamp per axis: c = min(bits(u + 1.5*2^23) - (kMagicBits - 1), n + 1) is rint(u) + 1
+// for in-range nodes and lands in a halo plane (0 or n + 1) otherwise — below-range values wrap
+// to huge unsigned and clamp to n + 1 (VIADDMNMX: one instruction).  For |u| < 2^22 the magic add
+// equals rintf; every |u| >= 2^22, inf or NaN lands in the halo (dims < 2^21), exactly like the
+// oracle's float test 0 <= rint(u) <= n-1.
 struct GridGeom {
   int nx, ny, nz;          // interior dims
   unsigned NX, NXY;        // padded row / plane pitch: nx+2, (nx+2)(ny+2)
-  unsigned K;              // (1 + NX + NXY) * (1 - kMagicBits) mod 2^32
 };
 __device__ __forceinline__ unsigned clamp_bits(float u, int n) {
-  const int b = __float_as_int(__fadd_rn(u, kMagic));
-  return (unsigned)min(max(b, kMagicBits - 1), kMagicBits + n);
+  const unsigned b = (unsigned)__float_as_int(__fadd_rn(u, kMagic)) - (unsigned)(kMagicBits - 1);
+  return min(b, (unsigned)(n + 1));
 }
 __device__ __forceinline__ int node_index(const GridGeom &g, float ux, float uy, float uz) {
-  return (int)(clamp_bits(ux, g.nx) + g.NX * clamp_bits(uy, g.ny) + g.NXY * clamp_bits(uz, g.nz) + g.K);
+  return (int)(clamp_bits(ux, g.nx) + g.NX * clamp_bits(uy, g.ny) + g.NXY * clamp_bits(uz, g.nz));
 }
 
 // ---- P5: starting pose parameters of restart r: R0s = (Rz(g) (x) (Ry(b) (x) Rx(a))) * inv_s,

@@ -31,8 +31,6 @@ struct OptWarpSmem {
   uint8_t clist[kMaxA];     // complement atom indices, ascending
   uint8_t cl[kMaxA][kCand]; // bump-candidate atom indices per moving atom
   uint8_t cn[kMaxA];        // candidate count, 255 = overflow (scan all of C')
-  int ascore[32];           // per-angle sums over M (current angle block)
-  unsigned abump;           // bumped-angle bits (current angle block)
   int geom[DS_MAX_RESTARTS];
   int valid[DS_MAX_RESTARTS];
   unsigned dis[DS_MAX_RESTARTS];   // dissimilarity bitsets (select_poses)
@@ -94,7 +92,8 @@ __device__ __forceinline__ long long rescore_pose(const OptWarpSmem &S, int A, c
         int b = __float_as_int(x.w);
         if (NB > 0) {
 #pragma unroll
-          for (int q = 0; q < NB; ++q) b += !(d2 < u[q]);
+          for (int q = 0; q < NB; ++q)  // b += !(d2 < u[q]) as one predicated add
+            asm("{\n\t.reg .pred p;\n\tsetp.geu.f32 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}" : "+r"(b) : "f"(d2), "f"(u[q]));
         } else {
           for (int q = 0; q < nb; ++q) b += !(d2 < u[q]);
         }
@@ -226,56 +225,72 @@ __global__ void __launch_bounds__(256, 4)
           S.cn[m] = (uint8_t)(cnt > kCand ? 255 : cnt);
         }
         unsigned best_key = 0;  // (score + 32768) << 16 | (65535 - angle); 0 = no clean angle
+        __syncwarp();
+        // ---- all angles at once: lane = (angle a, moving-atom group gi); the lane keeps its angle's
+        // rotation, bump flag and partial score in registers over moving atoms m = gi, gi+G, ...
         for (int k0 = 0; k0 < dp.n_t; k0 += 32) {
           const int nA = min(32, dp.n_t - k0);
-          if (lane < nA) S.ascore[lane] = 0;
-          if (lane == 0) S.abump = 0u;
-          __syncwarp();
-          const int nslot = nA * nM;
-          const int nMd = nM > 0 ? nM : 1;
-          int sa = lane / nMd, sm = lane - sa * nMd;    // slot = lane + 32 * round -> (angle, moving atom)
-          const int qa = 32 / nMd, qm = 32 - qa * nMd;
-          for (int s0 = 0; s0 < nslot; s0 += 32) {
-            const bool valid = s0 + lane < nslot;
-            // with early exit, angles bumped in an earlier round are retired; without, every pair runs
-            const bool pre = valid && !(dp.early_exit && ((S.abump >> sa) & 1u));
-            const unsigned act0 = __ballot_sync(kFull, pre);
-            if (act0) {
-              pairs_total += (unsigned)__popc(act0) * (unsigned)nC;  // pairs resolved (P14)
-              if (pre) {
-                const float3 q = torsion_pos(pk, dp.step_t, k0 + sa, kx, ky, kz, a3, S.u[S.mlist[sm]]);
-                float mind = __int_as_float(0x7f800000);  // min squared distance (P9: bump iff < bd2)
-                const int cnt = S.cn[sm];
-                if (cnt != 255) {
-                  for (int t = 0; t < cnt; ++t) {
-                    const float4 y = S.u[S.cl[sm][t]];
-                    mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
-                  }
-                } else {
-                  for (int c = 0; c < nC; ++c) {
-                    const float4 y = S.u[S.clist[c]];
-                    mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
-                  }
-                }
-                if (mind < dp.bd2) atomicOr(&S.abump, 1u << sa);
-                else atomicAdd(&S.ascore[sa], grid_val(pk, node_index(g, q.x, q.y, q.z)));
-              }
-            }
-            sa += qa;
-            sm += qm;
-            if (sm >= nM) {
-              sm -= nM;
-              ++sa;
-            }
-            __syncwarp();
+          const int G = 32 / nA;                  // moving-atom groups per round
+          const int a = lane % nA, gi = lane / nA;
+          const bool lane_ok = gi < G;
+          const int kang = k0 + a;
+          float R[9];
+          if (kang > 0) {
+            const float2 cs = pk.trig[kang * dp.step_t];
+            torsion_matrix(kx, ky, kz, cs.x, cs.y, R);
           }
+          bool bumped = false;
+          int part = 0;
+          for (int m0 = 0; m0 < nM; m0 += G) {
+            const int m = m0 + gi;
+            const bool valid = lane_ok && m < nM;
+            // with early exit a bumped angle is retired; without it every pair is checked
+            const bool act = valid && !(dp.early_exit && bumped);
+            const unsigned am = __ballot_sync(kFull, act);
+            if (!am) break;
+            pairs_total += (unsigned)__popc(am) * (unsigned)nC;  // pairs resolved (P14)
+            bool hit = false;
+            if (act) {
+              const float4 p = S.u[S.mlist[m]];
+              const float3 q = kang == 0 ? make_float3(p.x, p.y, p.z) : torsion_apply(R, a3, p.x, p.y, p.z);
+              float mind = __int_as_float(0x7f800000);  // min squared distance (P9: bump iff < bd2)
+              const int cnt = S.cn[m];
+              if (cnt != 255) {
+                for (int t = 0; t < cnt; ++t) {
+                  const float4 y = S.u[S.cl[m][t]];
+                  mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+                }
+              } else {
+                for (int c = 0; c < nC; ++c) {
+                  const float4 y = S.u[S.clist[c]];
+                  mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+                }
+              }
+              hit = mind < dp.bd2;
+              if (!hit) part += grid_val(pk, node_index(g, q.x, q.y, q.z));
+            }
+            // OR the hits of the G lanes that share an angle
+            unsigned hb = __ballot_sync(kFull, hit);
+            unsigned fold = 0;
+            for (int t = 0; t < G; ++t) fold |= hb >> (t * nA);
+            bumped = bumped || ((fold >> a) & 1u);
+          }
+          // combine the G partial scores of an angle on its group-0 lane
+          int sum = part;
+          for (int t = 1; t < G; ++t) {
+            const int v = __shfl_down_sync(kFull, part, t * nA);
+            if (gi == 0) sum += v;
+          }
+          unsigned hb = __ballot_sync(kFull, bumped && lane_ok);
+          unsigned fold = 0;
+          for (int t = 0; t < G; ++t) fold |= hb >> (t * nA);
+          fold &= nA == 32 ? 0xFFFFFFFFu : ((1u << nA) - 1u);
           unsigned kk = 0;
-          if (lane < nA && !((S.abump >> lane) & 1u))
-            kk = ((unsigned)(base + S.ascore[lane] + 32768) << 16) | (unsigned)(65535 - (k0 + lane));
+          if (gi == 0 && !((fold >> a) & 1u))
+            kk = ((unsigned)(base + sum + 32768) << 16) | (unsigned)(65535 - kang);
           evals += (unsigned)nA;
-          if (dp.early_exit) early_exits += (unsigned)__popc(S.abump);
+          if (dp.early_exit) early_exits += (unsigned)__popc(fold);
           best_key = max(best_key, __reduce_max_sync(kFull, kk));
-          __syncwarp();
         }
         const int best_k = best_key ? 65535 - (int)(best_key & 0xFFFFu) : -1;
         // commit the winner before the next fragment

@@ -30,20 +30,17 @@ def thread_context(device: int = 0) -> Context:
 
 
 class PocketCache:
-    """Device copies of a pocket, one per context (read-only, shared by a context's calls)."""
-
-    def __init__(self):
-        self._lock = threading.Lock()
-        self._map: Dict[tuple, DevicePocket] = {}
+    """Device copies of a pocket, cached on the context that owns them (read-only, shared by all
+    of that context's calls); they are released with the context."""
 
     def get(self, ctx: Context, pocket: model.Pocket, table: Optional[InteractionTable]) -> DevicePocket:
-        key = (id(ctx), id(pocket), id(table))
-        with self._lock:
-            dp = self._map.get(key)
-            if dp is None or dp.pocket is not pocket:
-                dp = ctx.pocket(pocket, table)
-                self._map[key] = dp
-            return dp
+        cache = ctx.__dict__.setdefault("_pocket_cache", {})
+        key = (id(pocket), id(table))
+        hit = cache.get(key)
+        if hit is None or hit[0] is not pocket or hit[1] is not table:
+            hit = (pocket, table, ctx.pocket(pocket, table))
+            cache[key] = hit
+        return hit[2]
 
 
 _pockets = PocketCache()

@@ -71,12 +71,16 @@ class latency_engine:  # noqa: N801  (module-like namespace mirroring `dockscree
         nxt = [0]
         dev_ms = [0.0]
         allocs = []
+        workspaces = [0]
         t0 = time.perf_counter()
 
         def worker(wid: int):
             dev = devices[wid % len(devices)]
             ctx = thread_context(dev)
             dp = _pockets.get(ctx, pocket, table)
+            ctx.reserve(cfg)            # the worker's worst-case workspace, allocated once
+            with lock:
+                workspaces[0] += 1
             a0 = ctx.alloc_count()
             while True:
                 with lock:
@@ -104,7 +108,8 @@ class latency_engine:  # noqa: N801  (module-like namespace mirroring `dockscree
         for t in th:
             t.join()
         rep = _finish(n, slots, errors, model.Counters(), t0, dev_ms[0])
-        rep.extra_allocations = sum(allocs)
+        rep.workspace_allocations = workspaces[0]     # == workers
+        rep.extra_allocations = sum(allocs)           # allocations after the reserve: 0
         return rep
 
 

@@ -107,6 +107,7 @@ def lib():
             "ds_destroy": (None, [vp]), "ds_ctx_alloc_count": (C.c_int, [vp, vp]),
             "ds_ctx_stream": (vp, [vp]), "ds_synchronize": (C.c_int, [vp]),
             "ds_host_alloc": (vp, [C.c_size_t]), "ds_host_free": (None, [vp]),
+            "ds_ctx_reserve": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp]),
             "ds_pocket_create": (C.c_int, [vp, vp, vp]), "ds_pocket_destroy": (None, [vp]),
             "ds_dock": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, vp]),
             "ds_batch_upload": (C.c_int, [vp, vp, vp]),
@@ -398,6 +399,12 @@ class Context:
         check(lib().ds_create(int(device), C.byref(h)))
         self.handle = h
         self.device = device
+
+    def reserve(self, cfg: model.DockConfig, max_ligands: int = 1, max_atoms: int = model.MAX_ATOMS,
+                max_frags: int = model.MAX_ATOMS - 2):
+        """Allocate the worst-case workspace once: one ligand of 160 atoms by default."""
+        check(lib().ds_ctx_reserve(self.handle, int(max_ligands), int(max_atoms), int(max_frags),
+                                   C.byref(config_c(cfg))))
 
     def alloc_count(self) -> int:
         n = C.c_int64(0)
