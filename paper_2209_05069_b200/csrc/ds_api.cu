@@ -67,6 +67,8 @@ struct ds_ctx {
   int sm_count = 0;
   size_t smem_optin = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy = nullptr;      // H2D/D2H of the chunked ds_dock pipeline
+  std::vector<cudaEvent_t> pev;     // pipeline events (4 per chunk)
   cudaEvent_t ev[6] = {};
   int64_t allocs = 0;
   float2 *trig = nullptr;       // 360 (cos, sin)
@@ -149,7 +151,8 @@ int ds_create(int device, ds_ctx **out) {
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
   c->smem_optin = prop.sharedMemPerBlockOptin;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return fail(DS_ERR_CUDA, "cudaStreamCreate failed");
   }
@@ -183,6 +186,9 @@ void ds_destroy(ds_ctx *c) {
   if (c->h_stage) cudaFreeHost(c->h_stage);
   for (auto &e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto &e : c->pev)
+    if (e) cudaEventDestroy(e);
+  if (c->copy) cudaStreamDestroy(c->copy);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -400,22 +406,21 @@ int check_batch(const ds_batch_desc *b) {
 }
 
 // LPT orders: alignment work ~ A (counting sort, descending); optimisation work ~ F*(A^2)/4 + A
-void lpt_orders(const ds_batch_desc *b, std::vector<int> &oa, std::vector<int> &oo) {
-  const int L = b->n_ligands;
-  oa.resize(L);
-  oo.resize(L);
+// LPT orders of ligands [L0, L1) as indices relative to L0, written to oa/oo (L1-L0 entries each)
+void lpt_orders_range(const ds_batch_desc *b, int L0, int L1, int *oa, int *oo) {
+  const int L = L1 - L0;
   // counting sorts, descending cost: alignment ~ A, optimisation ~ (F + 2) * A (torsion slots
   // plus restart rebuild/rescore), both O(L)
-  auto csort = [&](std::vector<int> &out, int nkeys, auto key) {
+  auto csort = [&](int *out, int nkeys, auto key) {
     std::vector<int> cnt(nkeys + 1, 0);
-    for (int i = 0; i < L; ++i) cnt[nkeys - 1 - key(i)]++;
+    for (int i = 0; i < L; ++i) cnt[nkeys - 1 - key(L0 + i)]++;
     int run = 0;
     for (int k = 0; k < nkeys; ++k) {
       const int t = cnt[k];
       cnt[k] = run;
       run += t;
     }
-    for (int i = 0; i < L; ++i) out[cnt[nkeys - 1 - key(i)]++] = i;
+    for (int i = 0; i < L; ++i) out[cnt[nkeys - 1 - key(L0 + i)]++] = i;
   };
   csort(oa, DS_MAX_ATOMS + 1, [&](int i) { return b->atom_off[i + 1] - b->atom_off[i]; });
   const int kmax = 4096;
@@ -423,6 +428,12 @@ void lpt_orders(const ds_batch_desc *b, std::vector<int> &oa, std::vector<int> &
     const int A = b->atom_off[i + 1] - b->atom_off[i], F = b->frag_off[i + 1] - b->frag_off[i];
     return std::min(kmax - 1, ((F + 2) * A) >> 3);
   });
+}
+
+void lpt_orders(const ds_batch_desc *b, std::vector<int> &oa, std::vector<int> &oo) {
+  oa.resize(b->n_ligands);
+  oo.resize(b->n_ligands);
+  lpt_orders_range(b, 0, b->n_ligands, oa.data(), oo.data());
 }
 
 bool is_pinned(const void *p) {
@@ -491,17 +502,30 @@ int upload_batch(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
   return DS_OK;
 }
 
+int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, const DockParams &dp, bool want_coords,
+                      bool want_btors, bool want_rrec, ds_stats *st, cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2,
+                      int *queue);
+
 int run_batched(ds_ctx *c, const ds_pocket *pk, int L, int NA, int NF, const DockParams &dp, bool want_coords,
                 bool want_btors, bool want_rrec, ds_stats *st) {
-  BatchView bt;
-  bt.L = L;
-  bt.atom_off = (const int *)c->b_atom_off.p;
-  bt.atoms = (const float4 *)c->b_atoms.p;
-  bt.frag_off = (const int *)c->b_frag_off.p;
-  bt.frags = (const uint4 *)c->b_frags.p;
-  bt.idh = (const uint64_t *)c->b_idh.p;
   int *queue = (int *)c->b_queue.p;
   DS_CUDA(cudaMemsetAsync(queue, 0, 256, c->stream));
+  return run_batched_range(c, pk, 0, L, dp, want_coords, want_btors, want_rrec, st, c->ev[1], c->ev[2], c->ev[3],
+                           queue);
+}
+
+// Batched family on ligands [L0, L1) of the resident batch (absolute atom/fragment offsets; the
+// per-ligand outputs and the order arrays are offset by L0).
+int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, const DockParams &dp, bool want_coords,
+                      bool want_btors, bool want_rrec, ds_stats *st, cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2,
+                      int *queue) {
+  BatchView bt;
+  bt.L = L1 - L0;
+  bt.atom_off = (const int *)c->b_atom_off.p + L0;
+  bt.atoms = (const float4 *)c->b_atoms.p;
+  bt.frag_off = (const int *)c->b_frag_off.p + L0;
+  bt.frags = (const uint4 *)c->b_frags.p;
+  bt.idh = (const uint64_t *)c->b_idh.p + L0;
   // --- alignment: one CTA per SM, grid staged into smem when it fits ---
   const size_t per_warp = (size_t)align_warp_smem_bytes_host(dp.N);
   const size_t fixed = (size_t)dp.n_a * 16;
@@ -510,11 +534,11 @@ int run_batched(ds_ctx *c, const ds_pocket *pk, int L, int NA, int NF, const Doc
   int in_smem = gb + fixed + per_warp * 8 <= c->smem_optin;
   if (in_smem) warps_a = (int)std::min<size_t>(32, (c->smem_optin - gb - fixed) / per_warp);
   const size_t smem_a = (in_smem ? gb : 0) + fixed + per_warp * warps_a;
-  AlignOut ao{(uint32_t *)c->b_keys.p};
-  cudaEventRecord(c->ev[1], c->stream);
-  launch_align_batched(pk->view, bt, dp, (const int *)c->b_order_a.p, ao, queue, in_smem, c->sm_count, warps_a, smem_a,
-                       c->stream);
-  cudaEventRecord(c->ev[2], c->stream);
+  AlignOut ao{(uint32_t *)c->b_keys.p + (size_t)L0 * dp.N};
+  cudaEventRecord(e0, c->stream);
+  launch_align_batched(pk->view, bt, dp, (const int *)c->b_order_a.p + L0, ao, queue, in_smem, c->sm_count, warps_a,
+                       smem_a, c->stream);
+  cudaEventRecord(e1, c->stream);
   // --- optimisation + select + rescore: warp per ligand, persistent, occupancy-sized ---
   const int warps_o = 8;
   const size_t smem_o = optimize_cta_smem_bytes(pk->view.n_atoms, pk->view.nb) + optimize_warp_smem_bytes() * warps_o;
@@ -523,15 +547,15 @@ int run_batched(ds_ctx *c, const ds_pocket *pk, int L, int NA, int NF, const Doc
   int rc;
   if ((rc = c->ensure(c->b_scratch, sizeof(float4) * (size_t)blocks_o * warps_o * dp.N * DS_MAX_ATOMS))) return rc;
   OptOut oo;
-  oo.res = (ds_result *)c->b_res.p;
-  oo.rrec = want_rrec ? (ds_restart_record *)c->b_rrec.p : nullptr;
+  oo.res = (ds_result *)c->b_res.p + L0;
+  oo.rrec = want_rrec ? (ds_restart_record *)c->b_rrec.p + (size_t)L0 * dp.N : nullptr;
   oo.rtors = (uint8_t *)c->b_rtors.p;
   oo.final_u = (float4 *)c->b_scratch.p;
   oo.best_coords = want_coords ? (float *)c->b_coords.p : nullptr;
   oo.best_tors = want_btors ? (uint8_t *)c->b_btors.p : nullptr;
-  launch_optimize_batched(pk->view, bt, dp, (const int *)c->b_order_o.p, (const uint32_t *)c->b_keys.p, oo, queue + 16,
-                          blocks_o, warps_o, smem_o, c->stream);
-  cudaEventRecord(c->ev[3], c->stream);
+  launch_optimize_batched(pk->view, bt, dp, (const int *)c->b_order_o.p + L0, ao.keys, oo, queue + 16, blocks_o,
+                          warps_o, smem_o, c->stream);
+  cudaEventRecord(e2, c->stream);
   if (st) st->launches += 2;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(DS_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
@@ -619,6 +643,122 @@ void fill_times(ds_ctx *c, ds_stats *st, bool with_copies) {
   st->total_ms = t;
 }
 
+// Large batched calls: the batch is split into nch contiguous chunks; chunk k's H2D on the copy
+// stream overlaps chunk k-1's kernels, and chunk k's D2H overlaps chunk k+1's kernels.
+int dock_pipelined(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const DockParams &dp,
+                   const ds_outputs *out, ds_stats *st, int nch) {
+  const int L = b->n_ligands, N = dp.N;
+  const int NA = b->atom_off[L], NF = b->frag_off[L];
+  int rc;
+  if ((rc = reserve_buffers(c, L, NA, NF, N)) || (rc = c->ensure(c->b_queue, 256ull * nch))) return rc;
+  while ((int)c->pev.size() < 4 * nch) {
+    cudaEvent_t e;
+    DS_CUDA(cudaEventCreate(&e));
+    c->pev.push_back(e);
+  }
+  std::vector<int> bounds(nch + 1);
+  for (int k = 0; k <= nch; ++k) bounds[k] = (int)((int64_t)L * k / nch);
+  // host side: LPT orders per chunk; pageable inputs go through the pinned staging buffer
+  struct Src {
+    const void *p;
+    size_t bytes;
+  } src[5] = {{b->atom_off, 4ull * (L + 1)}, {b->frag_off, 4ull * (L + 1)}, {b->id_hash, 8ull * L},
+              {b->atom_xyzt, 16ull * NA}, {b->frag_desc, 32ull * NF}};
+  size_t off[7], o = 0;
+  bool pinned[5];
+  for (int k = 0; k < 5; ++k) {
+    pinned[k] = src[k].bytes >= (1u << 16) && is_pinned(src[k].p);
+    off[k] = o;
+    if (!pinned[k]) o += (src[k].bytes + 255) & ~(size_t)255;
+  }
+  off[5] = o;
+  o += (4ull * L + 255) & ~(size_t)255;
+  off[6] = o;
+  o += (4ull * L + 255) & ~(size_t)255;
+  if ((rc = c->ensure_host(o))) return rc;
+  char *h = (char *)c->h_stage;
+  const char *hp[5];
+  for (int k = 0; k < 5; ++k) {
+    hp[k] = (const char *)src[k].p;
+    if (!pinned[k] && src[k].bytes) {
+      memcpy(h + off[k], src[k].p, src[k].bytes);
+      hp[k] = h + off[k];
+    }
+  }
+  int *oa = (int *)(h + off[5]), *oo = (int *)(h + off[6]);
+  for (int k = 0; k < nch; ++k) lpt_orders_range(b, bounds[k], bounds[k + 1], oa + bounds[k], oo + bounds[k]);
+  cudaStream_t cs = c->copy;
+  cudaEventRecord(c->ev[0], cs);
+  DS_CUDA(cudaMemcpyAsync(c->b_atom_off.p, hp[0], src[0].bytes, cudaMemcpyHostToDevice, cs));
+  DS_CUDA(cudaMemcpyAsync(c->b_frag_off.p, hp[1], src[1].bytes, cudaMemcpyHostToDevice, cs));
+  DS_CUDA(cudaMemcpyAsync(c->b_idh.p, hp[2], src[2].bytes, cudaMemcpyHostToDevice, cs));
+  for (int k = 0; k < nch; ++k) {
+    const int L0 = bounds[k], L1 = bounds[k + 1];
+    const size_t a0 = b->atom_off[L0], a1 = b->atom_off[L1], f0 = b->frag_off[L0], f1 = b->frag_off[L1];
+    DS_CUDA(cudaMemcpyAsync((float4 *)c->b_atoms.p + a0, hp[3] + 16 * a0, 16 * (a1 - a0), cudaMemcpyHostToDevice, cs));
+    if (f1 > f0)
+      DS_CUDA(cudaMemcpyAsync((char *)c->b_frags.p + 32 * f0, hp[4] + 32 * f0, 32 * (f1 - f0), cudaMemcpyHostToDevice, cs));
+    DS_CUDA(cudaMemcpyAsync((int *)c->b_order_a.p + L0, oa + L0, 4ull * (L1 - L0), cudaMemcpyHostToDevice, cs));
+    DS_CUDA(cudaMemcpyAsync((int *)c->b_order_o.p + L0, oo + L0, 4ull * (L1 - L0), cudaMemcpyHostToDevice, cs));
+    cudaEventRecord(c->pev[4 * k], cs);
+  }
+  if (st) st->h2d_bytes += (int64_t)(src[0].bytes + src[1].bytes + src[2].bytes + src[3].bytes + src[4].bytes + 8ull * L);
+  int *queue = (int *)c->b_queue.p;
+  DS_CUDA(cudaMemsetAsync(queue, 0, 256ull * nch, c->stream));
+  for (int k = 0; k < nch; ++k) {
+    const int L0 = bounds[k], L1 = bounds[k + 1];
+    DS_CUDA(cudaStreamWaitEvent(c->stream, c->pev[4 * k], 0));
+    if ((rc = run_batched_range(c, pk, L0, L1, dp, out->best_coords != nullptr, out->best_torsion != nullptr,
+                                out->restarts != nullptr, st, c->pev[4 * k + 1], c->pev[4 * k + 2], c->pev[4 * k + 3],
+                                queue + 64 * k)))
+      return rc;
+    DS_CUDA(cudaStreamWaitEvent(cs, c->pev[4 * k + 3], 0));
+    const size_t a0 = b->atom_off[L0], a1 = b->atom_off[L1], f0 = b->frag_off[L0], f1 = b->frag_off[L1];
+    DS_CUDA(cudaMemcpyAsync(out->results + L0, (ds_result *)c->b_res.p + L0, sizeof(ds_result) * (L1 - L0),
+                            cudaMemcpyDeviceToHost, cs));
+    if (out->best_coords && a1 > a0)
+      DS_CUDA(cudaMemcpyAsync(out->best_coords + 3 * a0, (float *)c->b_coords.p + 3 * a0, 12 * (a1 - a0),
+                              cudaMemcpyDeviceToHost, cs));
+    if (out->best_torsion && f1 > f0)
+      DS_CUDA(cudaMemcpyAsync(out->best_torsion + f0, (uint8_t *)c->b_btors.p + f0, f1 - f0, cudaMemcpyDeviceToHost, cs));
+    if (out->restarts)
+      DS_CUDA(cudaMemcpyAsync(out->restarts + (size_t)L0 * N, (ds_restart_record *)c->b_rrec.p + (size_t)L0 * N,
+                              sizeof(ds_restart_record) * (size_t)(L1 - L0) * N, cudaMemcpyDeviceToHost, cs));
+    if (out->restart_torsion && f1 > f0)
+      DS_CUDA(cudaMemcpyAsync(out->restart_torsion + f0 * N, (uint8_t *)c->b_rtors.p + f0 * N, (f1 - f0) * N,
+                              cudaMemcpyDeviceToHost, cs));
+    if (st)
+      st->d2h_bytes += (int64_t)(sizeof(ds_result) * (L1 - L0) + (out->best_coords ? 12 * (a1 - a0) : 0) +
+                                 (out->best_torsion ? f1 - f0 : 0) +
+                                 (out->restarts ? sizeof(ds_restart_record) * (size_t)(L1 - L0) * N : 0) +
+                                 (out->restart_torsion ? (f1 - f0) * N : 0));
+  }
+  cudaEventRecord(c->ev[4], cs);
+  DS_CUDA(cudaStreamSynchronize(cs));
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  if (st) {
+    float t = 0.f;
+    st->align_ms = st->optimize_ms = 0.f;
+    for (int k = 0; k < nch; ++k) {
+      cudaEventElapsedTime(&t, c->pev[4 * k + 1], c->pev[4 * k + 2]);
+      st->align_ms += t;
+      cudaEventElapsedTime(&t, c->pev[4 * k + 2], c->pev[4 * k + 3]);
+      st->optimize_ms += t;
+    }
+    cudaEventElapsedTime(&t, c->ev[0], c->ev[4]);
+    st->total_ms = t;
+  }
+  return DS_OK;
+}
+
+int pipeline_chunks(int L) {
+  const char *e = getenv("DS_PIPELINE_CHUNKS");
+  int n = e ? atoi(e) : 2;
+  if (n < 1) n = 1;
+  if (L < 20000) return 1;
+  return std::min(n, L / 5000);
+}
+
 }  // namespace
 
 extern "C" {
@@ -634,6 +774,10 @@ int ds_dock(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const ds_doc
   const int L = b->n_ligands;
   if (L == 0) return DS_OK;
   DS_CUDA(cudaSetDevice(c->device));
+  if (family == DS_FAMILY_BATCHED) {
+    const int nch = pipeline_chunks(L);
+    if (nch > 1) return dock_pipelined(c, pk, b, dp, out, st, nch);
+  }
   cudaEventRecord(c->ev[0], c->stream);
   if ((rc = upload_batch(c, b, dp.N, st))) return rc;
   const int NA = b->atom_off[L], NF = b->frag_off[L];

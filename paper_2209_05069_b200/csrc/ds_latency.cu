@@ -42,7 +42,11 @@ struct LatSmem {
   int heavy;
 };
 
-__device__ __forceinline__ int lat_grid_val(const PocketView &pk, int idx) { return (int)__ldg(pk.grid + idx) - 128; }
+// grid lookup: the CTA's shared-memory copy when the pocket fits, else the L2-resident global copy
+template <bool kSmemGrid>
+__device__ __forceinline__ int lat_grid_val(const uint8_t *grid, int idx) {
+  return (kSmemGrid ? (int)grid[idx] : (int)__ldg(grid + idx)) - 128;
+}
 
 __device__ __forceinline__ float2 lat_cyl(float4 p, float3 a, float kx, float ky, float kz) {
   const float wx = p.x - a.x, wy = p.y - a.y, wz = p.z - a.z;
@@ -50,24 +54,39 @@ __device__ __forceinline__ float2 lat_cyl(float4 p, float3 a, float kx, float ky
   return make_float2(h, sqrtf(fmaxf(wx * wx + wy * wy + wz * wz - h * h, 0.f)));
 }
 
-__device__ __forceinline__ float3 lat_torsion_pos(const PocketView &pk, int step_t, int k, float kx, float ky, float kz,
+__device__ __forceinline__ float3 lat_torsion_pos(const float2 *trig, int step_t, int k, float kx, float ky, float kz,
                                                   float3 a, float4 p) {
   if (k == 0) return make_float3(p.x, p.y, p.z);
-  const float2 cs = pk.trig[k * step_t];
+  const float2 cs = trig[k * step_t];
   float R[9];
   torsion_matrix(kx, ky, kz, cs.x, cs.y, R);
   return torsion_apply(R, a, p.x, p.y, p.z);
 }
 
+template <bool kSmemGrid>
 __global__ void __launch_bounds__(kLatThreads)
     k_optimize_latency(PocketView pk, BatchView bt, DockParams dp, const int *scores, OptOut out, LatRec *recs,
                        int *done) {
   __shared__ LatSmem S;
+  extern __shared__ __align__(16) unsigned char dsm[];  // [trig 360][fragment records][grid]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lig = blockIdx.x / dp.N, r = blockIdx.x - lig * dp.N;
   const int a0 = bt.atom_off[lig], A = bt.atom_off[lig + 1] - a0;
   const int f0 = bt.frag_off[lig], F = bt.frag_off[lig + 1] - f0;
   const GridGeom g = pk.g;
+  // stage the trig table, this ligand's fragment records and (if it fits) the pocket grid: every
+  // later lookup is a shared-memory access instead of an L2 round trip on the fragment chain
+  float2 *strig = reinterpret_cast<float2 *>(dsm);
+  uint4 *sfrag = reinterpret_cast<uint4 *>(dsm + 360 * sizeof(float2));
+  const uint8_t *grid = pk.grid;
+  for (int i = tid; i < 360; i += kLatThreads) strig[i] = pk.trig[i];
+  for (int i = tid; i < 2 * F; i += kLatThreads) sfrag[i] = __ldg(bt.frags + 2 * (size_t)f0 + i);
+  if (kSmemGrid) {
+    int4 *dst = reinterpret_cast<int4 *>(dsm + 360 * sizeof(float2) + 2 * (DS_MAX_ATOMS - 2) * sizeof(uint4));
+    const int4 *src = reinterpret_cast<const int4 *>(pk.grid);
+    for (int i = tid; i < pk.grid_bytes / 16; i += kLatThreads) dst[i] = __ldg(src + i);
+    grid = reinterpret_cast<const uint8_t *>(dst);
+  }
   if (tid == 0) {
     S.key = 0u;
     S.pairs = 0u;
@@ -91,9 +110,9 @@ __global__ void __launch_bounds__(kLatThreads)
   const int ix = rot / dp.n_a, iy = rot - ix * dp.n_a;
   {
     float R0s[9], T[3], Rp[9];
-    start_params(bt.idh[lig], dp.seed, r, pk.trig, pk.inv_s, g.nx, g.ny, g.nz, R0s, T);
-    align_rx(pk.trig[ix * dp.step_a], R0s, Rp);
-    const float2 cy = pk.trig[iy * dp.step_a];
+    start_params(bt.idh[lig], dp.seed, r, strig, pk.inv_s, g.nx, g.ny, g.nz, R0s, T);
+    align_rx(strig[ix * dp.step_a], R0s, Rp);
+    const float2 cy = strig[iy * dp.step_a];
     for (int i = tid; i < A; i += kLatThreads) {
       const float4 d = __ldg(bt.atoms + a0 + i);
       const float3 u = align_u(align_v(Rp, d.x, d.y, d.z), cy.x, cy.y, T);
@@ -106,8 +125,8 @@ __global__ void __launch_bounds__(kLatThreads)
   for (int f = 0; f < F; ++f) {
     // ---- compaction of M and C' (warp 0, ascending order), axis (thread 0) ----
     if (warp == 0) {
-      const uint4 fa = __ldg(bt.frags + 2 * (size_t)(f0 + f));
-      const uint4 fb = __ldg(bt.frags + 2 * (size_t)(f0 + f) + 1);
+      const uint4 fa = sfrag[2 * f];
+      const uint4 fb = sfrag[2 * f + 1];
       const unsigned mw[5] = {fa.x, fa.y, fa.z, fa.w, fb.x};
       const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
       const unsigned lt = lanemask_lt();
@@ -124,7 +143,7 @@ __global__ void __launch_bounds__(kLatThreads)
         if (in && !mv) {
           const float4 p = S.u[i];
           if (cp) S.cmp[nC + __popc(bc & lt)] = p;
-          base += lat_grid_val(pk, node_index(g, p.x, p.y, p.z));
+          base += lat_grid_val<kSmemGrid>(grid, node_index(g, p.x, p.y, p.z));
         }
         nM += __popc(bm);
         nC += __popc(bc);
@@ -151,7 +170,7 @@ __global__ void __launch_bounds__(kLatThreads)
     __syncthreads();
     if (S.degen) break;
     const int nM = S.nM, nC = S.nC;
-    const uint4 fb = __ldg(bt.frags + 2 * (size_t)(f0 + f) + 1);
+    const uint4 fb = sfrag[2 * f + 1];
     const float4 pa = S.u[fb.y & 0xFFu];
     const float3 a3 = make_float3(pa.x, pa.y, pa.z);
     const float kx = S.kx, ky = S.ky, kz = S.kz;
@@ -184,7 +203,7 @@ __global__ void __launch_bounds__(kLatThreads)
       for (int s = tid; s < nA * nM; s += kLatThreads) {
         const int a = s / nM, m = s - a * nM;
         if (dp.early_exit && ((*(volatile unsigned *)&S.abump >> a) & 1u)) continue;
-        const float3 q = lat_torsion_pos(pk, dp.step_t, k0 + a, kx, ky, kz, a3, S.u[S.mlist[m]]);
+        const float3 q = lat_torsion_pos(strig, dp.step_t, k0 + a, kx, ky, kz, a3, S.u[S.mlist[m]]);
         float mind = __int_as_float(0x7f800000);
         my_pairs += (unsigned)nC;  // pairs resolved (P14)
         const int cnt = S.cn[m];
@@ -203,7 +222,7 @@ __global__ void __launch_bounds__(kLatThreads)
           }
         }
         if (mind < dp.bd2) atomicOr(&S.abump, 1u << a);
-        else atomicAdd(&S.ascore[a], lat_grid_val(pk, node_index(g, q.x, q.y, q.z)));
+        else atomicAdd(&S.ascore[a], lat_grid_val<kSmemGrid>(grid, node_index(g, q.x, q.y, q.z)));
       }
       my_pairs = __reduce_add_sync(kFull, my_pairs);
       if (lane == 0) atomicAdd(&S.pairs, my_pairs);
@@ -229,7 +248,7 @@ __global__ void __launch_bounds__(kLatThreads)
       for (int m = tid; m < nM; m += kLatThreads) {
         const int i = S.mlist[m];
         const float4 p = S.u[i];
-        const float3 q = lat_torsion_pos(pk, dp.step_t, best_k, kx, ky, kz, a3, p);
+        const float3 q = lat_torsion_pos(strig, dp.step_t, best_k, kx, ky, kz, a3, p);
         S.u[i] = make_float4(q.x, q.y, q.z, p.w);
       }
     if (best_k < 0) ++all_bumped;
@@ -242,7 +261,7 @@ __global__ void __launch_bounds__(kLatThreads)
     int sc = 0, hv = 0;
     for (int i = tid; i < A; i += kLatThreads) {
       const float4 p = S.u[i];
-      sc += lat_grid_val(pk, node_index(g, p.x, p.y, p.z));
+      sc += lat_grid_val<kSmemGrid>(grid, node_index(g, p.x, p.y, p.z));
       hv += p.w != 0.f;
       scr[i] = p;
     }
@@ -429,7 +448,18 @@ size_t latency_rec_bytes() { return sizeof(LatRec); }
 
 void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *scores,
                              OptOut out, void *recs, int *done, cudaStream_t st) {
-  k_optimize_latency<<<bt.L * dp.N, kLatThreads, 0, st>>>(pk, bt, dp, scores, out, (LatRec *)recs, done);
+  const size_t base = 360 * sizeof(float2) + 2 * (DS_MAX_ATOMS - 2) * sizeof(uint4);
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t with_grid = base + (size_t)pk.grid_bytes;
+  if (with_grid + sizeof(LatSmem) + 1024 <= (size_t)optin) {
+    cudaFuncSetAttribute(k_optimize_latency<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)with_grid);
+    k_optimize_latency<true><<<bt.L * dp.N, kLatThreads, with_grid, st>>>(pk, bt, dp, scores, out, (LatRec *)recs, done);
+  } else {
+    cudaFuncSetAttribute(k_optimize_latency<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)base);
+    k_optimize_latency<false><<<bt.L * dp.N, kLatThreads, base, st>>>(pk, bt, dp, scores, out, (LatRec *)recs, done);
+  }
 }
 
 }  // namespace ds

@@ -23,6 +23,7 @@ namespace ds {
 
 constexpr int kMaxA = DS_MAX_ATOMS;
 constexpr int kCand = 6;             // bump-candidate slots per moving atom (overflow: full scan)
+constexpr int kOptWarps = 8;         // warps per CTA (one ligand each)
 
 struct OptWarpSmem {
   float4 u[kMaxA];          // committed pose of the current restart (grid frame), .w = type
@@ -30,7 +31,7 @@ struct OptWarpSmem {
   uint8_t mlist[kMaxA];     // moving atom indices, ascending
   uint8_t clist[kMaxA];     // complement atom indices, ascending
   uint8_t cl[kMaxA][kCand]; // bump-candidate atom indices per moving atom
-  uint8_t cn[kMaxA];        // candidate count, 255 = overflow (scan all of C')
+  unsigned cnw[kMaxA / 4];  // candidate counts, one byte per moving atom (> kCand: scan all of C')
   int geom[DS_MAX_RESTARTS];
   int valid[DS_MAX_RESTARTS];
   unsigned dis[DS_MAX_RESTARTS];   // dissimilarity bitsets (select_poses)
@@ -91,9 +92,12 @@ __device__ __forceinline__ long long rescore_pose(const OptWarpSmem &S, int A, c
         const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
         int b = __float_as_int(x.w);
         if (NB > 0) {
+          // bin = #{q : !(d2 < u_q)}; d2 >= +0 and u_q > 0, so float order == bit order and
+          // (bits(d2) - bits(u_q)) >> 31 is -1 exactly when d2 < u_q (NaN/inf count as beyond)
+          const int d2b = __float_as_int(d2);
+          b += NB;
 #pragma unroll
-          for (int q = 0; q < NB; ++q)  // b += !(d2 < u[q]) as one predicated add
-            asm("{\n\t.reg .pred p;\n\tsetp.geu.f32 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}" : "+r"(b) : "f"(d2), "f"(u[q]));
+          for (int q = 0; q < NB; ++q) b += (d2b - __float_as_int(u[q])) >> 31;
         } else {
           for (int q = 0; q < nb; ++q) b += !(d2 < u[q]);
         }
@@ -105,7 +109,46 @@ __device__ __forceinline__ long long rescore_pose(const OptWarpSmem &S, int A, c
   return acc;
 }
 
-__global__ void __launch_bounds__(256, 4)
+// cold paths kept out of line so the hot loops stay compact in the instruction cache
+__device__ __noinline__ long long rescore_pose_generic(const OptWarpSmem &S, int A, const float4 *pat, int P,
+                                                       const int32_t *wfx, int nb, const float *ub2) {
+  return rescore_pose<0>(S, A, pat, P, wfx, nb, ub2);
+}
+
+// select_poses (P12) dissimilarity bitsets: pairs (p < q) of valid poses over lanes; heavy-atom sum
+// of squared deltas in f64, in atom order (same order as the oracle)
+__device__ __noinline__ void pose_dissimilarity(OptWarpSmem &S, const float4 *scr, int A, int N, int heavy,
+                                                double thr2) {
+  const int npairs = N * (N - 1) / 2;
+  for (int pidx = threadIdx.x & 31; pidx < npairs; pidx += 32) {
+    int p = 0, rem = pidx;
+    while (rem >= N - 1 - p) {
+      rem -= N - 1 - p;
+      ++p;
+    }
+    const int q = p + 1 + rem;
+    if (!S.valid[p] || !S.valid[q]) continue;
+    double sum = 0.0;
+    const float4 *up = scr + (size_t)p * kMaxA, *uq = scr + (size_t)q * kMaxA;
+    for (int i = 0; i < A; ++i) {
+      const float4 x = up[i], y = uq[i];
+      if (x.w == 0.f) continue;
+      const double dx = __dsub_rn((double)x.x, (double)y.x);
+      const double dy = __dsub_rn((double)x.y, (double)y.y);
+      const double dz = __dsub_rn((double)x.z, (double)y.z);
+      double t = __dmul_rn(dx, dx);
+      t = __dadd_rn(t, __dmul_rn(dy, dy));
+      t = __dadd_rn(t, __dmul_rn(dz, dz));
+      sum = __dadd_rn(sum, t);
+    }
+    if (heavy > 0 && sum >= __dmul_rn(thr2, (double)heavy)) {
+      atomicOr(&S.dis[p], 1u << q);
+      atomicOr(&S.dis[q], 1u << p);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kOptWarps * 32, 4)
     k_optimize_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
                        OptOut out, int *queue) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -116,9 +159,10 @@ __global__ void __launch_bounds__(256, 4)
   int32_t *s_w = reinterpret_cast<int32_t *>(s_pat + pk.n_atoms);
   const int wsz = DS_N_TYPES * DS_N_TYPES * nb1;
   float *s_ub2 = reinterpret_cast<float *>(s_w + wsz);
-  size_t fixed = (size_t)pk.n_atoms * 16 + (size_t)wsz * 4 + DS_MAX_BINS * 4;
-  fixed = (fixed + 15) & ~(size_t)15;
-  OptWarpSmem &S = reinterpret_cast<OptWarpSmem *>(smem + fixed)[warp];
+  // per-warp scratch is a static array: its address is a compile-time base + warp * stride, so the
+  // compiler never has to rematerialise it from launch parameters inside the hot loops
+  __shared__ OptWarpSmem s_warp[kOptWarps];
+  OptWarpSmem &S = s_warp[warp];
   for (int j = threadIdx.x; j < pk.n_atoms; j += blockDim.x) {
     float4 y = __ldg(pk.patoms + j);
     y.w = __int_as_float((int)y.w * nb1);  // column offset of the pocket atom's type in the weight table
@@ -208,21 +252,39 @@ __global__ void __launch_bounds__(256, 4)
           kz = __fdiv_rn(vz, len);
         }
         __syncwarp();
-        // ---- bump candidates (CSR per moving atom) ----
+        // ---- bump candidates per moving atom: cylindrical coordinates of C' in chr[0, nC) and of M
+        // in chr[kMaxA-1-m] (nM + nC <= A - 2), then every (m, c) pair tested by a flat lane loop;
+        // survivors are appended with byte-packed shared atomics (order is irrelevant: only the
+        // minimum distance is used) ----
         for (int c = lane; c < nC; c += 32) S.chr[c] = cyl_coords(S.u[S.clist[c]], a3, kx, ky, kz);
+        for (int m = lane; m < nM; m += 32) S.chr[kMaxA - 1 - m] = cyl_coords(S.u[S.mlist[m]], a3, kx, ky, kz);
+        for (int w = lane; w < (nM + 3) / 4; w += 32) S.cnw[w] = 0u;
         __syncwarp();
-        for (int m = lane; m < nM; m += 32) {
-          const float2 hm = cyl_coords(S.u[S.mlist[m]], a3, kx, ky, kz);
-          int cnt = 0;
-          for (int c = 0; c < nC; ++c) {
-            const float2 hc = S.chr[c];
-            const float dh = hm.x - hc.x, dr = hm.y - hc.y;
-            if (dh * dh + dr * dr < dp.cull2) {
-              if (cnt < kCand) S.cl[m][cnt] = S.clist[c];
-              ++cnt;
+        {
+          const unsigned total = (unsigned)nM * (unsigned)nC;
+          int pm = 0, pc = lane;
+          if (nC > 0) {
+            pm = lane / nC;
+            pc = lane - pm * nC;
+          }
+          const int dm = nC > 0 ? 32 / nC : 0, dc = nC > 0 ? 32 - dm * nC : 0;
+          for (unsigned p0 = 0; p0 < total; p0 += 32) {
+            if (p0 + (unsigned)lane < total) {
+              const float2 hm = S.chr[kMaxA - 1 - pm], hc = S.chr[pc];
+              const float dh = hm.x - hc.x, dr = hm.y - hc.y;
+              if (dh * dh + dr * dr < dp.cull2) {
+                const unsigned sh = 8u * (pm & 3);
+                const unsigned k = (atomicAdd(&S.cnw[pm >> 2], 1u << sh) >> sh) & 0xFFu;
+                if (k < (unsigned)kCand) S.cl[pm][k] = S.clist[pc];
+              }
+            }
+            pm += dm;
+            pc += dc;
+            if (pc >= nC) {
+              pc -= nC;
+              ++pm;
             }
           }
-          S.cn[m] = (uint8_t)(cnt > kCand ? 255 : cnt);
         }
         unsigned best_key = 0;  // (score + 32768) << 16 | (65535 - angle); 0 = no clean angle
         __syncwarp();
@@ -234,28 +296,29 @@ __global__ void __launch_bounds__(256, 4)
           const int a = lane % nA, gi = lane / nA;
           const bool lane_ok = gi < G;
           const int kang = k0 + a;
+          unsigned same = 0;                      // lanes that share this lane's angle
+          for (int t = 0; t < G; ++t) same |= 1u << (a + t * nA);
           float R[9];
           if (kang > 0) {
             const float2 cs = pk.trig[kang * dp.step_t];
             torsion_matrix(kx, ky, kz, cs.x, cs.y, R);
           }
           bool bumped = false;
-          int part = 0;
+          int part = 0, nact = 0;
           for (int m0 = 0; m0 < nM; m0 += G) {
             const int m = m0 + gi;
             const bool valid = lane_ok && m < nM;
             // with early exit a bumped angle is retired; without it every pair is checked
             const bool act = valid && !(dp.early_exit && bumped);
-            const unsigned am = __ballot_sync(kFull, act);
-            if (!am) break;
-            pairs_total += (unsigned)__popc(am) * (unsigned)nC;  // pairs resolved (P14)
+            if (!__any_sync(kFull, act)) break;
             bool hit = false;
             if (act) {
               const float4 p = S.u[S.mlist[m]];
               const float3 q = kang == 0 ? make_float3(p.x, p.y, p.z) : torsion_apply(R, a3, p.x, p.y, p.z);
+              const int gv = grid_val(pk, node_index(g, q.x, q.y, q.z));  // issued early: hides L2 latency
               float mind = __int_as_float(0x7f800000);  // min squared distance (P9: bump iff < bd2)
-              const int cnt = S.cn[m];
-              if (cnt != 255) {
+              const int cnt = (int)((S.cnw[m >> 2] >> (8 * (m & 3))) & 0xFFu);
+              if (cnt <= kCand) {
                 for (int t = 0; t < cnt; ++t) {
                   const float4 y = S.u[S.cl[m][t]];
                   mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
@@ -267,14 +330,16 @@ __global__ void __launch_bounds__(256, 4)
                 }
               }
               hit = mind < dp.bd2;
-              if (!hit) part += grid_val(pk, node_index(g, q.x, q.y, q.z));
+              if (!hit) part += gv;
+              ++nact;
             }
-            // OR the hits of the G lanes that share an angle
-            unsigned hb = __ballot_sync(kFull, hit);
-            unsigned fold = 0;
-            for (int t = 0; t < G; ++t) fold |= hb >> (t * nA);
-            bumped = bumped || ((fold >> a) & 1u);
+            if (dp.early_exit) {  // OR the hits of the G lanes that share an angle
+              bumped = bumped || (__ballot_sync(kFull, hit) & same) != 0u;
+            } else {
+              bumped = bumped || hit;
+            }
           }
+          pairs_total += (unsigned)warp_sum(nact) * (unsigned)nC;  // pairs resolved (P14)
           // combine the G partial scores of an angle on its group-0 lane
           int sum = part;
           for (int t = 1; t < G; ++t) {
@@ -373,34 +438,7 @@ __global__ void __launch_bounds__(256, 4)
       S.dis[r] = 0u;
     }
     __syncwarp();
-    // pairwise dissimilarity of valid poses: heavy-atom sum of squared deltas in f64, atom order
-    const int npairs = dp.N * (dp.N - 1) / 2;
-    for (int pidx = lane; pidx < npairs; pidx += 32) {
-      int p = 0, rem = pidx;
-      while (rem >= dp.N - 1 - p) {
-        rem -= dp.N - 1 - p;
-        ++p;
-      }
-      const int q = p + 1 + rem;
-      if (!S.valid[p] || !S.valid[q]) continue;
-      double sum = 0.0;
-      const float4 *up = scr + (size_t)p * kMaxA, *uq = scr + (size_t)q * kMaxA;
-      for (int i = 0; i < A; ++i) {
-        const float4 x = up[i], y = uq[i];
-        if (x.w == 0.f) continue;
-        const double dx = __dsub_rn((double)x.x, (double)y.x);
-        const double dy = __dsub_rn((double)x.y, (double)y.y);
-        const double dz = __dsub_rn((double)x.z, (double)y.z);
-        double t = __dmul_rn(dx, dx);
-        t = __dadd_rn(t, __dmul_rn(dy, dy));
-        t = __dadd_rn(t, __dmul_rn(dz, dz));
-        sum = __dadd_rn(sum, t);
-      }
-      if (heavy > 0 && sum >= __dmul_rn(dp.thr2, (double)heavy)) {
-        atomicOr(&S.dis[p], 1u << q);
-        atomicOr(&S.dis[q], 1u << p);
-      }
-    }
+    pose_dissimilarity(S, scr, A, dp.N, heavy, dp.thr2);
     __syncwarp();
     // greedy keep (warp-uniform)
     int nk = 0;
@@ -427,7 +465,7 @@ __global__ void __launch_bounds__(256, 4)
       }
       __syncwarp();
       long long acc = pk.nb == 4 ? rescore_pose<4>(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2)
-                                 : rescore_pose<0>(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2);
+                                 : rescore_pose_generic(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2);
       acc = warp_sum64(acc);
       if (best_r < 0 || acc > best_chem || (acc == best_chem && r < best_r)) {
         best_chem = acc;
@@ -461,7 +499,7 @@ __global__ void __launch_bounds__(256, 4)
   }
 }
 
-size_t optimize_warp_smem_bytes() { return sizeof(OptWarpSmem); }
+size_t optimize_warp_smem_bytes() { return 0; }  // per-warp scratch is static (kOptWarps per CTA)
 size_t optimize_cta_smem_bytes(int n_patoms, int nb) {
   size_t fixed = (size_t)n_patoms * 16 + (size_t)DS_N_TYPES * DS_N_TYPES * (nb + 1) * 4 + DS_MAX_BINS * 4;
   return (fixed + 15) & ~(size_t)15;

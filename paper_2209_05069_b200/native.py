@@ -20,7 +20,7 @@ import numpy as np
 from . import model
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdockscreen.so")
+LIB_PATH = os.environ.get("DOCKSCREEN_LIB") or os.path.join(_HERE, "libdockscreen.so")  # override: A/B builds
 
 DS_OK = 0
 ERRORS = {

@@ -57,11 +57,11 @@ def raw(rep):
                     v *= 1e3
                 elif unit == "Gbyte":
                     v *= 1e9
-                elif unit == "msecond":
+                elif unit in ("msecond", "ms"):
                     v *= 1e-3
-                elif unit == "usecond":
+                elif unit in ("usecond", "us"):
                     v *= 1e-6
-                elif unit == "nsecond":
+                elif unit in ("nsecond", "ns"):
                     v *= 1e-9
                 k[name] = v
         res.append(k)
