@@ -64,7 +64,7 @@ __device__ __forceinline__ float3 lat_torsion_pos(const float2 *trig, int step_t
 }
 
 template <bool kSmemGrid>
-__global__ void __launch_bounds__(kLatThreads)
+__global__ void __launch_bounds__(kLatThreads, 1)
     k_optimize_latency(PocketView pk, BatchView bt, DockParams dp, const int *scores, OptOut out, LatRec *recs,
                        int *done) {
   __shared__ LatSmem S;
@@ -199,30 +199,50 @@ __global__ void __launch_bounds__(kLatThreads)
         if (tid == 0) S.abump = 0u;
         __syncthreads();
       }
+      // thread = (angle a, moving-atom group mg): the rotation and the partial score stay in
+      // registers over m = mg, mg + G, ...; one shared atomic per thread at the end
       unsigned my_pairs = 0;
-      for (int s = tid; s < nA * nM; s += kLatThreads) {
-        const int a = s / nM, m = s - a * nM;
-        if (dp.early_exit && ((*(volatile unsigned *)&S.abump >> a) & 1u)) continue;
-        const float3 q = lat_torsion_pos(strig, dp.step_t, k0 + a, kx, ky, kz, a3, S.u[S.mlist[m]]);
-        float mind = __int_as_float(0x7f800000);
-        my_pairs += (unsigned)nC;  // pairs resolved (P14)
-        const int cnt = S.cn[m];
-        if (cnt != 255) {
-          for (int t = 0; t < cnt; ++t) {
-            const float4 y = S.cmp[S.cl[m][t]];
-            mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
-          }
-        } else {
-          for (int c = 0; c < nC; c += kLatChunk) {
-#pragma unroll
-            for (int t = 0; t < kLatChunk; ++t) {
-              const float4 y = S.cmp[c + t];
+      const int G = kLatThreads / nA;
+      const int a = tid % nA, mg = tid / nA;
+      if (mg < G) {
+        float R[9];
+        const int kang = k0 + a;
+        if (kang > 0) {
+          const float2 cs = strig[kang * dp.step_t];
+          torsion_matrix(kx, ky, kz, cs.x, cs.y, R);
+        }
+        int part = 0;
+        bool hit_any = false;
+        for (int m = mg; m < nM; m += G) {
+          if (dp.early_exit && (hit_any || ((*(volatile unsigned *)&S.abump >> a) & 1u))) break;
+          const float4 p = S.u[S.mlist[m]];
+          const float3 q = kang == 0 ? make_float3(p.x, p.y, p.z) : torsion_apply(R, a3, p.x, p.y, p.z);
+          const int gv = lat_grid_val<kSmemGrid>(grid, node_index(g, q.x, q.y, q.z));
+          float mind = __int_as_float(0x7f800000);
+          my_pairs += (unsigned)nC;  // pairs resolved (P14)
+          const int cnt = S.cn[m];
+          if (cnt != 255) {
+            for (int t = 0; t < cnt; ++t) {
+              const float4 y = S.cmp[S.cl[m][t]];
               mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
             }
+          } else {
+            for (int c = 0; c < nC; c += kLatChunk) {
+#pragma unroll
+              for (int t = 0; t < kLatChunk; ++t) {
+                const float4 y = S.cmp[c + t];
+                mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+              }
+            }
+          }
+          if (mind < dp.bd2) {
+            hit_any = true;
+            atomicOr(&S.abump, 1u << a);
+          } else {
+            part += gv;
           }
         }
-        if (mind < dp.bd2) atomicOr(&S.abump, 1u << a);
-        else atomicAdd(&S.ascore[a], lat_grid_val<kSmemGrid>(grid, node_index(g, q.x, q.y, q.z)));
+        if (part) atomicAdd(&S.ascore[a], part);
       }
       my_pairs = __reduce_add_sync(kFull, my_pairs);
       if (lane == 0) atomicAdd(&S.pairs, my_pairs);

@@ -89,10 +89,18 @@ def launches(path):
 
 
 def main():
-    rep, out = sys.argv[1], sys.argv[2]
-    doc = {"report": rep, "kernels": raw(rep)}
-    if len(sys.argv) > 3:
-        doc["launch_list"] = launches(sys.argv[3])
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("report")
+    ap.add_argument("out")
+    ap.add_argument("launch_csv", nargs="?")
+    ap.add_argument("--ligands", type=int, default=0, help="ligands docked per profiled launch (per-ligand calibration)")
+    ap.add_argument("--workload", default="")
+    a = ap.parse_args()
+    rep, out = a.report, a.out
+    doc = {"report": rep, "kernels": raw(rep), "ligands": a.ligands, "workload": a.workload}
+    if a.launch_csv:
+        doc["launch_list"] = launches(a.launch_csv)
     with open(out + ".json", "w") as fh:
         json.dump(doc, fh, indent=1)
     lines = ["| kernel | ms | warp-inst | issue % | warps % | DRAM B | L2 hit % | regs |", "|---|---|---|---|---|---|---|---|"]
