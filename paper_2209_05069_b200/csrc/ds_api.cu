@@ -55,6 +55,14 @@ int fail(int code, const char *fmt, ...) {
     if (e_ != cudaSuccess) return fail(DS_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
   } while (0)
 
+// API entry: make the context's device current and drop any non-sticky error left in this thread
+// by an earlier, unrelated runtime call, so the launch checks below report only this call's errors
+cudaError_t enter_device(int device) {
+  cudaGetLastError();
+  const cudaError_t e = cudaSetDevice(device);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 // device buffer that grows geometrically; counts cudaMalloc calls
 struct DevBuf {
   void *p = nullptr;
@@ -252,7 +260,7 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
   for (int t = 0; t < DS_N_TYPES * DS_N_TYPES; ++t)
     if (d->table[t] != d->table[(t % DS_N_TYPES) * DS_N_TYPES + t / DS_N_TYPES])
       return fail(DS_ERR_INVALID_ARG, "interaction table must be symmetric");
-  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(enter_device(c->device));
   ds_pocket *p = new ds_pocket();
   p->ctx = c;
   PocketView &v = p->view;
@@ -773,7 +781,7 @@ int ds_dock(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const ds_doc
   if (st) memset(st, 0, sizeof *st);
   const int L = b->n_ligands;
   if (L == 0) return DS_OK;
-  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(enter_device(c->device));
   if (family == DS_FAMILY_BATCHED) {
     const int nch = pipeline_chunks(L);
     if (nch > 1) return dock_pipelined(c, pk, b, dp, out, st, nch);
@@ -798,7 +806,7 @@ int ds_ctx_reserve(ds_ctx *c, int max_ligands, int max_atoms, int max_frags, con
   if (cfg->restarts_n < 1 || cfg->restarts_n > DS_MAX_RESTARTS || cfg->alignment_step_deg < 1 ||
       360 % cfg->alignment_step_deg)
     return fail(DS_ERR_INVALID_ARG, "bad config");
-  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(enter_device(c->device));
   const int N = cfg->restarts_n, na = 360 / cfg->alignment_step_deg;
   const size_t L = (size_t)max_ligands;
   int rc;
@@ -815,7 +823,7 @@ int ds_batch_upload(ds_ctx *c, const ds_batch_desc *b, ds_dev_batch **out) {
   if (!c || !out) return fail(DS_ERR_INVALID_ARG, "NULL argument");
   int rc;
   if ((rc = check_batch(b))) return rc;
-  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(enter_device(c->device));
   ds_dev_batch *d = new ds_dev_batch();
   d->ctx = c;
   d->L = b->n_ligands;
@@ -840,7 +848,7 @@ int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_d
   if ((rc = check_config(cfg, pk, &dp))) return rc;
   if (st) memset(st, 0, sizeof *st);
   if (d->L == 0) return DS_OK;
-  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(enter_device(c->device));
   int max_atoms = 0;
   for (int i = 0; i < d->L; ++i) max_atoms = std::max(max_atoms, d->atom_off[i + 1] - d->atom_off[i]);
   if ((rc = run_family(c, pk, family, d->L, d->n_atoms, d->n_frags, max_atoms, dp, true, true, true, st))) return rc;
@@ -873,7 +881,7 @@ int ds_query_capacity(ds_ctx *c, int range_idx, int *ligands) {
 int ds_op_grid_score(ds_ctx *c, const ds_pocket *pk, const float *coords, int n_atoms, int n_poses, int32_t *out) {
   if (!c || !pk || !coords || !out || n_atoms < 0 || n_poses < 0) return fail(DS_ERR_INVALID_ARG, "bad argument");
   if (!n_poses) return DS_OK;
-  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(enter_device(c->device));
   const size_t nc = 12ull * n_atoms * n_poses;
   int rc;
   if ((rc = c->ensure(c->b_coords, std::max<size_t>(nc, 16))) || (rc = c->ensure(c->b_keys, 4ull * n_poses))) return rc;
@@ -890,7 +898,7 @@ int ds_op_rescore(ds_ctx *c, const ds_pocket *pk, const float *coords, const uin
   if (!c || !pk || !coords || !types || !out || n_atoms < 0 || n_poses < 0) return fail(DS_ERR_INVALID_ARG, "bad argument");
   if (cutoff != pk->cutoff) return fail(DS_ERR_INVALID_ARG, "cutoff must equal the last bin bound");
   if (!n_poses) return DS_OK;
-  DS_CUDA(cudaSetDevice(c->device));
+  DS_CUDA(enter_device(c->device));
   const size_t nc = 12ull * n_atoms * n_poses;
   int rc;
   if ((rc = c->ensure(c->b_coords, std::max<size_t>(nc, 16))) || (rc = c->ensure(c->b_rtors, std::max(n_atoms, 1))) ||

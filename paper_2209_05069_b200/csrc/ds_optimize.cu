@@ -334,7 +334,9 @@ __global__ void __launch_bounds__(kOptWarps * 32, 4)
               ++nact;
             }
             if (dp.early_exit) {  // OR the hits of the G lanes that share an angle
-              bumped = bumped || (__ballot_sync(kFull, hit) & same) != 0u;
+              // every lane must reach the ballot: never put it behind a short-circuit operator
+              const unsigned hb = __ballot_sync(kFull, hit);
+              bumped = bumped || (hb & same) != 0u;
             } else {
               bumped = bumped || hit;
             }
