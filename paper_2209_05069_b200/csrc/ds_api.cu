@@ -389,6 +389,7 @@ int check_config(const ds_dock_config *cfg, const ds_pocket *pk, DockParams *dp)
   const double th = (double)cfg->similarity_rmsd / s;
   dp->thr2 = th * th;                                      // P12
   dp->cull2 = (float)((bd + 0.02) * (bd + 0.02));          // conservative bump-candidate bound
+  dp->cull_r = (float)((bd + 0.02) * (1.0 + 1e-6));
   return DS_OK;
 }
 

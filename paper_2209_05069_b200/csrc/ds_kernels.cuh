@@ -37,6 +37,7 @@ struct DockParams {
   float eps_axis;            // DegenerateAxis threshold, grid frame
   double thr2;               // squared similarity RMSD, grid frame
   float cull2;               // squared bump-candidate bound (bump distance + 0.02 nodes), grid frame
+  float cull_r;              // the bound itself (rounded up), for the per-fragment (h, r) box
 };
 
 struct AlignOut {

@@ -24,6 +24,9 @@ namespace ds {
 constexpr int kMaxA = DS_MAX_ATOMS;
 constexpr int kCand = 6;             // bump-candidate slots per moving atom (overflow: full scan)
 constexpr int kOptWarps = 8;         // warps per CTA (one ligand each)
+#ifndef DS_OPT_MIN_BLOCKS
+#define DS_OPT_MIN_BLOCKS 4          // resident CTAs per SM the register budget is sized for
+#endif
 
 struct OptWarpSmem {
   float4 u[kMaxA];          // committed pose of the current restart (grid frame), .w = type
@@ -57,6 +60,13 @@ __device__ __forceinline__ float2 cyl_coords(float4 p, float3 a, float kx, float
   const float r2 = wx * wx + wy * wy + wz * wz - h * h;
   return make_float2(h, sqrtf(fmaxf(r2, 0.f)));
 }
+
+// order-preserving float <-> int map (an involution), so warp min/max reductions run on REDUX
+__device__ __forceinline__ int ordered_bits(float f) {
+  const int b = __float_as_int(f);
+  return b ^ ((b >> 31) & 0x7FFFFFFF);
+}
+__device__ __forceinline__ float from_ordered_bits(int b) { return __int_as_float(b ^ ((b >> 31) & 0x7FFFFFFF)); }
 
 // rotated position of a moving atom for torsion angle index k (k == 0: identity, P8)
 __device__ __forceinline__ float3 torsion_pos(const PocketView &pk, int step_t, int k, float kx, float ky, float kz,
@@ -148,7 +158,7 @@ __device__ __noinline__ void pose_dissimilarity(OptWarpSmem &S, const float4 *sc
   }
 }
 
-__global__ void __launch_bounds__(kOptWarps * 32, 4)
+__global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
     k_optimize_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
                        OptOut out, int *queue) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -256,18 +266,51 @@ __global__ void __launch_bounds__(kOptWarps * 32, 4)
         // in chr[kMaxA-1-m] (nM + nC <= A - 2), then every (m, c) pair tested by a flat lane loop;
         // survivors are appended with byte-packed shared atomics (order is irrelevant: only the
         // minimum distance is used) ----
-        for (int c = lane; c < nC; c += 32) S.chr[c] = cyl_coords(S.u[S.clist[c]], a3, kx, ky, kz);
-        for (int m = lane; m < nM; m += 32) S.chr[kMaxA - 1 - m] = cyl_coords(S.u[S.mlist[m]], a3, kx, ky, kz);
+        // The (h, r) box of M grown by the culling radius prefilters C': an atom outside it is
+        // farther than the radius from every moving atom's circle, so it can never bump and is
+        // dropped from the pair loop, the candidate lists and the overflow scan (nCf <= nC; the
+        // P14 counters still count all nC complement atoms).
+        int hlo = 0x7FFFFFFF, hhi = (int)0x80000000, rhi = 0;
+        for (int m = lane; m < nM; m += 32) {
+          const float2 hr = cyl_coords(S.u[S.mlist[m]], a3, kx, ky, kz);
+          S.chr[kMaxA - 1 - m] = hr;
+          hlo = min(hlo, ordered_bits(hr.x));
+          hhi = max(hhi, ordered_bits(hr.x));
+          rhi = max(rhi, __float_as_int(hr.y));  // r >= +0: bit order is float order
+        }
+        const float cut = dp.cull_r;
+        const float h0 = __fsub_rn(from_ordered_bits(__reduce_min_sync(kFull, hlo)), cut);
+        const float h1 = __fadd_rn(from_ordered_bits(__reduce_max_sync(kFull, hhi)), cut);
+        const float r1 = __fadd_rn(__int_as_float(__reduce_max_sync(kFull, rhi)), cut);
+        int nCf = 0;
+        for (int c0 = 0; c0 < nC; c0 += 32) {
+          const int c = c0 + lane;
+          float2 hr = make_float2(0.f, 0.f);
+          uint8_t ci = 0;
+          bool keep = false;
+          if (c < nC) {
+            ci = S.clist[c];
+            hr = cyl_coords(S.u[ci], a3, kx, ky, kz);
+            keep = hr.x > h0 && hr.x < h1 && hr.y < r1;
+          }
+          const unsigned bk = __ballot_sync(kFull, keep);  // in-place compaction: slot <= c
+          if (keep) {
+            const int slot = nCf + __popc(bk & lt);
+            S.chr[slot] = hr;
+            S.clist[slot] = ci;
+          }
+          nCf += __popc(bk);
+        }
         for (int w = lane; w < (nM + 3) / 4; w += 32) S.cnw[w] = 0u;
         __syncwarp();
         {
-          const unsigned total = (unsigned)nM * (unsigned)nC;
+          const unsigned total = (unsigned)nM * (unsigned)nCf;
           int pm = 0, pc = lane;
-          if (nC > 0) {
-            pm = lane / nC;
-            pc = lane - pm * nC;
+          if (nCf > 0) {
+            pm = lane / nCf;
+            pc = lane - pm * nCf;
           }
-          const int dm = nC > 0 ? 32 / nC : 0, dc = nC > 0 ? 32 - dm * nC : 0;
+          const int dm = nCf > 0 ? 32 / nCf : 0, dc = nCf > 0 ? 32 - dm * nCf : 0;
           for (unsigned p0 = 0; p0 < total; p0 += 32) {
             if (p0 + (unsigned)lane < total) {
               const float2 hm = S.chr[kMaxA - 1 - pm], hc = S.chr[pc];
@@ -280,8 +323,8 @@ __global__ void __launch_bounds__(kOptWarps * 32, 4)
             }
             pm += dm;
             pc += dc;
-            if (pc >= nC) {
-              pc -= nC;
+            if (pc >= nCf) {
+              pc -= nCf;
               ++pm;
             }
           }
@@ -324,7 +367,7 @@ __global__ void __launch_bounds__(kOptWarps * 32, 4)
                   mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
                 }
               } else {
-                for (int c = 0; c < nC; ++c) {
+                for (int c = 0; c < nCf; ++c) {
                   const float4 y = S.u[S.clist[c]];
                   mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
                 }
