@@ -142,7 +142,9 @@ def ncu_calibration():
             name = k["kernel"].split("(")[0].split("<")[0].replace("void ", "").strip().split("::")[-1]
             out[name] = {"inst_per_ligand": k.get("warp_inst_executed", 0) / nlig,
                          "dram_bytes_per_ligand": (k.get("dram_read", 0) + k.get("dram_write", 0)) / nlig,
-                         "issue_active_pct": k.get("issue_active_pct")}
+                         "issue_active_pct": k.get("issue_active_pct"),
+                         "pipe_fmaheavy_pct": k.get("pipe_fmaheavy_pct"),
+                         "smem_wavefront_pct": k.get("smem_wavefront_pct")}
         return out
     return {}
 
@@ -290,7 +292,10 @@ def main():
                     f"ligands / launch time / peak; traffic = ncu DRAM bytes per ligand x ligands"}
     roof_align = {"kernel": "k_align_batched", "frac": (w_align / (a_ms / 1e3)) / peak_winst,
                   "executed_issue_frac": (cal["k_align_batched"]["inst_per_ligand"] * n / (a_ms / 1e3) / peak_winst)
-                  if "inst_per_ligand" in cal.get("k_align_batched", {}) else None}
+                  if "inst_per_ligand" in cal.get("k_align_batched", {}) else None,
+                  "ncu_pipe_fmaheavy_pct": cal.get("k_align_batched", {}).get("pipe_fmaheavy_pct"),
+                  "ncu_smem_wavefront_pct": cal.get("k_align_batched", {}).get("smem_wavefront_pct"),
+                  "note": "binding unit: the FMA-heavy pipe (FFMA2/FADD2/IMAD), per the committed ncu capture"}
     whole = {"achieved": (w_total / (ms / 1e3)) / 1e9, "frac": (w_total / (ms / 1e3)) / peak_winst,
              "unit": "Gwarp-inst/s"}
     in_bytes = int(packed.atom_xyzt.nbytes + packed.frag_desc.nbytes + packed.atom_off.nbytes * 2 + packed.id_hash.nbytes)

@@ -8,18 +8,29 @@
 // Work split: a lane owns a (restart, ax) unit and sweeps every atom of the ligand for ALL ay.
 // Because the pose is Ry(ay) (Rx(ax) (R0s d)) + t (DESIGN.md §3 P6), the inner vector
 // v = Rx(ax) R0s d and the whole y coordinate (clamp and row offset included) are shared by the
-// n_a values of ay, leaving 4 FFMA + a branch-free nearest-node lookup (2 FADD, 4 IMNMX, 1-2 IMAD,
-// 1 LDS.U8) + 1 add per (atom, ay).  For the default 12° step the 30 (cos, sin) pairs of ay are
-// __constant__ and the ay loop is fully unrolled, so they are FFMA constant-bank operands; the
-// 30 running scores are packed two per register as biased 16-bit sums.  Every lane is busy
-// whatever the atom count (the paper's lanes-over-atoms mapping idles lanes when A % 32 != 0,
-// PAPER.md:717).  Output: one packed argmax key per (ligand, restart):
-// (score + 32768) << 16 | (65535 - (ix * n_a + iy)).
+// n_a values of ay.  For the default 12° step the 30 (cos, sin) pairs of ay are __constant__ and
+// the ay loop is fully unrolled; angles are processed in pairs with Blackwell's packed f32x2
+// FFMA2/FADD2 (each half bit-identical to the scalar __fmaf_rn/__fadd_rn of the recipe; the angle
+// pairs become uniform-register operands), so per (atom, ay pair): 4 FFMA2 + 2 FADD2 + 4
+// VIADDMNMX (unsigned clamp) + 4 IMAD + 2 LDS.U8 + 2 adds into scores packed two per register as
+// biased 16-bit sums (9 SASS instructions per (atom, ay), 13.3 before f32x2).  The binding unit is
+// the FMA-heavy pipe (FFMA2, FADD2 and IMAD all issue there; ncu: 82 % of its peak, shared-memory
+// wavefronts 82 %), not issue.  Every lane is busy whatever the atom count (the paper's
+// lanes-over-atoms mapping idles lanes when A % 32 != 0).  Output: one packed
+// argmax key per (ligand, restart): (score + 32768) << 16 | (65535 - (ix * n_a + iy)).
+#include <string.h>
+
 #include "ds_kernels.cuh"
 
 namespace ds {
 
 __constant__ float4 c_trig_ay[360];  // (cos, sin, -sin, 0) of iy * step_a
+// the same angles as packed pairs for the f32x2 path: [k/2] = {(c_k, c_k+1), (s_k, s_k+1), (-s_k, -s_k+1)}
+__constant__ unsigned long long c_pair_ay[180][3];
+
+#ifndef DS_ALIGN_F32X2
+#define DS_ALIGN_F32X2 1
+#endif
 
 // dynamic smem layout: [grid bytes (16-aligned)] [trig_a float4[n_a]] [per warp: stage float4[32],
 // params float[N*12], keys u32[N]]
@@ -29,12 +40,67 @@ __device__ __forceinline__ unsigned grid_u8(const uint8_t *grid, int idx, bool s
   return smem ? (unsigned)grid[idx] : (unsigned)__ldg(grid + idx);
 }
 
+// ---- Blackwell packed f32x2 arithmetic (FFMA2 / FADD2): two IEEE round-to-nearest operations
+// per instruction, each lane of the pair bit-identical to the scalar __fmaf_rn / __fadd_rn ----
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// f32x2 form of unit_atom for the constant-angle path: per pair of angles (k, k+1)
+//   UX = fma2(S, VZ, fma2(C, VX, TX)),  UZ = fma2(C, VZ, fma2(-S, VX, TZ)),  + (magic, magic)
+// — lane-for-lane the same operations as the scalar recipe P6/P4, in half the FP32 issue slots.
+template <int G, bool kSmemGrid>
+__device__ __forceinline__ void unit_atom_x2(const float3 v, f2_t TX, f2_t TZ, unsigned yk, const GridGeom &g,
+                                             const uint8_t *grid, unsigned *acc) {
+  const f2_t VX = f2_pack(v.x, v.x), VZ = f2_pack(v.z, v.z);
+  const f2_t MM = f2_pack(kMagic, kMagic);
+#pragma unroll
+  for (int k = 0; k < G; k += 2) {
+    const f2_t C = c_pair_ay[k >> 1][0], S = c_pair_ay[k >> 1][1], NS = c_pair_ay[k >> 1][2];
+    const f2_t UX = f2_add(f2_fma(S, VZ, f2_fma(C, VX, TX)), MM);
+    const f2_t UZ = f2_add(f2_fma(C, VZ, f2_fma(NS, VX, TZ)), MM);
+    float mx0, mx1, mz0, mz1;
+    f2_unpack(UX, mx0, mx1);
+    f2_unpack(UZ, mz0, mz1);
+    const unsigned K = (unsigned)(kMagicBits - 1);
+    const unsigned cx0 = min((unsigned)__float_as_int(mx0) - K, (unsigned)(g.nx + 1));
+    const unsigned cx1 = min((unsigned)__float_as_int(mx1) - K, (unsigned)(g.nx + 1));
+    const unsigned cz0 = min((unsigned)__float_as_int(mz0) - K, (unsigned)(g.nz + 1));
+    const unsigned cz1 = min((unsigned)__float_as_int(mz1) - K, (unsigned)(g.nz + 1));
+    const int i0 = (int)(cx0 + g.NXY * cz0 + yk);
+    const int i1 = (int)(cx1 + g.NXY * cz1 + yk);
+    acc[k >> 1] += grid_u8(grid, i0, kSmemGrid) + (grid_u8(grid, i1, kSmemGrid) << 16);
+  }
+}
+
 // Accumulate the biased grid values of angles iy = iy0 .. iy0+G-1 for one atom's v into G/2
 // packed registers (low half: even k, high half: odd k).
 template <int G, bool kConst, bool kSmemGrid>
 __device__ __forceinline__ void unit_atom(const float3 v, const float *t, unsigned yk, const GridGeom &g,
                                           const uint8_t *grid, const float4 *strig, int iy0, int n_a,
                                           unsigned *acc) {
+#if DS_ALIGN_F32X2
+  if (kConst) {
+    unit_atom_x2<G, kSmemGrid>(v, f2_pack(t[0], t[0]), f2_pack(t[2], t[2]), yk, g, grid, acc);
+    return;
+  }
+#endif
 #pragma unroll
   for (int k = 0; k < G; k += 2) {
     const float4 c0 = kConst ? c_trig_ay[k] : strig[min(iy0 + k, n_a - 1)];
@@ -205,19 +271,38 @@ __global__ void __launch_bounds__(32)
   }
 }
 
+// the n_a = 30 angle table in __constant__ (scalar and packed-pair forms); same values as the ctx
+// trig table (P0), identical for every caller
+static void upload_const_angles(int step_a, cudaStream_t st) {
+  static float4 h[30];
+  static unsigned long long hp[15][3];
+  for (int i = 0; i < 30; ++i) {
+    const double rad = (double)(i * step_a) * 0.017453292519943295;
+    const float c = (float)cos(rad), s = (float)sin(rad);
+    h[i] = make_float4(c, s, -s, 0.f);
+  }
+  auto pk = [](float lo, float hi) {
+    unsigned a, b;
+    memcpy(&a, &lo, 4);
+    memcpy(&b, &hi, 4);
+    return (unsigned long long)a | ((unsigned long long)b << 32);
+  };
+  for (int p = 0; p < 15; ++p) {
+    hp[p][0] = pk(h[2 * p].x, h[2 * p + 1].x);
+    hp[p][1] = pk(h[2 * p].y, h[2 * p + 1].y);
+    hp[p][2] = pk(h[2 * p].z, h[2 * p + 1].z);
+  }
+  cudaMemcpyToSymbolAsync(c_trig_ay, h, sizeof h, 0, cudaMemcpyHostToDevice, st);
+  cudaMemcpyToSymbolAsync(c_pair_ay, hp, sizeof hp, 0, cudaMemcpyHostToDevice, st);
+}
+
 void launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
                           cudaStream_t st) {
   const int ach = 4;
   const int nchunks = (max_atoms + ach - 1) / ach;
   const int blocks = bt.L * dp.N * nchunks;
   if (dp.n_a == 30) {
-    static float4 h[30];
-    for (int i = 0; i < 30; ++i) {
-      const double rad = (double)(i * dp.step_a) * 0.017453292519943295;
-      const float c = (float)cos(rad), s = (float)sin(rad);
-      h[i] = make_float4(c, s, -s, 0.f);
-    }
-    cudaMemcpyToSymbolAsync(c_trig_ay, h, sizeof h, 0, cudaMemcpyHostToDevice, st);
+    upload_const_angles(dp.step_a, st);
     k_align_latency<30><<<blocks, 32, 0, st>>>(pk, bt, dp, ach, nchunks, scores);
   } else {
     k_align_latency<0><<<blocks, 32, 0, st>>>(pk, bt, dp, ach, nchunks, scores);
@@ -237,13 +322,7 @@ void launch_align_batched(const PocketView &pk, const BatchView &bt, const DockP
                           AlignOut out, int *queue, int grid_in_smem, int blocks, int warps, size_t smem,
                           cudaStream_t st) {
   if (dp.n_a == 30) {  // default 12° step: all 30 ay per unit, constant-bank angles
-    static float4 h[30];  // same values as the ctx trig table (P0); identical for every caller
-    for (int i = 0; i < 30; ++i) {
-      const double rad = (double)(i * dp.step_a) * 0.017453292519943295;
-      const float c = (float)cos(rad), s = (float)sin(rad);
-      h[i] = make_float4(c, s, -s, 0.f);
-    }
-    cudaMemcpyToSymbolAsync(c_trig_ay, h, sizeof h, 0, cudaMemcpyHostToDevice, st);
+    upload_const_angles(dp.step_a, st);
     if (grid_in_smem) launch_t<30, 30, true>(pk, bt, dp, order, out, queue, blocks, warps, smem, st);
     else launch_t<30, 30, false>(pk, bt, dp, order, out, queue, blocks, warps, smem, st);
   } else {

@@ -17,6 +17,8 @@ KEYS = {
     "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "pipe_fma_pct",
     "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "pipe_alu_pct",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed": "pipe_fmaheavy_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_wavefront_pct",
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active": "pipe_lsu_pct",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "smem_wavefronts",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
@@ -103,11 +105,14 @@ def main():
         doc["launch_list"] = launches(a.launch_csv)
     with open(out + ".json", "w") as fh:
         json.dump(doc, fh, indent=1)
-    lines = ["| kernel | ms | warp-inst | issue % | warps % | DRAM B | L2 hit % | regs |", "|---|---|---|---|---|---|---|---|"]
+    lines = ["| kernel | ms | warp-inst | issue % | warps % | fma pipe % | alu pipe % | smem wavefronts | bank conflicts | DRAM B | L2 hit % | regs |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for k in doc["kernels"]:
-        lines.append("| %s | %.3f | %.3e | %.1f | %.1f | %.3e | %.1f | %d |" % (
+        lines.append("| %s | %.3f | %.3e | %.1f | %.1f | %.1f | %.1f | %.3e | %.3e | %.3e | %.1f | %d |" % (
             k["kernel"].split("(")[0][:40], 1e3 * k.get("duration", 0), k.get("warp_inst_executed", 0),
-            k.get("issue_active_pct", 0), k.get("warps_active_pct", 0), k.get("dram_read", 0) + k.get("dram_write", 0),
+            k.get("issue_active_pct", 0), k.get("warps_active_pct", 0), k.get("pipe_fma_pct", 0),
+            k.get("pipe_alu_pct", 0), k.get("smem_wavefronts", 0), k.get("smem_bank_conflicts", 0),
+            k.get("dram_read", 0) + k.get("dram_write", 0),
             k.get("l2_hit_pct", 0), int(k.get("regs", 0))))
     if "launch_list" in doc:
         lines += ["", "launch list (ncu gpu__time_duration.sum, cold-cache, serialised):", ""]
