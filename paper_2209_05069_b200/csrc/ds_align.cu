@@ -29,7 +29,7 @@ __constant__ float4 c_trig_ay[360];  // (cos, sin, -sin, 0) of iy * step_a
 __constant__ unsigned long long c_pair_ay[180][3];
 
 #ifndef DS_ALIGN_F32X2
-#define DS_ALIGN_F32X2 1
+#define DS_ALIGN_F32X2 2   // 0 scalar, 1 all packed, 2 packed x + scalar z (fastest), 3 packed FMAs + scalar rounding adds
 #endif
 
 // dynamic smem layout: [grid bytes (16-aligned)] [trig_a float4[n_a]] [per warp: stage float4[32],
@@ -73,18 +73,38 @@ __device__ __forceinline__ void unit_atom_x2(const float3 v, f2_t TX, f2_t TZ, u
 #pragma unroll
   for (int k = 0; k < G; k += 2) {
     const f2_t C = c_pair_ay[k >> 1][0], S = c_pair_ay[k >> 1][1], NS = c_pair_ay[k >> 1][2];
+#if DS_ALIGN_F32X2 == 3  // packed FMAs, scalar magic adds (FADD may issue on the FMA-lite pipe)
+    float ux0, ux1, uz0, uz1;
+    f2_unpack(f2_fma(S, VZ, f2_fma(C, VX, TX)), ux0, ux1);
+    f2_unpack(f2_fma(C, VZ, f2_fma(NS, VX, TZ)), uz0, uz1);
+    const float mx0 = __fadd_rn(ux0, kMagic), mx1 = __fadd_rn(ux1, kMagic);
+    const float mz0 = __fadd_rn(uz0, kMagic), mz1 = __fadd_rn(uz1, kMagic);
+#elif DS_ALIGN_F32X2 == 2  // packed x, scalar z
+    float mx0, mx1;
+    f2_unpack(f2_add(f2_fma(S, VZ, f2_fma(C, VX, TX)), MM), mx0, mx1);
+    float c0, c1, s0, s1;
+    f2_unpack(C, c0, c1);
+    f2_unpack(S, s0, s1);
+    float vx, vz, tz, tz1;
+    f2_unpack(VX, vx, tz1);
+    f2_unpack(VZ, vz, tz1);
+    f2_unpack(TZ, tz, tz1);
+    const float mz0 = __fadd_rn(__fmaf_rn(c0, vz, __fmaf_rn(-s0, vx, tz)), kMagic);
+    const float mz1 = __fadd_rn(__fmaf_rn(c1, vz, __fmaf_rn(-s1, vx, tz)), kMagic);
+#else
     const f2_t UX = f2_add(f2_fma(S, VZ, f2_fma(C, VX, TX)), MM);
     const f2_t UZ = f2_add(f2_fma(C, VZ, f2_fma(NS, VX, TZ)), MM);
     float mx0, mx1, mz0, mz1;
     f2_unpack(UX, mx0, mx1);
     f2_unpack(UZ, mz0, mz1);
+#endif
     const unsigned K = (unsigned)(kMagicBits - 1);
     const unsigned cx0 = min((unsigned)__float_as_int(mx0) - K, (unsigned)(g.nx + 1));
     const unsigned cx1 = min((unsigned)__float_as_int(mx1) - K, (unsigned)(g.nx + 1));
     const unsigned cz0 = min((unsigned)__float_as_int(mz0) - K, (unsigned)(g.nz + 1));
     const unsigned cz1 = min((unsigned)__float_as_int(mz1) - K, (unsigned)(g.nz + 1));
-    const int i0 = (int)(cx0 + g.NXY * cz0 + yk);
-    const int i1 = (int)(cx1 + g.NXY * cz1 + yk);
+    const int i0 = (int)((cx0 + g.NXY * cz0) + yk);
+    const int i1 = (int)((cx1 + g.NXY * cz1) + yk);
     acc[k >> 1] += grid_u8(grid, i0, kSmemGrid) + (grid_u8(grid, i1, kSmemGrid) << 16);
   }
 }
@@ -199,7 +219,8 @@ __global__ void __launch_bounds__(1024, 1)
         for (int a = 0; a < n; ++a) {
           const float4 d = stage[a];
           const float3 v = align_v(Rp, d.x, d.y, d.z);
-          const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny);  // u_y is shared by all ay
+          // u_y is shared by all ay; the opaque XOR keeps the row offset an ALU add per angle
+          const unsigned yk = (g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny)) ^ dp.opaque0;
           unit_atom<G, kConst, kSmemGrid>(v, t, yk, g, grid, strig, iy0, n_a, acc);
         }
       }

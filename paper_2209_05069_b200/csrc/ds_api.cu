@@ -390,6 +390,7 @@ int check_config(const ds_dock_config *cfg, const ds_pocket *pk, DockParams *dp)
   dp->thr2 = th * th;                                      // P12
   dp->cull2 = (float)((bd + 0.02) * (bd + 0.02));          // conservative bump-candidate bound
   dp->cull_r = (float)((bd + 0.02) * (1.0 + 1e-6));
+  dp->opaque0 = 0u;
   return DS_OK;
 }
 

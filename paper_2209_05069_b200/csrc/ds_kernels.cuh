@@ -38,6 +38,8 @@ struct DockParams {
   double thr2;               // squared similarity RMSD, grid frame
   float cull2;               // squared bump-candidate bound (bump distance + 0.02 nodes), grid frame
   float cull_r;              // the bound itself (rounded up), for the per-fragment (h, r) box
+  unsigned opaque0;          // always 0: XORed into loop-invariant index terms so ptxas keeps them as
+                             // ALU adds instead of re-deriving them with FMA-pipe IMADs
 };
 
 struct AlignOut {
