@@ -325,7 +325,7 @@ def main():
                            "parallelism": f"dp{world} (contiguous ligand shards, no collective)"},
                 "e2e": e2e, "roofline": roof, "roofline_align": roof_align, "roofline_whole_step": whole,
                 "roofline_hbm": hbm,
-                "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": 2 * args.steps,
+                "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": 3 * args.steps,
                 "kernel_ms": {"align": a_ms, "optimize": o_ms}, "status_ok_frac": status_ok}
         print(json.dumps(line), flush=True)
     rb.close()

@@ -129,8 +129,8 @@ __device__ __forceinline__ void unit_atom(const float3 v, const float *t, unsign
     const float uz0 = __fmaf_rn(c0.x, v.z, __fmaf_rn(c0.z, v.x, t[2]));
     const float ux1 = __fmaf_rn(c1.y, v.z, __fmaf_rn(c1.x, v.x, t[0]));
     const float uz1 = __fmaf_rn(c1.x, v.z, __fmaf_rn(c1.z, v.x, t[2]));
-    const int i0 = (int)(clamp_bits(ux0, g.nx) + g.NXY * clamp_bits(uz0, g.nz) + yk);
-    const int i1 = (int)(clamp_bits(ux1, g.nx) + g.NXY * clamp_bits(uz1, g.nz) + yk);
+    const int i0 = (int)(clamp_bits(ux0, g.nx + 1) + g.NXY * clamp_bits(uz0, g.nz + 1) + yk);
+    const int i1 = (int)(clamp_bits(ux1, g.nx + 1) + g.NXY * clamp_bits(uz1, g.nz + 1) + yk);
     acc[k >> 1] += grid_u8(grid, i0, kSmemGrid) + (grid_u8(grid, i1, kSmemGrid) << 16);
   }
 }
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(1024, 1)
           const float4 d = stage[a];
           const float3 v = align_v(Rp, d.x, d.y, d.z);
           // u_y is shared by all ay; the opaque XOR keeps the row offset an ALU add per angle
-          const unsigned yk = (g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny)) ^ dp.opaque0;
+          const unsigned yk = (g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny + 1)) ^ dp.opaque0;
           unit_atom<G, kConst, kSmemGrid>(v, t, yk, g, grid, strig, iy0, n_a, acc);
         }
       }
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(32)
       for (int a = c0; a < c1; ++a) {
         const float4 d = __ldg(bt.atoms + a0 + a);
         const float3 v = align_v(Rp, d.x, d.y, d.z);
-        const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny);
+        const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny + 1);
         unit_atom<G, kConst, false>(v, t, yk, g, pk.grid, strig, iy0, n_a, acc);
       }
       const int bias = 128 * (c1 - c0);

@@ -19,12 +19,13 @@ int align_warp_smem_bytes_host(int N);
 void launch_align_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                           AlignOut out, int *queue, int grid_in_smem, int blocks, int warps, size_t smem,
                           cudaStream_t st);
-void launch_optimize_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
-                             const uint32_t *keys, OptOut out, int *queue, int blocks, int warps, size_t smem,
-                             cudaStream_t st);
-size_t optimize_warp_smem_bytes();
-size_t optimize_cta_smem_bytes(int n_patoms, int nb);
-int optimize_blocks_per_sm(int warps, size_t smem);
+void launch_torsion_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
+                            const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st);
+void launch_select_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const uint32_t *keys,
+                           OptOut out, int *queue, int blocks, size_t smem, cudaStream_t st);
+size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap);
+int torsion_blocks_per_sm();
+int select_blocks_per_sm(size_t smem);
 void launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
                           cudaStream_t st);
 size_t latency_rec_bytes();
@@ -82,7 +83,7 @@ struct ds_ctx {
   float2 *trig = nullptr;       // 360 (cos, sin)
   // batch-sized device buffers
   DevBuf b_atom_off, b_atoms, b_frag_off, b_frags, b_idh, b_order_a, b_order_o, b_keys, b_res, b_rrec, b_rtors,
-      b_coords, b_btors, b_queue, b_scratch, b_lat_scores, b_lat_recs, b_lat_done;
+      b_coords, b_btors, b_queue, b_scratch, b_rgv, b_lat_scores, b_lat_recs, b_lat_done;
   // pinned host staging
   void *h_stage = nullptr;
   size_t h_cap = 0;
@@ -117,6 +118,7 @@ struct ds_pocket {
   ds_ctx *ctx = nullptr;
   PocketView view{};
   uint8_t *d_grid = nullptr;
+  uint8_t *d_lut = nullptr;
   float4 *d_patoms = nullptr;
   int32_t *d_wfx = nullptr;
   float cutoff = 0.f;
@@ -187,7 +189,7 @@ void ds_destroy(ds_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   DevBuf *bufs[] = {&c->b_atom_off, &c->b_atoms, &c->b_frag_off, &c->b_frags, &c->b_idh, &c->b_order_a,
                     &c->b_order_o, &c->b_keys, &c->b_res, &c->b_rrec, &c->b_rtors, &c->b_coords, &c->b_btors,
-                    &c->b_queue, &c->b_scratch, &c->b_lat_scores, &c->b_lat_recs, &c->b_lat_done};
+                    &c->b_queue, &c->b_scratch, &c->b_rgv, &c->b_lat_scores, &c->b_lat_recs, &c->b_lat_done};
   for (DevBuf *b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->trig) cudaFree(c->trig);
@@ -267,6 +269,9 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
   v.g.nx = d->dims[0];
   v.g.ny = d->dims[1];
   v.g.nz = d->dims[2];
+  v.g.bx = (unsigned)(NX - 1);
+  v.g.by = (unsigned)(NY - 1);
+  v.g.bz = (unsigned)(NZ - 1);
   v.g.NX = (unsigned)NX;
   v.g.NXY = (unsigned)(NX * NY);
   v.grid_bytes = gbytes;
@@ -282,6 +287,35 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
     v.ub2[b] = (float)(ub * ub);  // P11
   }
   p->cutoff = d->bin_ub[d->n_bins - 1];
+  // exact bin LUT (P11): with S = the common count of trailing zero bits of the squared bounds,
+  // d2 >= ub2_b  <=>  bits(d2) >> S >= bits(ub2_b) >> S  for every d2 >= +0 (and NaN -> beyond)
+  std::vector<uint8_t> lut;
+  {
+    int S = 23;
+    for (int b = 0; b < d->n_bins; ++b) {
+      uint32_t u;
+      memcpy(&u, &v.ub2[b], 4);
+      if (u) S = std::min(S, __builtin_ctz(u));
+    }
+    uint32_t ul;
+    memcpy(&ul, &v.ub2[d->n_bins - 1], 4);
+    const uint32_t cap = ul >> S;
+    v.lut_shift = S;
+    v.lut_cap = -1;
+    if (cap < 4096) {
+      lut.resize(cap + 1);
+      for (uint32_t k = 0; k <= cap; ++k) {
+        int n = 0;
+        for (int b = 0; b < d->n_bins; ++b) {
+          uint32_t u;
+          memcpy(&u, &v.ub2[b], 4);
+          n += (u >> S) <= k;
+        }
+        lut[k] = (uint8_t)n;
+      }
+      v.lut_cap = (int)cap;
+    }
+  }
   // pocket atoms in the grid frame: f32((p - o) / s) evaluated in f64 (P11)
   std::vector<float4> pa(std::max(d->n_atoms, 1));
   for (int j = 0; j < d->n_atoms; ++j) {
@@ -314,6 +348,15 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
     return fail(DS_ERR_OOM, "pocket allocation failed");
   }
   c->allocs += 3;
+  if (!lut.empty()) {
+    if (cudaMalloc(&p->d_lut, lut.size()) != cudaSuccess) {
+      ds_pocket_destroy(p);
+      return fail(DS_ERR_OOM, "pocket allocation failed");
+    }
+    c->allocs += 1;
+    cudaMemcpy(p->d_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice);
+  }
+  v.bin_lut = p->d_lut;
   cudaMemcpy(p->d_grid, g8.data(), gbytes, cudaMemcpyHostToDevice);
   cudaMemcpy(p->d_patoms, pa.data(), pa.size() * sizeof(float4), cudaMemcpyHostToDevice);
   cudaMemcpy(p->d_wfx, w.data(), w.size() * 4, cudaMemcpyHostToDevice);
@@ -350,6 +393,7 @@ void ds_pocket_destroy(ds_pocket *p) {
   if (p->d_grid) cudaFree(p->d_grid);
   if (p->d_patoms) cudaFree(p->d_patoms);
   if (p->d_wfx) cudaFree(p->d_wfx);
+  if (p->d_lut) cudaFree(p->d_lut);
   delete p;
 }
 
@@ -512,23 +556,23 @@ int upload_batch(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
   return DS_OK;
 }
 
-int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, const DockParams &dp, bool want_coords,
-                      bool want_btors, bool want_rrec, ds_stats *st, cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2,
-                      int *queue);
+int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t atom_base, int64_t n_atoms_range,
+                      const DockParams &dp, bool want_coords, bool want_btors, bool want_rrec, ds_stats *st,
+                      cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2, int *queue);
 
 int run_batched(ds_ctx *c, const ds_pocket *pk, int L, int NA, int NF, const DockParams &dp, bool want_coords,
                 bool want_btors, bool want_rrec, ds_stats *st) {
   int *queue = (int *)c->b_queue.p;
   DS_CUDA(cudaMemsetAsync(queue, 0, 256, c->stream));
-  return run_batched_range(c, pk, 0, L, dp, want_coords, want_btors, want_rrec, st, c->ev[1], c->ev[2], c->ev[3],
-                           queue);
+  return run_batched_range(c, pk, 0, L, 0, NA, dp, want_coords, want_btors, want_rrec, st, c->ev[1], c->ev[2],
+                           c->ev[3], queue);
 }
 
 // Batched family on ligands [L0, L1) of the resident batch (absolute atom/fragment offsets; the
 // per-ligand outputs and the order arrays are offset by L0).
-int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, const DockParams &dp, bool want_coords,
-                      bool want_btors, bool want_rrec, ds_stats *st, cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2,
-                      int *queue) {
+int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t atom_base, int64_t n_atoms_range,
+                      const DockParams &dp, bool want_coords, bool want_btors, bool want_rrec, ds_stats *st,
+                      cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2, int *queue) {
   BatchView bt;
   bt.L = L1 - L0;
   bt.atom_off = (const int *)c->b_atom_off.p + L0;
@@ -549,24 +593,28 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, const Dock
   launch_align_batched(pk->view, bt, dp, (const int *)c->b_order_a.p + L0, ao, queue, in_smem, c->sm_count, warps_a,
                        smem_a, c->stream);
   cudaEventRecord(e1, c->stream);
-  // --- optimisation + select + rescore: warp per ligand, persistent, occupancy-sized ---
-  const int warps_o = 8;
-  const size_t smem_o = optimize_cta_smem_bytes(pk->view.n_atoms, pk->view.nb) + optimize_warp_smem_bytes() * warps_o;
-  const int per_sm = std::max(1, optimize_blocks_per_sm(warps_o, smem_o));
-  const int blocks_o = c->sm_count * per_sm;
+  // --- torsion optimisation, then select + rescore: warp per ligand, persistent, occupancy-sized ---
+  const int blocks_t = c->sm_count * std::max(1, torsion_blocks_per_sm());
+  const size_t smem_s = select_cta_smem_bytes(pk->view.n_atoms, pk->view.nb, pk->view.lut_cap);
+  const int blocks_s = c->sm_count * std::max(1, select_blocks_per_sm(smem_s));
   int rc;
-  if ((rc = c->ensure(c->b_scratch, sizeof(float4) * (size_t)blocks_o * warps_o * dp.N * DS_MAX_ATOMS))) return rc;
+  if ((rc = c->ensure(c->b_scratch, sizeof(float4) * (size_t)dp.N * (size_t)n_atoms_range)) ||
+      (rc = c->ensure(c->b_rgv, sizeof(int) * (size_t)dp.N * (size_t)(L1 - L0))))
+    return rc;
   OptOut oo;
   oo.res = (ds_result *)c->b_res.p + L0;
   oo.rrec = want_rrec ? (ds_restart_record *)c->b_rrec.p + (size_t)L0 * dp.N : nullptr;
   oo.rtors = (uint8_t *)c->b_rtors.p;
   oo.final_u = (float4 *)c->b_scratch.p;
+  oo.rgv = (int *)c->b_rgv.p;
+  oo.atom_base = atom_base;
   oo.best_coords = want_coords ? (float *)c->b_coords.p : nullptr;
   oo.best_tors = want_btors ? (uint8_t *)c->b_btors.p : nullptr;
-  launch_optimize_batched(pk->view, bt, dp, (const int *)c->b_order_o.p + L0, ao.keys, oo, queue + 16, blocks_o,
-                          warps_o, smem_o, c->stream);
+  launch_torsion_batched(pk->view, bt, dp, (const int *)c->b_order_o.p + L0, ao.keys, oo, queue + 16, blocks_t,
+                         c->stream);
+  launch_select_batched(pk->view, bt, dp, ao.keys, oo, queue + 32, blocks_s, smem_s, c->stream);
   cudaEventRecord(e2, c->stream);
-  if (st) st->launches += 2;
+  if (st) st->launches += 3;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(DS_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return DS_OK;
@@ -718,9 +766,9 @@ int dock_pipelined(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const
   for (int k = 0; k < nch; ++k) {
     const int L0 = bounds[k], L1 = bounds[k + 1];
     DS_CUDA(cudaStreamWaitEvent(c->stream, c->pev[4 * k], 0));
-    if ((rc = run_batched_range(c, pk, L0, L1, dp, out->best_coords != nullptr, out->best_torsion != nullptr,
-                                out->restarts != nullptr, st, c->pev[4 * k + 1], c->pev[4 * k + 2], c->pev[4 * k + 3],
-                                queue + 64 * k)))
+    if ((rc = run_batched_range(c, pk, L0, L1, b->atom_off[L0], (int64_t)b->atom_off[L1] - b->atom_off[L0], dp,
+                                out->best_coords != nullptr, out->best_torsion != nullptr, out->restarts != nullptr,
+                                st, c->pev[4 * k + 1], c->pev[4 * k + 2], c->pev[4 * k + 3], queue + 64 * k)))
       return rc;
     DS_CUDA(cudaStreamWaitEvent(cs, c->pev[4 * k + 3], 0));
     const size_t a0 = b->atom_off[L0], a1 = b->atom_off[L1], f0 = b->frag_off[L0], f1 = b->frag_off[L1];
@@ -815,7 +863,8 @@ int ds_ctx_reserve(ds_ctx *c, int max_ligands, int max_atoms, int max_frags, con
   if ((rc = reserve_buffers(c, max_ligands, max_atoms, max_frags, DS_MAX_RESTARTS)) ||
       (rc = c->ensure(c->b_lat_scores, 4 * L * N * na * na)) ||
       (rc = c->ensure(c->b_lat_recs, latency_rec_bytes() * L * N)) || (rc = c->ensure(c->b_lat_done, 4 * L)) ||
-      (rc = c->ensure(c->b_scratch, sizeof(float4) * L * N * DS_MAX_ATOMS)) ||
+      (rc = c->ensure(c->b_scratch, sizeof(float4) * std::max(L * DS_MAX_ATOMS, (size_t)max_atoms) * N)) ||
+      (rc = c->ensure(c->b_rgv, sizeof(int) * L * N)) ||
       (rc = c->ensure_host((size_t)max_atoms * 16 + (size_t)max_frags * 32 + L * 32 + 4096)))
     return rc;
   return DS_OK;

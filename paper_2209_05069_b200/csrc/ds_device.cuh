@@ -53,13 +53,15 @@ __device__ __forceinline__ float3 apply_mt(const float *M, const float *t, float
 struct GridGeom {
   int nx, ny, nz;          // interior dims
   unsigned NX, NXY;        // padded row / plane pitch: nx+2, (nx+2)(ny+2)
+  unsigned bx, by, bz;     // nx+1, ny+1, nz+1: index of the far halo plane (the clamp bound)
 };
-__device__ __forceinline__ unsigned clamp_bits(float u, int n) {
+// bound = n + 1
+__device__ __forceinline__ unsigned clamp_bits(float u, unsigned bound) {
   const unsigned b = (unsigned)__float_as_int(__fadd_rn(u, kMagic)) - (unsigned)(kMagicBits - 1);
-  return min(b, (unsigned)(n + 1));
+  return min(b, bound);
 }
 __device__ __forceinline__ int node_index(const GridGeom &g, float ux, float uy, float uz) {
-  return (int)(clamp_bits(ux, g.nx) + g.NX * clamp_bits(uy, g.ny) + g.NXY * clamp_bits(uz, g.nz));
+  return (int)(clamp_bits(ux, g.bx) + g.NX * clamp_bits(uy, g.by) + g.NXY * clamp_bits(uz, g.bz));
 }
 
 // ---- P5: starting pose parameters of restart r: R0s = (Rz(g) (x) (Ry(b) (x) Rx(a))) * inv_s,

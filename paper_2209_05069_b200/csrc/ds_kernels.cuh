@@ -15,6 +15,10 @@ struct PocketView {
   const int32_t *wfx;        // [16][16][nb+1] fixed-point table*mult (2^-24); entry nb = 0
   int nb;
   float ub2[DS_MAX_BINS];    // squared bin upper bounds, grid frame
+  // bin look-up table, exact when every ub2 has its low lut_shift bits zero (the defaults do):
+  // bin = bin_lut[min(bits(d2) >> lut_shift, lut_cap)]; lut_cap < 0: no table (compare path)
+  const uint8_t *bin_lut;
+  int lut_shift, lut_cap;
   const float2 *trig;        // (cos, sin) of integer degrees 0..359 (f32 of f64)
 };
 
@@ -50,7 +54,10 @@ struct OptOut {
   ds_result *res;            // L
   ds_restart_record *rrec;   // L*N (may be null)
   uint8_t *rtors;            // frag_total*N (always)
-  float4 *final_u;           // scratch: per ligand slot? no: per global warp N*160
+  float4 *final_u;           // final poses. latency: (lig*N + r)*DS_MAX_ATOMS; batched: per ligand,
+                             // ((atom_off - atom_base)*N + r*A)
+  int *rgv;                  // batched: L*N (final geom << 1) | valid
+  long long atom_base;       // batched: first atom of the launch range
   float *best_coords;        // atom_total*3 (may be null)
   uint8_t *best_tors;        // frag_total (may be null)
 };

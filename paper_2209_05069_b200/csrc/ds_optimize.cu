@@ -1,45 +1,59 @@
 // Pose optimisation, pose selection and rescoring (Alg. 1 lines 10-21, PAPER.md:227-247;
-// SPEC.md:257-285) — batched family, one warp per ligand.
+// SPEC.md:257-285) — batched family, one warp per ligand, as two kernels so
+// each gets the whole register file for its own loop nest:
 //
-// Per restart the warp rebuilds the aligned pose from the packed argmax key of the alignment
-// kernel, then walks the fragments in list order (they are stateful).  Per
-// fragment:
-//  * ballots compact the moving set M and the bump-relevant complement C' (not M, not an axis atom);
+// k_torsion_batched — per restart the warp rebuilds the aligned pose from the packed argmax key of
+// the alignment kernel, then walks the fragments in list order (they are stateful,
+// PAPER.md:278-279).  Per fragment:
+//  * ballots compact the moving set M (positions into a per-fragment record array) and the
+//    bump-relevant complement C' (not M, not an axis atom);
 //  * bump candidates: a torsion keeps each moving atom on its circle about the axis, so (i, j)
 //    can only bump if the distance between i's circle and j — sqrt(dh^2 + dr^2) in cylindrical
 //    coordinates about the axis — is below the bump distance.  Pairs failing that bound (with a
 //    0.02-node margin that dwarfs f32 rounding) are resolved once per fragment instead of once per
-//    angle; the survivors (~1.5 % of pairs on the config-3 mix) form a CSR candidate list per
-//    moving atom and are checked exactly with P9 for every angle;
+//    angle; the survivors (~1.5 % of pairs on the config-3 mix) are recorded with the moving atom
+//    (three inline, the rest in a short per-fragment list) and checked exactly with P9 per angle;
 //  * all torsion angles at once: lanes own (angle, moving atom) slots, rotate their atom in
 //    registers and test its candidates; a hit marks the angle bumped, clean slots add their grid
-//    value (exact integer smem adds) to base + sum over M (non-moving atoms do not change);
+//    value to base + sum over M (non-moving atoms do not change);
 //  * the best clean angle (ties -> smallest) is committed.
-// Then select_poses (heavy-atom RMSD in f64, lanes over pose pairs) and an integer fixed-point
-// rescore (order-free, exact) with pocket atoms and weights staged in shared memory.
+// The final pose of every restart goes to a per-ligand slot in HBM (L2-resident in practice).
+//
+// k_select_batched — select_poses (heavy-atom RMSD in f64, lanes over pose pairs) and an integer
+// fixed-point rescore (order-free, exact) with pocket atoms, weights and the bin table staged in
+// shared memory.
 #include "ds_kernels.cuh"
 
 namespace ds {
 
-constexpr int kMaxA = DS_MAX_ATOMS;
-constexpr int kCand = 6;             // bump-candidate slots per moving atom (overflow: full scan)
+constexpr int kMaxA = DS_MAX_ATOMS;  // atom stride of the global final-pose scratch
+constexpr int kInline = 3;           // bump candidates kept inline per moving atom
+constexpr int kOvf = 32;             // per-fragment overflow list of further (moving, candidate) pairs
 constexpr int kOptWarps = 8;         // warps per CTA (one ligand each)
 #ifndef DS_OPT_MIN_BLOCKS
 #define DS_OPT_MIN_BLOCKS 4          // resident CTAs per SM the register budget is sized for
 #endif
 
-struct OptWarpSmem {
+// Per-warp shared scratch of the torsion kernel (53 KB per 8-warp CTA: 4 CTAs per SM).
+struct TorWarpSmem {
   float4 u[kMaxA];          // committed pose of the current restart (grid frame), .w = type
-  float2 chr[kMaxA];        // cylindrical (h, r) of the C' atoms about the fragment axis
-  uint8_t mlist[kMaxA];     // moving atom indices, ascending
+  // moving atoms of the current fragment, ascending: position + an info word
+  //   bits 0-7 bump-candidate count, 8-15 / 16-23 / 24-31 the first three candidates
+  float4 mw[kMaxA];
+  float2 chr[kMaxA];        // cylindrical (h, r): C' atoms in [0, nC), moving atom m at kMaxA-1-m
   uint8_t clist[kMaxA];     // complement atom indices, ascending
-  uint8_t cl[kMaxA][kCand]; // bump-candidate atom indices per moving atom
-  unsigned cnw[kMaxA / 4];  // candidate counts, one byte per moving atom (> kCand: scan all of C')
+  uint16_t ovf[kOvf];       // candidates beyond kInline: moving slot << 8 | atom index
+  int n_ovf;                // entries appended (> kOvf: the list overflowed, scan C')
+};
+
+// Per-warp shared scratch of the select/rescore kernel.
+struct SelWarpSmem {
+  float4 u[kMaxA];          // the pose being rescored (grid frame), .w = weight-table row offset
   int geom[DS_MAX_RESTARTS];
-  int valid[DS_MAX_RESTARTS];
   unsigned dis[DS_MAX_RESTARTS];   // dissimilarity bitsets (select_poses)
-  int ord[DS_MAX_RESTARTS];
-  int kept[DS_MAX_RESTARTS];
+  uint8_t valid[DS_MAX_RESTARTS];
+  uint8_t ord[DS_MAX_RESTARTS];
+  uint8_t kept[DS_MAX_RESTARTS];
 };
 
 __device__ __forceinline__ int grid_val(const PocketView &pk, int idx) { return (int)__ldg(pk.grid + idx) - 128; }
@@ -81,14 +95,18 @@ __device__ __forceinline__ float3 torsion_pos(const PocketView &pk, int step_t, 
 // rescore sum of one pose against all pocket atoms (P11).  Lanes own pocket atoms (staged in
 // smem with .w = the integer column offset tj*(nb+1)); ligand atoms are broadcast from S.u whose
 // .w holds the integer row offset ti*16*(nb+1).  Partial sums stay in int32 for <= 64 atoms
-// (|W| <= 2^24) before widening.
-template <int NB>
-__device__ __forceinline__ long long rescore_pose(const OptWarpSmem &S, int A, const float4 *pat, int P,
-                                                  const int32_t *wfx, int nb, const float *ub2) {
+// (|W| <= 2^24) before widening.  The bin comes from the exact look-up table (3 instructions:
+// shift, unsigned min, LDS) when the pocket has one, else from NB compares.
+template <int NB, class SM>
+__device__ __forceinline__ long long rescore_pose(const SM &S, int A, const float4 *pat, int P,
+                                                  const int32_t *wfx, int nb, const float *ub2,
+                                                  const uint8_t *lut, int lut_shift, int lut_cap) {
   long long acc = 0;
   float u[DS_MAX_BINS];
+  if (NB >= 0) {
 #pragma unroll
-  for (int q = 0; q < DS_MAX_BINS; ++q) u[q] = ub2[q];
+    for (int q = 0; q < DS_MAX_BINS; ++q) u[q] = ub2[q];
+  }
   for (int j0 = 0; j0 < P; j0 += 32) {
     const int j = j0 + (threadIdx.x & 31);
     // past-the-end lanes use a far sentinel: its bin is nb, whose weight is 0
@@ -101,7 +119,10 @@ __device__ __forceinline__ long long rescore_pose(const OptWarpSmem &S, int A, c
         const float4 x = S.u[i];
         const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
         int b = __float_as_int(x.w);
-        if (NB > 0) {
+        if (NB < 0) {
+          // d2 >= +0 (never -0), so bits order is value order; NaN/inf clamp to the last entry (nb)
+          b += lut[min((unsigned)__float_as_int(d2) >> lut_shift, (unsigned)lut_cap)];
+        } else if (NB > 0) {
           // bin = #{q : !(d2 < u_q)}; d2 >= +0 and u_q > 0, so float order == bit order and
           // (bits(d2) - bits(u_q)) >> 31 is -1 exactly when d2 < u_q (NaN/inf count as beyond)
           const int d2b = __float_as_int(d2);
@@ -120,14 +141,16 @@ __device__ __forceinline__ long long rescore_pose(const OptWarpSmem &S, int A, c
 }
 
 // cold paths kept out of line so the hot loops stay compact in the instruction cache
-__device__ __noinline__ long long rescore_pose_generic(const OptWarpSmem &S, int A, const float4 *pat, int P,
+template <class SM>
+__device__ __noinline__ long long rescore_pose_generic(const SM &S, int A, const float4 *pat, int P,
                                                        const int32_t *wfx, int nb, const float *ub2) {
-  return rescore_pose<0>(S, A, pat, P, wfx, nb, ub2);
+  return rescore_pose<0, SM>(S, A, pat, P, wfx, nb, ub2, nullptr, 0, 0);
 }
 
 // select_poses (P12) dissimilarity bitsets: pairs (p < q) of valid poses over lanes; heavy-atom sum
 // of squared deltas in f64, in atom order (same order as the oracle)
-__device__ __noinline__ void pose_dissimilarity(OptWarpSmem &S, const float4 *scr, int A, int N, int heavy,
+template <class SM>
+__device__ __noinline__ void pose_dissimilarity(SM &S, const float4 *scr, int A, int N, int heavy,
                                                 double thr2) {
   const int npairs = N * (N - 1) / 2;
   for (int pidx = threadIdx.x & 31; pidx < npairs; pidx += 32) {
@@ -139,7 +162,7 @@ __device__ __noinline__ void pose_dissimilarity(OptWarpSmem &S, const float4 *sc
     const int q = p + 1 + rem;
     if (!S.valid[p] || !S.valid[q]) continue;
     double sum = 0.0;
-    const float4 *up = scr + (size_t)p * kMaxA, *uq = scr + (size_t)q * kMaxA;
+    const float4 *up = scr + (size_t)p * A, *uq = scr + (size_t)q * A;
     for (int i = 0; i < A; ++i) {
       const float4 x = up[i], y = uq[i];
       if (x.w == 0.f) continue;
@@ -158,32 +181,37 @@ __device__ __noinline__ void pose_dissimilarity(OptWarpSmem &S, const float4 *sc
   }
 }
 
-__global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
-    k_optimize_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
-                       OptOut out, int *queue) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  // per-CTA: pocket atoms + fixed-point weights + bin bounds, then the per-warp scratch
-  const int nb1 = pk.nb + 1;
-  float4 *s_pat = reinterpret_cast<float4 *>(smem);
-  int32_t *s_w = reinterpret_cast<int32_t *>(s_pat + pk.n_atoms);
-  const int wsz = DS_N_TYPES * DS_N_TYPES * nb1;
-  float *s_ub2 = reinterpret_cast<float *>(s_w + wsz);
-  // per-warp scratch is a static array: its address is a compile-time base + warp * stride, so the
-  // compiler never has to rematerialise it from launch parameters inside the hot loops
-  __shared__ OptWarpSmem s_warp[kOptWarps];
-  OptWarpSmem &S = s_warp[warp];
-  for (int j = threadIdx.x; j < pk.n_atoms; j += blockDim.x) {
-    float4 y = __ldg(pk.patoms + j);
-    y.w = __int_as_float((int)y.w * nb1);  // column offset of the pocket atom's type in the weight table
-    s_pat[j] = y;
+// minimum squared distance from q to the bump candidates of moving slot m beyond the inline ones:
+// the fragment's overflow list, or every prefiltered C' atom when that list overflowed (cold path)
+__device__ __forceinline__ float overflow_min(const TorWarpSmem &S, int m, int n_ovf, int nCf, float3 q) {
+  float mind = __int_as_float(0x7f800000);
+  if (n_ovf <= kOvf) {
+#pragma unroll 1
+    for (int t = 0; t < n_ovf; ++t) {
+      const unsigned e = S.ovf[t];
+      if ((int)(e >> 8) == m) {
+        const float4 y = S.u[e & 0xFFu];
+        mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < nCf; ++c) {
+      const float4 y = S.u[S.clist[c]];
+      mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+    }
   }
-  for (int j = threadIdx.x; j < wsz; j += blockDim.x) s_w[j] = __ldg(pk.wfx + j);
-  if (threadIdx.x < DS_MAX_BINS) s_ub2[threadIdx.x] = pk.ub2[threadIdx.x];
-  __syncthreads();
+  return mind;
+}
 
-  const int gwarp = blockIdx.x * nwarps + warp;
-  float4 *scr = out.final_u + (size_t)gwarp * dp.N * kMaxA;  // final poses of the N restarts
+__global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
+    k_torsion_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
+                      OptOut out, int *queue) {
+  // per-warp scratch at a compile-time offset of the shared window (nothing to rematerialise from
+  // launch parameters); dynamic because it exceeds the 48 KB static limit
+  extern __shared__ __align__(16) TorWarpSmem s_warp[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  TorWarpSmem &S = s_warp[warp];
   const GridGeom g = pk.g;
   const unsigned lt = lanemask_lt();
 
@@ -200,7 +228,7 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
     const uint64_t idh = bt.idh[lig];
     unsigned pairs_total = 0, early_exits = 0, evals = 0;
     bool degenerate = false;
-    int heavy = 0;
+    float4 *fin = out.final_u + (size_t)(a0 - out.atom_base) * dp.N;  // final poses, restart r at r*A
 
     for (int r = 0; r < dp.N && !degenerate; ++r) {
       // ---- rebuild the aligned pose from the argmax key (P6) ----
@@ -226,23 +254,25 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
       for (int f = 0; f < F; ++f) {
         const uint4 fa = __ldg(bt.frags + 2 * (size_t)(f0 + f));
         const uint4 fb = __ldg(bt.frags + 2 * (size_t)(f0 + f) + 1);
-        const unsigned mw[5] = {fa.x, fa.y, fa.z, fa.w, fb.x};
+        const unsigned mw5[5] = {fa.x, fa.y, fa.z, fa.w, fb.x};
         const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
+        // compaction of the moving set M (positions into mw) and of the bump-relevant complement C'
+        // (not M, not an axis atom); base = grid score of the atoms the torsion does not move
         int nM = 0, nC = 0, base = 0;
 #pragma unroll
         for (int s = 0; s < 5; ++s) {
           if (s * 32 >= A) break;
           const int i = s * 32 + lane;
           const bool in = i < A;
-          const bool mv = in && ((mw[s] >> lane) & 1u);
+          const bool mv = in && ((mw5[s] >> lane) & 1u);
           const bool cp = in && !mv && i != ab && i != ae;
           const unsigned bm = __ballot_sync(kFull, mv), bc = __ballot_sync(kFull, cp);
-          if (mv) S.mlist[nM + __popc(bm & lt)] = (uint8_t)i;
-          if (cp) S.clist[nC + __popc(bc & lt)] = (uint8_t)i;
-          if (in && !mv) {
+          if (in) {
             const float4 p = S.u[i];
-            base += grid_val(pk, node_index(g, p.x, p.y, p.z));
+            if (mv) S.mw[nM + __popc(bm & lt)] = make_float4(p.x, p.y, p.z, 0.f);  // info word = 0
+            else base += grid_val(pk, node_index(g, p.x, p.y, p.z));
           }
+          if (cp) S.clist[nC + __popc(bc & lt)] = (uint8_t)i;
           nM += __popc(bm);
           nC += __popc(bc);
         }
@@ -264,15 +294,17 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
         __syncwarp();
         // ---- bump candidates per moving atom: cylindrical coordinates of C' in chr[0, nC) and of M
         // in chr[kMaxA-1-m] (nM + nC <= A - 2), then every (m, c) pair tested by a flat lane loop;
-        // survivors are appended with byte-packed shared atomics (order is irrelevant: only the
-        // minimum distance is used) ----
+        // survivors are counted into the moving atom's info word, the first kInline of them are kept
+        // inline and the rest go to a short per-fragment overflow list (their order is irrelevant:
+        // only the minimum distance is used).
         // The (h, r) box of M grown by the culling radius prefilters C': an atom outside it is
         // farther than the radius from every moving atom's circle, so it can never bump and is
-        // dropped from the pair loop, the candidate lists and the overflow scan (nCf <= nC; the
-        // P14 counters still count all nC complement atoms).
+        // dropped from the pair loop and the overflow scan (nCf <= nC; the P14 counters still count
+        // all nC complement atoms).
         int hlo = 0x7FFFFFFF, hhi = (int)0x80000000, rhi = 0;
+        if (lane == 0) S.n_ovf = 0;
         for (int m = lane; m < nM; m += 32) {
-          const float2 hr = cyl_coords(S.u[S.mlist[m]], a3, kx, ky, kz);
+          const float2 hr = cyl_coords(S.mw[m], a3, kx, ky, kz);
           S.chr[kMaxA - 1 - m] = hr;
           hlo = min(hlo, ordered_bits(hr.x));
           hhi = max(hhi, ordered_bits(hr.x));
@@ -301,7 +333,6 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
           }
           nCf += __popc(bk);
         }
-        for (int w = lane; w < (nM + 3) / 4; w += 32) S.cnw[w] = 0u;
         __syncwarp();
         {
           const unsigned total = (unsigned)nM * (unsigned)nCf;
@@ -316,9 +347,15 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
               const float2 hm = S.chr[kMaxA - 1 - pm], hc = S.chr[pc];
               const float dh = hm.x - hc.x, dr = hm.y - hc.y;
               if (dh * dh + dr * dr < dp.cull2) {
-                const unsigned sh = 8u * (pm & 3);
-                const unsigned k = (atomicAdd(&S.cnw[pm >> 2], 1u << sh) >> sh) & 0xFFu;
-                if (k < (unsigned)kCand) S.cl[pm][k] = S.clist[pc];
+                unsigned *info = reinterpret_cast<unsigned *>(&S.mw[pm].w);
+                const unsigned k = atomicAdd(info, 1u) & 0xFFu;  // count <= nCf < 256: no carry
+                const unsigned ci = S.clist[pc];
+                if (k < (unsigned)kInline) {
+                  atomicOr(info, ci << (8 + 8 * k));
+                } else {
+                  const int slot = atomicAdd(&S.n_ovf, 1);
+                  if (slot < kOvf) S.ovf[slot] = (uint16_t)((pm << 8) | ci);
+                }
               }
             }
             pm += dm;
@@ -331,8 +368,12 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
         }
         unsigned best_key = 0;  // (score + 32768) << 16 | (65535 - angle); 0 = no clean angle
         __syncwarp();
+        const int n_ovf = S.n_ovf;
         // ---- all angles at once: lane = (angle a, moving-atom group gi); the lane keeps its angle's
         // rotation, bump flag and partial score in registers over moving atoms m = gi, gi+G, ...
+        // Angle 0 (the identity, P7) runs the same code with R = I about the origin: w = p - 0 = p and
+        // fma(0, ., fma(0, ., fma(1, p, 0))) = p up to the sign of a zero, which changes neither a
+        // node nor a squared distance (and angle 0 is never committed).
         for (int k0 = 0; k0 < dp.n_t; k0 += 32) {
           const int nA = min(32, dp.n_t - k0);
           const int G = 32 / nA;                  // moving-atom groups per round
@@ -341,10 +382,12 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
           const int kang = k0 + a;
           unsigned same = 0;                      // lanes that share this lane's angle
           for (int t = 0; t < G; ++t) same |= 1u << (a + t * nA);
-          float R[9];
+          float R[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
+          float3 ar = make_float3(0.f, 0.f, 0.f);
           if (kang > 0) {
             const float2 cs = pk.trig[kang * dp.step_t];
             torsion_matrix(kx, ky, kz, cs.x, cs.y, R);
+            ar = a3;
           }
           bool bumped = false;
           int part = 0, nact = 0;
@@ -356,23 +399,25 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
             if (!__any_sync(kFull, act)) break;
             bool hit = false;
             if (act) {
-              const float4 p = S.u[S.mlist[m]];
-              const float3 q = kang == 0 ? make_float3(p.x, p.y, p.z) : torsion_apply(R, a3, p.x, p.y, p.z);
+              const float4 W = S.mw[m];
+              const float3 q = torsion_apply(R, ar, W.x, W.y, W.z);
               const int gv = grid_val(pk, node_index(g, q.x, q.y, q.z));  // issued early: hides L2 latency
-              float mind = __int_as_float(0x7f800000);  // min squared distance (P9: bump iff < bd2)
-              const int cnt = (int)((S.cnw[m >> 2] >> (8 * (m & 3))) & 0xFFu);
-              if (cnt <= kCand) {
-                for (int t = 0; t < cnt; ++t) {
-                  const float4 y = S.u[S.cl[m][t]];
-                  mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+              const unsigned info = __float_as_uint(W.w);
+              const unsigned cnt = info & 0xFFu;
+              if (cnt != 0u) {
+                const float4 y0 = S.u[(info >> 8) & 0xFFu];
+                float mind = dist2(q.x, q.y, q.z, y0.x, y0.y, y0.z);  // min squared distance (P9)
+                if (cnt > 1u) {
+                  const float4 y1 = S.u[(info >> 16) & 0xFFu];
+                  mind = fminf(mind, dist2(q.x, q.y, q.z, y1.x, y1.y, y1.z));
+                  if (cnt > 2u) {
+                    const float4 y2 = S.u[info >> 24];
+                    mind = fminf(mind, dist2(q.x, q.y, q.z, y2.x, y2.y, y2.z));
+                    if (cnt > (unsigned)kInline) mind = fminf(mind, overflow_min(S, m, n_ovf, nCf, q));
+                  }
                 }
-              } else {
-                for (int c = 0; c < nCf; ++c) {
-                  const float4 y = S.u[S.clist[c]];
-                  mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
-                }
+                hit = mind < dp.bd2;
               }
-              hit = mind < dp.bd2;
               if (!hit) part += gv;
               ++nact;
             }
@@ -403,13 +448,21 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
           best_key = max(best_key, __reduce_max_sync(kFull, kk));
         }
         const int best_k = best_key ? 65535 - (int)(best_key & 0xFFFFu) : -1;
-        // commit the winner before the next fragment
+        // commit the winner before the next fragment; moving slot m of atom i is its rank in the mask
         if (best_k > 0) {
-          for (int m = lane; m < nM; m += 32) {
-            const int i = S.mlist[m];
-            const float4 p = S.u[i];
-            const float3 q = torsion_pos(pk, dp.step_t, best_k, kx, ky, kz, a3, p);
-            S.u[i] = make_float4(q.x, q.y, q.z, p.w);
+          const uint4 ga = __ldg(bt.frags + 2 * (size_t)(f0 + f));
+          const unsigned gm[5] = {ga.x, ga.y, ga.z, ga.w, __ldg(bt.frags + 2 * (size_t)(f0 + f) + 1).x};
+          int mr = 0;
+          for (int s = 0; s < 5 && s * 32 < A; ++s) {
+            const int i = s * 32 + lane;
+            const bool mv = i < A && ((gm[s] >> lane) & 1u);
+            const unsigned bm = __ballot_sync(kFull, mv);
+            if (mv) {
+              const float4 W = S.mw[mr + __popc(bm & lt)];
+              const float3 q = torsion_pos(pk, dp.step_t, best_k, kx, ky, kz, a3, W);
+              S.u[i] = make_float4(q.x, q.y, q.z, S.u[i].w);
+            }
+            mr += __popc(bm);
           }
         }
         if (best_k < 0) ++all_bumped;
@@ -419,19 +472,15 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
       if (degenerate) break;
       // final geometric score + store the final pose
       int sc = 0;
-      int hv = 0;
       for (int i = lane; i < A; i += 32) {
         const float4 p = S.u[i];
         sc += grid_val(pk, node_index(g, p.x, p.y, p.z));
-        scr[(size_t)r * kMaxA + i] = p;
-        hv += p.w != 0.f;
+        fin[(size_t)r * A + i] = p;
       }
       sc = warp_sum(sc);
-      heavy = warp_sum(hv);
       const int valid = !(F >= 1 && all_bumped == F);  // P10
       if (lane == 0) {
-        S.geom[r] = sc;
-        S.valid[r] = valid;
+        out.rgv[(size_t)lig * dp.N + r] = (sc * 2) | valid;
         if (out.rrec) {
           ds_restart_record rec;
           rec.align_score = align_score;
@@ -447,24 +496,71 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
       __syncwarp();
     }
 
-    ds_result res;
-    res.geom_score = 0;
-    res.chem_fx = 0;
-    res.best_restart = 0;
-    res.best_ax = 0;
-    res.best_ay = 0;
-    res.n_kept = 0;
-    res.poses_scored = (unsigned)(dp.N * dp.n_rot) + evals;
-    res.bump_checks = pairs_total;
-    res.bump_early_exits = early_exits;
-    if (degenerate) {
-      res.status = DS_STATUS_DEGENERATE_AXIS;
-      if (lane == 0) out.res[lig] = res;
-      __syncwarp();
-      continue;
+    // counters and the degenerate status; k_select_batched completes the record
+    if (lane == 0) {
+      ds_result res;
+      res.geom_score = 0;
+      res.chem_fx = 0;
+      res.best_restart = 0;
+      res.best_ax = 0;
+      res.best_ay = 0;
+      res.n_kept = 0;
+      res.poses_scored = (unsigned)(dp.N * dp.n_rot) + evals;
+      res.bump_checks = pairs_total;
+      res.bump_early_exits = early_exits;
+      res.status = degenerate ? DS_STATUS_DEGENERATE_AXIS : DS_STATUS_OK;
+      out.res[lig] = res;
     }
     __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(kOptWarps * 32)
+    k_select_batched(PocketView pk, BatchView bt, DockParams dp, const uint32_t *keys, OptOut out, int *queue) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ SelWarpSmem s_warp[kOptWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  SelWarpSmem &S = s_warp[warp];
+  // per-CTA: pocket atoms + fixed-point weights + bin bounds + bin LUT
+  const int nb1 = pk.nb + 1;
+  float4 *s_pat = reinterpret_cast<float4 *>(smem);
+  int32_t *s_w = reinterpret_cast<int32_t *>(s_pat + pk.n_atoms);
+  const int wsz = DS_N_TYPES * DS_N_TYPES * nb1;
+  float *s_ub2 = reinterpret_cast<float *>(s_w + wsz);
+  uint8_t *s_lut = reinterpret_cast<uint8_t *>(s_ub2 + DS_MAX_BINS);
+  for (int j = threadIdx.x; j < pk.n_atoms; j += blockDim.x) {
+    float4 y = __ldg(pk.patoms + j);
+    y.w = __int_as_float((int)y.w * nb1);  // column offset of the pocket atom's type in the weight table
+    s_pat[j] = y;
+  }
+  for (int j = threadIdx.x; j < wsz; j += blockDim.x) s_w[j] = __ldg(pk.wfx + j);
+  if (threadIdx.x < DS_MAX_BINS) s_ub2[threadIdx.x] = pk.ub2[threadIdx.x];
+  for (int j = threadIdx.x; j <= pk.lut_cap; j += blockDim.x) s_lut[j] = __ldg(pk.bin_lut + j);
+  __syncthreads();
+
+  for (;;) {
+    int lig = 0;
+    if (lane == 0) lig = atomicAdd(queue, 1);
+    lig = __shfl_sync(kFull, lig, 0);
+    if (lig >= bt.L) break;
+    ds_result res = out.res[lig];
+    if (res.status != DS_STATUS_OK) continue;  // DegenerateAxis: already final
+    const int a0 = bt.atom_off[lig];
+    const int A = bt.atom_off[lig + 1] - a0;
+    const int f0 = bt.frag_off[lig];
+    const int F = bt.frag_off[lig + 1] - f0;
+    const float4 *fin = out.final_u + (size_t)(a0 - out.atom_base) * dp.N;
     // ---- select_poses (P12): order valid poses by (geom desc, restart asc) ----
+    for (int r = lane; r < dp.N; r += 32) {
+      const int gv = out.rgv[(size_t)lig * dp.N + r];
+      S.geom[r] = gv >> 1;
+      S.valid[r] = (uint8_t)(gv & 1);
+      S.dis[r] = 0u;
+    }
+    int hv = 0;
+    for (int i = lane; i < A; i += 32) hv += fin[i].w != 0.f;
+    const int heavy = warp_sum(hv);
+    __syncwarp();
     int nvalid = 0;
     for (int r = 0; r < dp.N; ++r) nvalid += S.valid[r];
     if (nvalid == 0) {
@@ -474,16 +570,15 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
       continue;
     }
     for (int r = lane; r < dp.N; r += 32) {
-      int rank = 0;
       if (S.valid[r]) {
+        int rank = 0;
         for (int q = 0; q < dp.N; ++q)
           rank += S.valid[q] && (S.geom[q] > S.geom[r] || (S.geom[q] == S.geom[r] && q < r));
-        S.ord[rank] = r;
+        S.ord[rank] = (uint8_t)r;
       }
-      S.dis[r] = 0u;
     }
     __syncwarp();
-    pose_dissimilarity(S, scr, A, dp.N, heavy, dp.thr2);
+    pose_dissimilarity(S, fin, A, dp.N, heavy, dp.thr2);
     __syncwarp();
     // greedy keep (warp-uniform)
     int nk = 0;
@@ -492,7 +587,7 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
       bool ok = true;
       for (int t = 0; t < nk; ++t) ok = ok && ((S.dis[c] >> S.kept[t]) & 1u);
       if (ok) {
-        if (lane == 0) S.kept[nk] = c;
+        if (lane == 0) S.kept[nk] = (uint8_t)c;
         ++nk;
         __syncwarp();
       }
@@ -504,13 +599,14 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
       const int r = S.kept[t];
       __syncwarp();
       for (int i = lane; i < A; i += 32) {
-        float4 x = scr[(size_t)r * kMaxA + i];
+        float4 x = fin[(size_t)r * A + i];
         x.w = __int_as_float((int)x.w * DS_N_TYPES * nb1);  // row offset of the ligand atom's type
         S.u[i] = x;
       }
       __syncwarp();
-      long long acc = pk.nb == 4 ? rescore_pose<4>(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2)
-                                 : rescore_pose_generic(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2);
+      long long acc = pk.lut_cap >= 0 ? rescore_pose<-1>(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2, s_lut,
+                                                         pk.lut_shift, pk.lut_cap)
+                                      : rescore_pose_generic(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2);
       acc = warp_sum64(acc);
       if (best_r < 0 || acc > best_chem || (acc == best_chem && r < best_r)) {
         best_chem = acc;
@@ -529,7 +625,7 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
     res.n_kept = (uint8_t)nk;
     if (lane == 0) out.res[lig] = res;
     if (out.best_coords) {
-      const float4 *ub = scr + (size_t)best_r * kMaxA;
+      const float4 *ub = fin + (size_t)best_r * A;
       for (int i = lane; i < A; i += 32) {  // back to Å: q = fma(u, s, o)   (P2)
         const float4 x = ub[i];
         float *o = out.best_coords + 3 * (size_t)(a0 + i);
@@ -544,23 +640,37 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
   }
 }
 
-size_t optimize_warp_smem_bytes() { return 0; }  // per-warp scratch is static (kOptWarps per CTA)
-size_t optimize_cta_smem_bytes(int n_patoms, int nb) {
-  size_t fixed = (size_t)n_patoms * 16 + (size_t)DS_N_TYPES * DS_N_TYPES * (nb + 1) * 4 + DS_MAX_BINS * 4;
+size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap) {
+  size_t fixed = (size_t)n_patoms * 16 + (size_t)DS_N_TYPES * DS_N_TYPES * (nb + 1) * 4 + DS_MAX_BINS * 4 +
+                 (size_t)(lut_cap + 1);
   return (fixed + 15) & ~(size_t)15;
 }
 
-void launch_optimize_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
-                             const uint32_t *keys, OptOut out, int *queue, int blocks, int warps, size_t smem,
-                             cudaStream_t st) {
-  cudaFuncSetAttribute(k_optimize_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_optimize_batched<<<blocks, warps * 32, smem, st>>>(pk, bt, dp, order, keys, out, queue);
+constexpr size_t kTorSmem = kOptWarps * sizeof(TorWarpSmem);
+
+void launch_torsion_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
+                            const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st) {
+  cudaFuncSetAttribute(k_torsion_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
+  k_torsion_batched<<<blocks, kOptWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
 }
 
-int optimize_blocks_per_sm(int warps, size_t smem) {
+void launch_select_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const uint32_t *keys,
+                           OptOut out, int *queue, int blocks, size_t smem, cudaStream_t st) {
+  cudaFuncSetAttribute(k_select_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_select_batched<<<blocks, kOptWarps * 32, smem, st>>>(pk, bt, dp, keys, out, queue);
+}
+
+int torsion_blocks_per_sm() {
   int n = 0;
-  cudaFuncSetAttribute(k_optimize_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_optimize_batched, warps * 32, smem);
+  cudaFuncSetAttribute(k_torsion_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_torsion_batched, kOptWarps * 32, kTorSmem);
+  return n;
+}
+
+int select_blocks_per_sm(size_t smem) {
+  int n = 0;
+  cudaFuncSetAttribute(k_select_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_select_batched, kOptWarps * 32, smem);
   return n;
 }
 
