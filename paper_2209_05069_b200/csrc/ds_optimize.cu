@@ -204,6 +204,26 @@ __device__ __forceinline__ float overflow_min(const TorWarpSmem &S, int m, int n
   return mind;
 }
 
+// P9 bump test of a rotated moving atom q against its candidates (info word of its record):
+// true iff some candidate lies strictly closer than the bump distance
+__device__ __forceinline__ bool bump_hit(const TorWarpSmem &S, unsigned info, float3 q, int m, int n_ovf, int nCf,
+                                         float bd2) {
+  const unsigned cnt = info & 0xFFu;
+  if (cnt == 0u) return false;
+  const float4 y0 = S.u[(info >> 8) & 0xFFu];
+  float mind = dist2(q.x, q.y, q.z, y0.x, y0.y, y0.z);  // min squared distance
+  if (cnt > 1u) {
+    const float4 y1 = S.u[(info >> 16) & 0xFFu];
+    mind = fminf(mind, dist2(q.x, q.y, q.z, y1.x, y1.y, y1.z));
+    if (cnt > 2u) {
+      const float4 y2 = S.u[info >> 24];
+      mind = fminf(mind, dist2(q.x, q.y, q.z, y2.x, y2.y, y2.z));
+      if (cnt > (unsigned)kInline) mind = fminf(mind, overflow_min(S, m, n_ovf, nCf, q));
+    }
+  }
+  return mind < bd2;
+}
+
 __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
     k_torsion_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
                       OptOut out, int *queue) {
@@ -391,35 +411,28 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
           }
           bool bumped = false;
           int part = 0, nact = 0;
-          for (int m0 = 0; m0 < nM; m0 += G) {
-            const int m = m0 + gi;
-            const bool valid = lane_ok && m < nM;
+          // two moving atoms per lane and round (m0 + gi and m0 + G + gi): twice the independent work
+          // (two grid loads in flight) for the same loop and retirement overhead
+          for (int m0 = 0; m0 < nM; m0 += 2 * G) {
+            const int m1 = m0 + gi, m2 = m1 + G;
             // with early exit a bumped angle is retired; without it every pair is checked
-            const bool act = valid && !(dp.early_exit && bumped);
-            if (!__any_sync(kFull, act)) break;
+            const bool live = lane_ok && !(dp.early_exit && bumped);
+            const bool act1 = live && m1 < nM, act2 = live && m2 < nM;
+            if (!__any_sync(kFull, act1)) break;
             bool hit = false;
-            if (act) {
-              const float4 W = S.mw[m];
-              const float3 q = torsion_apply(R, ar, W.x, W.y, W.z);
-              const int gv = grid_val(pk, node_index(g, q.x, q.y, q.z));  // issued early: hides L2 latency
-              const unsigned info = __float_as_uint(W.w);
-              const unsigned cnt = info & 0xFFu;
-              if (cnt != 0u) {
-                const float4 y0 = S.u[(info >> 8) & 0xFFu];
-                float mind = dist2(q.x, q.y, q.z, y0.x, y0.y, y0.z);  // min squared distance (P9)
-                if (cnt > 1u) {
-                  const float4 y1 = S.u[(info >> 16) & 0xFFu];
-                  mind = fminf(mind, dist2(q.x, q.y, q.z, y1.x, y1.y, y1.z));
-                  if (cnt > 2u) {
-                    const float4 y2 = S.u[info >> 24];
-                    mind = fminf(mind, dist2(q.x, q.y, q.z, y2.x, y2.y, y2.z));
-                    if (cnt > (unsigned)kInline) mind = fminf(mind, overflow_min(S, m, n_ovf, nCf, q));
-                  }
-                }
-                hit = mind < dp.bd2;
-              }
-              if (!hit) part += gv;
-              ++nact;
+            if (act1) {
+              const float4 W1 = S.mw[m1];
+              const float4 W2 = S.mw[act2 ? m2 : m1];
+              const float3 q1 = torsion_apply(R, ar, W1.x, W1.y, W1.z);
+              const float3 q2 = torsion_apply(R, ar, W2.x, W2.y, W2.z);
+              // both grid loads are issued before the candidate checks: they hide each other's latency
+              const int gv1 = grid_val(pk, node_index(g, q1.x, q1.y, q1.z));
+              const int gv2 = grid_val(pk, node_index(g, q2.x, q2.y, q2.z));
+              const bool h1 = bump_hit(S, __float_as_uint(W1.w), q1, m1, n_ovf, nCf, dp.bd2);
+              const bool h2 = act2 && bump_hit(S, __float_as_uint(W2.w), q2, m2, n_ovf, nCf, dp.bd2);
+              part += (h1 ? 0 : gv1) + (act2 && !h2 ? gv2 : 0);
+              nact += act2 ? 2 : 1;
+              hit = h1 || h2;
             }
             if (dp.early_exit) {  // OR the hits of the G lanes that share an angle
               // every lane must reach the ballot: never put it behind a short-circuit operator
