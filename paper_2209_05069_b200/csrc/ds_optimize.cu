@@ -29,7 +29,8 @@ namespace ds {
 constexpr int kMaxA = DS_MAX_ATOMS;  // atom stride of the global final-pose scratch
 constexpr int kInline = 3;           // bump candidates kept inline per moving atom
 constexpr int kOvf = 32;             // per-fragment overflow list of further (moving, candidate) pairs
-constexpr int kOptWarps = 8;         // warps per CTA (one ligand each)
+constexpr int kOptWarps = 8;         // warps per CTA of the select kernel (one ligand each)
+constexpr int kTorWarps = 8;         // warps per CTA of the torsion kernel (1-warp CTAs measured slower)
 #ifndef DS_OPT_MIN_BLOCKS
 #define DS_OPT_MIN_BLOCKS 4          // resident CTAs per SM the register budget is sized for
 #endif
@@ -224,7 +225,7 @@ __device__ __forceinline__ bool bump_hit(const TorWarpSmem &S, unsigned info, fl
   return mind < bd2;
 }
 
-__global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
+__global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
     k_torsion_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
                       OptOut out, int *queue) {
   // per-warp scratch at a compile-time offset of the shared window (nothing to rematerialise from
@@ -354,37 +355,28 @@ __global__ void __launch_bounds__(kOptWarps * 32, DS_OPT_MIN_BLOCKS)
           nCf += __popc(bk);
         }
         __syncwarp();
-        {
-          const unsigned total = (unsigned)nM * (unsigned)nCf;
-          int pm = 0, pc = lane;
-          if (nCf > 0) {
-            pm = lane / nCf;
-            pc = lane - pm * nCf;
-          }
-          const int dm = nCf > 0 ? 32 / nCf : 0, dc = nCf > 0 ? 32 - dm * nCf : 0;
-          for (unsigned p0 = 0; p0 < total; p0 += 32) {
-            if (p0 + (unsigned)lane < total) {
-              const float2 hm = S.chr[kMaxA - 1 - pm], hc = S.chr[pc];
-              const float dh = hm.x - hc.x, dr = hm.y - hc.y;
-              if (dh * dh + dr * dr < dp.cull2) {
-                unsigned *info = reinterpret_cast<unsigned *>(&S.mw[pm].w);
-                const unsigned k = atomicAdd(info, 1u) & 0xFFu;  // count <= nCf < 256: no carry
-                const unsigned ci = S.clist[pc];
-                if (k < (unsigned)kInline) {
-                  atomicOr(info, ci << (8 + 8 * k));
-                } else {
-                  const int slot = atomicAdd(&S.n_ovf, 1);
-                  if (slot < kOvf) S.ovf[slot] = (uint16_t)((pm << 8) | ci);
-                }
+        // lane = moving atom, loop over the prefiltered C' (broadcast reads): the lane owns its info
+        // word, so candidates are recorded without shared atomics (only the rare overflow appends)
+        for (int m0 = 0; m0 < nM; m0 += 32) {
+          const int m = m0 + lane;
+          const bool ok = m < nM;
+          const float2 hm = ok ? S.chr[kMaxA - 1 - m] : make_float2(3.0e38f, 3.0e38f);
+          unsigned cnt = 0, inl = 0;
+          for (int c = 0; c < nCf; ++c) {
+            const float2 hc = S.chr[c];
+            const float dh = __fsub_rn(hm.x, hc.x), dr = __fsub_rn(hm.y, hc.y);
+            if (__fmaf_rn(dh, dh, __fmul_rn(dr, dr)) < dp.cull2) {
+              const unsigned ci = S.clist[c];
+              if (cnt < (unsigned)kInline) {
+                inl |= ci << (8 + 8 * cnt);
+              } else {
+                const int slot = atomicAdd(&S.n_ovf, 1);
+                if (slot < kOvf) S.ovf[slot] = (uint16_t)((m << 8) | ci);
               }
-            }
-            pm += dm;
-            pc += dc;
-            if (pc >= nCf) {
-              pc -= nCf;
-              ++pm;
+              ++cnt;
             }
           }
+          if (ok) reinterpret_cast<unsigned *>(&S.mw[m].w)[0] = cnt | inl;  // cnt <= nCf < 256
         }
         unsigned best_key = 0;  // (score + 32768) << 16 | (65535 - angle); 0 = no clean angle
         __syncwarp();
@@ -659,12 +651,12 @@ size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap) {
   return (fixed + 15) & ~(size_t)15;
 }
 
-constexpr size_t kTorSmem = kOptWarps * sizeof(TorWarpSmem);
+constexpr size_t kTorSmem = kTorWarps * sizeof(TorWarpSmem);
 
 void launch_torsion_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                             const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st) {
   cudaFuncSetAttribute(k_torsion_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
-  k_torsion_batched<<<blocks, kOptWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
+  k_torsion_batched<<<blocks, kTorWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
 }
 
 void launch_select_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const uint32_t *keys,
@@ -676,7 +668,7 @@ void launch_select_batched(const PocketView &pk, const BatchView &bt, const Dock
 int torsion_blocks_per_sm() {
   int n = 0;
   cudaFuncSetAttribute(k_torsion_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_torsion_batched, kOptWarps * 32, kTorSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_torsion_batched, kTorWarps * 32, kTorSmem);
   return n;
 }
 
