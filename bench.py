@@ -119,8 +119,10 @@ def work_model(batch, res, cfg):
     u_score = N * n_t * msum  # upper bound: clean angles score only the moving atoms (base hoisted)
     u_resc = res["n_kept"].astype(np.float64) * A * 200.0
     w_align = C_ALIGN * u_align / 32.0
-    w_total = (C_ALIGN * u_align + C_ROT * u_rot + C_PAIR * u_pair + C_SCORE * u_score + C_RESC * u_resc) / 32.0
-    return float(w_align.sum()), float(w_total.sum())
+    w_tors = (C_ROT * u_rot + C_PAIR * u_pair + C_SCORE * u_score) / 32.0
+    w_sel = C_RESC * u_resc / 32.0
+    return {"k_align_batched": float(w_align.sum()), "k_torsion_batched": float(w_tors.sum()),
+            "k_select_batched": float(w_sel.sum())}
 
 
 def ncu_calibration():
@@ -234,13 +236,14 @@ def main():
     for _ in range(args.warmup):
         rb.dock(dp, cfg, seed=0)
     barrier()
-    step_ms, align_ms, opt_ms = [], [], []
+    step_ms, align_ms, opt_ms, sel_ms = [], [], [], []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             st = rb.dock(dp, cfg, seed=0)
             step_ms.append(st.total_ms)
             align_ms.append(st.align_ms)
             opt_ms.append(st.optimize_ms)
+            sel_ms.append(st.select_ms)
     barrier()
     res = rb.download()
     ms = max_over_ranks(float(np.mean(step_ms)))
@@ -270,32 +273,39 @@ def main():
     f_mhz = peaks.get("sm_max_mhz", 1965.0)
     n_sm = torch.cuda.get_device_properties(local).multi_processor_count
     peak_winst = n_sm * 4 * f_mhz * 1e6
-    w_align, w_total = work_model(batch, res, cfg)
-    a_ms, o_ms = float(np.mean(align_ms)), float(np.mean(opt_ms))
-    dom_is_align = a_ms >= o_ms
-    dom = "k_align_batched" if dom_is_align else "k_optimize_batched"
-    dom_ms = a_ms if dom_is_align else o_ms
-    achieved = (w_align if dom_is_align else (w_total - w_align)) / (dom_ms / 1e3)
+    work = work_model(batch, res, cfg)
+    w_total = sum(work.values())
+    a_ms, o_ms, s_ms = float(np.mean(align_ms)), float(np.mean(opt_ms)), float(np.mean(sel_ms))
+    kms = {"k_align_batched": a_ms, "k_torsion_batched": o_ms - s_ms, "k_select_batched": s_ms}
     # executed-instruction and DRAM calibration of the same kernels on the same workload generator,
     # from the committed ncu capture (profiles/, per ligand), applied to this run's live timing
     cal = ncu_calibration()
+    per_kernel = {}
+    for k, t in kms.items():
+        kc = cal.get(k, {})
+        per_kernel[k] = {
+            "ms": t, "share": t / (a_ms + o_ms),
+            "algorithmic_frac": (work[k] / (t / 1e3)) / peak_winst if t > 0 else None,
+            "executed_issue_frac": (kc["inst_per_ligand"] * n / (t / 1e3) / peak_winst)
+            if "inst_per_ligand" in kc and t > 0 else None,
+            "ncu_issue_active_pct": kc.get("issue_active_pct"),
+            "ncu_pipe_fmaheavy_pct": kc.get("pipe_fmaheavy_pct"),
+            "ncu_smem_wavefront_pct": kc.get("smem_wavefront_pct")}
+    dom = max(kms, key=kms.get)
     kc = cal.get(dom, {})
-    exec_frac = (kc["inst_per_ligand"] * n / (dom_ms / 1e3) / peak_winst) if "inst_per_ligand" in kc else None
-    traffic = kc["dram_bytes_per_ligand"] * n if "dram_bytes_per_ligand" in kc else None
+    achieved = work[dom] / (kms[dom] / 1e3)
     roof = {"bound": "issue", "kernel": dom,
             "achieved": achieved / 1e9, "peak": peak_winst / 1e9, "unit": "Gwarp-inst/s",
-            "frac": achieved / peak_winst, "traffic": traffic,
-            "executed_issue_frac": exec_frac, "ncu_issue_active_pct": kc.get("issue_active_pct"),
-            "note": f"achieved = algorithmic warp-instructions of the SURVEY §8d cost model / CUDA-event launch "
-                    f"time; peak = {n_sm} SM x 4 issue/clk x {f_mhz} MHz (MEASURED_PEAKS.json sm_max_mhz); "
-                    f"executed_issue_frac = ncu-counted warp-instructions per ligand ({cal.get('source')}) x "
-                    f"ligands / launch time / peak; traffic = ncu DRAM bytes per ligand x ligands"}
-    roof_align = {"kernel": "k_align_batched", "frac": (w_align / (a_ms / 1e3)) / peak_winst,
-                  "executed_issue_frac": (cal["k_align_batched"]["inst_per_ligand"] * n / (a_ms / 1e3) / peak_winst)
-                  if "inst_per_ligand" in cal.get("k_align_batched", {}) else None,
-                  "ncu_pipe_fmaheavy_pct": cal.get("k_align_batched", {}).get("pipe_fmaheavy_pct"),
-                  "ncu_smem_wavefront_pct": cal.get("k_align_batched", {}).get("smem_wavefront_pct"),
-                  "note": "binding unit: the FMA-heavy pipe (FFMA2/FADD2/IMAD), per the committed ncu capture"}
+            "frac": achieved / peak_winst,
+            "traffic": kc["dram_bytes_per_ligand"] * n if "dram_bytes_per_ligand" in kc else None,
+            "executed_issue_frac": per_kernel[dom]["executed_issue_frac"],
+            "ncu_issue_active_pct": kc.get("issue_active_pct"),
+            "note": f"achieved = algorithmic warp-instructions of the SURVEY §8d cost model (24 per alignment "
+                    f"unit, 20 per torsion rotation, 8 per bump pair, 14 per torsion score, 20 per rescore pair; "
+                    f"/32) / CUDA-event kernel time; peak = {n_sm} SM x 4 issue/clk x {f_mhz} MHz "
+                    f"(MEASURED_PEAKS.json sm_max_mhz); executed_issue_frac = ncu-counted warp-instructions "
+                    f"per ligand ({cal.get('source')}) x ligands / kernel time / peak (the paper's method); "
+                    f"traffic = ncu DRAM bytes per ligand x ligands"}
     whole = {"achieved": (w_total / (ms / 1e3)) / 1e9, "frac": (w_total / (ms / 1e3)) / peak_winst,
              "unit": "Gwarp-inst/s"}
     in_bytes = int(packed.atom_xyzt.nbytes + packed.frag_desc.nbytes + packed.atom_off.nbytes * 2 + packed.id_hash.nbytes)
@@ -323,10 +333,10 @@ def main():
                            "ligands_per_rank": n, "grid_dims": list(pocket.grid_dims),
                            "l2": "inputs larger than L2 (per-step ligand data > 126 MB at 200k ligands)",
                            "parallelism": f"dp{world} (contiguous ligand shards, no collective)"},
-                "e2e": e2e, "roofline": roof, "roofline_align": roof_align, "roofline_whole_step": whole,
+                "e2e": e2e, "roofline": roof, "roofline_kernels": per_kernel, "roofline_whole_step": whole,
                 "roofline_hbm": hbm,
                 "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": 3 * args.steps,
-                "kernel_ms": {"align": a_ms, "optimize": o_ms}, "status_ok_frac": status_ok}
+                "kernel_ms": {"align": a_ms, "torsion": o_ms - s_ms, "select": s_ms}, "status_ok_frac": status_ok}
         print(json.dumps(line), flush=True)
     rb.close()
     dp.close()

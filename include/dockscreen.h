@@ -156,7 +156,8 @@ typedef struct ds_stats {
   float align_ms;                  /* alignment kernel(s) */
   float optimize_ms;               /* torsion + select + rescore kernel(s) */
   int32_t launches;                /* kernels launched by the call */
-  int32_t reserved;
+  float select_ms;                 /* batched family: the select + rescore kernel, part of optimize_ms
+                                      (0 when the call is chunked and it is not timed separately) */
   int64_t h2d_bytes;
   int64_t d2h_bytes;
 } ds_stats;

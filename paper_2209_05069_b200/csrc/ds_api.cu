@@ -612,6 +612,7 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t at
   oo.best_tors = want_btors ? (uint8_t *)c->b_btors.p : nullptr;
   launch_torsion_batched(pk->view, bt, dp, (const int *)c->b_order_o.p + L0, ao.keys, oo, queue + 16, blocks_t,
                          c->stream);
+  if (e2 == c->ev[3]) cudaEventRecord(c->ev[5], c->stream);  // unchunked: time the select kernel too
   launch_select_batched(pk->view, bt, dp, ao.keys, oo, queue + 32, blocks_s, smem_s, c->stream);
   cudaEventRecord(e2, c->stream);
   if (st) st->launches += 3;
@@ -690,13 +691,15 @@ int download(ds_ctx *c, int L, int NA, int NF, int N, const ds_outputs *out, ds_
   return DS_OK;
 }
 
-void fill_times(ds_ctx *c, ds_stats *st, bool with_copies) {
+void fill_times(ds_ctx *c, ds_stats *st, bool with_copies, bool family_batched) {
   if (!st) return;
   float t = 0.f;
   cudaEventElapsedTime(&t, c->ev[1], c->ev[2]);
   st->align_ms = t;
   cudaEventElapsedTime(&t, c->ev[2], c->ev[3]);
   st->optimize_ms = t;
+  st->select_ms = 0.f;
+  if (family_batched && cudaEventElapsedTime(&t, c->ev[5], c->ev[3]) == cudaSuccess) st->select_ms = t;
   cudaEventElapsedTime(&t, with_copies ? c->ev[0] : c->ev[1], with_copies ? c->ev[4] : c->ev[3]);
   st->total_ms = t;
 }
@@ -847,7 +850,7 @@ int ds_dock(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const ds_doc
   if ((rc = download(c, L, NA, NF, dp.N, out, st))) return rc;
   cudaEventRecord(c->ev[4], c->stream);
   DS_CUDA(cudaStreamSynchronize(c->stream));
-  fill_times(c, st, true);
+  fill_times(c, st, true, family == DS_FAMILY_BATCHED);
   return DS_OK;
 }
 
@@ -906,7 +909,7 @@ int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_d
   DS_CUDA(cudaStreamSynchronize(c->stream));
   d->N = dp.N;
   d->docked = true;
-  fill_times(c, st, false);
+  fill_times(c, st, false, family == DS_FAMILY_BATCHED);
   return DS_OK;
 }
 

@@ -70,7 +70,7 @@ class Outputs(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("total_ms", C.c_float), ("align_ms", C.c_float), ("optimize_ms", C.c_float),
-                ("launches", C.c_int32), ("reserved", C.c_int32), ("h2d_bytes", C.c_int64),
+                ("launches", C.c_int32), ("select_ms", C.c_float), ("h2d_bytes", C.c_int64),
                 ("d2h_bytes", C.c_int64)]
 
 
