@@ -435,6 +435,16 @@ int check_config(const ds_dock_config *cfg, const ds_pocket *pk, DockParams *dp)
   dp->cull2 = (float)((bd + 0.02) * (bd + 0.02));          // conservative bump-candidate bound
   dp->cull_r = (float)((bd + 0.02) * (1.0 + 1e-6));
   dp->opaque0 = 0u;
+  {
+    const int nA = std::min(32, dp->n_t), G = 32 / nA;
+    for (int l = 0; l < 32; ++l) {
+      const int a = l % nA, gi = l / nA;
+      unsigned same = 0;
+      for (int t = 0; t < G; ++t) same |= 1u << (a + t * nA);
+      dp->sweep_lane[l] = (unsigned)a | ((unsigned)gi << 8) | ((unsigned)(gi < G) << 16);
+      dp->sweep_same[l] = same;
+    }
+  }
   return DS_OK;
 }
 

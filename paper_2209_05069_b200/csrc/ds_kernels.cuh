@@ -44,6 +44,10 @@ struct DockParams {
   float cull_r;              // the bound itself (rounded up), for the per-fragment (h, r) box
   unsigned opaque0;          // always 0: XORed into loop-invariant index terms so ptxas keeps them as
                              // ALU adds instead of re-deriving them with FMA-pipe IMADs
+  // torsion sweep lane layout of the first angle block (angles 0 .. min(32, n_t) - 1): lane ->
+  // a | gi << 8 | (gi < G) << 16, and the mask of the lanes sharing its angle (no divisions on device)
+  unsigned sweep_lane[32];
+  unsigned sweep_same[32];
 };
 
 struct AlignOut {

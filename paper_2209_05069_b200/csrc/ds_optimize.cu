@@ -388,12 +388,23 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         // node nor a squared distance (and angle 0 is never committed).
         for (int k0 = 0; k0 < dp.n_t; k0 += 32) {
           const int nA = min(32, dp.n_t - k0);
-          const int G = 32 / nA;                  // moving-atom groups per round
-          const int a = lane % nA, gi = lane / nA;
+          int G, a, gi;                           // moving-atom groups per round, lane's angle and group
+          unsigned same;                          // lanes that share this lane's angle
+          if (k0 == 0) {                          // host-built layout of the first block
+            const unsigned e = dp.sweep_lane[lane];
+            a = (int)(e & 0xFFu);
+            gi = (int)((e >> 8) & 0xFFu);
+            same = dp.sweep_same[lane];
+            G = __popc(dp.sweep_same[0]);
+          } else {
+            G = 32 / nA;
+            a = lane % nA;
+            gi = lane / nA;
+            same = 0;
+            for (int t = 0; t < G; ++t) same |= 1u << (a + t * nA);
+          }
           const bool lane_ok = gi < G;
           const int kang = k0 + a;
-          unsigned same = 0;                      // lanes that share this lane's angle
-          for (int t = 0; t < G; ++t) same |= 1u << (a + t * nA);
           float R[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
           float3 ar = make_float3(0.f, 0.f, 0.f);
           if (kang > 0) {
