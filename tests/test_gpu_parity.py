@@ -119,3 +119,28 @@ def test_batched_parity_no_early_exit(gpu_ctx, synth_pocket, table):
     g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg)
     compare(batch, g, o, cfg)
     assert np.array_equal(g.results["bump_checks"].astype(np.int64), o.results["bump_checks"])
+
+
+def _scaled(batch, scale):
+    """The same ligands with every coordinate scaled (crowded when scale < 1: bonds of 1.5*scale Å)."""
+    from paper_2209_05069_b200.native import LigandBatch
+    return LigandBatch(batch.atom_off, (batch.atom_xyz * np.float32(scale)).astype(np.float32), batch.atom_type,
+                       batch.bond_off, batch.bonds, batch.frag_off, batch.frag_axis, batch.frag_mask, batch.ids)
+
+
+@pytest.mark.parametrize("scale", [0.7, 0.45])
+def test_batched_parity_crowded(gpu_ctx, synth_pocket, table, scale):
+    """Crowded ligands: many bump candidates per moving atom, so the inline slots, the per-fragment
+    overflow list and its full-scan fallback (> 32 overflow pairs) all run; both early-exit modes."""
+    batch = _scaled(io.generate_dataset_batch(36, 20, 40, seed=4), scale)
+    for cfg in (model.DockConfig(), model.DockConfig(early_exit=False)):
+        g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg)
+        compare(batch, g, o, cfg, check_r32=not cfg.early_exit)
+
+
+def test_batched_parity_fine_torsion_step(gpu_ctx, synth_pocket, table):
+    """torsion_step_deg = 10: 36 angles, so the sweep runs a second (device-computed) lane block."""
+    batch = io.generate_mixed_batch(60, seed=6)
+    cfg = model.DockConfig(torsion_step_deg=10)
+    g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg)
+    compare(batch, g, o, cfg)
