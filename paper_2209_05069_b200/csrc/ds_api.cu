@@ -84,6 +84,23 @@ struct ds_ctx {
   // batch-sized device buffers
   DevBuf b_atom_off, b_atoms, b_frag_off, b_frags, b_idh, b_order_a, b_order_o, b_keys, b_res, b_rrec, b_rtors,
       b_coords, b_btors, b_queue, b_scratch, b_rgv, b_lat_scores, b_lat_recs, b_lat_done;
+  // device pointers of the batch being docked: the per-array buffers above, or for small calls
+  // (ds_dock "express" path) two arenas moved with one H2D and one D2H each
+  struct IoView {
+    int *atom_off;
+    float4 *atoms;
+    int *frag_off;
+    uint4 *frags;
+    uint64_t *idh;
+    int *order_a, *order_o;
+    ds_result *res;
+    ds_restart_record *rrec;
+    uint8_t *rtors;
+    float *coords;
+    uint8_t *btors;
+  } io{};
+  DevBuf x_in, x_out;
+  size_t x_in_bytes = 0, x_out_bytes = 0, x_out_off[5] = {};
   // pinned host staging
   void *h_stage = nullptr;
   size_t h_cap = 0;
@@ -189,7 +206,8 @@ void ds_destroy(ds_ctx *c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   DevBuf *bufs[] = {&c->b_atom_off, &c->b_atoms, &c->b_frag_off, &c->b_frags, &c->b_idh, &c->b_order_a,
                     &c->b_order_o, &c->b_keys, &c->b_res, &c->b_rrec, &c->b_rtors, &c->b_coords, &c->b_btors,
-                    &c->b_queue, &c->b_scratch, &c->b_rgv, &c->b_lat_scores, &c->b_lat_recs, &c->b_lat_done};
+                    &c->b_queue, &c->b_scratch, &c->b_rgv, &c->b_lat_scores, &c->b_lat_recs, &c->b_lat_done,
+                    &c->x_in, &c->x_out};
   for (DevBuf *b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->trig) cudaFree(c->trig);
@@ -522,6 +540,13 @@ bool is_pinned(const void *p) {
 }
 
 
+void io_from_buffers(ds_ctx *c) {
+  c->io = {(int *)c->b_atom_off.p,    (float4 *)c->b_atoms.p,           (int *)c->b_frag_off.p,
+           (uint4 *)c->b_frags.p,     (uint64_t *)c->b_idh.p,           (int *)c->b_order_a.p,
+           (int *)c->b_order_o.p,     (ds_result *)c->b_res.p,          (ds_restart_record *)c->b_rrec.p,
+           (uint8_t *)c->b_rtors.p,   (float *)c->b_coords.p,           (uint8_t *)c->b_btors.p};
+}
+
 // batch-sized device buffers (both families); grows geometrically, never shrinks
 int reserve_buffers(ds_ctx *c, int L, int NA, int NF, int N) {
   int rc;
@@ -534,6 +559,7 @@ int reserve_buffers(ds_ctx *c, int L, int NA, int NF, int N) {
       (rc = c->ensure(c->b_rtors, (size_t)std::max(NF, 1) * N)) || (rc = c->ensure(c->b_coords, 12ull * std::max(NA, 1))) ||
       (rc = c->ensure(c->b_btors, (size_t)std::max(NF, 1))) || (rc = c->ensure(c->b_queue, 256)))
     return rc;
+  io_from_buffers(c);
   return DS_OK;
 }
 
@@ -578,6 +604,105 @@ int upload_batch(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
   return DS_OK;
 }
 
+// Express path for small calls (the latency family's single ligands): every input array is
+// packed into the pinned staging buffer and moved with ONE H2D into an input arena, the kernels
+// write their outputs into an output arena that comes back with ONE D2H (each transfer costs a
+// PCIe round trip of several microseconds, which dominated the time to result of one ligand).
+constexpr size_t kExpressMaxBytes = 4u << 20;
+
+size_t express_in_bytes(const ds_batch_desc *b) {
+  const size_t L = (size_t)b->n_ligands, NA = (size_t)b->atom_off[L], NF = (size_t)b->frag_off[L];
+  return 2 * 4 * (L + 1) + 16 * NA + 32 * NF + 8 * L + 2 * 4 * L + 7 * 256;
+}
+
+// arena sizes for a call of L ligands / NA atoms / NF fragments (256-byte aligned sub-arrays)
+void express_sizes(int L, int NA, int NF, int N, size_t *in_bytes, size_t *out_bytes) {
+  const size_t sz[7] = {4ull * (L + 1), 16ull * NA, 4ull * (L + 1), 32ull * NF, 8ull * L, 4ull * L, 4ull * L};
+  const size_t osz[5] = {sizeof(ds_result) * (size_t)L, sizeof(ds_restart_record) * (size_t)L * N, (size_t)NF * N,
+                         12ull * NA, (size_t)NF};
+  size_t o = 0;
+  for (size_t v : sz) o += (v + 255) & ~(size_t)255;
+  *in_bytes = o;
+  o = 0;
+  for (size_t v : osz) o += (v + 255) & ~(size_t)255;
+  *out_bytes = std::max<size_t>(o, 256);
+}
+
+int reserve_express(ds_ctx *c, int L, int NA, int NF) {
+  size_t ib, ob;
+  express_sizes(L, NA, NF, DS_MAX_RESTARTS, &ib, &ob);
+  if (ib > kExpressMaxBytes) return DS_OK;  // such calls take the per-array path
+  int rc;
+  if ((rc = c->ensure(c->x_in, ib)) || (rc = c->ensure(c->x_out, ob)) || (rc = c->ensure_host(ib + ob))) return rc;
+  return DS_OK;
+}
+
+int upload_express(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
+  const int L = b->n_ligands;
+  const int NA = b->atom_off[L], NF = b->frag_off[L];
+  std::vector<int> oa, oo;
+  lpt_orders(b, oa, oo);
+  int rc;
+  if ((rc = reserve_buffers(c, L, NA, NF, N))) return rc;  // device-only scratch (keys, queue, ...)
+  const void *src[7] = {b->atom_off, b->atom_xyzt, b->frag_off, b->frag_desc, b->id_hash, oa.data(), oo.data()};
+  const size_t sz[7] = {4ull * (L + 1), 16ull * NA, 4ull * (L + 1), 32ull * NF, 8ull * L, 4ull * L, 4ull * L};
+  size_t off[7], o = 0;
+  for (int k = 0; k < 7; ++k) {
+    off[k] = o;
+    o += (sz[k] + 255) & ~(size_t)255;
+  }
+  const size_t in_bytes = o;
+  const size_t osz[5] = {sizeof(ds_result) * (size_t)L, sizeof(ds_restart_record) * (size_t)L * N, (size_t)NF * N,
+                         12ull * NA, (size_t)NF};
+  o = 0;
+  for (int k = 0; k < 5; ++k) {
+    c->x_out_off[k] = o;
+    o += (osz[k] + 255) & ~(size_t)255;
+  }
+  const size_t out_bytes = std::max<size_t>(o, 256);
+  if ((rc = c->ensure(c->x_in, in_bytes)) || (rc = c->ensure(c->x_out, out_bytes)) ||
+      (rc = c->ensure_host(in_bytes + out_bytes)))
+    return rc;
+  char *h = (char *)c->h_stage;
+  for (int k = 0; k < 7; ++k)
+    if (sz[k]) memcpy(h + off[k], src[k], sz[k]);
+  DS_CUDA(cudaMemcpyAsync(c->x_in.p, h, in_bytes, cudaMemcpyHostToDevice, c->stream));
+  char *di = (char *)c->x_in.p, *dout = (char *)c->x_out.p;
+  c->io.atom_off = (int *)(di + off[0]);
+  c->io.atoms = (float4 *)(di + off[1]);
+  c->io.frag_off = (int *)(di + off[2]);
+  c->io.frags = (uint4 *)(di + off[3]);
+  c->io.idh = (uint64_t *)(di + off[4]);
+  c->io.order_a = (int *)(di + off[5]);
+  c->io.order_o = (int *)(di + off[6]);
+  c->io.res = (ds_result *)(dout + c->x_out_off[0]);
+  c->io.rrec = (ds_restart_record *)(dout + c->x_out_off[1]);
+  c->io.rtors = (uint8_t *)(dout + c->x_out_off[2]);
+  c->io.coords = (float *)(dout + c->x_out_off[3]);
+  c->io.btors = (uint8_t *)(dout + c->x_out_off[4]);
+  c->x_in_bytes = in_bytes;
+  c->x_out_bytes = out_bytes;
+  if (st) st->h2d_bytes += (int64_t)in_bytes;
+  return DS_OK;
+}
+
+int download_express(ds_ctx *c, ds_stats *st) {
+  DS_CUDA(cudaMemcpyAsync((char *)c->h_stage + c->x_in_bytes, c->x_out.p, c->x_out_bytes, cudaMemcpyDeviceToHost,
+                          c->stream));
+  if (st) st->d2h_bytes += (int64_t)c->x_out_bytes;
+  return DS_OK;
+}
+
+// after the stream has synchronised: scatter the output arena into the caller's buffers
+void finish_express(ds_ctx *c, int L, int NA, int NF, int N, const ds_outputs *out) {
+  const char *h = (const char *)c->h_stage + c->x_in_bytes;
+  if (out->results) memcpy(out->results, h + c->x_out_off[0], sizeof(ds_result) * (size_t)L);
+  if (out->restarts) memcpy(out->restarts, h + c->x_out_off[1], sizeof(ds_restart_record) * (size_t)L * N);
+  if (out->restart_torsion && NF) memcpy(out->restart_torsion, h + c->x_out_off[2], (size_t)NF * N);
+  if (out->best_coords && NA) memcpy(out->best_coords, h + c->x_out_off[3], 12ull * NA);
+  if (out->best_torsion && NF) memcpy(out->best_torsion, h + c->x_out_off[4], (size_t)NF);
+}
+
 int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t atom_base, int64_t n_atoms_range,
                       const DockParams &dp, bool want_coords, bool want_btors, bool want_rrec, ds_stats *st,
                       cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2, int *queue);
@@ -597,11 +722,11 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t at
                       cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2, int *queue) {
   BatchView bt;
   bt.L = L1 - L0;
-  bt.atom_off = (const int *)c->b_atom_off.p + L0;
-  bt.atoms = (const float4 *)c->b_atoms.p;
-  bt.frag_off = (const int *)c->b_frag_off.p + L0;
-  bt.frags = (const uint4 *)c->b_frags.p;
-  bt.idh = (const uint64_t *)c->b_idh.p + L0;
+  bt.atom_off = c->io.atom_off + L0;
+  bt.atoms = c->io.atoms;
+  bt.frag_off = c->io.frag_off + L0;
+  bt.frags = c->io.frags;
+  bt.idh = c->io.idh + L0;
   // --- alignment: one CTA per SM, grid staged into smem when it fits ---
   const size_t per_warp = (size_t)align_warp_smem_bytes_host(dp.N);
   const size_t fixed = (size_t)dp.n_a * 16;
@@ -612,7 +737,7 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t at
   const size_t smem_a = (in_smem ? gb : 0) + fixed + per_warp * warps_a;
   AlignOut ao{(uint32_t *)c->b_keys.p + (size_t)L0 * dp.N};
   cudaEventRecord(e0, c->stream);
-  launch_align_batched(pk->view, bt, dp, (const int *)c->b_order_a.p + L0, ao, queue, in_smem, c->sm_count, warps_a,
+  launch_align_batched(pk->view, bt, dp, c->io.order_a + L0, ao, queue, in_smem, c->sm_count, warps_a,
                        smem_a, c->stream);
   cudaEventRecord(e1, c->stream);
   // --- torsion optimisation, then select + rescore: warp per ligand, persistent, occupancy-sized ---
@@ -624,15 +749,15 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t at
       (rc = c->ensure(c->b_rgv, sizeof(int) * (size_t)dp.N * (size_t)(L1 - L0))))
     return rc;
   OptOut oo;
-  oo.res = (ds_result *)c->b_res.p + L0;
-  oo.rrec = want_rrec ? (ds_restart_record *)c->b_rrec.p + (size_t)L0 * dp.N : nullptr;
-  oo.rtors = (uint8_t *)c->b_rtors.p;
+  oo.res = c->io.res + L0;
+  oo.rrec = want_rrec ? c->io.rrec + (size_t)L0 * dp.N : nullptr;
+  oo.rtors = c->io.rtors;
   oo.final_u = (float4 *)c->b_scratch.p;
   oo.rgv = (int *)c->b_rgv.p;
   oo.atom_base = atom_base;
-  oo.best_coords = want_coords ? (float *)c->b_coords.p : nullptr;
-  oo.best_tors = want_btors ? (uint8_t *)c->b_btors.p : nullptr;
-  launch_torsion_batched(pk->view, bt, dp, (const int *)c->b_order_o.p + L0, ao.keys, oo, queue + 16, blocks_t,
+  oo.best_coords = want_coords ? c->io.coords : nullptr;
+  oo.best_tors = want_btors ? c->io.btors : nullptr;
+  launch_torsion_batched(pk->view, bt, dp, c->io.order_o + L0, ao.keys, oo, queue + 16, blocks_t,
                          c->stream);
   if (e2 == c->ev[3]) cudaEventRecord(c->ev[5], c->stream);  // unchunked: time the select kernel too
   launch_select_batched(pk->view, bt, dp, ao.keys, oo, queue + 32, blocks_s, smem_s, c->stream);
@@ -649,11 +774,11 @@ int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const Dock
                 bool want_btors, bool want_rrec, ds_stats *st) {
   BatchView bt;
   bt.L = L;
-  bt.atom_off = (const int *)c->b_atom_off.p;
-  bt.atoms = (const float4 *)c->b_atoms.p;
-  bt.frag_off = (const int *)c->b_frag_off.p;
-  bt.frags = (const uint4 *)c->b_frags.p;
-  bt.idh = (const uint64_t *)c->b_idh.p;
+  bt.atom_off = c->io.atom_off;
+  bt.atoms = c->io.atoms;
+  bt.frag_off = c->io.frag_off;
+  bt.frags = c->io.frags;
+  bt.idh = c->io.idh;
   int rc;
   const size_t nsc = (size_t)L * dp.N * dp.n_rot;
   if ((rc = c->ensure(c->b_lat_scores, 4 * nsc)) || (rc = c->ensure(c->b_lat_recs, latency_rec_bytes() * (size_t)L * dp.N)) ||
@@ -666,12 +791,12 @@ int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const Dock
   launch_align_latency(pk->view, bt, dp, max_atoms, (int *)c->b_lat_scores.p, c->stream);
   cudaEventRecord(c->ev[2], c->stream);
   OptOut oo;
-  oo.res = (ds_result *)c->b_res.p;
-  oo.rrec = want_rrec ? (ds_restart_record *)c->b_rrec.p : nullptr;
-  oo.rtors = (uint8_t *)c->b_rtors.p;
+  oo.res = c->io.res;
+  oo.rrec = want_rrec ? c->io.rrec : nullptr;
+  oo.rtors = c->io.rtors;
   oo.final_u = (float4 *)c->b_scratch.p;
-  oo.best_coords = want_coords ? (float *)c->b_coords.p : nullptr;
-  oo.best_tors = want_btors ? (uint8_t *)c->b_btors.p : nullptr;
+  oo.best_coords = want_coords ? c->io.coords : nullptr;
+  oo.best_tors = want_btors ? c->io.btors : nullptr;
   launch_optimize_latency(pk->view, bt, dp, (const int *)c->b_lat_scores.p, oo, c->b_lat_recs.p,
                           (int *)c->b_lat_done.p, c->stream);
   cudaEventRecord(c->ev[3], c->stream);
@@ -861,17 +986,19 @@ int ds_dock(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const ds_doc
     const int nch = pipeline_chunks(L);
     if (nch > 1) return dock_pipelined(c, pk, b, dp, out, st, nch);
   }
-  cudaEventRecord(c->ev[0], c->stream);
-  if ((rc = upload_batch(c, b, dp.N, st))) return rc;
   const int NA = b->atom_off[L], NF = b->frag_off[L];
+  const bool express = express_in_bytes(b) <= kExpressMaxBytes;
+  cudaEventRecord(c->ev[0], c->stream);
+  if ((rc = express ? upload_express(c, b, dp.N, st) : upload_batch(c, b, dp.N, st))) return rc;
   int max_atoms = 0;
   for (int i = 0; i < L; ++i) max_atoms = std::max(max_atoms, b->atom_off[i + 1] - b->atom_off[i]);
   if ((rc = run_family(c, pk, family, L, NA, NF, max_atoms, dp, out->best_coords != nullptr,
                        out->best_torsion != nullptr, out->restarts != nullptr, st)))
     return rc;
-  if ((rc = download(c, L, NA, NF, dp.N, out, st))) return rc;
+  if ((rc = express ? download_express(c, st) : download(c, L, NA, NF, dp.N, out, st))) return rc;
   cudaEventRecord(c->ev[4], c->stream);
   DS_CUDA(cudaStreamSynchronize(c->stream));
+  if (express) finish_express(c, L, NA, NF, dp.N, out);
   fill_times(c, st, true, family == DS_FAMILY_BATCHED);
   return DS_OK;
 }
@@ -890,6 +1017,7 @@ int ds_ctx_reserve(ds_ctx *c, int max_ligands, int max_atoms, int max_frags, con
       (rc = c->ensure(c->b_lat_recs, latency_rec_bytes() * L * N)) || (rc = c->ensure(c->b_lat_done, 4 * L)) ||
       (rc = c->ensure(c->b_scratch, sizeof(float4) * std::max(L * DS_MAX_ATOMS, (size_t)max_atoms) * N)) ||
       (rc = c->ensure(c->b_rgv, sizeof(int) * L * N)) ||
+      (rc = reserve_express(c, max_ligands, max_atoms, max_frags)) ||
       (rc = c->ensure_host((size_t)max_atoms * 16 + (size_t)max_frags * 32 + L * 32 + 4096)))
     return rc;
   return DS_OK;
@@ -927,6 +1055,7 @@ int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_d
   DS_CUDA(enter_device(c->device));
   int max_atoms = 0;
   for (int i = 0; i < d->L; ++i) max_atoms = std::max(max_atoms, d->atom_off[i + 1] - d->atom_off[i]);
+  io_from_buffers(c);  // the resident batch lives in the per-array buffers (not an express arena)
   if ((rc = run_family(c, pk, family, d->L, d->n_atoms, d->n_frags, max_atoms, dp, true, true, true, st))) return rc;
   DS_CUDA(cudaStreamSynchronize(c->stream));
   d->N = dp.N;

@@ -3,10 +3,17 @@
 //  k_align_latency    (ds_align.cu)  blocks = ligand x restart x atom chunk, lane = ax
 //  k_optimize_latency (this file)    one CTA per (ligand, restart) — the paper's "grid level =
 //                                    initial poses" — with every thread of the
-//                                    CTA on the (angle, moving atom) slots of a fragment; the CTA
-//                                    barrier is the paper's block-level synchronisation
-//                                    (PAPER.md:732-737).  The last CTA of a ligand to finish runs
-//                                    select_poses + rescore.
+//                                    CTA on each step of a fragment; the CTA barrier is the paper's
+//                                    block-level synchronisation.  Per fragment
+//                                    five barrier-separated phases, all 256 threads busy in each:
+//                                    (A) per-warp ballots of M / C' over 32-atom slots + the base
+//                                    score + the axis, (B) compaction + cylindrical coordinates,
+//                                    (C) flat (moving, complement) candidate test, (D) the angle
+//                                    sweep, (E) best angle (every warp, redundantly) + commit.
+//                                    Each CTA rescores its own final pose (speculatively, so the
+//                                    rescore runs on N SMs at once); the last CTA of a ligand to
+//                                    finish runs select_poses and picks the best kept pose
+//                                    (PAPER.md:344-348).
 // Numeric recipe identical to the batched family: results are bit-identical.
 #include "ds_kernels.cuh"
 
@@ -18,17 +25,21 @@ constexpr int kLatChunk = 8;
 struct LatRec {  // per (ligand, restart), read by the ligand's last CTA
   int geom, valid, degen, align_score;
   unsigned evals, pairs, exits, rot;
+  long long chem;  // rescore of the restart's final pose (P11), valid poses only
 };
 
 constexpr int kLatCand = 8;
 
 struct LatSmem {
   float4 u[DS_MAX_ATOMS];
-  float4 cmp[DS_MAX_ATOMS + kLatChunk];
-  float2 chr[DS_MAX_ATOMS];
+  float2 chr[DS_MAX_ATOMS];     // cylindrical (h, r) of the C' atoms
+  float2 chm[DS_MAX_ATOMS];     // ... and of the moving atoms
   uint8_t mlist[DS_MAX_ATOMS];
-  uint8_t cl[DS_MAX_ATOMS][kLatCand];
-  uint8_t cn[DS_MAX_ATOMS];
+  uint8_t clist[DS_MAX_ATOMS];
+  uint8_t cl[DS_MAX_ATOMS][kLatCand];  // bump candidates (atom indices) per moving atom
+  unsigned cn[DS_MAX_ATOMS];           // their count (> kLatCand: scan all of C')
+  unsigned bm[8], bc[8];        // per 32-atom slot: ballots of M and C'
+  int bpart[8];                 // per 32-atom slot: grid score of the non-moving atoms
   int ascore[32];
   unsigned abump;
   unsigned key;
@@ -41,6 +52,14 @@ struct LatSmem {
   unsigned long long chem;
   int heavy;
 };
+
+// exact rescore bin (P11): the pocket's LUT when it has one, else the compares
+__device__ __forceinline__ int lat_bin(const PocketView &pk, float d2) {
+  if (pk.lut_cap >= 0) return __ldg(pk.bin_lut + min((unsigned)__float_as_int(d2) >> pk.lut_shift, (unsigned)pk.lut_cap));
+  int b = 0;
+  for (int q = 0; q < pk.nb; ++q) b += !(d2 < pk.ub2[q]);
+  return b;
+}
 
 // grid lookup: the CTA's shared-memory copy when the pocket fits, else the L2-resident global copy
 template <bool kSmemGrid>
@@ -122,85 +141,112 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   __syncthreads();
   unsigned evals = 0, exits = 0;
   int all_bumped = 0;
+  const unsigned lt = lanemask_lt();
+  const int nslot = (A + 31) >> 5;
   for (int f = 0; f < F; ++f) {
-    // ---- compaction of M and C' (warp 0, ascending order), axis (thread 0) ----
-    if (warp == 0) {
-      const uint4 fa = sfrag[2 * f];
-      const uint4 fb = sfrag[2 * f + 1];
-      const unsigned mw[5] = {fa.x, fa.y, fa.z, fa.w, fb.x};
-      const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
-      const unsigned lt = lanemask_lt();
-      int nM = 0, nC = 0, base = 0;
-#pragma unroll
-      for (int s = 0; s < 5; ++s) {
-        if (s * 32 >= A) break;
-        const int i = s * 32 + lane;
-        const bool in = i < A;
-        const bool mv = in && ((mw[s] >> lane) & 1u);
-        const bool cp = in && !mv && i != ab && i != ae;
-        const unsigned bm = __ballot_sync(kFull, mv), bc = __ballot_sync(kFull, cp);
-        if (mv) S.mlist[nM + __popc(bm & lt)] = (uint8_t)i;
-        if (in && !mv) {
-          const float4 p = S.u[i];
-          if (cp) S.cmp[nC + __popc(bc & lt)] = p;
-          base += lat_grid_val<kSmemGrid>(grid, node_index(g, p.x, p.y, p.z));
-        }
-        nM += __popc(bm);
-        nC += __popc(bc);
+    const uint4 fa = sfrag[2 * f];
+    const uint4 fb = sfrag[2 * f + 1];
+    const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
+    // ---- (A) warp w: ballots of M and C' over atoms 32w..32w+31 and their non-moving grid score;
+    // thread 0 also builds the axis ----
+    if (warp < nslot) {
+      const unsigned mword = warp == 0 ? fa.x : warp == 1 ? fa.y : warp == 2 ? fa.z : warp == 3 ? fa.w : fb.x;
+      const int i = warp * 32 + lane;
+      const bool in = i < A;
+      const bool mv = in && ((mword >> lane) & 1u);
+      const bool cp = in && !mv && i != ab && i != ae;
+      const unsigned bm = __ballot_sync(kFull, mv), bc = __ballot_sync(kFull, cp);
+      int part = 0;
+      if (in && !mv) {
+        const float4 p = S.u[i];
+        part = lat_grid_val<kSmemGrid>(grid, node_index(g, p.x, p.y, p.z));
       }
-      base = (int)__reduce_add_sync(kFull, (unsigned)base);
-      if (lane < kLatChunk) S.cmp[nC + lane] = make_float4(1e19f, 1e19f, 1e19f, 0.f);
+      part = (int)__reduce_add_sync(kFull, (unsigned)part);
       if (lane == 0) {
-        S.nM = nM;
-        S.nC = nC;
-        S.base = base;
-        S.abump = 0u;
-        const float4 pa = S.u[ab], pb = S.u[ae];
-        if (dp.n_t > 1) {
-          const float vx = __fsub_rn(pb.x, pa.x), vy = __fsub_rn(pb.y, pa.y), vz = __fsub_rn(pb.z, pa.z);
-          const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
-          if (!(len >= dp.eps_axis)) S.degen = 1;
-          S.kx = __fdiv_rn(vx, len);
-          S.ky = __fdiv_rn(vy, len);
-          S.kz = __fdiv_rn(vz, len);
-        }
+        S.bm[warp] = bm;
+        S.bc[warp] = bc;
+        S.bpart[warp] = part;
       }
-      S.ascore[lane] = 0;
     }
+    if (tid == 0) {
+      S.abump = 0u;
+      const float4 pa = S.u[ab], pb = S.u[ae];
+      if (dp.n_t > 1) {
+        const float vx = __fsub_rn(pb.x, pa.x), vy = __fsub_rn(pb.y, pa.y), vz = __fsub_rn(pb.z, pa.z);
+        const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
+        if (!(len >= dp.eps_axis)) S.degen = 1;
+        S.kx = __fdiv_rn(vx, len);
+        S.ky = __fdiv_rn(vy, len);
+        S.kz = __fdiv_rn(vz, len);
+      }
+    }
+    if (tid < 32) S.ascore[tid] = 0;
     __syncthreads();
     if (S.degen) break;
-    const int nM = S.nM, nC = S.nC;
-    const uint4 fb = sfrag[2 * f + 1];
-    const float4 pa = S.u[fb.y & 0xFFu];
+    int nM = 0, nC = 0, base = 0, mpre = 0, cpre = 0;
+    for (int w = 0; w < nslot; ++w) {
+      if (w == warp) {
+        mpre = nM;
+        cpre = nC;
+      }
+      nM += __popc(S.bm[w]);
+      nC += __popc(S.bc[w]);
+      base += S.bpart[w];
+    }
+    const float4 pa = S.u[ab];
     const float3 a3 = make_float3(pa.x, pa.y, pa.z);
     const float kx = S.kx, ky = S.ky, kz = S.kz;
-    // bump candidates per moving atom (cylindrical bound, see ds_optimize.cu)
-    for (int c = tid; c < nC; c += kLatThreads) S.chr[c] = lat_cyl(S.cmp[c], a3, kx, ky, kz);
-    __syncthreads();
-    for (int m = tid; m < nM; m += kLatThreads) {
-      const float2 hm = lat_cyl(S.u[S.mlist[m]], a3, kx, ky, kz);
-      int cnt = 0;
-      for (int c = 0; c < nC; ++c) {
-        const float2 hc = S.chr[c];
-        const float dh = hm.x - hc.x, dr = hm.y - hc.y;
-        if (dh * dh + dr * dr < dp.cull2) {
-          if (cnt < kLatCand) S.cl[m][cnt] = (uint8_t)c;
-          ++cnt;
-        }
+    // ---- (B) compaction (ascending) + cylindrical coordinates of M and C' ----
+    if (warp < nslot) {
+      const int i = warp * 32 + lane;
+      const unsigned bm = S.bm[warp], bc = S.bc[warp];
+      if ((bm >> lane) & 1u) {
+        const int m = mpre + __popc(bm & lt);
+        S.mlist[m] = (uint8_t)i;
+        S.chm[m] = lat_cyl(S.u[i], a3, kx, ky, kz);
+        S.cn[m] = 0;
+      } else if ((bc >> lane) & 1u) {
+        const int c = cpre + __popc(bc & lt);
+        S.clist[c] = (uint8_t)i;
+        S.chr[c] = lat_cyl(S.u[i], a3, kx, ky, kz);
       }
-      S.cn[m] = (uint8_t)(cnt > kLatCand ? 255 : cnt);
     }
     __syncthreads();
+    // ---- (C) bump candidates: every (moving, complement) pair over all threads (cylindrical
+    // bound, see ds_optimize.cu) ----
+    if (nC > 0) {
+      const int total = nM * nC;
+      int pm = tid / nC, pc = tid - (tid / nC) * nC;
+      const int dm = kLatThreads / nC, dc = kLatThreads - dm * nC;
+      for (int p0 = 0; p0 < total; p0 += kLatThreads) {
+        if (p0 + tid < total) {
+          const float2 hm = S.chm[pm], hc = S.chr[pc];
+          const float dh = hm.x - hc.x, dr = hm.y - hc.y;
+          if (dh * dh + dr * dr < dp.cull2) {
+            const unsigned k = atomicAdd(&S.cn[pm], 1u);
+            if (k < (unsigned)kLatCand) S.cl[pm][k] = S.clist[pc];
+          }
+        }
+        pm += dm;
+        pc += dc;
+        if (pc >= nC) {
+          pc -= nC;
+          ++pm;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- (D) the angle sweep: thread = (angle a, moving-atom group mg); rotation and partial score
+    // in registers over m = mg, mg + G, ...; one shared atomic per thread at the end ----
     unsigned best_key = 0u;
     for (int k0 = 0; k0 < dp.n_t; k0 += 32) {
       const int nA = min(32, dp.n_t - k0);
       if (k0 > 0) {
+        __syncthreads();
         if (tid < 32) S.ascore[tid] = 0;
         if (tid == 0) S.abump = 0u;
         __syncthreads();
       }
-      // thread = (angle a, moving-atom group mg): the rotation and the partial score stay in
-      // registers over m = mg, mg + G, ...; one shared atomic per thread at the end
       unsigned my_pairs = 0;
       const int G = kLatThreads / nA;
       const int a = tid % nA, mg = tid / nA;
@@ -220,19 +266,16 @@ __global__ void __launch_bounds__(kLatThreads, 1)
           const int gv = lat_grid_val<kSmemGrid>(grid, node_index(g, q.x, q.y, q.z));
           float mind = __int_as_float(0x7f800000);
           my_pairs += (unsigned)nC;  // pairs resolved (P14)
-          const int cnt = S.cn[m];
-          if (cnt != 255) {
-            for (int t = 0; t < cnt; ++t) {
-              const float4 y = S.cmp[S.cl[m][t]];
+          const unsigned cnt = S.cn[m];
+          if (cnt <= (unsigned)kLatCand) {
+            for (unsigned t = 0; t < cnt; ++t) {
+              const float4 y = S.u[S.cl[m][t]];
               mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
             }
           } else {
-            for (int c = 0; c < nC; c += kLatChunk) {
-#pragma unroll
-              for (int t = 0; t < kLatChunk; ++t) {
-                const float4 y = S.cmp[c + t];
-                mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
-              }
+            for (int c = 0; c < nC; ++c) {
+              const float4 y = S.u[S.clist[c]];
+              mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
             }
           }
           if (mind < dp.bd2) {
@@ -245,25 +288,19 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         if (part) atomicAdd(&S.ascore[a], part);
       }
       my_pairs = __reduce_add_sync(kFull, my_pairs);
-      if (lane == 0) atomicAdd(&S.pairs, my_pairs);
+      if (lane == 0 && my_pairs) atomicAdd(&S.pairs, my_pairs);
       __syncthreads();
-      if (warp == 0) {
-        unsigned kk = 0;
-        if (lane < nA && !((S.abump >> lane) & 1u))
-          kk = ((unsigned)(S.base + S.ascore[lane] + 32768) << 16) | (unsigned)(65535 - (k0 + lane));
-        best_key = max(best_key, __reduce_max_sync(kFull, kk));
-      }
+      // ---- (E) best clean angle, computed by every warp (no extra barrier) ----
+      const unsigned abump = S.abump;
+      unsigned kk = 0;
+      if (lane < nA && !((abump >> lane) & 1u))
+        kk = ((unsigned)(base + S.ascore[lane] + 32768) << 16) | (unsigned)(65535 - (k0 + lane));
+      best_key = max(best_key, __reduce_max_sync(kFull, kk));
       evals += (unsigned)nA;
-      if (dp.early_exit) exits += (unsigned)__popc(S.abump);
-      __syncthreads();
+      if (dp.early_exit) exits += (unsigned)__popc(abump);
     }
-    if (warp == 0 && lane == 0) {
-      const int bk = best_key ? 65535 - (int)(best_key & 0xFFFFu) : -1;
-      S.best_k = bk;
-      out.rtors[(size_t)(f0 + f) * dp.N + r] = bk < 0 ? (uint8_t)DS_TORSION_NONE : (uint8_t)bk;
-    }
-    __syncthreads();
-    const int best_k = S.best_k;
+    const int best_k = best_key ? 65535 - (int)(best_key & 0xFFFFu) : -1;
+    if (tid == 0) out.rtors[(size_t)(f0 + f) * dp.N + r] = best_k < 0 ? (uint8_t)DS_TORSION_NONE : (uint8_t)best_k;
     if (best_k > 0)
       for (int m = tid; m < nM; m += kLatThreads) {
         const int i = S.mlist[m];
@@ -292,10 +329,39 @@ __global__ void __launch_bounds__(kLatThreads, 1)
       atomicAdd(&S.heavy, hv);
     }
   }
+  if (tid == 0) S.chem = 0ull;
   __syncthreads();
   const int valid = !(F >= 1 && all_bumped == F);
+  // ---- speculative rescore of this restart's pose (P11, exact fixed point): every CTA of the
+  // ligand does its own in parallel, the last one only picks among the kept poses ----
+  if (!degen && valid) {
+    const int nb1 = pk.nb + 1;
+    long long acc = 0;
+    for (int j = tid; j < pk.n_atoms; j += kLatThreads) {
+      const float4 y = __ldg(pk.patoms + j);
+      const int32_t *wcol = pk.wfx + (int)y.w * nb1;
+      int part = 0, cntp = 0;
+      for (int i = 0; i < A; ++i) {
+        const float4 x = S.u[i];
+        const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
+        part += __ldg(wcol + (int)x.w * DS_N_TYPES * nb1 + lat_bin(pk, d2));
+        if (++cntp == 64) {  // int32 partials over <= 64 atoms (|W| <= 2^24)
+          acc += part;
+          part = 0;
+          cntp = 0;
+        }
+      }
+      acc += part;
+    }
+    // warp sum then one shared 64-bit add per warp (two's complement: exact for signed sums)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if (lane == 0) atomicAdd(&S.chem, (unsigned long long)acc);
+  }
+  __syncthreads();
   if (tid == 0) {
     LatRec rec;
+    rec.chem = (long long)S.chem;
     rec.geom = S.geom;
     rec.valid = valid;
     rec.degen = degen;
@@ -323,7 +389,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   if (!S.is_last) return;
   __threadfence();
 
-  // ---- the ligand's last CTA: select_poses + rescore (P11, P12) ----
+  // ---- the ligand's last CTA: select_poses (P12), best rescored kept pose ----
   const LatRec *lr = recs + (size_t)lig * dp.N;
   __shared__ int s_geom[DS_MAX_RESTARTS], s_valid[DS_MAX_RESTARTS];
   __shared__ unsigned s_cnt[4];
@@ -412,35 +478,16 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   }
   __syncthreads();
   const int nk = S.nkept;
-  const int nb1 = pk.nb + 1;
   long long best_chem = 0;
   int best_r = -1;
   for (int t = 0; t < nk; ++t) {
     const int rr = S.kept[t];
-    for (int i = tid; i < A; i += kLatThreads) S.u[i] = __ldcg(base_scr + (size_t)rr * DS_MAX_ATOMS + i);
-    if (tid == 0) S.chem = 0ull;
-    __syncthreads();
-    long long acc = 0;
-    for (int j = tid; j < pk.n_atoms; j += kLatThreads) {
-      const float4 y = __ldg(pk.patoms + j);
-      const int tj = (int)y.w * nb1;
-      for (int i = 0; i < A; ++i) {
-        const float4 x = S.u[i];
-        const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
-        int b = 0;
-        for (int q = 0; q < pk.nb; ++q) b += !(d2 < pk.ub2[q]);
-        acc += __ldg(pk.wfx + (int)x.w * DS_N_TYPES * nb1 + tj + b);
-      }
-    }
-    atomicAdd(&S.chem, (unsigned long long)acc);
-    __syncthreads();
-    const long long chem = (long long)S.chem;
+    const long long chem = __ldcg(&lr[rr].chem);
     if (best_r < 0 || chem > best_chem || (chem == best_chem && rr < best_r)) {
       best_chem = chem;
       best_r = rr;
     }
     if (tid == 0 && out.rrec) out.rrec[(size_t)lig * dp.N + rr].kept = (uint8_t)(t + 1);
-    __syncthreads();
   }
   const int brot = (int)__ldcg(&lr[best_r].rot);
   res.status = DS_STATUS_OK;
