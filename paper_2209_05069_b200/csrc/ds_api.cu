@@ -894,33 +894,17 @@ int dock_pipelined(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const
     }
   }
   int *oa = (int *)(h + off[5]), *oo = (int *)(h + off[6]);
-  for (int k = 0; k < nch; ++k) lpt_orders_range(b, bounds[k], bounds[k + 1], oa + bounds[k], oo + bounds[k]);
   cudaStream_t cs = c->copy;
   cudaEventRecord(c->ev[0], cs);
   DS_CUDA(cudaMemcpyAsync(c->b_atom_off.p, hp[0], src[0].bytes, cudaMemcpyHostToDevice, cs));
   DS_CUDA(cudaMemcpyAsync(c->b_frag_off.p, hp[1], src[1].bytes, cudaMemcpyHostToDevice, cs));
   DS_CUDA(cudaMemcpyAsync(c->b_idh.p, hp[2], src[2].bytes, cudaMemcpyHostToDevice, cs));
-  for (int k = 0; k < nch; ++k) {
-    const int L0 = bounds[k], L1 = bounds[k + 1];
-    const size_t a0 = b->atom_off[L0], a1 = b->atom_off[L1], f0 = b->frag_off[L0], f1 = b->frag_off[L1];
-    DS_CUDA(cudaMemcpyAsync((float4 *)c->b_atoms.p + a0, hp[3] + 16 * a0, 16 * (a1 - a0), cudaMemcpyHostToDevice, cs));
-    if (f1 > f0)
-      DS_CUDA(cudaMemcpyAsync((char *)c->b_frags.p + 32 * f0, hp[4] + 32 * f0, 32 * (f1 - f0), cudaMemcpyHostToDevice, cs));
-    DS_CUDA(cudaMemcpyAsync((int *)c->b_order_a.p + L0, oa + L0, 4ull * (L1 - L0), cudaMemcpyHostToDevice, cs));
-    DS_CUDA(cudaMemcpyAsync((int *)c->b_order_o.p + L0, oo + L0, 4ull * (L1 - L0), cudaMemcpyHostToDevice, cs));
-    cudaEventRecord(c->pev[4 * k], cs);
-  }
-  if (st) st->h2d_bytes += (int64_t)(src[0].bytes + src[1].bytes + src[2].bytes + src[3].bytes + src[4].bytes + 8ull * L);
   int *queue = (int *)c->b_queue.p;
   DS_CUDA(cudaMemsetAsync(queue, 0, 256ull * nch, c->stream));
-  for (int k = 0; k < nch; ++k) {
-    const int L0 = bounds[k], L1 = bounds[k + 1];
-    DS_CUDA(cudaStreamWaitEvent(c->stream, c->pev[4 * k], 0));
-    if ((rc = run_batched_range(c, pk, L0, L1, b->atom_off[L0], (int64_t)b->atom_off[L1] - b->atom_off[L0], dp,
-                                out->best_coords != nullptr, out->best_torsion != nullptr, out->restarts != nullptr,
-                                st, c->pev[4 * k + 1], c->pev[4 * k + 2], c->pev[4 * k + 3], queue + 64 * k)))
-      return rc;
-    DS_CUDA(cudaStreamWaitEvent(cs, c->pev[4 * k + 3], 0));
+  // D2H of chunk j on the copy stream, after its kernels
+  auto d2h = [&](int j) -> int {
+    const int L0 = bounds[j], L1 = bounds[j + 1];
+    DS_CUDA(cudaStreamWaitEvent(cs, c->pev[4 * j + 3], 0));
     const size_t a0 = b->atom_off[L0], a1 = b->atom_off[L1], f0 = b->frag_off[L0], f1 = b->frag_off[L1];
     DS_CUDA(cudaMemcpyAsync(out->results + L0, (ds_result *)c->b_res.p + L0, sizeof(ds_result) * (L1 - L0),
                             cudaMemcpyDeviceToHost, cs));
@@ -940,7 +924,30 @@ int dock_pipelined(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const
                                  (out->best_torsion ? f1 - f0 : 0) +
                                  (out->restarts ? sizeof(ds_restart_record) * (size_t)(L1 - L0) * N : 0) +
                                  (out->restart_torsion ? (f1 - f0) * N : 0));
+    return DS_OK;
+  };
+  // copy stream order: H2D(0), H2D(1), D2H(0), H2D(2), D2H(1), ...: every H2D is queued before the
+  // D2H that waits on the previous chunk's kernels, so uploads run ahead of the compute stream
+  for (int k = 0; k < nch; ++k) {
+    const int L0 = bounds[k], L1 = bounds[k + 1];
+    // chunk k's LPT orders are computed on the host while the device works on chunk k-1
+    lpt_orders_range(b, L0, L1, oa + L0, oo + L0);
+    const size_t a0 = b->atom_off[L0], a1 = b->atom_off[L1], f0 = b->frag_off[L0], f1 = b->frag_off[L1];
+    DS_CUDA(cudaMemcpyAsync((float4 *)c->b_atoms.p + a0, hp[3] + 16 * a0, 16 * (a1 - a0), cudaMemcpyHostToDevice, cs));
+    if (f1 > f0)
+      DS_CUDA(cudaMemcpyAsync((char *)c->b_frags.p + 32 * f0, hp[4] + 32 * f0, 32 * (f1 - f0), cudaMemcpyHostToDevice, cs));
+    DS_CUDA(cudaMemcpyAsync((int *)c->b_order_a.p + L0, oa + L0, 4ull * (L1 - L0), cudaMemcpyHostToDevice, cs));
+    DS_CUDA(cudaMemcpyAsync((int *)c->b_order_o.p + L0, oo + L0, 4ull * (L1 - L0), cudaMemcpyHostToDevice, cs));
+    cudaEventRecord(c->pev[4 * k], cs);
+    DS_CUDA(cudaStreamWaitEvent(c->stream, c->pev[4 * k], 0));
+    if ((rc = run_batched_range(c, pk, L0, L1, b->atom_off[L0], (int64_t)b->atom_off[L1] - b->atom_off[L0], dp,
+                                out->best_coords != nullptr, out->best_torsion != nullptr, out->restarts != nullptr,
+                                st, c->pev[4 * k + 1], c->pev[4 * k + 2], c->pev[4 * k + 3], queue + 64 * k)))
+      return rc;
+    if (k > 0 && (rc = d2h(k - 1))) return rc;
   }
+  if ((rc = d2h(nch - 1))) return rc;
+  if (st) st->h2d_bytes += (int64_t)(src[0].bytes + src[1].bytes + src[2].bytes + src[3].bytes + src[4].bytes + 8ull * L);
   cudaEventRecord(c->ev[4], cs);
   DS_CUDA(cudaStreamSynchronize(cs));
   DS_CUDA(cudaStreamSynchronize(c->stream));
