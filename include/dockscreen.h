@@ -242,6 +242,12 @@ int ds_generate_pocket_atoms(int64_t seed, int32_t n, float rmin, float rmax,
 /* SPEC.md:453 build_pocket grid (x-fastest).  values == NULL: size query. */
 int ds_build_pocket_grid(const float *atom_xyz, int32_t n_atoms, float spacing, float padding,
                          float origin[3], int32_t dims[3], int32_t *values);
+/* The same grid built on the ctx's device (thread per node; bit-identical to ds_build_pocket_grid,
+ * DESIGN.md §3 P18).  values: host buffer of dims[0]*dims[1]*dims[2] int32 (query the size with
+ * ds_build_pocket_grid(..., NULL) first); device_ms (optional): kernel time.  SURVEY §8(f) rank 2. */
+int ds_build_pocket_grid_device(ds_ctx *ctx, const float *atom_xyz, int32_t n_atoms, float spacing,
+                                float padding, float origin[3], int32_t dims[3], int32_t *values,
+                                float *device_ms);
 /* Seeded symmetric 16x16 interaction table in [-1, 1]. */
 int ds_default_table(int64_t seed, float *table /* 256 */);
 

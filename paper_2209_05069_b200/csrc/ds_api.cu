@@ -29,6 +29,8 @@ int select_blocks_per_sm(size_t smem);
 void launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
                           cudaStream_t st);
 size_t latency_rec_bytes();
+void launch_build_pocket(const float *atom_xyz, int P, const double *origin, double s, const int *dims,
+                         int32_t *values, int sm_count, cudaStream_t st);
 void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *scores,
                              OptOut out, void *recs, int *done, cudaStream_t st);
 void launch_grid_score(const PocketView &pk, const float *coords, int n_atoms, int n_poses, int32_t *out,
@@ -1081,6 +1083,36 @@ int ds_batch_download(ds_ctx *c, ds_dev_batch *d, const ds_outputs *out) {
 }
 
 void ds_batch_destroy(ds_dev_batch *d) { delete d; }
+
+int ds_build_pocket_grid_device(ds_ctx *c, const float *atom_xyz, int32_t n_atoms, float spacing, float padding,
+                                float origin[3], int32_t dims[3], int32_t *values, float *device_ms) {
+  if (!c || !values) return fail(DS_ERR_INVALID_ARG, "NULL argument");
+  int rc = ds_build_pocket_grid(atom_xyz, n_atoms, spacing, padding, origin, dims, nullptr);  // origin, dims
+  if (rc == DS_ERR_EMPTY_POCKET) return fail(rc, "build_pocket needs at least one atom");
+  if (rc) return fail(rc, "bad build_pocket arguments");
+  DS_CUDA(enter_device(c->device));
+  const size_t n = (size_t)dims[0] * dims[1] * dims[2];
+  void *d_atoms = nullptr, *d_vals = nullptr;
+  if (cudaMalloc(&d_atoms, 12ull * n_atoms) != cudaSuccess || cudaMalloc(&d_vals, 4 * n) != cudaSuccess) {
+    cudaFree(d_atoms);
+    return fail(DS_ERR_OOM, "build_pocket buffers");
+  }
+  c->allocs += 2;
+  const double o[3] = {(double)origin[0], (double)origin[1], (double)origin[2]};
+  const int dd[3] = {dims[0], dims[1], dims[2]};
+  cudaMemcpyAsync(d_atoms, atom_xyz, 12ull * n_atoms, cudaMemcpyHostToDevice, c->stream);
+  cudaEventRecord(c->ev[1], c->stream);
+  launch_build_pocket((const float *)d_atoms, n_atoms, o, (double)spacing, dd, (int32_t *)d_vals, c->sm_count,
+                      c->stream);
+  cudaEventRecord(c->ev[2], c->stream);
+  cudaMemcpyAsync(values, d_vals, 4 * n, cudaMemcpyDeviceToHost, c->stream);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess && device_ms) cudaEventElapsedTime(device_ms, c->ev[1], c->ev[2]);
+  cudaFree(d_atoms);
+  cudaFree(d_vals);
+  if (e != cudaSuccess) return fail(DS_ERR_CUDA, "build_pocket: %s", cudaGetErrorString(e));
+  return DS_OK;
+}
 
 int ds_query_capacity(ds_ctx *c, int range_idx, int *ligands) {
   if (!c || !ligands || range_idx < 0 || range_idx > 4) return fail(DS_ERR_INVALID_ARG, "bad argument");

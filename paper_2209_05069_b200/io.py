@@ -79,14 +79,18 @@ def pocket_atoms(n_atoms: int = 200, seed: int = 7, rmin: float = 7.0, rmax: flo
     return [model.Atom.of(*xyz[i], int(typ[i])) for i in range(n_atoms)]
 
 
-def build_pocket(pocket_atoms: Sequence[model.Atom], spacing: float, padding: float) -> model.Pocket:
+def build_pocket(pocket_atoms: Sequence[model.Atom], spacing: float, padding: float, ctx=None) -> model.Pocket:
     """grid over the atom bounding box + padding; node = round(10 g(d)),
-    d = distance to the nearest pocket atom (DESIGN.md §3 P18)."""
+    d = distance to the nearest pocket atom (DESIGN.md §3 P18).  With a `native.Context` the
+    per-node scan runs on its GPU (bit-identical grid)."""
     if len(pocket_atoms) == 0:
         raise model.EmptyPocket("build_pocket needs at least one atom")
     if not spacing > 0:
         raise ValueError("spacing must be > 0")
     xyz = np.ascontiguousarray(np.array([a.position for a in pocket_atoms], dtype=np.float32))
+    if ctx is not None:
+        origin, dims, vals, _ = ctx.build_pocket_grid(xyz, spacing, padding)
+        return model.Pocket(origin, float(np.float32(spacing)), dims, vals, tuple(pocket_atoms))
     origin = (C.c_float * 3)()
     dims = (C.c_int32 * 3)()
     L = lib()

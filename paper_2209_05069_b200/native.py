@@ -123,6 +123,7 @@ def lib():
             "ds_pack_ligands": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "ds_generate_pocket_atoms": (C.c_int, [i64, i32, C.c_float, C.c_float, vp, vp]),
             "ds_build_pocket_grid": (C.c_int, [vp, i32, C.c_float, C.c_float, vp, vp, vp]),
+            "ds_build_pocket_grid_device": (C.c_int, [vp, vp, i32, C.c_float, C.c_float, vp, vp, vp, vp]),
             "ds_default_table": (C.c_int, [i64, vp]),
         }
         for name, (res, args) in sig.items():
@@ -413,6 +414,19 @@ class Context:
 
     def pocket(self, pocket: model.Pocket, table: Optional[InteractionTable] = None) -> DevicePocket:
         return DevicePocket(self, pocket, table or InteractionTable.default())
+
+    def build_pocket_grid(self, atom_xyz: np.ndarray, spacing: float, padding: float):
+        """build_pocket's grid on this context's device, bit-identical to the host build.
+        Returns (origin, dims, values x-fastest int32, kernel ms)."""
+        xyz = np.ascontiguousarray(atom_xyz, dtype=np.float32).reshape(-1, 3)
+        origin = (C.c_float * 3)()
+        dims = (C.c_int32 * 3)()
+        check(lib().ds_build_pocket_grid(_p(xyz), len(xyz), float(spacing), float(padding), origin, dims, None))
+        vals = np.zeros(int(dims[0]) * int(dims[1]) * int(dims[2]), np.int32)
+        ms = C.c_float(0.0)
+        check(lib().ds_build_pocket_grid_device(self.handle, _p(xyz), len(xyz), float(spacing), float(padding), origin,
+                                                dims, _p(vals), C.byref(ms)))
+        return tuple(float(o) for o in origin), tuple(int(d) for d in dims), vals, float(ms.value)
 
     def dock(self, dpocket: DevicePocket, packed: PackedBatch, cfg: model.DockConfig, seed: int = 0,
              family: int = FAMILY_BATCHED, coords: bool = True, detail: bool = False,

@@ -144,3 +144,13 @@ def test_batched_parity_fine_torsion_step(gpu_ctx, synth_pocket, table):
     cfg = model.DockConfig(torsion_step_deg=10)
     g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg)
     compare(batch, g, o, cfg)
+
+
+@pytest.mark.parametrize("spacing,padding,natoms", [(0.5, 4.0, 200), (0.375, 4.0, 200), (0.8, 2.0, 30), (1.0, 4.0, 1)])
+def test_build_pocket_device_matches_host(gpu_ctx, spacing, padding, natoms):
+    """the GPU build_pocket grid is bit-identical to the host build (P18)."""
+    atoms = io.pocket_atoms(natoms, seed=7) if natoms > 1 else [model.Atom.of(0.0, 0.0, 0.0, 3)]
+    host = io.build_pocket(atoms, spacing, padding)
+    dev = io.build_pocket(atoms, spacing, padding, ctx=gpu_ctx)
+    assert dev.grid_origin == host.grid_origin and dev.grid_dims == host.grid_dims
+    assert np.array_equal(np.asarray(dev.grid_values), np.asarray(host.grid_values))
