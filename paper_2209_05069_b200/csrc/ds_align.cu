@@ -40,28 +40,6 @@ __device__ __forceinline__ unsigned grid_u8(const uint8_t *grid, int idx, bool s
   return smem ? (unsigned)grid[idx] : (unsigned)__ldg(grid + idx);
 }
 
-// ---- Blackwell packed f32x2 arithmetic (FFMA2 / FADD2): two IEEE round-to-nearest operations
-// per instruction, each lane of the pair bit-identical to the scalar __fmaf_rn / __fadd_rn ----
-typedef unsigned long long f2_t;
-__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
-  f2_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void f2_unpack(f2_t v, float &lo, float &hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
-  f2_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
-  f2_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-
 // f32x2 form of unit_atom for the constant-angle path: per pair of angles (k, k+1)
 //   UX = fma2(S, VZ, fma2(C, VX, TX)),  UZ = fma2(C, VZ, fma2(-S, VX, TZ)),  + (magic, magic)
 // — lane-for-lane the same operations as the scalar recipe P6/P4, in half the FP32 issue slots.

@@ -93,59 +93,46 @@ __device__ __forceinline__ float3 torsion_pos(const PocketView &pk, int step_t, 
   return torsion_apply(R, a, p.x, p.y, p.z);
 }
 
-// rescore sum of one pose against all pocket atoms (P11).  Lanes own pocket atoms (staged in
-// smem with .w = the integer column offset tj*(nb+1)); ligand atoms are broadcast from S.u whose
-// .w holds the integer row offset ti*16*(nb+1).  Partial sums stay in int32 for <= 64 atoms
-// (|W| <= 2^24) before widening.  The bin comes from the exact look-up table (3 instructions:
-// shift, unsigned min, LDS) when the pocket has one, else from NB compares.
-template <int NB, class SM>
-__device__ __forceinline__ long long rescore_pose(const SM &S, int A, const float4 *pat, int P,
-                                                  const int32_t *wfx, int nb, const float *ub2,
-                                                  const uint8_t *lut, int lut_shift, int lut_cap) {
+// Packed rescore (P11): each lane owns TWO pocket atoms (j and j + 32 of a 64-atom round), staged
+// in shared memory as negated-coordinate pairs, so the squared distances of a ligand atom to both
+// come from FADD2 / FMUL2 / FFMA2 (each half bit-identical to dist2: x - y == x + (-y) exactly).
+// The ligand atom (broadcast) is loaded once for the two pairs.  Bin: LUT or compares.
+template <bool kLut>
+__device__ __forceinline__ long long rescore_pose_x2(const SelWarpSmem &S, int A, const f2_t *pnx, const f2_t *pny,
+                                                     const f2_t *pnz, const int2 *pcol, int nrounds,
+                                                     const int32_t *wfx, int nb, const float *ub2,
+                                                     const uint8_t *lut, int lut_shift, int lut_cap) {
+  const int lane = threadIdx.x & 31;
   long long acc = 0;
-  float u[DS_MAX_BINS];
-  if (NB >= 0) {
-#pragma unroll
-    for (int q = 0; q < DS_MAX_BINS; ++q) u[q] = ub2[q];
-  }
-  for (int j0 = 0; j0 < P; j0 += 32) {
-    const int j = j0 + (threadIdx.x & 31);
-    // past-the-end lanes use a far sentinel: its bin is nb, whose weight is 0
-    const float4 y = j < P ? pat[j] : make_float4(1e19f, 1e19f, 1e19f, 0.f);
-    const int32_t *wcol = wfx + __float_as_int(y.w);
-    for (int i0 = 0; i0 < A; i0 += 64) {
+  for (int k = 0; k < nrounds; ++k) {
+    const f2_t NX = pnx[k * 32 + lane], NY = pny[k * 32 + lane], NZ = pnz[k * 32 + lane];
+    const int2 col = pcol[k * 32 + lane];
+    for (int i0 = 0; i0 < A; i0 += 64) {  // int32 partials over <= 64 atoms (|W| <= 2^24)
       int part = 0;
       const int i1 = min(A, i0 + 64);
       for (int i = i0; i < i1; ++i) {
         const float4 x = S.u[i];
-        const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
-        int b = __float_as_int(x.w);
-        if (NB < 0) {
-          // d2 >= +0 (never -0), so bits order is value order; NaN/inf clamp to the last entry (nb)
-          b += lut[min((unsigned)__float_as_int(d2) >> lut_shift, (unsigned)lut_cap)];
-        } else if (NB > 0) {
-          // bin = #{q : !(d2 < u_q)}; d2 >= +0 and u_q > 0, so float order == bit order and
-          // (bits(d2) - bits(u_q)) >> 31 is -1 exactly when d2 < u_q (NaN/inf count as beyond)
-          const int d2b = __float_as_int(d2);
-          b += NB;
-#pragma unroll
-          for (int q = 0; q < NB; ++q) b += (d2b - __float_as_int(u[q])) >> 31;
+        const f2_t DX = f2_add(f2_pack(x.x, x.x), NX);
+        const f2_t DY = f2_add(f2_pack(x.y, x.y), NY);
+        const f2_t DZ = f2_add(f2_pack(x.z, x.z), NZ);
+        float d0, d1;
+        f2_unpack(f2_fma(DZ, DZ, f2_fma(DY, DY, f2_mul(DX, DX))), d0, d1);
+        int b0 = __float_as_int(x.w) + col.x, b1 = __float_as_int(x.w) + col.y;
+        if (kLut) {
+          b0 += lut[min((unsigned)__float_as_int(d0) >> lut_shift, (unsigned)lut_cap)];
+          b1 += lut[min((unsigned)__float_as_int(d1) >> lut_shift, (unsigned)lut_cap)];
         } else {
-          for (int q = 0; q < nb; ++q) b += !(d2 < u[q]);
+          for (int q = 0; q < nb; ++q) {
+            b0 += !(d0 < ub2[q]);
+            b1 += !(d1 < ub2[q]);
+          }
         }
-        part += wcol[b];
+        part += wfx[b0] + wfx[b1];
       }
       acc += part;
     }
   }
   return acc;
-}
-
-// cold paths kept out of line so the hot loops stay compact in the instruction cache
-template <class SM>
-__device__ __noinline__ long long rescore_pose_generic(const SM &S, int A, const float4 *pat, int P,
-                                                       const int32_t *wfx, int nb, const float *ub2) {
-  return rescore_pose<0, SM>(S, A, pat, P, wfx, nb, ub2, nullptr, 0, 0);
 }
 
 // select_poses (P12) dissimilarity bitsets: pairs (p < q) of valid poses over lanes; heavy-atom sum
@@ -539,15 +526,28 @@ __global__ void __launch_bounds__(kOptWarps * 32)
   SelWarpSmem &S = s_warp[warp];
   // per-CTA: pocket atoms + fixed-point weights + bin bounds + bin LUT
   const int nb1 = pk.nb + 1;
-  float4 *s_pat = reinterpret_cast<float4 *>(smem);
-  int32_t *s_w = reinterpret_cast<int32_t *>(s_pat + pk.n_atoms);
+  // pocket atoms as 64-atom rounds of lane pairs (j, j + 32): negated coordinates + weight columns
+  const int nrounds = (pk.n_atoms + 63) / 64;
+  f2_t *s_nx = reinterpret_cast<f2_t *>(smem);
+  f2_t *s_ny = s_nx + nrounds * 32;
+  f2_t *s_nz = s_ny + nrounds * 32;
+  int2 *s_col = reinterpret_cast<int2 *>(s_nz + nrounds * 32);
+  int32_t *s_w = reinterpret_cast<int32_t *>(s_col + nrounds * 32);
   const int wsz = DS_N_TYPES * DS_N_TYPES * nb1;
   float *s_ub2 = reinterpret_cast<float *>(s_w + wsz);
   uint8_t *s_lut = reinterpret_cast<uint8_t *>(s_ub2 + DS_MAX_BINS);
-  for (int j = threadIdx.x; j < pk.n_atoms; j += blockDim.x) {
-    float4 y = __ldg(pk.patoms + j);
-    y.w = __int_as_float((int)y.w * nb1);  // column offset of the pocket atom's type in the weight table
-    s_pat[j] = y;
+  for (int e = threadIdx.x; e < nrounds * 32; e += blockDim.x) {
+    const int k = e >> 5, l = e & 31;
+    float4 y[2];
+    for (int h = 0; h < 2; ++h) {
+      const int j = k * 64 + h * 32 + l;
+      // past-the-end: a far sentinel, beyond every bin (weight column of type 0, entry nb -> 0)
+      y[h] = j < pk.n_atoms ? __ldg(pk.patoms + j) : make_float4(1e19f, 1e19f, 1e19f, 0.f);
+    }
+    s_nx[e] = f2_pack(-y[0].x, -y[1].x);
+    s_ny[e] = f2_pack(-y[0].y, -y[1].y);
+    s_nz[e] = f2_pack(-y[0].z, -y[1].z);
+    s_col[e] = make_int2((int)y[0].w * nb1, (int)y[1].w * nb1);
   }
   for (int j = threadIdx.x; j < wsz; j += blockDim.x) s_w[j] = __ldg(pk.wfx + j);
   if (threadIdx.x < DS_MAX_BINS) s_ub2[threadIdx.x] = pk.ub2[threadIdx.x];
@@ -620,9 +620,11 @@ __global__ void __launch_bounds__(kOptWarps * 32)
         S.u[i] = x;
       }
       __syncwarp();
-      long long acc = pk.lut_cap >= 0 ? rescore_pose<-1>(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2, s_lut,
-                                                         pk.lut_shift, pk.lut_cap)
-                                      : rescore_pose_generic(S, A, s_pat, pk.n_atoms, s_w, pk.nb, s_ub2);
+      long long acc = pk.lut_cap >= 0
+                          ? rescore_pose_x2<true>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut,
+                                                  pk.lut_shift, pk.lut_cap)
+                          : rescore_pose_x2<false>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2,
+                                                   s_lut, 0, 0);
       acc = warp_sum64(acc);
       if (best_r < 0 || acc > best_chem || (acc == best_chem && r < best_r)) {
         best_chem = acc;
@@ -657,8 +659,8 @@ __global__ void __launch_bounds__(kOptWarps * 32)
 }
 
 size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap) {
-  size_t fixed = (size_t)n_patoms * 16 + (size_t)DS_N_TYPES * DS_N_TYPES * (nb + 1) * 4 + DS_MAX_BINS * 4 +
-                 (size_t)(lut_cap + 1);
+  size_t fixed = (size_t)((n_patoms + 63) / 64) * 32 * 32 + (size_t)DS_N_TYPES * DS_N_TYPES * (nb + 1) * 4 +
+                 DS_MAX_BINS * 4 + (size_t)(lut_cap + 1);
   return (fixed + 15) & ~(size_t)15;
 }
 
