@@ -60,6 +60,12 @@ __device__ __forceinline__ unsigned clamp_bits(float u, unsigned bound) {
   const unsigned b = (unsigned)__float_as_int(__fadd_rn(u, kMagic)) - (unsigned)(kMagicBits - 1);
   return min(b, bound);
 }
+// node index from coordinates that already carry the +1.5*2^23 magic add (packed callers)
+__device__ __forceinline__ int node_index_magic(const GridGeom &g, float mx, float my, float mz) {
+  const unsigned K = (unsigned)(kMagicBits - 1);
+  return (int)(min((unsigned)__float_as_int(mx) - K, g.bx) + g.NX * min((unsigned)__float_as_int(my) - K, g.by) +
+               g.NXY * min((unsigned)__float_as_int(mz) - K, g.bz));
+}
 __device__ __forceinline__ int node_index(const GridGeom &g, float ux, float uy, float uz) {
   return (int)(clamp_bits(ux, g.bx) + g.NX * clamp_bits(uy, g.by) + g.NXY * clamp_bits(uz, g.bz));
 }

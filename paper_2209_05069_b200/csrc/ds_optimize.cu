@@ -38,9 +38,11 @@ constexpr int kTorWarps = 8;         // warps per CTA of the torsion kernel (1-w
 // Per-warp shared scratch of the torsion kernel (53 KB per 8-warp CTA: 4 CTAs per SM).
 struct TorWarpSmem {
   float4 u[kMaxA];          // committed pose of the current restart (grid frame), .w = type
-  // moving atoms of the current fragment, ascending: position + an info word
+  // moving atoms of the current fragment, ascending, as structure-of-arrays so that the two atoms a
+  // sweep lane takes per round (slots 2j, 2j+1) load as one f32x2 pair per coordinate; info word:
   //   bits 0-7 bump-candidate count, 8-15 / 16-23 / 24-31 the first three candidates
-  float4 mw[kMaxA];
+  f2_t mxp[kMaxA / 2 + 1], myp[kMaxA / 2 + 1], mzp[kMaxA / 2 + 1];
+  uint2 mip[kMaxA / 2 + 1];
   float2 chr[kMaxA];        // cylindrical (h, r): C' atoms in [0, nC), moving atom m at kMaxA-1-m
   uint8_t clist[kMaxA];     // complement atom indices, ascending
   uint16_t ovf[kOvf];       // candidates beyond kInline: moving slot << 8 | atom index
@@ -277,7 +279,13 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           const unsigned bm = __ballot_sync(kFull, mv), bc = __ballot_sync(kFull, cp);
           if (in) {
             const float4 p = S.u[i];
-            if (mv) S.mw[nM + __popc(bm & lt)] = make_float4(p.x, p.y, p.z, 0.f);  // info word = 0
+            if (mv) {
+              const int m = nM + __popc(bm & lt);
+              reinterpret_cast<float *>(S.mxp)[m] = p.x;
+              reinterpret_cast<float *>(S.myp)[m] = p.y;
+              reinterpret_cast<float *>(S.mzp)[m] = p.z;
+              reinterpret_cast<unsigned *>(S.mip)[m] = 0u;  // info word
+            }
             else base += grid_val(pk, node_index(g, p.x, p.y, p.z));
           }
           if (cp) S.clist[nC + __popc(bc & lt)] = (uint8_t)i;
@@ -312,7 +320,9 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         int hlo = 0x7FFFFFFF, hhi = (int)0x80000000, rhi = 0;
         if (lane == 0) S.n_ovf = 0;
         for (int m = lane; m < nM; m += 32) {
-          const float2 hr = cyl_coords(S.mw[m], a3, kx, ky, kz);
+          const float4 pm = make_float4(reinterpret_cast<const float *>(S.mxp)[m], reinterpret_cast<const float *>(S.myp)[m],
+                                        reinterpret_cast<const float *>(S.mzp)[m], 0.f);
+          const float2 hr = cyl_coords(pm, a3, kx, ky, kz);
           S.chr[kMaxA - 1 - m] = hr;
           hlo = min(hlo, ordered_bits(hr.x));
           hhi = max(hhi, ordered_bits(hr.x));
@@ -363,7 +373,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
               ++cnt;
             }
           }
-          if (ok) reinterpret_cast<unsigned *>(&S.mw[m].w)[0] = cnt | inl;  // cnt <= nCf < 256
+          if (ok) reinterpret_cast<unsigned *>(S.mip)[m] = cnt | inl;  // cnt <= nCf < 256
         }
         unsigned best_key = 0;  // (score + 32768) << 16 | (65535 - angle); 0 = no clean angle
         __syncwarp();
@@ -401,25 +411,43 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           }
           bool bumped = false;
           int part = 0, nact = 0;
-          // two moving atoms per lane and round (m0 + gi and m0 + G + gi): twice the independent work
-          // (two grid loads in flight) for the same loop and retirement overhead
+          // two moving atoms per lane and round (slots m0 + 2 gi and m0 + 2 gi + 1): twice the
+          // independent work (two grid loads in flight) for the same loop and retirement overhead,
+          // and the two rotations run as packed f32x2 (FADD2 / FFMA2, each half the scalar recipe)
+          const f2_t R0 = f2_pack(R[0], R[0]), R1 = f2_pack(R[1], R[1]), R2 = f2_pack(R[2], R[2]);
+          const f2_t R3 = f2_pack(R[3], R[3]), R4 = f2_pack(R[4], R[4]), R5 = f2_pack(R[5], R[5]);
+          const f2_t R6 = f2_pack(R[6], R[6]), R7 = f2_pack(R[7], R[7]), R8 = f2_pack(R[8], R[8]);
+          const f2_t AX = f2_pack(ar.x, ar.x), AY = f2_pack(ar.y, ar.y), AZ = f2_pack(ar.z, ar.z);
+          const f2_t NAX = f2_pack(-ar.x, -ar.x), NAY = f2_pack(-ar.y, -ar.y), NAZ = f2_pack(-ar.z, -ar.z);
+          const f2_t MM = f2_pack(kMagic, kMagic);
           for (int m0 = 0; m0 < nM; m0 += 2 * G) {
-            const int m1 = m0 + gi, m2 = m1 + G;
+            const int m1 = m0 + 2 * gi, m2 = m1 + 1;
             // with early exit a bumped angle is retired; without it every pair is checked
             const bool live = lane_ok && !(dp.early_exit && bumped);
             const bool act1 = live && m1 < nM, act2 = live && m2 < nM;
             if (!__any_sync(kFull, act1)) break;
             bool hit = false;
             if (act1) {
-              const float4 W1 = S.mw[m1];
-              const float4 W2 = S.mw[act2 ? m2 : m1];
-              const float3 q1 = torsion_apply(R, ar, W1.x, W1.y, W1.z);
-              const float3 q2 = torsion_apply(R, ar, W2.x, W2.y, W2.z);
+              const int j = m1 >> 1;
+              // w = p - a (as p + (-a): exact negation), p' = R w + a (P8), then + magic (P4)
+              const f2_t WX = f2_add(S.mxp[j], NAX), WY = f2_add(S.myp[j], NAY), WZ = f2_add(S.mzp[j], NAZ);
+              const f2_t QX = f2_fma(R2, WZ, f2_fma(R1, WY, f2_fma(R0, WX, AX)));
+              const f2_t QY = f2_fma(R5, WZ, f2_fma(R4, WY, f2_fma(R3, WX, AY)));
+              const f2_t QZ = f2_fma(R8, WZ, f2_fma(R7, WY, f2_fma(R6, WX, AZ)));
+              float mx1, mx2, my1, my2, mz1, mz2;
+              f2_unpack(f2_add(QX, MM), mx1, mx2);
+              f2_unpack(f2_add(QY, MM), my1, my2);
+              f2_unpack(f2_add(QZ, MM), mz1, mz2);
               // both grid loads are issued before the candidate checks: they hide each other's latency
-              const int gv1 = grid_val(pk, node_index(g, q1.x, q1.y, q1.z));
-              const int gv2 = grid_val(pk, node_index(g, q2.x, q2.y, q2.z));
-              const bool h1 = bump_hit(S, __float_as_uint(W1.w), q1, m1, n_ovf, nCf, dp.bd2);
-              const bool h2 = act2 && bump_hit(S, __float_as_uint(W2.w), q2, m2, n_ovf, nCf, dp.bd2);
+              const int gv1 = grid_val(pk, node_index_magic(g, mx1, my1, mz1));
+              const int gv2 = grid_val(pk, node_index_magic(g, mx2, my2, mz2));
+              float3 q1, q2;
+              f2_unpack(QX, q1.x, q2.x);
+              f2_unpack(QY, q1.y, q2.y);
+              f2_unpack(QZ, q1.z, q2.z);
+              const uint2 info = S.mip[j];
+              const bool h1 = bump_hit(S, info.x, q1, m1, n_ovf, nCf, dp.bd2);
+              const bool h2 = act2 && bump_hit(S, info.y, q2, m2, n_ovf, nCf, dp.bd2);
               part += (h1 ? 0 : gv1) + (act2 && !h2 ? gv2 : 0);
               nact += act2 ? 2 : 1;
               hit = h1 || h2;
@@ -461,7 +489,10 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
             const bool mv = i < A && ((gm[s] >> lane) & 1u);
             const unsigned bm = __ballot_sync(kFull, mv);
             if (mv) {
-              const float4 W = S.mw[mr + __popc(bm & lt)];
+              const int m = mr + __popc(bm & lt);
+              const float4 W = make_float4(reinterpret_cast<const float *>(S.mxp)[m],
+                                           reinterpret_cast<const float *>(S.myp)[m],
+                                           reinterpret_cast<const float *>(S.mzp)[m], 0.f);
               const float3 q = torsion_pos(pk, dp.step_t, best_k, kx, ky, kz, a3, W);
               S.u[i] = make_float4(q.x, q.y, q.z, S.u[i].w);
             }
