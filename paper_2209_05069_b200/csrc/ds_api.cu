@@ -867,7 +867,21 @@ int dock_pipelined(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const
     c->pev.push_back(e);
   }
   std::vector<int> bounds(nch + 1);
-  for (int k = 0; k <= nch; ++k) bounds[k] = (int)((int64_t)L * k / nch);
+  // tapered chunks: the first and last are a quarter of the inner ones, so the un-overlapped head
+  // (first H2D) and tail (last D2H) of the pipeline stay short (DS_PIPELINE_TAPER=0: equal chunks)
+  {
+    const char *e = getenv("DS_PIPELINE_TAPER");
+    const bool taper = (e ? atoi(e) : 1) && nch >= 3;
+    std::vector<double> w(nch, 1.0);
+    if (taper) w[0] = w[nch - 1] = 0.25;
+    double tot = 0, run = 0;
+    for (double x : w) tot += x;
+    bounds[0] = 0;
+    for (int k = 0; k < nch; ++k) {
+      run += w[k];
+      bounds[k + 1] = k + 1 == nch ? L : (int)((double)L * run / tot);
+    }
+  }
   // host side: LPT orders per chunk; pageable inputs go through the pinned staging buffer
   struct Src {
     const void *p;
