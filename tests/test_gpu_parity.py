@@ -154,3 +154,30 @@ def test_build_pocket_device_matches_host(gpu_ctx, spacing, padding, natoms):
     dev = io.build_pocket(atoms, spacing, padding, ctx=gpu_ctx)
     assert dev.grid_origin == host.grid_origin and dev.grid_dims == host.grid_dims
     assert np.array_equal(np.asarray(dev.grid_values), np.asarray(host.grid_values))
+
+
+@pytest.mark.parametrize("n", [64, 6000])
+def test_ds_dock_transfer_paths_match_resident(gpu_ctx, synth_pocket, table, n):
+    """Both unchunked ds_dock transfer paths — the express path (n = 64: one H2D of a packed input
+    arena, one D2H of an output arena) and the per-array path (n = 6000: > 4 MB of inputs) — give
+    the resident path's records, best poses and per-restart detail, for both kernel families."""
+    from paper_2209_05069_b200.native import FAMILY_LATENCY, ResidentBatch
+    batch = io.generate_mixed_batch(n, seed=23)
+    cfg = model.DockConfig()
+    dp = gpu_ctx.pocket(synth_pocket, table)
+    packed = pack(batch)
+    for fam in (FAMILY_BATCHED, FAMILY_LATENCY) if n <= 64 else (FAMILY_BATCHED,):
+        g = gpu_ctx.dock(dp, packed, cfg, 1, fam, coords=True, detail=True)
+        rb = ResidentBatch(gpu_ctx, packed)
+        rb.dock(dp, cfg, seed=1, family=fam)
+        r = rb.download()
+        rb.close()
+        # the latency family retires bumped angles through a shared flag other threads poll, so how
+        # many pairs are resolved before retirement (bump_checks, P14) varies run to run; every
+        # result field and the exact counters must agree
+        fields = [f for f in r.dtype.names if not (fam == FAMILY_LATENCY and f == "bump_checks")]
+        for f in fields:
+            assert np.array_equal(g.results[f], r[f]), (fam, f)
+    if n <= 64:
+        o = oracle.dock_batch(batch, synth_pocket, table, cfg, 1)
+        compare(batch, g, o, cfg)
