@@ -195,6 +195,11 @@ def run_reference(args, rank, world):
 def main():
     args = parse()
     rank, world, local = dist_env()
+    # one process per GPU shares the host: split the cores between the local ranks so the OpenMP
+    # host work (batch validation, generation, the CPU baseline) does not oversubscribe them
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if local_world > 1 and "OMP_NUM_THREADS" not in os.environ:
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // local_world))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
