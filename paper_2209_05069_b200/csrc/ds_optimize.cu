@@ -13,15 +13,16 @@
 //    0.02-node margin that dwarfs f32 rounding) are resolved once per fragment instead of once per
 //    angle; the survivors (~1.5 % of pairs on the config-3 mix) are recorded with the moving atom
 //    (three inline, the rest in a short per-fragment list) and checked exactly with P9 per angle;
-//  * all torsion angles at once: lanes own (angle, moving atom) slots, rotate their atom in
-//    registers and test its candidates; a hit marks the angle bumped, clean slots add their grid
-//    value to base + sum over M (non-moving atoms do not change);
+//  * all torsion angles at once: lanes own (angle, two moving atoms) slots from a host-built lane
+//    table, rotate their atoms with packed f32x2 arithmetic in registers and test their candidates;
+//    a hit marks the angle bumped, clean slots add their grid values to base + sum over M
+//    (non-moving atoms do not change);
 //  * the best clean angle (ties -> smallest) is committed.
 // The final pose of every restart goes to a per-ligand slot in HBM (L2-resident in practice).
 //
 // k_select_batched — select_poses (heavy-atom RMSD in f64, lanes over pose pairs) and an integer
-// fixed-point rescore (order-free, exact) with pocket atoms, weights and the bin table staged in
-// shared memory.
+// fixed-point rescore (order-free, exact) with pocket atoms (negated-coordinate f32x2 pairs, two
+// per lane), weights and the bin look-up table staged in shared memory.
 #include "ds_kernels.cuh"
 
 namespace ds {
