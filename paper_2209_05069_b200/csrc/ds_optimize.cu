@@ -44,7 +44,9 @@ struct TorWarpSmem {
   //   bits 0-7 bump-candidate count, 8-15 / 16-23 / 24-31 the first three candidates
   f2_t mxp[kMaxA / 2 + 1], myp[kMaxA / 2 + 1], mzp[kMaxA / 2 + 1];
   uint2 mip[kMaxA / 2 + 1];
-  float2 chr[kMaxA];        // cylindrical (h, r): C' atoms in [0, nC), moving atom m at kMaxA-1-m
+  // cylindrical (h, r) as two arrays (C' pairs load as f32x2): C' atoms in [0, nCf) (+ one far pad
+  // entry), moving atom m at kMaxA-1-m
+  f2_t chh2[kMaxA / 2], chr2[kMaxA / 2];
   uint8_t clist[kMaxA];     // complement atom indices, ascending
   uint16_t ovf[kOvf];       // candidates beyond kInline: moving slot << 8 | atom index
   int n_ovf;                // entries appended (> kOvf: the list overflowed, scan C')
@@ -324,7 +326,8 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           const float4 pm = make_float4(reinterpret_cast<const float *>(S.mxp)[m], reinterpret_cast<const float *>(S.myp)[m],
                                         reinterpret_cast<const float *>(S.mzp)[m], 0.f);
           const float2 hr = cyl_coords(pm, a3, kx, ky, kz);
-          S.chr[kMaxA - 1 - m] = hr;
+          reinterpret_cast<float *>(S.chh2)[kMaxA - 1 - m] = hr.x;
+          reinterpret_cast<float *>(S.chr2)[kMaxA - 1 - m] = hr.y;
           hlo = min(hlo, ordered_bits(hr.x));
           hhi = max(hhi, ordered_bits(hr.x));
           rhi = max(rhi, __float_as_int(hr.y));  // r >= +0: bit order is float order
@@ -347,10 +350,17 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           const unsigned bk = __ballot_sync(kFull, keep);  // in-place compaction: slot <= c
           if (keep) {
             const int slot = nCf + __popc(bk & lt);
-            S.chr[slot] = hr;
+            reinterpret_cast<float *>(S.chh2)[slot] = hr.x;
+            reinterpret_cast<float *>(S.chr2)[slot] = hr.y;
             S.clist[slot] = ci;
           }
           nCf += __popc(bk);
+        }
+        // far pad after the last C' entry (slot nCf < kMaxA - nM since nCf + nM <= A - 2): an odd
+        // nCf still tests whole f32x2 pairs and the pad never passes the bound
+        if (lane == 0) {
+          reinterpret_cast<float *>(S.chh2)[nCf] = 3.0e38f;
+          reinterpret_cast<float *>(S.chr2)[nCf] = 3.0e38f;
         }
         __syncwarp();
         // lane = moving atom, loop over the prefiltered C' (broadcast reads): the lane owns its info
@@ -358,20 +368,30 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         for (int m0 = 0; m0 < nM; m0 += 32) {
           const int m = m0 + lane;
           const bool ok = m < nM;
-          const float2 hm = ok ? S.chr[kMaxA - 1 - m] : make_float2(3.0e38f, 3.0e38f);
+          const float hmh = ok ? reinterpret_cast<const float *>(S.chh2)[kMaxA - 1 - m] : 3.0e38f;
+          const float hmr = ok ? reinterpret_cast<const float *>(S.chr2)[kMaxA - 1 - m] : 3.0e38f;
+          const f2_t HM = f2_pack(hmh, hmh), RM = f2_pack(hmr, hmr);
           unsigned cnt = 0, inl = 0;
-          for (int c = 0; c < nCf; ++c) {
-            const float2 hc = S.chr[c];
-            const float dh = __fsub_rn(hm.x, hc.x), dr = __fsub_rn(hm.y, hc.y);
-            if (__fmaf_rn(dh, dh, __fmul_rn(dr, dr)) < dp.cull2) {
-              const unsigned ci = S.clist[c];
-              if (cnt < (unsigned)kInline) {
-                inl |= ci << (8 + 8 * cnt);
-              } else {
-                const int slot = atomicAdd(&S.n_ovf, 1);
-                if (slot < kOvf) S.ovf[slot] = (uint16_t)((m << 8) | ci);
+          // two C' atoms per iteration with packed f32x2 (the bound is conservative, so any rounding
+          // of this test is fine)
+          for (int c = 0; c < nCf; c += 2) {
+            const f2_t DH = f2_sub(HM, S.chh2[c >> 1]), DR = f2_sub(RM, S.chr2[c >> 1]);
+            float d0, d1;
+            f2_unpack(f2_fma(DH, DH, f2_mul(DR, DR)), d0, d1);
+            const bool k0 = d0 < dp.cull2, k1 = d1 < dp.cull2;
+            if (k0 || k1) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                if (!(h ? k1 : k0)) continue;
+                const unsigned ci = S.clist[c + h];
+                if (cnt < (unsigned)kInline) {
+                  inl |= ci << (8 + 8 * cnt);
+                } else {
+                  const int slot = atomicAdd(&S.n_ovf, 1);
+                  if (slot < kOvf) S.ovf[slot] = (uint16_t)((m << 8) | ci);
+                }
+                ++cnt;
               }
-              ++cnt;
             }
           }
           if (ok) reinterpret_cast<unsigned *>(S.mip)[m] = cnt | inl;  // cnt <= nCf < 256
