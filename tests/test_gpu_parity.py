@@ -181,3 +181,15 @@ def test_ds_dock_transfer_paths_match_resident(gpu_ctx, synth_pocket, table, n):
     if n <= 64:
         o = oracle.dock_batch(batch, synth_pocket, table, cfg, 1)
         compare(batch, g, o, cfg)
+
+
+def test_parity_large_mixed_both_families(gpu_ctx, synth_pocket, table):
+    """2,000 mixed config-3 ligands through the batched family and 300 through the latency family,
+    every field against the oracle (rare paths: overflow lists, all-bump fragments, invalid poses)."""
+    batch = io.generate_mixed_batch(2000, seed=31)
+    cfg = model.DockConfig()
+    g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg, seed=5)
+    compare(batch, g, o, cfg)
+    sub = batch.subset(range(0, 2000, 7)[:300])
+    g, o = _run(gpu_ctx, sub, synth_pocket, table, cfg, seed=5, family=FAMILY_LATENCY)
+    compare(sub, g, o, cfg)
