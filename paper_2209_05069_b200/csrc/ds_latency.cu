@@ -53,9 +53,16 @@ struct LatSmem {
   int heavy;
 };
 
-// exact rescore bin (P11): the pocket's LUT when it has one, else the compares
-__device__ __forceinline__ int lat_bin(const PocketView &pk, float d2) {
-  if (pk.lut_cap >= 0) return __ldg(pk.bin_lut + min((unsigned)__float_as_int(d2) >> pk.lut_shift, (unsigned)pk.lut_cap));
+// dynamic shared memory: [trig 360][fragment records][weights][bin LUT][grid (if it fits)]
+__host__ __device__ inline size_t lat_w_bytes(int nb) { return ((size_t)DS_N_TYPES * DS_N_TYPES * (nb + 1) * 4 + 15) & ~(size_t)15; }
+__host__ __device__ inline size_t lat_lut_bytes(int lut_cap) { return ((size_t)(lut_cap + 1) + 15) & ~(size_t)15; }
+__host__ __device__ inline size_t lat_base_bytes(int nb, int lut_cap) {
+  return 360 * sizeof(float2) + 2 * (DS_MAX_ATOMS - 2) * sizeof(uint4) + lat_w_bytes(nb) + lat_lut_bytes(lut_cap);
+}
+
+// exact rescore bin (P11): the pocket's LUT (staged in shared memory) when it has one, else the compares
+__device__ __forceinline__ int lat_bin(const PocketView &pk, const uint8_t *slut, float d2) {
+  if (pk.lut_cap >= 0) return slut[min((unsigned)__float_as_int(d2) >> pk.lut_shift, (unsigned)pk.lut_cap)];
   int b = 0;
   for (int q = 0; q < pk.nb; ++q) b += !(d2 < pk.ub2[q]);
   return b;
@@ -100,8 +107,12 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   const uint8_t *grid = pk.grid;
   for (int i = tid; i < 360; i += kLatThreads) strig[i] = pk.trig[i];
   for (int i = tid; i < 2 * F; i += kLatThreads) sfrag[i] = __ldg(bt.frags + 2 * (size_t)f0 + i);
+  int32_t *sw = reinterpret_cast<int32_t *>(dsm + 360 * sizeof(float2) + 2 * (DS_MAX_ATOMS - 2) * sizeof(uint4));
+  uint8_t *slut = reinterpret_cast<uint8_t *>(sw) + lat_w_bytes(pk.nb);
+  for (int i = tid; i < DS_N_TYPES * DS_N_TYPES * (pk.nb + 1); i += kLatThreads) sw[i] = __ldg(pk.wfx + i);
+  for (int i = tid; i <= pk.lut_cap; i += kLatThreads) slut[i] = __ldg(pk.bin_lut + i);
   if (kSmemGrid) {
-    int4 *dst = reinterpret_cast<int4 *>(dsm + 360 * sizeof(float2) + 2 * (DS_MAX_ATOMS - 2) * sizeof(uint4));
+    int4 *dst = reinterpret_cast<int4 *>(dsm + lat_base_bytes(pk.nb, pk.lut_cap));
     const int4 *src = reinterpret_cast<const int4 *>(pk.grid);
     for (int i = tid; i < pk.grid_bytes / 16; i += kLatThreads) dst[i] = __ldg(src + i);
     grid = reinterpret_cast<const uint8_t *>(dst);
@@ -339,12 +350,12 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     long long acc = 0;
     for (int j = tid; j < pk.n_atoms; j += kLatThreads) {
       const float4 y = __ldg(pk.patoms + j);
-      const int32_t *wcol = pk.wfx + (int)y.w * nb1;
+      const int32_t *wcol = sw + (int)y.w * nb1;
       int part = 0, cntp = 0;
       for (int i = 0; i < A; ++i) {
         const float4 x = S.u[i];
         const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
-        part += __ldg(wcol + (int)x.w * DS_N_TYPES * nb1 + lat_bin(pk, d2));
+        part += wcol[(int)x.w * DS_N_TYPES * nb1 + lat_bin(pk, slut, d2)];
         if (++cntp == 64) {  // int32 partials over <= 64 atoms (|W| <= 2^24)
           acc += part;
           part = 0;
@@ -515,7 +526,7 @@ size_t latency_rec_bytes() { return sizeof(LatRec); }
 
 void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *scores,
                              OptOut out, void *recs, int *done, cudaStream_t st) {
-  const size_t base = 360 * sizeof(float2) + 2 * (DS_MAX_ATOMS - 2) * sizeof(uint4);
+  const size_t base = lat_base_bytes(pk.nb, pk.lut_cap);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
