@@ -54,7 +54,8 @@ enum {
   DS_ERR_UNSUPPORTED = -8,
   DS_ERR_CUDA = -9,
   DS_ERR_NO_DEVICE = -10,
-  DS_ERR_OOM = -11
+  DS_ERR_OOM = -11,
+  DS_ERR_PARSE = -12               /* ParseError (malformed .ligq text) */
 };
 
 /* per-ligand status in ds_result.status */
@@ -248,6 +249,19 @@ int ds_build_pocket_grid(const float *atom_xyz, int32_t n_atoms, float spacing, 
 int ds_build_pocket_grid_device(ds_ctx *ctx, const float *atom_xyz, int32_t n_atoms, float spacing,
                                 float padding, float origin[3], int32_t dims[3], int32_t *values,
                                 float *device_ms);
+/* Native .ligq parser (io.parse_ligand_file): molecules parsed and validated
+ * (validate_ligand) in parallel, kept in file order.  ds_ligq_parse returns counts
+ * {ligands, atoms, bonds, fragments, id bytes, skipped invalid} and a handle; ds_ligq_fill copies
+ * the CSR batch into caller arrays (offset arrays have ligands + 1 entries); ds_ligq_free.  Errors:
+ * DS_ERR_PARSE (message in err) or the validation code of the first invalid molecule unless
+ * skip_invalid. */
+typedef struct ds_ligq ds_ligq;
+int ds_ligq_parse(const char *text, int64_t len, int32_t skip_invalid, ds_ligq **out, int64_t counts[6],
+                  char *err, int32_t err_len);
+int ds_ligq_fill(const ds_ligq *h, int32_t *atom_off, float *atom_xyz, uint8_t *atom_type, int32_t *bond_off,
+                 int32_t *bonds, int32_t *frag_off, int32_t *frag_axis, uint32_t *frag_mask, char *ids,
+                 int64_t *id_off);
+void ds_ligq_free(ds_ligq *h);
 /* Seeded symmetric 16x16 interaction table in [-1, 1]. */
 int ds_default_table(int64_t seed, float *table /* 256 */);
 

@@ -12,10 +12,18 @@
 #include "../../include/dockscreen.h"
 
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdio.h>
 #include <string.h>
 
+#include <errno.h>
+#include <stdlib.h>
+
 #include <algorithm>
+#include <charconv>
+#include <string>
 #include <vector>
 
 namespace {
@@ -343,5 +351,406 @@ int ds_default_table(int64_t seed, float *table) {
     }
   return DS_OK;
 }
+
+}  // extern "C"
+
+// ---- native .ligq parser (io.parse_ligand_file restated) -------------------
+// The text is cut at its MOL records; molecules are parsed and validated (validate_ligand,
+// SPEC.md:81-89, including the bond-cut invariants) in parallel, then concatenated in file order.
+// Semantics follow io.parse_ligand_file line for line: records are the first whitespace-separated
+// token; a MOL id is the stripped line minus "MOL "; a molecule without END that is followed by
+// another MOL is dropped; a non-empty line outside a molecule, a malformed record or a missing
+// final END is a parse error; the first error in file order is reported.
+namespace {
+
+struct LigqMol {
+  std::string id;
+  std::vector<float> xyz;
+  std::vector<uint8_t> type;
+  std::vector<int32_t> bonds;   // pairs
+  std::vector<int32_t> axis;    // pairs
+  std::vector<uint32_t> mask;   // DS_MASK_WORDS per fragment
+  int64_t line = 0;             // line of the MOL record
+  int code = 0;                 // parse error before END (DS_ERR_PARSE) or validation DS_ERR_*
+  int64_t err_line = 0;
+  std::string err;
+  bool ended = false;
+  bool invalid = false;         // code is a validation error (the reference raises it at END)
+  std::string trail_err;        // "record outside MOL" after END (reported after a validation error)
+};
+
+inline bool ws(char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\v' || c == '\f'; }
+
+// split [b, e) into tokens
+int tokens(const char *b, const char *e, const char **tb, const char **te, int maxt) {
+  int n = 0;
+  while (b < e) {
+    while (b < e && ws(*b)) ++b;
+    if (b >= e) break;
+    const char *s = b;
+    while (b < e && !ws(*b)) ++b;
+    if (n < maxt) {
+      tb[n] = s;
+      te[n] = b;
+    }
+    ++n;
+  }
+  return n;
+}
+
+bool tok_eq(const char *b, const char *e, const char *lit) {
+  const size_t n = strlen(lit);
+  return (size_t)(e - b) == n && memcmp(b, lit, n) == 0;
+}
+
+// Python int() / float() on one token (a leading '+' allowed, the whole token consumed); floats are
+// parsed to the nearest double and rounded to f32, as float(np.float32(float(t)))
+bool parse_int(const char *b, const char *e, long long *v) {
+  if (b < e && *b == '+' && e - b > 1 && b[1] != '-') ++b;
+  const auto r = std::from_chars(b, e, *v);
+  return r.ec == std::errc() && r.ptr == e && b < e;
+}
+
+bool parse_f32(const char *b, const char *e, float *v) {
+  if (b < e && *b == '+' && e - b > 1 && b[1] != '-') ++b;
+  double x;
+  const auto r = std::from_chars(b, e, x);
+  if (r.ec != std::errc() || r.ptr != e || b == e) {
+    // from_chars reports out-of-range values as errors; Python gives +-inf or a subnormal/0
+    if (r.ec == std::errc::result_out_of_range && r.ptr == e) {
+      std::string s(b, e);
+      x = strtod(s.c_str(), nullptr);
+    } else {
+      return false;
+    }
+  }
+  *v = (float)x;
+  return true;
+}
+
+// validate_ligand on a parsed molecule; returns 0 or the DS_ERR_* code
+int validate_mol(const LigqMol &m, const std::vector<uint8_t> &heavy_flag, const std::vector<std::vector<long long>> &fr,
+                 const std::vector<long long> &type_raw, std::string *why) {
+  const int n = (int)m.type.size();
+  if (n > DS_MAX_ATOMS) return *why = "atoms > max", DS_ERR_TOO_MANY_ATOMS;
+  if (n < 1) return *why = "ligand has no atoms", DS_ERR_INDEX_OUT_OF_RANGE;
+  for (int i = 0; i < n; ++i) {
+    if (type_raw[i] < 0 || type_raw[i] >= DS_N_TYPES) return *why = "element_type outside 0..15", DS_ERR_INDEX_OUT_OF_RANGE;
+    if ((bool)heavy_flag[i] != (type_raw[i] != 0)) return *why = "is_heavy inconsistent with element_type", DS_ERR_MALFORMED_FRAGMENT;
+  }
+  const int nb = (int)m.bonds.size() / 2;
+  for (int k = 0; k < nb; ++k)
+    if (m.bonds[2 * k] < 0 || m.bonds[2 * k] >= n || m.bonds[2 * k + 1] < 0 || m.bonds[2 * k + 1] >= n)
+      return *why = "bond out of range", DS_ERR_INDEX_OUT_OF_RANGE;
+  std::vector<std::vector<int>> adj(n);
+  for (int k = 0; k < nb; ++k) {
+    adj[m.bonds[2 * k]].push_back(k);
+    adj[m.bonds[2 * k + 1]].push_back(k);
+  }
+  const int nf = (int)fr.size();
+  for (int f = 0; f < nf; ++f) {
+    const long long ab = m.axis[2 * f], ae = m.axis[2 * f + 1];
+    if (!(0 <= ab && ab < n && 0 <= ae && ae < n)) return *why = "fragment axis out of range", DS_ERR_INDEX_OUT_OF_RANGE;
+    for (long long v : fr[f])
+      if (!(0 <= v && v < n)) return *why = "moving_mask index out of range", DS_ERR_INDEX_OUT_OF_RANGE;
+    std::vector<char> inm(n, 0);
+    int msize = 0;
+    for (long long v : fr[f])
+      if (!inm[v]) inm[v] = 1, ++msize;
+    if (ab == ae || inm[ab] || inm[ae]) return *why = "axis atoms must be distinct and outside the mask", DS_ERR_MALFORMED_FRAGMENT;
+    if (msize == 0 || msize >= n) return *why = "moving_mask must be a non-empty proper subset", DS_ERR_MALFORMED_FRAGMENT;
+    bool is_bond = false;
+    for (int k = 0; k < nb && !is_bond; ++k)
+      is_bond = (m.bonds[2 * k] == ab && m.bonds[2 * k + 1] == ae) || (m.bonds[2 * k] == ae && m.bonds[2 * k + 1] == ab);
+    if (!is_bond) return *why = "fragment axis is not a bond", DS_ERR_MALFORMED_FRAGMENT;
+    // connected components of the bond graph without every (ab, ae) / (ae, ab) bond
+    std::vector<int> comp(n, -1);
+    int nc = 0;
+    for (int s = 0; s < n; ++s) {
+      if (comp[s] >= 0) continue;
+      std::vector<int> st{s};
+      comp[s] = nc;
+      while (!st.empty()) {
+        const int u = st.back();
+        st.pop_back();
+        for (int k : adj[u]) {
+          const int a = m.bonds[2 * k], b = m.bonds[2 * k + 1];
+          if ((a == ab && b == ae) || (a == ae && b == ab)) continue;
+          const int w = a == u ? b : a;
+          if (comp[w] < 0) comp[w] = nc, st.push_back(w);
+        }
+      }
+      ++nc;
+    }
+    if (comp[ab] == comp[ae]) return *why = "removing the axis bond does not split the ligand", DS_ERR_MALFORMED_FRAGMENT;
+    if (nc != 2) return *why = "cutting the axis bond must leave exactly two parts", DS_ERR_MALFORMED_FRAGMENT;
+    bool side_b = true, side_e = true;
+    for (int i = 0; i < n; ++i) {
+      const bool pb = comp[i] == comp[ab] && i != ab && i != ae, pe = comp[i] == comp[ae] && i != ab && i != ae;
+      if ((bool)inm[i] != pb) side_b = false;
+      if ((bool)inm[i] != pe) side_e = false;
+    }
+    if (!side_b && !side_e) return *why = "moving_mask is not one side of the axis bond", DS_ERR_MALFORMED_FRAGMENT;
+  }
+  return DS_OK;
+}
+
+// parse one molecule: [b, e) starts at its MOL line (line number `line`)
+void parse_mol(const char *b, const char *e, int64_t line, LigqMol *m) {
+  m->line = line;
+  std::vector<uint8_t> heavy;
+  std::vector<long long> type_raw;
+  std::vector<std::vector<long long>> fr;
+  const char *p = b;
+  int64_t ln = line;
+  bool first = true;
+  const char *tb[8], *te[8];
+  auto perr = [&](const std::string &msg) {
+    m->code = DS_ERR_PARSE;
+    m->err_line = ln;
+    m->err = "line " + std::to_string(ln) + ": " + msg;
+  };
+  while (p < e && !m->ended && !m->code) {
+    const char *q = (const char *)memchr(p, '\n', (size_t)(e - p));
+    const char *le = q ? q : e;
+    const int nt = tokens(p, le, tb, te, 8);
+    if (first) {  // the MOL record: id = stripped line minus "MOL "
+      const char *s = p, *t = le;
+      while (s < t && ws(*s)) ++s;
+      while (t > s && ws(t[-1])) --t;
+      m->id = t - s > 4 ? std::string(s + 4, t) : std::string();
+      first = false;
+    } else if (nt > 0) {
+      if (tok_eq(tb[0], te[0], "ATOM")) {
+        long long idx, typ;
+        float x, y, z;
+        if (nt < 7) return perr("list index out of range");
+        if (!parse_int(tb[1], te[1], &idx) || !parse_int(tb[2], te[2], &typ)) return perr("invalid literal for int()");
+        if (idx != (long long)m->type.size()) return perr("atom index " + std::to_string(idx) + " out of order");
+        if (!parse_f32(tb[3], te[3], &x) || !parse_f32(tb[4], te[4], &y) || !parse_f32(tb[5], te[5], &z))
+          return perr("could not convert string to float");
+        m->xyz.insert(m->xyz.end(), {x, y, z});
+        type_raw.push_back(typ);
+        m->type.push_back((uint8_t)(typ & 0xFF));
+        heavy.push_back(!tok_eq(tb[6], te[6], "H"));
+      } else if (tok_eq(tb[0], te[0], "BOND")) {
+        long long a, c;
+        if (nt < 3) return perr("list index out of range");
+        if (!parse_int(tb[1], te[1], &a) || !parse_int(tb[2], te[2], &c)) return perr("invalid literal for int()");
+        m->bonds.push_back((int32_t)std::max(std::min(a, (long long)INT32_MAX), (long long)INT32_MIN));
+        m->bonds.push_back((int32_t)std::max(std::min(c, (long long)INT32_MAX), (long long)INT32_MIN));
+      } else if (tok_eq(tb[0], te[0], "FRAG")) {
+        long long a, c;
+        if (nt < 3) return perr("list index out of range");
+        if (!parse_int(tb[1], te[1], &a) || !parse_int(tb[2], te[2], &c)) return perr("invalid literal for int()");
+        std::vector<long long> mv;
+        // the moving atoms: every token after the axis (re-tokenise, there may be many)
+        const char *s = te[2];
+        while (s < le) {
+          while (s < le && ws(*s)) ++s;
+          if (s >= le) break;
+          const char *t = s;
+          while (t < le && !ws(*t)) ++t;
+          long long v;
+          if (!parse_int(s, t, &v)) return perr("invalid literal for int()");
+          mv.push_back(v);
+          s = t;
+        }
+        m->axis.push_back((int32_t)std::max(std::min(a, (long long)INT32_MAX), (long long)INT32_MIN));
+        m->axis.push_back((int32_t)std::max(std::min(c, (long long)INT32_MAX), (long long)INT32_MIN));
+        fr.push_back(std::move(mv));
+      } else if (tok_eq(tb[0], te[0], "END")) {
+        m->ended = true;
+      } else {
+        return perr("unknown record '" + std::string(tb[0], te[0]) + "'");
+      }
+    }
+    p = q ? q + 1 : e;
+    ++ln;
+  }
+  if (!m->ended || m->code) return;
+  // validated at END (the reference raises there, before it reads any later line)
+  std::string why;
+  const int v = validate_mol(*m, heavy, fr, type_raw, &why);
+  if (v) {
+    m->code = v;
+    m->invalid = true;
+    m->err_line = m->line;
+    m->err = "molecule " + m->id + " (line " + std::to_string(m->line) + "): " + why;
+  }
+  // anything after END up to the next MOL must be blank ("record outside MOL")
+  while (p < e) {
+    const char *q = (const char *)memchr(p, '\n', (size_t)(e - p));
+    const char *le = q ? q : e;
+    if (tokens(p, le, tb, te, 1) > 0) {
+      m->trail_err = "line " + std::to_string(ln) + ": record outside MOL";
+      break;
+    }
+    p = q ? q + 1 : e;
+    ++ln;
+  }
+  if (v) return;
+  const int n = (int)m->type.size();
+  m->mask.assign(fr.size() * DS_MASK_WORDS, 0u);
+  for (size_t f = 0; f < fr.size(); ++f)
+    for (long long v2 : fr[f]) m->mask[f * DS_MASK_WORDS + (v2 >> 5)] |= 1u << (v2 & 31);
+  (void)n;
+}
+
+}  // namespace
+
+struct ds_ligq {
+  std::vector<LigqMol> mols;  // kept molecules, file order
+  int64_t atoms = 0, bonds = 0, frags = 0, id_bytes = 0;
+  int32_t skipped = 0;
+};
+
+extern "C" {
+
+int ds_ligq_parse(const char *text, int64_t len, int32_t skip_invalid, ds_ligq **out, int64_t counts[6],
+                  char *err, int32_t err_len) {
+  if (!out || !counts || (!text && len > 0) || len < 0) return DS_ERR_INVALID_ARG;
+  *out = nullptr;
+  auto set_err = [&](const std::string &s) {
+    if (err && err_len > 0) {
+      strncpy(err, s.c_str(), (size_t)err_len - 1);
+      err[err_len - 1] = 0;
+    }
+  };
+  // MOL line starts: the text is cut into per-thread pieces at line boundaries, each piece scanned
+  // for line heads (and newlines, for line numbers), then stitched in order
+  int nthr = 1;
+#ifdef _OPENMP
+  nthr = std::max(1, std::min(omp_get_max_threads(), (int)(len / (1 << 20)) + 1));
+#endif
+  std::vector<int64_t> cut(nthr + 1);
+  cut[0] = 0;
+  cut[nthr] = len;
+  for (int t = 1; t < nthr; ++t) {
+    int64_t p = std::max(len * t / nthr, cut[t - 1]);
+    const char *q = p < len ? (const char *)memchr(text + p, '\n', (size_t)(len - p)) : nullptr;
+    cut[t] = q ? (q - text) + 1 : len;
+  }
+  std::vector<std::vector<int64_t>> pst(nthr), pln(nthr);
+  std::vector<int64_t> nlines(nthr, 0), pre_nb(nthr, -1), pre_nb_ln(nthr, 0);
+#pragma omp parallel for schedule(static, 1) num_threads(nthr)
+  for (int t = 0; t < nthr; ++t) {
+    int64_t ln = 0;
+    for (int64_t p = cut[t]; p < cut[t + 1];) {
+      const char *q = (const char *)memchr(text + p, '\n', (size_t)(cut[t + 1] - p));
+      const int64_t le = q ? q - text : cut[t + 1];
+      int64_t s2 = p;
+      while (s2 < le && ws(text[s2])) ++s2;
+      if (s2 < le) {
+        int64_t e2 = s2;
+        while (e2 < le && !ws(text[e2])) ++e2;
+        if (e2 - s2 == 3 && memcmp(text + s2, "MOL", 3) == 0) {
+          pst[t].push_back(p);
+          pln[t].push_back(ln);
+        } else if (pst[t].empty() && pre_nb[t] < 0) {
+          pre_nb[t] = p;
+          pre_nb_ln[t] = ln;
+        }
+      }
+      p = q ? le + 1 : cut[t + 1];
+      ++ln;
+    }
+    nlines[t] = ln;
+  }
+  std::vector<int64_t> starts, lines;
+  int64_t base_ln = 1;
+  for (int t = 0; t < nthr; ++t) {
+    if (starts.empty() && pre_nb[t] >= 0) {  // a record before the first MOL
+      set_err("line " + std::to_string(base_ln + pre_nb_ln[t]) + ": record outside MOL");
+      return DS_ERR_PARSE;
+    }
+    for (size_t k = 0; k < pst[t].size(); ++k) {
+      starts.push_back(pst[t][k]);
+      lines.push_back(base_ln + pln[t][k]);
+    }
+    base_ln += nlines[t];
+  }
+  const int64_t nm = (int64_t)starts.size();
+  std::vector<LigqMol> mols((size_t)nm);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t k = 0; k < nm; ++k)
+    parse_mol(text + starts[k], text + (k + 1 < nm ? starts[k + 1] : len), lines[k], &mols[k]);
+  ds_ligq *h = new ds_ligq();
+  for (int64_t k = 0; k < nm; ++k) {
+    LigqMol &m = mols[k];
+    if (m.code == DS_ERR_PARSE) {
+      set_err(m.err);
+      delete h;
+      return DS_ERR_PARSE;
+    }
+    if (!m.ended) {
+      if (k + 1 == nm) {  // unterminated last molecule
+        set_err("missing END");
+        delete h;
+        return DS_ERR_PARSE;
+      }
+      continue;  // the reference parser silently drops a molecule cut short by the next MOL
+    }
+    if (m.code) {
+      if (!skip_invalid) {
+        set_err(m.err);
+        delete h;
+        return m.code;
+      }
+      ++h->skipped;
+    }
+    if (!m.trail_err.empty()) {
+      set_err(m.trail_err);
+      delete h;
+      return DS_ERR_PARSE;
+    }
+    if (m.code) continue;
+    h->atoms += (int64_t)m.type.size();
+    h->bonds += (int64_t)m.bonds.size() / 2;
+    h->frags += (int64_t)m.axis.size() / 2;
+    h->id_bytes += (int64_t)m.id.size();
+    h->mols.push_back(std::move(m));
+  }
+  counts[0] = (int64_t)h->mols.size();
+  counts[1] = h->atoms;
+  counts[2] = h->bonds;
+  counts[3] = h->frags;
+  counts[4] = h->id_bytes;
+  counts[5] = h->skipped;
+  *out = h;
+  return DS_OK;
+}
+
+int ds_ligq_fill(const ds_ligq *h, int32_t *atom_off, float *atom_xyz, uint8_t *atom_type, int32_t *bond_off,
+                 int32_t *bonds, int32_t *frag_off, int32_t *frag_axis, uint32_t *frag_mask, char *ids, int64_t *id_off) {
+  if (!h || !atom_off || !bond_off || !frag_off || !id_off) return DS_ERR_INVALID_ARG;
+  const int64_t n = (int64_t)h->mols.size();
+  atom_off[0] = bond_off[0] = frag_off[0] = 0;
+  id_off[0] = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    const LigqMol &m = h->mols[k];
+    atom_off[k + 1] = atom_off[k] + (int32_t)m.type.size();
+    bond_off[k + 1] = bond_off[k] + (int32_t)(m.bonds.size() / 2);
+    frag_off[k + 1] = frag_off[k] + (int32_t)(m.axis.size() / 2);
+    id_off[k + 1] = id_off[k] + (int64_t)m.id.size();
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < n; ++k) {
+    const LigqMol &m = h->mols[k];
+    if (!m.type.empty()) {
+      memcpy(atom_xyz + 3 * (size_t)atom_off[k], m.xyz.data(), m.xyz.size() * 4);
+      memcpy(atom_type + atom_off[k], m.type.data(), m.type.size());
+    }
+    if (!m.bonds.empty()) memcpy(bonds + 2 * (size_t)bond_off[k], m.bonds.data(), m.bonds.size() * 4);
+    if (!m.axis.empty()) {
+      memcpy(frag_axis + 2 * (size_t)frag_off[k], m.axis.data(), m.axis.size() * 4);
+      memcpy(frag_mask + (size_t)DS_MASK_WORDS * frag_off[k], m.mask.data(), m.mask.size() * 4);
+    }
+    if (!m.id.empty()) memcpy(ids + id_off[k], m.id.data(), m.id.size());
+  }
+  return DS_OK;
+}
+
+void ds_ligq_free(ds_ligq *h) { delete h; }
 
 }  // extern "C"

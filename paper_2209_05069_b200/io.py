@@ -171,6 +171,38 @@ def parse_ligand_file(path: str, skip_invalid: bool = False) -> List[model.Ligan
     return out
 
 
+def parse_ligand_batch(path: str, skip_invalid: bool = False) -> LigandBatch:
+    """Native `.ligq` reader (ds_ligq_parse): the same records, validation and errors as
+    parse_ligand_file, parsed on all host cores straight into the packed CSR batch (host ingest at
+    scale); no per-ligand Python objects until `.ligand(i)` / `.to_ligands()`."""
+    with open(path, "rb") as fh:
+        text = fh.read()
+    L = lib()
+    h = C.c_void_p()
+    counts = (C.c_int64 * 6)()
+    err = C.create_string_buffer(512)
+    rc = L.ds_ligq_parse(text, len(text), int(bool(skip_invalid)), C.byref(h), counts, err, 512)
+    if rc != 0:
+        msg = err.value.decode(errors="replace")
+        if rc == -12:
+            raise model.ParseError(msg)
+        raise model.ValidationError(msg)
+    try:
+        n, na, nb, nf, nid = (int(counts[k]) for k in range(5))
+        ao, bo, fo = np.zeros(n + 1, np.int32), np.zeros(n + 1, np.int32), np.zeros(n + 1, np.int32)
+        xyz, typ = np.zeros((max(na, 1), 3), np.float32), np.zeros(max(na, 1), np.uint8)
+        bonds, axis = np.zeros((max(nb, 1), 2), np.int32), np.zeros((max(nf, 1), 2), np.int32)
+        mask = np.zeros((max(nf, 1), MASK_WORDS), np.uint32)
+        ids, id_off = C.create_string_buffer(max(nid, 1)), np.zeros(n + 1, np.int64)
+        check(L.ds_ligq_fill(h, _p(ao), _p(xyz), _p(typ), _p(bo), _p(bonds), _p(fo), _p(axis), _p(mask),
+                             C.cast(ids, C.c_void_p), _p(id_off)))
+    finally:
+        L.ds_ligq_free(h)
+    raw = ids.raw
+    names = [raw[id_off[i]:id_off[i + 1]].decode("ascii") for i in range(n)]
+    return LigandBatch(ao, xyz[:na], typ[:na], bo, bonds[:nb], fo, axis[:nf], mask[:nf], names)
+
+
 def write_pocket_file(path: str, pocket: model.Pocket) -> None:
     with open(path, "w", encoding="ascii", newline="\n") as fh:
         o = pocket.grid_origin

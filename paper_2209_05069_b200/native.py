@@ -125,6 +125,9 @@ def lib():
             "ds_build_pocket_grid": (C.c_int, [vp, i32, C.c_float, C.c_float, vp, vp, vp]),
             "ds_build_pocket_grid_device": (C.c_int, [vp, vp, i32, C.c_float, C.c_float, vp, vp, vp, vp]),
             "ds_default_table": (C.c_int, [i64, vp]),
+            "ds_ligq_parse": (C.c_int, [C.c_char_p, i64, i32, vp, vp, C.c_char_p, i32]),
+            "ds_ligq_fill": (C.c_int, [vp] * 11),
+            "ds_ligq_free": (None, [vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

@@ -2,7 +2,7 @@
 import numpy as np
 import pytest
 
-from paper_2209_05069_b200 import io, model
+from paper_2209_05069_b200 import io, model, native
 from paper_2209_05069_b200.bucketizer import classify
 
 
@@ -117,3 +117,60 @@ def test_pocket_file_roundtrip(tmp_path):
 def _write(path, text):
     path.write_text(text)
     return path
+
+
+def _same_batch(a, b):
+    for f in ("atom_off", "atom_xyz", "atom_type", "bond_off", "bonds", "frag_off", "frag_axis", "frag_mask"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert list(a.ids) == list(b.ids)
+
+
+def test_native_ligq_parser_matches_reference_parser(tmp_path):
+    """ds_ligq_parse (SURVEY §8(f) host ingest) == io.parse_ligand_file on a mixed database."""
+    ligs = io.generate_mixed_batch(300, seed=12).to_ligands()
+    f = tmp_path / "db.ligq"
+    io.write_ligand_file(str(f), ligs)
+    fast = io.parse_ligand_batch(str(f))
+    ref = native.LigandBatch.from_ligands(io.parse_ligand_file(str(f)))
+    _same_batch(fast, ref)
+    assert fast.to_ligands() == io.parse_ligand_file(str(f))
+    empty = io.parse_ligand_batch(str(_write(tmp_path / "e.ligq", "\n\n")))
+    assert empty.n == 0
+
+
+VALID = ("MOL m{}\nATOM 0 1 0 0 0 heavy\nATOM 1 1 1.5 0 0 heavy\nATOM 2 0 2.5 0 0 H\n"
+         "BOND 0 1\nBOND 1 2\nFRAG 0 1 2\nEND\n")
+
+
+@pytest.mark.parametrize("text", [
+    "ATOM 0 1 0 0 0 heavy\n",                                   # record outside MOL
+    VALID.format(1) + "BOND 0 1\n",                             # record outside MOL after END
+    "MOL a\nATOM 0 1 0 0 0\nEND\n",                             # missing field
+    "MOL a\nATOM 1 1 0 0 0 heavy\nEND\n",                       # atom index out of order
+    "MOL a\nATOM 0 1 x 0 0 heavy\nEND\n",                       # bad float
+    "MOL a\nATOM 0 1 0 0 0 heavy\nFOO 1\nEND\n",                # unknown record
+    VALID.format(1) + "MOL b\nATOM 0 1 0 0 0 heavy\n",          # missing final END
+])
+def test_native_ligq_parse_errors(tmp_path, text):
+    f = _write(tmp_path / "bad.ligq", text)
+    with pytest.raises(model.ParseError):
+        io.parse_ligand_file(str(f))
+    with pytest.raises(model.ParseError):
+        io.parse_ligand_batch(str(f))
+
+
+@pytest.mark.parametrize("frag", ["FRAG 0 1 1 2", "FRAG 0 2 2", "FRAG 0 1 7", "FRAG 0 1", "FRAG 0 2 1"])
+def test_native_ligq_validation_errors(tmp_path, frag):
+    """invalid fragments: raised (ValidationError) or skipped exactly like the reference parser;
+    a molecule cut short by the next MOL is dropped by both."""
+    text = ("MOL x\nATOM 0 1 0 0 0 heavy\nATOM 1 1 1.5 0 0 heavy\nATOM 2 1 3 0 0 heavy\nBOND 0 1\nBOND 1 2\n"
+            + frag + "\nEND\n" + "MOL cut\nATOM 0 1 0 0 0 heavy\n" + VALID.format(2))
+    f = _write(tmp_path / "v.ligq", text)
+    with pytest.raises(model.ValidationError):
+        io.parse_ligand_file(str(f))
+    with pytest.raises(model.ValidationError):
+        io.parse_ligand_batch(str(f))
+    ref = io.parse_ligand_file(str(f), skip_invalid=True)
+    fast = io.parse_ligand_batch(str(f), skip_invalid=True)
+    assert [l.id for l in ref] == list(fast.ids) == ["m2"]
+    _same_batch(fast, native.LigandBatch.from_ligands(ref))
