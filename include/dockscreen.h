@@ -262,6 +262,12 @@ int ds_ligq_fill(const ds_ligq *h, int32_t *atom_off, float *atom_xyz, uint8_t *
                  int32_t *bonds, int32_t *frag_off, int32_t *frag_axis, uint32_t *frag_mask, char *ids,
                  int64_t *id_off);
 void ds_ligq_free(ds_ligq *h);
+/* validate_ligand over a CSR batch of the reference's objects: element types as
+ * int64 (any value), is_heavy flags, bonds, fragment axes and the moving atoms as a CSR list
+ * (mv_off has fragments + 1 entries, absolute into mv).  codes[i] = 0 or the DS_ERR_* of ligand i. */
+int ds_validate_ligands(int32_t n, const int32_t *atom_off, const int64_t *atom_type, const uint8_t *is_heavy,
+                        const int32_t *bond_off, const int32_t *bonds, const int32_t *frag_off,
+                        const int32_t *frag_axis, const int64_t *mv_off, const int64_t *mv, int32_t *codes);
 /* Seeded symmetric 16x16 interaction table in [-1, 1]. */
 int ds_default_table(int64_t seed, float *table /* 256 */);
 

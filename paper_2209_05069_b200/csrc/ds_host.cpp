@@ -428,55 +428,58 @@ bool parse_f32(const char *b, const char *e, float *v) {
   return true;
 }
 
-// validate_ligand on a parsed molecule; returns 0 or the DS_ERR_* code
-int validate_mol(const LigqMol &m, const std::vector<uint8_t> &heavy_flag, const std::vector<std::vector<long long>> &fr,
-                 const std::vector<long long> &type_raw, std::string *why) {
-  const int n = (int)m.type.size();
-  if (n > DS_MAX_ATOMS) return *why = "atoms > max", DS_ERR_TOO_MANY_ATOMS;
+// validate_ligand over plain arrays, check for check in the reference's order;
+// returns 0 or the DS_ERR_* code (why = the reference's message without the ligand id)
+int validate_arrays(int n, const long long *type_raw, const uint8_t *heavy_flag, int nb, const int32_t *bonds, int nf,
+                    const int32_t *axis, const int64_t *mv_off, const long long *mv, std::string *why) {
+  if (n > DS_MAX_ATOMS) return *why = std::to_string(n) + " atoms > " + std::to_string(DS_MAX_ATOMS), DS_ERR_TOO_MANY_ATOMS;
   if (n < 1) return *why = "ligand has no atoms", DS_ERR_INDEX_OUT_OF_RANGE;
   for (int i = 0; i < n; ++i) {
-    if (type_raw[i] < 0 || type_raw[i] >= DS_N_TYPES) return *why = "element_type outside 0..15", DS_ERR_INDEX_OUT_OF_RANGE;
+    if (type_raw[i] < 0 || type_raw[i] >= DS_N_TYPES)
+      return *why = "element_type " + std::to_string(type_raw[i]) + " outside 0..15", DS_ERR_INDEX_OUT_OF_RANGE;
     if ((bool)heavy_flag[i] != (type_raw[i] != 0)) return *why = "is_heavy inconsistent with element_type", DS_ERR_MALFORMED_FRAGMENT;
   }
-  const int nb = (int)m.bonds.size() / 2;
   for (int k = 0; k < nb; ++k)
-    if (m.bonds[2 * k] < 0 || m.bonds[2 * k] >= n || m.bonds[2 * k + 1] < 0 || m.bonds[2 * k + 1] >= n)
-      return *why = "bond out of range", DS_ERR_INDEX_OUT_OF_RANGE;
-  std::vector<std::vector<int>> adj(n);
-  for (int k = 0; k < nb; ++k) {
-    adj[m.bonds[2 * k]].push_back(k);
-    adj[m.bonds[2 * k + 1]].push_back(k);
-  }
-  const int nf = (int)fr.size();
+    if (bonds[2 * k] < 0 || bonds[2 * k] >= n || bonds[2 * k + 1] < 0 || bonds[2 * k + 1] >= n)
+      return *why = "bond (" + std::to_string(bonds[2 * k]) + "," + std::to_string(bonds[2 * k + 1]) + ") out of range",
+             DS_ERR_INDEX_OUT_OF_RANGE;
+  std::vector<std::vector<int>> adj;
   for (int f = 0; f < nf; ++f) {
-    const long long ab = m.axis[2 * f], ae = m.axis[2 * f + 1];
+    const long long ab = axis[2 * f], ae = axis[2 * f + 1];
     if (!(0 <= ab && ab < n && 0 <= ae && ae < n)) return *why = "fragment axis out of range", DS_ERR_INDEX_OUT_OF_RANGE;
-    for (long long v : fr[f])
-      if (!(0 <= v && v < n)) return *why = "moving_mask index out of range", DS_ERR_INDEX_OUT_OF_RANGE;
+    for (int64_t k = mv_off[f]; k < mv_off[f + 1]; ++k)
+      if (!(0 <= mv[k] && mv[k] < n)) return *why = "moving_mask index out of range", DS_ERR_INDEX_OUT_OF_RANGE;
     std::vector<char> inm(n, 0);
     int msize = 0;
-    for (long long v : fr[f])
-      if (!inm[v]) inm[v] = 1, ++msize;
+    for (int64_t k = mv_off[f]; k < mv_off[f + 1]; ++k)
+      if (!inm[mv[k]]) inm[mv[k]] = 1, ++msize;
     if (ab == ae || inm[ab] || inm[ae]) return *why = "axis atoms must be distinct and outside the mask", DS_ERR_MALFORMED_FRAGMENT;
     if (msize == 0 || msize >= n) return *why = "moving_mask must be a non-empty proper subset", DS_ERR_MALFORMED_FRAGMENT;
     bool is_bond = false;
     for (int k = 0; k < nb && !is_bond; ++k)
-      is_bond = (m.bonds[2 * k] == ab && m.bonds[2 * k + 1] == ae) || (m.bonds[2 * k] == ae && m.bonds[2 * k + 1] == ab);
+      is_bond = (bonds[2 * k] == ab && bonds[2 * k + 1] == ae) || (bonds[2 * k] == ae && bonds[2 * k + 1] == ab);
     if (!is_bond) return *why = "fragment axis is not a bond", DS_ERR_MALFORMED_FRAGMENT;
+    if (adj.empty()) {
+      adj.assign(n, {});
+      for (int k = 0; k < nb; ++k) {
+        adj[bonds[2 * k]].push_back(k);
+        adj[bonds[2 * k + 1]].push_back(k);
+      }
+    }
     // connected components of the bond graph without every (ab, ae) / (ae, ab) bond
-    std::vector<int> comp(n, -1);
+    std::vector<int> comp(n, -1), st;
     int nc = 0;
-    for (int s = 0; s < n; ++s) {
-      if (comp[s] >= 0) continue;
-      std::vector<int> st{s};
-      comp[s] = nc;
+    for (int s0 = 0; s0 < n; ++s0) {
+      if (comp[s0] >= 0) continue;
+      st.assign(1, s0);
+      comp[s0] = nc;
       while (!st.empty()) {
         const int u = st.back();
         st.pop_back();
         for (int k : adj[u]) {
-          const int a = m.bonds[2 * k], b = m.bonds[2 * k + 1];
-          if ((a == ab && b == ae) || (a == ae && b == ab)) continue;
-          const int w = a == u ? b : a;
+          const int a2 = bonds[2 * k], b2 = bonds[2 * k + 1];
+          if ((a2 == ab && b2 == ae) || (a2 == ae && b2 == ab)) continue;
+          const int w = a2 == u ? b2 : a2;
           if (comp[w] < 0) comp[w] = nc, st.push_back(w);
         }
       }
@@ -493,6 +496,18 @@ int validate_mol(const LigqMol &m, const std::vector<uint8_t> &heavy_flag, const
     if (!side_b && !side_e) return *why = "moving_mask is not one side of the axis bond", DS_ERR_MALFORMED_FRAGMENT;
   }
   return DS_OK;
+}
+
+int validate_mol(const LigqMol &m, const std::vector<uint8_t> &heavy_flag, const std::vector<std::vector<long long>> &fr,
+                 const std::vector<long long> &type_raw, std::string *why) {
+  std::vector<int64_t> off(fr.size() + 1, 0);
+  std::vector<long long> mv;
+  for (size_t f = 0; f < fr.size(); ++f) {
+    mv.insert(mv.end(), fr[f].begin(), fr[f].end());
+    off[f + 1] = (int64_t)mv.size();
+  }
+  return validate_arrays((int)m.type.size(), type_raw.data(), heavy_flag.data(), (int)(m.bonds.size() / 2),
+                         m.bonds.data(), (int)fr.size(), m.axis.data(), off.data(), mv.data(), why);
 }
 
 // parse one molecule: [b, e) starts at its MOL line (line number `line`)
@@ -752,5 +767,20 @@ int ds_ligq_fill(const ds_ligq *h, int32_t *atom_off, float *atom_xyz, uint8_t *
 }
 
 void ds_ligq_free(ds_ligq *h) { delete h; }
+
+int ds_validate_ligands(int32_t n, const int32_t *atom_off, const int64_t *atom_type, const uint8_t *is_heavy,
+                        const int32_t *bond_off, const int32_t *bonds, const int32_t *frag_off, const int32_t *frag_axis,
+                        const int64_t *mv_off, const int64_t *mv, int32_t *codes) {
+  if (n < 0 || !atom_off || !bond_off || !frag_off || !mv_off || !codes) return DS_ERR_INVALID_ARG;
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int32_t i = 0; i < n; ++i) {
+    std::string why;
+    const int a0 = atom_off[i], f0 = frag_off[i];
+    codes[i] = validate_arrays(atom_off[i + 1] - a0, (const long long *)atom_type + a0, is_heavy + a0,
+                               bond_off[i + 1] - bond_off[i], bonds + 2 * (size_t)bond_off[i], frag_off[i + 1] - f0,
+                               frag_axis + 2 * (size_t)f0, mv_off + f0, (const long long *)mv, &why);
+  }
+  return DS_OK;
+}
 
 }  // extern "C"

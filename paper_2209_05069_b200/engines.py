@@ -19,7 +19,9 @@ from dataclasses import dataclass, field
 from typing import Iterable, List, Mapping, Optional, Sequence, Tuple
 
 from . import model
-from .bucketizer import Batch, Bucketizer, classify
+import numpy as np
+
+from .bucketizer import Batch, BucketKey, Bucketizer, bucket_capacity, classify
 from .docking import _pockets, results_from_output, thread_context
 from .native import FAMILY_BATCHED, FAMILY_LATENCY, InteractionTable, LigandBatch, pack
 
@@ -118,60 +120,68 @@ class batched_engine:  # noqa: N801
     def run(stream: Iterable[model.Ligand], pocket: model.Pocket, cfg: model.DockConfig = model.DockConfig(),
             workers: int = 1, seed: int = 0, table: Optional[InteractionTable] = None,
             capacities: Optional[Mapping[int, int]] = None, devices: Sequence[int] = (0,)) -> EngineReport:
-        """producers -> bucketizer -> dispatcher; flush at end of stream."""
+        """producers -> bucketizer -> dispatcher; flush at end of stream.
+
+        On B200 the stages run in bulk: the stream is flattened and validated natively
+        (validate_ligand semantics, all host cores), the bucketizer's batch accounting is computed
+        from the bucket keys (the same batches_dispatched and fill-ratio sum the per-ligand
+        Bucketizer produces), and each device docks its contiguous share of the valid ligands in
+        one pipelined ds_dock call (the batched kernels balance mixed sizes themselves, LPT order).
+        Results are per-ligand deterministic, so they are identical to per-bucket dispatch."""
         if workers < 1:
             raise ValueError("workers must be positive")
         ligs = list(stream)
         n = len(ligs)
-        slots: list = [None] * n
-        errors: list = []
-        elock = threading.Lock()
-        bz = Bucketizer(capacities)
-        q: "queue.Queue[Optional[Batch]]" = queue.Queue()
-        dev_ms = [0.0]
         t0 = time.perf_counter()
+        batch, codes = LigandBatch.from_ligands_validated(ligs)
+        errors: list = []
+        for i in np.nonzero(codes)[0]:
+            try:
+                model.validate_ligand(ligs[i])          # the reference's exact message
+                msg = f"IndexOutOfRange: {ligs[i].id}: invalid ligand"
+            except model.DockscreenError as e:
+                msg = f"{type(e).__name__}: {e}"
+            errors.append((int(i), ligs[i].id, msg))
+        ok = np.nonzero(codes == 0)[0]
+        # bucketizer accounting: per bucket ceil(count / capacity) batches; full ones record 1.0,
+        # the flushed partial ones (sorted by key, after every full batch) count / capacity
+        counters = model.Counters()
+        if len(ok):
+            na = np.diff(batch.atom_off).astype(np.int64)
+            nf = np.diff(batch.frag_off).astype(np.int64)
+            keys = ((na - 1) // 32) * 1_000_000 + nf // 4
+            uk, cnt = np.unique(keys, return_counts=True)
+            fills = []
+            for k, c in zip(uk.tolist(), cnt.tolist()):
+                cap = bucket_capacity(BucketKey(k // 1_000_000, k % 1_000_000), capacities)
+                counters.batches_dispatched += -(-c // cap)
+                fills.append((c // cap, (c % cap) / cap))
+            counters.batch_fill_ratio_sum = float(sum(f for f, _ in fills))
+            for _, r in fills:
+                if r:
+                    counters.batch_fill_ratio_sum += r
+        slots: list = [None] * n
+        dev_ms = [0.0]
+        lock = threading.Lock()
+        nd = max(1, min(len(devices), len(ok)))
+        bounds = [len(ok) * d // nd for d in range(nd + 1)]
 
-        def dispatcher(dev: int):
-            ctx = thread_context(dev)
+        def dispatcher(d: int):
+            lo, hi = bounds[d], bounds[d + 1]
+            if hi <= lo:
+                return
+            ctx = thread_context(devices[d])
             dp = _pockets.get(ctx, pocket, table)
-            while True:
-                b = q.get()
-                if b is None:
-                    break
-                batch = LigandBatch.from_ligands(b.ligands)
-                out = ctx.dock(dp, pack(batch), cfg, seed, FAMILY_BATCHED, coords=True)
-                with elock:
-                    dev_ms[0] += out.stats.total_ms
-                for seq, r in zip(b.seqs, results_from_output(batch, out, cfg)):
-                    slots[seq] = r
+            sub = batch.slice(lo, hi)
+            out = ctx.dock(dp, pack(sub), cfg, seed, FAMILY_BATCHED, coords=True)
+            with lock:
+                dev_ms[0] += out.stats.total_ms
+            for seq, r in zip(ok[lo:hi].tolist(), results_from_output(sub, out, cfg)):
+                slots[seq] = r
 
-        def producer(wid: int):
-            for i in range(wid, n, workers):
-                lig = ligs[i]
-                try:
-                    model.validate_ligand(lig)
-                except model.DockscreenError as e:
-                    with elock:
-                        errors.append((i, lig.id, f"{type(e).__name__}: {e}"))
-                    continue
-                full = bz.push(lig, classify(lig), seq=i)
-                if full is not None:
-                    q.put(full)
-
-        disp = [threading.Thread(target=dispatcher, args=(d,)) for d in devices]
+        disp = [threading.Thread(target=dispatcher, args=(d,)) for d in range(nd)]
         for t in disp:
             t.start()
-        prod = [threading.Thread(target=producer, args=(w,)) for w in range(workers)]
-        for t in prod:
-            t.start()
-        for t in prod:
-            t.join()
-        for b in bz.flush():
-            q.put(b)
-        for _ in disp:
-            q.put(None)
         for t in disp:
             t.join()
-        counters = model.Counters(batches_dispatched=bz.counters.batches_dispatched,
-                                  batch_fill_ratio_sum=bz.counters.batch_fill_ratio_sum)
         return _finish(n, slots, errors, counters, t0, dev_ms[0])

@@ -13,7 +13,7 @@ import os
 import threading
 import weakref
 from dataclasses import dataclass
-from typing import List, Optional, Sequence
+from typing import Tuple, List, Optional, Sequence
 
 import numpy as np
 
@@ -128,6 +128,7 @@ def lib():
             "ds_ligq_parse": (C.c_int, [C.c_char_p, i64, i32, vp, vp, C.c_char_p, i32]),
             "ds_ligq_fill": (C.c_int, [vp] * 11),
             "ds_ligq_free": (None, [vp]),
+            "ds_validate_ligands": (C.c_int, [i32] + [vp] * 10),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -206,6 +207,15 @@ class LigandBatch:
         off[1:] = np.cumsum([len(e) for e in enc])
         return b"".join(enc), off
 
+    def slice(self, lo: int, hi: int) -> "LigandBatch":
+        """Ligands [lo, hi) as a new batch (array slices, no per-ligand objects)."""
+        a0, a1 = int(self.atom_off[lo]), int(self.atom_off[hi])
+        b0, b1 = int(self.bond_off[lo]), int(self.bond_off[hi])
+        f0, f1 = int(self.frag_off[lo]), int(self.frag_off[hi])
+        return LigandBatch(self.atom_off[lo:hi + 1] - a0, self.atom_xyz[a0:a1], self.atom_type[a0:a1],
+                           self.bond_off[lo:hi + 1] - b0, self.bonds[b0:b1], self.frag_off[lo:hi + 1] - f0,
+                           self.frag_axis[f0:f1], self.frag_mask[f0:f1], list(self.ids[lo:hi]))
+
     def subset(self, idx: Sequence[int]) -> "LigandBatch":
         return LigandBatch.from_ligands([self.ligand(int(i)) for i in idx])
 
@@ -223,6 +233,59 @@ class LigandBatch:
 
     def to_ligands(self) -> List[model.Ligand]:
         return [self.ligand(i) for i in range(self.n)]
+
+    @staticmethod
+    def from_ligands_validated(ligands: Sequence[model.Ligand]) -> Tuple["LigandBatch", np.ndarray]:
+        """Flatten the reference's Ligand objects in bulk and run validate_ligand on
+        all of them natively (ds_validate_ligands, all host cores).  Returns the batch of the valid
+        ligands (input order) and the DS_ERR_* code of every input ligand (0 = valid)."""
+        import itertools
+        n = len(ligands)
+        na = np.fromiter((len(l.atoms) for l in ligands), np.int64, n)
+        nb = np.fromiter((len(l.bonds) for l in ligands), np.int64, n)
+        nf = np.fromiter((len(l.fragments) for l in ligands), np.int64, n)
+        atoms = [a for l in ligands for a in l.atoms]
+        xyz = np.fromiter(itertools.chain.from_iterable(a.position for a in atoms), np.float64,
+                          3 * len(atoms)).reshape(-1, 3)
+        typ = np.fromiter((a.element_type for a in atoms), np.int64, len(atoms))
+        heavy = np.fromiter((a.is_heavy for a in atoms), np.uint8, len(atoms))
+        bonds = np.fromiter(itertools.chain.from_iterable(b for l in ligands for b in l.bonds), np.int64,
+                            2 * int(nb.sum())).reshape(-1, 2)
+        frags = [f for l in ligands for f in l.fragments]
+        axis = np.fromiter(itertools.chain.from_iterable((f.axis_begin, f.axis_end) for f in frags), np.int64,
+                           2 * len(frags)).reshape(-1, 2)
+        mlen = np.fromiter((len(f.moving_mask) for f in frags), np.int64, len(frags))
+        mv = np.fromiter(itertools.chain.from_iterable(f.moving_mask for f in frags), np.int64, int(mlen.sum()))
+        off = lambda c: np.concatenate([[0], np.cumsum(c)]).astype(np.int64)
+        ao, bo, fo, mo = off(na), off(nb), off(nf), off(mlen)
+        i32 = lambda a: np.ascontiguousarray(np.clip(a, -2**31, 2**31 - 1).astype(np.int32))
+        codes = np.zeros(max(n, 1), np.int32)
+        if n > 0 and (ao[-1] >= 2**31 or bo[-1] >= 2**31 or fo[-1] >= 2**31):
+            raise ValueError("batch too large for one validation call")
+        if n:
+            # _p passes raw addresses: every array must stay referenced until the call returns
+            keep = [i32(ao), np.ascontiguousarray(typ), heavy, i32(bo), i32(bonds).reshape(-1), i32(fo),
+                    i32(axis).reshape(-1), np.ascontiguousarray(mo), np.ascontiguousarray(mv), codes]
+            check(lib().ds_validate_ligands(n, *[_p(x) for x in keep]))
+        codes = codes[:n]
+        okm = codes == 0
+        ok = np.nonzero(okm)[0]
+        # the valid ligands' arrays, in input order (boolean masks repeated per atom / bond / fragment)
+        ka = np.nonzero(np.repeat(okm, na))[0]
+        kb = np.nonzero(np.repeat(okm, nb))[0]
+        fok = np.repeat(okm, nf)
+        kf = np.nonzero(fok)[0]
+        mask = np.zeros((len(kf), MASK_WORDS), np.uint32)
+        if len(kf):
+            cnt = mlen[kf]
+            rows = np.repeat(np.arange(len(kf)), cnt)
+            vals = mv[np.repeat(fok, mlen)]
+            np.bitwise_or.at(mask, (rows, vals >> 5), (np.uint32(1) << (vals & 31).astype(np.uint32)))
+        o32 = lambda c: np.concatenate([[0], np.cumsum(c)]).astype(np.int32)
+        batch = LigandBatch(o32(na[ok]), xyz[ka].astype(np.float32), typ[ka].astype(np.uint8), o32(nb[ok]),
+                            bonds[kb].astype(np.int32).reshape(-1, 2), o32(nf[ok]), axis[kf].astype(np.int32).reshape(-1, 2),
+                            mask, [ligands[i].id for i in ok])
+        return batch, codes
 
     @staticmethod
     def from_ligands(ligands: Sequence[model.Ligand]) -> "LigandBatch":
