@@ -193,3 +193,14 @@ def test_parity_large_mixed_both_families(gpu_ctx, synth_pocket, table):
     sub = batch.subset(range(0, 2000, 7)[:300])
     g, o = _run(gpu_ctx, sub, synth_pocket, table, cfg, seed=5, family=FAMILY_LATENCY)
     compare(sub, g, o, cfg)
+
+
+def test_parity_maximum_ligands(gpu_ctx, synth_pocket, table):
+    """DS_MAX_ATOMS (160-atom) ligands with 60 rotatable bonds: five 32-atom slots, up to 158 moving
+    atoms per fragment, the largest per-warp records — both families against the oracle."""
+    batch = io.generate_dataset_batch(70, 60, 6, seed=9)
+    assert int(np.diff(batch.atom_off).max()) == 160
+    cfg = model.DockConfig()
+    for fam in (FAMILY_BATCHED, FAMILY_LATENCY):
+        g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg, seed=2, family=fam)
+        compare(batch, g, o, cfg)
