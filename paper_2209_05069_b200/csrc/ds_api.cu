@@ -31,7 +31,7 @@ void launch_align_latency(const PocketView &pk, const BatchView &bt, const DockP
 size_t latency_rec_bytes();
 void launch_build_pocket(const float *atom_xyz, int P, const double *origin, double s, const int *dims,
                          int32_t *values, int sm_count, cudaStream_t st);
-void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *scores,
+void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
                              OptOut out, void *recs, int *done, cudaStream_t st);
 void launch_grid_score(const PocketView &pk, const float *coords, int n_atoms, int n_poses, int32_t *out,
                        cudaStream_t st);
@@ -102,6 +102,10 @@ struct ds_ctx {
     uint8_t *btors;
   } io{};
   DevBuf x_in, x_out;
+  // latency-family scratch (alignment scores, per-ligand done counters) is left zeroed by the
+  // kernels; cleared here only after a (re)allocation or a failed call
+  bool lat_dirty = true;
+  void *lat_scores_seen = nullptr, *lat_done_seen = nullptr;
   size_t x_in_bytes = 0, x_out_bytes = 0, x_out_off[5] = {};
   // pinned host staging
   void *h_stage = nullptr;
@@ -787,8 +791,14 @@ int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const Dock
       (rc = c->ensure(c->b_lat_done, 4ull * L)) ||
       (rc = c->ensure(c->b_scratch, sizeof(float4) * (size_t)L * dp.N * DS_MAX_ATOMS)))
     return rc;
-  DS_CUDA(cudaMemsetAsync(c->b_lat_scores.p, 0, 4 * nsc, c->stream));
-  DS_CUDA(cudaMemsetAsync(c->b_lat_done.p, 0, 4ull * L, c->stream));
+  // the kernels leave both buffers zeroed for the next call; clear them only when (re)allocated
+  if (c->lat_dirty || c->b_lat_scores.p != c->lat_scores_seen || c->b_lat_done.p != c->lat_done_seen) {
+    DS_CUDA(cudaMemsetAsync(c->b_lat_scores.p, 0, c->b_lat_scores.cap, c->stream));
+    DS_CUDA(cudaMemsetAsync(c->b_lat_done.p, 0, c->b_lat_done.cap, c->stream));
+    c->lat_scores_seen = c->b_lat_scores.p;
+    c->lat_done_seen = c->b_lat_done.p;
+    c->lat_dirty = false;
+  }
   cudaEventRecord(c->ev[1], c->stream);
   launch_align_latency(pk->view, bt, dp, max_atoms, (int *)c->b_lat_scores.p, c->stream);
   cudaEventRecord(c->ev[2], c->stream);
@@ -799,7 +809,8 @@ int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const Dock
   oo.final_u = (float4 *)c->b_scratch.p;
   oo.best_coords = want_coords ? c->io.coords : nullptr;
   oo.best_tors = want_btors ? c->io.btors : nullptr;
-  launch_optimize_latency(pk->view, bt, dp, (const int *)c->b_lat_scores.p, oo, c->b_lat_recs.p,
+  c->lat_dirty = true;  // until the call has completed (set clean again below / by ds_dock)
+  launch_optimize_latency(pk->view, bt, dp, (int *)c->b_lat_scores.p, oo, c->b_lat_recs.p,
                           (int *)c->b_lat_done.p, c->stream);
   cudaEventRecord(c->ev[3], c->stream);
   if (st) st->launches += 2;
@@ -1021,6 +1032,7 @@ int ds_dock(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const ds_doc
   if ((rc = express ? download_express(c, st) : download(c, L, NA, NF, dp.N, out, st))) return rc;
   cudaEventRecord(c->ev[4], c->stream);
   DS_CUDA(cudaStreamSynchronize(c->stream));
+  if (family == DS_FAMILY_LATENCY) c->lat_dirty = false;  // a completed call leaves its scratch zeroed
   if (express) finish_express(c, L, NA, NF, dp.N, out);
   fill_times(c, st, true, family == DS_FAMILY_BATCHED);
   return DS_OK;
@@ -1081,6 +1093,7 @@ int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_d
   io_from_buffers(c);  // the resident batch lives in the per-array buffers (not an express arena)
   if ((rc = run_family(c, pk, family, d->L, d->n_atoms, d->n_frags, max_atoms, dp, true, true, true, st))) return rc;
   DS_CUDA(cudaStreamSynchronize(c->stream));
+  if (family == DS_FAMILY_LATENCY) c->lat_dirty = false;
   d->N = dp.N;
   d->docked = true;
   fill_times(c, st, false, family == DS_FAMILY_BATCHED);

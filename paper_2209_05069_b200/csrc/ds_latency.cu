@@ -91,7 +91,7 @@ __device__ __forceinline__ float3 lat_torsion_pos(const float2 *trig, int step_t
 
 template <bool kSmemGrid>
 __global__ void __launch_bounds__(kLatThreads, 1)
-    k_optimize_latency(PocketView pk, BatchView bt, DockParams dp, const int *scores, OptOut out, LatRec *recs,
+    k_optimize_latency(PocketView pk, BatchView bt, DockParams dp, int *scores, OptOut out, LatRec *recs,
                        int *done) {
   __shared__ LatSmem S;
   extern __shared__ __align__(16) unsigned char dsm[];  // [trig 360][fragment records][grid]
@@ -125,12 +125,15 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     S.heavy = 0;
   }
   __syncthreads();
-  // ---- argmax of the alignment scores (ties -> smallest rotation index) ----
+  // ---- argmax of the alignment scores (ties -> smallest rotation index); each slot is zeroed by
+  // the thread that read it, so the buffer is clean for the next call (no memset per call) ----
   {
-    const int *sc = scores + ((size_t)lig * dp.N + r) * dp.n_rot;
+    int *sc = scores + ((size_t)lig * dp.N + r) * dp.n_rot;
     unsigned best = 0u;
-    for (int q = tid; q < dp.n_rot; q += kLatThreads)
+    for (int q = tid; q < dp.n_rot; q += kLatThreads) {
       best = max(best, ((unsigned)(__ldcg(sc + q) + 32768) << 16) | (unsigned)(65535 - q));
+      __stcg(sc + q, 0);
+    }
     best = __reduce_max_sync(kFull, best);
     if (lane == 0) atomicMax(&S.key, best);
   }
@@ -399,6 +402,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   __syncthreads();
   if (!S.is_last) return;
   __threadfence();
+  if (tid == 0) done[lig] = 0;  // every CTA of the ligand has counted in: reset for the next call
 
   // ---- the ligand's last CTA: select_poses (P12), best rescored kept pose ----
   const LatRec *lr = recs + (size_t)lig * dp.N;
@@ -524,7 +528,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
 
 size_t latency_rec_bytes() { return sizeof(LatRec); }
 
-void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *scores,
+void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
                              OptOut out, void *recs, int *done, cudaStream_t st) {
   const size_t base = lat_base_bytes(pk.nb, pk.lut_cap);
   int dev = 0, optin = 0;
