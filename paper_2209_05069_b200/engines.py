@@ -115,6 +115,34 @@ class latency_engine:  # noqa: N801  (module-like namespace mirroring `dockscree
         return rep
 
 
+def bucket_accounting(n_atoms: np.ndarray, n_frags: np.ndarray,
+                      capacities: Optional[Mapping[int, int]] = None) -> model.Counters:
+    """The batches the bucketizer detaches for ligands of these sizes, without
+    pushing them one by one: per bucket ceil(count / capacity) batches; full ones record a fill
+    ratio of 1.0 as they are detached, the partial ones at flush (sorted by key, after every full
+    batch) count / capacity — the same sums, in the same order, as Bucketizer.push + flush."""
+    counters = model.Counters()
+    na = np.asarray(n_atoms, np.int64)
+    nf = np.asarray(n_frags, np.int64)
+    if len(na) == 0:
+        return counters
+    keys = ((na - 1) // 32) * 1_000_000 + nf // 4
+    uk, cnt = np.unique(keys, return_counts=True)
+    full, partial = 0, []
+    for k, c in zip(uk.tolist(), cnt.tolist()):
+        cap = bucket_capacity(BucketKey(k // 1_000_000, k % 1_000_000), capacities)
+        counters.batches_dispatched += -(-c // cap)
+        full += c // cap
+        if c % cap:
+            partial.append((c % cap) / cap)
+    counters.batch_fill_ratio_sum = 0.0
+    for _ in range(full):
+        counters.batch_fill_ratio_sum += 1.0
+    for r in partial:
+        counters.batch_fill_ratio_sum += r
+    return counters
+
+
 class batched_engine:  # noqa: N801
     @staticmethod
     def run(stream: Iterable[model.Ligand], pocket: model.Pocket, cfg: model.DockConfig = model.DockConfig(),
@@ -143,23 +171,7 @@ class batched_engine:  # noqa: N801
                 msg = f"{type(e).__name__}: {e}"
             errors.append((int(i), ligs[i].id, msg))
         ok = np.nonzero(codes == 0)[0]
-        # bucketizer accounting: per bucket ceil(count / capacity) batches; full ones record 1.0,
-        # the flushed partial ones (sorted by key, after every full batch) count / capacity
-        counters = model.Counters()
-        if len(ok):
-            na = np.diff(batch.atom_off).astype(np.int64)
-            nf = np.diff(batch.frag_off).astype(np.int64)
-            keys = ((na - 1) // 32) * 1_000_000 + nf // 4
-            uk, cnt = np.unique(keys, return_counts=True)
-            fills = []
-            for k, c in zip(uk.tolist(), cnt.tolist()):
-                cap = bucket_capacity(BucketKey(k // 1_000_000, k % 1_000_000), capacities)
-                counters.batches_dispatched += -(-c // cap)
-                fills.append((c // cap, (c % cap) / cap))
-            counters.batch_fill_ratio_sum = float(sum(f for f, _ in fills))
-            for _, r in fills:
-                if r:
-                    counters.batch_fill_ratio_sum += r
+        counters = bucket_accounting(np.diff(batch.atom_off), np.diff(batch.frag_off), capacities)
         slots: list = [None] * n
         dev_ms = [0.0]
         lock = threading.Lock()
