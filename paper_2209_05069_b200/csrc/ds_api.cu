@@ -365,6 +365,11 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
       }
       w[(size_t)t * nb1 + b] = (int32_t)llrint(s);
     }
+  {
+    int64_t wmax = 1;
+    for (int32_t x : w) wmax = std::max<int64_t>(wmax, x < 0 ? -(int64_t)x : (int64_t)x);
+    v.part_terms = (int)std::min<int64_t>((int64_t)INT32_MAX / wmax, 1 << 30);
+  }
   v.trig = c->trig;
   if (cudaMalloc(&p->d_grid, gbytes) != cudaSuccess || cudaMalloc(&p->d_patoms, pa.size() * sizeof(float4)) != cudaSuccess ||
       cudaMalloc(&p->d_wfx, w.size() * 4) != cudaSuccess) {

@@ -13,6 +13,8 @@ struct PocketView {
   int n_atoms;
   const float4 *patoms;      // pocket atoms in the grid frame, .w = element code
   const int32_t *wfx;        // [16][16][nb+1] fixed-point table*mult (2^-24); entry nb = 0
+  int part_terms;            // weight terms an int32 partial sum can hold without overflow:
+                             // floor((2^31 - 1) / max |W|) (2^7 for the default table)
   int nb;
   float ub2[DS_MAX_BINS];    // squared bin upper bounds, grid frame
   // bin look-up table, exact when every ub2 has its low lut_shift bits zero (the defaults do):

@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         const float4 x = S.u[i];
         const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
         part += wcol[(int)x.w * DS_N_TYPES * nb1 + lat_bin(pk, slut, d2)];
-        if (++cntp == 64) {  // int32 partials over <= 64 atoms (|W| <= 2^24)
+        if (++cntp == pk.part_terms) {  // int32 partials sized by the host so they cannot overflow
           acc += part;
           part = 0;
           cntp = 0;

@@ -102,19 +102,22 @@ __device__ __forceinline__ float3 torsion_pos(const PocketView &pk, int step_t, 
 // in shared memory as negated-coordinate pairs, so the squared distances of a ligand atom to both
 // come from FADD2 / FMUL2 / FFMA2 (each half bit-identical to dist2: x - y == x + (-y) exactly).
 // The ligand atom (broadcast) is loaded once for the two pairs.  Bin: LUT or compares.
-template <bool kLut>
+template <bool kLut, typename Part>
 __device__ __forceinline__ long long rescore_pose_x2(const SelWarpSmem &S, int A, const f2_t *pnx, const f2_t *pny,
                                                      const f2_t *pnz, const int2 *pcol, int nrounds,
                                                      const int32_t *wfx, int nb, const float *ub2,
-                                                     const uint8_t *lut, int lut_shift, int lut_cap) {
+                                                     const uint8_t *lut, int lut_shift, int lut_cap,
+                                                     int part_atoms) {
   const int lane = threadIdx.x & 31;
   long long acc = 0;
   for (int k = 0; k < nrounds; ++k) {
     const f2_t NX = pnx[k * 32 + lane], NY = pny[k * 32 + lane], NZ = pnz[k * 32 + lane];
     const int2 col = pcol[k * 32 + lane];
-    for (int i0 = 0; i0 < A; i0 += 64) {  // int32 partials over <= 64 atoms (|W| <= 2^24)
-      int part = 0;
-      const int i1 = min(A, i0 + 64);
+    // int32 partials over part_atoms ligand atoms (2 terms each), which the host sized so that no
+    // partial can overflow (PocketView::part_terms); widened to int64 between chunks
+    for (int i0 = 0; i0 < A; i0 += part_atoms) {
+      Part part = 0;
+      const int i1 = min(A, i0 + part_atoms);
       for (int i = i0; i < i1; ++i) {
         const float4 x = S.u[i];
         const f2_t DX = f2_add(f2_pack(x.x, x.x), NX);
@@ -132,7 +135,7 @@ __device__ __forceinline__ long long rescore_pose_x2(const SelWarpSmem &S, int A
             b1 += !(d1 < ub2[q]);
           }
         }
-        part += wfx[b0] + wfx[b1];
+        part += (Part)wfx[b0] + (Part)wfx[b1];
       }
       acc += part;
     }
@@ -672,11 +675,16 @@ __global__ void __launch_bounds__(kOptWarps * 32)
         S.u[i] = x;
       }
       __syncwarp();
-      long long acc = pk.lut_cap >= 0
-                          ? rescore_pose_x2<true>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut,
-                                                  pk.lut_shift, pk.lut_cap)
-                          : rescore_pose_x2<false>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2,
-                                                   s_lut, 0, 0);
+      // int32 partials when two weight terms fit (every default-like table), int64 otherwise
+      long long acc;
+      if (pk.part_terms >= 2)
+        acc = pk.lut_cap >= 0 ? rescore_pose_x2<true, int>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2,
+                                                           s_lut, pk.lut_shift, pk.lut_cap, pk.part_terms / 2)
+                              : rescore_pose_x2<false, int>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2,
+                                                            s_lut, 0, 0, pk.part_terms / 2);
+      else
+        acc = rescore_pose_x2<false, long long>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0,
+                                                0, A);
       acc = warp_sum64(acc);
       if (best_r < 0 || acc > best_chem || (acc == best_chem && r < best_r)) {
         best_chem = acc;

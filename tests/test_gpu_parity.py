@@ -204,3 +204,16 @@ def test_parity_maximum_ligands(gpu_ctx, synth_pocket, table):
     for fam in (FAMILY_BATCHED, FAMILY_LATENCY):
         g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg, seed=2, family=fam)
         compare(batch, g, o, cfg)
+
+
+def test_parity_large_weights_no_int32_overflow(gpu_ctx, synth_pocket):
+    """Bin multipliers near the fixed-point limit (|W| ~ 2^30): the rescore's int32 partial sums
+    must be sized so they cannot overflow (PocketView::part_terms) — both families vs the oracle."""
+    from paper_2209_05069_b200.native import InteractionTable
+    base = InteractionTable.default()
+    table = InteractionTable(np.clip(base.table * 1.0, -1, 1), ((2.0, 100.0), (4.0, 64.0), (6.0, 32.0), (8.0, 16.0)))
+    batch = io.generate_mixed_batch(48, seed=41)
+    cfg = model.DockConfig()
+    for fam in (FAMILY_BATCHED, FAMILY_LATENCY):
+        g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg, seed=1, family=fam)
+        compare(batch, g, o, cfg)
