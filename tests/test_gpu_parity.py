@@ -139,11 +139,13 @@ def test_batched_parity_crowded(gpu_ctx, synth_pocket, table, scale):
 
 
 def test_batched_parity_fine_torsion_step(gpu_ctx, synth_pocket, table):
-    """torsion_step_deg = 10: 36 angles, so the sweep runs a second (device-computed) lane block."""
+    """torsion_step_deg = 10: 36 angles, so the sweep runs a second angle block (device-computed
+    lane layout in the batched family, a second CTA block pass in the latency family)."""
     batch = io.generate_mixed_batch(60, seed=6)
     cfg = model.DockConfig(torsion_step_deg=10)
-    g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg)
-    compare(batch, g, o, cfg)
+    for fam in (FAMILY_BATCHED, FAMILY_LATENCY):
+        g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg, family=fam)
+        compare(batch, g, o, cfg)
 
 
 @pytest.mark.parametrize("spacing,padding,natoms", [(0.5, 4.0, 200), (0.375, 4.0, 200), (0.8, 2.0, 30), (1.0, 4.0, 1)])
