@@ -116,7 +116,10 @@ __device__ __forceinline__ void unit_atom(const float3 v, const float *t, unsign
 // NA > 0: n_a == NA fixed (G == NA, one unit per (restart, ax)); NA == 0: runtime n_a, ay in chunks
 // of G with units ordered chunk-major so a warp round shares its chunk.
 template <int NA, int G, bool kSmemGrid>
-__global__ void __launch_bounds__(1024, 1)
+#ifndef DS_ALIGN_WARPS
+#define DS_ALIGN_WARPS 32
+#endif
+__global__ void __launch_bounds__(DS_ALIGN_WARPS * 32, 1)
     k_align_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, AlignOut out, int *queue) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr bool kConst = NA > 0;

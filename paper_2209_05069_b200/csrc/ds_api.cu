@@ -741,10 +741,13 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t at
   // --- alignment: one CTA per SM, grid staged into smem when it fits ---
   const size_t per_warp = (size_t)align_warp_smem_bytes_host(dp.N);
   const size_t fixed = (size_t)dp.n_a * 16;
-  int warps_a = 32;
+#ifndef DS_ALIGN_WARPS
+#define DS_ALIGN_WARPS 32
+#endif
+  int warps_a = DS_ALIGN_WARPS;
   const size_t gb = (size_t)pk->view.grid_bytes;
   int in_smem = gb + fixed + per_warp * 8 <= c->smem_optin;
-  if (in_smem) warps_a = (int)std::min<size_t>(32, (c->smem_optin - gb - fixed) / per_warp);
+  if (in_smem) warps_a = (int)std::min<size_t>(DS_ALIGN_WARPS, (c->smem_optin - gb - fixed) / per_warp);
   const size_t smem_a = (in_smem ? gb : 0) + fixed + per_warp * warps_a;
   AlignOut ao{(uint32_t *)c->b_keys.p + (size_t)L0 * dp.N};
   cudaEventRecord(e0, c->stream);
