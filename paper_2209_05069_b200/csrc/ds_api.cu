@@ -323,7 +323,11 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
     }
     uint32_t ul;
     memcpy(&ul, &v.ub2[d->n_bins - 1], 4);
-    const uint32_t cap = ul >> S;
+    // full range when it is small: every non-negative float's bits >> S index the table directly
+    // (no clamp in the kernels); else entries up to the last bound and a clamp
+    const uint32_t full = 0x7FFFFFFFu >> S;
+    v.lut_full = full < 4096;
+    const uint32_t cap = v.lut_full ? full : ul >> S;
     v.lut_shift = S;
     v.lut_cap = -1;
     if (cap < 4096) {

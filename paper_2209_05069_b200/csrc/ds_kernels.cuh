@@ -21,6 +21,7 @@ struct PocketView {
   // bin = bin_lut[min(bits(d2) >> lut_shift, lut_cap)]; lut_cap < 0: no table (compare path)
   const uint8_t *bin_lut;
   int lut_shift, lut_cap;
+  int lut_full;              // the table covers every non-negative float (lut_cap = 0x7FFFFFFF >> shift)
   const float2 *trig;        // (cos, sin) of integer degrees 0..359 (f32 of f64)
 };
 

@@ -102,7 +102,7 @@ __device__ __forceinline__ float3 torsion_pos(const PocketView &pk, int step_t, 
 // in shared memory as negated-coordinate pairs, so the squared distances of a ligand atom to both
 // come from FADD2 / FMUL2 / FFMA2 (each half bit-identical to dist2: x - y == x + (-y) exactly).
 // The ligand atom (broadcast) is loaded once for the two pairs.  Bin: LUT or compares.
-template <bool kLut, typename Part>
+template <int kLut, typename Part>  // kLut: 0 compares, 1 clamped table, 2 full-range table
 __device__ __forceinline__ long long rescore_pose_x2(const SelWarpSmem &S, int A, const f2_t *pnx, const f2_t *pny,
                                                      const f2_t *pnz, const int2 *pcol, int nrounds,
                                                      const int32_t *wfx, int nb, const float *ub2,
@@ -126,7 +126,10 @@ __device__ __forceinline__ long long rescore_pose_x2(const SelWarpSmem &S, int A
         float d0, d1;
         f2_unpack(f2_fma(DZ, DZ, f2_fma(DY, DY, f2_mul(DX, DX))), d0, d1);
         int b0 = __float_as_int(x.w) + col.x, b1 = __float_as_int(x.w) + col.y;
-        if (kLut) {
+        if (kLut == 2) {  // d2 >= +0: bits >> shift <= lut_cap by construction
+          b0 += lut[(unsigned)__float_as_int(d0) >> lut_shift];
+          b1 += lut[(unsigned)__float_as_int(d1) >> lut_shift];
+        } else if (kLut == 1) {
           b0 += lut[min((unsigned)__float_as_int(d0) >> lut_shift, (unsigned)lut_cap)];
           b1 += lut[min((unsigned)__float_as_int(d1) >> lut_shift, (unsigned)lut_cap)];
         } else {
@@ -677,14 +680,17 @@ __global__ void __launch_bounds__(kOptWarps * 32)
       __syncwarp();
       // int32 partials when two weight terms fit (every default-like table), int64 otherwise
       long long acc;
-      if (pk.part_terms >= 2)
-        acc = pk.lut_cap >= 0 ? rescore_pose_x2<true, int>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2,
-                                                           s_lut, pk.lut_shift, pk.lut_cap, pk.part_terms / 2)
-                              : rescore_pose_x2<false, int>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2,
-                                                            s_lut, 0, 0, pk.part_terms / 2);
+      if (pk.part_terms >= 2 && pk.lut_cap >= 0 && pk.lut_full)
+        acc = rescore_pose_x2<2, int>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, pk.lut_shift,
+                                      pk.lut_cap, pk.part_terms / 2);
+      else if (pk.part_terms >= 2 && pk.lut_cap >= 0)
+        acc = rescore_pose_x2<1, int>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, pk.lut_shift,
+                                      pk.lut_cap, pk.part_terms / 2);
+      else if (pk.part_terms >= 2)
+        acc = rescore_pose_x2<0, int>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0, 0,
+                                      pk.part_terms / 2);
       else
-        acc = rescore_pose_x2<false, long long>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0,
-                                                0, A);
+        acc = rescore_pose_x2<0, long long>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0, 0, A);
       acc = warp_sum64(acc);
       if (best_r < 0 || acc > best_chem || (acc == best_chem && r < best_r)) {
         best_chem = acc;
