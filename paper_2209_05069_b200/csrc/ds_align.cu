@@ -20,9 +20,20 @@
 // argmax key per (ligand, restart): (score + 32768) << 16 | (65535 - (ix * n_a + iy)).
 #include <string.h>
 
+#include <cooperative_groups.h>
+#include <mutex>
+
 #include "ds_kernels.cuh"
 
 namespace ds {
+namespace cg = cooperative_groups;
+
+#ifndef DS_LAT_CS
+#define DS_LAT_CS 8   // CTAs per (ligand, restart) cluster in the latency align kernel
+#endif
+#ifndef DS_LAT_W
+#define DS_LAT_W 4    // warps per CTA there
+#endif
 
 __constant__ float4 c_trig_ay[360];  // (cos, sin, -sin, 0) of iy * step_a
 // the same angles as packed pairs for the f32x2 path: [k/2] = {(c_k, c_k+1), (s_k, s_k+1), (-s_k, -s_k+1)}
@@ -274,10 +285,17 @@ __global__ void __launch_bounds__(32)
 }
 
 // the n_a = 30 angle table in __constant__ (scalar and packed-pair forms); same values as the ctx
-// trig table (P0), identical for every caller
-static void upload_const_angles(int step_a, cudaStream_t st) {
-  static float4 h[30];
-  static unsigned long long hp[15][3];
+// trig table (P0), identical for every caller (n_a = 30 <=> step_a = 12), so it is uploaded once
+// per device (a blocking copy, so no stream can launch before it lands) instead of per call
+static void upload_const_angles(int step_a, cudaStream_t) {
+  static std::mutex mu;
+  static bool done[256];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev >= 0 && dev < 256 && done[dev]) return;
+  float4 h[30];
+  unsigned long long hp[15][3];
   for (int i = 0; i < 30; ++i) {
     const double rad = (double)(i * step_a) * 0.017453292519943295;
     const float c = (float)cos(rad), s = (float)sin(rad);
@@ -294,21 +312,88 @@ static void upload_const_angles(int step_a, cudaStream_t st) {
     hp[p][1] = pk(h[2 * p].y, h[2 * p + 1].y);
     hp[p][2] = pk(h[2 * p].z, h[2 * p + 1].z);
   }
-  cudaMemcpyToSymbolAsync(c_trig_ay, h, sizeof h, 0, cudaMemcpyHostToDevice, st);
-  cudaMemcpyToSymbolAsync(c_pair_ay, hp, sizeof hp, 0, cudaMemcpyHostToDevice, st);
+  if (cudaMemcpyToSymbol(c_trig_ay, h, sizeof h) == cudaSuccess &&
+      cudaMemcpyToSymbol(c_pair_ay, hp, sizeof hp) == cudaSuccess && dev >= 0 && dev < 256)
+    done[dev] = true;
 }
 
-void launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
-                          cudaStream_t st) {
+// ---- latency family, n_a = 30: one thread-block cluster per (ligand, restart) ---------------
+// CS CTAs x W warps split the ligand's atoms into CS*W contiguous ranges; lane = ax scores every
+// ay over its warp's range (packed f32x2 path, grid through L1).  The 900 partial sums are added
+// across the CTA's warps in shared memory, then across the cluster through distributed shared
+// memory (CTA k sums rotation slice k over all CS CTAs and folds its best key into CTA 0 with a
+// DSMEM atomicMax) — no global atomics, no scores buffer to clear, and the optimisation kernel
+// reads one key per (ligand, restart).  Integer sums: the key is exactly the argmax of the
+// single-pass sum (ties -> smallest rotation index).
+template <int CS, int W>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(W * 32)
+    k_align_latency_cl(PocketView pk, BatchView bt, DockParams dp, unsigned *keys) {
+  constexpr int NA = 30, NR = NA * NA, SL = (NR + CS - 1) / CS;
+  __shared__ int part[W][NR];
+  __shared__ unsigned s_best;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lr = blockIdx.x / CS;
+  const int lig = lr / dp.N, r = lr - lig * dp.N;
+  const int a0 = bt.atom_off[lig], A = bt.atom_off[lig + 1] - a0;
+  const int gw = rank * W + warp;
+  const int c0 = A * gw / (CS * W), c1 = A * (gw + 1) / (CS * W);
+  if (threadIdx.x == 0) s_best = 0u;
+  const GridGeom g = pk.g;
+  float R0s[9], t[3];
+  start_params(bt.idh[lig], dp.seed, r, pk.trig, pk.inv_s, g.nx, g.ny, g.nz, R0s, t);
+  if (lane < NA) {
+    float Rp[9];
+    align_rx(pk.trig[lane * dp.step_a], R0s, Rp);
+    unsigned acc[NA / 2];
+#pragma unroll
+    for (int k = 0; k < NA / 2; ++k) acc[k] = 0u;
+    for (int a = c0; a < c1; ++a) {
+      const float4 d = __ldg(bt.atoms + a0 + a);
+      const float3 v = align_v(Rp, d.x, d.y, d.z);
+      const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny + 1);
+      unit_atom<NA, true, false>(v, t, yk, g, pk.grid, nullptr, 0, NA, acc);
+    }
+    const int bias = 128 * (c1 - c0);
+#pragma unroll
+    for (int k = 0; k < NA; ++k) part[warp][lane * NA + k] = (int)((acc[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) - bias;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < NR; q += W * 32) {
+    int s = part[0][q];
+#pragma unroll
+    for (int w = 1; w < W; ++w) s += part[w][q];
+    part[0][q] = s;
+  }
+  cl.sync();
+  unsigned best = 0u;
+  for (int q = rank * SL + (int)threadIdx.x; q < min(NR, (rank + 1) * SL); q += W * 32) {
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < CS; ++k) s += cl.map_shared_rank(&part[0][0], k)[q];
+    best = max(best, ((unsigned)(s + 32768) << 16) | (unsigned)(65535 - q));
+  }
+  best = __reduce_max_sync(kFull, best);
+  if (lane == 0 && best) atomicMax(cl.map_shared_rank(&s_best, 0), best);
+  cl.sync();  // also keeps every CTA's shared memory alive until all remote reads are done
+  if (rank == 0 && threadIdx.x == 0) keys[lr] = s_best;
+}
+
+// returns true when the cluster kernel wrote one key per (ligand, restart) into keys (n_a = 30),
+// false when the generic kernel accumulated into scores
+bool launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
+                          unsigned *keys, cudaStream_t st) {
+  if (dp.n_a == 30) {
+    upload_const_angles(dp.step_a, st);
+    k_align_latency_cl<DS_LAT_CS, DS_LAT_W><<<bt.L * dp.N * DS_LAT_CS, DS_LAT_W * 32, 0, st>>>(pk, bt, dp, keys);
+    return true;
+  }
   const int ach = 4;
   const int nchunks = (max_atoms + ach - 1) / ach;
   const int blocks = bt.L * dp.N * nchunks;
-  if (dp.n_a == 30) {
-    upload_const_angles(dp.step_a, st);
-    k_align_latency<30><<<blocks, 32, 0, st>>>(pk, bt, dp, ach, nchunks, scores);
-  } else {
-    k_align_latency<0><<<blocks, 32, 0, st>>>(pk, bt, dp, ach, nchunks, scores);
-  }
+  k_align_latency<0><<<blocks, 32, 0, st>>>(pk, bt, dp, ach, nchunks, scores);
+  return false;
 }
 
 int align_warp_smem_bytes_host(int N) { return align_warp_smem_bytes(N); }

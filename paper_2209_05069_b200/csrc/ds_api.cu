@@ -26,13 +26,13 @@ void launch_select_batched(const PocketView &pk, const BatchView &bt, const Dock
 size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap);
 int torsion_blocks_per_sm();
 int select_blocks_per_sm(size_t smem);
-void launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
-                          cudaStream_t st);
+bool launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
+                          unsigned *keys, cudaStream_t st);
 size_t latency_rec_bytes();
 void launch_build_pocket(const float *atom_xyz, int P, const double *origin, double s, const int *dims,
                          int32_t *values, int sm_count, cudaStream_t st);
 void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
-                             OptOut out, void *recs, int *done, cudaStream_t st);
+                             const unsigned *keys, OptOut out, void *recs, int *done, cudaStream_t st);
 void launch_grid_score(const PocketView &pk, const float *coords, int n_atoms, int n_poses, int32_t *out,
                        cudaStream_t st);
 void launch_rescore(const PocketView &pk, const float *coords, const uint8_t *types, int n_atoms, int n_poses,
@@ -800,7 +800,7 @@ int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const Dock
   int rc;
   const size_t nsc = (size_t)L * dp.N * dp.n_rot;
   if ((rc = c->ensure(c->b_lat_scores, 4 * nsc)) || (rc = c->ensure(c->b_lat_recs, latency_rec_bytes() * (size_t)L * dp.N)) ||
-      (rc = c->ensure(c->b_lat_done, 4ull * L)) ||
+      (rc = c->ensure(c->b_lat_done, 4ull * L)) || (rc = c->ensure(c->b_keys, 4ull * L * dp.N)) ||
       (rc = c->ensure(c->b_scratch, sizeof(float4) * (size_t)L * dp.N * DS_MAX_ATOMS)))
     return rc;
   // the kernels leave both buffers zeroed for the next call; clear them only when (re)allocated
@@ -812,7 +812,8 @@ int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const Dock
     c->lat_dirty = false;
   }
   cudaEventRecord(c->ev[1], c->stream);
-  launch_align_latency(pk->view, bt, dp, max_atoms, (int *)c->b_lat_scores.p, c->stream);
+  const bool keyed =
+      launch_align_latency(pk->view, bt, dp, max_atoms, (int *)c->b_lat_scores.p, (unsigned *)c->b_keys.p, c->stream);
   cudaEventRecord(c->ev[2], c->stream);
   OptOut oo;
   oo.res = c->io.res;
@@ -822,7 +823,8 @@ int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const Dock
   oo.best_coords = want_coords ? c->io.coords : nullptr;
   oo.best_tors = want_btors ? c->io.btors : nullptr;
   c->lat_dirty = true;  // until the call has completed (set clean again below / by ds_dock)
-  launch_optimize_latency(pk->view, bt, dp, (int *)c->b_lat_scores.p, oo, c->b_lat_recs.p,
+  launch_optimize_latency(pk->view, bt, dp, (int *)c->b_lat_scores.p, keyed ? (const unsigned *)c->b_keys.p : nullptr,
+                          oo, c->b_lat_recs.p,
                           (int *)c->b_lat_done.p, c->stream);
   cudaEventRecord(c->ev[3], c->stream);
   if (st) st->launches += 2;

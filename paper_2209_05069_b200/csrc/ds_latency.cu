@@ -19,7 +19,10 @@
 
 namespace ds {
 
-constexpr int kLatThreads = 256;
+#ifndef DS_LAT_THREADS
+#define DS_LAT_THREADS 256
+#endif
+constexpr int kLatThreads = DS_LAT_THREADS;
 constexpr int kLatChunk = 8;
 
 struct LatRec {  // per (ligand, restart), read by the ligand's last CTA
@@ -91,8 +94,8 @@ __device__ __forceinline__ float3 lat_torsion_pos(const float2 *trig, int step_t
 
 template <bool kSmemGrid>
 __global__ void __launch_bounds__(kLatThreads, 1)
-    k_optimize_latency(PocketView pk, BatchView bt, DockParams dp, int *scores, OptOut out, LatRec *recs,
-                       int *done) {
+    k_optimize_latency(PocketView pk, BatchView bt, DockParams dp, int *scores, const unsigned *keys, OptOut out,
+                       LatRec *recs, int *done) {
   __shared__ LatSmem S;
   extern __shared__ __align__(16) unsigned char dsm[];  // [trig 360][fragment records][grid]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -127,7 +130,9 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   __syncthreads();
   // ---- argmax of the alignment scores (ties -> smallest rotation index); each slot is zeroed by
   // the thread that read it, so the buffer is clean for the next call (no memset per call) ----
-  {
+  if (keys) {  // the cluster align kernel already reduced this (ligand, restart) to its key
+    if (tid == 0) S.key = __ldcg(keys + (size_t)lig * dp.N + r);
+  } else {
     int *sc = scores + ((size_t)lig * dp.N + r) * dp.n_rot;
     unsigned best = 0u;
     for (int q = tid; q < dp.n_rot; q += kLatThreads) {
@@ -529,7 +534,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
 size_t latency_rec_bytes() { return sizeof(LatRec); }
 
 void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
-                             OptOut out, void *recs, int *done, cudaStream_t st) {
+                             const unsigned *keys, OptOut out, void *recs, int *done, cudaStream_t st) {
   const size_t base = lat_base_bytes(pk.nb, pk.lut_cap);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
@@ -537,10 +542,10 @@ void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const Do
   const size_t with_grid = base + (size_t)pk.grid_bytes;
   if (with_grid + sizeof(LatSmem) + 1024 <= (size_t)optin) {
     cudaFuncSetAttribute(k_optimize_latency<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)with_grid);
-    k_optimize_latency<true><<<bt.L * dp.N, kLatThreads, with_grid, st>>>(pk, bt, dp, scores, out, (LatRec *)recs, done);
+    k_optimize_latency<true><<<bt.L * dp.N, kLatThreads, with_grid, st>>>(pk, bt, dp, scores, keys, out, (LatRec *)recs, done);
   } else {
     cudaFuncSetAttribute(k_optimize_latency<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)base);
-    k_optimize_latency<false><<<bt.L * dp.N, kLatThreads, base, st>>>(pk, bt, dp, scores, out, (LatRec *)recs, done);
+    k_optimize_latency<false><<<bt.L * dp.N, kLatThreads, base, st>>>(pk, bt, dp, scores, keys, out, (LatRec *)recs, done);
   }
 }
 
