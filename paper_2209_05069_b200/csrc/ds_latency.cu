@@ -23,6 +23,7 @@ namespace ds {
 #define DS_LAT_THREADS 256
 #endif
 constexpr int kLatThreads = DS_LAT_THREADS;
+static_assert(kLatThreads >= DS_MAX_ATOMS, "phase (A) gives every atom its own thread");
 constexpr int kLatChunk = 8;
 
 struct LatRec {  // per (ligand, restart), read by the ligand's last CTA
@@ -41,13 +42,11 @@ struct LatSmem {
   uint8_t clist[DS_MAX_ATOMS];
   uint8_t cl[DS_MAX_ATOMS][kLatCand];  // bump candidates (atom indices) per moving atom
   unsigned cn[DS_MAX_ATOMS];           // their count (> kLatCand: scan all of C')
-  unsigned bm[8], bc[8];        // per 32-atom slot: ballots of M and C'
-  int bpart[8];                 // per 32-atom slot: grid score of the non-moving atoms
+  int base[2];                  // grid score of the non-moving atoms, by fragment parity
   int ascore[32];
   unsigned abump;
   unsigned key;
-  int nM, nC, base, degen, best_k, is_last;
-  float kx, ky, kz;
+  int degen, is_last;
   unsigned pairs;
   int geom;
   int ord[DS_MAX_RESTARTS], kept[DS_MAX_RESTARTS], nkept;
@@ -103,30 +102,39 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   const int a0 = bt.atom_off[lig], A = bt.atom_off[lig + 1] - a0;
   const int f0 = bt.frag_off[lig], F = bt.frag_off[lig + 1] - f0;
   const GridGeom g = pk.g;
-  // stage the trig table, this ligand's fragment records and (if it fits) the pocket grid: every
-  // later lookup is a shared-memory access instead of an L2 round trip on the fragment chain
+  // stage the trig table, this ligand's fragment records, the weights, the bin LUT and (if it
+  // fits) the pocket grid with bulk async copies (one thread issues, the TMA engine moves them;
+  // ~200 KB would otherwise take 50 dependent load/store rounds of the CTA): the trig table
+  // lands on bar[0] (needed for the initial pose), the rest on bar[1], awaited only before the
+  // fragment loop so the copies overlap the argmax and the initial pose
+  __shared__ __align__(8) unsigned long long bar[2];
   float2 *strig = reinterpret_cast<float2 *>(dsm);
   uint4 *sfrag = reinterpret_cast<uint4 *>(dsm + 360 * sizeof(float2));
-  const uint8_t *grid = pk.grid;
-  for (int i = tid; i < 360; i += kLatThreads) strig[i] = pk.trig[i];
-  for (int i = tid; i < 2 * F; i += kLatThreads) sfrag[i] = __ldg(bt.frags + 2 * (size_t)f0 + i);
   int32_t *sw = reinterpret_cast<int32_t *>(dsm + 360 * sizeof(float2) + 2 * (DS_MAX_ATOMS - 2) * sizeof(uint4));
   uint8_t *slut = reinterpret_cast<uint8_t *>(sw) + lat_w_bytes(pk.nb);
-  for (int i = tid; i < DS_N_TYPES * DS_N_TYPES * (pk.nb + 1); i += kLatThreads) sw[i] = __ldg(pk.wfx + i);
-  for (int i = tid; i <= pk.lut_cap; i += kLatThreads) slut[i] = __ldg(pk.bin_lut + i);
-  if (kSmemGrid) {
-    int4 *dst = reinterpret_cast<int4 *>(dsm + lat_base_bytes(pk.nb, pk.lut_cap));
-    const int4 *src = reinterpret_cast<const int4 *>(pk.grid);
-    for (int i = tid; i < pk.grid_bytes / 16; i += kLatThreads) dst[i] = __ldg(src + i);
-    grid = reinterpret_cast<const uint8_t *>(dst);
-  }
+  const uint8_t *grid = kSmemGrid ? dsm + lat_base_bytes(pk.nb, pk.lut_cap) : pk.grid;
+  const unsigned wbytes = (unsigned)(DS_N_TYPES * DS_N_TYPES * (pk.nb + 1) * 4);
+  const int lut_n = pk.lut_cap + 1, lut_bulk = lut_n & ~15;
   if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar[0], 360 * sizeof(float2));
+    bulk_g2s(strig, pk.trig, 360 * sizeof(float2), &bar[0]);
+    mbar_expect_tx(&bar[1], 32u * F + wbytes + lut_bulk + (kSmemGrid ? pk.grid_bytes : 0));
+    if (F) bulk_g2s(sfrag, bt.frags + 2 * (size_t)f0, 32u * F, &bar[1]);
+    bulk_g2s(sw, pk.wfx, wbytes, &bar[1]);
+    if (lut_bulk) bulk_g2s(slut, pk.bin_lut, lut_bulk, &bar[1]);
+    if (kSmemGrid) bulk_g2s(const_cast<uint8_t *>(grid), pk.grid, pk.grid_bytes, &bar[1]);
     S.key = 0u;
     S.pairs = 0u;
     S.geom = 0;
     S.degen = 0;
     S.heavy = 0;
+    S.base[0] = 0;
+    S.base[1] = 0;
   }
+  for (int i = lut_bulk + tid; i < lut_n; i += kLatThreads) slut[i] = __ldg(pk.bin_lut + i);  // < 16 B tail
   __syncthreads();
   // ---- argmax of the alignment scores (ties -> smallest rotation index); each slot is zeroed by
   // the thread that read it, so the buffer is clean for the next call (no memset per call) ----
@@ -143,6 +151,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     if (lane == 0) atomicMax(&S.key, best);
   }
   __syncthreads();
+  mbar_wait(&bar[0], 0);
   const unsigned key = S.key;
   const int rot = 65535 - (int)(key & 0xFFFFu);
   const int ix = rot / dp.n_a, iy = rot - ix * dp.n_a;
@@ -162,73 +171,77 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   int all_bumped = 0;
   const unsigned lt = lanemask_lt();
   const int nslot = (A + 31) >> 5;
+  mbar_wait(&bar[1], 0);
   for (int f = 0; f < F; ++f) {
     const uint4 fa = sfrag[2 * f];
     const uint4 fb = sfrag[2 * f + 1];
     const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
-    // ---- (A) warp w: ballots of M and C' over atoms 32w..32w+31 and their non-moving grid score;
-    // thread 0 also builds the axis ----
-    if (warp < nslot) {
-      const unsigned mword = warp == 0 ? fa.x : warp == 1 ? fa.y : warp == 2 ? fa.z : warp == 3 ? fa.w : fb.x;
-      const int i = warp * 32 + lane;
-      const bool in = i < A;
-      const bool mv = in && ((mword >> lane) & 1u);
-      const bool cp = in && !mv && i != ab && i != ae;
-      const unsigned bm = __ballot_sync(kFull, mv), bc = __ballot_sync(kFull, cp);
+    // ---- (A) one phase, one barrier: every thread derives the compaction of M / C' from the
+    // fragment's mask words (registers only), builds the axis itself (the same bits in every
+    // thread, so the degenerate-axis break is uniform), writes its atom's list slot and
+    // cylindrical coordinates, and adds the non-moving atoms' grid values into base[f & 1] ----
+    const float4 pa = S.u[ab], pb = S.u[ae];
+    const float3 a3 = make_float3(pa.x, pa.y, pa.z);
+    float kx = 0.f, ky = 0.f, kz = 0.f;
+    if (dp.n_t > 1) {
+      const float vx = __fsub_rn(pb.x, pa.x), vy = __fsub_rn(pb.y, pa.y), vz = __fsub_rn(pb.z, pa.z);
+      const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
+      if (!(len >= dp.eps_axis)) {
+        if (tid == 0) S.degen = 1;
+        break;
+      }
+      kx = __fdiv_rn(vx, len);
+      ky = __fdiv_rn(vy, len);
+      kz = __fdiv_rn(vz, len);
+    }
+    int nM = 0, nC = 0, mpre = 0, cpre = 0;
+    unsigned my_bm = 0u, my_bc = 0u;
+#pragma unroll
+    for (int w = 0; w < 5; ++w) {
+      if (w < nslot) {
+        const unsigned word = w == 0 ? fa.x : w == 1 ? fa.y : w == 2 ? fa.z : w == 3 ? fa.w : fb.x;
+        const int lim = A - 32 * w;
+        const unsigned vmask = lim >= 32 ? kFull : ((1u << lim) - 1u);
+        const unsigned bm = word & vmask;
+        unsigned bc = ~word & vmask;
+        if ((ab >> 5) == w) bc &= ~(1u << (ab & 31));
+        if ((ae >> 5) == w) bc &= ~(1u << (ae & 31));
+        if (w < warp) {
+          mpre += __popc(bm);
+          cpre += __popc(bc);
+        } else if (w == warp) {
+          mpre += __popc(bm & lt);
+          cpre += __popc(bc & lt);
+          my_bm = bm;
+          my_bc = bc;
+        }
+        nM += __popc(bm);
+        nC += __popc(bc);
+      }
+    }
+    {
       int part = 0;
-      if (in && !mv) {
-        const float4 p = S.u[i];
-        part = lat_grid_val<kSmemGrid>(grid, node_index(g, p.x, p.y, p.z));
+      if (tid < A) {
+        const float4 p = S.u[tid];
+        if ((my_bm >> lane) & 1u) {
+          S.mlist[mpre] = (uint8_t)tid;
+          S.chm[mpre] = lat_cyl(p, a3, kx, ky, kz);
+          S.cn[mpre] = 0;
+        } else {
+          if ((my_bc >> lane) & 1u) {
+            S.clist[cpre] = (uint8_t)tid;
+            S.chr[cpre] = lat_cyl(p, a3, kx, ky, kz);
+          }
+          part = lat_grid_val<kSmemGrid>(grid, node_index(g, p.x, p.y, p.z));
+        }
       }
       part = (int)__reduce_add_sync(kFull, (unsigned)part);
-      if (lane == 0) {
-        S.bm[warp] = bm;
-        S.bc[warp] = bc;
-        S.bpart[warp] = part;
-      }
-    }
-    if (tid == 0) {
-      S.abump = 0u;
-      const float4 pa = S.u[ab], pb = S.u[ae];
-      if (dp.n_t > 1) {
-        const float vx = __fsub_rn(pb.x, pa.x), vy = __fsub_rn(pb.y, pa.y), vz = __fsub_rn(pb.z, pa.z);
-        const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
-        if (!(len >= dp.eps_axis)) S.degen = 1;
-        S.kx = __fdiv_rn(vx, len);
-        S.ky = __fdiv_rn(vy, len);
-        S.kz = __fdiv_rn(vz, len);
-      }
+      if (lane == 0 && part) atomicAdd(&S.base[f & 1], part);
     }
     if (tid < 32) S.ascore[tid] = 0;
-    __syncthreads();
-    if (S.degen) break;
-    int nM = 0, nC = 0, base = 0, mpre = 0, cpre = 0;
-    for (int w = 0; w < nslot; ++w) {
-      if (w == warp) {
-        mpre = nM;
-        cpre = nC;
-      }
-      nM += __popc(S.bm[w]);
-      nC += __popc(S.bc[w]);
-      base += S.bpart[w];
-    }
-    const float4 pa = S.u[ab];
-    const float3 a3 = make_float3(pa.x, pa.y, pa.z);
-    const float kx = S.kx, ky = S.ky, kz = S.kz;
-    // ---- (B) compaction (ascending) + cylindrical coordinates of M and C' ----
-    if (warp < nslot) {
-      const int i = warp * 32 + lane;
-      const unsigned bm = S.bm[warp], bc = S.bc[warp];
-      if ((bm >> lane) & 1u) {
-        const int m = mpre + __popc(bm & lt);
-        S.mlist[m] = (uint8_t)i;
-        S.chm[m] = lat_cyl(S.u[i], a3, kx, ky, kz);
-        S.cn[m] = 0;
-      } else if ((bc >> lane) & 1u) {
-        const int c = cpre + __popc(bc & lt);
-        S.clist[c] = (uint8_t)i;
-        S.chr[c] = lat_cyl(S.u[i], a3, kx, ky, kz);
-      }
+    if (tid == 0) {
+      S.abump = 0u;
+      S.base[(f + 1) & 1] = 0;  // last read in fragment f - 1's (E)
     }
     __syncthreads();
     // ---- (C) bump candidates: every (moving, complement) pair over all threads (cylindrical
@@ -312,6 +325,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
       // ---- (E) best clean angle, computed by every warp (no extra barrier) ----
       const unsigned abump = S.abump;
       unsigned kk = 0;
+      const int base = S.base[f & 1];
       if (lane < nA && !((abump >> lane) & 1u))
         kk = ((unsigned)(base + S.ascore[lane] + 32768) << 16) | (unsigned)(65535 - (k0 + lane));
       best_key = max(best_key, __reduce_max_sync(kFull, kk));
@@ -331,6 +345,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     __syncthreads();
   }
   // ---- final pose, geometric score, per-restart record ----
+  __syncthreads();  // S.degen (a degenerate axis breaks every thread out at the same fragment)
   const int degen = S.degen;
   float4 *scr = out.final_u + ((size_t)lig * dp.N + r) * DS_MAX_ATOMS;
   if (!degen) {

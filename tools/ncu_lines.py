@@ -1,6 +1,6 @@
 """Per-CUDA-source-line instruction and stall attribution of one kernel in an ncu report.
 
-    python tools/ncu_lines.py report.ncu-rep kernel_regex [top]
+    python tools/ncu_lines.py report.ncu-rep kernel_regex [top] [inst|stall]
 """
 import csv
 import io
@@ -9,6 +9,7 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+by = sys.argv[4] if len(sys.argv) > 4 else "inst"  # or "stall"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "regex:" + kern, "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -37,5 +38,5 @@ for r in rows:
 ti = sum(v[0] for v in agg.values()) or 1
 ts = sum(v[1] for v in agg.values()) or 1
 print("total warp-inst %.3e" % ti)
-for (f, ln), (i, s, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+for (f, ln), (i, s, src) in sorted(agg.items(), key=lambda kv: -kv[1][0 if by == "inst" else 1])[:top]:
     print("%5.1f%% inst %5.1f%% stall  %s:%d  %s" % (100 * i / ti, 100 * s / ts, f, ln, src))
