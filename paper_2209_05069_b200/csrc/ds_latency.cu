@@ -23,6 +23,7 @@ namespace ds {
 #define DS_LAT_THREADS 256
 #endif
 constexpr int kLatThreads = DS_LAT_THREADS;
+constexpr int kLatWarps = kLatThreads / 32;
 static_assert(kLatThreads >= DS_MAX_ATOMS, "phase (A) gives every atom its own thread");
 constexpr int kLatChunk = 8;
 
@@ -89,6 +90,33 @@ __device__ __forceinline__ float3 lat_torsion_pos(const float2 *trig, int step_t
   float R[9];
   torsion_matrix(kx, ky, kz, cs.x, cs.y, R);
   return torsion_apply(R, a, p.x, p.y, p.z);
+}
+
+// exact n / d for 0 <= n <= 2^16, 1 <= d <= 2^16: float estimate, then a one-step correction
+__device__ __forceinline__ int small_div(int n, int d) {
+  int q = (int)__fmul_rn((float)n, __frcp_rn((float)d));
+  const int r = n - q * d;
+  q += (r >= d) - (r < 0);
+  return q;
+}
+
+// nearest bump candidate of moving atom m at its rotated position q (the cylindrical candidates,
+// or all of C' when they overflowed the list)
+__device__ __forceinline__ float lat_min_d2(const LatSmem &S, int m, int nC, float3 q) {
+  float mind = __int_as_float(0x7f800000);
+  const unsigned cnt = S.cn[m];
+  if (cnt <= (unsigned)kLatCand) {
+    for (unsigned t = 0; t < cnt; ++t) {
+      const float4 y = S.u[S.cl[m][t]];
+      mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+    }
+  } else {
+    for (int c = 0; c < nC; ++c) {
+      const float4 y = S.u[S.clist[c]];
+      mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+    }
+  }
+  return mind;
 }
 
 template <bool kSmemGrid>
@@ -248,8 +276,8 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     // bound, see ds_optimize.cu) ----
     if (nC > 0) {
       const int total = nM * nC;
-      int pm = tid / nC, pc = tid - (tid / nC) * nC;
-      const int dm = kLatThreads / nC, dc = kLatThreads - dm * nC;
+      int pm = small_div(tid, nC), pc = tid - pm * nC;
+      const int dm = small_div(kLatThreads, nC), dc = kLatThreads - dm * nC;
       for (int p0 = 0; p0 < total; p0 += kLatThreads) {
         if (p0 + tid < total) {
           const float2 hm = S.chm[pm], hc = S.chr[pc];
@@ -280,8 +308,9 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         __syncthreads();
       }
       unsigned my_pairs = 0;
-      const int G = kLatThreads / nA;
-      const int a = tid % nA, mg = tid / nA;
+      // the default 32 angles: lane = angle, warp = group (no integer division on the chain)
+      const int G = nA == 32 ? kLatWarps : kLatThreads / nA;
+      const int a = nA == 32 ? lane : tid % nA, mg = nA == 32 ? warp : tid / nA;
       if (mg < G) {
         float R[9];
         const int kang = k0 + a;
@@ -291,30 +320,24 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         }
         int part = 0;
         bool hit_any = false;
-        for (int m = mg; m < nM; m += G) {
+        // two moving atoms per step (independent chains: twice the loads in flight); a bump on
+        // either marks the angle, whose partial score is then never read
+        for (int m = mg; m < nM; m += 2 * G) {
           if (dp.early_exit && (hit_any || ((*(volatile unsigned *)&S.abump >> a) & 1u))) break;
-          const float4 p = S.u[S.mlist[m]];
-          const float3 q = kang == 0 ? make_float3(p.x, p.y, p.z) : torsion_apply(R, a3, p.x, p.y, p.z);
-          const int gv = lat_grid_val<kSmemGrid>(grid, node_index(g, q.x, q.y, q.z));
-          float mind = __int_as_float(0x7f800000);
-          my_pairs += (unsigned)nC;  // pairs resolved (P14)
-          const unsigned cnt = S.cn[m];
-          if (cnt <= (unsigned)kLatCand) {
-            for (unsigned t = 0; t < cnt; ++t) {
-              const float4 y = S.u[S.cl[m][t]];
-              mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
-            }
-          } else {
-            for (int c = 0; c < nC; ++c) {
-              const float4 y = S.u[S.clist[c]];
-              mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
-            }
-          }
-          if (mind < dp.bd2) {
+          const bool two = m + G < nM;
+          const int m1 = two ? m + G : m;
+          const float4 p0 = S.u[S.mlist[m]], p1 = S.u[S.mlist[m1]];
+          const float3 q0 = kang == 0 ? make_float3(p0.x, p0.y, p0.z) : torsion_apply(R, a3, p0.x, p0.y, p0.z);
+          const float3 q1 = kang == 0 ? make_float3(p1.x, p1.y, p1.z) : torsion_apply(R, a3, p1.x, p1.y, p1.z);
+          const int gv0 = lat_grid_val<kSmemGrid>(grid, node_index(g, q0.x, q0.y, q0.z));
+          const int gv1 = lat_grid_val<kSmemGrid>(grid, node_index(g, q1.x, q1.y, q1.z));
+          my_pairs += (unsigned)(two ? 2 * nC : nC);  // pairs resolved (P14)
+          const float d0 = lat_min_d2(S, m, nC, q0), d1 = lat_min_d2(S, m1, nC, q1);
+          if (d0 < dp.bd2 || d1 < dp.bd2) {
             hit_any = true;
             atomicOr(&S.abump, 1u << a);
           } else {
-            part += gv;
+            part += two ? gv0 + gv1 : gv0;
           }
         }
         if (part) atomicAdd(&S.ascore[a], part);
