@@ -893,12 +893,14 @@ int dock_pipelined(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const
   }
   std::vector<int> bounds(nch + 1);
   // tapered chunks: the first and last are a quarter of the inner ones, so the un-overlapped head
-  // (first H2D) and tail (last D2H) of the pipeline stay short (DS_PIPELINE_TAPER=0: equal chunks)
+  // (first H2D) and tail (last D2H) of the pipeline stay short (DS_PIPELINE_TAPER = the end-chunk
+  // weight; 0 or >= 1: equal chunks)
   {
     const char *e = getenv("DS_PIPELINE_TAPER");
-    const bool taper = (e ? atoi(e) : 1) && nch >= 3;
+    const double tw = e ? atof(e) : 0.25;
+    const bool taper = tw > 0.0 && tw < 1.0 && nch >= 3;
     std::vector<double> w(nch, 1.0);
-    if (taper) w[0] = w[nch - 1] = 0.25;
+    if (taper) w[0] = w[nch - 1] = tw;
     double tot = 0, run = 0;
     for (double x : w) tot += x;
     bounds[0] = 0;
