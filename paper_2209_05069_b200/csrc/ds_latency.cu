@@ -308,9 +308,9 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         __syncthreads();
       }
       unsigned my_pairs = 0;
-      // the default 32 angles: lane = angle, warp = group (no integer division on the chain)
-      const int G = nA == 32 ? kLatWarps : kLatThreads / nA;
-      const int a = nA == 32 ? lane : tid % nA, mg = nA == 32 ? warp : tid / nA;
+      // thread = (angle a, group mg), exact reciprocal division (no integer divide on the chain)
+      const int G = small_div(kLatThreads, nA);
+      const int mg = small_div(tid, nA), a = tid - mg * nA;
       if (mg < G) {
         float R[9];
         const int kang = k0 + a;
