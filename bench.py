@@ -129,7 +129,13 @@ def ncu_calibration():
     """Per-ligand executed warp-instructions / DRAM bytes of each kernel from the newest committed
     ncu summary (tools/ncu_summary.py --ligands) of this workload generator."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_kernels_*.json")), key=os.path.getmtime)
+    import re
+
+    def version(path):  # (round directory, vNN): file mtimes do not survive the copy to the GPU box
+        m = re.search(r"_v(\d+)\.json$", path)
+        return (os.path.basename(os.path.dirname(path)), int(m.group(1)) if m else -1)
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_kernels_*.json")), key=version)
     for path in reversed(files):
         try:
             with open(path) as fh:
