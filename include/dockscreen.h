@@ -198,6 +198,19 @@ int ds_dock_resident(ds_ctx *ctx, const ds_pocket *pocket, ds_dev_batch *batch,
                      const ds_dock_config *cfg, int family, ds_stats *stats);
 int ds_batch_download(ds_ctx *ctx, ds_dev_batch *batch, const ds_outputs *out);
 void ds_batch_destroy(ds_dev_batch *batch);
+
+/* Device-side ingest: generate ligands first_index .. first_index +
+ * count - 1 of a synthetic dataset (the same ligands as ds_generate_ligands with these shapes,
+ * SPEC.md:443 generate_dataset) directly into the ctx's device buffers, packed as ds_pack_ligands
+ * would (bit-identical atoms, fragment descriptors and id hashes of "lig_<seed>_<index>"), ready
+ * for ds_dock_resident.  Replaces generate + pack + ds_batch_upload (io.generate_batch,
+ * native.pack, ResidentBatch in the Python layer).  *device_ms (may be NULL) = the kernel time. */
+int ds_generate_resident(ds_ctx *ctx, int64_t seed, int64_t first_index, int32_t count, const int32_t *shapes,
+                         ds_dev_batch **out, float *device_ms);
+/* Read a resident batch's packed inputs back (any pointer may be NULL): atom_xyzt float[4 * atoms],
+ * frag_desc uint32[8 * fragments], id_hash uint64[ligands]. */
+int ds_batch_read_inputs(ds_ctx *ctx, const ds_dev_batch *batch, float *atom_xyzt, uint32_t *frag_desc,
+                         uint64_t *id_hash);
 /* Ligands one batched launch keeps resident on this device for atom range
  * `range_idx` (0..4) — the B200 analogue of the paper's occupancy-derived
  * capacity. */
@@ -217,6 +230,10 @@ int ds_op_rescore(ds_ctx *ctx, const ds_pocket *pocket, const float *coords,
 uint64_t ds_ligand_id_hash(const char *id, size_t len);
 /* Canonical id of generated ligand `index`: "lig_<seed>_<index>"; returns length. */
 int ds_generated_id(int64_t seed, int64_t index, char *buf, size_t cap);
+/* ids first_index .. first_index + count - 1 of a generated dataset as one blob (no separators)
+ * with offsets off[0..count]; buf == NULL fills only off (size query).  Same strings as
+ * ds_generated_id. */
+int ds_generated_ids(int64_t seed, int64_t first_index, int32_t count, char *buf, int64_t *off);
 /* Per-ligand (heavy, frags) shapes of the mixed datasets (BASELINE configs 3, 5):
  * heavy ~ U{heavy_min..heavy_max}, frags ~ U{0..min(frag_max, heavy-2)}. */
 int ds_mixed_shapes(int64_t seed, int64_t first_index, int32_t count, int32_t heavy_min,

@@ -29,6 +29,9 @@ int select_blocks_per_sm(size_t smem);
 bool launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
                           unsigned *keys, cudaStream_t st);
 size_t latency_rec_bytes();
+void launch_generate_ligands(long long seed, long long first_index, int count, const int *shapes, const int *atom_off,
+                             const int *frag_off, float4 *atoms, uint32_t *frag_desc, uint64_t *id_hash, int sm_count,
+                             cudaStream_t st);
 void launch_build_pocket(const float *atom_xyz, int P, const double *origin, double s, const int *dims,
                          int32_t *values, int sm_count, cudaStream_t st);
 void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
@@ -1126,6 +1129,67 @@ int ds_batch_download(ds_ctx *c, ds_dev_batch *d, const ds_outputs *out) {
 }
 
 void ds_batch_destroy(ds_dev_batch *d) { delete d; }
+
+int ds_generate_resident(ds_ctx *c, int64_t seed, int64_t first_index, int32_t count, const int32_t *shapes,
+                         ds_dev_batch **out, float *device_ms) {
+  if (!c || !out || !shapes || count < 0) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  // offsets on the host (hydrogen counts only: ~20 ns per ligand), InfeasibleShape checked there
+  std::vector<int32_t> ao((size_t)count + 1), bo((size_t)count + 1), fo((size_t)count + 1);
+  int rc = ds_generate_ligands(seed, first_index, count, shapes, ao.data(), bo.data(), fo.data(), nullptr, nullptr,
+                               nullptr, nullptr, nullptr);
+  if (rc == DS_ERR_INFEASIBLE_SHAPE) return fail(rc, "InfeasibleShape: fragments >= heavy - 1 or atoms out of range");
+  if (rc) return fail(rc, "bad generator arguments");
+  const int L = count, NA = ao[L], NF = fo[L];
+  DS_CUDA(enter_device(c->device));
+  ds_batch_desc b;
+  memset(&b, 0, sizeof b);
+  b.n_ligands = L;
+  b.atom_off = ao.data();
+  b.frag_off = fo.data();
+  std::vector<int> oa, oo;
+  lpt_orders(&b, oa, oo);
+  if ((rc = reserve_buffers(c, L, NA, NF, DS_MAX_RESTARTS)) || (rc = c->ensure_host(16ull * L + 64))) return rc;
+  // the shapes ride in the key buffer (8 B per ligand <= 4 N B; the alignment kernel overwrites it)
+  int *d_shapes = (int *)c->b_keys.p;
+  char *h = (char *)c->h_stage;
+  memcpy(h, shapes, 8ull * L);
+  cudaStream_t st = c->stream;
+  cudaEventRecord(c->ev[0], st);
+  DS_CUDA(cudaMemcpyAsync(d_shapes, h, 8ull * L, cudaMemcpyHostToDevice, st));
+  DS_CUDA(cudaMemcpyAsync(c->b_atom_off.p, ao.data(), 4ull * (L + 1), cudaMemcpyHostToDevice, st));
+  DS_CUDA(cudaMemcpyAsync(c->b_frag_off.p, fo.data(), 4ull * (L + 1), cudaMemcpyHostToDevice, st));
+  DS_CUDA(cudaMemcpyAsync(c->b_order_a.p, oa.data(), 4ull * L, cudaMemcpyHostToDevice, st));
+  DS_CUDA(cudaMemcpyAsync(c->b_order_o.p, oo.data(), 4ull * L, cudaMemcpyHostToDevice, st));
+  cudaEventRecord(c->ev[1], st);
+  launch_generate_ligands(seed, first_index, L, d_shapes, (const int *)c->b_atom_off.p, (const int *)c->b_frag_off.p,
+                          (float4 *)c->b_atoms.p, (uint32_t *)c->b_frags.p, (uint64_t *)c->b_idh.p, c->sm_count, st);
+  cudaEventRecord(c->ev[2], st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DS_ERR_CUDA, "generator launch: %s", cudaGetErrorString(e));
+  DS_CUDA(cudaStreamSynchronize(st));
+  if (device_ms) cudaEventElapsedTime(device_ms, c->ev[1], c->ev[2]);
+  ds_dev_batch *d = new ds_dev_batch();
+  d->ctx = c;
+  d->L = L;
+  d->atom_off.assign(ao.begin(), ao.end());
+  d->frag_off.assign(fo.begin(), fo.end());
+  d->n_atoms = NA;
+  d->n_frags = NF;
+  *out = d;
+  return DS_OK;
+}
+
+int ds_batch_read_inputs(ds_ctx *c, const ds_dev_batch *d, float *atom_xyzt, uint32_t *frag_desc, uint64_t *id_hash) {
+  if (!c || !d || d->ctx != c) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  DS_CUDA(enter_device(c->device));
+  if (atom_xyzt && d->n_atoms)
+    DS_CUDA(cudaMemcpyAsync(atom_xyzt, c->b_atoms.p, 16ull * d->n_atoms, cudaMemcpyDeviceToHost, c->stream));
+  if (frag_desc && d->n_frags)
+    DS_CUDA(cudaMemcpyAsync(frag_desc, c->b_frags.p, 32ull * d->n_frags, cudaMemcpyDeviceToHost, c->stream));
+  if (id_hash && d->L) DS_CUDA(cudaMemcpyAsync(id_hash, c->b_idh.p, 8ull * d->L, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  return DS_OK;
+}
 
 int ds_build_pocket_grid_device(ds_ctx *c, const float *atom_xyz, int32_t n_atoms, float spacing, float padding,
                                 float origin[3], int32_t dims[3], int32_t *values, float *device_ms) {

@@ -98,6 +98,27 @@ int ds_generated_id(int64_t seed, int64_t index, char *buf, size_t cap) {
   return snprintf(buf, cap, "lig_%lld_%lld", (long long)seed, (long long)index);
 }
 
+// ids first_index .. first_index + count - 1 as one byte blob + offsets (off[count] = total):
+// with buf == NULL only the offsets are filled (size query); both passes OpenMP-parallel
+int ds_generated_ids(int64_t seed, int64_t first_index, int32_t count, char *buf, int64_t *off) {
+  if (count < 0 || !off) return DS_ERR_INVALID_ARG;
+  std::vector<int32_t> len((size_t)count);
+#pragma omp parallel for schedule(static)
+  for (int32_t i = 0; i < count; ++i)
+    len[i] = snprintf(nullptr, 0, "lig_%lld_%lld", (long long)seed, (long long)(first_index + i));
+  off[0] = 0;
+  for (int32_t i = 0; i < count; ++i) off[i + 1] = off[i] + len[i];
+  if (buf) {
+#pragma omp parallel for schedule(static)
+    for (int32_t i = 0; i < count; ++i) {
+      char tmp[64];
+      snprintf(tmp, sizeof tmp, "lig_%lld_%lld", (long long)seed, (long long)(first_index + i));
+      memcpy(buf + off[i], tmp, (size_t)len[i]);
+    }
+  }
+  return DS_OK;
+}
+
 int ds_mixed_shapes(int64_t seed, int64_t first_index, int32_t count, int32_t heavy_min, int32_t heavy_max,
                     int32_t frag_max, int32_t *shapes) {
   if (count < 0 || !shapes || heavy_min < 1 || heavy_max < heavy_min || heavy_max > DS_MAX_ATOMS || frag_max < 0)

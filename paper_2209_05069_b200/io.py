@@ -12,7 +12,7 @@ from typing import Iterable, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import model
-from .native import LigandBatch, InteractionTable, _p, check, lib, MASK_WORDS
+from .native import GeneratedIds, LigandBatch, InteractionTable, _p, check, lib, MASK_WORDS
 
 SYNTH_POCKET = dict(n_atoms=200, seed=7, rmin=7.0, rmax=10.0, spacing=0.5, padding=4.0)
 
@@ -40,7 +40,7 @@ def generate_batch(shapes: np.ndarray, seed: int, first_index: int = 0) -> Ligan
     mask = np.zeros((max(int(fo[-1]), 1), MASK_WORDS), np.uint32)
     check(L.ds_generate_ligands(int(seed), int(first_index), n, _p(shapes), _p(ao), _p(bo), _p(fo),
                                 _p(xyz), _p(typ), _p(bonds), _p(axis), _p(mask)))
-    ids = [generated_id(seed, first_index + i) for i in range(n)]
+    ids = GeneratedIds(seed, first_index, n)
     return LigandBatch(ao, xyz[:ao[-1]], typ[:ao[-1]], bo, bonds[:bo[-1]], fo, axis[:fo[-1]], mask[:fo[-1]], ids)
 
 

@@ -14,6 +14,7 @@ import threading
 import weakref
 from dataclasses import dataclass
 from typing import Tuple, List, Optional, Sequence
+import collections.abc as _abc
 
 import numpy as np
 
@@ -118,6 +119,7 @@ def lib():
             "ds_op_rescore": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.c_float, vp]),
             "ds_ligand_id_hash": (u64, [C.c_char_p, C.c_size_t]),
             "ds_generated_id": (C.c_int, [i64, i64, C.c_char_p, C.c_size_t]),
+            "ds_generated_ids": (C.c_int, [i64, i64, i32, C.c_void_p, C.c_void_p]),
             "ds_mixed_shapes": (C.c_int, [i64, i64, i32, i32, i32, i32, vp]),
             "ds_generate_ligands": (C.c_int, [i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "ds_pack_ligands": (C.c_int, [i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
@@ -129,6 +131,8 @@ def lib():
             "ds_ligq_fill": (C.c_int, [vp] * 11),
             "ds_ligq_free": (None, [vp]),
             "ds_validate_ligands": (C.c_int, [i32] + [vp] * 10),
+            "ds_generate_resident": (C.c_int, [vp, i64, i64, i32, vp, vp, vp]),
+            "ds_batch_read_inputs": (C.c_int, [vp, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -177,6 +181,41 @@ def device_count() -> int:
 
 
 # ---- ligand batches --------------------------------------------------------------------
+class GeneratedIds(_abc.Sequence):
+    """The ids of generated ligands first .. first + n - 1 ("lig_<seed>_<index>"),
+    materialised only on access: a 10M-ligand screen never builds 10M Python strings, and
+    id_blob() makes the packed id bytes natively (ds_generated_ids)."""
+
+    def __init__(self, seed: int, first: int, n: int):
+        self.seed, self.first, self.n = int(seed), int(first), int(n)
+
+    def __len__(self) -> int:
+        return self.n
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            lo, hi, step = i.indices(self.n)
+            if step != 1:
+                return [self[k] for k in range(lo, hi, step)]
+            return GeneratedIds(self.seed, self.first + lo, max(hi - lo, 0))
+        i = int(i)
+        if i < 0:
+            i += self.n
+        if not 0 <= i < self.n:
+            raise IndexError(i)
+        return f"lig_{self.seed}_{self.first + i}"
+
+    def __eq__(self, other) -> bool:
+        return list(self) == list(other) if isinstance(other, (list, tuple, GeneratedIds)) else NotImplemented
+
+    def id_blob(self):
+        off = np.zeros(self.n + 1, np.int64)
+        check(lib().ds_generated_ids(self.seed, self.first, self.n, None, _p(off)))
+        buf = np.zeros(max(int(off[-1]), 1), np.uint8)
+        check(lib().ds_generated_ids(self.seed, self.first, self.n, _p(buf), _p(off)))
+        return buf[:int(off[-1])].tobytes(), off
+
+
 @dataclass
 class LigandBatch:
     """CSR ligand batch in the reference's terms (absolute Å coordinates, element codes,
@@ -202,6 +241,8 @@ class LigandBatch:
         return np.diff(self.frag_off)
 
     def id_bytes(self):
+        if isinstance(self.ids, GeneratedIds):
+            return self.ids.id_blob()
         enc = [s.encode() for s in self.ids]
         off = np.zeros(len(enc) + 1, dtype=np.int64)
         off[1:] = np.cumsum([len(e) for e in enc])
@@ -214,7 +255,8 @@ class LigandBatch:
         f0, f1 = int(self.frag_off[lo]), int(self.frag_off[hi])
         return LigandBatch(self.atom_off[lo:hi + 1] - a0, self.atom_xyz[a0:a1], self.atom_type[a0:a1],
                            self.bond_off[lo:hi + 1] - b0, self.bonds[b0:b1], self.frag_off[lo:hi + 1] - f0,
-                           self.frag_axis[f0:f1], self.frag_mask[f0:f1], list(self.ids[lo:hi]))
+                           self.frag_axis[f0:f1], self.frag_mask[f0:f1],
+                           self.ids[lo:hi] if isinstance(self.ids, GeneratedIds) else list(self.ids[lo:hi]))
 
     def subset(self, idx: Sequence[int]) -> "LigandBatch":
         return LigandBatch.from_ligands([self.ligand(int(i)) for i in idx])
@@ -537,10 +579,41 @@ class Context:
 class ResidentBatch:
     """A packed batch kept in device memory (kernel-only timing, bench.py `value`)."""
 
-    def __init__(self, ctx: Context, packed: PackedBatch):
-        h = C.c_void_p()
-        check(lib().ds_batch_upload(ctx.handle, C.byref(packed.desc()), C.byref(h)))
-        self.ctx, self.packed, self.handle = ctx, packed, h
+    def __init__(self, ctx: Context, packed: Optional[PackedBatch], handle=None, n: int = 0,
+                 atom_off: Optional[np.ndarray] = None, frag_off: Optional[np.ndarray] = None):
+        if handle is None:
+            handle = C.c_void_p()
+            check(lib().ds_batch_upload(ctx.handle, C.byref(packed.desc()), C.byref(handle)))
+            n, atom_off, frag_off = packed.n, packed.atom_off, packed.frag_off
+        self.ctx, self.packed, self.handle, self.n = ctx, packed, handle, n
+        self.atom_off, self.frag_off = atom_off, frag_off
+        self.generate_ms = 0.0
+
+    @classmethod
+    def generated(cls, ctx: Context, seed: int, first_index: int, shapes: np.ndarray) -> "ResidentBatch":
+        """Device-side ingest (ds_generate_resident): ligands first_index .. + len(shapes) of the
+        synthetic dataset generated and packed on the GPU — the same arrays as
+        ResidentBatch(ctx, pack(io.generate_batch(shapes, seed, first_index)))."""
+        shapes = np.ascontiguousarray(np.asarray(shapes, np.int32).reshape(-1, 2))
+        h, ms = C.c_void_p(), C.c_float(0.0)
+        check(lib().ds_generate_resident(ctx.handle, int(seed), int(first_index), len(shapes), _p(shapes), C.byref(h),
+                                         C.byref(ms)))
+        n = len(shapes)
+        ao, bo, fo = (np.zeros(n + 1, np.int32) for _ in range(3))
+        check(lib().ds_generate_ligands(int(seed), int(first_index), n, _p(shapes), _p(ao), _p(bo), _p(fo),
+                                        None, None, None, None, None))
+        rb = cls(ctx, None, handle=h, n=n, atom_off=ao, frag_off=fo)
+        rb.generate_ms = float(ms.value)
+        return rb
+
+    def read_inputs(self):
+        """(atom_xyzt [atoms, 4] f32, frag_desc [frags, 8] u32, id_hash [n] u64) as resident."""
+        na, nf = int(self.atom_off[-1]), int(self.frag_off[-1])
+        xyzt = np.zeros((max(na, 1), 4), np.float32)
+        fd = np.zeros((max(nf, 1), FRAG_WORDS), np.uint32)
+        idh = np.zeros(max(self.n, 1), np.uint64)
+        check(lib().ds_batch_read_inputs(self.ctx.handle, self.handle, _p(xyzt), _p(fd), _p(idh)))
+        return xyzt[:na], fd[:nf], idh[:self.n]
 
     def dock(self, dpocket: DevicePocket, cfg: model.DockConfig, seed: int = 0, family: int = FAMILY_BATCHED) -> Stats:
         st = Stats()
@@ -550,10 +623,10 @@ class ResidentBatch:
         return st
 
     def download(self) -> np.ndarray:
-        res = np.zeros(max(self.packed.n, 1), dtype=RESULT_DTYPE)
+        res = np.zeros(max(self.n, 1), dtype=RESULT_DTYPE)
         out = Outputs(_p(res), None, None, None, None)
         check(lib().ds_batch_download(self.ctx.handle, self.handle, C.byref(out)))
-        return res[:self.packed.n]
+        return res[:self.n]
 
     def close(self):
         if self.handle:
