@@ -56,6 +56,20 @@ def test_latency_parity_mixed_and_options(gpu_ctx, synth_pocket, table):
             assert np.array_equal(g.results["bump_checks"].astype(np.int64), o.results["bump_checks"])
 
 
+@pytest.mark.parametrize("restarts", [1, 12, 32])
+def test_latency_cluster_alignment_restart_counts(gpu_ctx, synth_pocket, table, restarts):
+    """The latency alignment for the default 12-degree step is one 8-CTA cluster per (ligand,
+    restart) with a DSMEM reduction to the argmax key: grids of L x N clusters for N = 1 .. 32,
+    ligands from 3 to 160 atoms (fewer atoms than the cluster's 32 warps included)."""
+    batch = io.generate_mixed_batch(12, seed=13)
+    small = io.generate_dataset_batch(1, 0, 2, seed=3)     # 2-3 atoms
+    big = io.generate_dataset_batch(70, 30, 2, seed=4)     # 160 atoms
+    cfg = model.DockConfig(restarts_n=restarts, rescore_top_k=min(4, restarts))
+    for b in (batch, small, big):
+        g, o = _run(gpu_ctx, b, synth_pocket, table, cfg, seed=5, family=FAMILY_LATENCY)
+        compare(b, g, o, cfg)
+
+
 def test_families_agree(gpu_ctx, synth_pocket, table):
     """Engine equivalence on the device: both families, identical records."""
     batch = io.generate_mixed_batch(100, seed=8)
