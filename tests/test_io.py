@@ -174,3 +174,22 @@ def test_native_ligq_validation_errors(tmp_path, frag):
     fast = io.parse_ligand_batch(str(f), skip_invalid=True)
     assert [l.id for l in ref] == list(fast.ids) == ["m2"]
     _same_batch(fast, native.LigandBatch.from_ligands(ref))
+
+
+def test_generated_ids_lazy_sequence():
+    """Generated ligands carry a lazy id sequence (native.GeneratedIds): the same strings as
+    ds_generated_id, slices stay lazy, and the packed id bytes come from one native call."""
+    from paper_2209_05069_b200.native import GeneratedIds
+    ids = GeneratedIds(-7, 99, 50)
+    want = [io.generated_id(-7, 99 + i) for i in range(50)]
+    assert list(ids) == want and len(ids) == 50 and ids[-1] == want[-1]
+    assert isinstance(ids[10:20], GeneratedIds) and list(ids[10:20]) == want[10:20]
+    assert ids[::7] == want[::7]
+    blob, off = ids.id_blob()
+    assert blob == b"".join(s.encode() for s in want)
+    assert off.tolist() == np.cumsum([0] + [len(s) for s in want]).tolist()
+    b = io.generate_mixed_batch(20, seed=3, first_index=5)
+    assert isinstance(b.ids, GeneratedIds) and b.ids[0] == "lig_3_5"
+    assert list(b.slice(4, 9).ids) == [f"lig_3_{5 + k}" for k in range(4, 9)]
+    with pytest.raises(IndexError):
+        ids[50]
