@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(32)
   const int a0 = bt.atom_off[lig];
   const int A = bt.atom_off[lig + 1] - a0;
   const int c0 = c * ach, c1 = min(A, c0 + ach);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (c0 >= A) return;
   __shared__ float4 strig[360];
   const int n_a = kConst ? NA : dp.n_a;
@@ -329,6 +330,9 @@ template <int CS, int W>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(W * 32)
     k_align_latency_cl(PocketView pk, BatchView bt, DockParams dp, unsigned *keys) {
   constexpr int NA = 30, NR = NA * NA, SL = (NR + CS - 1) / CS;
+  // the optimisation kernel may launch now (programmatic dependent launch): it stages its shared
+  // memory while this kernel runs and waits (griddepcontrol.wait) before reading the keys
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ int part[W][NR];
   __shared__ unsigned s_best;
   cg::cluster_group cl = cg::this_cluster();

@@ -164,6 +164,10 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   }
   for (int i = lut_bulk + tid; i < lut_n; i += kLatThreads) slut[i] = __ldg(pk.bin_lut + i);  // < 16 B tail
   __syncthreads();
+  // everything above only read inputs that were complete before the alignment kernel started; the
+  // keys / scores it writes are read below, after the programmatic-dependent-launch wait (a no-op
+  // when the kernel was launched without the attribute)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // ---- argmax of the alignment scores (ties -> smallest rotation index); each slot is zeroed by
   // the thread that read it, so the buffer is clean for the next call (no memset per call) ----
   if (keys) {  // the cluster align kernel already reduced this (ligand, restart) to its key
@@ -572,19 +576,27 @@ __global__ void __launch_bounds__(kLatThreads, 1)
 size_t latency_rec_bytes() { return sizeof(LatRec); }
 
 void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
-                             const unsigned *keys, OptOut out, void *recs, int *done, cudaStream_t st) {
+                             const unsigned *keys, OptOut out, void *recs, int *done, bool pdl, cudaStream_t st) {
   const size_t base = lat_base_bytes(pk.nb, pk.lut_cap);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t with_grid = base + (size_t)pk.grid_bytes;
-  if (with_grid + sizeof(LatSmem) + 1024 <= (size_t)optin) {
-    cudaFuncSetAttribute(k_optimize_latency<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)with_grid);
-    k_optimize_latency<true><<<bt.L * dp.N, kLatThreads, with_grid, st>>>(pk, bt, dp, scores, keys, out, (LatRec *)recs, done);
-  } else {
-    cudaFuncSetAttribute(k_optimize_latency<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)base);
-    k_optimize_latency<false><<<bt.L * dp.N, kLatThreads, base, st>>>(pk, bt, dp, scores, keys, out, (LatRec *)recs, done);
-  }
+  const bool fits = with_grid + sizeof(LatSmem) + 1024 <= (size_t)optin;
+  auto kern = fits ? k_optimize_latency<true> : k_optimize_latency<false>;
+  const size_t smem = fits ? with_grid : base;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(bt.L * dp.N);
+  cfg.blockDim = dim3(kLatThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, pk, bt, dp, scores, keys, out, (LatRec *)recs, done);
 }
 
 }  // namespace ds
