@@ -111,6 +111,10 @@ struct ds_ctx {
   bool lat_dirty = true;
   void *lat_scores_seen = nullptr, *lat_done_seen = nullptr;
   size_t x_in_bytes = 0, x_out_bytes = 0, x_out_off[5] = {};
+  // express latency calls write their outputs straight into the pinned staging buffer (zero-copy,
+  // no D2H); x_rtors_host is where the last CTA copies the per-restart torsion indices
+  bool x_zero_copy = false;
+  uint8_t *x_rtors_host = nullptr;
   // pinned host staging
   void *h_stage = nullptr;
   size_t h_cap = 0;
@@ -656,7 +660,7 @@ int reserve_express(ds_ctx *c, int L, int NA, int NF) {
   return DS_OK;
 }
 
-int upload_express(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
+int upload_express(ds_ctx *c, const ds_batch_desc *b, int N, bool zero_copy_out, ds_stats *st) {
   const int L = b->n_ligands;
   const int NA = b->atom_off[L], NF = b->frag_off[L];
   std::vector<int> oa, oo;
@@ -701,6 +705,24 @@ int upload_express(ds_ctx *c, const ds_batch_desc *b, int N, ds_stats *st) {
   c->io.btors = (uint8_t *)(dout + c->x_out_off[4]);
   c->x_in_bytes = in_bytes;
   c->x_out_bytes = out_bytes;
+  c->x_zero_copy = false;
+  c->x_rtors_host = nullptr;
+  char *hd = nullptr;  // device view of the pinned staging buffer (UVA)
+  static const bool zc_env = [] {
+    const char *e = getenv("DS_ZERO_COPY");
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (zero_copy_out && zc_env && cudaHostGetDevicePointer((void **)&hd, c->h_stage, 0) == cudaSuccess && hd) {
+    hd += in_bytes;
+    c->io.res = (ds_result *)(hd + c->x_out_off[0]);
+    c->io.rrec = (ds_restart_record *)(hd + c->x_out_off[1]);
+    c->io.coords = (float *)(hd + c->x_out_off[3]);
+    c->io.btors = (uint8_t *)(hd + c->x_out_off[4]);
+    c->x_rtors_host = (uint8_t *)(hd + c->x_out_off[2]);  // rtors itself stays in device memory
+    c->x_zero_copy = true;
+  } else {
+    cudaGetLastError();
+  }
   if (st) st->h2d_bytes += (int64_t)in_bytes;
   return DS_OK;
 }
@@ -770,7 +792,7 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t at
   if ((rc = c->ensure(c->b_scratch, sizeof(float4) * (size_t)dp.N * (size_t)n_atoms_range)) ||
       (rc = c->ensure(c->b_rgv, sizeof(int) * (size_t)dp.N * (size_t)(L1 - L0))))
     return rc;
-  OptOut oo;
+  OptOut oo = {};
   oo.res = c->io.res + L0;
   oo.rrec = want_rrec ? c->io.rrec + (size_t)L0 * dp.N : nullptr;
   oo.rtors = c->io.rtors;
@@ -826,13 +848,14 @@ int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const Dock
   const bool keyed =
       launch_align_latency(pk->view, bt, dp, max_atoms, (int *)c->b_lat_scores.p, (unsigned *)c->b_keys.p, c->stream);
   if (!pdl) cudaEventRecord(c->ev[2], c->stream);
-  OptOut oo;
+  OptOut oo = {};
   oo.res = c->io.res;
   oo.rrec = want_rrec ? c->io.rrec : nullptr;
   oo.rtors = c->io.rtors;
   oo.final_u = (float4 *)c->b_scratch.p;
   oo.best_coords = want_coords ? c->io.coords : nullptr;
   oo.best_tors = want_btors ? c->io.btors : nullptr;
+  oo.rtors_host = c->x_zero_copy ? c->x_rtors_host : nullptr;
   c->lat_dirty = true;  // until the call has completed (set clean again below / by ds_dock)
   launch_optimize_latency(pk->view, bt, dp, (int *)c->b_lat_scores.p, keyed ? (const unsigned *)c->b_keys.p : nullptr,
                           oo, c->b_lat_recs.p,
@@ -1056,13 +1079,20 @@ int ds_dock(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const ds_doc
   const int NA = b->atom_off[L], NF = b->frag_off[L];
   const bool express = express_in_bytes(b) <= kExpressMaxBytes;
   cudaEventRecord(c->ev[0], c->stream);
-  if ((rc = express ? upload_express(c, b, dp.N, st) : upload_batch(c, b, dp.N, st))) return rc;
+  c->x_zero_copy = false;
+  if ((rc = express ? upload_express(c, b, dp.N, family == DS_FAMILY_LATENCY, st) : upload_batch(c, b, dp.N, st)))
+    return rc;
   int max_atoms = 0;
   for (int i = 0; i < L; ++i) max_atoms = std::max(max_atoms, b->atom_off[i + 1] - b->atom_off[i]);
   if ((rc = run_family(c, pk, family, L, NA, NF, max_atoms, dp, out->best_coords != nullptr,
                        out->best_torsion != nullptr, out->restarts != nullptr, st)))
     return rc;
-  if ((rc = express ? download_express(c, st) : download(c, L, NA, NF, dp.N, out, st))) return rc;
+  if (express && c->x_zero_copy) {
+    if (st) st->d2h_bytes += (int64_t)c->x_out_bytes;  // written by the kernels over the bus instead
+  } else if ((rc = express ? download_express(c, st) : download(c, L, NA, NF, dp.N, out, st))) {
+    return rc;
+  }
+  c->x_zero_copy = false;
   cudaEventRecord(c->ev[4], c->stream);
   DS_CUDA(cudaStreamSynchronize(c->stream));
   if (family == DS_FAMILY_LATENCY) c->lat_dirty = false;  // a completed call leaves its scratch zeroed
@@ -1124,6 +1154,7 @@ int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_d
   int max_atoms = 0;
   for (int i = 0; i < d->L; ++i) max_atoms = std::max(max_atoms, d->atom_off[i + 1] - d->atom_off[i]);
   io_from_buffers(c);  // the resident batch lives in the per-array buffers (not an express arena)
+  c->x_zero_copy = false;
   if ((rc = run_family(c, pk, family, d->L, d->n_atoms, d->n_frags, max_atoms, dp, true, true, true, st))) return rc;
   DS_CUDA(cudaStreamSynchronize(c->stream));
   if (family == DS_FAMILY_LATENCY) c->lat_dirty = false;

@@ -67,6 +67,7 @@ struct OptOut {
   long long atom_base;       // batched: first atom of the launch range
   float *best_coords;        // atom_total*3 (may be null)
   uint8_t *best_tors;        // frag_total (may be null)
+  uint8_t *rtors_host;       // latency, zero-copy outputs: the last CTA copies its ligand's rtors here
 };
 
 }  // namespace ds

@@ -571,6 +571,9 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   if (out.best_tors)
     for (int f = tid; f < F; f += kLatThreads)
       out.best_tors[f0 + f] = __ldcg(out.rtors + (size_t)(f0 + f) * dp.N + best_r);
+  if (out.rtors_host)  // zero-copy outputs: every restart's torsion indices, straight to the host
+    for (int q = tid; q < F * dp.N; q += kLatThreads)
+      out.rtors_host[(size_t)f0 * dp.N + q] = __ldcg(out.rtors + (size_t)f0 * dp.N + q);
 }
 
 size_t latency_rec_bytes() { return sizeof(LatRec); }
