@@ -1149,7 +1149,11 @@ int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_d
   int rc;
   if ((rc = check_config(cfg, pk, &dp))) return rc;
   if (st) memset(st, 0, sizeof *st);
-  if (d->L == 0) return DS_OK;
+  if (d->L == 0) {  // nothing to dock; the (empty) download is still valid
+    d->N = dp.N;
+    d->docked = true;
+    return DS_OK;
+  }
   DS_CUDA(enter_device(c->device));
   int max_atoms = 0;
   for (int i = 0; i < d->L; ++i) max_atoms = std::max(max_atoms, d->atom_off[i + 1] - d->atom_off[i]);
@@ -1167,6 +1171,7 @@ int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_d
 int ds_batch_download(ds_ctx *c, ds_dev_batch *d, const ds_outputs *out) {
   if (!c || !d || !out) return fail(DS_ERR_INVALID_ARG, "NULL argument");
   if (!d->docked) return fail(DS_ERR_INVALID_ARG, "batch has not been docked");
+  if (d->L == 0) return DS_OK;
   int rc;
   if ((rc = download(c, d->L, d->n_atoms, d->n_frags, d->N, out, nullptr))) return rc;
   DS_CUDA(cudaStreamSynchronize(c->stream));

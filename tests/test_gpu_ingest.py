@@ -45,3 +45,23 @@ def test_generated_batch_docks_like_host(gpu_ctx, synth_pocket, table):
 def test_generator_rejects_infeasible_shape(gpu_ctx):
     with pytest.raises(model.InfeasibleShape):
         native.ResidentBatch.generated(gpu_ctx, 1, 0, np.array([[10, 9]], np.int32))
+
+
+def test_generate_empty_and_reuse(gpu_ctx, synth_pocket, table):
+    """An empty generated batch docks to nothing; a generated batch followed by a host-packed one on
+    the same context (shared device buffers) still matches the host path."""
+    dp = gpu_ctx.pocket(synth_pocket, table)
+    cfg = model.DockConfig()
+    rb = native.ResidentBatch.generated(gpu_ctx, 2, 0, np.zeros((0, 2), np.int32))
+    assert rb.n == 0
+    rb.dock(dp, cfg)
+    assert len(rb.download()) == 0
+    rb.close()
+    shapes = io.mixed_shapes(300, 8, 0)
+    g = native.ResidentBatch.generated(gpu_ctx, 8, 0, shapes)
+    g.dock(dp, cfg, family=native.FAMILY_LATENCY)
+    got = g.download()
+    g.close()
+    out = gpu_ctx.dock(dp, _host_packed(8, 0, shapes), cfg, 0, native.FAMILY_LATENCY)
+    for f in ("status", "geom_score", "chem_fx", "best_restart", "best_ax", "best_ay", "n_kept"):
+        assert np.array_equal(got[f], out.results[f]), f
