@@ -29,6 +29,7 @@ constexpr int kLatChunk = 8;
 
 struct LatRec {  // per (ligand, restart), read by the ligand's last CTA
   int geom, valid, degen, align_score;
+  int degen_f;     // the fragment a DegenerateAxis stopped this restart at
   unsigned evals, pairs, exits, rot;
   long long chem;  // rescore of the restart's final pose (P11), valid poses only
 };
@@ -47,7 +48,7 @@ struct LatSmem {
   int ascore[32];
   unsigned abump;
   unsigned key;
-  int degen, is_last;
+  int degen, degen_f, is_last;
   unsigned pairs;
   int geom;
   int ord[DS_MAX_RESTARTS], kept[DS_MAX_RESTARTS], nkept;
@@ -219,7 +220,10 @@ __global__ void __launch_bounds__(kLatThreads, 1)
       const float vx = __fsub_rn(pb.x, pa.x), vy = __fsub_rn(pb.y, pa.y), vz = __fsub_rn(pb.z, pa.z);
       const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
       if (!(len >= dp.eps_axis)) {
-        if (tid == 0) S.degen = 1;
+        if (tid == 0) {
+          S.degen = 1;
+          S.degen_f = f;
+        }
         break;
       }
       kx = __fdiv_rn(vx, len);
@@ -426,6 +430,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     rec.geom = S.geom;
     rec.valid = valid;
     rec.degen = degen;
+    rec.degen_f = degen ? S.degen_f : 0;
     rec.align_score = (int)(key >> 16) - 32768;
     rec.evals = evals;
     rec.pairs = S.pairs;
@@ -454,35 +459,58 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   // ---- the ligand's last CTA: select_poses (P12), best rescored kept pose ----
   const LatRec *lr = recs + (size_t)lig * dp.N;
   __shared__ int s_geom[DS_MAX_RESTARTS], s_valid[DS_MAX_RESTARTS];
-  __shared__ unsigned s_cnt[4];
+  __shared__ unsigned s_cnt[4], s_nal;
+  __shared__ int s_degf;
   if (tid < dp.N) {
     s_geom[tid] = __ldcg(&lr[tid].geom);
     s_valid[tid] = __ldcg(&lr[tid].valid);
     S.dis[tid] = 0u;
   }
   if (tid == 0) {
-    unsigned ev = 0, pr = 0, ex = 0, dg = 0;
-    for (int q = 0; q < dp.N; ++q) {
+    // counters in the oracle's sequential order: restarts run in order and a DegenerateAxis stops
+    // the ligand, so only restarts up to the first degenerate one count (P14)
+    unsigned ev = 0, pr = 0, ex = 0, dg = 0, nal = 0;
+    for (int q = 0; q < dp.N && !dg; ++q) {
       ev += __ldcg(&lr[q].evals);
       pr += __ldcg(&lr[q].pairs);
       ex += __ldcg(&lr[q].exits);
-      dg |= (unsigned)__ldcg(&lr[q].degen);
+      dg = (unsigned)__ldcg(&lr[q].degen);
+      ++nal;
     }
     s_cnt[0] = ev;
     s_cnt[1] = pr;
     s_cnt[2] = ex;
     s_cnt[3] = dg;
+    s_nal = nal;
+    s_degf = dg ? __ldcg(&lr[nal - 1].degen_f) : 0;
     S.chem = 0ull;
   }
   __syncthreads();
   ds_result res;
   memset(&res, 0, sizeof res);
-  res.poses_scored = (unsigned)(dp.N * dp.n_rot) + s_cnt[0];
+  res.poses_scored = s_nal * (unsigned)dp.n_rot + s_cnt[0];
   res.bump_checks = s_cnt[1];
   res.bump_early_exits = s_cnt[2];
   if (s_cnt[3]) {
     res.status = DS_STATUS_DEGENERATE_AXIS;
     if (tid == 0) out.res[lig] = res;
+    // the sequential oracle stops at restart rd, fragment fd: later records stay zero
+    const int rd = (int)s_nal - 1, fd = s_degf;
+    if (out.rrec)
+      for (int q = rd + tid; q < dp.N; q += kLatThreads) {
+        ds_restart_record z;
+        memset(&z, 0, sizeof z);
+        out.rrec[(size_t)lig * dp.N + q] = z;
+      }
+    for (int q = tid; q < F * dp.N; q += kLatThreads) {
+      const int f = q / dp.N, rr = q - f * dp.N;
+      uint8_t v = __ldcg(out.rtors + (size_t)f0 * dp.N + q);
+      if (rr > rd || (rr == rd && f >= fd)) {
+        v = 0;
+        out.rtors[(size_t)f0 * dp.N + q] = 0;
+      }
+      if (out.rtors_host) out.rtors_host[(size_t)f0 * dp.N + q] = v;
+    }
     return;
   }
   int nvalid = 0;

@@ -223,6 +223,23 @@ __device__ __forceinline__ bool bump_hit(const TorWarpSmem &S, unsigned info, fl
   return mind < bd2;
 }
 
+// A DegenerateAxis stops the ligand where the sequential oracle stops: restart records from the
+// stopping restart on and torsion indices of (restart rd, fragments >= fd) and of later restarts
+// are left zero, as the oracle leaves them (warp-cooperative, cold path)
+__device__ __noinline__ void clear_unreached(const OptOut &out, int N, int f0, int F, int rd, int fd, int lig) {
+  const int lane = threadIdx.x & 31;
+  if (out.rrec)
+    for (int r = rd + lane; r < N; r += 32) {
+      ds_restart_record z;
+      memset(&z, 0, sizeof z);
+      out.rrec[(size_t)lig * N + r] = z;
+    }
+  for (int q = lane; q < F * N; q += 32) {
+    const int f = q / N, r = q - f * N;
+    if (r > rd || (r == rd && f >= fd)) out.rtors[(size_t)(f0 + f) * N + r] = 0;
+  }
+}
+
 __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
     k_torsion_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
                       OptOut out, int *queue) {
@@ -247,6 +264,8 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
     const uint64_t idh = bt.idh[lig];
     unsigned pairs_total = 0, early_exits = 0, evals = 0;
     bool degenerate = false;
+    int n_aligned = dp.N;  // restarts whose alignment counts (P14; all unless a DegenerateAxis stops early)
+    int deg_f = 0;         // the fragment that stopped it
     float4 *fin = out.final_u + (size_t)(a0 - out.atom_base) * dp.N;  // final poses, restart r at r*A
 
     for (int r = 0; r < dp.N && !degenerate; ++r) {
@@ -310,6 +329,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
           if (!(len >= dp.eps_axis)) {  // DegenerateAxis
             degenerate = true;
+            deg_f = f;
             break;
           }
           kx = __fdiv_rn(vx, len);
@@ -530,7 +550,10 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         if (lane == 0) out.rtors[(size_t)(f0 + f) * dp.N + r] = best_k < 0 ? (uint8_t)DS_TORSION_NONE : (uint8_t)best_k;
         __syncwarp();
       }
-      if (degenerate) break;
+      if (degenerate) {  // the oracle stops the ligand here: restarts 0..r were aligned
+        n_aligned = r + 1;
+        break;
+      }
       // final geometric score + store the final pose
       int sc = 0;
       for (int i = lane; i < A; i += 32) {
@@ -557,6 +580,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
       __syncwarp();
     }
 
+    if (degenerate) clear_unreached(out, dp.N, f0, F, n_aligned - 1, deg_f, lig);
     // counters and the degenerate status; k_select_batched completes the record
     if (lane == 0) {
       ds_result res;
@@ -566,7 +590,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
       res.best_ax = 0;
       res.best_ay = 0;
       res.n_kept = 0;
-      res.poses_scored = (unsigned)(dp.N * dp.n_rot) + evals;
+      res.poses_scored = (unsigned)(n_aligned * dp.n_rot) + evals;
       res.bump_checks = pairs_total;
       res.bump_early_exits = early_exits;
       res.status = degenerate ? DS_STATUS_DEGENERATE_AXIS : DS_STATUS_OK;

@@ -4,7 +4,7 @@ import pytest
 
 import oracle
 from helpers import compare
-from paper_2209_05069_b200 import io, model
+from paper_2209_05069_b200 import io, model, native
 from paper_2209_05069_b200.native import FAMILY_BATCHED, FAMILY_LATENCY, pack
 
 pytestmark = pytest.mark.gpu
@@ -233,3 +233,22 @@ def test_parity_large_weights_no_int32_overflow(gpu_ctx, synth_pocket):
     for fam in (FAMILY_BATCHED, FAMILY_LATENCY):
         g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg, seed=1, family=fam)
         compare(batch, g, o, cfg)
+
+
+def test_degenerate_axis_both_families(gpu_ctx, synth_pocket, table):
+    """DegenerateAxis: a fragment whose two axis atoms coincide stops the ligand
+    with status DEGENERATE_AXIS in both families, as in the oracle; the other ligands of the batch
+    are unaffected."""
+    batch = io.generate_dataset_batch(20, 6, 8, seed=21)
+    xyz = batch.atom_xyz.copy()
+    for i in (1, 4, 6):  # ligands with a degenerate fragment (fragment i % 3 of the ligand)
+        a0, f0 = int(batch.atom_off[i]), int(batch.frag_off[i])
+        b, e = batch.frag_axis[f0 + i % 3]
+        xyz[a0 + e] = xyz[a0 + b]
+    bad = native.LigandBatch(batch.atom_off, xyz, batch.atom_type, batch.bond_off, batch.bonds, batch.frag_off,
+                             batch.frag_axis, batch.frag_mask, list(batch.ids))
+    cfg = model.DockConfig()
+    for fam in (FAMILY_BATCHED, FAMILY_LATENCY):
+        g, o = _run(gpu_ctx, bad, synth_pocket, table, cfg, seed=1, family=fam)
+        assert (o.results["status"][[1, 4, 6]] == native.STATUS_DEGENERATE_AXIS).all()
+        compare(bad, g, o, cfg)
