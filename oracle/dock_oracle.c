@@ -316,65 +316,109 @@ static int bump_check(const or_lig *L, int f, const float (*u)[3], float bd2, in
 }
 
 /* ---------------------------------------------------------------- SPEC.md:277 dock_ligand */
-int or_dock_ligand(const or_lig *L, const or_pk *k, const or_config *cfg, or_result *res, or_restart *rr,
-                   uint8_t *tors /* F*N: [f*N + r] */, float *best_xyz /* A*3 Å, may be NULL */) {
-  trig_init();
+/* One restart of Alg. 1 (starting pose, align, optimize_pose) into U; its own counters in *cnt.
+ * Returns 2 on DegenerateAxis (cnt then holds the counts up to that point, like the sequential
+ * scan), else 0. */
+typedef struct {
+  int64_t poses_scored, bump_checks, bump_checks_r32, bump_early_exits;
+  int geom, valid, ax, ay, align_score;
+} or_restart_out;
+
+static int dock_restart(const or_lig *L, const or_pk *k, const or_config *cfg, int r, float (*U)[3],
+                        uint8_t *tors /* F*N or NULL */, or_restart_out *o) {
   const int N = cfg->restarts_n, na = 360 / cfg->alignment_step_deg, nt = 360 / cfg->torsion_step_deg;
   const double s = (double)k->p->spacing;
   const float bd2 = (float)(((double)cfg->bump_distance / s) * ((double)cfg->bump_distance / s));
   const float eps = (float)(1e-9 / s);
-  const double thr = (double)cfg->similarity_rmsd / s;
+  memset(o, 0, sizeof *o);
+  float R0s[9], t[3];
+  starting_pose(L, k, r, cfg->seed, R0s, t);
+  int ix = 0, iy = 0;
+  o->align_score = align_pose(L, k, cfg, R0s, t, &ix, &iy, U);
+  o->poses_scored += (int64_t)na * na;
+  o->ax = ix;
+  o->ay = iy;
+  /* SPEC.md:257 optimize_pose */
+  int all_bumped = 0;
+  for (int f = 0; f < L->F; ++f) {
+    float cand[OR_MAX_ATOMS][3];
+    int best = 0, best_k = -1;
+    for (int a = 0; a < nt; ++a) {
+      if (apply_torsion(L, f, (const float(*)[3])U, a * cfg->torsion_step_deg, eps, cand) < 0 && nt > 1)
+        return 2; /* DegenerateAxis */
+      o->poses_scored += 1;
+      if (bump_check(L, f, (const float(*)[3])cand, bd2, cfg->early_exit, &o->bump_checks, &o->bump_checks_r32,
+                     &o->bump_early_exits))
+        continue;
+      int sc = grid_score(k, (const float(*)[3])cand, L->A);
+      if (best_k < 0 || sc > best) {
+        best = sc;
+        best_k = a;
+      }
+    }
+    if (best_k > 0) {
+      apply_torsion(L, f, (const float(*)[3])U, best_k * cfg->torsion_step_deg, eps, cand);
+      memcpy(U, cand, sizeof(float) * 3 * L->A);
+    }
+    if (best_k < 0) ++all_bumped;
+    if (tors) tors[f * N + r] = best_k < 0 ? 255 : (uint8_t)best_k;
+  }
+  o->valid = !(L->F >= 1 && all_bumped == L->F);
+  o->geom = grid_score(k, (const float(*)[3])U, L->A);
+  return 0;
+}
+
+/* dock_ligand; inner_threads > 1 runs the restarts on an inner pool (the latency engine's
+ * pose-level parallelism) with results identical to the sequential loop. */
+static int dock_ligand_impl(const or_lig *L, const or_pk *k, const or_config *cfg, or_result *res, or_restart *rr,
+                            uint8_t *tors, float *best_xyz, int inner_threads) {
+  trig_init();
+  const int N = cfg->restarts_n;
+  const double thr = (double)cfg->similarity_rmsd / (double)k->p->spacing;
   const double thr2 = thr * thr;
   static __thread float U[OR_MAX_RESTARTS][OR_MAX_ATOMS][3];
+  or_restart_out ro[OR_MAX_RESTARTS];
+  int st[OR_MAX_RESTARTS];
   int geom[OR_MAX_RESTARTS], valid[OR_MAX_RESTARTS], aix[OR_MAX_RESTARTS], aiy[OR_MAX_RESTARTS];
   memset(res, 0, sizeof *res);
-  res->poses_scored = 0;
+  float(*Ub)[OR_MAX_ATOMS][3] = U; /* the calling thread's buffer, shared with the inner pool */
+  if (inner_threads > 1) {
+#pragma omp parallel for schedule(dynamic, 1) num_threads(inner_threads)
+    for (int r = 0; r < N; ++r) st[r] = dock_restart(L, k, cfg, r, Ub[r], tors, &ro[r]);
+  } else {
+    for (int r = 0; r < N; ++r)
+      if ((st[r] = dock_restart(L, k, cfg, r, Ub[r], tors, &ro[r])) != 0) {
+        for (int q = r + 1; q < N; ++q) st[q] = -1;
+        break;
+      }
+  }
   for (int r = 0; r < N; ++r) {
-    float R0s[9], t[3];
-    starting_pose(L, k, r, cfg->seed, R0s, t);
-    int ix = 0, iy = 0;
-    int as = align_pose(L, k, cfg, R0s, t, &ix, &iy, U[r]);
-    res->poses_scored += (int64_t)na * na;
-    aix[r] = ix;
-    aiy[r] = iy;
-    /* SPEC.md:257 optimize_pose */
-    int all_bumped = 0;
-    for (int f = 0; f < L->F; ++f) {
-      float cand[OR_MAX_ATOMS][3];
-      int best = 0, best_k = -1;
-      for (int a = 0; a < nt; ++a) {
-        if (apply_torsion(L, f, (const float(*)[3])U[r], a * cfg->torsion_step_deg, eps, cand) < 0 && nt > 1) {
-          res->status = 2; /* DegenerateAxis */
-          return 2;
-        }
-        res->poses_scored += 1;
-        if (bump_check(L, f, (const float(*)[3])cand, bd2, cfg->early_exit, &res->bump_checks, &res->bump_checks_r32,
-                       &res->bump_early_exits))
-          continue;
-        int sc = grid_score(k, (const float(*)[3])cand, L->A);
-        if (best_k < 0 || sc > best) {
-          best = sc;
-          best_k = a;
-        }
-      }
-      if (best_k > 0) {
-        apply_torsion(L, f, (const float(*)[3])U[r], best_k * cfg->torsion_step_deg, eps, cand);
-        memcpy(U[r], cand, sizeof(float) * 3 * L->A);
-      }
-      if (best_k < 0) ++all_bumped;
-      if (tors) tors[f * N + r] = best_k < 0 ? 255 : (uint8_t)best_k;
+    res->poses_scored += ro[r].poses_scored;
+    res->bump_checks += ro[r].bump_checks;
+    res->bump_checks_r32 += ro[r].bump_checks_r32;
+    res->bump_early_exits += ro[r].bump_early_exits;
+    if (st[r] == 2) { /* the sequential loop stops here: later restarts never ran */
+      res->status = 2;
+      if (tors)
+        for (int q = r + 1; q < N; ++q)
+          for (int f = 0; f < L->F; ++f) tors[f * N + q] = 0;
+      return 2;
     }
-    valid[r] = !(L->F >= 1 && all_bumped == L->F);
-    geom[r] = grid_score(k, (const float(*)[3])U[r], L->A);
+    geom[r] = ro[r].geom;
+    valid[r] = ro[r].valid;
+    aix[r] = ro[r].ax;
+    aiy[r] = ro[r].ay;
     if (rr) {
-      rr[r].align_score = as;
+      rr[r].align_score = ro[r].align_score;
       rr[r].final_geom = geom[r];
-      rr[r].ax = ix;
-      rr[r].ay = iy;
+      rr[r].ax = aix[r];
+      rr[r].ay = aiy[r];
       rr[r].valid = valid[r];
       rr[r].kept = 0;
     }
   }
+  float(*Uc)[OR_MAX_ATOMS][3] = Ub;
+#define U Uc
   /* SPEC.md:267 select_poses: valid poses by (geom desc, restart asc), greedy heavy-atom RMSD >= thr */
   int ord[OR_MAX_RESTARTS], nv = 0;
   for (int r = 0; r < N; ++r)
@@ -440,6 +484,12 @@ int or_dock_ligand(const or_lig *L, const or_pk *k, const or_config *cfg, or_res
     for (int i = 0; i < L->A; ++i)
       for (int c = 0; c < 3; ++c) best_xyz[3 * i + c] = fmaf(U[best_r][i][c], k->p->spacing, k->p->origin[c]);
   return 0;
+#undef U
+}
+
+int or_dock_ligand(const or_lig *L, const or_pk *k, const or_config *cfg, or_result *res, or_restart *rr,
+                   uint8_t *tors /* F*N: [f*N + r] */, float *best_xyz /* A*3 Å, may be NULL */) {
+  return dock_ligand_impl(L, k, cfg, res, rr, tors, best_xyz, 1);
 }
 
 /* P2: c0 = f32(f64 sequential mean), d = f32(p - c0) */
@@ -485,6 +535,32 @@ int or_dock_batch(int n, const int32_t *atom_off, const float *atom_xyz, const u
              frag_mask + (size_t)OR_MASK_WORDS * frag_off[i], ids + id_off[i], (size_t)(id_off[i + 1] - id_off[i]));
     or_dock_ligand(&L, k, cfg, res + i, rr ? rr + (size_t)i * N : NULL, tors ? tors + (size_t)frag_off[i] * N : NULL,
                    best_xyz ? best_xyz + 3 * (size_t)atom_off[i] : NULL);
+  }
+  pk_free(k);
+  free(k);
+  return 0;
+}
+
+/* The latency engine's CPU shape: ligands one after another, each ligand's
+ * restarts spread over an inner pool of `threads` workers; results identical to or_dock_batch. */
+int or_dock_batch_latency(int n, const int32_t *atom_off, const float *atom_xyz, const uint8_t *atom_type,
+                          const int32_t *frag_off, const int32_t *frag_axis, const uint32_t *frag_mask,
+                          const char *ids, const int64_t *id_off, const or_pocket *pocket, const or_config *cfg,
+                          int threads, or_result *res, or_restart *rr, uint8_t *tors, float *best_xyz) {
+  trig_init();
+  or_pk *k = (or_pk *)malloc(sizeof(or_pk));
+  if (pk_init(k, pocket)) {
+    free(k);
+    return -1;
+  }
+  const int N = cfg->restarts_n;
+  for (int i = 0; i < n; ++i) {
+    or_lig L;
+    lig_init(&L, atom_off[i + 1] - atom_off[i], atom_xyz + 3 * (size_t)atom_off[i], atom_type + atom_off[i],
+             frag_off[i + 1] - frag_off[i], frag_axis + 2 * (size_t)frag_off[i],
+             frag_mask + (size_t)OR_MASK_WORDS * frag_off[i], ids + id_off[i], (size_t)(id_off[i + 1] - id_off[i]));
+    dock_ligand_impl(&L, k, cfg, res + i, rr ? rr + (size_t)i * N : NULL, tors ? tors + (size_t)frag_off[i] * N : NULL,
+                     best_xyz ? best_xyz + 3 * (size_t)atom_off[i] : NULL, threads > 1 ? threads : 1);
   }
   pk_free(k);
   free(k);

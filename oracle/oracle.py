@@ -16,11 +16,11 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "liboracle.so")
-SRC = os.path.join(HERE, "dock_oracle.c")
+SRCS = [os.path.join(HERE, f) for f in ("dock_oracle.c", "gen_oracle.c", "Makefile")]
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(SO) or os.path.getmtime(SO) < os.path.getmtime(SRC):
+    if force or not os.path.exists(SO) or any(os.path.getmtime(SO) < os.path.getmtime(f) for f in SRCS):
         subprocess.check_call(["make", "-s", "-C", HERE])
     return SO
 
@@ -53,6 +53,8 @@ def lib():
         vp = C.c_void_p
         L.or_dock_batch.restype = C.c_int
         L.or_dock_batch.argtypes = [C.c_int] + [vp] * 10 + [C.c_int, vp, vp, vp, vp]
+        L.or_dock_batch_latency.restype = C.c_int
+        L.or_dock_batch_latency.argtypes = [C.c_int] + [vp] * 10 + [C.c_int, vp, vp, vp, vp]
         L.or_grid_score.restype = C.c_int
         L.or_grid_score.argtypes = [vp, vp, C.c_int]
         L.or_rescore.restype = C.c_int64
@@ -61,6 +63,16 @@ def lib():
         L.or_rot.argtypes = [C.c_int, C.c_int, vp]
         L.or_fnv1a64.restype = C.c_uint64
         L.or_fnv1a64.argtypes = [C.c_char_p, C.c_size_t]
+        i32, i64 = C.c_int32, C.c_int64
+        for name, args in (("go_generated_id", [i64, i64, C.c_char_p, C.c_size_t]),
+                           ("go_mixed_shapes", [i64, i64, i32, i32, i32, i32, vp]),
+                           ("go_generate_ligands", [i64, i64, i32] + [vp] * 7),
+                           ("go_pocket_atoms", [i64, i32, C.c_float, C.c_float, vp, vp]),
+                           ("go_build_pocket", [vp, i32, C.c_float, C.c_float, vp, vp, vp]),
+                           ("go_default_table", [i64, vp])):
+            fn = getattr(L, name)
+            fn.restype = C.c_int
+            fn.argtypes = args
         _lib = L
     return _lib
 
@@ -109,8 +121,11 @@ class OracleOutput:
     best_coords: np.ndarray
 
 
-def dock_batch(batch, pocket, table, cfg, seed: int = 0, threads: Optional[int] = None) -> OracleOutput:
-    """Sequential dock_ligand per ligand, OpenMP over ligands."""
+def dock_batch(batch, pocket, table, cfg, seed: int = 0, threads: Optional[int] = None,
+               latency: bool = False) -> OracleOutput:
+    """Sequential dock_ligand per ligand, OpenMP over ligands (the batched engine's CPU
+    shape); latency=True: ligands one after another, each ligand's restarts on an inner pool of
+    `threads` workers (the latency engine's CPU shape) — identical results."""
     n, N = batch.n, cfg.restarts_n
     ids, id_off = batch.id_bytes()
     idbuf = C.create_string_buffer(ids, max(len(ids), 1))
@@ -126,7 +141,8 @@ def dock_batch(batch, pocket, table, cfg, seed: int = 0, threads: Optional[int] 
     fo, fax, fm = c(batch.frag_off, np.int32), c(batch.frag_axis, np.int32), c(batch.frag_mask, np.uint32)
     if fax.size == 0:
         fax, fm = np.zeros((1, 2), np.int32), np.zeros((1, 5), np.uint32)
-    rc = lib().or_dock_batch(n, _p(ao), _p(xyz), _p(typ), _p(fo), _p(fax), _p(fm), C.cast(idbuf, C.c_void_p),
+    fn = lib().or_dock_batch_latency if latency else lib().or_dock_batch
+    rc = fn(n, _p(ao), _p(xyz), _p(typ), _p(fo), _p(fax), _p(fm), C.cast(idbuf, C.c_void_p),
                              _p(id_off), C.byref(pk.c), C.byref(ccfg), int(threads or os.cpu_count() or 1),
                              _p(res), _p(rr), _p(rt), _p(bx))
     if rc != 0:
@@ -156,3 +172,90 @@ def rot(axis: int, deg: int) -> np.ndarray:
 def fnv1a64(s: str) -> int:
     b = s.encode()
     return int(lib().or_fnv1a64(b, len(b)))
+
+
+# ---- oracle-side input makers (gen_oracle.c): the reference arm of bench.py builds its inputs with
+# these so its process never loads the product library ------------------------------------------
+class OracleBatch:
+    """The packed CSR ligand arrays dock_batch consumes (same field names as the product's LigandBatch)."""
+
+    def __init__(self, atom_off, atom_xyz, atom_type, frag_off, frag_axis, frag_mask, ids):
+        self.atom_off, self.atom_xyz, self.atom_type = atom_off, atom_xyz, atom_type
+        self.frag_off, self.frag_axis, self.frag_mask, self.ids = frag_off, frag_axis, frag_mask, ids
+
+    @property
+    def n(self) -> int:
+        return len(self.atom_off) - 1
+
+    def id_bytes(self):
+        raw = [s.encode() for s in self.ids]
+        off = np.zeros(len(raw) + 1, np.int64)
+        off[1:] = np.cumsum([len(b) for b in raw]) if raw else []
+        return b"".join(raw), off
+
+
+def generated_id(seed: int, index: int) -> str:
+    buf = C.create_string_buffer(64)
+    n = lib().go_generated_id(int(seed), int(index), buf, 64)
+    return buf.raw[:n].decode()
+
+
+def mixed_shapes(count: int, seed: int, first_index: int = 0, heavy_range=(8, 40), frag_max: int = 20) -> np.ndarray:
+    out = np.zeros((count, 2), np.int32)
+    if lib().go_mixed_shapes(int(seed), int(first_index), int(count), int(heavy_range[0]), int(heavy_range[1]),
+                             int(frag_max), _p(out)) != 0:
+        raise ValueError("bad mixed-shape arguments")
+    return out
+
+
+def generate_batch(shapes: np.ndarray, seed: int, first_index: int = 0) -> OracleBatch:
+    """SPEC.md:443 generate_dataset (oracle restatement) for ligands first_index + i of these shapes."""
+    shapes = np.ascontiguousarray(np.asarray(shapes, np.int32).reshape(-1, 2))
+    n = len(shapes)
+    ao, fo = np.zeros(n + 1, np.int32), np.zeros(n + 1, np.int32)
+    L = lib()
+    if L.go_generate_ligands(int(seed), int(first_index), n, _p(shapes), _p(ao), _p(fo), None, None, None, None):
+        raise ValueError("InfeasibleShape")
+    na, nf = int(ao[-1]), int(fo[-1])
+    xyz, typ = np.zeros((max(na, 1), 3), np.float32), np.zeros(max(na, 1), np.uint8)
+    axis, mask = np.zeros((max(nf, 1), 2), np.int32), np.zeros((max(nf, 1), 5), np.uint32)
+    L.go_generate_ligands(int(seed), int(first_index), n, _p(shapes), _p(ao), _p(fo), _p(xyz), _p(typ), _p(axis),
+                          _p(mask))
+    ids = [generated_id(seed, first_index + i) for i in range(n)]
+    return OracleBatch(ao, xyz[:na], typ[:na], fo, axis[:nf], mask[:nf], ids)
+
+
+def generate_mixed_batch(count: int, seed: int, first_index: int = 0, heavy_range=(8, 40),
+                         frag_max: int = 20) -> OracleBatch:
+    return generate_batch(mixed_shapes(count, seed, first_index, heavy_range, frag_max), seed, first_index)
+
+
+class OracleTable:
+    """InteractionTable as the oracle reads it: .table (16x16) and .bins."""
+
+    def __init__(self, table, bins=((2.0, 0.5), (4.0, 1.0), (6.0, 0.5), (8.0, 0.25))):
+        self.table, self.bins = table, tuple(bins)
+
+
+def default_table(seed: int = 11) -> OracleTable:
+    t = np.zeros(256, np.float32)
+    lib().go_default_table(int(seed), _p(t))
+    return OracleTable(t.reshape(16, 16))
+
+
+def synthetic_pocket(spacing: float = 0.5, n_atoms: int = 200, seed: int = 7, rmin: float = 7.0, rmax: float = 10.0,
+                     padding: float = 4.0):
+    """The shared synthetic pocket built by the oracle restatement of build_pocket; a
+    plain model.Pocket (pure Python, no product library)."""
+    from paper_2209_05069_b200 import model
+    xyz, typ = np.zeros((n_atoms, 3), np.float32), np.zeros(n_atoms, np.uint8)
+    L = lib()
+    L.go_pocket_atoms(int(seed), int(n_atoms), float(rmin), float(rmax), _p(xyz), _p(typ))
+    origin, dims = (C.c_float * 3)(), (C.c_int32 * 3)()
+    if L.go_build_pocket(_p(xyz), n_atoms, float(spacing), float(padding), origin, dims, None):
+        raise ValueError("EmptyPocket")
+    vals = np.zeros(int(dims[0]) * int(dims[1]) * int(dims[2]), np.int32)
+    L.go_build_pocket(_p(xyz), n_atoms, float(spacing), float(padding), origin, dims, _p(vals))
+    atoms = tuple(model.Atom.of(*xyz[i], int(typ[i])) for i in range(n_atoms))
+    return model.Pocket(tuple(float(o) for o in origin), float(np.float32(spacing)), tuple(int(d) for d in dims), vals,
+                        atoms)

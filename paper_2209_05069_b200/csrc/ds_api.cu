@@ -85,6 +85,9 @@ struct ds_ctx {
   std::vector<cudaEvent_t> pev;     // pipeline events (4 per chunk)
   cudaEvent_t ev[6] = {};
   int64_t allocs = 0;
+  // generation of the per-array batch buffers: bumped by every call that may overwrite or
+  // reallocate them; a resident batch handle is valid only while its stamp is current
+  uint64_t gen = 1;
   float2 *trig = nullptr;       // 360 (cos, sin)
   // batch-sized device buffers
   DevBuf b_atom_off, b_atoms, b_frag_off, b_frags, b_idh, b_order_a, b_order_o, b_keys, b_res, b_rrec, b_rtors,
@@ -146,7 +149,8 @@ struct ds_ctx {
 };
 
 struct ds_pocket {
-  ds_ctx *ctx = nullptr;
+  ds_ctx *ctx = nullptr;        // creating context (not dereferenced after creation)
+  int device = 0;               // its device: the pocket may outlive the context
   PocketView view{};
   uint8_t *d_grid = nullptr;
   uint8_t *d_lut = nullptr;
@@ -157,6 +161,7 @@ struct ds_pocket {
 
 struct ds_dev_batch {
   ds_ctx *ctx = nullptr;
+  uint64_t gen = 0;             // ds_ctx::gen when the batch was placed in the ctx's buffers
   int L = 0, n_atoms = 0, n_frags = 0;
   int N = 0;
   std::vector<int> atom_off, frag_off;  // host copies for downloads
@@ -297,6 +302,7 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
   DS_CUDA(enter_device(c->device));
   ds_pocket *p = new ds_pocket();
   p->ctx = c;
+  p->device = c->device;
   PocketView &v = p->view;
   v.g.nx = d->dims[0];
   v.g.ny = d->dims[1];
@@ -430,7 +436,7 @@ int ds_pocket_create(ds_ctx *c, const ds_pocket_desc *d, ds_pocket **out) {
 
 void ds_pocket_destroy(ds_pocket *p) {
   if (!p) return;
-  if (p->ctx) cudaSetDevice(p->ctx->device);
+  cudaSetDevice(p->device);
   if (p->d_grid) cudaFree(p->d_grid);
   if (p->d_patoms) cudaFree(p->d_patoms);
   if (p->d_wfx) cudaFree(p->d_wfx);
@@ -572,6 +578,7 @@ void io_from_buffers(ds_ctx *c) {
 
 // batch-sized device buffers (both families); grows geometrically, never shrinks
 int reserve_buffers(ds_ctx *c, int L, int NA, int NF, int N) {
+  ++c->gen;  // every caller overwrites (or may reallocate) the per-array buffers
   int rc;
   if ((rc = c->ensure(c->b_atom_off, sizeof(int) * (L + 1))) || (rc = c->ensure(c->b_atoms, 16ull * std::max(NA, 1))) ||
       (rc = c->ensure(c->b_frag_off, sizeof(int) * (L + 1))) || (rc = c->ensure(c->b_frags, 32ull * std::max(NF, 1))) ||
@@ -1137,14 +1144,23 @@ int ds_batch_upload(ds_ctx *c, const ds_batch_desc *b, ds_dev_batch **out) {
     delete d;
     return rc;
   }
+  d->gen = c->gen;
   DS_CUDA(cudaStreamSynchronize(c->stream));
   *out = d;
   return DS_OK;
 }
 
+static int stale(const ds_ctx *c, const ds_dev_batch *d) {
+  return fail(DS_ERR_INVALID_ARG,
+              "stale resident batch: ctx %p reused its buffers (generation %llu, batch %llu) for a later "
+              "upload / generation / ds_dock / op call", (const void *)c, (unsigned long long)c->gen,
+              (unsigned long long)d->gen);
+}
+
 int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_dock_config *cfg, int family,
                      ds_stats *st) {
   if (!c || !pk || !d || d->ctx != c) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  if (d->gen != c->gen) return stale(c, d);
   DockParams dp;
   int rc;
   if ((rc = check_config(cfg, pk, &dp))) return rc;
@@ -1169,7 +1185,8 @@ int ds_dock_resident(ds_ctx *c, const ds_pocket *pk, ds_dev_batch *d, const ds_d
 }
 
 int ds_batch_download(ds_ctx *c, ds_dev_batch *d, const ds_outputs *out) {
-  if (!c || !d || !out) return fail(DS_ERR_INVALID_ARG, "NULL argument");
+  if (!c || !d || !out || d->ctx != c) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  if (d->gen != c->gen) return stale(c, d);
   if (!d->docked) return fail(DS_ERR_INVALID_ARG, "batch has not been docked");
   if (d->L == 0) return DS_OK;
   int rc;
@@ -1220,6 +1237,7 @@ int ds_generate_resident(ds_ctx *c, int64_t seed, int64_t first_index, int32_t c
   if (device_ms) cudaEventElapsedTime(device_ms, c->ev[1], c->ev[2]);
   ds_dev_batch *d = new ds_dev_batch();
   d->ctx = c;
+  d->gen = c->gen;
   d->L = L;
   d->atom_off.assign(ao.begin(), ao.end());
   d->frag_off.assign(fo.begin(), fo.end());
@@ -1231,6 +1249,7 @@ int ds_generate_resident(ds_ctx *c, int64_t seed, int64_t first_index, int32_t c
 
 int ds_batch_read_inputs(ds_ctx *c, const ds_dev_batch *d, float *atom_xyzt, uint32_t *frag_desc, uint64_t *id_hash) {
   if (!c || !d || d->ctx != c) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  if (d->gen != c->gen) return stale(c, d);
   DS_CUDA(enter_device(c->device));
   if (atom_xyzt && d->n_atoms)
     DS_CUDA(cudaMemcpyAsync(atom_xyzt, c->b_atoms.p, 16ull * d->n_atoms, cudaMemcpyDeviceToHost, c->stream));
@@ -1284,6 +1303,7 @@ int ds_op_grid_score(ds_ctx *c, const ds_pocket *pk, const float *coords, int n_
   if (!n_poses) return DS_OK;
   DS_CUDA(enter_device(c->device));
   const size_t nc = 12ull * n_atoms * n_poses;
+  ++c->gen;  // overwrites the per-array buffers of any resident batch
   int rc;
   if ((rc = c->ensure(c->b_coords, std::max<size_t>(nc, 16))) || (rc = c->ensure(c->b_keys, 4ull * n_poses))) return rc;
   DS_CUDA(cudaMemcpyAsync(c->b_coords.p, coords, nc, cudaMemcpyHostToDevice, c->stream));
@@ -1301,6 +1321,7 @@ int ds_op_rescore(ds_ctx *c, const ds_pocket *pk, const float *coords, const uin
   if (!n_poses) return DS_OK;
   DS_CUDA(enter_device(c->device));
   const size_t nc = 12ull * n_atoms * n_poses;
+  ++c->gen;
   int rc;
   if ((rc = c->ensure(c->b_coords, std::max<size_t>(nc, 16))) || (rc = c->ensure(c->b_rtors, std::max(n_atoms, 1))) ||
       (rc = c->ensure(c->b_res, 8ull * n_poses)))

@@ -46,6 +46,7 @@ struct LatSmem {
   unsigned cn[DS_MAX_ATOMS];           // their count (> kLatCand: scan all of C')
   int base[2];                  // grid score of the non-moving atoms, by fragment parity
   int ascore[32];
+  int bcode[32];                // early exit: min (moving rank * nC + C' rank) over bumping pairs (P14)
   unsigned abump;
   unsigned key;
   int degen, degen_f, is_last;
@@ -118,6 +119,27 @@ __device__ __forceinline__ float lat_min_d2(const LatSmem &S, int m, int nC, flo
     }
   }
   return mind;
+}
+
+// the bumping pair the sequential scan of P9 meets first for moving atom m at q (cold path): the
+// smallest C' atom within the bump distance (candidates are unordered; C' is ascending)
+__device__ __noinline__ int lat_first_bump(const LatSmem &S, int m, int nC, float3 q, float bd2) {
+  const unsigned cnt = S.cn[m];
+  int best = 0x7FFFFFFF;
+  if (cnt <= (unsigned)kLatCand) {
+    for (unsigned t = 0; t < cnt; ++t) {
+      const int j = S.cl[m][t];
+      const float4 y = S.u[j];
+      if (j < best && dist2(q.x, q.y, q.z, y.x, y.y, y.z) < bd2) best = j;
+    }
+    return best;
+  }
+  for (int c = 0; c < nC; ++c) {
+    const int j = S.clist[c];
+    const float4 y = S.u[j];
+    if (dist2(q.x, q.y, q.z, y.x, y.y, y.z) < bd2) return j;
+  }
+  return best;
 }
 
 template <bool kSmemGrid>
@@ -274,7 +296,10 @@ __global__ void __launch_bounds__(kLatThreads, 1)
       part = (int)__reduce_add_sync(kFull, (unsigned)part);
       if (lane == 0 && part) atomicAdd(&S.base[f & 1], part);
     }
-    if (tid < 32) S.ascore[tid] = 0;
+    if (tid < 32) {
+      S.ascore[tid] = 0;
+      S.bcode[tid] = 0x7FFFFFFF;
+    }
     if (tid == 0) {
       S.abump = 0u;
       S.base[(f + 1) & 1] = 0;  // last read in fragment f - 1's (E)
@@ -311,11 +336,13 @@ __global__ void __launch_bounds__(kLatThreads, 1)
       const int nA = min(32, dp.n_t - k0);
       if (k0 > 0) {
         __syncthreads();
-        if (tid < 32) S.ascore[tid] = 0;
+        if (tid < 32) {
+          S.ascore[tid] = 0;
+          S.bcode[tid] = 0x7FFFFFFF;
+        }
         if (tid == 0) S.abump = 0u;
         __syncthreads();
       }
-      unsigned my_pairs = 0;
       // thread = (angle a, group mg), exact reciprocal division (no integer divide on the chain)
       const int G = small_div(kLatThreads, nA);
       const int mg = small_div(tid, nA), a = tid - mg * nA;
@@ -330,8 +357,11 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         bool hit_any = false;
         // two moving atoms per step (independent chains: twice the loads in flight); a bump on
         // either marks the angle, whose partial score is then never read
+        // early exit: a thread stops once its next atom lies beyond the first bump found so far for
+        // its angle; every atom up to the sequential scan's first bump is then tested, so the pair
+        // count derived from the minimum code is exact and independent of thread timing (P14)
         for (int m = mg; m < nM; m += 2 * G) {
-          if (dp.early_exit && (hit_any || ((*(volatile unsigned *)&S.abump >> a) & 1u))) break;
+          if (dp.early_exit && (hit_any || m * nC > *(volatile int *)&S.bcode[a])) break;
           const bool two = m + G < nM;
           const int m1 = two ? m + G : m;
           const float4 p0 = S.u[S.mlist[m]], p1 = S.u[S.mlist[m1]];
@@ -339,20 +369,41 @@ __global__ void __launch_bounds__(kLatThreads, 1)
           const float3 q1 = kang == 0 ? make_float3(p1.x, p1.y, p1.z) : torsion_apply(R, a3, p1.x, p1.y, p1.z);
           const int gv0 = lat_grid_val<kSmemGrid>(grid, node_index(g, q0.x, q0.y, q0.z));
           const int gv1 = lat_grid_val<kSmemGrid>(grid, node_index(g, q1.x, q1.y, q1.z));
-          my_pairs += (unsigned)(two ? 2 * nC : nC);  // pairs resolved (P14)
           const float d0 = lat_min_d2(S, m, nC, q0), d1 = lat_min_d2(S, m1, nC, q1);
           if (d0 < dp.bd2 || d1 < dp.bd2) {
             hit_any = true;
             atomicOr(&S.abump, 1u << a);
+            if (dp.early_exit) {
+              const bool b0 = d0 < dp.bd2;
+              const int mb = b0 ? m : m1;
+              const int jb = lat_first_bump(S, mb, nC, b0 ? q0 : q1, dp.bd2);
+              // C' rank of jb: atoms below it minus the moving and axis atoms among them
+              int below = 0;
+              for (int w = 0; w < 5; ++w) {
+                const unsigned word = w == 0 ? fa.x : w == 1 ? fa.y : w == 2 ? fa.z : w == 3 ? fa.w : fb.x;
+                const int lo = 32 * w;
+                if (jb >= lo + 32) below += __popc(word);
+                else if (jb > lo) below += __popc(word & ((1u << (jb - lo)) - 1u));
+              }
+              atomicMin(&S.bcode[a], mb * nC + (jb - below - (ab < jb) - (ae < jb)));
+            }
           } else {
             part += two ? gv0 + gv1 : gv0;
           }
         }
         if (part) atomicAdd(&S.ascore[a], part);
       }
-      my_pairs = __reduce_add_sync(kFull, my_pairs);
-      if (lane == 0 && my_pairs) atomicAdd(&S.pairs, my_pairs);
       __syncthreads();
+      // pairs the sequential scan evaluates (P14): up to its first bump, or all nM * nC
+      if (warp == 0) {
+        unsigned np = 0;
+        if (lane < nA) {
+          const int bc = S.bcode[lane];
+          np = (dp.early_exit && bc != 0x7FFFFFFF) ? (unsigned)bc + 1u : (unsigned)(nM * nC);
+        }
+        np = __reduce_add_sync(kFull, np);
+        if (lane == 0) S.pairs += np;
+      }
       // ---- (E) best clean angle, computed by every warp (no extra barrier) ----
       const unsigned abump = S.abump;
       unsigned kk = 0;

@@ -50,6 +50,8 @@ struct TorWarpSmem {
   uint8_t clist[kMaxA];     // complement atom indices, ascending
   uint16_t ovf[kOvf];       // candidates beyond kInline: moving slot << 8 | atom index
   int n_ovf;                // entries appended (> kOvf: the list overflowed, scan C')
+  int bcode[32];            // early exit: per angle of the block, min over bumping pairs of
+                            // (moving rank * nC + C' rank) — the sequential scan's stop point (P14)
 };
 
 // Per-warp shared scratch of the select/rescore kernel.
@@ -221,6 +223,51 @@ __device__ __forceinline__ bool bump_hit(const TorWarpSmem &S, unsigned info, fl
     }
   }
   return mind < bd2;
+}
+
+// The bumping pair the sequential scan of P9 meets first for moving atom m at q (cold path, called
+// only after bump_hit said yes): the smallest C' atom within the bump distance.  Inline candidates
+// are in ascending C' order and precede every overflow entry; the overflow list is unordered.
+__device__ __noinline__ int first_bump_atom(const TorWarpSmem &S, unsigned info, float3 q, int m, int n_ovf, int nCf,
+                                            float bd2) {
+  const unsigned cnt = info & 0xFFu;
+  const unsigned nin = cnt < (unsigned)kInline ? cnt : (unsigned)kInline;
+  for (unsigned t = 0; t < nin; ++t) {
+    const unsigned j = (info >> (8 + 8 * t)) & 0xFFu;
+    const float4 y = S.u[j];
+    if (dist2(q.x, q.y, q.z, y.x, y.y, y.z) < bd2) return (int)j;
+  }
+  int best = 0x7FFFFFFF;
+  if (n_ovf <= kOvf) {
+    for (int t = 0; t < n_ovf; ++t) {
+      const unsigned e = S.ovf[t];
+      if ((int)(e >> 8) != m) continue;
+      const int j = (int)(e & 0xFFu);
+      const float4 y = S.u[j];
+      if (j < best && dist2(q.x, q.y, q.z, y.x, y.y, y.z) < bd2) best = j;
+    }
+  } else {
+    for (int c = 0; c < nCf; ++c) {  // ascending: the first hit is the smallest
+      const int j = S.clist[c];
+      const float4 y = S.u[j];
+      if (dist2(q.x, q.y, q.z, y.x, y.y, y.z) < bd2) return j;
+    }
+  }
+  return best;
+}
+
+// rank of atom j (not moving, not an axis atom) in the fragment's complement C' (ascending)
+__device__ __forceinline__ int complement_rank(const uint4 *frag, int j, int ab, int ae) {
+  const uint4 fa = __ldg(frag), fb = __ldg(frag + 1);
+  const unsigned w[5] = {fa.x, fa.y, fa.z, fa.w, fb.x};
+  int below = 0;
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    const int lo = s * 32;
+    if (j >= lo + 32) below += __popc(w[s]);
+    else if (j > lo) below += __popc(w[s] & ((1u << (j - lo)) - 1u));
+  }
+  return j - below - (ab < j) - (ae < j);
 }
 
 // A DegenerateAxis stops the ligand where the sequential oracle stops: restart records from the
@@ -423,6 +470,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           if (ok) reinterpret_cast<unsigned *>(S.mip)[m] = cnt | inl;  // cnt <= nCf < 256
         }
         unsigned best_key = 0;  // (score + 32768) << 16 | (65535 - angle); 0 = no clean angle
+        S.bcode[lane] = 0x7FFFFFFF;
         __syncwarp();
         const int n_ovf = S.n_ovf;
         // ---- all angles at once: lane = (angle a, moving-atom group gi); the lane keeps its angle's
@@ -457,7 +505,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
             ar = a3;
           }
           bool bumped = false;
-          int part = 0, nact = 0;
+          int part = 0;
           // two moving atoms per lane and round (slots m0 + 2 gi and m0 + 2 gi + 1): twice the
           // independent work (two grid loads in flight) for the same loop and retirement overhead,
           // and the two rotations run as packed f32x2 (FADD2 / FFMA2, each half the scalar recipe)
@@ -496,8 +544,12 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
               const bool h1 = bump_hit(S, info.x, q1, m1, n_ovf, nCf, dp.bd2);
               const bool h2 = act2 && bump_hit(S, info.y, q2, m2, n_ovf, nCf, dp.bd2);
               part += (h1 ? 0 : gv1) + (act2 && !h2 ? gv2 : 0);
-              nact += act2 ? 2 : 1;
               hit = h1 || h2;
+              if (hit && dp.early_exit) {  // where the sequential scan stops for this angle (P14)
+                const int mb = h1 ? m1 : m2;
+                const int jb = first_bump_atom(S, h1 ? info.x : info.y, h1 ? q1 : q2, mb, n_ovf, nCf, dp.bd2);
+                atomicMin(&S.bcode[a], mb * nC + complement_rank(bt.frags + 2 * (size_t)(f0 + f), jb, ab, ae));
+              }
             }
             if (dp.early_exit) {  // OR the hits of the G lanes that share an angle
               // every lane must reach the ballot: never put it behind a short-circuit operator
@@ -507,7 +559,19 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
               bumped = bumped || hit;
             }
           }
-          pairs_total += (unsigned)warp_sum(nact) * (unsigned)nC;  // pairs resolved (P14)
+          __syncwarp();
+          // pairs the sequential scan evaluates (P14): up to and including its first bump, or all
+          // nM * nC; without early exit every pair
+          {
+            unsigned np = 0;
+            if (gi == 0 && lane_ok) {
+              const int bc = S.bcode[a];
+              np = (dp.early_exit && bc != 0x7FFFFFFF) ? (unsigned)bc + 1u : (unsigned)(nM * nC);
+            }
+            pairs_total += (unsigned)warp_sum((int)np);
+          }
+          __syncwarp();
+          S.bcode[lane] = 0x7FFFFFFF;
           // combine the G partial scores of an angle on its group-0 lane
           int sum = part;
           for (int t = 1; t < G; ++t) {

@@ -559,6 +559,12 @@ class Context:
                           rr[:n] if rr is not None else None, rt[:nf] if rt is not None else None, st)
 
     def close(self):
+        # pockets cached on this context (docking.PocketCache) are released first, deterministically,
+        # instead of being left to the cyclic GC in arbitrary order
+        cache = self.__dict__.pop("_pocket_cache", None)
+        if cache:
+            for hit in cache.values():
+                hit[2].close()
         if getattr(self, "handle", None):
             lib().ds_destroy(self.handle)
             self.handle = None

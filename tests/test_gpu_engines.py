@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 def _key(r):
     p = r.best_pose
     return (r.ligand_id, p.geometric_score, p.chem_fx, p.restart_index, p.align_indices, p.torsion_indices,
-            p.coordinates.tobytes(), r.counters.poses_scored, r.counters.bump_early_exits)
+            p.coordinates.tobytes(), r.counters.poses_scored, r.counters.bump_checks, r.counters.bump_early_exits)
 
 
 @pytest.fixture(scope="module")
