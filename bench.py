@@ -1,26 +1,40 @@
 #!/usr/bin/env python
-"""Benchmark of the docking hot path (BASELINE.json metric: ligands/sec docked, device-timed,
-at 1/2/4/8 B200, and the fraction of the instruction roofline).
+"""Benchmark of the docking hot path (BASELINE.json metric: ligands/sec docked, device-timed, at
+1/2/4/8 B200, and the fraction of the instruction roofline).
 
-Workload (per rank, weak scaling): BASELINE config 3 — mixed synthetic ligands (heavy atoms
-U{8..40}, rotatable bonds U{0..min(20, heavy-2)}, seed 3, each rank its own contiguous shard of
-the global index space as in config 5) docked against the shared synthetic pocket (P=200, 57^3
-class grid, spacing 0.5 Å) with the default DockConfig, batched kernel family.  A "step" docks
-the rank's whole shard: alignment kernel + optimisation/select/rescore kernel.
+Default workload (per rank, weak scaling): BASELINE config 3 — mixed synthetic ligands (heavy atoms
+U{8..40}, rotatable bonds U{0..min(20, heavy-2)}, seed 3, each rank its own contiguous shard of the
+global index space) docked against the shared synthetic pocket (P=200, spacing 0.5 Å) with the
+default DockConfig, batched kernel family.  A "step" docks the rank's whole shard: the alignment,
+torsion and select/rescore kernels.
 
-  value  = total ligands / step time, inputs resident in HBM (kernel-only, CUDA events on the
-           library's stream, max over ranks)
-  e2e    = the same through the public C ABI call ds_dock with host buffers (pinned staging,
-           H2D, kernels, D2H of the result records + best poses), host wall-clock, max over ranks
+  value    = total ligands / step time, inputs resident in HBM (kernel-only, CUDA events on the
+             library's stream, max over ranks)
+  e2e      = the same through the public C ABI call ds_dock with pinned host buffers (H2D, kernels,
+             D2H of the result records + best poses + best torsions), host wall clock, max over ranks
+  e2e_api  = the reference-facing entry point engines.batched_engine.run on a LigandBatch stream
+             (validation, bucketizer, dispatch, results), host wall clock
+  roofline = the dominant kernel on the instruction-issue roofline: ncu-counted warp-instructions
+             per ligand (committed capture of this build, profiles/) x ligands / live kernel time /
+             (SMs x 4 x f_max); parity = the CPU oracle vs the GPU on the first --cpu-sample ligands
+  config2 / config4 = BASELINE configs 2 and 4 (latency vs batched family), with their own clocks
+
+`--config 5`: BASELINE config 5 — a --total ligand screen (default 10M) split over the ranks
+(strong scaling), device-side ingest, with the result records and best torsion indices gathered
+to rank 0 inside the e2e timing.
 
 `--impl reference` times the CPU oracle (the reference's algorithm restated in C, all host
-threads) on a bounded sample of the same workload.
+threads) on a bounded sample of the same workload; its inputs come from the oracle's own
+generators, so that process never loads the product library.
 """
 from __future__ import annotations
 
 import argparse
+import glob
+import hashlib
 import json
 import os
+import re
 import sys
 import threading
 import time
@@ -29,9 +43,13 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+LIB = os.path.join(ROOT, "paper_2209_05069_b200", "libdockscreen.so")
 
 # algorithmic thread-instruction costs per unit
 C_ALIGN, C_ROT, C_PAIR, C_SCORE, C_RESC = 24, 20, 8, 14, 20
+KERNELS = ("k_align_batched", "k_torsion_batched", "k_select_batched")
+PARITY_FIELDS = ("status", "geom_score", "chem_fx", "best_restart", "best_ax", "best_ay", "n_kept", "poses_scored",
+                 "bump_checks", "bump_early_exits")
 
 
 def parse():
@@ -40,23 +58,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ligands", type=int, default=200_000, help="ligands per rank per step")
+    ap.add_argument("--config", type=int, default=3, choices=[3, 5])
+    ap.add_argument("--ligands", type=int, default=200_000, help="config 3: ligands per rank per step")
+    ap.add_argument("--total", type=int, default=10_000_000, help="config 5: ligands in the whole screen")
     ap.add_argument("--seed", type=int, default=3)
-    ap.add_argument("--cpu-sample", type=int, default=1024, help="ligands in the CPU-baseline sample")
+    ap.add_argument("--cpu-sample", type=int, default=10_000, help="ligands in the CPU-baseline / parity sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config-2 / config-4 / API legs")
     return ap.parse_args()
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
 class ClockSampler:
-    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+    """Samples SM clocks and throttle reasons with NVML during a timed region."""
 
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -84,7 +102,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.05)
+            time.sleep(0.02)
 
     def __enter__(self):
         if self.nv:
@@ -102,107 +120,354 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def work_model(batch, res, cfg):
-    """Algorithmic warp-instructions per ligand from the device's own counters."""
-    A = np.diff(batch.atom_off).astype(np.float64)
-    F = np.diff(batch.frag_off).astype(np.float64)
-    N = cfg.restarts_n
-    n_rot = (360 // cfg.alignment_step_deg) ** 2
-    u_align = N * n_rot * A
-    # torsion rotations: sum over fragments of |M| x (n_t - 1) x N
-    pop = np.array([bin(int(w)).count("1") for w in batch.frag_mask.reshape(-1)], np.float64).reshape(-1, 5).sum(1)
-    msum = np.add.reduceat(pop, batch.frag_off[:-1]) if len(pop) else np.zeros(batch.n)
-    msum = np.where(F > 0, msum, 0.0)
-    n_t = 360 // cfg.torsion_step_deg
-    u_rot = N * (n_t - 1) * msum
-    u_pair = res["bump_checks"].astype(np.float64)
-    u_score = N * n_t * msum  # upper bound: clean angles score only the moving atoms (base hoisted)
-    u_resc = res["n_kept"].astype(np.float64) * A * 200.0
-    w_align = C_ALIGN * u_align / 32.0
-    w_tors = (C_ROT * u_rot + C_PAIR * u_pair + C_SCORE * u_score) / 32.0
-    w_sel = C_RESC * u_resc / 32.0
-    return {"k_align_batched": float(w_align.sum()), "k_torsion_batched": float(w_tors.sum()),
-            "k_select_batched": float(w_sel.sum())}
+def lib_sha16() -> str:
+    try:
+        with open(LIB, "rb") as fh:
+            return hashlib.sha256(fh.read()).hexdigest()[:16]
+    except OSError:
+        return "missing"
 
 
-def ncu_calibration():
-    """Per-ligand executed warp-instructions / DRAM bytes of each kernel from the newest committed
-    ncu summary (tools/ncu_summary.py --ligands) of this workload generator."""
-    import glob
-    import re
-
-    def version(path):  # (round directory, vNN): file mtimes do not survive the copy to the GPU box
+def ncu_calibration(sha: str):
+    """Per-ligand executed warp-instructions, DRAM bytes and L2 hit rate of each kernel from the
+    committed ncu summaries (tools/ncu_summary.py --ligands) of this workload generator: the newest
+    capture of THIS library build (lib_sha16), else the newest one (flagged as another build)."""
+    def version(path):  # (round directory, vNN): mtimes do not survive the copy to the GPU box
         m = re.search(r"_v(\d+)\.json$", path)
         return (os.path.basename(os.path.dirname(path)), int(m.group(1)) if m else -1)
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_kernels_*.json")), key=version)
-    for path in reversed(files):
+    docs = []
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_kernels_*.json")), key=version):
         try:
             with open(path) as fh:
                 doc = json.load(fh)
         except Exception:
             continue
-        nlig = doc.get("ligands")
-        if not nlig:
-            continue
-        out = {"source": os.path.relpath(path, ROOT)}
-        for k in doc.get("kernels", []):
-            name = k["kernel"].split("(")[0].split("<")[0].replace("void ", "").strip().split("::")[-1]
-            out[name] = {"inst_per_ligand": k.get("warp_inst_executed", 0) / nlig,
-                         "dram_bytes_per_ligand": (k.get("dram_read", 0) + k.get("dram_write", 0)) / nlig,
-                         "issue_active_pct": k.get("issue_active_pct"),
-                         "pipe_fmaheavy_pct": k.get("pipe_fmaheavy_pct"),
-                         "smem_wavefront_pct": k.get("smem_wavefront_pct")}
-        return out
-    return {}
+        if doc.get("ligands"):
+            docs.append((path, doc))
+    if not docs:
+        return {}
+    match = [d for d in docs if d[1].get("lib_sha16") == sha]
+    path, doc = (match or docs)[-1]
+    nlig = doc["ligands"]
+    out = {"source": os.path.relpath(path, ROOT), "matches_build": bool(match), "lib_sha16": doc.get("lib_sha16")}
+    for k in doc.get("kernels", []):
+        name = k["kernel"].split("(")[0].split("<")[0].replace("void ", "").strip().split("::")[-1]
+        out[name] = {"inst_per_ligand": k.get("warp_inst_executed", 0) / nlig,
+                     "dram_bytes_per_ligand": (k.get("dram_read", 0) + k.get("dram_write", 0)) / nlig,
+                     "l2_hit_pct": k.get("l2_hit_pct"), "issue_active_pct": k.get("issue_active_pct"),
+                     "pipe_fmaheavy_pct": k.get("pipe_fmaheavy_pct"), "smem_wavefront_pct": k.get("smem_wavefront_pct"),
+                     "active_threads_per_inst": k.get("active_threads_per_inst")}
+    return out
 
 
 def measured_peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(p) as fh:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             return json.load(fh)
     except Exception:
         return {}
 
 
+def work_model(batch, res, cfg):
+    """§8d algorithmic warp-instructions per kernel (a reference cost model, not the roofline)."""
+    A = np.diff(batch.atom_off).astype(np.float64)
+    F = np.diff(batch.frag_off).astype(np.float64)
+    N = cfg.restarts_n
+    u_align = N * (360 // cfg.alignment_step_deg) ** 2 * A
+    pop = np.unpackbits(np.ascontiguousarray(batch.frag_mask).view(np.uint8), axis=None).reshape(-1, 160).sum(1) \
+        if len(batch.frag_mask) else np.zeros(0)
+    msum = np.add.reduceat(pop.astype(np.float64), batch.frag_off[:-1]) if len(pop) else np.zeros(batch.n)
+    msum = np.where(F > 0, msum, 0.0)
+    n_t = 360 // cfg.torsion_step_deg
+    u_rot, u_score = N * (n_t - 1) * msum, N * n_t * msum
+    u_pair = res["bump_checks"].astype(np.float64)
+    u_resc = res["n_kept"].astype(np.float64) * A * 200.0
+    return {"k_align_batched": float((C_ALIGN * u_align / 32.0).sum()),
+            "k_torsion_batched": float(((C_ROT * u_rot + C_PAIR * u_pair + C_SCORE * u_score) / 32.0).sum()),
+            "k_select_batched": float((C_RESC * u_resc / 32.0).sum())}
+
+
+def parity_check(batch, pocket, table, cfg, gpu_res, gpu_coords, gpu_tors, n, threads):
+    """CPU oracle on the first n ligands vs the GPU's records / best poses / best torsions."""
+    import oracle.oracle as orc
+    sample = batch.slice(0, n)
+    t0 = time.perf_counter()
+    o = orc.dock_batch(sample, pocket, table, cfg, seed=0, threads=threads)
+    dt = time.perf_counter() - t0
+    mism = {}
+    ok = o.results["status"] == 0
+    for f in PARITY_FIELDS:
+        g, r = gpu_res[f][:n].astype(np.int64), o.results[f].astype(np.int64)
+        bad = (g != r) if f in ("status", "poses_scored", "bump_checks", "bump_early_exits") else ((g != r) & ok)
+        mism[f] = int(bad.sum())
+    na, nf = int(sample.atom_off[-1]), int(sample.frag_off[-1])
+    coords_bad = tors_bad = 0
+    if gpu_coords is not None:
+        for i in np.nonzero(ok)[0]:
+            a0, a1 = sample.atom_off[i], sample.atom_off[i + 1]
+            coords_bad += int(not np.array_equal(gpu_coords[a0:a1], o.best_coords[a0:a1]))
+            f0, f1 = sample.frag_off[i], sample.frag_off[i + 1]
+            ref_t = o.restart_torsion[f0:f1, int(o.results[i]["best_restart"])]
+            tors_bad += int(not np.array_equal(gpu_tors[f0:f1], ref_t))
+        mism["best_coords"], mism["best_torsion"] = coords_bad, tors_bad
+    total = sum(mism.values())
+    return {"checked": int(n), "mismatches": total, "by_field": mism, "fields": list(mism),
+            "oracle": "oracle/dock_oracle.c", "atoms": na, "fragments": nf}, n / dt, threads
+
+
 def run_reference(args, rank, world):
+    """The reference arm: the CPU oracle on all host threads (kind "port": the reference ships no
+    code to build), inputs from oracle/gen_oracle.c (libdockscreen is never loaded)."""
     if rank != 0:
         return
     import oracle.oracle as orc
-    from paper_2209_05069_b200 import io, model
-    from paper_2209_05069_b200.native import InteractionTable
+    from paper_2209_05069_b200 import model   # pure-Python records only
     cfg = model.DockConfig()
-    pocket = io.synthetic_pocket()
-    table = InteractionTable.default()
+    pocket = orc.synthetic_pocket()
+    table = orc.default_table()
     threads = os.cpu_count() or 1
-    n = args.cpu_sample
+    # about 10k ligands per step (BASELINE.md §4), fewer when many steps are asked for, so the whole
+    # run stays within a few minutes; every step docks the same leading slice of the workload
+    n = max(1024, min(args.cpu_sample, 120_000 // max(1, args.steps + args.warmup)))
+    batch = orc.generate_mixed_batch(n, seed=args.seed, first_index=0)
     times = []
     for step in range(args.warmup + args.steps):
-        batch = io.generate_mixed_batch(n, seed=args.seed, first_index=step * n)
         t0 = time.perf_counter()
         orc.dock_batch(batch, pocket, table, cfg, seed=0, threads=threads)
-        dt = time.perf_counter() - t0
         if step >= args.warmup:
-            times.append(dt)
+            times.append(time.perf_counter() - t0)
     v = n / float(np.mean(times))
+    assert "libdockscreen" not in open("/proc/self/maps").read(), "the reference arm loaded the product library"
     line = {"impl": "reference", "metric": "ligands/sec docked", "value": v, "unit": "ligands/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * float(np.mean(times)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+int32", "data": "synthetic",
             "config": {"workload": "config3 mixed ligands (heavy U{8..40}, F U{0..20}), synthetic pocket 200 atoms, "
-                                   "DockConfig defaults", "ligands_per_step": n},
+                                   "DockConfig defaults", "ligands_per_step": n, "first_index": 0},
             "cpu_baseline": {"value": v, "unit": "ligands/s", "cores": threads, "kind": "port",
-                             "sample": f"{n} ligands of the config-3 distribution per step, oracle/dock_oracle.c, "
-                                       f"OpenMP {threads} threads"},
+                             "sample": f"the first {n} ligands of the GPU arm's config-3 workload per step (same slice "
+                                       f"every step), oracle/dock_oracle.c, OpenMP {threads} threads; inputs from "
+                                       f"oracle/gen_oracle.c"},
             "e2e": {"value": v, "unit": "ligands/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def roofline_block(cal, kms, n, ms_step, peak_winst, work, peaks):
+    per_kernel, w_exec = {}, 0.0
+    for k, t in kms.items():
+        kc = cal.get(k, {})
+        inst = kc.get("inst_per_ligand")
+        exec_frac = inst * n / (t / 1e3) / peak_winst if inst and t > 0 else None
+        w_exec += inst * n if inst else 0.0
+        per_kernel[k] = {"ms": t, "share": t / sum(kms.values()), "executed_issue_frac": exec_frac,
+                         "model_frac": (work[k] / (t / 1e3)) / peak_winst if t > 0 else None,
+                         "ncu_inst_per_ligand": inst, "dram_bytes_per_ligand": kc.get("dram_bytes_per_ligand"),
+                         "l2_hit_pct": kc.get("l2_hit_pct"), "ncu_issue_active_pct": kc.get("issue_active_pct"),
+                         "active_threads_per_inst": kc.get("active_threads_per_inst")}
+    dom = max(kms, key=kms.get)
+    d = per_kernel[dom]
+    kc = cal.get(dom, {})
+    achieved = (kc.get("inst_per_ligand") or 0.0) * n / (kms[dom] / 1e3)
+    roof = {"bound": "issue", "kernel": dom, "achieved": achieved / 1e9, "peak": peak_winst / 1e9,
+            "unit": "Gwarp-inst/s", "frac": d["executed_issue_frac"],
+            "traffic": kc["dram_bytes_per_ligand"] * n if "dram_bytes_per_ligand" in kc else None,
+            "l2_hit_pct": kc.get("l2_hit_pct"), "model_frac": d["model_frac"],
+            "calibration": {k: cal.get(k) for k in ("source", "matches_build", "lib_sha16")},
+            "note": "achieved = ncu-counted warp-instructions per ligand of this kernel (committed capture of this "
+                    "library build, 20k ligands of the same generator) x ligands / live CUDA-event kernel time; peak = "
+                    "SMs x 4 issue/clk x sm_max_mhz (MEASURED_PEAKS.json); traffic = ncu dram__bytes read+write per "
+                    "ligand x ligands (one launch); model_frac = the SURVEY §8d cost model (24 per alignment unit, "
+                    "20 per torsion rotation, 8 per bump pair, 14 per torsion score, 20 per rescore pair, /32), which "
+                    "the kernels beat (the alignment executes ~12 instructions per unit), hence > 1"}
+    whole = {"achieved": w_exec / (ms_step / 1e3) / 1e9, "frac": w_exec / (ms_step / 1e3) / peak_winst,
+             "unit": "Gwarp-inst/s", "model_frac": sum(work.values()) / (ms_step / 1e3) / peak_winst}
+    dram = sum((cal.get(k, {}).get("dram_bytes_per_ligand") or 0.0) for k in kms) * n
+    hbm_peak = peaks.get("hbm_gbs", 6453.7)
+    hbm = {"bound": "hbm", "achieved": dram / (ms_step / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+           "frac": dram / (ms_step / 1e3) / 1e9 / hbm_peak, "traffic": dram,
+           "dram_bytes_per_ligand": dram / n if n else None,
+           "note": "ncu dram__bytes (read + write) per ligand of the three kernels x ligands / step time"}
+    return roof, per_kernel, whole, hbm
+
+
+def config2_leg(ctx, dp, pocket, table, cfg, local, reps=30):
+    """BASELINE config 2: one ~90-atom, 20-bond ligand, time to result (H2D + kernels + D2H) of the
+    latency vs the batched family, the CPU oracle on one core and the latency engine's CPU shape on
+    all cores; parity of both families against the oracle."""
+    from paper_2209_05069_b200 import io, native
+    import oracle.oracle as orc
+    cands = io.generate_dataset_batch(36, 20, 64, seed=2)
+    A = np.diff(cands.atom_off)
+    pick = int(np.nonzero((A >= 86) & (A <= 94))[0][0])
+    lig = cands.subset([pick])
+    packed = native.pack(lig)
+    out = {"workload": "config2: generate_dataset(heavy=36, F=20, seed=2), first ligand with 86-94 atoms",
+           "atoms": int(A[pick]), "fragments": 20}
+    o = orc.dock_batch(lig, pocket, table, cfg, seed=0, threads=1)
+    with ClockSampler(local) as clk:
+        for name, fam in (("latency", native.FAMILY_LATENCY), ("batched", native.FAMILY_BATCHED)):
+            for _ in range(5):
+                g = ctx.dock(dp, packed, cfg, 0, fam, coords=True)
+            dev, wall = [], []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                g = ctx.dock(dp, packed, cfg, 0, fam, coords=True)
+                wall.append(time.perf_counter() - t0)
+                dev.append(g.stats.total_ms)
+            same = all(np.array_equal(g.results[f].astype(np.int64), o.results[f].astype(np.int64))
+                       for f in PARITY_FIELDS) and np.array_equal(g.best_coords, o.best_coords)
+            out[name] = {"device_ms_median": float(np.median(dev)), "device_ms_min": float(np.min(dev)),
+                         "wall_ms_median": 1e3 * float(np.median(wall)), "parity_ok": bool(same)}
+    out["clocks"] = clk.summary()
+    t0 = time.perf_counter()
+    orc.dock_batch(lig, pocket, table, cfg, seed=0, threads=1)
+    out["cpu_oracle_1core_ms"] = 1e3 * (time.perf_counter() - t0)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    orc.dock_batch(lig, pocket, table, cfg, seed=0, threads=cores, latency=True)
+    out["cpu_latency_engine_ms"] = 1e3 * (time.perf_counter() - t0)
+    out["cpu_latency_engine_cores"] = cores
+    out["latency_beats_batched"] = out["latency"]["device_ms_median"] < out["batched"]["device_ms_median"]
+    out["latency_speedup_vs_batched"] = out["batched"]["device_ms_median"] / out["latency"]["device_ms_median"]
+    return out
+
+
+def config4_leg(ctx, dp, pocket, table, cfg, local, count=4096, reps=3):
+    """BASELINE config 4 (compact): the paper's Small / Medium / Large classes
+    and a database-size ladder of the mixed distribution, both families, device-timed; 16 ligands
+    per class checked against the oracle.  The full 9 x 8 grid is tools/shape_sweep.py."""
+    from paper_2209_05069_b200 import io, native
+    import oracle.oracle as orc
+    fams = {"batched": native.FAMILY_BATCHED, "latency": native.FAMILY_LATENCY}
+    out = {"classes": {}, "ladder": []}
+    with ClockSampler(local) as clk:
+        for cname, (heavy, frags) in (("small", (20, 1)), ("medium", (35, 12)), ("large", (50, 20))):
+            b = io.generate_dataset_batch(heavy, frags, count, seed=4)
+            rb = native.ResidentBatch(ctx, native.pack(b))
+            row = {"heavy": heavy, "fragments": frags, "ligands": count, "mean_atoms": float(np.diff(b.atom_off).mean())}
+            for fname, fam in fams.items():
+                rb.dock(dp, cfg, family=fam)
+                ms = min(rb.dock(dp, cfg, family=fam).total_ms for _ in range(reps))
+                res = rb.download()
+                row[fname] = {"ms": ms, "ligands_per_s": count / (ms / 1e3)}
+                o = orc.dock_batch(b.slice(0, 16), pocket, table, cfg, seed=0, threads=os.cpu_count() or 1)
+                row[fname]["parity_ok"] = all(np.array_equal(res[f][:16].astype(np.int64), o.results[f].astype(np.int64))
+                                              for f in PARITY_FIELDS)
+            rb.close()
+            row["batched_over_latency"] = row["batched"]["ligands_per_s"] / row["latency"]["ligands_per_s"]
+            out["classes"][cname] = row
+        for size in (10, 100, 1000, 10000):
+            b = io.generate_mixed_batch(size, seed=3)
+            rb = native.ResidentBatch(ctx, native.pack(b))
+            row = {"ligands": size}
+            for fname, fam in fams.items():
+                rb.dock(dp, cfg, family=fam)
+                ms = min(rb.dock(dp, cfg, family=fam).total_ms for _ in range(reps))
+                row[fname] = size / (ms / 1e3)
+            rb.close()
+            row["winner"] = max(fams, key=lambda f: row[f])
+            out["ladder"].append(row)
+    out["clocks"] = clk.summary()
+    return out
+
+
+def api_leg(batch, pocket, table, cfg, steps):
+    """e2e through the reference-facing entry point: engines.batched_engine.run on a LigandBatch
+    stream (bucketizer + dispatchers + result table), results compared with ds_dock's."""
+    from paper_2209_05069_b200 import engines
+    engines.batched_engine.run(batch.slice(0, min(batch.n, 20000)), pocket, cfg, table=table)   # warm-up
+    times, rep = [], None
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        rep = engines.batched_engine.run(batch, pocket, cfg, table=table)
+        times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    c = rep.counters
+    return rep, {"value": batch.n / dt, "unit": "ligands/s", "ms_per_step": 1e3 * dt,
+                 "path": "engines.batched_engine.run(LigandBatch) -> bucketizer -> dispatchers -> ds_dock",
+                 "batches_dispatched": c.batches_dispatched, "batch_fill_ratio_mean":
+                     c.batch_fill_ratio_sum / c.batches_dispatched if c.batches_dispatched else None,
+                 "dispatchers": getattr(rep, "dispatchers", None)}
+
+
+def run_config5(args, rank, world, local, dist, gloo):
+    """BASELINE config 5: a --total screen split over the ranks (strong scaling); per step each rank
+    generates its shard on its GPU (device-side ingest), docks it, reads back the records and best
+    torsion indices, and rank 0 gathers them (host gather over gloo; nothing exchanged while docking)."""
+    import torch
+    from paper_2209_05069_b200 import io, model, native, shard
+    cfg = model.DockConfig()
+    seed = 5
+    lo, hi = shard.shard_range(args.total, world, rank)
+    shapes = io.mixed_shapes(hi - lo, seed, lo)
+    ctx = native.Context(local)
+    dp = ctx.pocket(io.synthetic_pocket(), native.InteractionTable.default())
+    rb = native.ResidentBatch.generated(ctx, seed, lo, shapes)
+    na, nf = int(rb.atom_off[-1]), int(rb.frag_off[-1])
+    res_buf = native.pinned_empty(max(hi - lo, 1), native.RESULT_DTYPE)
+    tor_buf = native.pinned_empty(max(nf, 1), np.uint8)
+
+    def barrier():
+        dist.barrier() if dist is not None else None
+        torch.cuda.synchronize(local)
+
+    def max_over(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=gloo)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        rb.dock(dp, cfg)
+    barrier()
+    dev_ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            dev_ms.append(rb.dock(dp, cfg).total_ms)
+    barrier()
+    ms = max_over(float(np.mean(dev_ms)))
+    # e2e: generate on the device + dock + D2H of records and torsions + host gather to rank 0
+    gathered = None
+    e2e_t = []
+    for it in range(1 + max(1, args.steps // 2)):
+        barrier()
+        t0 = time.perf_counter()
+        rb2 = native.ResidentBatch.generated(ctx, seed, lo, shapes)
+        rb2.dock(dp, cfg)
+        res, _, tors = rb2.download(torsion=True, results=res_buf, best_torsion=tor_buf)
+        rb2.close()
+        gathered = shard.gather_to_root([res, tors], rank, world, group=gloo)
+        dt = time.perf_counter() - t0
+        if it > 0:
+            e2e_t.append(dt)
+    e2e_s = max_over(float(np.mean(e2e_t)))
+    if rank == 0:
+        g_res, g_tors = gathered
+        sha = hashlib.sha256(g_res.tobytes() + g_tors.tobytes()).hexdigest()[:16]
+        line = {"metric": "ligands/sec docked", "value": args.total / (ms / 1e3), "unit": "ligands/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32+int32", "data": "synthetic",
+                "config": {"workload": f"config5 screen of {args.total} mixed ligands (seed {seed}) split into "
+                                       f"{world} contiguous shards, device-side ingest, batched family",
+                           "total_ligands": args.total, "parallelism": f"dp{world} (no collective on the docking path)",
+                           "l2": "inputs larger than L2"},
+                "e2e": {"value": args.total / e2e_s, "unit": "ligands/s", "ms_per_step": 1e3 * e2e_s,
+                        "h2d_bytes_per_step": int(shapes.nbytes) * world,
+                        "d2h_bytes_per_step": int(g_res.nbytes + g_tors.nbytes),
+                        "includes": "device generation + docking + D2H of records and best torsions + gloo gather"},
+                "gathered": {"records": int(len(g_res)), "torsion_bytes": int(g_tors.nbytes), "sha16": sha,
+                             "status_ok_frac": float(np.mean(g_res["status"] == 0))},
+                "clocks": clk.summary(), "gpu_launches": 3 * args.steps}
+        print(json.dumps(line), flush=True)
+    rb.close()
+    dp.close()
+    ctx.close()
 
 
 def main():
     args = parse()
     rank, world, local = dist_env()
-    # one process per GPU shares the host: split the cores between the local ranks so the OpenMP
-    # host work (batch validation, generation, the CPU baseline) does not oversubscribe them
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     if local_world > 1 and "OMP_NUM_THREADS" not in os.environ:
         os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // local_world))
@@ -210,13 +475,18 @@ def main():
         run_reference(args, rank, world)
         return
     import torch
-    # one process per GPU; ranks beyond the visible device count share devices (plumbing tests only)
-    local = local % max(torch.cuda.device_count(), 1)
-    dist = None
+    local = local % max(torch.cuda.device_count(), 1)   # ranks beyond the devices share them (plumbing tests)
+    dist = gloo = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl" if torch.cuda.device_count() >= world else "gloo")
+        gloo = dist.new_group(backend="gloo")   # host-side gather / timing reduction
+    if args.config == 5:
+        run_config5(args, rank, world, local, dist, gloo)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
     from paper_2209_05069_b200 import io, model, native
     from paper_2209_05069_b200.native import InteractionTable, ResidentBatch, pack
 
@@ -237,9 +507,8 @@ def main():
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=gloo)
         return float(t.item())
 
     # ---- kernel-only (resident inputs) ----
@@ -257,16 +526,16 @@ def main():
             sel_ms.append(st.select_ms)
     barrier()
     res = rb.download()
+    rb.close()
     ms = max_over_ranks(float(np.mean(step_ms)))
-    value = n * world / (ms / 1000.0)
+    value = n * world / (ms / 1e3)
     status_ok = float(np.mean(res["status"] == 0))
 
     # ---- end to end through ds_dock with host buffers ----
-    e2e = None
+    e2e, bufs = None, None
     if not args.no_e2e:
-        bufs = native.OutputBuffers(packed, pinned=True)   # pinned result records + best poses
-        for _ in range(1):
-            out = ctx.dock(dp, packed, cfg, 0, native.FAMILY_BATCHED, coords=True, buffers=bufs)
+        bufs = native.OutputBuffers(packed, pinned=True)
+        ctx.dock(dp, packed, cfg, 0, native.FAMILY_BATCHED, coords=True, buffers=bufs)
         barrier()
         t0 = time.perf_counter()
         h2d = d2h = 0
@@ -275,65 +544,47 @@ def main():
             h2d, d2h = out.stats.h2d_bytes, out.stats.d2h_bytes
         barrier()
         dt = max_over_ranks((time.perf_counter() - t0) / args.steps)
-        e2e = {"value": n * world / dt, "unit": "ligands/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": 1000 * dt}
+        e2e = {"value": n * world / dt, "unit": "ligands/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000 * dt,
+               "records_equal_resident": bool(np.array_equal(out.results, res))}
 
-    # ---- roofline of the dominant kernel (instruction issue) ----
+    # ---- rooflines (instruction issue; HBM) from the live kernel times + the ncu calibration ----
     peaks = measured_peaks()
-    clocks = clk.summary()
     f_mhz = peaks.get("sm_max_mhz", 1965.0)
     n_sm = torch.cuda.get_device_properties(local).multi_processor_count
     peak_winst = n_sm * 4 * f_mhz * 1e6
-    work = work_model(batch, res, cfg)
-    w_total = sum(work.values())
     a_ms, o_ms, s_ms = float(np.mean(align_ms)), float(np.mean(opt_ms)), float(np.mean(sel_ms))
     kms = {"k_align_batched": a_ms, "k_torsion_batched": o_ms - s_ms, "k_select_batched": s_ms}
-    # executed-instruction and DRAM calibration of the same kernels on the same workload generator,
-    # from the committed ncu capture (profiles/, per ligand), applied to this run's live timing
-    cal = ncu_calibration()
-    per_kernel = {}
-    for k, t in kms.items():
-        kc = cal.get(k, {})
-        per_kernel[k] = {
-            "ms": t, "share": t / (a_ms + o_ms),
-            "algorithmic_frac": (work[k] / (t / 1e3)) / peak_winst if t > 0 else None,
-            "executed_issue_frac": (kc["inst_per_ligand"] * n / (t / 1e3) / peak_winst)
-            if "inst_per_ligand" in kc and t > 0 else None,
-            "ncu_issue_active_pct": kc.get("issue_active_pct"),
-            "ncu_pipe_fmaheavy_pct": kc.get("pipe_fmaheavy_pct"),
-            "ncu_smem_wavefront_pct": kc.get("smem_wavefront_pct")}
-    dom = max(kms, key=kms.get)
-    kc = cal.get(dom, {})
-    achieved = work[dom] / (kms[dom] / 1e3)
-    roof = {"bound": "issue", "kernel": dom,
-            "achieved": achieved / 1e9, "peak": peak_winst / 1e9, "unit": "Gwarp-inst/s",
-            "frac": achieved / peak_winst,
-            "traffic": kc["dram_bytes_per_ligand"] * n if "dram_bytes_per_ligand" in kc else None,
-            "executed_issue_frac": per_kernel[dom]["executed_issue_frac"],
-            "ncu_issue_active_pct": kc.get("issue_active_pct"),
-            "note": f"achieved = algorithmic warp-instructions of the SURVEY §8d cost model (24 per alignment "
-                    f"unit, 20 per torsion rotation, 8 per bump pair, 14 per torsion score, 20 per rescore pair; "
-                    f"/32) / CUDA-event kernel time; peak = {n_sm} SM x 4 issue/clk x {f_mhz} MHz "
-                    f"(MEASURED_PEAKS.json sm_max_mhz); executed_issue_frac = ncu-counted warp-instructions "
-                    f"per ligand ({cal.get('source')}) x ligands / kernel time / peak (the paper's method); "
-                    f"traffic = ncu DRAM bytes per ligand x ligands"}
-    whole = {"achieved": (w_total / (ms / 1e3)) / 1e9, "frac": (w_total / (ms / 1e3)) / peak_winst,
-             "unit": "Gwarp-inst/s"}
-    in_bytes = int(packed.atom_xyzt.nbytes + packed.frag_desc.nbytes + packed.atom_off.nbytes * 2 + packed.id_hash.nbytes)
-    hbm = {"bound": "hbm", "achieved": in_bytes / (ms / 1e3) / 1e9, "peak": peaks.get("hbm_gbs", 6535.4),
-           "unit": "GB/s", "frac": in_bytes / (ms / 1e3) / 1e9 / peaks.get("hbm_gbs", 6535.4), "traffic": None}
+    sha = lib_sha16()
+    cal = ncu_calibration(sha)
+    roof, per_kernel, whole, hbm = roofline_block(cal, kms, n, ms, peak_winst, work_model(batch, res, cfg), peaks)
 
-    # ---- CPU baseline (oracle, bounded sample, rank 0 at N=1 only) ----
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        import oracle.oracle as orc
-        sample = batch.subset(range(0, min(args.cpu_sample, n)))
-        threads = os.cpu_count() or 1
-        t0 = time.perf_counter()
-        orc.dock_batch(sample, pocket, table, cfg, seed=0, threads=threads)
-        dt = time.perf_counter() - t0
-        cpu = {"value": sample.n / dt, "unit": "ligands/s", "cores": threads, "kind": "port",
-               "sample": f"first {sample.n} ligands of this workload, oracle/dock_oracle.c (OpenMP, {threads} threads)"}
+    # ---- parity + CPU baseline (oracle, bounded sample; rank 0) ----
+    cpu = parity = None
+    threads = os.cpu_count() or 1
+    if rank == 0 and not args.no_cpu:
+        ns = min(args.cpu_sample if world == 1 else min(args.cpu_sample, 2048), n)
+        gc = bufs.best_coords if bufs is not None else None
+        gt = bufs.best_torsion if bufs is not None else None
+        parity, rate, threads = parity_check(batch, pocket, table, cfg, res, gc, gt, ns, threads)
+        if world == 1:
+            cpu = {"value": rate, "unit": "ligands/s", "cores": threads, "kind": "port",
+                   "sample": f"the first {ns} ligands of this workload, oracle/dock_oracle.c (OpenMP, {threads} "
+                             f"threads); also the parity sample"}
+        if parity["mismatches"]:
+            print(json.dumps({"parity_failure": parity}), file=sys.stderr, flush=True)
+
+    extras = {}
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras["config2"] = config2_leg(ctx, dp, pocket, table, cfg, local)
+        extras["config4"] = config4_leg(ctx, dp, pocket, table, cfg, local)
+        try:
+            rep, api = api_leg(batch, pocket, table, cfg, max(1, min(args.steps, 3)))
+            rec = rep.records
+            api["records_equal_ds_dock"] = bool(np.array_equal(rec["results"], res))
+            extras["e2e_api"] = api
+        except Exception as e:  # the API leg must not hide the main line; report why it is missing
+            extras["e2e_api"] = {"error": f"{type(e).__name__}: {e}"}
 
     if rank == 0:
         line = {"metric": "ligands/sec docked", "value": value, "unit": "ligands/s", "n_gpus": world,
@@ -345,15 +596,17 @@ def main():
                            "l2": "inputs larger than L2 (per-step ligand data > 126 MB at 200k ligands)",
                            "parallelism": f"dp{world} (contiguous ligand shards, no collective)"},
                 "e2e": e2e, "roofline": roof, "roofline_kernels": per_kernel, "roofline_whole_step": whole,
-                "roofline_hbm": hbm,
-                "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": 3 * args.steps,
-                "kernel_ms": {"align": a_ms, "torsion": o_ms - s_ms, "select": s_ms}, "status_ok_frac": status_ok}
+                "roofline_hbm": hbm, "cpu_baseline": cpu, "parity": parity, "clocks": clk.summary(),
+                "gpu_launches": 3 * args.steps, "kernel_ms": {"align": a_ms, "torsion": o_ms - s_ms, "select": s_ms},
+                "status_ok_frac": status_ok, "lib_sha16": sha}
+        line.update(extras)
         print(json.dumps(line), flush=True)
-    rb.close()
     dp.close()
     ctx.close()
     if dist is not None:
         dist.destroy_process_group()
+    if parity is not None and parity["mismatches"]:
+        sys.exit(3)
 
 
 if __name__ == "__main__":

@@ -628,11 +628,19 @@ class ResidentBatch:
                                      C.byref(st)))
         return st
 
-    def download(self) -> np.ndarray:
-        res = np.zeros(max(self.n, 1), dtype=RESULT_DTYPE)
-        out = Outputs(_p(res), None, None, None, None)
+    def download(self, coords: bool = False, torsion: bool = False, results: Optional[np.ndarray] = None,
+                 best_torsion: Optional[np.ndarray] = None):
+        """The result records; with coords / torsion also the best poses (Å) and the best pose's
+        per-fragment torsion indices: (records, coords or None, torsion or None)."""
+        na, nf = int(self.atom_off[-1]) if self.n else 0, int(self.frag_off[-1]) if self.n else 0
+        res = results if results is not None else np.zeros(max(self.n, 1), dtype=RESULT_DTYPE)
+        bc = np.zeros((max(na, 1), 3), np.float32) if coords else None
+        bt = (best_torsion if best_torsion is not None else np.zeros(max(nf, 1), np.uint8)) if torsion else None
+        out = Outputs(_p(res), _p(bc), _p(bt), None, None)
         check(lib().ds_batch_download(self.ctx.handle, self.handle, C.byref(out)))
-        return res[:self.n]
+        if not coords and not torsion:
+            return res[:self.n]
+        return res[:self.n], (bc[:na] if bc is not None else None), (bt[:nf] if bt is not None else None)
 
     def close(self):
         if self.handle:

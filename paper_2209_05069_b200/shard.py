@@ -65,3 +65,28 @@ def gather_records(local: np.ndarray, rank: int, world: int, group=None) -> np.n
     dist.all_gather(outs, buf, group=group)
     parts = [o[:int(s.item())].cpu().numpy() for o, s in zip(outs, sizes)]
     return np.concatenate(parts).view(local.dtype)
+
+
+def gather_to_root(parts: Sequence[np.ndarray], rank: int, world: int, group=None) -> List[np.ndarray]:
+    """Host gather of per-rank arrays to rank 0 (gloo group: host memory, no NCCL): returns, on rank
+    0, each array concatenated over ranks in rank order; on other ranks an empty list.  One
+    size exchange + one gather per array; variable lengths allowed."""
+    if world == 1:
+        return [np.ascontiguousarray(p) for p in parts]
+    import torch
+    import torch.distributed as dist
+    out = []
+    for p in parts:
+        raw = np.ascontiguousarray(p).view(np.uint8).reshape(-1)
+        n = torch.tensor([raw.size], dtype=torch.int64)
+        sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(sizes, n, group=group)
+        m = max(int(s.item()) for s in sizes)
+        buf = torch.zeros(max(m, 1), dtype=torch.uint8)
+        buf[:raw.size] = torch.from_numpy(raw)
+        bufs = [torch.zeros(max(m, 1), dtype=torch.uint8) for _ in range(world)] if rank == 0 else None
+        dist.gather(buf, bufs, dst=0, group=group)
+        if rank == 0:
+            cat = np.concatenate([b[:int(s.item())].numpy() for b, s in zip(bufs, sizes)])
+            out.append(cat.view(p.dtype).reshape((-1,) + tuple(p.shape[1:])))
+    return out

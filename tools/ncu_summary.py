@@ -98,9 +98,15 @@ def main():
     ap.add_argument("launch_csv", nargs="?")
     ap.add_argument("--ligands", type=int, default=0, help="ligands docked per profiled launch (per-ligand calibration)")
     ap.add_argument("--workload", default="")
+    ap.add_argument("--lib", default="", help="the profiled libdockscreen.so: its sha256[:16] ties the "
+                                               "calibration to this build (bench.py checks it)")
     a = ap.parse_args()
     rep, out = a.report, a.out
     doc = {"report": rep, "kernels": raw(rep), "ligands": a.ligands, "workload": a.workload}
+    if a.lib:
+        import hashlib
+        with open(a.lib, "rb") as fh:
+            doc["lib_sha16"] = hashlib.sha256(fh.read()).hexdigest()[:16]
     if a.launch_csv:
         doc["launch_list"] = launches(a.launch_csv)
     with open(out + ".json", "w") as fh:
