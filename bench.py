@@ -198,7 +198,8 @@ def parity_check(batch, pocket, table, cfg, gpu_res, gpu_coords, gpu_tors, n, th
     mism = {}
     ok = o.results["status"] == 0
     for f in PARITY_FIELDS:
-        g, r = gpu_res[f][:n].astype(np.int64), o.results[f].astype(np.int64)
+        of = "bump_checks_rows" if f == "bump_checks" else f   # the device's counting unit (P14)
+        g, r = gpu_res[f][:n].astype(np.int64), o.results[of].astype(np.int64)
         bad = (g != r) if f in ("status", "poses_scored", "bump_checks", "bump_early_exits") else ((g != r) & ok)
         mism[f] = int(bad.sum())
     na, nf = int(sample.atom_off[-1]), int(sample.frag_off[-1])
@@ -314,7 +315,8 @@ def config2_leg(ctx, dp, pocket, table, cfg, local, reps=30):
                 g = ctx.dock(dp, packed, cfg, 0, fam, coords=True)
                 wall.append(time.perf_counter() - t0)
                 dev.append(g.stats.total_ms)
-            same = all(np.array_equal(g.results[f].astype(np.int64), o.results[f].astype(np.int64))
+            same = all(np.array_equal(g.results[f].astype(np.int64),
+                                      o.results["bump_checks_rows" if f == "bump_checks" else f].astype(np.int64))
                        for f in PARITY_FIELDS) and np.array_equal(g.best_coords, o.best_coords)
             out[name] = {"device_ms_median": float(np.median(dev)), "device_ms_min": float(np.min(dev)),
                          "wall_ms_median": 1e3 * float(np.median(wall)), "parity_ok": bool(same)}
@@ -351,8 +353,10 @@ def config4_leg(ctx, dp, pocket, table, cfg, local, count=4096, reps=3):
                 res = rb.download()
                 row[fname] = {"ms": ms, "ligands_per_s": count / (ms / 1e3)}
                 o = orc.dock_batch(b.slice(0, 16), pocket, table, cfg, seed=0, threads=os.cpu_count() or 1)
-                row[fname]["parity_ok"] = all(np.array_equal(res[f][:16].astype(np.int64), o.results[f].astype(np.int64))
-                                              for f in PARITY_FIELDS)
+                row[fname]["parity_ok"] = all(
+                    np.array_equal(res[f][:16].astype(np.int64),
+                                   o.results["bump_checks_rows" if f == "bump_checks" else f].astype(np.int64))
+                    for f in PARITY_FIELDS)
             rb.close()
             row["batched_over_latency"] = row["batched"]["ligands_per_s"] / row["latency"]["ligands_per_s"]
             out["classes"][cname] = row

@@ -56,7 +56,7 @@ typedef struct {
   int32_t best_restart, best_ax, best_ay, n_kept;
   int64_t poses_scored;
   int64_t bump_checks;     /* sequential pair evaluations */
-  int64_t bump_checks_r32; /* same scan counted in rounds of 32 pairs (device granularity) */
+  int64_t bump_checks_rows; /* the same scan counted in whole moving-atom rows (device granularity, P14) */
   int64_t bump_early_exits;
 } or_result;
 
@@ -283,10 +283,10 @@ static int apply_torsion(const or_lig *L, int f, const float (*u)[3], int deg, f
 
 /* SPEC.md:193 bump_check: i in mask (ascending) x j not in mask and not an axis atom (ascending) */
 static int bump_check(const or_lig *L, int f, const float (*u)[3], float bd2, int early_exit, int64_t *pairs,
-                      int64_t *pairs_r32, int64_t *exits) {
+                      int64_t *pairs_rows, int64_t *exits) {
   const int ab = L->axis[2 * f], ae = L->axis[2 * f + 1];
   const uint32_t *m = L->mask + OR_MASK_WORDS * f;
-  int64_t n = 0, total = 0;
+  int64_t n = 0, total = 0, rows = 0;
   int bump = 0, nm = 0, nc = 0;
   for (int i = 0; i < L->A; ++i) {
     if (in_mask(m, i)) ++nm;
@@ -295,6 +295,7 @@ static int bump_check(const or_lig *L, int f, const float (*u)[3], float bd2, in
   total = (int64_t)nm * nc;
   for (int i = 0; i < L->A && !(bump && early_exit); ++i) {
     if (!in_mask(m, i)) continue;
+    rows += nc;
     for (int j = 0; j < L->A; ++j) {
       if (in_mask(m, j) || j == ab || j == ae) continue;
       float dx = u[i][0] - u[j][0], dy = u[i][1] - u[j][1], dz = u[i][2] - u[j][2];
@@ -307,10 +308,7 @@ static int bump_check(const or_lig *L, int f, const float (*u)[3], float bd2, in
     }
   }
   *pairs += n;
-  {
-    int64_t r = early_exit && bump ? ((n + 31) / 32) * 32 : total;
-    *pairs_r32 += r < total ? r : total;
-  }
+  *pairs_rows += early_exit && bump ? rows : total;
   if (bump && early_exit) ++*exits;
   return bump;
 }
@@ -320,7 +318,7 @@ static int bump_check(const or_lig *L, int f, const float (*u)[3], float bd2, in
  * Returns 2 on DegenerateAxis (cnt then holds the counts up to that point, like the sequential
  * scan), else 0. */
 typedef struct {
-  int64_t poses_scored, bump_checks, bump_checks_r32, bump_early_exits;
+  int64_t poses_scored, bump_checks, bump_checks_rows, bump_early_exits;
   int geom, valid, ax, ay, align_score;
 } or_restart_out;
 
@@ -347,7 +345,7 @@ static int dock_restart(const or_lig *L, const or_pk *k, const or_config *cfg, i
       if (apply_torsion(L, f, (const float(*)[3])U, a * cfg->torsion_step_deg, eps, cand) < 0 && nt > 1)
         return 2; /* DegenerateAxis */
       o->poses_scored += 1;
-      if (bump_check(L, f, (const float(*)[3])cand, bd2, cfg->early_exit, &o->bump_checks, &o->bump_checks_r32,
+      if (bump_check(L, f, (const float(*)[3])cand, bd2, cfg->early_exit, &o->bump_checks, &o->bump_checks_rows,
                      &o->bump_early_exits))
         continue;
       int sc = grid_score(k, (const float(*)[3])cand, L->A);
@@ -395,7 +393,7 @@ static int dock_ligand_impl(const or_lig *L, const or_pk *k, const or_config *cf
   for (int r = 0; r < N; ++r) {
     res->poses_scored += ro[r].poses_scored;
     res->bump_checks += ro[r].bump_checks;
-    res->bump_checks_r32 += ro[r].bump_checks_r32;
+    res->bump_checks_rows += ro[r].bump_checks_rows;
     res->bump_early_exits += ro[r].bump_early_exits;
     if (st[r] == 2) { /* the sequential loop stops here: later restarts never ran */
       res->status = 2;

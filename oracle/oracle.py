@@ -39,7 +39,7 @@ class OrConfig(C.Structure):
 
 RESULT = np.dtype([("status", "<i4"), ("geom_score", "<i4"), ("chem_fx", "<i8"), ("best_restart", "<i4"),
                    ("best_ax", "<i4"), ("best_ay", "<i4"), ("n_kept", "<i4"), ("poses_scored", "<i8"),
-                   ("bump_checks", "<i8"), ("bump_checks_r32", "<i8"), ("bump_early_exits", "<i8")])
+                   ("bump_checks", "<i8"), ("bump_checks_rows", "<i8"), ("bump_early_exits", "<i8")])
 RESTART = np.dtype([("align_score", "<i4"), ("final_geom", "<i4"), ("ax", "<i4"), ("ay", "<i4"), ("valid", "<i4"),
                     ("kept", "<i4")])
 

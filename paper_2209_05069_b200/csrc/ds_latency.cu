@@ -46,7 +46,7 @@ struct LatSmem {
   unsigned cn[DS_MAX_ATOMS];           // their count (> kLatCand: scan all of C')
   int base[2];                  // grid score of the non-moving atoms, by fragment parity
   int ascore[32];
-  int bcode[32];                // early exit: min (moving rank * nC + C' rank) over bumping pairs (P14)
+  int bcode[32];                // early exit: the smallest bumping moving slot per angle (P14 rows)
   unsigned abump;
   unsigned key;
   int degen, degen_f, is_last;
@@ -119,27 +119,6 @@ __device__ __forceinline__ float lat_min_d2(const LatSmem &S, int m, int nC, flo
     }
   }
   return mind;
-}
-
-// the bumping pair the sequential scan of P9 meets first for moving atom m at q (cold path): the
-// smallest C' atom within the bump distance (candidates are unordered; C' is ascending)
-__device__ __noinline__ int lat_first_bump(const LatSmem &S, int m, int nC, float3 q, float bd2) {
-  const unsigned cnt = S.cn[m];
-  int best = 0x7FFFFFFF;
-  if (cnt <= (unsigned)kLatCand) {
-    for (unsigned t = 0; t < cnt; ++t) {
-      const int j = S.cl[m][t];
-      const float4 y = S.u[j];
-      if (j < best && dist2(q.x, q.y, q.z, y.x, y.y, y.z) < bd2) best = j;
-    }
-    return best;
-  }
-  for (int c = 0; c < nC; ++c) {
-    const int j = S.clist[c];
-    const float4 y = S.u[j];
-    if (dist2(q.x, q.y, q.z, y.x, y.y, y.z) < bd2) return j;
-  }
-  return best;
 }
 
 template <bool kSmemGrid>
@@ -357,11 +336,11 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         bool hit_any = false;
         // two moving atoms per step (independent chains: twice the loads in flight); a bump on
         // either marks the angle, whose partial score is then never read
-        // early exit: a thread stops once its next atom lies beyond the first bump found so far for
-        // its angle; every atom up to the sequential scan's first bump is then tested, so the pair
-        // count derived from the minimum code is exact and independent of thread timing (P14)
+        // early exit: a thread stops once its next atom lies beyond the first bumping slot found so far
+        // for its angle; every slot up to the sequential scan's first bump is then tested, so the
+        // minimum (and the pair count derived from it) is independent of thread timing (P14)
         for (int m = mg; m < nM; m += 2 * G) {
-          if (dp.early_exit && (hit_any || m * nC > *(volatile int *)&S.bcode[a])) break;
+          if (dp.early_exit && (hit_any || m > *(volatile int *)&S.bcode[a])) break;
           const bool two = m + G < nM;
           const int m1 = two ? m + G : m;
           const float4 p0 = S.u[S.mlist[m]], p1 = S.u[S.mlist[m1]];
@@ -373,20 +352,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
           if (d0 < dp.bd2 || d1 < dp.bd2) {
             hit_any = true;
             atomicOr(&S.abump, 1u << a);
-            if (dp.early_exit) {
-              const bool b0 = d0 < dp.bd2;
-              const int mb = b0 ? m : m1;
-              const int jb = lat_first_bump(S, mb, nC, b0 ? q0 : q1, dp.bd2);
-              // C' rank of jb: atoms below it minus the moving and axis atoms among them
-              int below = 0;
-              for (int w = 0; w < 5; ++w) {
-                const unsigned word = w == 0 ? fa.x : w == 1 ? fa.y : w == 2 ? fa.z : w == 3 ? fa.w : fb.x;
-                const int lo = 32 * w;
-                if (jb >= lo + 32) below += __popc(word);
-                else if (jb > lo) below += __popc(word & ((1u << (jb - lo)) - 1u));
-              }
-              atomicMin(&S.bcode[a], mb * nC + (jb - below - (ab < jb) - (ae < jb)));
-            }
+            if (dp.early_exit) atomicMin(&S.bcode[a], d0 < dp.bd2 ? m : m1);
           } else {
             part += two ? gv0 + gv1 : gv0;
           }
@@ -394,12 +360,13 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         if (part) atomicAdd(&S.ascore[a], part);
       }
       __syncthreads();
-      // pairs the sequential scan evaluates (P14): up to its first bump, or all nM * nC
+      // pairs evaluated at moving-row granularity (P14): the whole rows of the moving slots up to
+      // and including the first bumping one, or all nM * nC
       if (warp == 0) {
         unsigned np = 0;
         if (lane < nA) {
-          const int bc = S.bcode[lane];
-          np = (dp.early_exit && bc != 0x7FFFFFFF) ? (unsigned)bc + 1u : (unsigned)(nM * nC);
+          const int mb = S.bcode[lane];
+          np = (dp.early_exit && mb != 0x7FFFFFFF) ? (unsigned)((mb + 1) * nC) : (unsigned)(nM * nC);
         }
         np = __reduce_add_sync(kFull, np);
         if (lane == 0) S.pairs += np;

@@ -50,8 +50,7 @@ struct TorWarpSmem {
   uint8_t clist[kMaxA];     // complement atom indices, ascending
   uint16_t ovf[kOvf];       // candidates beyond kInline: moving slot << 8 | atom index
   int n_ovf;                // entries appended (> kOvf: the list overflowed, scan C')
-  int bcode[32];            // early exit: per angle of the block, min over bumping pairs of
-                            // (moving rank * nC + C' rank) — the sequential scan's stop point (P14)
+  int mhit[32];             // early exit: per sweep lane, the moving slot of its bump (P14 row count)
 };
 
 // Per-warp shared scratch of the select/rescore kernel.
@@ -225,51 +224,6 @@ __device__ __forceinline__ bool bump_hit(const TorWarpSmem &S, unsigned info, fl
   return mind < bd2;
 }
 
-// The bumping pair the sequential scan of P9 meets first for moving atom m at q (cold path, called
-// only after bump_hit said yes): the smallest C' atom within the bump distance.  Inline candidates
-// are in ascending C' order and precede every overflow entry; the overflow list is unordered.
-__device__ __noinline__ int first_bump_atom(const TorWarpSmem &S, unsigned info, float3 q, int m, int n_ovf, int nCf,
-                                            float bd2) {
-  const unsigned cnt = info & 0xFFu;
-  const unsigned nin = cnt < (unsigned)kInline ? cnt : (unsigned)kInline;
-  for (unsigned t = 0; t < nin; ++t) {
-    const unsigned j = (info >> (8 + 8 * t)) & 0xFFu;
-    const float4 y = S.u[j];
-    if (dist2(q.x, q.y, q.z, y.x, y.y, y.z) < bd2) return (int)j;
-  }
-  int best = 0x7FFFFFFF;
-  if (n_ovf <= kOvf) {
-    for (int t = 0; t < n_ovf; ++t) {
-      const unsigned e = S.ovf[t];
-      if ((int)(e >> 8) != m) continue;
-      const int j = (int)(e & 0xFFu);
-      const float4 y = S.u[j];
-      if (j < best && dist2(q.x, q.y, q.z, y.x, y.y, y.z) < bd2) best = j;
-    }
-  } else {
-    for (int c = 0; c < nCf; ++c) {  // ascending: the first hit is the smallest
-      const int j = S.clist[c];
-      const float4 y = S.u[j];
-      if (dist2(q.x, q.y, q.z, y.x, y.y, y.z) < bd2) return j;
-    }
-  }
-  return best;
-}
-
-// rank of atom j (not moving, not an axis atom) in the fragment's complement C' (ascending)
-__device__ __forceinline__ int complement_rank(const uint4 *frag, int j, int ab, int ae) {
-  const uint4 fa = __ldg(frag), fb = __ldg(frag + 1);
-  const unsigned w[5] = {fa.x, fa.y, fa.z, fa.w, fb.x};
-  int below = 0;
-#pragma unroll
-  for (int s = 0; s < 5; ++s) {
-    const int lo = s * 32;
-    if (j >= lo + 32) below += __popc(w[s]);
-    else if (j > lo) below += __popc(w[s] & ((1u << (j - lo)) - 1u));
-  }
-  return j - below - (ab < j) - (ae < j);
-}
-
 // A DegenerateAxis stops the ligand where the sequential oracle stops: restart records from the
 // stopping restart on and torsion indices of (restart rd, fragments >= fd) and of later restarts
 // are left zero, as the oracle leaves them (warp-cooperative, cold path)
@@ -287,6 +241,7 @@ __device__ __noinline__ void clear_unreached(const OptOut &out, int N, int f0, i
   }
 }
 
+template <bool kEarly>  // DockConfig.early_exit, compiled in
 __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
     k_torsion_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
                       OptOut out, int *queue) {
@@ -470,7 +425,6 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           if (ok) reinterpret_cast<unsigned *>(S.mip)[m] = cnt | inl;  // cnt <= nCf < 256
         }
         unsigned best_key = 0;  // (score + 32768) << 16 | (65535 - angle); 0 = no clean angle
-        S.bcode[lane] = 0x7FFFFFFF;
         __syncwarp();
         const int n_ovf = S.n_ovf;
         // ---- all angles at once: lane = (angle a, moving-atom group gi); the lane keeps its angle's
@@ -506,6 +460,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           }
           bool bumped = false;
           int part = 0;
+          S.mhit[lane] = 0x7FFFFFFF;
           // two moving atoms per lane and round (slots m0 + 2 gi and m0 + 2 gi + 1): twice the
           // independent work (two grid loads in flight) for the same loop and retirement overhead,
           // and the two rotations run as packed f32x2 (FADD2 / FFMA2, each half the scalar recipe)
@@ -518,7 +473,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           for (int m0 = 0; m0 < nM; m0 += 2 * G) {
             const int m1 = m0 + 2 * gi, m2 = m1 + 1;
             // with early exit a bumped angle is retired; without it every pair is checked
-            const bool live = lane_ok && !(dp.early_exit && bumped);
+            const bool live = lane_ok && !(kEarly && bumped);
             const bool act1 = live && m1 < nM, act2 = live && m2 < nM;
             if (!__any_sync(kFull, act1)) break;
             bool hit = false;
@@ -545,13 +500,10 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
               const bool h2 = act2 && bump_hit(S, info.y, q2, m2, n_ovf, nCf, dp.bd2);
               part += (h1 ? 0 : gv1) + (act2 && !h2 ? gv2 : 0);
               hit = h1 || h2;
-              if (hit && dp.early_exit) {  // where the sequential scan stops for this angle (P14)
-                const int mb = h1 ? m1 : m2;
-                const int jb = first_bump_atom(S, h1 ? info.x : info.y, h1 ? q1 : q2, mb, n_ovf, nCf, dp.bd2);
-                atomicMin(&S.bcode[a], mb * nC + complement_rank(bt.frags + 2 * (size_t)(f0 + f), jb, ab, ae));
-              }
+              // with early exit an angle bumps in one round only (it is retired after it)
+              if (kEarly && hit) S.mhit[lane] = h1 ? m1 : m2;
             }
-            if (dp.early_exit) {  // OR the hits of the G lanes that share an angle
+            if (kEarly) {  // OR the hits of the G lanes that share an angle
               // every lane must reach the ballot: never put it behind a short-circuit operator
               const unsigned hb = __ballot_sync(kFull, hit);
               bumped = bumped || (hb & same) != 0u;
@@ -560,18 +512,19 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
             }
           }
           __syncwarp();
-          // pairs the sequential scan evaluates (P14): up to and including its first bump, or all
-          // nM * nC; without early exit every pair
+          // pairs evaluated at moving-row granularity (P14): all nM * nC of a clean angle (or without
+          // early exit), else the whole rows of the moving slots up to and including the first
+          // bumping one, m* = the smallest bumping slot of the angle's G lanes
           {
             unsigned np = 0;
             if (gi == 0 && lane_ok) {
-              const int bc = S.bcode[a];
-              np = (dp.early_exit && bc != 0x7FFFFFFF) ? (unsigned)bc + 1u : (unsigned)(nM * nC);
+              int mb = 0x7FFFFFFF;
+              for (int t = 0; t < G; ++t) mb = min(mb, S.mhit[a + t * nA]);
+              np = mb == 0x7FFFFFFF ? (unsigned)(nM * nC) : (unsigned)((mb + 1) * nC);
             }
             pairs_total += (unsigned)warp_sum((int)np);
           }
           __syncwarp();
-          S.bcode[lane] = 0x7FFFFFFF;
           // combine the G partial scores of an angle on its group-0 lane
           int sum = part;
           for (int t = 1; t < G; ++t) {
@@ -586,7 +539,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           if (gi == 0 && !((fold >> a) & 1u))
             kk = ((unsigned)(base + sum + 32768) << 16) | (unsigned)(65535 - kang);
           evals += (unsigned)nA;
-          if (dp.early_exit) early_exits += (unsigned)__popc(fold);
+          if (kEarly) early_exits += (unsigned)__popc(fold);
           best_key = max(best_key, __reduce_max_sync(kFull, kk));
         }
         const int best_k = best_key ? 65535 - (int)(best_key & 0xFFFFu) : -1;
@@ -822,8 +775,13 @@ constexpr size_t kTorSmem = kTorWarps * sizeof(TorWarpSmem);
 
 void launch_torsion_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                             const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st) {
-  cudaFuncSetAttribute(k_torsion_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
-  k_torsion_batched<<<blocks, kTorWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
+  if (dp.early_exit) {
+    cudaFuncSetAttribute(k_torsion_batched<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
+    k_torsion_batched<true><<<blocks, kTorWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
+  } else {
+    cudaFuncSetAttribute(k_torsion_batched<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
+    k_torsion_batched<false><<<blocks, kTorWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
+  }
 }
 
 void launch_select_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const uint32_t *keys,
@@ -834,8 +792,8 @@ void launch_select_batched(const PocketView &pk, const BatchView &bt, const Dock
 
 int torsion_blocks_per_sm() {
   int n = 0;
-  cudaFuncSetAttribute(k_torsion_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_torsion_batched, kTorWarps * 32, kTorSmem);
+  cudaFuncSetAttribute(k_torsion_batched<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_torsion_batched<true>, kTorWarps * 32, kTorSmem);
   return n;
 }
 
