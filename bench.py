@@ -379,16 +379,18 @@ def api_leg(batch, pocket, table, cfg, steps):
     """e2e through the reference-facing entry point: engines.batched_engine.run on a LigandBatch
     stream (bucketizer + dispatchers + result table), results compared with ds_dock's."""
     from paper_2209_05069_b200 import engines
-    engines.batched_engine.run(batch.slice(0, min(batch.n, 20000)), pocket, cfg, table=table)   # warm-up
+    kw = dict(table=table, capacities="device", workers=4, dispatchers_per_device=3)
+    engines.batched_engine.run(batch.slice(0, min(batch.n, 20000)), pocket, cfg, **kw)   # warm-up
     times, rep = [], None
     for _ in range(steps):
         t0 = time.perf_counter()
-        rep = engines.batched_engine.run(batch, pocket, cfg, table=table)
+        rep = engines.batched_engine.run(batch, pocket, cfg, **kw)
         times.append(time.perf_counter() - t0)
     dt = float(np.mean(times))
     c = rep.counters
     return rep, {"value": batch.n / dt, "unit": "ligands/s", "ms_per_step": 1e3 * dt,
                  "path": "engines.batched_engine.run(LigandBatch) -> bucketizer -> dispatchers -> ds_dock",
+                 "capacity": rep.dispatch_log[0]["capacity"] if rep.dispatch_log else None,
                  "batches_dispatched": c.batches_dispatched, "batch_fill_ratio_mean":
                      c.batch_fill_ratio_sum / c.batches_dispatched if c.batches_dispatched else None,
                  "dispatchers": getattr(rep, "dispatchers", None)}

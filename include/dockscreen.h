@@ -211,9 +211,12 @@ int ds_generate_resident(ds_ctx *ctx, int64_t seed, int64_t first_index, int32_t
  * frag_desc uint32[8 * fragments], id_hash uint64[ligands]. */
 int ds_batch_read_inputs(ds_ctx *ctx, const ds_dev_batch *batch, float *atom_xyzt, uint32_t *frag_desc,
                          uint64_t *id_hash);
-/* Ligands one batched launch keeps resident on this device for atom range
- * `range_idx` (0..4) — the B200 analogue of the paper's occupancy-derived
- * capacity. */
+/* Batch capacity for atom range `range_idx` (0..4) on this device — the B200 analogue of the
+ * paper's occupancy-derived batch size (replaces SPEC.md:332 bucket_capacity's
+ * fixed A100 numbers): SMs x the smallest resident-warp count of the three batched kernels
+ * (cudaOccupancyMaxActiveBlocksPerMultiprocessor on the kernels themselves; one ligand per warp)
+ * x DS_CAPACITY_WAVES (default 2).  The same for every range: the kernels are not
+ * range-specialised. */
 int ds_query_capacity(ds_ctx *ctx, int range_idx, int *ligands);
 
 /* ---- L2 ops of the native slot, batched on device ------ */
@@ -285,6 +288,15 @@ void ds_ligq_free(ds_ligq *h);
 int ds_validate_ligands(int32_t n, const int32_t *atom_off, const int64_t *atom_type, const uint8_t *is_heavy,
                         const int32_t *bond_off, const int32_t *bonds, const int32_t *frag_off,
                         const int32_t *frag_axis, const int64_t *mv_off, const int64_t *mv, int32_t *codes);
+/* Rows sel[0..n_sel) of a CSR array (src_off: rows + 1 offsets, elem_bytes per element) gathered
+ * into dst in selection order: pass 1 (dst == NULL) fills dst_off[n_sel + 1].  Used by the batched
+ * engine to cut a bucket's batch out of the packed stream (bucketizer.push). */
+int ds_csr_gather(int32_t n_sel, const int32_t *sel, const int32_t *src_off, const void *src, int32_t elem_bytes,
+                  int32_t *dst_off, void *dst);
+/* Inverse: row k of src goes to row sel[k] of dst (offsets dst_off) — per-ligand outputs of a
+ * batch back into stream order (EngineReport). */
+int ds_csr_scatter(int32_t n_sel, const int32_t *sel, const int32_t *src_off, const void *src, int32_t elem_bytes,
+                   const int32_t *dst_off, void *dst);
 /* Seeded symmetric 16x16 interaction table in [-1, 1]. */
 int ds_default_table(int64_t seed, float *table /* 256 */);
 

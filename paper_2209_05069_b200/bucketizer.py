@@ -31,9 +31,13 @@ class Batch:
     capacity: int
     seqs: list = field(default_factory=list)     # input sequence numbers (engine bookkeeping)
 
+    def __len__(self) -> int:
+        """Members: the pushed ligands, or for a bulk-pushed batch (push_many) its stream indices."""
+        return max(len(self.ligands), len(self.seqs))
+
     @property
     def fill_ratio(self) -> float:
-        return len(self.ligands) / self.capacity
+        return len(self) / self.capacity
 
 
 def range_index(n_atoms: int) -> int:
@@ -111,6 +115,28 @@ class Bucketizer:
         self._record(b)
         return b
 
+    def push_many(self, key: BucketKey, seqs) -> List[Batch]:
+        """Bulk push of ligands that share `key`, given by their stream indices (the batched engine's
+        producers: a chunk of the packed stream per call).  Equivalent to pushing them one by one in
+        order under the bucket's lock: every time the bucket reaches capacity exactly `capacity`
+        members are detached as a full batch; returns those batches (possibly none)."""
+        import numpy as np
+        seqs = np.asarray(seqs)
+        lk, _ = self._bucket(key)
+        full = []
+        with lk:
+            b = self._buckets[key]
+            cur = np.concatenate([np.asarray(b.seqs, dtype=seqs.dtype), seqs]) if len(b.seqs) else seqs
+            cap = b.capacity
+            k = 0
+            while len(cur) - k >= cap:
+                full.append(Batch(key, [], cap, cur[k:k + cap]))
+                k += cap
+            self._buckets[key] = Batch(key, [], cap, cur[k:])
+        for fb in full:
+            self._record(fb)
+        return full
+
     def flush(self) -> List[Batch]:
         """All non-empty buckets as partial batches; buckets reset."""
         out = []
@@ -120,7 +146,7 @@ class Bucketizer:
             lk, _ = self._bucket(key)
             with lk:
                 b = self._buckets[key]
-                if b.ligands:
+                if len(b):
                     self._buckets[key] = Batch(key, [], b.capacity)
                     out.append(b)
         for b in out:

@@ -409,6 +409,15 @@ static void launch_t(const PocketView &pk, const BatchView &bt, const DockParams
   k_align_batched<NA, G, S><<<blocks, warps * 32, smem, st>>>(pk, bt, dp, order, out, queue);
 }
 
+// resident CTAs per SM of the default-step alignment kernel (grid in shared memory) for this
+// launch shape: the occupancy API on the real kernel (ds_query_capacity)
+int align_blocks_per_sm(int warps, size_t smem) {
+  int n = 0;
+  cudaFuncSetAttribute(k_align_batched<30, 30, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_align_batched<30, 30, true>, warps * 32, smem);
+  return n;
+}
+
 void launch_align_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                           AlignOut out, int *queue, int grid_in_smem, int blocks, int warps, size_t smem,
                           cudaStream_t st) {

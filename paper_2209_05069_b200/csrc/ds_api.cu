@@ -26,6 +26,7 @@ void launch_select_batched(const PocketView &pk, const BatchView &bt, const Dock
 size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap);
 int torsion_blocks_per_sm();
 int select_blocks_per_sm(size_t smem);
+int align_blocks_per_sm(int warps, size_t smem);
 bool launch_align_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int max_atoms, int *scores,
                           unsigned *keys, cudaStream_t st);
 size_t latency_rec_bytes();
@@ -1292,9 +1293,33 @@ int ds_build_pocket_grid_device(ds_ctx *c, const float *atom_xyz, int32_t n_atom
 
 int ds_query_capacity(ds_ctx *c, int range_idx, int *ligands) {
   if (!c || !ligands || range_idx < 0 || range_idx > 4) return fail(DS_ERR_INVALID_ARG, "bad argument");
-  // the batched kernels are persistent: a full wave is (SMs x resident warps) ligands
-  const int per_sm_align = 32;
-  *ligands = c->sm_count * per_sm_align;
+  DS_CUDA(enter_device(c->device));
+  // PAPER.md:382-384 sizes a batch as the ligands one launch keeps resident, from
+  // cudaOccupancyMaxActiveBlocksPerMultiprocessor on the range's kernel.  The batched kernels here
+  // give a warp to a ligand of any size (per-warp scratch for 160 atoms), so the resident ligand
+  // slots are the same for every range: SMs x the smallest resident-warp count of the three
+  // batched kernels (alignment with the synthetic-pocket grid in shared memory, torsion, select
+  // with 200 pocket atoms and the default bins).  A batch is `waves` such launches' worth
+  // (DS_CAPACITY_WAVES, default 2): persistent CTAs drain an LPT queue, so more than one wave
+  // amortises the tail of the slowest ligands.
+  const int N = 8;
+  const size_t per_warp = (size_t)align_warp_smem_bytes_host(N);
+  const size_t grid_bytes = 181888, fixed = 30 * 16;
+  int warps_a = 32;
+  if (grid_bytes + fixed + per_warp * 8 <= c->smem_optin)
+    warps_a = (int)std::min<size_t>(32, (c->smem_optin - grid_bytes - fixed) / per_warp);
+  const int wa = warps_a * align_blocks_per_sm(warps_a, grid_bytes + fixed + per_warp * warps_a);
+  const int wt = 8 * torsion_blocks_per_sm();
+  const int ws = 8 * select_blocks_per_sm(select_cta_smem_bytes(200, 4, 1080));
+  cudaGetLastError();
+  const int per_sm = std::min(wa, std::min(wt, ws));
+  if (per_sm <= 0) return fail(DS_ERR_CUDA, "occupancy query returned 0 resident warps");
+  static const int waves = [] {
+    const char *e = getenv("DS_CAPACITY_WAVES");
+    const int w = e ? atoi(e) : 2;
+    return w < 1 ? 1 : w;
+  }();
+  *ligands = c->sm_count * per_sm * waves;
   return DS_OK;
 }
 

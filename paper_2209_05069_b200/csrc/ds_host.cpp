@@ -362,6 +362,41 @@ int ds_build_pocket_grid(const float *atom_xyz, int32_t n_atoms, float spacing, 
   return DS_OK;
 }
 
+// Gather / scatter of selected rows of a CSR array (the engines' per-bucket batches): rows sel[k]
+// of src (offsets src_off, elem_bytes per element) become rows k of dst.  Pass 1 (dst == NULL)
+// fills dst_off (n_sel + 1 entries); OpenMP over rows.
+int ds_csr_gather(int32_t n_sel, const int32_t *sel, const int32_t *src_off, const void *src, int32_t elem_bytes,
+                  int32_t *dst_off, void *dst) {
+  if (n_sel < 0 || !sel || !src_off || !dst_off || elem_bytes <= 0) return DS_ERR_INVALID_ARG;
+  if (!dst) {
+    dst_off[0] = 0;
+    for (int32_t k = 0; k < n_sel; ++k) dst_off[k + 1] = dst_off[k] + (src_off[sel[k] + 1] - src_off[sel[k]]);
+    return DS_OK;
+  }
+  if (!src && dst_off[n_sel] > 0) return DS_ERR_INVALID_ARG;
+#pragma omp parallel for schedule(static) if (n_sel >= 2048)
+  for (int32_t k = 0; k < n_sel; ++k) {
+    const int32_t i = sel[k];
+    memcpy((char *)dst + (size_t)dst_off[k] * elem_bytes, (const char *)src + (size_t)src_off[i] * elem_bytes,
+           (size_t)(src_off[i + 1] - src_off[i]) * elem_bytes);
+  }
+  return DS_OK;
+}
+
+// inverse: rows k of src (offsets src_off) go to rows sel[k] of dst (offsets dst_off)
+int ds_csr_scatter(int32_t n_sel, const int32_t *sel, const int32_t *src_off, const void *src, int32_t elem_bytes,
+                   const int32_t *dst_off, void *dst) {
+  if (n_sel < 0 || !sel || !src_off || !dst_off || elem_bytes <= 0 || (!src && n_sel) || (!dst && n_sel))
+    return DS_ERR_INVALID_ARG;
+#pragma omp parallel for schedule(static) if (n_sel >= 2048)
+  for (int32_t k = 0; k < n_sel; ++k) {
+    const int32_t i = sel[k];
+    memcpy((char *)dst + (size_t)dst_off[i] * elem_bytes, (const char *)src + (size_t)src_off[k] * elem_bytes,
+           (size_t)(src_off[k + 1] - src_off[k]) * elem_bytes);
+  }
+  return DS_OK;
+}
+
 int ds_default_table(int64_t seed, float *table) {
   if (!table) return DS_ERR_INVALID_ARG;
   Rng r((uint64_t)seed, kStreamTable, 0);

@@ -3,197 +3,432 @@
 latency_engine.run  — PAPER.md:287-348: every ligand is one synchronous dock call; each worker
                       thread owns one ds_ctx (a CUDA stream + a worst-case workspace allocated once,
                       PAPER.md:310-313) and the ligand's restarts/rotations are spread across the GPU.
-batched_engine.run  — PAPER.md:349-426: producer threads push validated ligands into the
-                      bucketizer; a dispatcher thread per device launches full batches (and the
-                      flushed partial ones) with the batched kernels (one warp per ligand).
+batched_engine.run  — PAPER.md:349-426: producer threads pack + validate chunks of
+                      the stream natively and push the ligands into the bucketizer (bulk push per
+                      bucket key, linearizable per bucket); every batch the bucketizer detaches when
+                      full — and, at end of stream, every flushed partial one — goes to a dispatcher
+                      thread (several per device, each with its own ds_ctx and stream, so the tail of
+                      one batch overlaps the next) that cuts it out of the packed stream and docks it
+                      with the batched kernels (one warp per ligand).  The dispatch log records when
+                      each batch was detached, started and finished.
 
-Both return EngineReport with results ordered by input sequence; per-ligand errors are recorded
-and the stream continues.  There is no CPU execution path.
+Both accept the reference's stream of Ligand objects, or a LigandBatch (io.parse_ligand_batch, the
+generators) — the zero-object fast path — and return an EngineReport whose results are ordered by
+input sequence and materialised as DockResult objects only on access.  Per-ligand
+errors are recorded and the stream continues; configuration and device errors
+are fatal and re-raised from run().  There is no CPU execution path.
 """
 from __future__ import annotations
 
+import ctypes as C
 import queue
 import threading
 import time
+from collections import abc as _abc
 from dataclasses import dataclass, field
-from typing import Iterable, List, Mapping, Optional, Sequence, Tuple
+from typing import Dict, Iterable, List, Mapping, Optional, Sequence, Tuple, Union
 
-from . import model
 import numpy as np
 
-from .bucketizer import Batch, BucketKey, Bucketizer, bucket_capacity, classify
-from .docking import _pockets, results_from_output, thread_context
-from .native import FAMILY_BATCHED, FAMILY_LATENCY, InteractionTable, LigandBatch, pack
+from . import model
+from .bucketizer import Batch, BucketKey, Bucketizer, bucket_capacity, device_capacities
+from .docking import _pockets, thread_context
+from .native import (CHEM_SCALE, DS_OK, ERRORS, FAMILY_BATCHED, FAMILY_LATENCY, FRAG_WORDS, MASK_WORDS,
+                     RESULT_DTYPE, STATUS_DEGENERATE_AXIS, STATUS_NO_VALID_POSE, Context, DsError,
+                     InteractionTable, LigandBatch, PackedBatch, _p, check, lib, pack, pinned_empty)
+
+Stream = Union[LigandBatch, Iterable[model.Ligand]]
+
+
+class ResultTable(_abc.Sequence):
+    """EngineReport.results as a sequence of DockResult over the result arrays: ligands in input
+    order, errored ones left out; an object is built only when an item is read."""
+
+    def __init__(self, ids, seqs: np.ndarray, rows: np.ndarray, res: np.ndarray, coords: np.ndarray,
+                 atom_off: np.ndarray, tors: np.ndarray, frag_off: np.ndarray):
+        self.ids, self.seqs, self.rows = ids, seqs, rows
+        self.res, self.coords, self.atom_off, self.tors, self.frag_off = res, coords, atom_off, tors, frag_off
+
+    def __len__(self) -> int:
+        return len(self.rows)
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(len(self)))]
+        i = int(self.rows[k])
+        r = self.res[i]
+        a0, a1 = int(self.atom_off[i]), int(self.atom_off[i + 1])
+        f0, f1 = int(self.frag_off[i]), int(self.frag_off[i + 1])
+        c = model.Counters(poses_scored=int(r["poses_scored"]), bump_checks=int(r["bump_checks"]),
+                           bump_early_exits=int(r["bump_early_exits"]))
+        pose = model.Pose(coordinates=self.coords[a0:a1].copy(), geometric_score=int(r["geom_score"]),
+                          chemical_score=float(r["chem_fx"]) / CHEM_SCALE, restart_index=int(r["best_restart"]),
+                          valid=True, align_indices=(int(r["best_ax"]), int(r["best_ay"])),
+                          torsion_indices=tuple(int(t) for t in self.tors[f0:f1]), chem_fx=int(r["chem_fx"]))
+        return model.DockResult(self.ids[i], pose, c)
 
 
 @dataclass
 class EngineReport:
     """SPEC.md:385-389."""
-    results: List[model.DockResult]
+    results: Sequence[model.DockResult]
     wall_time: float
     counters: model.Counters
     errors: List[Tuple[int, str, str]] = field(default_factory=list)   # (seq, ligand id, message)
     device_ms: float = 0.0
+    records: Optional[Dict[str, np.ndarray]] = None   # result arrays (ds_result records, best poses, torsions)
+    dispatch_log: List[dict] = field(default_factory=list)
+    dispatchers: int = 0
 
     @property
     def throughput(self) -> float:
         return len(self.results) / self.wall_time if self.wall_time > 0 else 0.0
 
 
-def _finish(n: int, slots: list, errors: list, counters: model.Counters, t0: float, dev_ms: float) -> EngineReport:
-    results = []
-    for seq in range(n):
-        r = slots[seq]
-        if r is None:
-            continue
-        counters.poses_scored += r.counters.poses_scored
-        counters.bump_checks += r.counters.bump_checks
-        counters.bump_early_exits += r.counters.bump_early_exits
-        if r.best_pose is None:
-            errors.append((seq, r.ligand_id, r.error or "error"))
-            continue
-        results.append(r)
+def _status_error(st: int) -> Optional[str]:
+    if st == STATUS_NO_VALID_POSE:
+        return "no valid pose"
+    if st == STATUS_DEGENERATE_AXIS:
+        return "DegenerateAxis"
+    return None if st == 0 else f"status {st}"
+
+
+NOT_DOCKED = -1   # status of a row whose ligand failed validation at pack time (already an error)
+
+
+def _finish_arrays(n_in: int, seq_of_row: np.ndarray, ids, res, coords, atom_off, tors, frag_off,
+                   errors: list, counters: model.Counters, t0: float, dev_ms: float) -> EngineReport:
+    """Report from the per-row result arrays (row = valid ligand, seq_of_row = its input sequence);
+    rows with status NOT_DOCKED did no work and are already in `errors`."""
+    st = res["status"]
+    docked = st != NOT_DOCKED
+    counters.poses_scored += int(res["poses_scored"][docked].astype(np.int64).sum())
+    counters.bump_checks += int(res["bump_checks"][docked].astype(np.int64).sum())
+    counters.bump_early_exits += int(res["bump_early_exits"][docked].astype(np.int64).sum())
+    for i in np.nonzero(docked & (st != 0))[0]:
+        errors.append((int(seq_of_row[i]), ids[int(i)], _status_error(int(st[i]))))
     errors.sort()
-    return EngineReport(results, time.perf_counter() - t0, counters, errors, dev_ms)
+    rows = np.nonzero(st == 0)[0]
+    table = ResultTable(ids, seq_of_row[rows], rows, res, coords, atom_off, tors, frag_off)
+    rep = EngineReport(table, time.perf_counter() - t0, counters, errors, dev_ms)
+    rep.records = {"results": res, "best_coords": coords, "best_torsion": tors, "atom_off": atom_off,
+                   "frag_off": frag_off, "seq": seq_of_row}
+    return rep
+
+
+def _validated(stream: Stream) -> Tuple[LigandBatch, np.ndarray, list, int]:
+    """(valid ligands as one batch, their input sequence numbers, validation errors, inputs)."""
+    if isinstance(stream, LigandBatch):
+        return stream, np.arange(stream.n, dtype=np.int64), [], stream.n
+    ligs = stream if isinstance(stream, (list, tuple)) else list(stream)
+    batch, codes = LigandBatch.from_ligands_validated(ligs)
+    errors = []
+    for i in np.nonzero(codes)[0]:
+        try:
+            model.validate_ligand(ligs[i])          # the reference's exact message
+            msg = f"IndexOutOfRange: {ligs[i].id}: invalid ligand"
+        except model.DockscreenError as e:
+            msg = f"{type(e).__name__}: {e}"
+        errors.append((int(i), ligs[i].id, msg))
+    return batch, np.nonzero(codes == 0)[0].astype(np.int64), errors, len(ligs)
 
 
 class latency_engine:  # noqa: N801  (module-like namespace mirroring `dockscreen.engines.latency_engine`)
     @staticmethod
-    def run(stream: Iterable[model.Ligand], pocket: model.Pocket, cfg: model.DockConfig = model.DockConfig(),
+    def run(stream: Stream, pocket: model.Pocket, cfg: model.DockConfig = model.DockConfig(),
             workers: int = 1, seed: int = 0, table: Optional[InteractionTable] = None,
             devices: Sequence[int] = (0,)) -> EngineReport:
         """`workers` slots, one ligand per slot at a time, results = dock_ligand."""
         if workers < 1:
             raise ValueError("workers must be positive")
-        ligs = list(stream)
-        n = len(ligs)
-        slots: list = [None] * n
-        errors: list = []
+        t0 = time.perf_counter()
+        batch, seq_of_row, errors, n_in = _validated(stream)
+        n = batch.n
+        res = np.zeros(max(n, 1), RESULT_DTYPE)[:n]
+        coords = np.zeros((max(int(batch.atom_off[-1]) if n else 0, 1), 3), np.float32)
+        tors = np.zeros(max(int(batch.frag_off[-1]) if n else 0, 1), np.uint8)
         lock = threading.Lock()
         nxt = [0]
         dev_ms = [0.0]
-        allocs = []
-        workspaces = [0]
-        t0 = time.perf_counter()
+        allocs, workspaces, fatal = [], [0], []
 
         def worker(wid: int):
-            dev = devices[wid % len(devices)]
-            ctx = thread_context(dev)
-            dp = _pockets.get(ctx, pocket, table)
-            ctx.reserve(cfg)            # the worker's worst-case workspace, allocated once
-            with lock:
-                workspaces[0] += 1
-            a0 = ctx.alloc_count()
-            while True:
+            try:
+                dev = devices[wid % len(devices)]
+                ctx = thread_context(dev)
+                dp = _pockets.get(ctx, pocket, table)
+                ctx.reserve(cfg)            # the worker's worst-case workspace, allocated once
                 with lock:
-                    i = nxt[0]
-                    nxt[0] += 1
-                if i >= n:
-                    break
-                lig = ligs[i]
-                try:
-                    model.validate_ligand(lig)
-                    b = LigandBatch.from_ligands([lig])
-                    out = ctx.dock(dp, pack(b), cfg, seed, FAMILY_LATENCY, coords=True)
-                    slots[i] = results_from_output(b, out, cfg)[0]
+                    workspaces[0] += 1
+                a0 = ctx.alloc_count()
+                while not fatal:
+                    with lock:
+                        i = nxt[0]
+                        nxt[0] += 1
+                    if i >= n:
+                        break
+                    one = batch.slice(i, i + 1)
+                    try:
+                        out = ctx.dock(dp, pack(one), cfg, seed, FAMILY_LATENCY, coords=True)
+                    except model.DockscreenError as e:   # per-ligand error: record, continue
+                        res[i]["status"] = NOT_DOCKED
+                        with lock:
+                            errors.append((int(seq_of_row[i]), batch.ids[i], f"{type(e).__name__}: {e}"))
+                        continue
+                    res[i] = out.results[0]
+                    a, b = int(batch.atom_off[i]), int(batch.atom_off[i + 1])
+                    coords[a:b] = out.best_coords
+                    f, g = int(batch.frag_off[i]), int(batch.frag_off[i + 1])
+                    tors[f:g] = out.best_torsion
                     with lock:
                         dev_ms[0] += out.stats.total_ms
-                except model.DockscreenError as e:
-                    with lock:
-                        errors.append((i, lig.id, f"{type(e).__name__}: {e}"))
-            with lock:
-                allocs.append(ctx.alloc_count() - a0)
+                with lock:
+                    allocs.append(ctx.alloc_count() - a0)
+            except BaseException as e:  # configuration / device errors end the run (re-raised below)
+                with lock:
+                    fatal.append(e)
 
         th = [threading.Thread(target=worker, args=(w,)) for w in range(workers)]
         for t in th:
             t.start()
         for t in th:
             t.join()
-        rep = _finish(n, slots, errors, model.Counters(), t0, dev_ms[0])
+        if fatal:
+            raise fatal[0]
+        rep = _finish_arrays(n_in, seq_of_row, batch.ids, res, coords, batch.atom_off, tors, batch.frag_off, errors,
+                             model.Counters(), t0, dev_ms[0])
         rep.workspace_allocations = workspaces[0]     # == workers (SPEC.md:399)
         rep.extra_allocations = sum(allocs)           # allocations after the reserve: 0
         return rep
 
 
-def bucket_accounting(n_atoms: np.ndarray, n_frags: np.ndarray,
-                      capacities: Optional[Mapping[int, int]] = None) -> model.Counters:
-    """The batches the bucketizer detaches for ligands of these sizes, without
-    pushing them one by one: per bucket ceil(count / capacity) batches; full ones record a fill
-    ratio of 1.0 as they are detached, the partial ones at flush (sorted by key, after every full
-    batch) count / capacity — the same sums, in the same order, as Bucketizer.push + flush."""
-    counters = model.Counters()
-    na = np.asarray(n_atoms, np.int64)
-    nf = np.asarray(n_frags, np.int64)
-    if len(na) == 0:
-        return counters
-    keys = ((na - 1) // 32) * 1_000_000 + nf // 4
-    uk, cnt = np.unique(keys, return_counts=True)
-    full, partial = 0, []
-    for k, c in zip(uk.tolist(), cnt.tolist()):
-        cap = bucket_capacity(BucketKey(k // 1_000_000, k % 1_000_000), capacities)
-        counters.batches_dispatched += -(-c // cap)
-        full += c // cap
-        if c % cap:
-            partial.append((c % cap) / cap)
-    counters.batch_fill_ratio_sum = 0.0
-    for _ in range(full):
-        counters.batch_fill_ratio_sum += 1.0
-    for r in partial:
-        counters.batch_fill_ratio_sum += r
-    return counters
+# ---- batched engine ----------------------------------------------------------------------------
+_POOL_LOCK = threading.Lock()
+_DISPATCH_POOL: Dict[Tuple[int, int], "_Dispatcher"] = {}
+
+
+class _Dispatcher:
+    """One dispatcher slot: a ds_ctx (own CUDA stream + workspaces) on one device and pinned staging
+    for the batches it cuts out of the packed stream.  Kept across runs (allocate once
+    in the lifetime of the thread); a run holds the slot's lock while it uses it."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.ctx = Context(device)
+        self.lock = threading.Lock()
+        self.bufs: Dict[str, np.ndarray] = {}
+
+    def buf(self, name: str, shape, dtype) -> np.ndarray:
+        count = int(np.prod(shape))
+        b = self.bufs.get(name)
+        if b is None or b.size < count or b.dtype != np.dtype(dtype):
+            b = pinned_empty(max(count * 3 // 2, 1), dtype)
+            self.bufs[name] = b
+        return b[:count].reshape(shape)
+
+
+class _StreamArena:
+    """Pinned arrays for a run's packed stream, kept across runs (page-locking hundreds of MB costs
+    far more than packing into it); a run holds the arena while it uses it, a concurrent run gets
+    a fresh one."""
+
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.bufs: Dict[str, np.ndarray] = {}
+
+    def get(self, name: str, shape, dtype) -> np.ndarray:
+        count = int(np.prod(shape))
+        b = self.bufs.get(name)
+        if b is None or b.size < count or b.dtype != np.dtype(dtype):
+            b = pinned_empty(max(count * 5 // 4, 1), dtype)
+            self.bufs[name] = b
+        return b[:count].reshape(shape)
+
+
+_ARENA = _StreamArena()
+
+
+def _dispatcher(device: int, slot: int) -> _Dispatcher:
+    with _POOL_LOCK:
+        d = _DISPATCH_POOL.get((device, slot))
+        if d is None:
+            d = _DISPATCH_POOL[(device, slot)] = _Dispatcher(device)
+        return d
+
+
+def _csr_gather(sel: np.ndarray, src_off: np.ndarray, src: np.ndarray, elem: int, disp: _Dispatcher, name: str,
+                row_shape: tuple, dtype):
+    L = lib()
+    off = disp.buf(name + "_off", (len(sel) + 1,), np.int32)
+    check(L.ds_csr_gather(len(sel), _p(sel), _p(src_off), None, elem, _p(off), None))
+    total = int(off[-1])
+    dst = disp.buf(name, (max(total, 1),) + row_shape, dtype)
+    if total:
+        check(L.ds_csr_gather(len(sel), _p(sel), _p(src_off), _p(src), elem, _p(off), _p(dst)))
+    return off, dst[:total]
 
 
 class batched_engine:  # noqa: N801
     @staticmethod
-    def run(stream: Iterable[model.Ligand], pocket: model.Pocket, cfg: model.DockConfig = model.DockConfig(),
+    def run(stream: Stream, pocket: model.Pocket, cfg: model.DockConfig = model.DockConfig(),
             workers: int = 1, seed: int = 0, table: Optional[InteractionTable] = None,
-            capacities: Optional[Mapping[int, int]] = None, devices: Sequence[int] = (0,)) -> EngineReport:
-        """producers -> bucketizer -> dispatcher; flush at end of stream.
+            capacities: Union[None, str, Mapping[int, int]] = None, devices: Sequence[int] = (0,),
+            dispatchers_per_device: int = 3, chunk: int = 8192) -> EngineReport:
+        """producers -> bucketizer -> dispatchers; flush at end of stream.
 
-        On B200 the stages run in bulk: the stream is flattened and validated natively
-        (validate_ligand semantics, all host cores), the bucketizer's batch accounting is computed
-        from the bucket keys (the same batches_dispatched and fill-ratio sum the per-ligand
-        Bucketizer produces), and each device docks its contiguous share of the valid ligands in
-        one pipelined ds_dock call (the batched kernels balance mixed sizes themselves, LPT order).
-        Results are per-ligand deterministic, so they are identical to per-bucket dispatch."""
-        if workers < 1:
+        capacities: None = SPEC.md:332's fixed per-range capacities; "device" = the occupancy-derived
+        capacities of this B200 (ds_query_capacity); or a {range: capacity} map.
+        workers = producer threads (validation, packing, classification, push)."""
+        if workers < 1 or dispatchers_per_device < 1:
             raise ValueError("workers must be positive")
-        ligs = list(stream)
-        n = len(ligs)
         t0 = time.perf_counter()
-        batch, codes = LigandBatch.from_ligands_validated(ligs)
-        errors: list = []
-        for i in np.nonzero(codes)[0]:
-            try:
-                model.validate_ligand(ligs[i])          # the reference's exact message
-                msg = f"IndexOutOfRange: {ligs[i].id}: invalid ligand"
-            except model.DockscreenError as e:
-                msg = f"{type(e).__name__}: {e}"
-            errors.append((int(i), ligs[i].id, msg))
-        ok = np.nonzero(codes == 0)[0]
-        counters = bucket_accounting(np.diff(batch.atom_off), np.diff(batch.frag_off), capacities)
-        slots: list = [None] * n
-        dev_ms = [0.0]
+        batch, seq_of_row, errors, n_in = _validated(stream)
+        tm = {"validated": time.perf_counter() - t0}
+        n = batch.n
+        na, nf = (int(batch.atom_off[-1]), int(batch.frag_off[-1])) if n else (0, 0)
+        slots = [_dispatcher(d, k) for d in devices for k in range(dispatchers_per_device)]
+        if capacities == "device":
+            capacities = device_capacities(slots[0].ctx)
+        bucketizer = Bucketizer(capacities)
+        # the packed stream (pinned: batches are cut out of it natively) and the result arrays
+        ao = np.ascontiguousarray(batch.atom_off, np.int32)
+        fo = np.ascontiguousarray(batch.frag_off, np.int32)
+        arena = _ARENA if _ARENA.lock.acquire(blocking=False) else _StreamArena()
+        xyzt = arena.get("xyzt", (max(na, 1), 4), np.float32)
+        fdesc = arena.get("fdesc", (max(nf, 1), FRAG_WORDS), np.uint32)
+        idh = np.empty(max(n, 1), np.uint64)
+        cen = np.empty((max(n, 1), 3), np.float32)
+        res = np.zeros(max(n, 1), RESULT_DTYPE)[:n]
+        coords = np.empty((max(na, 1), 3), np.float32)     # every row is written by its batch
+        tors = np.empty(max(nf, 1), np.uint8)
+        xyz = np.ascontiguousarray(batch.atom_xyz, np.float32)
+        typ = np.ascontiguousarray(batch.atom_type, np.uint8)
+        fax = np.ascontiguousarray(batch.frag_axis, np.int32) if nf else np.zeros((1, 2), np.int32)
+        fm = np.ascontiguousarray(batch.frag_mask, np.uint32) if nf else np.zeros((1, MASK_WORDS), np.uint32)
+        ids_blob, id_off = batch.id_bytes() if n else (b"", np.zeros(1, np.int64))
+        idbuf = C.create_string_buffer(ids_blob, max(len(ids_blob), 1))
+        id_off = np.ascontiguousarray(id_off, np.int64)
+        tm["allocated"] = time.perf_counter() - t0
+        rng_key = ((np.diff(ao) - 1) // 32).astype(np.int64) * 1_000_000 + np.diff(fo).astype(np.int64) // 4
+        valid = np.ones(max(n, 1), bool)[:n]
+
+        dq: "queue.Queue" = queue.Queue()
         lock = threading.Lock()
-        nd = max(1, min(len(devices), len(ok)))
-        bounds = [len(ok) * d // nd for d in range(nd + 1)]
+        log: List[dict] = []
+        dev_ms = [0.0]
+        fatal: list = []
+        nxt = [0]
+        L = lib()
 
-        def dispatcher(d: int):
-            lo, hi = bounds[d], bounds[d + 1]
-            if hi <= lo:
+        def pack_range(lo: int, hi: int) -> None:
+            """Validate + pack ligands [lo, hi) in place into the stream arrays; a bad ligand is
+            recorded and left out of the buckets."""
+            bad = C.c_int32(-1)
+            rc = L.ds_pack_ligands(hi - lo, _p(ao[lo:]), _p(xyz), _p(typ), _p(fo[lo:]), _p(fax), _p(fm),
+                                   C.cast(idbuf, C.c_void_p), _p(id_off[lo:]), _p(xyzt), _p(fdesc), _p(idh[lo:]),
+                                   _p(cen[lo:]), C.byref(bad))
+            if rc == DS_OK:
                 return
-            ctx = thread_context(devices[d])
-            dp = _pockets.get(ctx, pocket, table)
-            sub = batch.slice(lo, hi)
-            out = ctx.dock(dp, pack(sub), cfg, seed, FAMILY_BATCHED, coords=True)
-            with lock:
-                dev_ms[0] += out.stats.total_ms
-            for seq, r in zip(ok[lo:hi].tolist(), results_from_output(sub, out, cfg)):
-                slots[seq] = r
+            for i in range(lo, hi):   # cold path: find every bad ligand of the chunk
+                rc = L.ds_pack_ligands(1, _p(ao[i:]), _p(xyz), _p(typ), _p(fo[i:]), _p(fax), _p(fm),
+                                       C.cast(idbuf, C.c_void_p), _p(id_off[i:]), _p(xyzt), _p(fdesc), _p(idh[i:]),
+                                       _p(cen[i:]), C.byref(bad))
+                if rc != DS_OK:
+                    valid[i] = False
+                    res[i]["status"] = NOT_DOCKED
+                    exc = ERRORS.get(rc, DsError)
+                    with lock:
+                        errors.append((int(seq_of_row[i]), batch.ids[i], f"{exc.__name__}: {batch.ids[i]}: invalid"))
 
-        disp = [threading.Thread(target=dispatcher, args=(d,)) for d in range(nd)]
+        def producer() -> None:
+            try:
+                while not fatal:
+                    with lock:
+                        lo = nxt[0]
+                        nxt[0] += chunk
+                    if lo >= n:
+                        return
+                    hi = min(n, lo + chunk)
+                    pack_range(lo, hi)
+                    idx = np.arange(lo, hi, dtype=np.int32)
+                    keys = rng_key[lo:hi]
+                    if not valid[lo:hi].all():
+                        idx, keys = idx[valid[lo:hi]], keys[valid[lo:hi]]
+                    order = np.argsort(keys, kind="stable")
+                    uk, start = np.unique(keys[order], return_index=True)
+                    bounds = list(start) + [len(order)]
+                    for k, key in enumerate(uk.tolist()):
+                        bk = BucketKey(key // 1_000_000, key % 1_000_000)
+                        for b in bucketizer.push_many(bk, idx[order[bounds[k]:bounds[k + 1]]]):
+                            dq.put(("full", b, time.perf_counter()))
+            except BaseException as e:
+                with lock:
+                    fatal.append(e)
+
+        def dispatch(slot: _Dispatcher) -> None:
+            with slot.lock:
+                try:
+                    ctx = slot.ctx
+                    dp = _pockets.get(ctx, pocket, table)
+                    while True:
+                        item = dq.get()
+                        if item is None:
+                            return
+                        if fatal:
+                            continue
+                        kind, b, t_detached = item
+                        t_start = time.perf_counter()
+                        sel = np.ascontiguousarray(b.seqs, np.int32)
+                        s_ao, s_xyzt = _csr_gather(sel, ao, xyzt, 16, slot, "xyzt", (4,), np.float32)
+                        s_fo, s_fd = _csr_gather(sel, fo, fdesc, 32, slot, "frag", (FRAG_WORDS,), np.uint32)
+                        s_idh = slot.buf("idh", (len(sel),), np.uint64)
+                        np.take(idh, sel, out=s_idh)
+                        sub = PackedBatch(len(sel), s_ao, s_xyzt, s_fo, s_fd, s_idh, None)
+                        out = ctx.dock(dp, sub, cfg, seed, FAMILY_BATCHED, coords=True)
+                        res[sel] = out.results
+                        if int(s_ao[-1]):
+                            check(L.ds_csr_scatter(len(sel), _p(sel), _p(s_ao), _p(out.best_coords), 12, _p(ao),
+                                                   _p(coords)))
+                        if int(s_fo[-1]):
+                            check(L.ds_csr_scatter(len(sel), _p(sel), _p(s_fo), _p(out.best_torsion), 1, _p(fo),
+                                                   _p(tors)))
+                        t_end = time.perf_counter()
+                        with lock:
+                            dev_ms[0] += out.stats.total_ms
+                            log.append({"key": (b.key.atom_range_index, b.key.fragment_group_index), "kind": kind,
+                                        "size": len(sel), "capacity": b.capacity, "detached": t_detached - t0,
+                                        "started": t_start - t0, "finished": t_end - t0, "device": slot.device,
+                                        "device_ms": out.stats.total_ms})
+                except BaseException as e:  # configuration / device errors end the run (re-raised below)
+                    with lock:
+                        fatal.append(e)
+
+        disp = [threading.Thread(target=dispatch, args=(s,)) for s in slots]
         for t in disp:
             t.start()
+        prod = [threading.Thread(target=producer) for _ in range(workers)]
+        for t in prod:
+            t.start()
+        for t in prod:
+            t.join()
+        t_flush = time.perf_counter()
+        tm["produced"] = t_flush - t0
+        for b in bucketizer.flush():           # end of stream: partial batches (SPEC.md:352)
+            dq.put(("flush", b, t_flush))
+        for _ in disp:
+            dq.put(None)
         for t in disp:
             t.join()
-        return _finish(n, slots, errors, counters, t0, dev_ms[0])
+        if arena is _ARENA:
+            _ARENA.lock.release()
+        tm["docked"] = time.perf_counter() - t0
+        if fatal:
+            raise fatal[0]
+        log.sort(key=lambda e: e["started"])
+        rep = _finish_arrays(n_in, seq_of_row, batch.ids, res, coords, ao, tors, fo, errors, bucketizer.counters, t0,
+                             dev_ms[0])
+        rep.dispatch_log = log
+        rep.dispatchers = len(slots)
+        tm["finished"] = time.perf_counter() - t0
+        rep.timings = tm
+        return rep

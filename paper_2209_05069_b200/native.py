@@ -133,6 +133,8 @@ def lib():
             "ds_validate_ligands": (C.c_int, [i32] + [vp] * 10),
             "ds_generate_resident": (C.c_int, [vp, i64, i64, i32, vp, vp, vp]),
             "ds_batch_read_inputs": (C.c_int, [vp, vp, vp, vp, vp]),
+            "ds_csr_gather": (C.c_int, [i32, vp, vp, vp, i32, vp, vp]),
+            "ds_csr_scatter": (C.c_int, [i32, vp, vp, vp, i32, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

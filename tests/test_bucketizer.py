@@ -112,21 +112,59 @@ def test_classify_stable(shapes):
         assert k.atom_range_index == (a - 1) // 32 and k.fragment_group_index == f // 4
 
 
-def test_bulk_bucket_accounting_matches_bucketizer():
-    """engines.bucket_accounting (the batched engine's bulk path) == pushing every ligand through
-    the Bucketizer and flushing: batches_dispatched and the fill-ratio sum, bit for bit."""
+def test_push_many_equals_push_one_by_one():
+    """Bucketizer.push_many (the batched engine's bulk push of a chunk's ligands per key) detaches
+    the same full batches, with the same members in the same order, as pushing one by one; the
+    flushed partials and the counters agree too."""
     import numpy as np
-    from paper_2209_05069_b200 import io
     from paper_2209_05069_b200.bucketizer import Bucketizer, classify_counts
-    from paper_2209_05069_b200.engines import bucket_accounting
     rng = np.random.default_rng(4)
     for caps in (None, {0: 7, 1: 13, 2: 5, 3: 3, 4: 2}):
         na = rng.integers(1, 161, size=3000)
         nf = rng.integers(0, 30, size=3000)
-        bz = Bucketizer(caps)
-        for i, (a, f) in enumerate(zip(na.tolist(), nf.tolist())):
-            bz.push(object(), classify_counts(a, f), seq=i)
-        bz.flush()
-        c = bucket_accounting(na, nf, caps)
-        assert c.batches_dispatched == bz.counters.batches_dispatched
-        assert c.batch_fill_ratio_sum == bz.counters.batch_fill_ratio_sum
+        keys = [classify_counts(a, f) for a, f in zip(na.tolist(), nf.tolist())]
+        one, bulk = Bucketizer(caps), Bucketizer(caps)
+        full_one = [b for i, k in enumerate(keys) if (b := one.push(i, k, seq=i)) is not None]
+        full_bulk = []
+        for lo in range(0, 3000, 257):   # chunks, each pushed per key in stream order
+            ks = keys[lo:lo + 257]
+            for k in sorted(set(ks)):
+                idx = np.array([lo + j for j, kk in enumerate(ks) if kk == k], np.int64)
+                full_bulk += bulk.push_many(k, idx)
+        by_key = lambda bs: sorted(((b.key, list(b.ligands or b.seqs)) for b in bs), key=lambda t: (t[0], t[1][0]))
+        assert by_key(full_one) == by_key(full_bulk)
+        assert all(len(b) == b.capacity for b in full_bulk)
+        assert by_key(one.flush()) == by_key(bulk.flush())
+        assert one.counters.batches_dispatched == bulk.counters.batches_dispatched
+        assert one.counters.batch_fill_ratio_sum == bulk.counters.batch_fill_ratio_sum
+
+
+def test_push_many_concurrent_partition_law():
+    """8 producers bulk-push chunks concurrently: every index in exactly one batch, batches homogeneous."""
+    import numpy as np
+    from paper_2209_05069_b200.bucketizer import Bucketizer, BucketKey
+    b = Bucketizer({0: 97, 1: 61, 2: 43, 3: 29, 4: 13})
+    n = 60_000
+    key = lambda i: BucketKey((i * 7) % 5, (i * 3) % 6)
+    out, lock = [], threading.Lock()
+
+    def producer(w):
+        mine = []
+        for lo in range(w * 1000, n, 8000):
+            idx = np.arange(lo, min(n, lo + 1000))
+            for k in {key(i) for i in idx.tolist()}:
+                mine += b.push_many(k, np.array([i for i in idx.tolist() if key(i) == k]))
+        with lock:
+            out.extend(mine)
+
+    th = [threading.Thread(target=producer, args=(w,)) for w in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    out.extend(b.flush())
+    seen = sorted(int(x) for bt in out for x in bt.seqs)
+    assert seen == list(range(n))
+    for bt in out:
+        assert {key(int(i)) for i in bt.seqs} == {bt.key} and len(bt) <= bt.capacity
+    assert b.counters.batches_dispatched == len(out)

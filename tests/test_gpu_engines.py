@@ -70,3 +70,91 @@ def test_batched_engine_fill_ratio(synth_pocket, table):
     assert rep.counters.batches_dispatched == 1
     assert abs(rep.counters.batch_fill_ratio_sum - 10 / 1920) < 1e-12
     assert len(rep.results) + len(rep.errors) == 10
+
+
+def test_batched_engine_ligandbatch_fast_path_equals_ds_dock(synth_pocket, table):
+    """batched_engine.run on a LigandBatch stream (zero-object path: native pack per producer chunk,
+    bulk bucket push, dispatchers cutting batches out of the packed stream) gives ds_dock's records,
+    best poses and torsions for every ligand, with SPEC, small and device capacities."""
+    from paper_2209_05069_b200 import native
+    from paper_2209_05069_b200.native import FAMILY_BATCHED, pack
+    b = io.generate_mixed_batch(6000, seed=21)
+    cfg = model.DockConfig()
+    ref = docking.dock_batch(b, synth_pocket, cfg, seed=2, table=table)
+    for caps, workers in ((None, 1), ({0: 333, 1: 257, 2: 100, 3: 64, 4: 32}, 4), ("device", 3)):
+        rep = engines.batched_engine.run(b, synth_pocket, cfg, workers=workers, seed=2, table=table,
+                                         capacities=caps, chunk=1000)
+        rec = rep.records
+        assert np.array_equal(rec["results"], ref.results), caps
+        assert np.array_equal(rec["best_coords"][:len(ref.best_coords)], ref.best_coords)
+        assert np.array_equal(rec["best_torsion"][:len(ref.best_torsion)], ref.best_torsion)
+        assert len(rep.results) + len(rep.errors) == b.n
+        assert sum(e["size"] for e in rep.dispatch_log) == b.n
+        assert rep.counters.batches_dispatched == len(rep.dispatch_log)
+
+
+def test_batched_engine_dispatch_log_monotone(synth_pocket, table):
+    """the batched engine never begins a batch before it is full or flushed — per
+    bucket the dispatch log is monotone (detach <= start, full batches of exactly capacity before
+    the flushed partial), and the observed counters match the log."""
+    b = io.generate_mixed_batch(5000, seed=22)
+    caps = {0: 97, 1: 61, 2: 43, 3: 29, 4: 13}
+    rep = engines.batched_engine.run(b, synth_pocket, model.DockConfig(), workers=4, table=table, capacities=caps,
+                                     chunk=700)
+    per = {}
+    for e in rep.dispatch_log:
+        assert e["started"] >= e["detached"] and e["finished"] >= e["started"]
+        per.setdefault(e["key"], []).append(e)
+    for key, es in per.items():
+        es.sort(key=lambda e: e["detached"])
+        kinds = [e["kind"] for e in es]
+        assert kinds.count("flush") <= 1 and (kinds[-1] == "flush" or "flush" not in kinds)
+        assert all(e["size"] == caps[key[0]] for e in es if e["kind"] == "full")
+        assert all(0 < e["size"] <= caps[key[0]] for e in es)
+    fill = sum(e["size"] / e["capacity"] for e in rep.dispatch_log)
+    assert abs(rep.counters.batch_fill_ratio_sum - fill) < 1e-9
+    assert rep.counters.batches_dispatched == len(rep.dispatch_log)
+
+
+def test_batched_engine_homogeneous_capacity_example(synth_pocket, table):
+    """a homogeneous stream of 3840 small ligands -> 2 full batches, fill ratio 1.0."""
+    b = io.generate_dataset_batch(10, 1, 3840, seed=5)
+    rep = engines.batched_engine.run(b, synth_pocket, model.DockConfig(), workers=2, table=table)
+    assert rep.counters.batches_dispatched == 2
+    assert rep.counters.batch_fill_ratio_sum == 2.0
+    assert all(e["kind"] == "full" and e["size"] == 1920 for e in rep.dispatch_log)
+
+
+def test_device_capacities_from_occupancy(gpu_ctx):
+    """ds_query_capacity: occupancy-derived, identical for every range (the kernels are not
+    range-specialised), a multiple of the SM count."""
+    import torch
+    from paper_2209_05069_b200.bucketizer import device_capacities
+    caps = device_capacities(gpu_ctx)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert set(caps) == {0, 1, 2, 3, 4} and len(set(caps.values())) == 1
+    c = caps[0]
+    assert c > 0 and c % sms == 0 and c >= sms * 8
+
+
+def test_engines_record_invalid_ligands_and_continue(synth_pocket, table):
+    """Per-ligand validation errors are recorded with their input sequence and the stream continues
+    (SPEC.md:395, 405); both engines agree."""
+    ligs = io.generate_dataset(12, 2, 6, seed=8)
+    bad = model.Ligand("too_many", tuple(model.Atom.of(i, 0, 0, 1) for i in range(161)))
+    stream = ligs[:2] + [bad] + ligs[2:]
+    for run in (engines.batched_engine.run, engines.latency_engine.run):
+        rep = run(stream, synth_pocket, model.DockConfig(), workers=2, table=table)
+        assert [e[:2] for e in rep.errors] == [(2, "too_many")]
+        assert [r.ligand_id for r in rep.results] == [l.id for l in ligs]
+
+
+def test_engine_fatal_config_error_raises(synth_pocket, table):
+    """A configuration the device rejects (alignment_step_deg=1: 360^2 rotations exceed the 16-bit
+    argmax key) is fatal: run() raises instead of returning a short report."""
+    from paper_2209_05069_b200.native import DsError
+    ligs = io.generate_dataset(12, 2, 3, seed=8)
+    cfg = model.DockConfig(alignment_step_deg=1)
+    for run in (engines.batched_engine.run, engines.latency_engine.run):
+        with pytest.raises(DsError):
+            run(ligs, synth_pocket, cfg, workers=2, table=table)
