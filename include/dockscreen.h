@@ -228,6 +228,23 @@ int ds_op_rescore(ds_ctx *ctx, const ds_pocket *pocket, const float *coords,
                   const uint8_t *types, int n_atoms, int n_poses, float cutoff,
                   int64_t *out_chem_fx);
 
+/* apply_rigid of n_poses poses, coordinates in Å: p' = m (p - c) + c with the
+ * pinned recipe w = p - c, p'_i = fma(m_i2, w_z, fma(m_i1, w_y, fma(m_i0, w_x, c_i))).  m: 9 floats
+ * (row-major) per pose, center: 3 per pose. */
+int ds_op_apply_rigid(ds_ctx *ctx, const float *coords, int n_atoms, int n_poses, const float *m,
+                      const float *center, float *out);
+/* apply_torsion of one fragment (axis atoms, 5-word moving mask) by angle_deg on
+ * n_poses poses in Å (DESIGN.md §3 P8, eps = 1e-9 Å); status[p] = 0, or DS_STATUS_DEGENERATE_AXIS
+ * with the pose unchanged.  Angle 0 leaves every coordinate bitwise unchanged. */
+int ds_op_apply_torsion(ds_ctx *ctx, const float *coords, int n_atoms, int n_poses, int axis_begin,
+                        int axis_end, const uint32_t *mask, int angle_deg, float *out, int32_t *status);
+/* bump_check of one fragment on n_poses poses in Å (P9, bd2 = f32(bump_distance^2)):
+ * bump[p] = 1 iff a moving atom lies closer than bump_distance to a non-moving, non-axis atom;
+ * pairs[p] = pair evaluations of the sequential scan (early_exit: up to the first bump). */
+int ds_op_bump_check(ds_ctx *ctx, const float *coords, int n_atoms, int n_poses, int axis_begin,
+                     int axis_end, const uint32_t *mask, float bump_distance, int early_exit, uint8_t *bump,
+                     int64_t *pairs);
+
 /* ---- host-side helpers (input makers and packing; not on the timed path) - */
 /* FNV-1a-64 of the id bytes (keys the starting-pose PRNG, DESIGN.md §3 P5). */
 uint64_t ds_ligand_id_hash(const char *id, size_t len);

@@ -369,7 +369,7 @@ static int dock_restart(const or_lig *L, const or_pk *k, const or_config *cfg, i
 /* dock_ligand; inner_threads > 1 runs the restarts on an inner pool (the latency engine's
  * pose-level parallelism) with results identical to the sequential loop. */
 static int dock_ligand_impl(const or_lig *L, const or_pk *k, const or_config *cfg, or_result *res, or_restart *rr,
-                            uint8_t *tors, float *best_xyz, int inner_threads) {
+                            uint8_t *tors, float *best_xyz, int inner_threads, float *restart_xyz) {
   trig_init();
   const int N = cfg->restarts_n;
   const double thr = (double)cfg->similarity_rmsd / (double)k->p->spacing;
@@ -481,13 +481,18 @@ static int dock_ligand_impl(const or_lig *L, const or_pk *k, const or_config *cf
   if (best_xyz)
     for (int i = 0; i < L->A; ++i)
       for (int c = 0; c < 3; ++c) best_xyz[3 * i + c] = fmaf(U[best_r][i][c], k->p->spacing, k->p->origin[c]);
+  if (restart_xyz) /* every restart's final pose in Å (N x A x 3), for tests of the rescore semantics */
+    for (int r = 0; r < N; ++r)
+      for (int i = 0; i < L->A; ++i)
+        for (int c = 0; c < 3; ++c)
+          restart_xyz[3 * ((size_t)r * L->A + i) + c] = fmaf(U[r][i][c], k->p->spacing, k->p->origin[c]);
   return 0;
 #undef U
 }
 
 int or_dock_ligand(const or_lig *L, const or_pk *k, const or_config *cfg, or_result *res, or_restart *rr,
                    uint8_t *tors /* F*N: [f*N + r] */, float *best_xyz /* A*3 Å, may be NULL */) {
-  return dock_ligand_impl(L, k, cfg, res, rr, tors, best_xyz, 1);
+  return dock_ligand_impl(L, k, cfg, res, rr, tors, best_xyz, 1, NULL);
 }
 
 /* P2: c0 = f32(f64 sequential mean), d = f32(p - c0) */
@@ -558,7 +563,7 @@ int or_dock_batch_latency(int n, const int32_t *atom_off, const float *atom_xyz,
              frag_off[i + 1] - frag_off[i], frag_axis + 2 * (size_t)frag_off[i],
              frag_mask + (size_t)OR_MASK_WORDS * frag_off[i], ids + id_off[i], (size_t)(id_off[i + 1] - id_off[i]));
     dock_ligand_impl(&L, k, cfg, res + i, rr ? rr + (size_t)i * N : NULL, tors ? tors + (size_t)frag_off[i] * N : NULL,
-                     best_xyz ? best_xyz + 3 * (size_t)atom_off[i] : NULL, threads > 1 ? threads : 1);
+                     best_xyz ? best_xyz + 3 * (size_t)atom_off[i] : NULL, threads > 1 ? threads : 1, NULL);
   }
   pk_free(k);
   free(k);
@@ -610,4 +615,102 @@ void or_rot(int axis, int deg, float *m) {
   if (axis == 0) rot_x(((deg % 360) + 360) % 360, m);
   else if (axis == 1) rot_y(((deg % 360) + 360) % 360, m);
   else rot_z(((deg % 360) + 360) % 360, m);
+}
+
+/* ---------------------------------------------------------------- the other L2 ops of the native
+ * slot in Å, pinned like the docking recipe: each pose of n atoms is 3n floats. */
+/* SPEC.md:135 apply_rigid: p' = m (p - c) + c, w = p - c, p'_i = fma(m_i2, w_z, fma(m_i1, w_y, fma(m_i0, w_x, c_i))) */
+void or_apply_rigid(int n_atoms, int n_poses, const float *coords, const float *m /* 9 per pose */,
+                    const float *center /* 3 per pose */, float *out) {
+  for (int p = 0; p < n_poses; ++p) {
+    const float *M = m + 9 * p, *c = center + 3 * p;
+    for (int i = 0; i < n_atoms; ++i) {
+      const float *q = coords + 3 * ((size_t)p * n_atoms + i);
+      float *o = out + 3 * ((size_t)p * n_atoms + i);
+      float wx = q[0] - c[0], wy = q[1] - c[1], wz = q[2] - c[2];
+      o[0] = fmaf(M[2], wz, fmaf(M[1], wy, fmaf(M[0], wx, c[0])));
+      o[1] = fmaf(M[5], wz, fmaf(M[4], wy, fmaf(M[3], wx, c[1])));
+      o[2] = fmaf(M[8], wz, fmaf(M[7], wy, fmaf(M[6], wx, c[2])));
+    }
+  }
+}
+
+/* SPEC.md:145 apply_torsion in Å (P8 with eps = f32(1e-9 Å)); status[p] = 0 or 2 (DegenerateAxis,
+ * pose left unchanged) */
+void or_apply_torsion(int n_atoms, int n_poses, const float *coords, int ab, int ae, const uint32_t mask[5],
+                      int deg, float *out, int32_t *status) {
+  trig_init();
+  deg = ((deg % 360) + 360) % 360;
+  for (int p = 0; p < n_poses; ++p) {
+    const float(*u)[3] = (const float(*)[3])(coords + 3 * (size_t)p * n_atoms);
+    float(*o)[3] = (float(*)[3])(out + 3 * (size_t)p * n_atoms);
+    memcpy(o, u, sizeof(float) * 3 * n_atoms);
+    float vx = u[ae][0] - u[ab][0], vy = u[ae][1] - u[ab][1], vz = u[ae][2] - u[ab][2];
+    float len = sqrtf(fmaf(vz, vz, fmaf(vy, vy, vx * vx)));
+    status[p] = !(len >= 1e-9f) ? 2 : 0;
+    if (status[p] || deg == 0) continue;
+    float R[9];
+    torsion_matrix(vx / len, vy / len, vz / len, deg, R);
+    const float *a = u[ab];
+    for (int i = 0; i < n_atoms; ++i) {
+      if (!in_mask(mask, i)) continue;
+      float wx = u[i][0] - a[0], wy = u[i][1] - a[1], wz = u[i][2] - a[2];
+      o[i][0] = fmaf(R[2], wz, fmaf(R[1], wy, fmaf(R[0], wx, a[0])));
+      o[i][1] = fmaf(R[5], wz, fmaf(R[4], wy, fmaf(R[3], wx, a[1])));
+      o[i][2] = fmaf(R[8], wz, fmaf(R[7], wy, fmaf(R[6], wx, a[2])));
+    }
+  }
+}
+
+/* SPEC.md:193 bump_check in Å: bd2 = f32(bump_distance^2 in f64); pairs[p] = pair evaluations of
+ * the sequential scan (i in mask ascending x j in the complement minus the axis atoms ascending) */
+void or_bump_check(int n_atoms, int n_poses, const float *coords, int ab, int ae, const uint32_t mask[5],
+                   float bump_distance, int early_exit, uint8_t *bump, int64_t *pairs) {
+  const float bd2 = (float)((double)bump_distance * (double)bump_distance);
+  for (int p = 0; p < n_poses; ++p) {
+    const float(*u)[3] = (const float(*)[3])(coords + 3 * (size_t)p * n_atoms);
+    int64_t n = 0;
+    int hit = 0;
+    for (int i = 0; i < n_atoms && !(hit && early_exit); ++i) {
+      if (!in_mask(mask, i)) continue;
+      for (int j = 0; j < n_atoms; ++j) {
+        if (in_mask(mask, j) || j == ab || j == ae) continue;
+        float dx = u[i][0] - u[j][0], dy = u[i][1] - u[j][1], dz = u[i][2] - u[j][2];
+        ++n;
+        if (fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < bd2) {
+          hit = 1;
+          if (early_exit) break;
+        }
+      }
+    }
+    bump[p] = (uint8_t)hit;
+    pairs[p] = n;
+  }
+}
+
+/* or_dock_batch plus every restart's final pose in Å: restart_xyz[(atom_off[i] * N + r * A_i + a) * 3 + c] */
+int or_dock_batch_poses(int n, const int32_t *atom_off, const float *atom_xyz, const uint8_t *atom_type,
+                        const int32_t *frag_off, const int32_t *frag_axis, const uint32_t *frag_mask, const char *ids,
+                        const int64_t *id_off, const or_pocket *pocket, const or_config *cfg, int threads,
+                        or_result *res, or_restart *rr, uint8_t *tors, float *best_xyz, float *restart_xyz) {
+  trig_init();
+  or_pk *k = (or_pk *)malloc(sizeof(or_pk));
+  if (pk_init(k, pocket)) {
+    free(k);
+    return -1;
+  }
+  const int N = cfg->restarts_n;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads > 0 ? threads : 1)
+  for (int i = 0; i < n; ++i) {
+    or_lig L;
+    lig_init(&L, atom_off[i + 1] - atom_off[i], atom_xyz + 3 * (size_t)atom_off[i], atom_type + atom_off[i],
+             frag_off[i + 1] - frag_off[i], frag_axis + 2 * (size_t)frag_off[i],
+             frag_mask + (size_t)OR_MASK_WORDS * frag_off[i], ids + id_off[i], (size_t)(id_off[i + 1] - id_off[i]));
+    dock_ligand_impl(&L, k, cfg, res + i, rr ? rr + (size_t)i * N : NULL, tors ? tors + (size_t)frag_off[i] * N : NULL,
+                     best_xyz ? best_xyz + 3 * (size_t)atom_off[i] : NULL, 1,
+                     restart_xyz + 3 * (size_t)atom_off[i] * N);
+  }
+  pk_free(k);
+  free(k);
+  return 0;
 }

@@ -63,6 +63,15 @@ def lib():
         L.or_rot.argtypes = [C.c_int, C.c_int, vp]
         L.or_fnv1a64.restype = C.c_uint64
         L.or_fnv1a64.argtypes = [C.c_char_p, C.c_size_t]
+        L.or_dock_batch_poses.restype = C.c_int
+        L.or_dock_batch_poses.argtypes = [C.c_int] + [vp] * 10 + [C.c_int, vp, vp, vp, vp, vp]
+        for name, args in (("or_apply_rigid", [C.c_int, C.c_int, vp, vp, vp, vp]),
+                           ("or_apply_torsion", [C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_int, vp, vp]),
+                           ("or_bump_check", [C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, C.c_float, C.c_int, vp,
+                                              vp])):
+            fn = getattr(L, name)
+            fn.restype = None
+            fn.argtypes = args
         i32, i64 = C.c_int32, C.c_int64
         for name, args in (("go_generated_id", [i64, i64, C.c_char_p, C.c_size_t]),
                            ("go_mixed_shapes", [i64, i64, i32, i32, i32, i32, vp]),
@@ -122,7 +131,7 @@ class OracleOutput:
 
 
 def dock_batch(batch, pocket, table, cfg, seed: int = 0, threads: Optional[int] = None,
-               latency: bool = False) -> OracleOutput:
+               latency: bool = False, restart_poses: bool = False) -> OracleOutput:
     """Sequential dock_ligand per ligand, OpenMP over ligands (the batched engine's CPU
     shape); latency=True: ligands one after another, each ligand's restarts on an inner pool of
     `threads` workers (the latency engine's CPU shape) — identical results."""
@@ -141,13 +150,19 @@ def dock_batch(batch, pocket, table, cfg, seed: int = 0, threads: Optional[int] 
     fo, fax, fm = c(batch.frag_off, np.int32), c(batch.frag_axis, np.int32), c(batch.frag_mask, np.uint32)
     if fax.size == 0:
         fax, fm = np.zeros((1, 2), np.int32), np.zeros((1, 5), np.uint32)
-    fn = lib().or_dock_batch_latency if latency else lib().or_dock_batch
-    rc = fn(n, _p(ao), _p(xyz), _p(typ), _p(fo), _p(fax), _p(fm), C.cast(idbuf, C.c_void_p),
-                             _p(id_off), C.byref(pk.c), C.byref(ccfg), int(threads or os.cpu_count() or 1),
-                             _p(res), _p(rr), _p(rt), _p(bx))
+    args = [n, _p(ao), _p(xyz), _p(typ), _p(fo), _p(fax), _p(fm), C.cast(idbuf, C.c_void_p), _p(id_off),
+            C.byref(pk.c), C.byref(ccfg), int(threads or os.cpu_count() or 1), _p(res), _p(rr), _p(rt), _p(bx)]
+    rx = None
+    if restart_poses:
+        rx = np.zeros((max(na, 1) * N, 3), np.float32)
+        rc = lib().or_dock_batch_poses(*args, _p(rx))
+    else:
+        rc = (lib().or_dock_batch_latency if latency else lib().or_dock_batch)(*args)
     if rc != 0:
         raise RuntimeError(f"oracle failed ({rc})")
-    return OracleOutput(res[:n], rr[:n], rt[:nf], bx[:na])
+    out = OracleOutput(res[:n], rr[:n], rt[:nf], bx[:na])
+    out.restart_xyz = rx   # [(atom_off[i] * N + r * A_i + a)] rows, Å
+    return out
 
 
 def grid_score(pocket, table, coords) -> int:
@@ -259,3 +274,38 @@ def synthetic_pocket(spacing: float = 0.5, n_atoms: int = 200, seed: int = 7, rm
     atoms = tuple(model.Atom.of(*xyz[i], int(typ[i])) for i in range(n_atoms))
     return model.Pocket(tuple(float(o) for o in origin), float(np.float32(spacing)), tuple(int(d) for d in dims), vals,
                         atoms)
+
+
+# ---- the other L2 ops in Å, batched over poses [P, n, 3] ----------------------
+def _mask_words(mask) -> np.ndarray:
+    m = np.zeros(5, np.uint32)
+    for i in mask:
+        m[int(i) >> 5] |= np.uint32(1 << (int(i) & 31))
+    return m
+
+
+def apply_rigid(coords, m, center) -> np.ndarray:
+    P = np.ascontiguousarray(coords, np.float32).reshape(-1, np.shape(coords)[-2], 3)
+    mm = np.ascontiguousarray(np.broadcast_to(np.asarray(m, np.float32).reshape(-1, 9), (P.shape[0], 9)))
+    cc = np.ascontiguousarray(np.broadcast_to(np.asarray(center, np.float32).reshape(-1, 3), (P.shape[0], 3)))
+    out = np.empty_like(P)
+    lib().or_apply_rigid(P.shape[1], P.shape[0], _p(P), _p(mm), _p(cc), _p(out))
+    return out
+
+
+def apply_torsion(coords, axis_begin: int, axis_end: int, mask, deg: int):
+    P = np.ascontiguousarray(coords, np.float32).reshape(-1, np.shape(coords)[-2], 3)
+    out = np.empty_like(P)
+    st = np.zeros(P.shape[0], np.int32)
+    lib().or_apply_torsion(P.shape[1], P.shape[0], _p(P), int(axis_begin), int(axis_end), _p(_mask_words(mask)),
+                           int(deg), _p(out), _p(st))
+    return out, st
+
+
+def bump_check(coords, axis_begin: int, axis_end: int, mask, bump_distance: float, early_exit: bool):
+    P = np.ascontiguousarray(coords, np.float32).reshape(-1, np.shape(coords)[-2], 3)
+    bump = np.zeros(P.shape[0], np.uint8)
+    pairs = np.zeros(P.shape[0], np.int64)
+    lib().or_bump_check(P.shape[1], P.shape[0], _p(P), int(axis_begin), int(axis_end), _p(_mask_words(mask)),
+                        float(bump_distance), int(bool(early_exit)), _p(bump), _p(pairs))
+    return bump.astype(bool), pairs

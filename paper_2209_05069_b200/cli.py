@@ -186,9 +186,15 @@ def build_parser() -> argparse.ArgumentParser:
 
 
 def console_main(argv: Optional[Sequence[str]] = None) -> int:
+    """Exit status: 0 ok, 2 missing input file, 1 any error that ended a run (an invalid
+    configuration, a device or library failure re-raised by an engine): never a short CSV with 0."""
     a = build_parser().parse_args(argv)
-    return {"dock": cmd_dock, "heatmap": cmd_heatmap, "scaling": cmd_scaling,
-            "ablate-early-exit": cmd_ablate_early_exit}[a.cmd](a)
+    try:
+        return {"dock": cmd_dock, "heatmap": cmd_heatmap, "scaling": cmd_scaling,
+                "ablate-early-exit": cmd_ablate_early_exit}[a.cmd](a)
+    except (model.DockscreenError, RuntimeError, ValueError) as e:
+        print(f"error: {type(e).__name__}: {e}", file=sys.stderr)
+        return 1
 
 
 if __name__ == "__main__":

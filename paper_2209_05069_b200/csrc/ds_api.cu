@@ -41,6 +41,12 @@ void launch_grid_score(const PocketView &pk, const float *coords, int n_atoms, i
                        cudaStream_t st);
 void launch_rescore(const PocketView &pk, const float *coords, const uint8_t *types, int n_atoms, int n_poses,
                     float cutoff2, int64_t *out, cudaStream_t st);
+void launch_apply_rigid(const float *coords, int n_atoms, int n_poses, const float *m, const float *center, float *out,
+                        cudaStream_t st);
+void launch_apply_torsion(const float *coords, int n_atoms, int n_poses, int ab, int ae, const uint32_t *mask,
+                          float2 cs, int identity, float *out, int32_t *status, cudaStream_t st);
+void launch_bump_check(const float *coords, int n_atoms, int n_poses, int ab, int ae, const uint32_t *mask, float bd2,
+                       int early_exit, uint8_t *bump, long long *pairs, cudaStream_t st);
 }  // namespace ds
 
 using namespace ds;
@@ -109,6 +115,7 @@ struct ds_ctx {
     uint8_t *btors;
   } io{};
   DevBuf x_in, x_out;
+  DevBuf op_in, op_aux, op_out;   // the ds_op_* entry points (never touch a resident batch)
   // latency-family scratch (alignment scores, per-ligand done counters) is left zeroed by the
   // kernels; cleared here only after a (re)allocation or a failed call
   bool lat_pdl = false;
@@ -227,7 +234,7 @@ void ds_destroy(ds_ctx *c) {
   DevBuf *bufs[] = {&c->b_atom_off, &c->b_atoms, &c->b_frag_off, &c->b_frags, &c->b_idh, &c->b_order_a,
                     &c->b_order_o, &c->b_keys, &c->b_res, &c->b_rrec, &c->b_rtors, &c->b_coords, &c->b_btors,
                     &c->b_queue, &c->b_scratch, &c->b_rgv, &c->b_lat_scores, &c->b_lat_recs, &c->b_lat_done,
-                    &c->x_in, &c->x_out};
+                    &c->x_in, &c->x_out, &c->op_in, &c->op_aux, &c->op_out};
   for (DevBuf *b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->trig) cudaFree(c->trig);
@@ -1328,13 +1335,12 @@ int ds_op_grid_score(ds_ctx *c, const ds_pocket *pk, const float *coords, int n_
   if (!n_poses) return DS_OK;
   DS_CUDA(enter_device(c->device));
   const size_t nc = 12ull * n_atoms * n_poses;
-  ++c->gen;  // overwrites the per-array buffers of any resident batch
   int rc;
-  if ((rc = c->ensure(c->b_coords, std::max<size_t>(nc, 16))) || (rc = c->ensure(c->b_keys, 4ull * n_poses))) return rc;
-  DS_CUDA(cudaMemcpyAsync(c->b_coords.p, coords, nc, cudaMemcpyHostToDevice, c->stream));
-  launch_grid_score(pk->view, (const float *)c->b_coords.p, n_atoms, n_poses, (int32_t *)c->b_keys.p, c->stream);
+  if ((rc = c->ensure(c->op_in, std::max<size_t>(nc, 16))) || (rc = c->ensure(c->op_out, 4ull * n_poses))) return rc;
+  DS_CUDA(cudaMemcpyAsync(c->op_in.p, coords, nc, cudaMemcpyHostToDevice, c->stream));
+  launch_grid_score(pk->view, (const float *)c->op_in.p, n_atoms, n_poses, (int32_t *)c->op_out.p, c->stream);
   DS_CUDA(cudaGetLastError());
-  DS_CUDA(cudaMemcpyAsync(out, c->b_keys.p, 4ull * n_poses, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaMemcpyAsync(out, c->op_out.p, 4ull * n_poses, cudaMemcpyDeviceToHost, c->stream));
   DS_CUDA(cudaStreamSynchronize(c->stream));
   return DS_OK;
 }
@@ -1346,17 +1352,98 @@ int ds_op_rescore(ds_ctx *c, const ds_pocket *pk, const float *coords, const uin
   if (!n_poses) return DS_OK;
   DS_CUDA(enter_device(c->device));
   const size_t nc = 12ull * n_atoms * n_poses;
-  ++c->gen;
   int rc;
-  if ((rc = c->ensure(c->b_coords, std::max<size_t>(nc, 16))) || (rc = c->ensure(c->b_rtors, std::max(n_atoms, 1))) ||
-      (rc = c->ensure(c->b_res, 8ull * n_poses)))
+  if ((rc = c->ensure(c->op_in, std::max<size_t>(nc, 16))) || (rc = c->ensure(c->op_aux, std::max(n_atoms, 1))) ||
+      (rc = c->ensure(c->op_out, 8ull * n_poses)))
     return rc;
-  DS_CUDA(cudaMemcpyAsync(c->b_coords.p, coords, nc, cudaMemcpyHostToDevice, c->stream));
-  DS_CUDA(cudaMemcpyAsync(c->b_rtors.p, types, (size_t)n_atoms, cudaMemcpyHostToDevice, c->stream));
-  launch_rescore(pk->view, (const float *)c->b_coords.p, (const uint8_t *)c->b_rtors.p, n_atoms, n_poses, 0.f,
-                 (int64_t *)c->b_res.p, c->stream);
+  DS_CUDA(cudaMemcpyAsync(c->op_in.p, coords, nc, cudaMemcpyHostToDevice, c->stream));
+  DS_CUDA(cudaMemcpyAsync(c->op_aux.p, types, (size_t)n_atoms, cudaMemcpyHostToDevice, c->stream));
+  launch_rescore(pk->view, (const float *)c->op_in.p, (const uint8_t *)c->op_aux.p, n_atoms, n_poses, 0.f,
+                 (int64_t *)c->op_out.p, c->stream);
   DS_CUDA(cudaGetLastError());
-  DS_CUDA(cudaMemcpyAsync(out, c->b_res.p, 8ull * n_poses, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaMemcpyAsync(out, c->op_out.p, 8ull * n_poses, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  return DS_OK;
+}
+
+namespace {
+// fragment arguments of the Å-frame ops: axis atoms in range and distinct, outside the mask; the
+// mask within the atoms (MalformedFragment / IndexOutOfRange like validate_ligand)
+int check_fragment(int n_atoms, int ab, int ae, const uint32_t *mask) {
+  if (n_atoms < 1 || n_atoms > DS_MAX_ATOMS) return fail(DS_ERR_TOO_MANY_ATOMS, "n_atoms %d not in 1..%d", n_atoms, DS_MAX_ATOMS);
+  if (!mask) return fail(DS_ERR_INVALID_ARG, "mask is NULL");
+  if (ab < 0 || ae < 0 || ab >= n_atoms || ae >= n_atoms) return fail(DS_ERR_INDEX_OUT_OF_RANGE, "axis atom out of range");
+  for (int w = 0; w < DS_MASK_WORDS; ++w) {
+    const uint32_t valid = n_atoms >= 32 * (w + 1) ? 0xFFFFFFFFu : (n_atoms <= 32 * w ? 0u : ((1u << (n_atoms - 32 * w)) - 1u));
+    if (mask[w] & ~valid) return fail(DS_ERR_INDEX_OUT_OF_RANGE, "mask atom out of range");
+  }
+  if (ab == ae || ((mask[ab >> 5] >> (ab & 31)) & 1u) || ((mask[ae >> 5] >> (ae & 31)) & 1u))
+    return fail(DS_ERR_MALFORMED_FRAGMENT, "axis atoms must be distinct and outside the moving mask");
+  return DS_OK;
+}
+}  // namespace
+
+int ds_op_apply_rigid(ds_ctx *c, const float *coords, int n_atoms, int n_poses, const float *m, const float *center,
+                      float *out) {
+  if (!c || !coords || !m || !center || !out || n_atoms < 0 || n_poses < 0) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  if (!n_poses || !n_atoms) return DS_OK;
+  DS_CUDA(enter_device(c->device));
+  const size_t nc = 12ull * n_atoms * n_poses;
+  int rc;
+  if ((rc = c->ensure(c->op_in, nc)) || (rc = c->ensure(c->op_aux, 48ull * n_poses)) || (rc = c->ensure(c->op_out, nc)))
+    return rc;
+  DS_CUDA(cudaMemcpyAsync(c->op_in.p, coords, nc, cudaMemcpyHostToDevice, c->stream));
+  DS_CUDA(cudaMemcpyAsync(c->op_aux.p, m, 36ull * n_poses, cudaMemcpyHostToDevice, c->stream));
+  DS_CUDA(cudaMemcpyAsync((char *)c->op_aux.p + 36ull * n_poses, center, 12ull * n_poses, cudaMemcpyHostToDevice, c->stream));
+  launch_apply_rigid((const float *)c->op_in.p, n_atoms, n_poses, (const float *)c->op_aux.p,
+                     (const float *)((char *)c->op_aux.p + 36ull * n_poses), (float *)c->op_out.p, c->stream);
+  DS_CUDA(cudaGetLastError());
+  DS_CUDA(cudaMemcpyAsync(out, c->op_out.p, nc, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  return DS_OK;
+}
+
+int ds_op_apply_torsion(ds_ctx *c, const float *coords, int n_atoms, int n_poses, int axis_begin, int axis_end,
+                        const uint32_t *mask, int angle_deg, float *out, int32_t *status) {
+  if (!c || !coords || !out || !status || n_poses < 0) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  int rc;
+  if ((rc = check_fragment(n_atoms, axis_begin, axis_end, mask))) return rc;
+  if (!n_poses) return DS_OK;
+  DS_CUDA(enter_device(c->device));
+  const size_t nc = 12ull * n_atoms * n_poses;
+  if ((rc = c->ensure(c->op_in, nc)) || (rc = c->ensure(c->op_out, nc)) || (rc = c->ensure(c->op_aux, 4ull * n_poses)))
+    return rc;
+  const int deg = ((angle_deg % 360) + 360) % 360;
+  float2 cs;  // P0: the ctx's f64 -> f32 table
+  DS_CUDA(cudaMemcpy(&cs, c->trig + deg, sizeof cs, cudaMemcpyDeviceToHost));
+  DS_CUDA(cudaMemcpyAsync(c->op_in.p, coords, nc, cudaMemcpyHostToDevice, c->stream));
+  launch_apply_torsion((const float *)c->op_in.p, n_atoms, n_poses, axis_begin, axis_end, mask, cs, deg == 0,
+                       (float *)c->op_out.p, (int32_t *)c->op_aux.p, c->stream);
+  DS_CUDA(cudaGetLastError());
+  DS_CUDA(cudaMemcpyAsync(out, c->op_out.p, nc, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaMemcpyAsync(status, c->op_aux.p, 4ull * n_poses, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  return DS_OK;
+}
+
+int ds_op_bump_check(ds_ctx *c, const float *coords, int n_atoms, int n_poses, int axis_begin, int axis_end,
+                     const uint32_t *mask, float bump_distance, int early_exit, uint8_t *bump, int64_t *pairs) {
+  if (!c || !coords || !bump || !pairs || n_poses < 0 || !(bump_distance > 0.f)) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  int rc;
+  if ((rc = check_fragment(n_atoms, axis_begin, axis_end, mask))) return rc;
+  if (!n_poses) return DS_OK;
+  DS_CUDA(enter_device(c->device));
+  const size_t nc = 12ull * n_atoms * n_poses;
+  if ((rc = c->ensure(c->op_in, nc)) || (rc = c->ensure(c->op_out, 9ull * n_poses))) return rc;
+  const float bd2 = (float)((double)bump_distance * (double)bump_distance);
+  DS_CUDA(cudaMemcpyAsync(c->op_in.p, coords, nc, cudaMemcpyHostToDevice, c->stream));
+  long long *d_pairs = (long long *)c->op_out.p;
+  uint8_t *d_bump = (uint8_t *)(d_pairs + n_poses);
+  launch_bump_check((const float *)c->op_in.p, n_atoms, n_poses, axis_begin, axis_end, mask, bd2, early_exit ? 1 : 0,
+                    d_bump, d_pairs, c->stream);
+  DS_CUDA(cudaGetLastError());
+  DS_CUDA(cudaMemcpyAsync(pairs, d_pairs, 8ull * n_poses, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaMemcpyAsync(bump, d_bump, (size_t)n_poses, cudaMemcpyDeviceToHost, c->stream));
   DS_CUDA(cudaStreamSynchronize(c->stream));
   return DS_OK;
 }

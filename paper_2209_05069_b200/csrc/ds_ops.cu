@@ -68,6 +68,119 @@ void launch_rescore(const PocketView &pk, const float *coords, const uint8_t *ty
   k_rescore<<<n_poses, 128, 0, st>>>(pk, coords, types, n_atoms, n_poses, o[0], o[1], o[2], out);
 }
 
+// ---- the other L2 ops of the slot in Å (SPEC.md:135 apply_rigid, :145 apply_torsion, :193
+// bump_check), the pinned recipes of DESIGN.md §3 (P8, P9) evaluated in the Å frame; bit-identical
+// to oracle/dock_oracle.c or_apply_rigid / or_apply_torsion / or_bump_check.
+
+// thread per (pose, atom): w = p - c, p' = fma(m_i2, w_z, fma(m_i1, w_y, fma(m_i0, w_x, c_i)))
+__global__ void k_apply_rigid(const float *coords, int n_atoms, int n_poses, const float *m, const float *center,
+                              float *out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)n_atoms * n_poses) return;
+  const int p = (int)(t / n_atoms);
+  const float *M = m + 9 * p;
+  const float3 c = make_float3(center[3 * p], center[3 * p + 1], center[3 * p + 2]);
+  const float *q = coords + 3 * t;
+  float R[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = M[k];
+  const float3 o = torsion_apply(R, c, q[0], q[1], q[2]);
+  out[3 * t] = o.x;
+  out[3 * t + 1] = o.y;
+  out[3 * t + 2] = o.z;
+}
+
+// warp per pose: axis (every lane, same bits), DegenerateAxis (status 2, pose unchanged), lanes over atoms
+__global__ void k_apply_torsion(const float *coords, int n_atoms, int n_poses, int ab, int ae, uint4 ma, unsigned mb,
+                                float2 cs, int identity, float *out, int32_t *status) {
+  const int pose = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pose >= n_poses) return;
+  const float *u = coords + 3 * (size_t)pose * n_atoms;
+  float *o = out + 3 * (size_t)pose * n_atoms;
+  const float3 a = make_float3(u[3 * ab], u[3 * ab + 1], u[3 * ab + 2]);
+  const float vx = __fsub_rn(u[3 * ae], a.x), vy = __fsub_rn(u[3 * ae + 1], a.y), vz = __fsub_rn(u[3 * ae + 2], a.z);
+  const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
+  const bool degen = !(len >= 1e-9f);
+  float R[9];
+  if (!degen && !identity)
+    torsion_matrix(__fdiv_rn(vx, len), __fdiv_rn(vy, len), __fdiv_rn(vz, len), cs.x, cs.y, R);
+  const unsigned w[5] = {ma.x, ma.y, ma.z, ma.w, mb};
+  for (int i = lane; i < n_atoms; i += 32) {
+    float3 q = make_float3(u[3 * i], u[3 * i + 1], u[3 * i + 2]);
+    if (!degen && !identity && ((w[i >> 5] >> (i & 31)) & 1u)) q = torsion_apply(R, a, q.x, q.y, q.z);
+    o[3 * i] = q.x;
+    o[3 * i + 1] = q.y;
+    o[3 * i + 2] = q.z;
+  }
+  if (lane == 0) status[pose] = degen ? 2 : 0;
+}
+
+// warp per pose: moving atoms i ascending (warp-uniform loop), lanes over the complement C' (not
+// moving, not an axis atom) in 32-atom rounds; the sequential scan's pair count is the C' atoms of
+// the rows before the first bump plus the rank of the first bumping j in its row, + 1 (P9, P14)
+__global__ void k_bump_check(const float *coords, int n_atoms, int n_poses, int ab, int ae, uint4 ma, unsigned mb,
+                             float bd2, int early_exit, uint8_t *bump, long long *pairs) {
+  __shared__ uint8_t s_c[8][DS_MAX_ATOMS];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pose = blockIdx.x * (blockDim.x >> 5) + wib;
+  if (pose >= n_poses) return;
+  const float *u = coords + 3 * (size_t)pose * n_atoms;
+  const unsigned w[5] = {ma.x, ma.y, ma.z, ma.w, mb};
+  int nC = 0;
+  for (int s = 0; s * 32 < n_atoms; ++s) {  // compaction of C'
+    const int j = s * 32 + lane;
+    const bool c = j < n_atoms && !((w[s] >> lane) & 1u) && j != ab && j != ae;
+    const unsigned bc = __ballot_sync(kFull, c);
+    if (c) s_c[wib][nC + __popc(bc & lanemask_lt())] = (uint8_t)j;
+    nC += __popc(bc);
+  }
+  __syncwarp();
+  long long n = 0;
+  bool hit = false;
+  for (int i = 0; i < n_atoms && !(hit && early_exit); ++i) {
+    if (!((w[i >> 5] >> (i & 31)) & 1u)) continue;
+    const float xi = u[3 * i], yi = u[3 * i + 1], zi = u[3 * i + 2];
+    int first = -1;
+    for (int c0 = 0; c0 < nC; c0 += 32) {
+      bool b = false;
+      if (c0 + lane < nC) {
+        const int j = s_c[wib][c0 + lane];
+        b = dist2(xi, yi, zi, u[3 * j], u[3 * j + 1], u[3 * j + 2]) < bd2;
+      }
+      const unsigned bb = __ballot_sync(kFull, b);
+      if (bb && first < 0) first = c0 + __ffs(bb) - 1;
+      if (bb && early_exit) break;
+    }
+    if (first >= 0) hit = true;
+    n += (early_exit && first >= 0) ? first + 1 : nC;
+  }
+  if (lane == 0) {
+    bump[pose] = hit ? 1 : 0;
+    pairs[pose] = n;
+  }
+}
+
+void launch_apply_rigid(const float *coords, int n_atoms, int n_poses, const float *m, const float *center, float *out,
+                        cudaStream_t st) {
+  const long long n = (long long)n_atoms * n_poses;
+  k_apply_rigid<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(coords, n_atoms, n_poses, m, center, out);
+}
+
+void launch_apply_torsion(const float *coords, int n_atoms, int n_poses, int ab, int ae, const uint32_t *mask,
+                          float2 cs, int identity, float *out, int32_t *status, cudaStream_t st) {
+  k_apply_torsion<<<(n_poses + 7) / 8, 256, 0, st>>>(coords, n_atoms, n_poses, ab, ae,
+                                                    make_uint4(mask[0], mask[1], mask[2], mask[3]), mask[4], cs,
+                                                    identity, out, status);
+}
+
+void launch_bump_check(const float *coords, int n_atoms, int n_poses, int ab, int ae, const uint32_t *mask, float bd2,
+                       int early_exit, uint8_t *bump, long long *pairs, cudaStream_t st) {
+  k_bump_check<<<(n_poses + 7) / 8, 256, 0, st>>>(coords, n_atoms, n_poses, ab, ae,
+                                                 make_uint4(mask[0], mask[1], mask[2], mask[3]), mask[4], bd2,
+                                                 early_exit, bump, pairs);
+}
+
 // ---- build_pocket on the device (DESIGN.md §3 P18): thread per grid node, the
 // pocket atoms staged in shared memory as f64; every operation is the host's (ds_host.cpp
 // ds_build_pocket_grid) in the same order with explicit IEEE f64 rounding, so the grid is

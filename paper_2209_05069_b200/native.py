@@ -31,6 +31,7 @@ ERRORS = {
 STATUS_OK, STATUS_NO_VALID_POSE, STATUS_DEGENERATE_AXIS = 0, 1, 2
 FAMILY_BATCHED, FAMILY_LATENCY = 0, 1
 MASK_WORDS, FRAG_WORDS, MAX_RESTARTS, TORSION_NONE = 5, 8, 32, 255
+MAX_BINS = 8
 CHEM_SCALE = float(1 << 24)
 
 
@@ -134,6 +135,9 @@ def lib():
             "ds_generate_resident": (C.c_int, [vp, i64, i64, i32, vp, vp, vp]),
             "ds_batch_read_inputs": (C.c_int, [vp, vp, vp, vp, vp]),
             "ds_csr_gather": (C.c_int, [i32, vp, vp, vp, i32, vp, vp]),
+            "ds_op_apply_rigid": (C.c_int, [vp, vp, i32, i32, vp, vp, vp]),
+            "ds_op_apply_torsion": (C.c_int, [vp, vp, i32, i32, i32, i32, vp, i32, vp, vp]),
+            "ds_op_bump_check": (C.c_int, [vp, vp, i32, i32, i32, i32, vp, C.c_float, i32, vp, vp]),
             "ds_csr_scatter": (C.c_int, [i32, vp, vp, vp, i32, vp, vp]),
         }
         for name, (res, args) in sig.items():
@@ -433,6 +437,49 @@ class InteractionTable:
     @property
     def cutoff(self) -> float:
         return float(self.bins[-1][0])
+
+    @staticmethod
+    def load(path: str) -> "InteractionTable":
+        """a plain-text table file — 16 lines of 16 reals (the symmetric weights), then
+        one line per distance bin "upper multiplier" (ascending upper bounds, the last = the rescore
+        cutoff).  Blank lines and '#' comments are ignored.  Malformed files raise ParseError."""
+        rows, bins = [], []
+        with open(path, encoding="ascii") as fh:
+            for ln, line in enumerate(fh, 1):
+                tok = line.split("#", 1)[0].split()
+                if not tok:
+                    continue
+                try:
+                    vals = [float(t) for t in tok]
+                except ValueError as e:
+                    raise model.ParseError(f"line {ln}: {e}") from e
+                if len(rows) < 16:
+                    if len(vals) != 16:
+                        raise model.ParseError(f"line {ln}: table row needs 16 values, found {len(vals)}")
+                    rows.append(vals)
+                elif len(vals) == 2:
+                    bins.append((vals[0], vals[1]))
+                else:
+                    raise model.ParseError(f"line {ln}: bin line needs 'upper multiplier'")
+        if len(rows) < 16:
+            raise model.ParseError(f"expected 16 table rows, found {len(rows)}")
+        if not bins:
+            raise model.ParseError("no distance bins")
+        t = np.array(rows, np.float32)
+        if not np.array_equal(t, t.T):
+            raise model.ParseError("interaction table must be symmetric (SPEC.md:180)")
+        ub = [b[0] for b in bins]
+        if any(not (b > a) for a, b in zip(ub, ub[1:])) or not ub[0] > 0 or len(bins) > MAX_BINS:
+            raise model.ParseError(f"bins must have 1..{MAX_BINS} ascending positive upper bounds")
+        return InteractionTable(t, tuple((float(np.float32(u)), float(np.float32(m))) for u, m in bins))
+
+    def save(self, path: str) -> None:
+        """Write the SPEC.md:225 text format (float32 values, round-trip exact)."""
+        with open(path, "w", encoding="ascii", newline="\n") as fh:
+            for row in np.asarray(self.table, np.float32).reshape(16, 16):
+                fh.write(" ".join(repr(float(v)) for v in row) + "\n")
+            for u, m in self.bins:
+                fh.write(f"{float(np.float32(u))!r} {float(np.float32(m))!r}\n")
 
 
 class DevicePocket:

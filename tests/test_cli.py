@@ -48,3 +48,21 @@ def test_scaling_and_ablation_and_dock(tmp_path, synth_pocket):
     assert cli.console_main(["dock", "--ligands", str(lig), "--pocket", str(poc), "--out", str(tmp_path / "d")]) == 0
     out = list(csv.reader(open(tmp_path / "d" / "results.csv")))
     assert out[0] == ["ligand_id", "geom_score", "chem_score", "valid"] and len(out) == 21
+
+
+@pytest.mark.gpu
+def test_dock_exits_nonzero_on_fatal_config(tmp_path):
+    """An engine's fatal error (a configuration the device rejects) gives a non-zero exit status."""
+    from paper_2209_05069_b200 import io
+    lig, pock = tmp_path / "l.ligq", tmp_path / "p.pock"
+    io.write_ligand_file(str(lig), io.generate_dataset(12, 2, 3, seed=1))
+    io.write_pocket_file(str(pock), io.synthetic_pocket())
+    args = ["dock", "--ligands", str(lig), "--pocket", str(pock), "--workers", "2", "--out", str(tmp_path / "o")]
+    assert cli.console_main(args) == 0
+    from paper_2209_05069_b200 import model
+    orig = cli._cfg
+    cli._cfg = lambda a: model.DockConfig(alignment_step_deg=1)
+    try:
+        assert cli.console_main(args) == 1
+    finally:
+        cli._cfg = orig

@@ -1,0 +1,117 @@
+"""BASELINE configs at their stated scale on the device against the CPU oracle:
+config 1 at its full 1,000 x (12, 5); the latency family on the 0.375 Å (L2-variant, global-grid)
+pocket; a 9 x 8 config-4 grid sample; and the chemical score against a float64 restatement of
+SPEC.md:206's real-valued ordered sum."""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import compare
+from paper_2209_05069_b200 import io, model
+from paper_2209_05069_b200.native import FAMILY_BATCHED, FAMILY_LATENCY, pack
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(ctx, batch, pocket, table, cfg, seed=0, family=FAMILY_BATCHED):
+    dp = ctx.pocket(pocket, table)
+    g = ctx.dock(dp, pack(batch), cfg, seed, family, coords=True, detail=True)
+    dp.close()
+    return g
+
+
+def test_config1_full_scale_both_families(gpu_ctx, synth_pocket, table):
+    """Config 1: generate_dataset(heavy=12, F=5, seed=1), 1,000 ligands, default DockConfig."""
+    batch = io.generate_dataset_batch(12, 5, 1000, seed=1)
+    cfg = model.DockConfig()
+    o = oracle.dock_batch(batch, synth_pocket, table, cfg, 0)
+    for fam in (FAMILY_BATCHED, FAMILY_LATENCY):
+        compare(batch, _run(gpu_ctx, batch, synth_pocket, table, cfg, 0, fam), o, cfg)
+
+
+def test_latency_family_global_grid_pocket(gpu_ctx, table):
+    """Spacing 0.375 Å: the 75^3-class grid does not fit in shared memory, so the latency family
+    runs k_optimize_latency<false> (grid lookups through the L2-resident global copy)."""
+    pocket = io.synthetic_pocket(spacing=0.375)
+    assert np.prod(np.array(pocket.grid_dims) + 2) > 227 * 1024
+    batch = io.generate_mixed_batch(80, seed=10)
+    cfg = model.DockConfig()
+    o = oracle.dock_batch(batch, pocket, table, cfg, 3)
+    compare(batch, _run(gpu_ctx, batch, pocket, table, cfg, 3, FAMILY_LATENCY), o, cfg)
+    one = batch.subset([5])
+    compare(one, _run(gpu_ctx, one, pocket, table, cfg, 3, FAMILY_LATENCY),
+            oracle.dock_batch(one, pocket, table, cfg, 3), cfg)
+
+
+HEAVY = (8, 12, 16, 20, 24, 28, 32, 36, 40)
+FRAGS = (0, 1, 2, 4, 8, 12, 16, 20)
+
+
+@pytest.mark.parametrize("heavy", HEAVY)
+def test_config4_grid_sample(gpu_ctx, synth_pocket, table, heavy):
+    """Config 4's 9 x 8 shape grid (infeasible F >= heavy - 1 skipped), 16 ligands per cell, both
+    families against the oracle."""
+    cfg = model.DockConfig()
+    for f in FRAGS:
+        if f > 0 and f >= heavy - 1:
+            continue
+        batch = io.generate_dataset_batch(heavy, f, 16, seed=100 + heavy * 31 + f)
+        o = oracle.dock_batch(batch, synth_pocket, table, cfg, 0)
+        for fam in (FAMILY_BATCHED, FAMILY_LATENCY):
+            compare(batch, _run(gpu_ctx, batch, synth_pocket, table, cfg, 0, fam), o, cfg)
+
+
+def _ordered_sum_f64(xyz, types, pocket, table):
+    """SPEC.md:206 restated in float64: sum over (i outer, j inner) of table[t_i][t_j] x
+    bin_multiplier(d) for d < cutoff, d the Å distance; also the pairs whose distance lies within
+    1e-5 Å of a bin bound (where the f32 grid-frame bin of P11 may differ from the f64 one)."""
+    pxyz, ptyp = pocket.atom_arrays()
+    ub = np.array([b[0] for b in table.bins], np.float64)
+    mult = np.array([b[1] for b in table.bins], np.float64)
+    d = np.sqrt(((xyz[:, None, :].astype(np.float64) - pxyz[None].astype(np.float64)) ** 2).sum(-1))
+    b = (d[..., None] >= ub).sum(-1)                       # first bin with d < ub
+    w = np.asarray(table.table, np.float64)[types[:, None], ptyp[None, :]]
+    m = np.where(b < len(ub), mult[np.minimum(b, len(ub) - 1)], 0.0)
+    total = 0.0
+    for i in range(len(xyz)):                             # i outer, j inner, sequential
+        for j in range(len(pxyz)):
+            total += w[i, j] * m[i, j]
+    near = (np.abs(d[..., None] - ub) < 1e-5).any(-1)
+    return total, w, d, near
+
+
+def test_chem_score_vs_f64_ordered_sum(gpu_ctx, synth_pocket, table):
+    """The device's exact fixed-point rescore (P11) against a float64 restatement of SPEC.md:206's
+    real-valued ordered sum, per ligand: |chem - ref| <= 1e-4 max(|ref|, 1) (north star), where
+    differences larger than that must be explained by pairs within 1e-5 Å of a bin bound (FP ties
+    of the bin choice, logged); and the best restart the f64 sums would pick among the kept poses
+    is compared with the device's, with the flips counted and each required to be such a tie."""
+    batch = io.generate_mixed_batch(150, seed=44)
+    cfg = model.DockConfig()
+    g = _run(gpu_ctx, batch, synth_pocket, table, cfg, 0)
+    o = oracle.dock_batch(batch, synth_pocket, table, cfg, 0, restart_poses=True)
+    N = cfg.restarts_n
+    ties = flips = checked = 0
+    for i in range(batch.n):
+        if g.results[i]["status"] != 0:
+            continue
+        a0, a1 = int(batch.atom_off[i]), int(batch.atom_off[i + 1])
+        A, types = a1 - a0, batch.atom_type[a0:a1]
+        chem = float(g.results[i]["chem_fx"]) / 2 ** 24
+        ref, w, d, near = _ordered_sum_f64(g.best_coords[a0:a1], types, synth_pocket, table)
+        checked += 1
+        if abs(chem - ref) > 1e-4 * max(abs(ref), 1.0):
+            assert near.any(), (i, chem, ref)
+            ties += 1
+        kept = [r for r in range(N) if o.restarts[i, r]["kept"]]
+        sums = []
+        for r in kept:
+            xyz = o.restart_xyz[a0 * N + r * A: a0 * N + (r + 1) * A]
+            sums.append((_ordered_sum_f64(xyz, types, synth_pocket, table)[0], r))
+        best = max(sums, key=lambda t: (t[0], -t[1]))[1]
+        if best != int(g.results[i]["best_restart"]):
+            flips += 1
+            top = sorted(s for s, _ in sums)
+            assert top[-1] - top[-2] <= 1e-4 * max(abs(top[-1]), 1.0) + 1.0, (i, sums)
+    print(f"\nf64 ordered-sum restatement: {checked} ligands, {ties} bin-boundary ties, {flips} best_restart flips")
+    assert checked > 100 and flips <= 2
