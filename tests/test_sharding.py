@@ -76,3 +76,48 @@ def test_two_rank_screen_equals_single_rank():
     whole = oracle.dock_batch(io.generate_mixed_batch(n_total, seed=5), io.synthetic_pocket(),
                               InteractionTable.default(), model.DockConfig(), threads=4)
     assert np.array_equal(got, whole.results)
+
+
+def _worker_root(rank, world, port, n_total, out_q):
+    """bench.py --config 5's gather: records AND best torsion indices (variable length per rank) to
+    rank 0 over gloo (shard.gather_to_root)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2209_05069_b200 import io, model
+    from paper_2209_05069_b200.native import InteractionTable
+    lo, hi = shard.shard_range(n_total, world, rank)
+    batch = io.generate_mixed_batch(hi - lo, seed=5, first_index=lo)
+    res = oracle.dock_batch(batch, io.synthetic_pocket(), InteractionTable.default(), model.DockConfig(), threads=2)
+    best_t = np.array([res.restart_torsion[f, int(res.results[i]["best_restart"])]
+                       for i in range(batch.n) for f in range(batch.frag_off[i], batch.frag_off[i + 1])], np.uint8)
+    got = shard.gather_to_root([res.results, best_t], rank, world)
+    if rank == 0:
+        out_q.put((got[0].tobytes(), got[1].tobytes()))
+    else:
+        assert got == []
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_gather_to_root_records_and_torsions():
+    import oracle
+    from paper_2209_05069_b200 import io, model
+    from paper_2209_05069_b200.native import InteractionTable
+    n_total = 21
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_root, args=(r, 2, port, n_total, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    rec, tors = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    b = io.generate_mixed_batch(n_total, seed=5)
+    whole = oracle.dock_batch(b, io.synthetic_pocket(), InteractionTable.default(), model.DockConfig(), threads=4)
+    want_t = np.array([whole.restart_torsion[f, int(whole.results[i]["best_restart"])]
+                       for i in range(b.n) for f in range(b.frag_off[i], b.frag_off[i + 1])], np.uint8)
+    assert np.array_equal(np.frombuffer(rec, dtype=oracle.RESULT), whole.results)
+    assert np.array_equal(np.frombuffer(tors, dtype=np.uint8), want_t)
