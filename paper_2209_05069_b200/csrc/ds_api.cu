@@ -702,8 +702,11 @@ int upload_express(ds_ctx *c, const ds_batch_desc *b, int N, bool zero_copy_out,
       (rc = c->ensure_host(in_bytes + out_bytes)))
     return rc;
   char *h = (char *)c->h_stage;
-  for (int k = 0; k < 7; ++k)
+  for (int k = 0; k < 7; ++k) {
     if (sz[k]) memcpy(h + off[k], src[k], sz[k]);
+    const size_t end = k + 1 < 7 ? off[k + 1] : in_bytes;  // alignment padding: defined bytes
+    if (end > off[k] + sz[k]) memset(h + off[k] + sz[k], 0, end - off[k] - sz[k]);
+  }
   DS_CUDA(cudaMemcpyAsync(c->x_in.p, h, in_bytes, cudaMemcpyHostToDevice, c->stream));
   char *di = (char *)c->x_in.p, *dout = (char *)c->x_out.p;
   c->io.atom_off = (int *)(di + off[0]);

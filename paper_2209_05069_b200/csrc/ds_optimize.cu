@@ -376,6 +376,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
             keep = hr.x > h0 && hr.x < h1 && hr.y < r1;
           }
           const unsigned bk = __ballot_sync(kFull, keep);  // in-place compaction: slot <= c
+          __syncwarp();  // every lane's read of clist[c] is ordered before the overwrites
           if (keep) {
             const int slot = nCf + __popc(bk & lt);
             reinterpret_cast<float *>(S.chh2)[slot] = hr.x;
