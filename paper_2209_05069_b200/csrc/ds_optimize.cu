@@ -275,6 +275,10 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
       const unsigned key = keys[(size_t)lig * dp.N + r];
       const int rot = 65535 - (int)(key & 0xFFFFu);
       const int align_score = (int)(key >> 16) - 32768;
+      // grid score of the current pose, carried along the fragment chain: the aligned pose scores
+      // align_score (the key), a committed angle scores its key; a fragment's non-moving atoms then
+      // score total - (its moving atoms at angle 0), so no per-fragment pass over them
+      int total = align_score;
       const int ix = rot / dp.n_a, iy = rot - ix * dp.n_a;
       {
         float R0s[9], T[3], Rp[9];
@@ -298,7 +302,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
         // compaction of the moving set M (positions into mw) and of the bump-relevant complement C'
         // (not M, not an axis atom); base = grid score of the atoms the torsion does not move
-        int nM = 0, nC = 0, base = 0;
+        int nM = 0, nC = 0;
 #pragma unroll
         for (int s = 0; s < 5; ++s) {
           if (s * 32 >= A) break;
@@ -316,13 +320,12 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
               reinterpret_cast<float *>(S.mzp)[m] = p.z;
               reinterpret_cast<unsigned *>(S.mip)[m] = 0u;  // info word
             }
-            else base += grid_val(pk, node_index(g, p.x, p.y, p.z));
           }
           if (cp) S.clist[nC + __popc(bc & lt)] = (uint8_t)i;
           nM += __popc(bm);
           nC += __popc(bc);
         }
-        base = warp_sum(base);
+        int base = 0;  // score of the atoms the torsion does not move: total - angle-0 sum over M
         const float4 pa = S.u[ab], pb = S.u[ae];
         const float3 a3 = make_float3(pa.x, pa.y, pa.z);
         float kx = 0.f, ky = 0.f, kz = 0.f;
@@ -474,7 +477,8 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           for (int m0 = 0; m0 < nM; m0 += 2 * G) {
             const int m1 = m0 + 2 * gi, m2 = m1 + 1;
             // with early exit a bumped angle is retired; without it every pair is checked
-            const bool live = lane_ok && !(kEarly && bumped);
+            // angle 0 is never retired: its complete sum gives the non-moving atoms' score
+            const bool live = lane_ok && !(kEarly && bumped && kang != 0);
             const bool act1 = live && m1 < nM, act2 = live && m2 < nM;
             if (!__any_sync(kFull, act1)) break;
             bool hit = false;
@@ -499,10 +503,10 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
               const uint2 info = S.mip[j];
               const bool h1 = bump_hit(S, info.x, q1, m1, n_ovf, nCf, dp.bd2);
               const bool h2 = act2 && bump_hit(S, info.y, q2, m2, n_ovf, nCf, dp.bd2);
-              part += (h1 ? 0 : gv1) + (act2 && !h2 ? gv2 : 0);
+              part += gv1 + (act2 ? gv2 : 0);  // a bumped angle's sum is never used
               hit = h1 || h2;
               // with early exit an angle bumps in one round only (it is retired after it)
-              if (kEarly && hit) S.mhit[lane] = h1 ? m1 : m2;
+              if (kEarly && hit && !bumped) S.mhit[lane] = h1 ? m1 : m2;
             }
             if (kEarly) {  // OR the hits of the G lanes that share an angle
               // every lane must reach the ballot: never put it behind a short-circuit operator
@@ -532,6 +536,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
             const int v = __shfl_down_sync(kFull, part, t * nA);
             if (gi == 0) sum += v;
           }
+          if (k0 == 0) base = total - __shfl_sync(kFull, sum, 0);  // lane 0: angle 0, group 0
           unsigned hb = __ballot_sync(kFull, bumped && lane_ok);
           unsigned fold = 0;
           for (int t = 0; t < G; ++t) fold |= hb >> (t * nA);
@@ -544,6 +549,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           best_key = max(best_key, __reduce_max_sync(kFull, kk));
         }
         const int best_k = best_key ? 65535 - (int)(best_key & 0xFFFFu) : -1;
+        if (best_key) total = (int)(best_key >> 16) - 32768;  // the committed pose's score
         // commit the winner before the next fragment; moving slot m of atom i is its rank in the mask
         if (best_k > 0) {
           const uint4 ga = __ldg(bt.frags + 2 * (size_t)(f0 + f));
@@ -572,14 +578,9 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         n_aligned = r + 1;
         break;
       }
-      // final geometric score + store the final pose
-      int sc = 0;
-      for (int i = lane; i < A; i += 32) {
-        const float4 p = S.u[i];
-        sc += grid_val(pk, node_index(g, p.x, p.y, p.z));
-        fin[(size_t)r * A + i] = p;
-      }
-      sc = warp_sum(sc);
+      // final geometric score (carried) + store the final pose
+      const int sc = total;
+      for (int i = lane; i < A; i += 32) fin[(size_t)r * A + i] = S.u[i];
       const int valid = !(F >= 1 && all_bumped == F);  // P10
       if (lane == 0) {
         out.rgv[(size_t)lig * dp.N + r] = (sc * 2) | valid;
