@@ -7,7 +7,7 @@ batched_engine.run  — PAPER.md:349-426: producer threads pack
                       the stream natively and push the ligands into the bucketizer (bulk push per
                       bucket key, linearizable per bucket); every batch the bucketizer detaches when
                       full — and, at end of stream, every flushed partial one — goes to a dispatcher
-                      thread (several per device, each with its own ds_ctx and stream, so the tail of
+                      thread (four per device, each with its own ds_ctx and stream, so the tail of
                       one batch overlaps the next) that cuts it out of the packed stream and docks it
                       with the batched kernels (one warp per ligand).  The dispatch log records when
                       each batch was detached, started and finished.
@@ -273,7 +273,7 @@ class batched_engine:  # noqa: N801
     def run(stream: Stream, pocket: model.Pocket, cfg: model.DockConfig = model.DockConfig(),
             workers: int = 1, seed: int = 0, table: Optional[InteractionTable] = None,
             capacities: Union[None, str, Mapping[int, int]] = None, devices: Sequence[int] = (0,),
-            dispatchers_per_device: int = 3, chunk: int = 8192) -> EngineReport:
+            dispatchers_per_device: int = 4, chunk: int = 8192) -> EngineReport:
         """producers -> bucketizer -> dispatchers; flush at end of stream.
 
         capacities: None = SPEC.md:332's fixed per-range capacities; "device" = the occupancy-derived
