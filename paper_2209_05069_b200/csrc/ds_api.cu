@@ -22,8 +22,8 @@ void launch_align_batched(const PocketView &pk, const BatchView &bt, const DockP
 void launch_torsion_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                             const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st);
 void launch_select_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const uint32_t *keys,
-                           OptOut out, int *queue, int blocks, size_t smem, cudaStream_t st);
-size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap);
+                           OptOut out, int *queue, int sm_count, size_t smem_optin, cudaStream_t st);
+size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap, int K, int slot_atoms);
 int torsion_blocks_per_sm();
 int select_blocks_per_sm(size_t smem);
 int align_blocks_per_sm(int warps, size_t smem);
@@ -762,23 +762,25 @@ void finish_express(ds_ctx *c, int L, int NA, int NF, int N, const ds_outputs *o
   if (out->best_torsion && NF) memcpy(out->best_torsion, h + c->x_out_off[4], (size_t)NF);
 }
 
-int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t atom_base, int64_t n_atoms_range,
+int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t atom_base, int max_atoms,
                       const DockParams &dp, bool want_coords, bool want_btors, bool want_rrec, ds_stats *st,
                       cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2, int *queue);
 
-int run_batched(ds_ctx *c, const ds_pocket *pk, int L, int NA, int NF, const DockParams &dp, bool want_coords,
+int run_batched(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const DockParams &dp, bool want_coords,
                 bool want_btors, bool want_rrec, ds_stats *st) {
   int *queue = (int *)c->b_queue.p;
   DS_CUDA(cudaMemsetAsync(queue, 0, 256, c->stream));
-  return run_batched_range(c, pk, 0, L, 0, NA, dp, want_coords, want_btors, want_rrec, st, c->ev[1], c->ev[2],
+  return run_batched_range(c, pk, 0, L, 0, max_atoms, dp, want_coords, want_btors, want_rrec, st, c->ev[1], c->ev[2],
                            c->ev[3], queue);
 }
 
 // Batched family on ligands [L0, L1) of the resident batch (absolute atom/fragment offsets; the
 // per-ligand outputs and the order arrays are offset by L0).
-int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t atom_base, int64_t n_atoms_range,
-                      const DockParams &dp, bool want_coords, bool want_btors, bool want_rrec, ds_stats *st,
+int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t atom_base, int max_atoms,
+                      const DockParams &dp_in, bool want_coords, bool want_btors, bool want_rrec, ds_stats *st,
                       cudaEvent_t e0, cudaEvent_t e1, cudaEvent_t e2, int *queue) {
+  DockParams dp = dp_in;
+  dp.slot_atoms = std::max(1, std::min(max_atoms, DS_MAX_ATOMS));  // select pose-slot stride
   BatchView bt;
   bt.L = L1 - L0;
   bt.atom_off = c->io.atom_off + L0;
@@ -804,17 +806,14 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t at
   cudaEventRecord(e1, c->stream);
   // --- torsion optimisation, then select + rescore: warp per ligand, persistent, occupancy-sized ---
   const int blocks_t = c->sm_count * std::max(1, torsion_blocks_per_sm());
-  const size_t smem_s = select_cta_smem_bytes(pk->view.n_atoms, pk->view.nb, pk->view.lut_cap);
-  const int blocks_s = c->sm_count * std::max(1, select_blocks_per_sm(smem_s));
   int rc;
-  if ((rc = c->ensure(c->b_scratch, sizeof(float4) * (size_t)dp.N * (size_t)n_atoms_range)) ||
-      (rc = c->ensure(c->b_rgv, sizeof(int) * (size_t)dp.N * (size_t)(L1 - L0))))
+  if ((rc = c->ensure(c->b_rgv, sizeof(int) * (size_t)dp.N * (size_t)(L1 - L0))))
     return rc;
   OptOut oo = {};
   oo.res = c->io.res + L0;
   oo.rrec = want_rrec ? c->io.rrec + (size_t)L0 * dp.N : nullptr;
   oo.rtors = c->io.rtors;
-  oo.final_u = (float4 *)c->b_scratch.p;
+  oo.final_u = nullptr;
   oo.rgv = (int *)c->b_rgv.p;
   oo.atom_base = atom_base;
   oo.best_coords = want_coords ? c->io.coords : nullptr;
@@ -822,7 +821,7 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t at
   launch_torsion_batched(pk->view, bt, dp, c->io.order_o + L0, ao.keys, oo, queue + 16, blocks_t,
                          c->stream);
   if (e2 == c->ev[3]) cudaEventRecord(c->ev[5], c->stream);  // unchunked: time the select kernel too
-  launch_select_batched(pk->view, bt, dp, ao.keys, oo, queue + 32, blocks_s, smem_s, c->stream);
+  launch_select_batched(pk->view, bt, dp, ao.keys, oo, queue + 32, c->sm_count, c->smem_optin, c->stream);
   cudaEventRecord(e2, c->stream);
   if (st) st->launches += 3;
   cudaError_t e = cudaGetLastError();
@@ -889,7 +888,9 @@ int run_family(ds_ctx *c, const ds_pocket *pk, int family, int L, int NA, int NF
                bool want_coords, bool want_btors, bool want_rrec, ds_stats *st) {
   if (family == DS_FAMILY_LATENCY)
     return run_latency(c, pk, L, max_atoms, dp, want_coords, want_btors, want_rrec, st);
-  return run_batched(c, pk, L, NA, NF, dp, want_coords, want_btors, want_rrec, st);
+  (void)NA;
+  (void)NF;
+  return run_batched(c, pk, L, max_atoms, dp, want_coords, want_btors, want_rrec, st);
 }
 
 int download(ds_ctx *c, int L, int NA, int NF, int N, const ds_outputs *out, ds_stats *st) {
@@ -1041,7 +1042,9 @@ int dock_pipelined(ds_ctx *c, const ds_pocket *pk, const ds_batch_desc *b, const
     DS_CUDA(cudaMemcpyAsync((int *)c->b_order_o.p + L0, oo + L0, 4ull * (L1 - L0), cudaMemcpyHostToDevice, cs));
     cudaEventRecord(c->pev[4 * k], cs);
     DS_CUDA(cudaStreamWaitEvent(c->stream, c->pev[4 * k], 0));
-    if ((rc = run_batched_range(c, pk, L0, L1, b->atom_off[L0], (int64_t)b->atom_off[L1] - b->atom_off[L0], dp,
+    int amax = 1;
+    for (int i = L0; i < L1; ++i) amax = std::max(amax, b->atom_off[i + 1] - b->atom_off[i]);
+    if ((rc = run_batched_range(c, pk, L0, L1, b->atom_off[L0], amax, dp,
                                 out->best_coords != nullptr, out->best_torsion != nullptr, out->restarts != nullptr,
                                 st, c->pev[4 * k + 1], c->pev[4 * k + 2], c->pev[4 * k + 3], queue + 64 * k)))
       return rc;
@@ -1320,7 +1323,7 @@ int ds_query_capacity(ds_ctx *c, int range_idx, int *ligands) {
     warps_a = (int)std::min<size_t>(32, (c->smem_optin - grid_bytes - fixed) / per_warp);
   const int wa = warps_a * align_blocks_per_sm(warps_a, grid_bytes + fixed + per_warp * warps_a);
   const int wt = 8 * torsion_blocks_per_sm();
-  const int ws = 8 * select_blocks_per_sm(select_cta_smem_bytes(200, 4, 1080));
+  const int ws = 8 * select_blocks_per_sm(select_cta_smem_bytes(200, 4, 1080, 4, 120));
   cudaGetLastError();
   const int per_sm = std::min(wa, std::min(wt, ws));
   if (per_sm <= 0) return fail(DS_ERR_CUDA, "occupancy query returned 0 resident warps");

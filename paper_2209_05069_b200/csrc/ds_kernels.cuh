@@ -45,6 +45,7 @@ struct DockParams {
   double thr2;               // squared similarity RMSD, grid frame
   float cull2;               // squared bump-candidate bound (bump distance + 0.02 nodes), grid frame
   float cull_r;              // the bound itself (rounded up), for the per-fragment (h, r) box
+  int slot_atoms;            // batched select: pose-slot stride (the launch's largest ligand)
   unsigned opaque0;          // always 0: XORed into loop-invariant index terms so ptxas keeps them as
                              // ALU adds instead of re-deriving them with FMA-pipe IMADs
   // torsion sweep lane layout of the first angle block (angles 0 .. min(32, n_t) - 1): lane ->

@@ -18,11 +18,13 @@
 //    a hit marks the angle bumped, clean slots add their grid values to base + sum over M
 //    (non-moving atoms do not change);
 //  * the best clean angle (ties -> smallest) is committed.
-// The final pose of every restart goes to a per-ligand slot in HBM (L2-resident in practice).
+// Only the per-restart (geom, valid) word and torsion indices leave the kernel.
 //
-// k_select_batched — select_poses (heavy-atom RMSD in f64, lanes over pose pairs) and an integer
-// fixed-point rescore (order-free, exact) with pocket atoms (negated-coordinate f32x2 pairs, two
-// per lane), weights and the bin look-up table staged in shared memory.
+// k_select_batched — select_poses (heavy-atom RMSD in f64) over poses REPLAYED from the argmax keys
+// and the committed torsion indices into shared-memory slots (no pose ever goes to device memory:
+// 14 KB less DRAM traffic per ligand and no N x atoms scratch), and an integer fixed-point rescore
+// (order-free, exact) with pocket atoms (negated-coordinate f32x2 pairs, two per lane), weights and
+// the bin look-up table staged in shared memory.
 #include "ds_kernels.cuh"
 
 namespace ds {
@@ -53,11 +55,11 @@ struct TorWarpSmem {
   int mhit[32];             // early exit: per sweep lane, the moving slot of its bump (P14 row count)
 };
 
-// Per-warp shared scratch of the select/rescore kernel.
-struct SelWarpSmem {
-  float4 u[kMaxA];          // the pose being rescored (grid frame), .w = weight-table row offset
+// Per-warp header of the select/rescore kernel's scratch; K pose slots of slot_atoms float4 follow
+// (the kept poses and the candidate being replayed; .w = the atom's weight-table row offset)
+struct SelHdr {
+  double cen[DS_MAX_RESTARTS + 1][3];  // heavy-atom coordinate sums of the slots (RMSD lower bound)
   int geom[DS_MAX_RESTARTS];
-  unsigned dis[DS_MAX_RESTARTS];   // dissimilarity bitsets (select_poses)
   uint8_t valid[DS_MAX_RESTARTS];
   uint8_t ord[DS_MAX_RESTARTS];
   uint8_t kept[DS_MAX_RESTARTS];
@@ -104,7 +106,7 @@ __device__ __forceinline__ float3 torsion_pos(const PocketView &pk, int step_t, 
 // come from FADD2 / FMUL2 / FFMA2 (each half bit-identical to dist2: x - y == x + (-y) exactly).
 // The ligand atom (broadcast) is loaded once for the two pairs.  Bin: LUT or compares.
 template <int kLut, typename Part>  // kLut: 0 compares, 1 clamped table, 2 full-range table
-__device__ __forceinline__ long long rescore_pose_x2(const SelWarpSmem &S, int A, const f2_t *pnx, const f2_t *pny,
+__device__ __forceinline__ long long rescore_pose_x2(const float4 *su, int A, const f2_t *pnx, const f2_t *pny,
                                                      const f2_t *pnz, const int2 *pcol, int nrounds,
                                                      const int32_t *wfx, int nb, const float *ub2,
                                                      const uint8_t *lut, int lut_shift, int lut_cap,
@@ -120,13 +122,13 @@ __device__ __forceinline__ long long rescore_pose_x2(const SelWarpSmem &S, int A
       Part part = 0;
       const int i1 = min(A, i0 + part_atoms);
       for (int i = i0; i < i1; ++i) {
-        const float4 x = S.u[i];
+        const float4 x = su[i];
         const f2_t DX = f2_add(f2_pack(x.x, x.x), NX);
         const f2_t DY = f2_add(f2_pack(x.y, x.y), NY);
         const f2_t DZ = f2_add(f2_pack(x.z, x.z), NZ);
         float d0, d1;
         f2_unpack(f2_fma(DZ, DZ, f2_fma(DY, DY, f2_mul(DX, DX))), d0, d1);
-        int b0 = __float_as_int(x.w) + col.x, b1 = __float_as_int(x.w) + col.y;
+        int b0 = __float_as_int(x.w) + col.x, b1 = __float_as_int(x.w) + col.y;  // .w: the row offset
         if (kLut == 2) {  // d2 >= +0: bits >> shift <= lut_cap by construction
           b0 += lut[(unsigned)__float_as_int(d0) >> lut_shift];
           b1 += lut[(unsigned)__float_as_int(d1) >> lut_shift];
@@ -147,38 +149,88 @@ __device__ __forceinline__ long long rescore_pose_x2(const SelWarpSmem &S, int A
   return acc;
 }
 
-// select_poses (P12) dissimilarity bitsets: pairs (p < q) of valid poses over lanes; heavy-atom sum
-// of squared deltas in f64, in atom order (same order as the oracle)
-template <class SM>
-__device__ __noinline__ void pose_dissimilarity(SM &S, const float4 *scr, int A, int N, int heavy,
-                                                double thr2) {
-  const int npairs = N * (N - 1) / 2;
-  for (int pidx = threadIdx.x & 31; pidx < npairs; pidx += 32) {
-    int p = 0, rem = pidx;
-    while (rem >= N - 1 - p) {
-      rem -= N - 1 - p;
-      ++p;
-    }
-    const int q = p + 1 + rem;
-    if (!S.valid[p] || !S.valid[q]) continue;
-    double sum = 0.0;
-    const float4 *up = scr + (size_t)p * A, *uq = scr + (size_t)q * A;
-    for (int i = 0; i < A; ++i) {
-      const float4 x = up[i], y = uq[i];
-      if (x.w == 0.f) continue;
-      const double dx = __dsub_rn((double)x.x, (double)y.x);
-      const double dy = __dsub_rn((double)x.y, (double)y.y);
-      const double dz = __dsub_rn((double)x.z, (double)y.z);
-      double t = __dmul_rn(dx, dx);
-      t = __dadd_rn(t, __dmul_rn(dy, dy));
-      t = __dadd_rn(t, __dmul_rn(dz, dz));
-      sum = __dadd_rn(sum, t);
-    }
-    if (heavy > 0 && sum >= __dmul_rn(thr2, (double)heavy)) {
-      atomicOr(&S.dis[p], 1u << q);
-      atomicOr(&S.dis[q], 1u << p);
+// Replay restart r of ligand lig into P (grid frame, .w = weight-table row offset): the aligned
+// pose from the argmax key (P6), then every committed torsion in fragment order (P8) with the axis
+// taken from the current positions — the torsion kernel's operations, so the same bits.  Returns the
+// heavy-atom coordinate sums (f64, any order: only used as a bound) in cen.
+__device__ __forceinline__ void replay_pose(float4 *P, double *cen, const PocketView &pk, const BatchView &bt,
+                                            const DockParams &dp, const uint32_t *keys, const OptOut &out, int lig,
+                                            int r, int a0, int A, int f0, int F, int rowmul) {
+  const int lane = threadIdx.x & 31;
+  const unsigned key = keys[(size_t)lig * dp.N + r];
+  const int rot = 65535 - (int)(key & 0xFFFFu);
+  const int ix = rot / dp.n_a, iy = rot - ix * dp.n_a;
+  {
+    float R0s[9], T[3], Rp[9];
+    start_params(bt.idh[lig], dp.seed, r, pk.trig, pk.inv_s, pk.g.nx, pk.g.ny, pk.g.nz, R0s, T);
+    align_rx(pk.trig[ix * dp.step_a], R0s, Rp);
+    const float2 cy = pk.trig[iy * dp.step_a];
+    for (int i = lane; i < A; i += 32) {
+      const float4 d = __ldg(bt.atoms + a0 + i);
+      const float3 u = align_u(align_v(Rp, d.x, d.y, d.z), cy.x, cy.y, T);
+      P[i] = make_float4(u.x, u.y, u.z, __int_as_float((int)d.w * rowmul));
     }
   }
+  __syncwarp();
+  for (int f = 0; f < F; ++f) {
+    const int k = out.rtors[(size_t)(f0 + f) * dp.N + r];
+    if (k == 0 || k == DS_TORSION_NONE) continue;  // angle 0 / all bumped: positions unchanged
+    const uint4 fa = __ldg(bt.frags + 2 * (size_t)(f0 + f));
+    const uint4 fb = __ldg(bt.frags + 2 * (size_t)(f0 + f) + 1);
+    const unsigned mw[5] = {fa.x, fa.y, fa.z, fa.w, fb.x};
+    const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
+    const float4 pa = P[ab], pb = P[ae];
+    const float vx = __fsub_rn(pb.x, pa.x), vy = __fsub_rn(pb.y, pa.y), vz = __fsub_rn(pb.z, pa.z);
+    const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
+    const float kx = __fdiv_rn(vx, len), ky = __fdiv_rn(vy, len), kz = __fdiv_rn(vz, len);
+    const float3 a3 = make_float3(pa.x, pa.y, pa.z);
+    for (int i = lane; i < A; i += 32)
+      if ((mw[i >> 5] >> (i & 31)) & 1u) {  // axis atoms are never in the mask: read before any write
+        const float4 p = P[i];
+        const float3 q = torsion_pos(pk, dp.step_t, k, kx, ky, kz, a3, p);
+        P[i] = make_float4(q.x, q.y, q.z, p.w);
+      }
+    __syncwarp();
+  }
+  double sx = 0.0, sy = 0.0, sz = 0.0;
+  for (int i = lane; i < A; i += 32) {
+    const float4 p = P[i];
+    if (__float_as_int(p.w) != 0) {
+      sx += (double)p.x;
+      sy += (double)p.y;
+      sz += (double)p.z;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_xor_sync(kFull, sx, o);
+    sy += __shfl_xor_sync(kFull, sy, o);
+    sz += __shfl_xor_sync(kFull, sz, o);
+  }
+  if (lane == 0) {
+    cen[0] = sx;
+    cen[1] = sy;
+    cen[2] = sz;
+  }
+  __syncwarp();
+}
+
+// P12 for one pair of poses: heavy-atom sum of squared deltas in f64 in atom order (the oracle's
+// order), keep iff H > 0 and sum >= thr2 * H.  Returns true iff the poses are dissimilar.
+__device__ __noinline__ bool pose_pair_dissimilar(const float4 *up, const float4 *uq, int A, int heavy, double thr2) {
+  double sum = 0.0;
+  for (int i = 0; i < A; ++i) {
+    const float4 x = up[i], y = uq[i];
+    if (__float_as_int(x.w) == 0) continue;
+    const double dx = __dsub_rn((double)x.x, (double)y.x);
+    const double dy = __dsub_rn((double)x.y, (double)y.y);
+    const double dz = __dsub_rn((double)x.z, (double)y.z);
+    double t = __dmul_rn(dx, dx);
+    t = __dadd_rn(t, __dmul_rn(dy, dy));
+    t = __dadd_rn(t, __dmul_rn(dz, dz));
+    sum = __dadd_rn(sum, t);
+  }
+  return heavy > 0 && sum >= __dmul_rn(thr2, (double)heavy);
 }
 
 // minimum squared distance from q to the bump candidates of moving slot m beyond the inline ones:
@@ -268,7 +320,6 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
     bool degenerate = false;
     int n_aligned = dp.N;  // restarts whose alignment counts (P14; all unless a DegenerateAxis stops early)
     int deg_f = 0;         // the fragment that stopped it
-    float4 *fin = out.final_u + (size_t)(a0 - out.atom_base) * dp.N;  // final poses, restart r at r*A
 
     for (int r = 0; r < dp.N && !degenerate; ++r) {
       // ---- rebuild the aligned pose from the argmax key (P6) ----
@@ -578,9 +629,9 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         n_aligned = r + 1;
         break;
       }
-      // final geometric score (carried) + store the final pose
+      // final geometric score (carried); the select kernel replays the pose from the key and the
+      // committed torsion indices, so no pose leaves the SM
       const int sc = total;
-      for (int i = lane; i < A; i += 32) fin[(size_t)r * A + i] = S.u[i];
       const int valid = !(F >= 1 && all_bumped == F);  // P10
       if (lane == 0) {
         out.rgv[(size_t)lig * dp.N + r] = (sc * 2) | valid;
@@ -619,12 +670,19 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
   }
 }
 
+// Replay-based select_poses (P12) + rescore (P11).  Warp per ligand; the valid restarts are visited
+// in (geom desc, restart asc) order and each is replayed into a free pose slot; the RMSD to every
+// kept pose is first bounded below by the heavy-atom centroid distance (RMSD^2 >= |dc|^2 exactly,
+// so a centroid distance beyond the threshold, with a 1e-6 relative margin that dwarfs the f64
+// rounding of the sums, decides "dissimilar" exactly as the oracle's sum would), and only close
+// pairs take the oracle's sequential f64 sum (one lane per kept pose).  The kept poses are then
+// rescored from their slots.  Nothing is read back from device memory but the inputs, the keys,
+// the torsion indices and the per-restart (geom, valid) words.
 __global__ void __launch_bounds__(kOptWarps * 32)
-    k_select_batched(PocketView pk, BatchView bt, DockParams dp, const uint32_t *keys, OptOut out, int *queue) {
+    k_select_batched(PocketView pk, BatchView bt, DockParams dp, const uint32_t *keys, OptOut out, int *queue,
+                     int tables_bytes, int warp_bytes) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ SelWarpSmem s_warp[kOptWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  SelWarpSmem &S = s_warp[warp];
   // per-CTA: pocket atoms + fixed-point weights + bin bounds + bin LUT
   const int nb1 = pk.nb + 1;
   // pocket atoms as 64-atom rounds of lane pairs (j, j + 32): negated coordinates + weight columns
@@ -653,6 +711,12 @@ __global__ void __launch_bounds__(kOptWarps * 32)
   for (int j = threadIdx.x; j < wsz; j += blockDim.x) s_w[j] = __ldg(pk.wfx + j);
   if (threadIdx.x < DS_MAX_BINS) s_ub2[threadIdx.x] = pk.ub2[threadIdx.x];
   for (int j = threadIdx.x; j <= pk.lut_cap; j += blockDim.x) s_lut[j] = __ldg(pk.bin_lut + j);
+  unsigned char *wbase = smem + tables_bytes + (size_t)warp * warp_bytes;
+  SelHdr &S = *reinterpret_cast<SelHdr *>(wbase);
+  float4 *slots = reinterpret_cast<float4 *>(wbase + ((sizeof(SelHdr) + 15) & ~(size_t)15));
+  const int rowmul = DS_N_TYPES * nb1;
+  // "dissimilar by the bound": |dc|^2 (in units of H^2: sums, not means) >= thr2 H^2 (1 + 1e-6)
+  const double thr2_margin = __dmul_rn(dp.thr2, 1.000001);
   __syncthreads();
 
   for (;;) {
@@ -666,16 +730,14 @@ __global__ void __launch_bounds__(kOptWarps * 32)
     const int A = bt.atom_off[lig + 1] - a0;
     const int f0 = bt.frag_off[lig];
     const int F = bt.frag_off[lig + 1] - f0;
-    const float4 *fin = out.final_u + (size_t)(a0 - out.atom_base) * dp.N;
     // ---- select_poses (P12): order valid poses by (geom desc, restart asc) ----
     for (int r = lane; r < dp.N; r += 32) {
       const int gv = out.rgv[(size_t)lig * dp.N + r];
       S.geom[r] = gv >> 1;
       S.valid[r] = (uint8_t)(gv & 1);
-      S.dis[r] = 0u;
     }
     int hv = 0;
-    for (int i = lane; i < A; i += 32) hv += fin[i].w != 0.f;
+    for (int i = lane; i < A; i += 32) hv += __ldg(bt.atoms + a0 + i).w != 0.f;
     const int heavy = warp_sum(hv);
     __syncwarp();
     int nvalid = 0;
@@ -695,49 +757,51 @@ __global__ void __launch_bounds__(kOptWarps * 32)
       }
     }
     __syncwarp();
-    pose_dissimilarity(S, fin, A, dp.N, heavy, dp.thr2);
-    __syncwarp();
-    // greedy keep (warp-uniform)
+    // greedy keep (warp-uniform): replay each candidate into the next free slot
+    const double hh = (double)heavy * (double)heavy;
     int nk = 0;
     for (int o = 0; o < nvalid && nk < dp.K; ++o) {
       const int c = S.ord[o];
-      bool ok = true;
-      for (int t = 0; t < nk; ++t) ok = ok && ((S.dis[c] >> S.kept[t]) & 1u);
-      if (ok) {
+      float4 *cand = slots + (size_t)nk * dp.slot_atoms;
+      replay_pose(cand, S.cen[nk], pk, bt, dp, keys, out, lig, c, a0, A, f0, F, rowmul);
+      bool close = false;  // kept poses the bound cannot separate from the candidate
+      if (lane < nk) {
+        const double dx = S.cen[nk][0] - S.cen[lane][0], dy = S.cen[nk][1] - S.cen[lane][1],
+                     dz = S.cen[nk][2] - S.cen[lane][2];
+        close = !(heavy > 0 && dx * dx + dy * dy + dz * dz >= thr2_margin * hh);
+      }
+      bool dis = true;
+      if (close) dis = pose_pair_dissimilar(cand, slots + (size_t)lane * dp.slot_atoms, A, heavy, dp.thr2);
+      if (__all_sync(kFull, dis)) {
         if (lane == 0) S.kept[nk] = (uint8_t)c;
         ++nk;
-        __syncwarp();
       }
+      __syncwarp();
     }
     // ---- rescore kept poses (P11): exact fixed-point sum over (ligand atom, pocket atom) ----
     long long best_chem = 0;
-    int best_r = -1;
+    int best_r = -1, best_t = 0;
     for (int t = 0; t < nk; ++t) {
       const int r = S.kept[t];
-      __syncwarp();
-      for (int i = lane; i < A; i += 32) {
-        float4 x = fin[(size_t)r * A + i];
-        x.w = __int_as_float((int)x.w * DS_N_TYPES * nb1);  // row offset of the ligand atom's type
-        S.u[i] = x;
-      }
-      __syncwarp();
+      const float4 *su = slots + (size_t)t * dp.slot_atoms;
       // int32 partials when two weight terms fit (every default-like table), int64 otherwise
       long long acc;
       if (pk.part_terms >= 2 && pk.lut_cap >= 0 && pk.lut_full)
-        acc = rescore_pose_x2<2, int>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, pk.lut_shift,
+        acc = rescore_pose_x2<2, int>(su, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, pk.lut_shift,
                                       pk.lut_cap, pk.part_terms / 2);
       else if (pk.part_terms >= 2 && pk.lut_cap >= 0)
-        acc = rescore_pose_x2<1, int>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, pk.lut_shift,
+        acc = rescore_pose_x2<1, int>(su, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, pk.lut_shift,
                                       pk.lut_cap, pk.part_terms / 2);
       else if (pk.part_terms >= 2)
-        acc = rescore_pose_x2<0, int>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0, 0,
+        acc = rescore_pose_x2<0, int>(su, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0, 0,
                                       pk.part_terms / 2);
       else
-        acc = rescore_pose_x2<0, long long>(S, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0, 0, A);
+        acc = rescore_pose_x2<0, long long>(su, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0, 0, A);
       acc = warp_sum64(acc);
       if (best_r < 0 || acc > best_chem || (acc == best_chem && r < best_r)) {
         best_chem = acc;
         best_r = r;
+        best_t = t;
       }
       if (lane == 0 && out.rrec) out.rrec[(size_t)lig * dp.N + r].kept = (uint8_t)(t + 1);
     }
@@ -752,7 +816,7 @@ __global__ void __launch_bounds__(kOptWarps * 32)
     res.n_kept = (uint8_t)nk;
     if (lane == 0) out.res[lig] = res;
     if (out.best_coords) {
-      const float4 *ub = fin + (size_t)best_r * A;
+      const float4 *ub = slots + (size_t)best_t * dp.slot_atoms;
       for (int i = lane; i < A; i += 32) {  // back to Å: q = fma(u, s, o)   (P2)
         const float4 x = ub[i];
         float *o = out.best_coords + 3 * (size_t)(a0 + i);
@@ -767,10 +831,19 @@ __global__ void __launch_bounds__(kOptWarps * 32)
   }
 }
 
-size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap) {
+static size_t select_tables_bytes(int n_patoms, int nb, int lut_cap) {
   size_t fixed = (size_t)((n_patoms + 63) / 64) * 32 * 32 + (size_t)DS_N_TYPES * DS_N_TYPES * (nb + 1) * 4 +
                  DS_MAX_BINS * 4 + (size_t)(lut_cap + 1);
   return (fixed + 15) & ~(size_t)15;
+}
+static size_t select_warp_bytes(int K, int slot_atoms) {
+  // the candidate is replayed into slot nk < K, so K slots hold the kept poses and the candidate
+  return ((sizeof(SelHdr) + 15) & ~(size_t)15) + (size_t)K * slot_atoms * sizeof(float4);
+}
+// dynamic shared memory of a k_select_batched CTA (kOptWarps warps) for top-K K and ligands of at
+// most slot_atoms atoms
+size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap, int K, int slot_atoms) {
+  return select_tables_bytes(n_patoms, nb, lut_cap) + kOptWarps * select_warp_bytes(K, slot_atoms);
 }
 
 constexpr size_t kTorSmem = kTorWarps * sizeof(TorWarpSmem);
@@ -786,10 +859,28 @@ void launch_torsion_batched(const PocketView &pk, const BatchView &bt, const Doc
   }
 }
 
+// warps per CTA (1..kOptWarps) chosen for the most resident warps per SM: every CTA carries its
+// own rescore tables beside its warps' pose slots (one warp always fits: 32 slots x 160 atoms x
+// 16 B + the tables)
 void launch_select_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const uint32_t *keys,
-                           OptOut out, int *queue, int blocks, size_t smem, cudaStream_t st) {
+                           OptOut out, int *queue, int sm_count, size_t smem_optin, cudaStream_t st) {
+  const size_t tb = select_tables_bytes(pk.n_atoms, pk.nb, pk.lut_cap), wb = select_warp_bytes(dp.K, dp.slot_atoms);
+  int best_w = 1, best_res = 0, best_per_sm = 1;
+  for (int w = 1; w <= kOptWarps; ++w) {
+    const size_t smem = tb + w * wb;
+    if (smem > smem_optin) break;
+    cudaFuncSetAttribute(k_select_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_batched, w * 32, smem);
+    if (per_sm * w >= best_res) {
+      best_res = per_sm * w;
+      best_w = w;
+      best_per_sm = std::max(1, per_sm);
+    }
+  }
+  const size_t smem = tb + best_w * wb;
   cudaFuncSetAttribute(k_select_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_select_batched<<<blocks, kOptWarps * 32, smem, st>>>(pk, bt, dp, keys, out, queue);
+  k_select_batched<<<sm_count * best_per_sm, best_w * 32, smem, st>>>(pk, bt, dp, keys, out, queue, (int)tb, (int)wb);
 }
 
 int torsion_blocks_per_sm() {

@@ -115,3 +115,15 @@ def test_chem_score_vs_f64_ordered_sum(gpu_ctx, synth_pocket, table):
             assert top[-1] - top[-2] <= 1e-4 * max(abs(top[-1]), 1.0) + 1.0, (i, sums)
     print(f"\nf64 ordered-sum restatement: {checked} ligands, {ties} bin-boundary ties, {flips} best_restart flips")
     assert checked > 100 and flips <= 2
+
+
+def test_select_replay_extremes(gpu_ctx, synth_pocket, table):
+    """The replay-based select (poses rebuilt from the keys and the committed torsions, K pose slots
+    per warp in shared memory): 160-atom ligands with N = K = 32 (the largest slots: one warp per
+    CTA) and K = 1, against the oracle."""
+    big = io.generate_dataset_batch(70, 30, 6, seed=12)
+    mixed = io.generate_mixed_batch(30, seed=13)
+    for cfg in (model.DockConfig(restarts_n=32, rescore_top_k=32), model.DockConfig(restarts_n=8, rescore_top_k=1)):
+        for b in (big, mixed):
+            o = oracle.dock_batch(b, synth_pocket, table, cfg, 2)
+            compare(b, _run(gpu_ctx, b, synth_pocket, table, cfg, 2), o, cfg)
