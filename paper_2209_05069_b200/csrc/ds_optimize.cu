@@ -293,7 +293,9 @@ __device__ __noinline__ void clear_unreached(const OptOut &out, int N, int f0, i
   }
 }
 
-template <bool kEarly>  // DockConfig.early_exit, compiled in
+// kEarly: DockConfig.early_exit; kNT: the torsion angle count when it is the default
+// 10 (torsion_step_deg = 36: the sweep's lane layout and loops become constants), 0 = runtime
+template <bool kEarly, int kNT>
 __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
     k_torsion_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
                       OptOut out, int *queue) {
@@ -487,11 +489,19 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         // Angle 0 (the identity, P7) runs the same code with R = I about the origin: w = p - 0 = p and
         // fma(0, ., fma(0, ., fma(1, p, 0))) = p up to the sign of a zero, which changes neither a
         // node nor a squared distance (and angle 0 is never committed).
-        for (int k0 = 0; k0 < dp.n_t; k0 += 32) {
-          const int nA = min(32, dp.n_t - k0);
+        const int n_t = kNT ? kNT : dp.n_t;
+        for (int k0 = 0; k0 < n_t; k0 += 32) {
+          const int nA = kNT ? kNT : min(32, n_t - k0);
           int G, a, gi;                           // moving-atom groups per round, lane's angle and group
           unsigned same;                          // lanes that share this lane's angle
-          if (k0 == 0) {                          // host-built layout of the first block
+          if (kNT) {                              // compile-time layout: lane = gi * kNT + a
+            G = 32 / kNT;
+            a = lane % kNT;
+            gi = lane / kNT;
+            same = 0;
+#pragma unroll
+            for (int t = 0; t < 32 / kNT; ++t) same |= 1u << (a + t * kNT);
+          } else if (k0 == 0) {                   // host-built layout of the first block
             const unsigned e = dp.sweep_lane[lane];
             a = (int)(e & 0xFFu);
             gi = (int)((e >> 8) & 0xFFu);
@@ -848,14 +858,22 @@ size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap, int K, int slot_
 
 constexpr size_t kTorSmem = kTorWarps * sizeof(TorWarpSmem);
 
+template <bool E, int NT>
+static void launch_tors(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
+                        const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st) {
+  cudaFuncSetAttribute(k_torsion_batched<E, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
+  k_torsion_batched<E, NT><<<blocks, kTorWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
+}
+
 void launch_torsion_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                             const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st) {
+  const bool nt10 = dp.n_t == 10;
   if (dp.early_exit) {
-    cudaFuncSetAttribute(k_torsion_batched<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
-    k_torsion_batched<true><<<blocks, kTorWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
+    if (nt10) launch_tors<true, 10>(pk, bt, dp, order, keys, out, queue, blocks, st);
+    else launch_tors<true, 0>(pk, bt, dp, order, keys, out, queue, blocks, st);
   } else {
-    cudaFuncSetAttribute(k_torsion_batched<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
-    k_torsion_batched<false><<<blocks, kTorWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
+    if (nt10) launch_tors<false, 10>(pk, bt, dp, order, keys, out, queue, blocks, st);
+    else launch_tors<false, 0>(pk, bt, dp, order, keys, out, queue, blocks, st);
   }
 }
 
@@ -885,8 +903,8 @@ void launch_select_batched(const PocketView &pk, const BatchView &bt, const Dock
 
 int torsion_blocks_per_sm() {
   int n = 0;
-  cudaFuncSetAttribute(k_torsion_batched<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_torsion_batched<true>, kTorWarps * 32, kTorSmem);
+  cudaFuncSetAttribute(k_torsion_batched<true, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_torsion_batched<true, 10>, kTorWarps * 32, kTorSmem);
   return n;
 }
 
