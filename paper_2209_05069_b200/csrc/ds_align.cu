@@ -405,7 +405,7 @@ int align_warp_smem_bytes_host(int N) { return align_warp_smem_bytes(N); }
 template <int NA, int G, bool S>
 static void launch_t(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order, AlignOut out,
                      int *queue, int blocks, int warps, size_t smem, cudaStream_t st) {
-  cudaFuncSetAttribute(k_align_batched<NA, G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_max_smem((const void *)k_align_batched<NA, G, S>);
   k_align_batched<NA, G, S><<<blocks, warps * 32, smem, st>>>(pk, bt, dp, order, out, queue);
 }
 
@@ -413,7 +413,7 @@ static void launch_t(const PocketView &pk, const BatchView &bt, const DockParams
 // launch shape: the occupancy API on the real kernel (ds_query_capacity)
 int align_blocks_per_sm(int warps, size_t smem) {
   int n = 0;
-  cudaFuncSetAttribute(k_align_batched<30, 30, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_max_smem((const void *)k_align_batched<30, 30, true>);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_align_batched<30, 30, true>, warps * 32, smem);
   return n;
 }

@@ -184,6 +184,22 @@ __device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
   return r;
 }
 
+// The per-function dynamic shared-memory limit is process-wide state: contexts on concurrent host
+// threads launching one kernel with different sizes would race on it (a launch after another
+// thread lowered it fails with "too many resources"), so it is always raised to the device's
+// opt-in maximum; every launch still passes its own size.
+inline void allow_max_smem(const void *func) {
+  static const int max_smem = [] {
+    int d = 0, v = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+    return v;
+  }();
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, func) != cudaSuccess) return;
+  cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem - (int)fa.sharedSizeBytes);
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

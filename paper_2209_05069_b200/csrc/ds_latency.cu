@@ -634,7 +634,7 @@ void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const Do
   const bool fits = with_grid + sizeof(LatSmem) + 1024 <= (size_t)optin;
   auto kern = fits ? k_optimize_latency<true> : k_optimize_latency<false>;
   const size_t smem = fits ? with_grid : base;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_max_smem((const void *)kern);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(bt.L * dp.N);
   cfg.blockDim = dim3(kLatThreads);

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256) k_build_pocket(const float *atom_xyz, int
 void launch_build_pocket(const float *atom_xyz, int P, const double *origin, double s, const int *dims,
                          int32_t *values, int sm_count, cudaStream_t st) {
   const size_t smem = sizeof(double) * 3 * (size_t)P;
-  cudaFuncSetAttribute(k_build_pocket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_max_smem((const void *)k_build_pocket);
   k_build_pocket<<<sm_count * 8, 256, smem, st>>>(atom_xyz, P, origin[0], origin[1], origin[2], s, dims[0], dims[1],
                                                   dims[2], values);
 }

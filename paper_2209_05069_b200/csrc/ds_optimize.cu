@@ -861,7 +861,7 @@ constexpr size_t kTorSmem = kTorWarps * sizeof(TorWarpSmem);
 template <bool E, int NT>
 static void launch_tors(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                         const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st) {
-  cudaFuncSetAttribute(k_torsion_batched<E, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
+  allow_max_smem((const void *)k_torsion_batched<E, NT>);
   k_torsion_batched<E, NT><<<blocks, kTorWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
 }
 
@@ -887,7 +887,7 @@ void launch_select_batched(const PocketView &pk, const BatchView &bt, const Dock
   for (int w = 1; w <= kOptWarps; ++w) {
     const size_t smem = tb + w * wb;
     if (smem > smem_optin) break;
-    cudaFuncSetAttribute(k_select_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    allow_max_smem((const void *)k_select_batched);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_batched, w * 32, smem);
     if (per_sm * w >= best_res) {
@@ -897,20 +897,20 @@ void launch_select_batched(const PocketView &pk, const BatchView &bt, const Dock
     }
   }
   const size_t smem = tb + best_w * wb;
-  cudaFuncSetAttribute(k_select_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_max_smem((const void *)k_select_batched);
   k_select_batched<<<sm_count * best_per_sm, best_w * 32, smem, st>>>(pk, bt, dp, keys, out, queue, (int)tb, (int)wb);
 }
 
 int torsion_blocks_per_sm() {
   int n = 0;
-  cudaFuncSetAttribute(k_torsion_batched<true, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTorSmem);
+  allow_max_smem((const void *)k_torsion_batched<true, 10>);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_torsion_batched<true, 10>, kTorWarps * 32, kTorSmem);
   return n;
 }
 
 int select_blocks_per_sm(size_t smem) {
   int n = 0;
-  cudaFuncSetAttribute(k_select_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  allow_max_smem((const void *)k_select_batched);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_select_batched, kOptWarps * 32, smem);
   return n;
 }
