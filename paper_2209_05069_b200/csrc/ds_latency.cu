@@ -121,7 +121,8 @@ __device__ __forceinline__ float lat_min_d2(const LatSmem &S, int m, int nC, flo
   return mind;
 }
 
-template <bool kSmemGrid>
+// kNT: the torsion angle count when it is the default 10 (compile-time sweep layout), 0 = runtime
+template <bool kSmemGrid, int kNT>
 __global__ void __launch_bounds__(kLatThreads, 1)
     k_optimize_latency(PocketView pk, BatchView bt, DockParams dp, int *scores, const unsigned *keys, OptOut out,
                        LatRec *recs, int *done) {
@@ -311,8 +312,9 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     // ---- (D) the angle sweep: thread = (angle a, moving-atom group mg); rotation and partial score
     // in registers over m = mg, mg + G, ...; one shared atomic per thread at the end ----
     unsigned best_key = 0u;
-    for (int k0 = 0; k0 < dp.n_t; k0 += 32) {
-      const int nA = min(32, dp.n_t - k0);
+    const int n_t = kNT ? kNT : dp.n_t;
+    for (int k0 = 0; k0 < n_t; k0 += 32) {
+      const int nA = kNT ? kNT : min(32, n_t - k0);
       if (k0 > 0) {
         __syncthreads();
         if (tid < 32) {
@@ -323,8 +325,8 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         __syncthreads();
       }
       // thread = (angle a, group mg), exact reciprocal division (no integer divide on the chain)
-      const int G = small_div(kLatThreads, nA);
-      const int mg = small_div(tid, nA), a = tid - mg * nA;
+      const int G = kNT ? kLatThreads / kNT : small_div(kLatThreads, nA);
+      const int mg = kNT ? tid / kNT : small_div(tid, nA), a = tid - mg * nA;
       if (mg < G) {
         float R[9];
         const int kang = k0 + a;
@@ -627,12 +629,17 @@ size_t latency_rec_bytes() { return sizeof(LatRec); }
 void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
                              const unsigned *keys, OptOut out, void *recs, int *done, bool pdl, cudaStream_t st) {
   const size_t base = lat_base_bytes(pk.nb, pk.lut_cap);
-  int dev = 0, optin = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  static const int optin = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+  }();
   const size_t with_grid = base + (size_t)pk.grid_bytes;
   const bool fits = with_grid + sizeof(LatSmem) + 1024 <= (size_t)optin;
-  auto kern = fits ? k_optimize_latency<true> : k_optimize_latency<false>;
+  const bool nt10 = dp.n_t == 10;
+  auto kern = fits ? (nt10 ? k_optimize_latency<true, 10> : k_optimize_latency<true, 0>)
+                   : (nt10 ? k_optimize_latency<false, 10> : k_optimize_latency<false, 0>);
   const size_t smem = fits ? with_grid : base;
   allow_max_smem((const void *)kern);
   cudaLaunchConfig_t cfg = {};
