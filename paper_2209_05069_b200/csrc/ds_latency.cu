@@ -44,7 +44,6 @@ struct LatSmem {
   uint8_t clist[DS_MAX_ATOMS];
   uint8_t cl[DS_MAX_ATOMS][kLatCand];  // bump candidates (atom indices) per moving atom
   unsigned cn[DS_MAX_ATOMS];           // their count (> kLatCand: scan all of C')
-  int base[2];                  // grid score of the non-moving atoms, by fragment parity
   int ascore[32];
   int bcode[32];                // early exit: the smallest bumping moving slot per angle (P14 rows)
   unsigned abump;
@@ -162,8 +161,6 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     S.geom = 0;
     S.degen = 0;
     S.heavy = 0;
-    S.base[0] = 0;
-    S.base[1] = 0;
   }
   for (int i = lut_bulk + tid; i < lut_n; i += kLatThreads) slut[i] = __ldg(pk.bin_lut + i);  // < 16 B tail
   __syncthreads();
@@ -188,6 +185,10 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   __syncthreads();
   mbar_wait(&bar[0], 0);
   const unsigned key = S.key;
+  // grid score of the current pose carried along the fragment chain (the aligned pose scores the
+  // key's score, a committed angle its key's): a fragment's non-moving atoms score total - the
+  // angle-0 sum of its moving atoms, so phase (A) reads no grid value and the end no pass
+  int total = (int)(key >> 16) - 32768;
   const int rot = 65535 - (int)(key & 0xFFFFu);
   const int ix = rot / dp.n_a, iy = rot - ix * dp.n_a;
   {
@@ -257,33 +258,22 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         nC += __popc(bc);
       }
     }
-    {
-      int part = 0;
-      if (tid < A) {
-        const float4 p = S.u[tid];
-        if ((my_bm >> lane) & 1u) {
-          S.mlist[mpre] = (uint8_t)tid;
-          S.chm[mpre] = lat_cyl(p, a3, kx, ky, kz);
-          S.cn[mpre] = 0;
-        } else {
-          if ((my_bc >> lane) & 1u) {
-            S.clist[cpre] = (uint8_t)tid;
-            S.chr[cpre] = lat_cyl(p, a3, kx, ky, kz);
-          }
-          part = lat_grid_val<kSmemGrid>(grid, node_index(g, p.x, p.y, p.z));
-        }
+    if (tid < A) {
+      const float4 p = S.u[tid];
+      if ((my_bm >> lane) & 1u) {
+        S.mlist[mpre] = (uint8_t)tid;
+        S.chm[mpre] = lat_cyl(p, a3, kx, ky, kz);
+        S.cn[mpre] = 0;
+      } else if ((my_bc >> lane) & 1u) {
+        S.clist[cpre] = (uint8_t)tid;
+        S.chr[cpre] = lat_cyl(p, a3, kx, ky, kz);
       }
-      part = (int)__reduce_add_sync(kFull, (unsigned)part);
-      if (lane == 0 && part) atomicAdd(&S.base[f & 1], part);
     }
     if (tid < 32) {
       S.ascore[tid] = 0;
       S.bcode[tid] = 0x7FFFFFFF;
     }
-    if (tid == 0) {
-      S.abump = 0u;
-      S.base[(f + 1) & 1] = 0;  // last read in fragment f - 1's (E)
-    }
+    if (tid == 0) S.abump = 0u;
     __syncthreads();
     // ---- (C) bump candidates: every (moving, complement) pair over all threads (cylindrical
     // bound, see ds_optimize.cu) ----
@@ -312,6 +302,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     // ---- (D) the angle sweep: thread = (angle a, moving-atom group mg); rotation and partial score
     // in registers over m = mg, mg + G, ...; one shared atomic per thread at the end ----
     unsigned best_key = 0u;
+    int base = 0;  // score of the atoms the torsion does not move
     const int n_t = kNT ? kNT : dp.n_t;
     for (int k0 = 0; k0 < n_t; k0 += 32) {
       const int nA = kNT ? kNT : min(32, n_t - k0);
@@ -341,8 +332,9 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         // early exit: a thread stops once its next atom lies beyond the first bumping slot found so far
         // for its angle; every slot up to the sequential scan's first bump is then tested, so the
         // minimum (and the pair count derived from it) is independent of thread timing (P14)
+        // angle 0 always runs to the end: its complete sum gives the non-moving atoms' score
         for (int m = mg; m < nM; m += 2 * G) {
-          if (dp.early_exit && (hit_any || m > *(volatile int *)&S.bcode[a])) break;
+          if (dp.early_exit && kang != 0 && (hit_any || m > *(volatile int *)&S.bcode[a])) break;
           const bool two = m + G < nM;
           const int m1 = two ? m + G : m;
           const float4 p0 = S.u[S.mlist[m]], p1 = S.u[S.mlist[m1]];
@@ -351,13 +343,13 @@ __global__ void __launch_bounds__(kLatThreads, 1)
           const int gv0 = lat_grid_val<kSmemGrid>(grid, node_index(g, q0.x, q0.y, q0.z));
           const int gv1 = lat_grid_val<kSmemGrid>(grid, node_index(g, q1.x, q1.y, q1.z));
           const float d0 = lat_min_d2(S, m, nC, q0), d1 = lat_min_d2(S, m1, nC, q1);
-          if (d0 < dp.bd2 || d1 < dp.bd2) {
+          const bool hit = d0 < dp.bd2 || d1 < dp.bd2;
+          if (hit) {
             hit_any = true;
             atomicOr(&S.abump, 1u << a);
             if (dp.early_exit) atomicMin(&S.bcode[a], d0 < dp.bd2 ? m : m1);
-          } else {
-            part += two ? gv0 + gv1 : gv0;
           }
+          if (!hit || kang == 0) part += two ? gv0 + gv1 : gv0;
         }
         if (part) atomicAdd(&S.ascore[a], part);
       }
@@ -376,7 +368,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
       // ---- (E) best clean angle, computed by every warp (no extra barrier) ----
       const unsigned abump = S.abump;
       unsigned kk = 0;
-      const int base = S.base[f & 1];
+      if (k0 == 0) base = total - S.ascore[0];
       if (lane < nA && !((abump >> lane) & 1u))
         kk = ((unsigned)(base + S.ascore[lane] + 32768) << 16) | (unsigned)(65535 - (k0 + lane));
       best_key = max(best_key, __reduce_max_sync(kFull, kk));
@@ -384,6 +376,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
       if (dp.early_exit) exits += (unsigned)__popc(abump);
     }
     const int best_k = best_key ? 65535 - (int)(best_key & 0xFFFFu) : -1;
+    if (best_key) total = (int)(best_key >> 16) - 32768;  // the committed pose's score
     if (tid == 0) out.rtors[(size_t)(f0 + f) * dp.N + r] = best_k < 0 ? (uint8_t)DS_TORSION_NONE : (uint8_t)best_k;
     if (best_k > 0)
       for (int m = tid; m < nM; m += kLatThreads) {
@@ -400,19 +393,15 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   const int degen = S.degen;
   float4 *scr = out.final_u + ((size_t)lig * dp.N + r) * DS_MAX_ATOMS;
   if (!degen) {
-    int sc = 0, hv = 0;
+    int hv = 0;
     for (int i = tid; i < A; i += kLatThreads) {
       const float4 p = S.u[i];
-      sc += lat_grid_val<kSmemGrid>(grid, node_index(g, p.x, p.y, p.z));
       hv += p.w != 0.f;
       scr[i] = p;
     }
-    sc = (int)__reduce_add_sync(kFull, (unsigned)sc);
     hv = (int)__reduce_add_sync(kFull, (unsigned)hv);
-    if (lane == 0) {
-      atomicAdd(&S.geom, sc);
-      atomicAdd(&S.heavy, hv);
-    }
+    if (lane == 0) atomicAdd(&S.heavy, hv);
+    if (tid == 0) S.geom = total;
   }
   if (tid == 0) S.chem = 0ull;
   __syncthreads();
