@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         const float4 pa = S.u[ab], pb = S.u[ae];
         const float3 a3 = make_float3(pa.x, pa.y, pa.z);
         float kx = 0.f, ky = 0.f, kz = 0.f;
-        if (dp.n_t > 1) {
+        if (kNT > 1 || (kNT == 0 && dp.n_t > 1)) {
           const float vx = __fsub_rn(pb.x, pa.x), vy = __fsub_rn(pb.y, pa.y), vz = __fsub_rn(pb.z, pa.z);
           const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
           if (!(len >= dp.eps_axis)) {  // DegenerateAxis
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           float R[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
           float3 ar = make_float3(0.f, 0.f, 0.f);
           if (kang > 0) {
-            const float2 cs = pk.trig[kang * dp.step_t];
+            const float2 cs = pk.trig[kang * (kNT ? 360 / kNT : dp.step_t)];
             torsion_matrix(kx, ky, kz, cs.x, cs.y, R);
             ar = a3;
           }
@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
               const float4 W = make_float4(reinterpret_cast<const float *>(S.mxp)[m],
                                            reinterpret_cast<const float *>(S.myp)[m],
                                            reinterpret_cast<const float *>(S.mzp)[m], 0.f);
-              const float3 q = torsion_pos(pk, dp.step_t, best_k, kx, ky, kz, a3, W);
+              const float3 q = torsion_pos(pk, kNT ? 360 / kNT : dp.step_t, best_k, kx, ky, kz, a3, W);
               S.u[i] = make_float4(q.x, q.y, q.z, S.u[i].w);
             }
             mr += __popc(bm);
