@@ -213,7 +213,7 @@ int ds_batch_read_inputs(ds_ctx *ctx, const ds_dev_batch *batch, float *atom_xyz
                          uint64_t *id_hash);
 /* Batch capacity for atom range `range_idx` (0..4) on this device — the B200 analogue of the
  * paper's occupancy-derived batch size (replaces SPEC.md:332 bucket_capacity's
- * fixed A100 numbers): SMs x the smallest resident-warp count of the three batched kernels
+ * fixed A100 numbers): SMs x the smaller resident-warp count of the alignment and torsion kernels
  * (cudaOccupancyMaxActiveBlocksPerMultiprocessor on the kernels themselves; one ligand per warp)
  * x DS_CAPACITY_WAVES (default 2).  The same for every range: the kernels are not
  * range-specialised. */

@@ -1310,9 +1310,10 @@ int ds_query_capacity(ds_ctx *c, int range_idx, int *ligands) {
   // PAPER.md:382-384 sizes a batch as the ligands one launch keeps resident, from
   // cudaOccupancyMaxActiveBlocksPerMultiprocessor on the range's kernel.  The batched kernels here
   // give a warp to a ligand of any size (per-warp scratch for 160 atoms), so the resident ligand
-  // slots are the same for every range: SMs x the smallest resident-warp count of the three
-  // batched kernels (alignment with the synthetic-pocket grid in shared memory, torsion, select
-  // with 200 pocket atoms and the default bins).  A batch is `waves` such launches' worth
+  // slots are the same for every range: SMs x the smaller resident-warp count of the alignment
+  // (synthetic-pocket grid in shared memory) and torsion kernels, ~90 % of the step; the select
+  // kernel's residency is set by its per-warp pose slots (top-K x the batch's largest ligand),
+  // which a batch does not know before it is filled.  A batch is `waves` such launches' worth
   // (DS_CAPACITY_WAVES, default 2): persistent CTAs drain an LPT queue, so more than one wave
   // amortises the tail of the slowest ligands.
   const int N = 8;
@@ -1323,9 +1324,8 @@ int ds_query_capacity(ds_ctx *c, int range_idx, int *ligands) {
     warps_a = (int)std::min<size_t>(32, (c->smem_optin - grid_bytes - fixed) / per_warp);
   const int wa = warps_a * align_blocks_per_sm(warps_a, grid_bytes + fixed + per_warp * warps_a);
   const int wt = 8 * torsion_blocks_per_sm();
-  const int ws = 8 * select_blocks_per_sm(select_cta_smem_bytes(200, 4, 1080, 4, 120));
   cudaGetLastError();
-  const int per_sm = std::min(wa, std::min(wt, ws));
+  const int per_sm = std::min(wa, wt);
   if (per_sm <= 0) return fail(DS_ERR_CUDA, "occupancy query returned 0 resident warps");
   static const int waves = [] {
     const char *e = getenv("DS_CAPACITY_WAVES");
