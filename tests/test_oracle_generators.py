@@ -70,3 +70,24 @@ def test_latency_shaped_oracle_equals_batched():
         assert np.array_equal(a.restarts, c.restarts)
         assert np.array_equal(a.restart_torsion, c.restart_torsion)
         assert np.array_equal(a.best_coords, c.best_coords)
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the driver's reference arm) on a tiny sample: one JSON line with the
+    contract's keys, the CPU oracle as a port, e2e == value with no copies, and the product library
+    never mapped into that process."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0", "--cpu-sample", "16"], capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, OMP_NUM_THREADS="4"))
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "cpu_baseline", "e2e", "config"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "port" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
