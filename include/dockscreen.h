@@ -161,6 +161,9 @@ typedef struct ds_stats {
                                       (0 when the call is chunked and it is not timed separately) */
   int64_t h2d_bytes;
   int64_t d2h_bytes;
+  int32_t lat_spread;              /* latency family: CTAs per (ligand, restart) in the optimisation
+                                      kernel — 1 = the sequential fragment chain on one SM, n_t = the
+                                      cluster-speculative kernel; 0 = batched family */
 } ds_stats;
 
 /* ---- library / context -------------------------------------------------- */

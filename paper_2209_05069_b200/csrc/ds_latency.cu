@@ -15,7 +15,16 @@
 //                                    finish runs select_poses and picks the best kept pose
 //                                    (PAPER.md:344-348).
 // Numeric recipe identical to the batched family: results are bit-identical.
+#include <cooperative_groups.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <map>
+#include <mutex>
+
 #include "ds_kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ds {
 
@@ -36,6 +45,22 @@ struct LatRec {  // per (ligand, restart), read by the ligand's last CTA
 
 constexpr int kLatCand = 8;
 
+// state of the per-restart tail (final pose, rescore, record; the ligand's last CTA: select)
+struct LatTail {
+  int is_last;
+  int geom;
+  int ord[DS_MAX_RESTARTS], kept[DS_MAX_RESTARTS], nkept;
+  unsigned dis[DS_MAX_RESTARTS];
+  unsigned long long chem;
+  int heavy;
+  int s_geom[DS_MAX_RESTARTS], s_valid[DS_MAX_RESTARTS];
+  unsigned s_cnt[4], s_nal;
+  int s_degf;
+  LatRec rec[DS_MAX_RESTARTS];  // the ligand's per-restart records, staged by the last CTA
+  int nvp;                      // valid restart pairs
+  uint16_t vp[DS_MAX_RESTARTS * (DS_MAX_RESTARTS - 1) / 2];  // ... as p | q << 8
+};
+
 struct LatSmem {
   float4 u[DS_MAX_ATOMS];
   float2 chr[DS_MAX_ATOMS];     // cylindrical (h, r) of the C' atoms
@@ -48,13 +73,9 @@ struct LatSmem {
   int bcode[32];                // early exit: the smallest bumping moving slot per angle (P14 rows)
   unsigned abump;
   unsigned key;
-  int degen, degen_f, is_last;
+  int degen, degen_f;
   unsigned pairs;
-  int geom;
-  int ord[DS_MAX_RESTARTS], kept[DS_MAX_RESTARTS], nkept;
-  unsigned dis[DS_MAX_RESTARTS];
-  unsigned long long chem;
-  int heavy;
+  LatTail t;
 };
 
 // dynamic shared memory: [trig 360][fragment records][weights][bin LUT][grid (if it fits)]
@@ -120,6 +141,340 @@ __device__ __forceinline__ float lat_min_d2(const LatSmem &S, int m, int nC, flo
   return mind;
 }
 
+#ifdef DS_SPEC_PROBE
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ unsigned long long g_marks[64][8];
+__device__ long long g_steps[16][16][8];  // spread kernel, cluster 0: [CTA][step][point] clock64 deltas
+#define SPROBE(k) \
+  if (blockIdx.x < kSpecH && (f >> 1) < 16) g_steps[blockIdx.x][f >> 1][k] = clock64() - t_step
+#define MARK(tag, id) \
+  if (threadIdx.x == 0) g_marks[(id) & 63][tag] = gtimer()
+#else
+#define MARK(tag, id)
+#define SPROBE(k)
+#endif
+
+// a slice of the rescore sum (P11) of the pose U by thread t of nth: with enough threads, one
+// work unit (pocket atom j, chunk of <= 16 ligand atoms) each, else a pocket atom per thread
+// (loaded once) over every chunk.  Each int32 partial holds at most part_terms terms, so it cannot
+// overflow; the 64-bit total is exact, hence independent of the split.
+__device__ __forceinline__ int lat_rescore_chunk(const float4 *U, int i0, int i1, float4 y, const int32_t *wcol, int nb1,
+                                                 const PocketView &pk, const uint8_t *slut) {
+  int part = 0;
+#pragma unroll 4
+  for (int i = i0; i < i1; ++i) {
+    const float4 x = U[i];
+    const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
+    part += wcol[(int)x.w * DS_N_TYPES * nb1 + lat_bin(pk, slut, d2)];
+  }
+  return part;
+}
+__device__ __forceinline__ long long lat_rescore_acc(const float4 *U, int A, const PocketView &pk, const int32_t *sw,
+                                                     const uint8_t *slut, int t, int nth) {
+  const int nb1 = pk.nb + 1;
+  const int CH = min(pk.part_terms, 16);
+  const int nch = (A + CH - 1) / CH;
+  long long acc = 0;
+  if (pk.n_atoms * nch <= nth) {
+    if (t < pk.n_atoms * nch) {
+      const int j = t / nch, c = t - j * nch;
+      const float4 y = __ldg(pk.patoms + j);
+      acc = lat_rescore_chunk(U, c * CH, min(A, c * CH + CH), y, sw + (int)y.w * nb1, nb1, pk, slut);
+    }
+    return acc;
+  }
+  for (int j = t; j < pk.n_atoms; j += nth) {
+    const float4 y = __ldg(pk.patoms + j);
+    const int32_t *wcol = sw + (int)y.w * nb1;
+    for (int i0 = 0; i0 < A; i0 += CH) acc += lat_rescore_chunk(U, i0, min(A, i0 + CH), y, wcol, nb1, pk, slut);
+  }
+  return acc;
+}
+
+// one atom's term of the RMSD sum (P12): (dx^2 + dy^2) + dz^2 in f64, 0 for a hydrogen
+__device__ __forceinline__ double rmsd_term(float4 x, float4 y) {
+  if (x.w == 0.f) return 0.0;
+  const double dx = __dsub_rn((double)x.x, (double)y.x);
+  const double dy = __dsub_rn((double)x.y, (double)y.y);
+  const double dz = __dsub_rn((double)x.z, (double)y.z);
+  double v = __dmul_rn(dx, dx);
+  v = __dadd_rn(v, __dmul_rn(dy, dy));
+  return __dadd_rn(v, __dmul_rn(dz, dz));
+}
+
+// the restart's tail, entered by every thread of the CTA with U final (after a barrier) and
+// T.heavy = T.geom = T.chem = 0: final pose to the scratch, grid score, speculative rescore
+// (P11; kRescore false: the caller has summed it into T.chem), the per-restart record; the
+// ligand's last CTA to finish runs select_poses (P12) and writes the ligand's result
+//
+template <int NTH, bool kRescore>
+__device__ __forceinline__ void lat_tail(LatTail &T, const float4 *U, int degen, int degen_f, int total, int valid,
+                                         unsigned key, int ix, int iy, int rot, unsigned evals, unsigned pairs,
+                                         unsigned exits, const PocketView &pk, const DockParams &dp, const int32_t *sw,
+                                         const uint8_t *slut, const OptOut &out, LatRec *recs, int *done, int lig,
+                                         int r, int a0, int A, int f0, int F, float4 *stage, int stage_bytes) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  // ---- final pose, geometric score, per-restart record ----
+  float4 *scr = out.final_u + ((size_t)lig * dp.N + r) * DS_MAX_ATOMS;
+  if (!degen) {
+    int hv = 0;
+    for (int i = tid; i < A; i += NTH) {
+      const float4 p = U[i];
+      hv += p.w != 0.f;
+      scr[i] = p;
+    }
+    hv = (int)__reduce_add_sync(kFull, (unsigned)hv);
+    if (lane == 0) atomicAdd(&T.heavy, hv);
+    if (tid == 0) T.geom = total;
+  }
+  __syncthreads();
+  // ---- speculative rescore of this restart's pose (P11, exact fixed point): every CTA of the
+  // ligand does its own in parallel, the last one only picks among the kept poses ----
+  if (kRescore && !degen && valid) {
+    long long acc = lat_rescore_acc(U, A, pk, sw, slut, tid, NTH);
+    // warp sum then one shared 64-bit add per warp (two's complement: exact for signed sums)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if (lane == 0) atomicAdd(&T.chem, (unsigned long long)acc);
+  }
+  __syncthreads();
+  MARK(3, lig * dp.N + r);
+  if (tid == 0) {
+    LatRec rec;
+    rec.chem = (long long)T.chem;
+    rec.geom = T.geom;
+    rec.valid = valid;
+    rec.degen = degen;
+    rec.degen_f = degen ? degen_f : 0;
+    rec.align_score = (int)(key >> 16) - 32768;
+    rec.evals = evals;
+    rec.pairs = pairs;
+    rec.exits = exits;
+    rec.rot = (unsigned)rot;
+    recs[(size_t)lig * dp.N + r] = rec;
+    if (out.rrec) {
+      ds_restart_record rr;
+      rr.align_score = rec.align_score;
+      rr.final_geom = rec.geom;
+      rr.ax = (uint8_t)ix;
+      rr.ay = (uint8_t)iy;
+      rr.valid = (uint8_t)valid;
+      rr.kept = 0;
+      rr.reserved = 0;
+      out.rrec[(size_t)lig * dp.N + r] = rr;
+    }
+    __threadfence();
+    T.is_last = atomicAdd(done + lig, 1) == dp.N - 1;
+  }
+  __syncthreads();
+  if (!T.is_last) return;
+  __threadfence();
+  if (tid == 0) done[lig] = 0;  // every CTA of the ligand has counted in: reset for the next call
+
+  // ---- the ligand's last CTA: select_poses (P12), best rescored kept pose ----
+  // every restart's record into shared memory at once (one L2 round trip, not one per field)
+  {
+    const unsigned *src = reinterpret_cast<const unsigned *>(recs + (size_t)lig * dp.N);
+    unsigned *dst = reinterpret_cast<unsigned *>(T.rec);
+    for (int w = tid; w < dp.N * (int)(sizeof(LatRec) / 4); w += NTH) dst[w] = __ldcg(src + w);
+  }
+  __syncthreads();
+  const LatRec *lr = T.rec;
+  if (tid < dp.N) {
+    T.s_geom[tid] = lr[tid].geom;
+    T.s_valid[tid] = lr[tid].valid;
+    T.dis[tid] = 0u;
+  }
+  if (tid == 0) {
+    // counters in the oracle's sequential order: restarts run in order and a DegenerateAxis stops
+    // the ligand, so only restarts up to the first degenerate one count (P14)
+    unsigned ev = 0, pr = 0, ex = 0, dg = 0, nal = 0;
+    for (int q = 0; q < dp.N && !dg; ++q) {
+      ev += lr[q].evals;
+      pr += lr[q].pairs;
+      ex += lr[q].exits;
+      dg = (unsigned)lr[q].degen;
+      ++nal;
+    }
+    T.s_cnt[0] = ev;
+    T.s_cnt[1] = pr;
+    T.s_cnt[2] = ex;
+    T.s_cnt[3] = dg;
+    T.s_nal = nal;
+    T.s_degf = dg ? lr[nal - 1].degen_f : 0;
+  }
+  __syncthreads();
+  ds_result res;
+  memset(&res, 0, sizeof res);
+  res.poses_scored = T.s_nal * (unsigned)dp.n_rot + T.s_cnt[0];
+  res.bump_checks = T.s_cnt[1];
+  res.bump_early_exits = T.s_cnt[2];
+  if (T.s_cnt[3]) {
+    res.status = DS_STATUS_DEGENERATE_AXIS;
+    if (tid == 0) out.res[lig] = res;
+    // the sequential oracle stops at restart rd, fragment fd: later records stay zero
+    const int rd = (int)T.s_nal - 1, fd = T.s_degf;
+    if (out.rrec)
+      for (int q = rd + tid; q < dp.N; q += NTH) {
+        ds_restart_record z;
+        memset(&z, 0, sizeof z);
+        out.rrec[(size_t)lig * dp.N + q] = z;
+      }
+    for (int q = tid; q < F * dp.N; q += NTH) {
+      const int f = q / dp.N, rr = q - f * dp.N;
+      uint8_t v = __ldcg(out.rtors + (size_t)f0 * dp.N + q);
+      if (rr > rd || (rr == rd && f >= fd)) {
+        v = 0;
+        out.rtors[(size_t)f0 * dp.N + q] = 0;
+      }
+      if (out.rtors_host) out.rtors_host[(size_t)f0 * dp.N + q] = v;
+    }
+    return;
+  }
+  int nvalid = 0;
+  for (int q = 0; q < dp.N; ++q) nvalid += T.s_valid[q];
+  if (nvalid == 0) {
+    res.status = DS_STATUS_NO_VALID_POSE;
+    if (tid == 0) out.res[lig] = res;
+    return;
+  }
+  if (tid < dp.N && T.s_valid[tid]) {
+    int rank = 0;
+    for (int q = 0; q < dp.N; ++q)
+      rank += T.s_valid[q] && (T.s_geom[q] > T.s_geom[tid] || (T.s_geom[q] == T.s_geom[tid] && q < tid));
+    T.ord[rank] = tid;
+  }
+  const float4 *base_scr = out.final_u + (size_t)lig * dp.N * DS_MAX_ATOMS;
+  const int heavy = T.heavy;
+  const int npairs = dp.N * (dp.N - 1) / 2;
+  // RMSD of every valid pair (P12) as the oracle's sequential f64 sum over the heavy atoms in atom
+  // order; hydrogens contribute +0.0 terms (an exact no-op), so terms can be made in parallel.
+  // Staged (the restarts' poses and the terms fit the free grid region): the poses in one parallel
+  // load, the terms by (pair, atom), then one thread per pair adds its terms in order.  Else a warp
+  // per pair: lanes make 32 atoms' terms at once, every lane adds them in order from shuffles.
+  const int nst = dp.N * A;
+  const bool posed = stage != nullptr && (size_t)nst * sizeof(float4) <= (size_t)stage_bytes;
+  bool staged = posed;
+  if (posed && tid == 0) T.nvp = 0;
+  __syncthreads();
+  if (posed) {
+    for (int pidx = tid; pidx < npairs; pidx += NTH) {  // the valid pairs, compacted
+      int p = 0, rem = pidx;
+      while (rem >= dp.N - 1 - p) {
+        rem -= dp.N - 1 - p;
+        ++p;
+      }
+      const int q = p + 1 + rem;
+      if (T.s_valid[p] && T.s_valid[q]) T.vp[atomicAdd(&T.nvp, 1)] = (uint16_t)(p | q << 8);
+    }
+    for (int w = tid; w < nst; w += NTH) {
+      const int q = w / A, i = w - q * A;
+      if (T.s_valid[q]) stage[w] = __ldcg(base_scr + (size_t)q * DS_MAX_ATOMS + i);
+    }
+    __syncthreads();
+    const int nvp = T.nvp;
+    staged = (size_t)nst * sizeof(float4) + (size_t)nvp * A * sizeof(double) <= (size_t)stage_bytes;
+    if (staged) {
+      double *terms = reinterpret_cast<double *>(stage + nst);  // [atom][pair]
+      for (int w = tid; w < nvp * A; w += NTH) {
+        const int i = w / nvp, k = w - i * nvp;
+        const int p = T.vp[k] & 0xFF, q = T.vp[k] >> 8;
+        terms[w] = rmsd_term(stage[p * A + i], stage[q * A + i]);
+      }
+      __syncthreads();
+      for (int k = tid; k < nvp; k += NTH) {
+        double sum = 0.0;
+        for (int i = 0; i < A; ++i) sum = __dadd_rn(sum, terms[i * nvp + k]);
+        const int p = T.vp[k] & 0xFF, q = T.vp[k] >> 8;
+        if (heavy > 0 && sum >= __dmul_rn(dp.thr2, (double)heavy)) {
+          atomicOr(&T.dis[p], 1u << q);
+          atomicOr(&T.dis[q], 1u << p);
+        }
+      }
+    }
+  }
+  const int warp = tid >> 5;
+  for (int pidx = staged ? npairs : warp; pidx < npairs; pidx += NTH / 32) {
+    int p = 0, rem = pidx;
+    while (rem >= dp.N - 1 - p) {
+      rem -= dp.N - 1 - p;
+      ++p;
+    }
+    const int q = p + 1 + rem;
+    if (!T.s_valid[p] || !T.s_valid[q]) continue;
+    const float4 *up = base_scr + (size_t)p * DS_MAX_ATOMS, *uq = base_scr + (size_t)q * DS_MAX_ATOMS;
+    double t[(DS_MAX_ATOMS + 31) / 32];
+#pragma unroll
+    for (int k = 0; k < (DS_MAX_ATOMS + 31) / 32; ++k) {
+      const int i = 32 * k + lane;
+      t[k] = 0.0;
+      if (i < A) t[k] = rmsd_term(__ldcg(up + i), __ldcg(uq + i));
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int k = 0; k < (DS_MAX_ATOMS + 31) / 32; ++k)
+      if (32 * k < A)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum = __dadd_rn(sum, __shfl_sync(kFull, t[k], j));
+    if (lane == 0 && heavy > 0 && sum >= __dmul_rn(dp.thr2, (double)heavy)) {
+      atomicOr(&T.dis[p], 1u << q);
+      atomicOr(&T.dis[q], 1u << p);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int nk = 0;
+    for (int o = 0; o < nvalid && nk < dp.K; ++o) {
+      const int c = T.ord[o];
+      bool ok = true;
+      for (int t = 0; t < nk; ++t) ok = ok && ((T.dis[c] >> T.kept[t]) & 1u);
+      if (ok) T.kept[nk++] = c;
+    }
+    T.nkept = nk;
+  }
+  __syncthreads();
+  const int nk = T.nkept;
+  long long best_chem = 0;
+  int best_r = -1;
+  for (int t = 0; t < nk; ++t) {
+    const int rr = T.kept[t];
+    const long long chem = lr[rr].chem;
+    if (best_r < 0 || chem > best_chem || (chem == best_chem && rr < best_r)) {
+      best_chem = chem;
+      best_r = rr;
+    }
+    if (tid == 0 && out.rrec) out.rrec[(size_t)lig * dp.N + rr].kept = (uint8_t)(t + 1);
+  }
+  const int brot = (int)lr[best_r].rot;
+  res.status = DS_STATUS_OK;
+  res.geom_score = T.s_geom[best_r];
+  res.chem_fx = best_chem;
+  res.best_restart = (uint8_t)best_r;
+  res.best_ax = (uint8_t)(brot / dp.n_a);
+  res.best_ay = (uint8_t)(brot - (brot / dp.n_a) * dp.n_a);
+  res.n_kept = (uint8_t)nk;
+  if (tid == 0) out.res[lig] = res;
+  if (out.best_coords)
+    for (int i = tid; i < A; i += NTH) {
+      const float4 x = posed ? stage[best_r * A + i] : __ldcg(base_scr + (size_t)best_r * DS_MAX_ATOMS + i);
+      float *o = out.best_coords + 3 * (size_t)(a0 + i);
+      o[0] = __fmaf_rn(x.x, pk.spacing, pk.ox);
+      o[1] = __fmaf_rn(x.y, pk.spacing, pk.oy);
+      o[2] = __fmaf_rn(x.z, pk.spacing, pk.oz);
+    }
+  if (out.best_tors)
+    for (int f = tid; f < F; f += NTH)
+      out.best_tors[f0 + f] = __ldcg(out.rtors + (size_t)(f0 + f) * dp.N + best_r);
+  if (out.rtors_host)  // zero-copy outputs: every restart's torsion indices, straight to the host
+    for (int q = tid; q < F * dp.N; q += NTH)
+      out.rtors_host[(size_t)f0 * dp.N + q] = __ldcg(out.rtors + (size_t)f0 * dp.N + q);
+  MARK(4, lig * dp.N + r);
+}
+
 // kNT: the torsion angle count when it is the default 10 (compile-time sweep layout), 0 = runtime
 template <bool kSmemGrid, int kNT>
 __global__ void __launch_bounds__(kLatThreads, 1)
@@ -129,6 +484,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   extern __shared__ __align__(16) unsigned char dsm[];  // [trig 360][fragment records][grid]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lig = blockIdx.x / dp.N, r = blockIdx.x - lig * dp.N;
+  MARK(0, blockIdx.x);
   const int a0 = bt.atom_off[lig], A = bt.atom_off[lig + 1] - a0;
   const int f0 = bt.frag_off[lig], F = bt.frag_off[lig + 1] - f0;
   const GridGeom g = pk.g;
@@ -158,9 +514,10 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     if (kSmemGrid) bulk_g2s(const_cast<uint8_t *>(grid), pk.grid, pk.grid_bytes, &bar[1]);
     S.key = 0u;
     S.pairs = 0u;
-    S.geom = 0;
     S.degen = 0;
-    S.heavy = 0;
+    S.t.geom = 0;
+    S.t.heavy = 0;
+    S.t.chem = 0ull;
   }
   for (int i = lut_bulk + tid; i < lut_n; i += kLatThreads) slut[i] = __ldg(pk.bin_lut + i);  // < 16 B tail
   __syncthreads();
@@ -208,6 +565,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
   const unsigned lt = lanemask_lt();
   const int nslot = (A + 31) >> 5;
   mbar_wait(&bar[1], 0);
+  MARK(1, blockIdx.x);
   for (int f = 0; f < F; ++f) {
     const uint4 fa = sfrag[2 * f];
     const uint4 fb = sfrag[2 * f + 1];
@@ -388,235 +746,444 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     if (best_k < 0) ++all_bumped;
     __syncthreads();
   }
-  // ---- final pose, geometric score, per-restart record ----
   __syncthreads();  // S.degen (a degenerate axis breaks every thread out at the same fragment)
-  const int degen = S.degen;
-  float4 *scr = out.final_u + ((size_t)lig * dp.N + r) * DS_MAX_ATOMS;
-  if (!degen) {
-    int hv = 0;
-    for (int i = tid; i < A; i += kLatThreads) {
-      const float4 p = S.u[i];
-      hv += p.w != 0.f;
-      scr[i] = p;
+  MARK(2, blockIdx.x);
+  lat_tail<kLatThreads, true>(S.t, S.u, S.degen, S.degen_f, total, !(F >= 1 && all_bumped == F), key, ix, iy, rot, evals,
+                        S.pairs, exits, pk, dp, sw, slut, out, recs, done, lig, r, a0, A, f0, F,
+                        kSmemGrid ? reinterpret_cast<float4 *>(const_cast<uint8_t *>(grid)) : nullptr,
+                        kSmemGrid ? pk.grid_bytes : 0);
+}
+
+// ==== cluster-speculative optimisation: one (ligand, restart) over a cluster of n_t CTAs ==========
+// The fragment chain is the latency family's critical path (~2.4 us per fragment of dependent,
+// barrier-separated phases on one SM).  Fragment f + 1 depends on f only through the angle f
+// commits, and there are n_t of those (every angle bumped = no commit = angle 0's positions), so
+// a cluster of n_t CTAs evaluates fragments in pairs: in every CTA, thread group 0 sweeps f on the
+// current pose (the same bits in every CTA), while group 1 of CTA h commits angle h of f on a copy
+// and sweeps f + 1 on it.  As soon as group 0 has a_f, group 1 of CTA a_f (CTA 0 when every angle
+// of f bumped) pushes its pose (f and f + 1 committed) and its outcome for f + 1 into every CTA's
+// shared memory through DSMEM stores; one cluster barrier later every CTA moves on to f + 2 with
+// only local reads: half the chain length, on n_t x N SMs instead of N.  Results are
+// bit-identical to the sequential chain (the pose is CTA a_f's, computed by the same operations).
+constexpr int kSpecH = 10;        // hypotheses per fragment = torsion angles = cluster size
+constexpr int kGrpThreads = 256;  // threads per group (two groups per CTA)
+
+struct LatGrp {                   // one thread group's per-fragment scratch
+  float2 chr[DS_MAX_ATOMS];
+  float2 chm[DS_MAX_ATOMS];
+  uint8_t mlist[DS_MAX_ATOMS];
+  uint8_t clist[DS_MAX_ATOMS];
+  uint8_t cl[DS_MAX_ATOMS][kLatCand];
+  unsigned cn[DS_MAX_ATOMS];
+  int ascore[32];
+  int bcode[32];
+  unsigned abump;
+};
+
+struct SpecRec {                  // one fragment's outcome (the group's thread 0 writes it)
+  int best_k;                     // committed angle, -1: every angle bumped
+  int delta;                      // grid-score change of the committed angle: ascore[k] - ascore[0]
+  unsigned pairs, exits;
+  int degen;
+};
+
+__device__ __forceinline__ void grp_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kGrpThreads) : "memory");
+}
+// named barrier across both groups: the producer arrives (its prior shared-memory writes become
+// visible to the waiters), the consumer waits
+__device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// the torsion axis of a fragment from the positions U (the recipe of the sequential kernel);
+// false when it is degenerate
+__device__ __forceinline__ bool lat_axis(const float4 *U, int ab, int ae, float eps, float3 &a3, float &kx, float &ky,
+                                         float &kz) {
+  const float4 pa = U[ab], pb = U[ae];
+  a3 = make_float3(pa.x, pa.y, pa.z);
+  const float vx = __fsub_rn(pb.x, pa.x), vy = __fsub_rn(pb.y, pa.y), vz = __fsub_rn(pb.z, pa.z);
+  const float len = __fsqrt_rn(__fmaf_rn(vz, vz, __fmaf_rn(vy, vy, __fmul_rn(vx, vx))));
+  if (!(len >= eps)) return false;
+  kx = __fdiv_rn(vx, len);
+  ky = __fdiv_rn(vy, len);
+  kz = __fdiv_rn(vz, len);
+  return true;
+}
+
+__device__ __forceinline__ unsigned frag_word(uint4 fa, uint4 fb, int w) {
+  return w == 0 ? fa.x : w == 1 ? fa.y : w == 2 ? fa.z : w == 3 ? fa.w : fb.x;
+}
+
+// nearest bump candidate of moving atom m at q (lat_min_d2 over a group's scratch)
+__device__ __forceinline__ float grp_min_d2(const float4 *U, const LatGrp &S, int m, int nC, float3 q) {
+  float mind = __int_as_float(0x7f800000);
+  const unsigned cnt = S.cn[m];
+  if (cnt <= (unsigned)kLatCand) {
+    for (unsigned t = 0; t < cnt; ++t) {
+      const float4 y = U[S.cl[m][t]];
+      mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
     }
-    hv = (int)__reduce_add_sync(kFull, (unsigned)hv);
-    if (lane == 0) atomicAdd(&S.heavy, hv);
-    if (tid == 0) S.geom = total;
+  } else {
+    for (int c = 0; c < nC; ++c) {
+      const float4 y = U[S.clist[c]];
+      mind = fminf(mind, dist2(q.x, q.y, q.z, y.x, y.y, y.z));
+    }
   }
-  if (tid == 0) S.chem = 0ull;
-  __syncthreads();
-  const int valid = !(F >= 1 && all_bumped == F);
-  // ---- speculative rescore of this restart's pose (P11, exact fixed point): every CTA of the
-  // ligand does its own in parallel, the last one only picks among the kept poses ----
-  if (!degen && valid) {
-    const int nb1 = pk.nb + 1;
-    long long acc = 0;
-    for (int j = tid; j < pk.n_atoms; j += kLatThreads) {
-      const float4 y = __ldg(pk.patoms + j);
-      const int32_t *wcol = sw + (int)y.w * nb1;
-      int part = 0, cntp = 0;
-      for (int i = 0; i < A; ++i) {
-        const float4 x = S.u[i];
-        const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
-        part += wcol[(int)x.w * DS_N_TYPES * nb1 + lat_bin(pk, slut, d2)];
-        if (++cntp == pk.part_terms) {  // int32 partials sized by the host so they cannot overflow
-          acc += part;
-          part = 0;
-          cntp = 0;
+  return mind;
+}
+
+// one fragment's phases (A) compaction + cylindrical coordinates, (C) bump candidates, (D) the
+// angle sweep, (E) best clean angle, by one group of kGrpThreads threads (gt = thread in group,
+// barrier id bar) on the positions U, which it does not modify.  Returns the committed angle
+// (-1: all bumped, -2: degenerate axis), the same in every thread of the group; the group's
+// thread 0 writes rec.  The axis and the moving count are left for the caller's commit.
+template <bool kSmemGrid>
+__device__ __forceinline__ int lat_frag(const float4 *U, LatGrp &S, uint4 fa, uint4 fb, int A, const GridGeom &g,
+                                        const uint8_t *grid, const float2 *strig, const DockParams &dp, int gt,
+                                        int bar, SpecRec &rec, float3 &a3, float &kx, float &ky, float &kz, int &nMo) {
+  constexpr int kNT = kSpecH;
+  const int lane = gt & 31, warp = gt >> 5;
+  const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
+  if (!lat_axis(U, ab, ae, dp.eps_axis, a3, kx, ky, kz)) {
+    if (gt == 0) rec.degen = 1;
+    return -2;
+  }
+  // ---- (A) ----
+  const unsigned lt = lanemask_lt();
+  const int nslot = (A + 31) >> 5;
+  int nM = 0, nC = 0, mpre = 0, cpre = 0;
+  unsigned my_bm = 0u, my_bc = 0u;
+#pragma unroll
+  for (int w = 0; w < 5; ++w) {
+    if (w < nslot) {
+      const unsigned word = frag_word(fa, fb, w);
+      const int lim = A - 32 * w;
+      const unsigned vmask = lim >= 32 ? kFull : ((1u << lim) - 1u);
+      const unsigned bm = word & vmask;
+      unsigned bc = ~word & vmask;
+      if ((ab >> 5) == w) bc &= ~(1u << (ab & 31));
+      if ((ae >> 5) == w) bc &= ~(1u << (ae & 31));
+      if (w < warp) {
+        mpre += __popc(bm);
+        cpre += __popc(bc);
+      } else if (w == warp) {
+        mpre += __popc(bm & lt);
+        cpre += __popc(bc & lt);
+        my_bm = bm;
+        my_bc = bc;
+      }
+      nM += __popc(bm);
+      nC += __popc(bc);
+    }
+  }
+  if (gt < A) {
+    const float4 p = U[gt];
+    if ((my_bm >> lane) & 1u) {
+      S.mlist[mpre] = (uint8_t)gt;
+      S.chm[mpre] = lat_cyl(p, a3, kx, ky, kz);
+      S.cn[mpre] = 0;
+    } else if ((my_bc >> lane) & 1u) {
+      S.clist[cpre] = (uint8_t)gt;
+      S.chr[cpre] = lat_cyl(p, a3, kx, ky, kz);
+    }
+  }
+  if (gt < 32) {
+    S.ascore[gt] = 0;
+    S.bcode[gt] = 0x7FFFFFFF;
+  }
+  if (gt == 0) S.abump = 0u;
+  grp_sync(bar);
+  // ---- (C) ----
+  if (nC > 0) {
+    const int total = nM * nC;
+    int pm = small_div(gt, nC), pc = gt - pm * nC;
+    const int dm = small_div(kGrpThreads, nC), dc = kGrpThreads - dm * nC;
+    for (int p0 = 0; p0 < total; p0 += kGrpThreads) {
+      if (p0 + gt < total) {
+        const float2 hm = S.chm[pm], hc = S.chr[pc];
+        const float dh = hm.x - hc.x, dr = hm.y - hc.y;
+        if (dh * dh + dr * dr < dp.cull2) {
+          const unsigned k = atomicAdd(&S.cn[pm], 1u);
+          if (k < (unsigned)kLatCand) S.cl[pm][k] = S.clist[pc];
         }
       }
-      acc += part;
+      pm += dm;
+      pc += dc;
+      if (pc >= nC) {
+        pc -= nC;
+        ++pm;
+      }
     }
-    // warp sum then one shared 64-bit add per warp (two's complement: exact for signed sums)
+  }
+  grp_sync(bar);
+  // ---- (D) thread = (angle a, moving-atom group mg), as in k_optimize_latency ----
+  {
+    constexpr int G = kGrpThreads / kNT;
+    const int mg = gt / kNT, a = gt - mg * kNT;
+    if (mg < G) {
+      float R[9];
+      if (a > 0) {
+        const float2 cs = strig[a * dp.step_t];
+        torsion_matrix(kx, ky, kz, cs.x, cs.y, R);
+      }
+      int part = 0;
+      bool hit_any = false;
+      for (int m = mg; m < nM; m += 2 * G) {
+        if (dp.early_exit && a != 0 && (hit_any || m > *(volatile int *)&S.bcode[a])) break;
+        const bool two = m + G < nM;
+        const int m1 = two ? m + G : m;
+        const float4 p0 = U[S.mlist[m]], p1 = U[S.mlist[m1]];
+        const float3 q0 = a == 0 ? make_float3(p0.x, p0.y, p0.z) : torsion_apply(R, a3, p0.x, p0.y, p0.z);
+        const float3 q1 = a == 0 ? make_float3(p1.x, p1.y, p1.z) : torsion_apply(R, a3, p1.x, p1.y, p1.z);
+        const int gv0 = lat_grid_val<kSmemGrid>(grid, node_index(g, q0.x, q0.y, q0.z));
+        const int gv1 = lat_grid_val<kSmemGrid>(grid, node_index(g, q1.x, q1.y, q1.z));
+        const float d0 = grp_min_d2(U, S, m, nC, q0), d1 = grp_min_d2(U, S, m1, nC, q1);
+        const bool hit = d0 < dp.bd2 || d1 < dp.bd2;
+        if (hit) {
+          hit_any = true;
+          atomicOr(&S.abump, 1u << a);
+          if (dp.early_exit) atomicMin(&S.bcode[a], d0 < dp.bd2 ? m : m1);
+        }
+        if (!hit || a == 0) part += two ? gv0 + gv1 : gv0;
+      }
+      if (part) atomicAdd(&S.ascore[a], part);
+    }
+  }
+  grp_sync(bar);
+  // ---- (E) best clean angle by the score change against angle 0 (the non-moving atoms' score is
+  // common to every angle), every warp redundantly; P14 pair rows by warp 0 ----
+  const unsigned abump = S.abump;
+  unsigned kk = 0u;
+  if (lane < kNT && !((abump >> lane) & 1u))
+    kk = ((unsigned)(S.ascore[lane] - S.ascore[0] + 65536) << 8) | (unsigned)(255 - lane);
+  const unsigned best = __reduce_max_sync(kFull, kk);
+  const int best_k = best ? 255 - (int)(best & 0xFFu) : -1;
+  if (warp == 0) {
+    unsigned np = 0;
+    if (lane < kNT) {
+      const int mb = S.bcode[lane];
+      np = (dp.early_exit && mb != 0x7FFFFFFF) ? (unsigned)((mb + 1) * nC) : (unsigned)(nM * nC);
+    }
+    np = __reduce_add_sync(kFull, np);
+    if (lane == 0) {
+      rec.best_k = best_k;
+      rec.delta = best ? (int)(best >> 8) - 65536 : 0;
+      rec.pairs = np;
+      rec.exits = dp.early_exit ? (unsigned)__popc(abump) : 0u;
+      rec.degen = 0;
+    }
+  }
+  nMo = nM;
+  return best_k;
+}
+
+// commit angle k (> 0) of the fragment whose moving atoms are S.mlist[0 .. nM) into U
+__device__ __forceinline__ void lat_commit(float4 *U, const LatGrp &S, int nM, const float2 *strig, int step_t, int k,
+                                           float3 a3, float kx, float ky, float kz, int t0, int nth) {
+  for (int m = t0; m < nM; m += nth) {
+    const int i = S.mlist[m];
+    const float4 p = U[i];
+    const float3 q = lat_torsion_pos(strig, step_t, k, kx, ky, kz, a3, p);
+    U[i] = make_float4(q.x, q.y, q.z, p.w);
+  }
+}
+
+template <bool kSmemGrid>
+__global__ void __launch_bounds__(2 * kGrpThreads, 1)
+    k_optimize_latency_spec(PocketView pk, BatchView bt, DockParams dp, const unsigned *keys, OptOut out,
+                            LatRec *recs, int *done) {
+  constexpr int NTH = 2 * kGrpThreads;
+  // P[cur]: the committed pose; P[cur ^ 1]: the next one, written by the winning CTA of the step
+  __shared__ __align__(16) float4 P[2][DS_MAX_ATOMS];
+  __shared__ __align__(16) float4 Q[DS_MAX_ATOMS];      // group 1's hypothesis pose
+  __shared__ LatGrp GS[2];
+  __shared__ SpecRec R0[2];                             // group 0's outcome for f (by step parity)
+  __shared__ SpecRec R1loc;                             // group 1's outcome for f + 1
+  __shared__ SpecRec R1in[2];                           // the winner's outcome for f + 1 (pushed)
+  __shared__ LatTail T;
+  __shared__ unsigned s_key;
+  __shared__ __align__(8) unsigned long long bar[2];
+  extern __shared__ __align__(16) unsigned char dsm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int h = (int)cl.block_rank();
+  const int tid = threadIdx.x, grp = tid / kGrpThreads, gt = tid - grp * kGrpThreads;
+  const int lr = blockIdx.x / kSpecH;
+  const int lig = lr / dp.N, r = lr - lig * dp.N;
+  if (h == 0) MARK(0, lr);
+  const int a0 = bt.atom_off[lig], A = bt.atom_off[lig + 1] - a0;
+  const int f0 = bt.frag_off[lig], F = bt.frag_off[lig + 1] - f0;
+  const GridGeom g = pk.g;
+  float2 *strig = reinterpret_cast<float2 *>(dsm);
+  uint4 *sfrag = reinterpret_cast<uint4 *>(dsm + 360 * sizeof(float2));
+  int32_t *sw = reinterpret_cast<int32_t *>(dsm + 360 * sizeof(float2) + 2 * (DS_MAX_ATOMS - 2) * sizeof(uint4));
+  uint8_t *slut = reinterpret_cast<uint8_t *>(sw) + lat_w_bytes(pk.nb);
+  const uint8_t *grid = kSmemGrid ? dsm + lat_base_bytes(pk.nb, pk.lut_cap) : pk.grid;
+  const unsigned wbytes = (unsigned)(DS_N_TYPES * DS_N_TYPES * (pk.nb + 1) * 4);
+  const int lut_n = pk.lut_cap + 1, lut_bulk = lut_n & ~15;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar[0], 360 * sizeof(float2));
+    bulk_g2s(strig, pk.trig, 360 * sizeof(float2), &bar[0]);
+    mbar_expect_tx(&bar[1], 32u * F + wbytes + lut_bulk + (kSmemGrid ? pk.grid_bytes : 0));
+    if (F) bulk_g2s(sfrag, bt.frags + 2 * (size_t)f0, 32u * F, &bar[1]);
+    bulk_g2s(sw, pk.wfx, wbytes, &bar[1]);
+    if (lut_bulk) bulk_g2s(slut, pk.bin_lut, lut_bulk, &bar[1]);
+    if (kSmemGrid) bulk_g2s(const_cast<uint8_t *>(grid), pk.grid, pk.grid_bytes, &bar[1]);
+    T.geom = 0;
+    T.heavy = 0;
+    T.chem = 0ull;
+  }
+  for (int i = lut_bulk + tid; i < lut_n; i += NTH) slut[i] = __ldg(pk.bin_lut + i);
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tid == 0) s_key = __ldcg(keys + (size_t)lig * dp.N + r);
+  __syncthreads();
+  mbar_wait(&bar[0], 0);
+  const unsigned key = s_key;
+  int total = (int)(key >> 16) - 32768;
+  const int rot = 65535 - (int)(key & 0xFFFFu);
+  const int ix = rot / dp.n_a, iy = rot - ix * dp.n_a;
+  if (tid < A) {
+    float R0s[9], Tt[3], Rp[9];
+    start_params(bt.idh[lig], dp.seed, r, strig, pk.inv_s, g.nx, g.ny, g.nz, R0s, Tt);
+    align_rx(strig[ix * dp.step_a], R0s, Rp);
+    const float2 cy = strig[iy * dp.step_a];
+    const float4 d = __ldg(bt.atoms + a0 + tid);
+    const float3 u = align_u(align_v(Rp, d.x, d.y, d.z), cy.x, cy.y, Tt);
+    P[0][tid] = make_float4(u.x, u.y, u.z, d.w);
+  }
+  __syncthreads();
+  mbar_wait(&bar[1], 0);
+  if (h == 0) MARK(1, lr);
+  unsigned evals = 0, exits = 0, pairs = 0;
+  int all_bumped = 0, degen = 0, degen_f = 0, cur = 0;
+#ifdef DS_SPEC_PROBE
+  long long t_step = clock64();
+#endif
+  for (int f = 0; f < F; f += 2) {
+    const int par = (f >> 1) & 1;
+    const bool two = f + 1 < F;  // uniform over the cluster
+    const uint4 fa = sfrag[2 * f], fb = sfrag[2 * f + 1];
+    float4 *Pc = P[cur];
+    if (grp == 0) {
+      float3 a3;
+      float kx = 0.f, ky = 0.f, kz = 0.f;
+      int nM = 0;
+      const int k = lat_frag<kSmemGrid>(Pc, GS[0], fa, fb, A, g, grid, strig, dp, gt, 1, R0[par], a3, kx, ky, kz, nM);
+      if (gt == 0) SPROBE(0);
+      if (two)
+        nb_arrive(3, NTH);  // a_f is known: group 1 may decide whether it won
+      else if (k > 0)       // the chain's last, unpaired fragment: commit here (group 1 is idle)
+        lat_commit(Pc, GS[0], nM, strig, dp.step_t, k, a3, kx, ky, kz, gt, kGrpThreads);
+    } else if (two) {
+      // commit hypothesis h of fragment f on a copy of the pose, then sweep f + 1 on it
+      float3 a3;
+      float kx, ky, kz;
+      const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
+      const bool ok = lat_axis(Pc, ab, ae, dp.eps_axis, a3, kx, ky, kz);  // else group 0 reports the break
+      if (ok) {
+        if (gt < A) {
+          const float4 p = Pc[gt];
+          const bool mv = (frag_word(fa, fb, gt >> 5) >> (gt & 31)) & 1u;
+          if (mv && h > 0) {
+            const float3 q = lat_torsion_pos(strig, dp.step_t, h, kx, ky, kz, a3, p);
+            Q[gt] = make_float4(q.x, q.y, q.z, p.w);
+          } else {
+            Q[gt] = p;
+          }
+        }
+        grp_sync(2);
+        if (gt == 0) SPROBE(1);
+        int nM = 0;
+        const int k = lat_frag<kSmemGrid>(Q, GS[1], sfrag[2 * f + 2], sfrag[2 * f + 3], A, g, grid, strig, dp, gt, 2,
+                                          R1loc, a3, kx, ky, kz, nM);
+        if (k > 0) lat_commit(Q, GS[1], nM, strig, dp.step_t, k, a3, kx, ky, kz, gt, kGrpThreads);
+        if (gt == 0) SPROBE(2);
+      }
+      nb_sync(3, NTH);  // also orders every group-1 thread's commit before the push reads Q
+      if (gt == 0) SPROBE(3);
+      const SpecRec r0 = R0[par];
+      // the winning hypothesis (CTA 0's when every angle of f bumped) pushes its pose after f and
+      // f + 1 and its outcome for f + 1 into every CTA's shared memory, before the cluster barrier
+      if (ok && !r0.degen && h == (r0.best_k < 0 ? 0 : r0.best_k)) {
+        for (int u = gt; u < kSpecH * A; u += kGrpThreads) {
+          const int c = u / A, i = u - c * A;
+          cl.map_shared_rank(&P[cur ^ 1][0], c)[i] = Q[i];
+        }
+        if (gt < kSpecH) *cl.map_shared_rank(&R1in[par], gt) = R1loc;
+      }
+      if (gt == 0) SPROBE(4);
+    }
+    if (two)
+      cl.sync();
+    else
+      __syncthreads();
+    if (tid == 0) SPROBE(5);
+#ifdef DS_SPEC_PROBE
+    t_step = clock64();
+#endif
+    const SpecRec r0 = R0[par];
+    if (r0.degen) {
+      degen = 1;
+      degen_f = f;
+      break;
+    }
+    evals += kSpecH;
+    pairs += r0.pairs;
+    exits += r0.exits;
+    all_bumped += r0.best_k < 0;
+    if (r0.best_k >= 0) total += r0.delta;
+    if (h == 0 && tid == 0)
+      out.rtors[(size_t)(f0 + f) * dp.N + r] = r0.best_k < 0 ? (uint8_t)DS_TORSION_NONE : (uint8_t)r0.best_k;
+    if (two) {
+      const SpecRec r1 = R1in[par];
+      if (r1.degen) {
+        degen = 1;
+        degen_f = f + 1;
+        break;
+      }
+      evals += kSpecH;
+      pairs += r1.pairs;
+      exits += r1.exits;
+      all_bumped += r1.best_k < 0;
+      if (r1.best_k >= 0) total += r1.delta;
+      if (h == 0 && tid == 0)
+        out.rtors[(size_t)(f0 + f + 1) * dp.N + r] = r1.best_k < 0 ? (uint8_t)DS_TORSION_NONE : (uint8_t)r1.best_k;
+      cur ^= 1;
+    }
+  }
+  const float4 *Pf = P[cur];
+  // every CTA holds the final pose: the rescore (P11) is split over the cluster and summed into
+  // CTA 0 (exact 64-bit integer sum, so the split does not change it)
+  const int valid = !(F >= 1 && all_bumped == F);
+  if (!degen && valid) {
+    long long acc = lat_rescore_acc(Pf, A, pk, sw, slut, h * NTH + tid, kSpecH * NTH);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-    if (lane == 0) atomicAdd(&S.chem, (unsigned long long)acc);
+    if ((tid & 31) == 0 && acc) atomicAdd(cl.map_shared_rank(&T.chem, 0), (unsigned long long)acc);
   }
-  __syncthreads();
-  if (tid == 0) {
-    LatRec rec;
-    rec.chem = (long long)S.chem;
-    rec.geom = S.geom;
-    rec.valid = valid;
-    rec.degen = degen;
-    rec.degen_f = degen ? S.degen_f : 0;
-    rec.align_score = (int)(key >> 16) - 32768;
-    rec.evals = evals;
-    rec.pairs = S.pairs;
-    rec.exits = exits;
-    rec.rot = (unsigned)rot;
-    recs[(size_t)lig * dp.N + r] = rec;
-    if (out.rrec) {
-      ds_restart_record rr;
-      rr.align_score = rec.align_score;
-      rr.final_geom = rec.geom;
-      rr.ax = (uint8_t)ix;
-      rr.ay = (uint8_t)iy;
-      rr.valid = (uint8_t)valid;
-      rr.kept = 0;
-      rr.reserved = 0;
-      out.rrec[(size_t)lig * dp.N + r] = rr;
-    }
-    __threadfence();
-    S.is_last = atomicAdd(done + lig, 1) == dp.N - 1;
-  }
-  __syncthreads();
-  if (!S.is_last) return;
-  __threadfence();
-  if (tid == 0) done[lig] = 0;  // every CTA of the ligand has counted in: reset for the next call
-
-  // ---- the ligand's last CTA: select_poses (P12), best rescored kept pose ----
-  const LatRec *lr = recs + (size_t)lig * dp.N;
-  __shared__ int s_geom[DS_MAX_RESTARTS], s_valid[DS_MAX_RESTARTS];
-  __shared__ unsigned s_cnt[4], s_nal;
-  __shared__ int s_degf;
-  if (tid < dp.N) {
-    s_geom[tid] = __ldcg(&lr[tid].geom);
-    s_valid[tid] = __ldcg(&lr[tid].valid);
-    S.dis[tid] = 0u;
-  }
-  if (tid == 0) {
-    // counters in the oracle's sequential order: restarts run in order and a DegenerateAxis stops
-    // the ligand, so only restarts up to the first degenerate one count (P14)
-    unsigned ev = 0, pr = 0, ex = 0, dg = 0, nal = 0;
-    for (int q = 0; q < dp.N && !dg; ++q) {
-      ev += __ldcg(&lr[q].evals);
-      pr += __ldcg(&lr[q].pairs);
-      ex += __ldcg(&lr[q].exits);
-      dg = (unsigned)__ldcg(&lr[q].degen);
-      ++nal;
-    }
-    s_cnt[0] = ev;
-    s_cnt[1] = pr;
-    s_cnt[2] = ex;
-    s_cnt[3] = dg;
-    s_nal = nal;
-    s_degf = dg ? __ldcg(&lr[nal - 1].degen_f) : 0;
-    S.chem = 0ull;
-  }
-  __syncthreads();
-  ds_result res;
-  memset(&res, 0, sizeof res);
-  res.poses_scored = s_nal * (unsigned)dp.n_rot + s_cnt[0];
-  res.bump_checks = s_cnt[1];
-  res.bump_early_exits = s_cnt[2];
-  if (s_cnt[3]) {
-    res.status = DS_STATUS_DEGENERATE_AXIS;
-    if (tid == 0) out.res[lig] = res;
-    // the sequential oracle stops at restart rd, fragment fd: later records stay zero
-    const int rd = (int)s_nal - 1, fd = s_degf;
-    if (out.rrec)
-      for (int q = rd + tid; q < dp.N; q += kLatThreads) {
-        ds_restart_record z;
-        memset(&z, 0, sizeof z);
-        out.rrec[(size_t)lig * dp.N + q] = z;
-      }
-    for (int q = tid; q < F * dp.N; q += kLatThreads) {
-      const int f = q / dp.N, rr = q - f * dp.N;
-      uint8_t v = __ldcg(out.rtors + (size_t)f0 * dp.N + q);
-      if (rr > rd || (rr == rd && f >= fd)) {
-        v = 0;
-        out.rtors[(size_t)f0 * dp.N + q] = 0;
-      }
-      if (out.rtors_host) out.rtors_host[(size_t)f0 * dp.N + q] = v;
-    }
-    return;
-  }
-  int nvalid = 0;
-  for (int q = 0; q < dp.N; ++q) nvalid += s_valid[q];
-  if (nvalid == 0) {
-    res.status = DS_STATUS_NO_VALID_POSE;
-    if (tid == 0) out.res[lig] = res;
-    return;
-  }
-  if (tid < dp.N && s_valid[tid]) {
-    int rank = 0;
-    for (int q = 0; q < dp.N; ++q)
-      rank += s_valid[q] && (s_geom[q] > s_geom[tid] || (s_geom[q] == s_geom[tid] && q < tid));
-    S.ord[rank] = tid;
-  }
-  const float4 *base_scr = out.final_u + (size_t)lig * dp.N * DS_MAX_ATOMS;
-  const int heavy = S.heavy;
-  const int npairs = dp.N * (dp.N - 1) / 2;
-  for (int pidx = tid; pidx < npairs; pidx += kLatThreads) {
-    int p = 0, rem = pidx;
-    while (rem >= dp.N - 1 - p) {
-      rem -= dp.N - 1 - p;
-      ++p;
-    }
-    const int q = p + 1 + rem;
-    if (!s_valid[p] || !s_valid[q]) continue;
-    double sum = 0.0;
-    const float4 *up = base_scr + (size_t)p * DS_MAX_ATOMS, *uq = base_scr + (size_t)q * DS_MAX_ATOMS;
-    for (int i = 0; i < A; ++i) {
-      const float4 x = __ldcg(up + i), y = __ldcg(uq + i);
-      if (x.w == 0.f) continue;
-      const double dx = __dsub_rn((double)x.x, (double)y.x);
-      const double dy = __dsub_rn((double)x.y, (double)y.y);
-      const double dz = __dsub_rn((double)x.z, (double)y.z);
-      double t = __dmul_rn(dx, dx);
-      t = __dadd_rn(t, __dmul_rn(dy, dy));
-      t = __dadd_rn(t, __dmul_rn(dz, dz));
-      sum = __dadd_rn(sum, t);
-    }
-    if (heavy > 0 && sum >= __dmul_rn(dp.thr2, (double)heavy)) {
-      atomicOr(&S.dis[p], 1u << q);
-      atomicOr(&S.dis[q], 1u << p);
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int nk = 0;
-    for (int o = 0; o < nvalid && nk < dp.K; ++o) {
-      const int c = S.ord[o];
-      bool ok = true;
-      for (int t = 0; t < nk; ++t) ok = ok && ((S.dis[c] >> S.kept[t]) & 1u);
-      if (ok) S.kept[nk++] = c;
-    }
-    S.nkept = nk;
-  }
-  __syncthreads();
-  const int nk = S.nkept;
-  long long best_chem = 0;
-  int best_r = -1;
-  for (int t = 0; t < nk; ++t) {
-    const int rr = S.kept[t];
-    const long long chem = __ldcg(&lr[rr].chem);
-    if (best_r < 0 || chem > best_chem || (chem == best_chem && rr < best_r)) {
-      best_chem = chem;
-      best_r = rr;
-    }
-    if (tid == 0 && out.rrec) out.rrec[(size_t)lig * dp.N + rr].kept = (uint8_t)(t + 1);
-  }
-  const int brot = (int)__ldcg(&lr[best_r].rot);
-  res.status = DS_STATUS_OK;
-  res.geom_score = s_geom[best_r];
-  res.chem_fx = best_chem;
-  res.best_restart = (uint8_t)best_r;
-  res.best_ax = (uint8_t)(brot / dp.n_a);
-  res.best_ay = (uint8_t)(brot - (brot / dp.n_a) * dp.n_a);
-  res.n_kept = (uint8_t)nk;
-  if (tid == 0) out.res[lig] = res;
-  if (out.best_coords)
-    for (int i = tid; i < A; i += kLatThreads) {
-      const float4 x = __ldcg(base_scr + (size_t)best_r * DS_MAX_ATOMS + i);
-      float *o = out.best_coords + 3 * (size_t)(a0 + i);
-      o[0] = __fmaf_rn(x.x, pk.spacing, pk.ox);
-      o[1] = __fmaf_rn(x.y, pk.spacing, pk.oy);
-      o[2] = __fmaf_rn(x.z, pk.spacing, pk.oz);
-    }
-  if (out.best_tors)
-    for (int f = tid; f < F; f += kLatThreads)
-      out.best_tors[f0 + f] = __ldcg(out.rtors + (size_t)(f0 + f) * dp.N + best_r);
-  if (out.rtors_host)  // zero-copy outputs: every restart's torsion indices, straight to the host
-    for (int q = tid; q < F * dp.N; q += kLatThreads)
-      out.rtors_host[(size_t)f0 * dp.N + q] = __ldcg(out.rtors + (size_t)f0 * dp.N + q);
+  cl.sync();  // no CTA leaves while another may still access its shared memory
+  if (h != 0) return;
+  MARK(2, lr);
+  lat_tail<NTH, false>(T, Pf, degen, degen_f, total, valid, key, ix, iy, rot, evals, pairs, exits, pk, dp, sw, slut,
+                       out, recs, done, lig, r, a0, A, f0, F,
+                       reinterpret_cast<float4 *>(const_cast<uint8_t *>(grid)), pk.grid_bytes);
 }
 
 size_t latency_rec_bytes() { return sizeof(LatRec); }
 
-void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
-                             const unsigned *keys, OptOut out, void *recs, int *done, bool pdl, cudaStream_t st) {
+// DS_LATENCY_SPEC: 0 = never the cluster-speculative kernel, 1 = whenever it applies, unset = when
+// every (ligand, restart) cluster is resident at once (one ligand spread over the GPU)
+static int spec_mode() {
+  const char *e = getenv("DS_LATENCY_SPEC");
+  return e ? atoi(e) : -1;
+}
+
+// returns the CTAs per (ligand, restart): kSpecH for the cluster-speculative kernel, else 1
+int launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
+                            const unsigned *keys, OptOut out, void *recs, int *done, bool pdl, cudaStream_t st) {
   const size_t base = lat_base_bytes(pk.nb, pk.lut_cap);
   static const int optin = [] {
     int dev = 0, v = 0;
@@ -625,6 +1192,53 @@ void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const Do
     return v;
   }();
   const size_t with_grid = base + (size_t)pk.grid_bytes;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  const int mode = spec_mode();
+  if (keys && dp.n_t == kSpecH && mode != 0) {
+    auto kern = k_optimize_latency_spec<true>;
+    static const size_t spec_static = [] {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, (const void *)k_optimize_latency_spec<true>);
+      cudaFuncSetAttribute((const void *)k_optimize_latency_spec<true>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      return (size_t)fa.sharedSizeBytes;
+    }();
+    if (with_grid + spec_static + 1024 <= (size_t)optin) {
+      allow_max_smem((const void *)kern);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(bt.L * dp.N * kSpecH);
+      cfg.blockDim = dim3(2 * kGrpThreads);
+      cfg.dynamicSmemBytes = with_grid;
+      cfg.stream = st;
+      attr[1].id = cudaLaunchAttributeClusterDimension;
+      attr[1].val.clusterDim.x = kSpecH;
+      attr[1].val.clusterDim.y = 1;
+      attr[1].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 2;
+      bool use = mode == 1;
+      if (!use) {  // resident clusters at this shared-memory size (cached per size)
+        static std::mutex mu;
+        static std::map<size_t, int> resident;
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = resident.find(with_grid);
+        if (it == resident.end()) {
+          int n = 0;
+          cudaLaunchConfig_t q = cfg;
+          q.numAttrs = 2;
+          if (cudaOccupancyMaxActiveClusters(&n, (const void *)kern, &q) != cudaSuccess) n = 0;
+          it = resident.emplace(with_grid, n).first;
+        }
+        use = bt.L * dp.N <= it->second;
+      }
+      if (use) {
+        cudaLaunchKernelEx(&cfg, kern, pk, bt, dp, keys, out, (LatRec *)recs, done);
+        return kSpecH;
+      }
+    }
+  }
   const bool fits = with_grid + sizeof(LatSmem) + 1024 <= (size_t)optin;
   const bool nt10 = dp.n_t == 10;
   auto kern = fits ? (nt10 ? k_optimize_latency<true, 10> : k_optimize_latency<true, 0>)
@@ -636,12 +1250,19 @@ void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const Do
   cfg.blockDim = dim3(kLatThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kern, pk, bt, dp, scores, keys, out, (LatRec *)recs, done);
+  return 1;
 }
 
 }  // namespace ds
+
+#ifdef DS_SPEC_PROBE
+extern "C" int ds_probe_marks(unsigned long long *out) {
+  return (int)cudaMemcpyFromSymbol(out, ds::g_marks, sizeof(ds::g_marks));
+}
+extern "C" int ds_probe_steps(long long *out) {
+  return (int)cudaMemcpyFromSymbol(out, ds::g_steps, sizeof(ds::g_steps));
+}
+#endif

@@ -73,7 +73,7 @@ class Outputs(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("total_ms", C.c_float), ("align_ms", C.c_float), ("optimize_ms", C.c_float),
                 ("launches", C.c_int32), ("select_ms", C.c_float), ("h2d_bytes", C.c_int64),
-                ("d2h_bytes", C.c_int64)]
+                ("d2h_bytes", C.c_int64), ("lat_spread", C.c_int32)]
 
 
 RESULT_DTYPE = np.dtype([("status", "<i4"), ("geom_score", "<i4"), ("chem_fx", "<i8"), ("best_restart", "u1"),

@@ -40,8 +40,8 @@ def test_struct_layouts_match_header():
 int main(void){
  printf("%zu %zu %zu %zu %zu %zu %zu\n", sizeof(ds_pocket_desc), sizeof(ds_dock_config), sizeof(ds_batch_desc),
         sizeof(ds_result), sizeof(ds_restart_record), sizeof(ds_outputs), sizeof(ds_stats));
- printf("%zu %zu %zu %zu\n", offsetof(ds_pocket_desc, n_bins), offsetof(ds_dock_config, seed),
-        offsetof(ds_result, poses_scored), offsetof(ds_stats, h2d_bytes));
+ printf("%zu %zu %zu %zu %zu\n", offsetof(ds_pocket_desc, n_bins), offsetof(ds_dock_config, seed),
+        offsetof(ds_result, poses_scored), offsetof(ds_stats, h2d_bytes), offsetof(ds_stats, lat_spread));
  return 0;}
 '''
     tmp = os.path.join(ROOT, "build")
@@ -56,7 +56,8 @@ int main(void){
                      C.sizeof(native.Stats)]
     offs = [int(x) for x in l2.split()]
     assert offs == [native.PocketDesc.n_bins.offset, native.DockConfigC.seed.offset,
-                    native.RESULT_DTYPE.fields["poses_scored"][1], native.Stats.h2d_bytes.offset]
+                    native.RESULT_DTYPE.fields["poses_scored"][1], native.Stats.h2d_bytes.offset,
+                    native.Stats.lat_spread.offset]
 
 
 def test_kernels_are_sm100a():
