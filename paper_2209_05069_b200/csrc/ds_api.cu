@@ -35,8 +35,10 @@ void launch_generate_ligands(long long seed, long long first_index, int count, c
                              cudaStream_t st);
 void launch_build_pocket(const float *atom_xyz, int P, const double *origin, double s, const int *dims,
                          int32_t *values, int sm_count, cudaStream_t st);
-int launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
-                            const unsigned *keys, OptOut out, void *recs, int *done, bool pdl, cudaStream_t st);
+void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
+                             const unsigned *keys, OptOut out, void *recs, int *done, bool pdl, cudaStream_t st);
+bool launch_spread_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, OptOut out, void *recs,
+                           int *done, cudaStream_t st);
 void launch_grid_score(const PocketView &pk, const float *coords, int n_atoms, int n_poses, int32_t *out,
                        cudaStream_t st);
 void launch_rescore(const PocketView &pk, const float *coords, const uint8_t *types, int n_atoms, int n_poses,
@@ -862,9 +864,6 @@ int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const Dock
   }();
   c->lat_pdl = pdl;
   cudaEventRecord(c->ev[1], c->stream);
-  const bool keyed =
-      launch_align_latency(pk->view, bt, dp, max_atoms, (int *)c->b_lat_scores.p, (unsigned *)c->b_keys.p, c->stream);
-  if (!pdl) cudaEventRecord(c->ev[2], c->stream);
   OptOut oo = {};
   oo.res = c->io.res;
   oo.rrec = want_rrec ? c->io.rrec : nullptr;
@@ -874,12 +873,26 @@ int run_latency(ds_ctx *c, const ds_pocket *pk, int L, int max_atoms, const Dock
   oo.best_tors = want_btors ? c->io.btors : nullptr;
   oo.rtors_host = c->x_zero_copy ? c->x_rtors_host : nullptr;
   c->lat_dirty = true;  // until the call has completed (set clean again below / by ds_dock)
-  const int spread =
-      launch_optimize_latency(pk->view, bt, dp, (int *)c->b_lat_scores.p, keyed ? (const unsigned *)c->b_keys.p : nullptr,
-                              oo, c->b_lat_recs.p, (int *)c->b_lat_done.p, pdl, c->stream);
-  if (st) st->lat_spread = spread;
+  // one ligand over the GPU: the cluster-speculative kernel aligns and optimises in one launch;
+  // else the alignment kernel, then the one-CTA-per-restart chain
+  if (launch_spread_latency(pk->view, bt, dp, oo, c->b_lat_recs.p, (int *)c->b_lat_done.p, c->stream)) {
+    c->lat_pdl = true;  // one kernel: align_ms is not split out
+    if (st) {
+      st->lat_spread = 10;
+      st->launches += 1;
+    }
+  } else {
+    const bool keyed =
+        launch_align_latency(pk->view, bt, dp, max_atoms, (int *)c->b_lat_scores.p, (unsigned *)c->b_keys.p, c->stream);
+    if (!pdl) cudaEventRecord(c->ev[2], c->stream);
+    launch_optimize_latency(pk->view, bt, dp, (int *)c->b_lat_scores.p, keyed ? (const unsigned *)c->b_keys.p : nullptr,
+                            oo, c->b_lat_recs.p, (int *)c->b_lat_done.p, pdl, c->stream);
+    if (st) {
+      st->lat_spread = 1;
+      st->launches += 2;
+    }
+  }
   cudaEventRecord(c->ev[3], c->stream);
-  if (st) st->launches += 2;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(DS_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return DS_OK;

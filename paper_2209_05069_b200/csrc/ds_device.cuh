@@ -225,6 +225,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_addr(bar))
                : "memory");
 }
+// the same copy into the same shared-memory offset of every CTA in mask (thread-block cluster);
+// each destination's mbarrier at bar's offset receives the complete_tx
+__device__ __forceinline__ void bulk_g2s_multicast(void *dst, const void *src, unsigned bytes, unsigned long long *bar,
+                                                   unsigned mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "h"((unsigned short)mask)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"

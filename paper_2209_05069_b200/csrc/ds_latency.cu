@@ -16,6 +16,7 @@
 //                                    (PAPER.md:344-348).
 // Numeric recipe identical to the batched family: results are bit-identical.
 #include <cooperative_groups.h>
+#include <limits.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -53,12 +54,11 @@ struct LatTail {
   unsigned dis[DS_MAX_RESTARTS];
   unsigned long long chem;
   int heavy;
-  int s_geom[DS_MAX_RESTARTS], s_valid[DS_MAX_RESTARTS];
   unsigned s_cnt[4], s_nal;
   int s_degf;
   LatRec rec[DS_MAX_RESTARTS];  // the ligand's per-restart records, staged by the last CTA
-  int nvp;                      // valid restart pairs
-  uint16_t vp[DS_MAX_RESTARTS * (DS_MAX_RESTARTS - 1) / 2];  // ... as p | q << 8
+  int nvp;                      // valid restarts
+  uint16_t vp[DS_MAX_RESTARTS * (DS_MAX_RESTARTS - 1) / 2];  // restart pairs as p | q << 8
 };
 
 struct LatSmem {
@@ -148,13 +148,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 __device__ unsigned long long g_marks[64][8];
+__device__ unsigned long long g_marks2[64][8];
+#define MARK2(tag, id) \
+  if (threadIdx.x == 0) g_marks2[(id) & 63][tag] = gtimer()
 __device__ long long g_steps[16][16][8];  // spread kernel, cluster 0: [CTA][step][point] clock64 deltas
 #define SPROBE(k) \
-  if (blockIdx.x < kSpecH && (f >> 1) < 16) g_steps[blockIdx.x][f >> 1][k] = clock64() - t_step
+  if (blockIdx.x < kSpecH && (f >> 1) < 16) g_steps[lead ? kSpecH : blockIdx.x][f >> 1][k] = clock64() - t_step
 #define MARK(tag, id) \
   if (threadIdx.x == 0) g_marks[(id) & 63][tag] = gtimer()
 #else
 #define MARK(tag, id)
+#define MARK2(tag, id)
 #define SPROBE(k)
 #endif
 
@@ -267,45 +271,80 @@ __device__ __forceinline__ void lat_tail(LatTail &T, const float4 *U, int degen,
       rr.reserved = 0;
       out.rrec[(size_t)lig * dp.N + r] = rr;
     }
-    __threadfence();
-    T.is_last = atomicAdd(done + lig, 1) == dp.N - 1;
+    __threadfence();  // release: this CTA's records and final pose before its count
+    const bool last = atomicAdd(done + lig, 1) == dp.N - 1;
+    if (last) {
+      __threadfence();  // acquire: every other CTA's records and poses
+      done[lig] = 0;    // every CTA of the ligand has counted in: reset for the next call
+    }
+    T.is_last = last;
   }
   __syncthreads();
+  MARK2(0, lig * dp.N + r);
   if (!T.is_last) return;
-  __threadfence();
-  if (tid == 0) done[lig] = 0;  // every CTA of the ligand has counted in: reset for the next call
 
   // ---- the ligand's last CTA: select_poses (P12), best rescored kept pose ----
-  // every restart's record into shared memory at once (one L2 round trip, not one per field)
+  // one L2 round trip: every restart's record, and (when they fit the free grid region) every
+  // restart's final pose and torsion indices
+  const float4 *base_scr = out.final_u + (size_t)lig * dp.N * DS_MAX_ATOMS;
+  const int N = dp.N, nst = N * A, nrt = F * N;
+  const int npairs = N * (N - 1) / 2;
+  const size_t pose_bytes = (size_t)nst * sizeof(float4), rt_bytes = ((size_t)nrt + 15) & ~(size_t)15;
+  const bool posed = stage != nullptr && pose_bytes + rt_bytes <= (size_t)stage_bytes;
+  uint8_t *srt = posed ? reinterpret_cast<uint8_t *>(stage + nst) : nullptr;
   {
-    const unsigned *src = reinterpret_cast<const unsigned *>(recs + (size_t)lig * dp.N);
+    const unsigned *src = reinterpret_cast<const unsigned *>(recs + (size_t)lig * N);
     unsigned *dst = reinterpret_cast<unsigned *>(T.rec);
-    for (int w = tid; w < dp.N * (int)(sizeof(LatRec) / 4); w += NTH) dst[w] = __ldcg(src + w);
+    for (int w = tid; w < N * (int)(sizeof(LatRec) / 4); w += NTH) dst[w] = __ldcg(src + w);
+    if (posed) {
+      for (int w = tid; w < nst; w += NTH) {
+        const int q = w / A, i = w - q * A;
+        stage[w] = __ldcg(base_scr + (size_t)q * DS_MAX_ATOMS + i);
+      }
+      for (int w = tid; w < nrt; w += NTH) srt[w] = __ldcg(out.rtors + (size_t)f0 * N + w);
+    }
   }
   __syncthreads();
+  MARK2(1, lig * dp.N + r);
   const LatRec *lr = T.rec;
-  if (tid < dp.N) {
-    T.s_geom[tid] = lr[tid].geom;
-    T.s_valid[tid] = lr[tid].valid;
-    T.dis[tid] = 0u;
-  }
-  if (tid == 0) {
-    // counters in the oracle's sequential order: restarts run in order and a DegenerateAxis stops
-    // the ligand, so only restarts up to the first degenerate one count (P14)
-    unsigned ev = 0, pr = 0, ex = 0, dg = 0, nal = 0;
-    for (int q = 0; q < dp.N && !dg; ++q) {
-      ev += lr[q].evals;
-      pr += lr[q].pairs;
-      ex += lr[q].exits;
-      dg = (unsigned)lr[q].degen;
-      ++nal;
+  // warp 0, lane = restart: the counters in the oracle's sequential order (restarts run in order
+  // and a DegenerateAxis stops the ligand, so only restarts up to the first degenerate one count,
+  // P14), and the valid restarts in (geom desc, restart asc) order; the others tabulate the pairs
+  if (tid < 32) {
+    const bool in = tid < N;
+    const int val = in ? lr[tid].valid : 0, gq = in ? lr[tid].geom : 0;
+    const unsigned dgm = __ballot_sync(kFull, in && lr[tid].degen);
+    const int nal = dgm ? __ffs((int)dgm) : N;
+    const bool cnt = tid < nal;
+    const unsigned ev = __reduce_add_sync(kFull, cnt ? lr[tid].evals : 0u);
+    const unsigned pr = __reduce_add_sync(kFull, cnt ? lr[tid].pairs : 0u);
+    const unsigned ex = __reduce_add_sync(kFull, cnt ? lr[tid].exits : 0u);
+    const unsigned vm = __ballot_sync(kFull, val);
+    int rank = 0;
+    for (int q = 0; q < N; ++q) {
+      const int gp = __shfl_sync(kFull, gq, q);
+      rank += ((vm >> q) & 1u) && (gp > gq || (gp == gq && q < tid));
     }
-    T.s_cnt[0] = ev;
-    T.s_cnt[1] = pr;
-    T.s_cnt[2] = ex;
-    T.s_cnt[3] = dg;
-    T.s_nal = nal;
-    T.s_degf = dg ? lr[nal - 1].degen_f : 0;
+    if (val) T.ord[rank] = tid;
+    if (in) T.dis[tid] = 0u;
+    if (tid == 0) {
+      T.s_cnt[0] = ev;
+      T.s_cnt[1] = pr;
+      T.s_cnt[2] = ex;
+      T.s_cnt[3] = dgm != 0u;
+      T.s_nal = (unsigned)nal;
+      T.s_degf = dgm ? lr[nal - 1].degen_f : 0;
+      T.nvp = __popc(vm);  // the valid restarts
+    }
+  } else {
+    for (int pidx = tid - 32; pidx < npairs; pidx += NTH - 32) {
+      int p = 0, rem = pidx;
+      while (rem >= N - 1 - p) {
+        rem -= N - 1 - p;
+        ++p;
+      }
+      T.vp[pidx] = (uint16_t)(p | (p + 1 + rem) << 8);
+    }
   }
   __syncthreads();
   ds_result res;
@@ -319,139 +358,115 @@ __device__ __forceinline__ void lat_tail(LatTail &T, const float4 *U, int degen,
     // the sequential oracle stops at restart rd, fragment fd: later records stay zero
     const int rd = (int)T.s_nal - 1, fd = T.s_degf;
     if (out.rrec)
-      for (int q = rd + tid; q < dp.N; q += NTH) {
+      for (int q = rd + tid; q < N; q += NTH) {
         ds_restart_record z;
         memset(&z, 0, sizeof z);
-        out.rrec[(size_t)lig * dp.N + q] = z;
+        out.rrec[(size_t)lig * N + q] = z;
       }
-    for (int q = tid; q < F * dp.N; q += NTH) {
-      const int f = q / dp.N, rr = q - f * dp.N;
-      uint8_t v = __ldcg(out.rtors + (size_t)f0 * dp.N + q);
+    for (int q = tid; q < nrt; q += NTH) {
+      const int f = q / N, rr = q - f * N;
+      uint8_t v = __ldcg(out.rtors + (size_t)f0 * N + q);
       if (rr > rd || (rr == rd && f >= fd)) {
         v = 0;
-        out.rtors[(size_t)f0 * dp.N + q] = 0;
+        out.rtors[(size_t)f0 * N + q] = 0;
       }
-      if (out.rtors_host) out.rtors_host[(size_t)f0 * dp.N + q] = v;
+      if (out.rtors_host) out.rtors_host[(size_t)f0 * N + q] = v;
     }
     return;
   }
-  int nvalid = 0;
-  for (int q = 0; q < dp.N; ++q) nvalid += T.s_valid[q];
+  const int nvalid = T.nvp;
   if (nvalid == 0) {
     res.status = DS_STATUS_NO_VALID_POSE;
     if (tid == 0) out.res[lig] = res;
     return;
   }
-  if (tid < dp.N && T.s_valid[tid]) {
-    int rank = 0;
-    for (int q = 0; q < dp.N; ++q)
-      rank += T.s_valid[q] && (T.s_geom[q] > T.s_geom[tid] || (T.s_geom[q] == T.s_geom[tid] && q < tid));
-    T.ord[rank] = tid;
-  }
-  const float4 *base_scr = out.final_u + (size_t)lig * dp.N * DS_MAX_ATOMS;
   const int heavy = T.heavy;
-  const int npairs = dp.N * (dp.N - 1) / 2;
-  // RMSD of every valid pair (P12) as the oracle's sequential f64 sum over the heavy atoms in atom
-  // order; hydrogens contribute +0.0 terms (an exact no-op), so terms can be made in parallel.
-  // Staged (the restarts' poses and the terms fit the free grid region): the poses in one parallel
-  // load, the terms by (pair, atom), then one thread per pair adds its terms in order.  Else a warp
-  // per pair: lanes make 32 atoms' terms at once, every lane adds them in order from shuffles.
-  const int nst = dp.N * A;
-  const bool posed = stage != nullptr && (size_t)nst * sizeof(float4) <= (size_t)stage_bytes;
-  bool staged = posed;
-  if (posed && tid == 0) T.nvp = 0;
-  __syncthreads();
-  if (posed) {
-    for (int pidx = tid; pidx < npairs; pidx += NTH) {  // the valid pairs, compacted
-      int p = 0, rem = pidx;
-      while (rem >= dp.N - 1 - p) {
-        rem -= dp.N - 1 - p;
-        ++p;
+  const double lim = __dmul_rn(dp.thr2, (double)heavy);
+  // RMSD of every valid pair (P12), a warp per pair.  The oracle compares its sequential f64 sum
+  // over the heavy atoms in atom order with thr2 * heavy; the lanes make the per-atom terms of 32
+  // atoms at once (hydrogens contribute +0.0, an exact no-op) and a tree sum T of them.  T and the
+  // sequential sum both lie within n u S of the exact sum S of the same terms (n <= 160 terms,
+  // u = 2^-53, so within 2e-14 S of each other), so a margin of 1e-12 relative decides the
+  // comparison exactly; only a pair inside the margin runs the sequential sum (every lane adds the
+  // terms in atom order from shuffles).
+  {
+    const int lane = tid & 31;
+    for (int k = tid >> 5; k < npairs; k += NTH / 32) {
+      const int p = T.vp[k] & 0xFF, q = T.vp[k] >> 8;
+      if (!lr[p].valid || !lr[q].valid) continue;
+      double t[(DS_MAX_ATOMS + 31) / 32];
+      double part = 0.0;
+#pragma unroll
+      for (int c = 0; c < (DS_MAX_ATOMS + 31) / 32; ++c) {
+        const int i = 32 * c + lane;
+        t[c] = 0.0;
+        if (i < A)
+          t[c] = posed ? rmsd_term(stage[p * A + i], stage[q * A + i])
+                       : rmsd_term(__ldcg(base_scr + (size_t)p * DS_MAX_ATOMS + i),
+                                   __ldcg(base_scr + (size_t)q * DS_MAX_ATOMS + i));
+        part = __dadd_rn(part, t[c]);
       }
-      const int q = p + 1 + rem;
-      if (T.s_valid[p] && T.s_valid[q]) T.vp[atomicAdd(&T.nvp, 1)] = (uint16_t)(p | q << 8);
-    }
-    for (int w = tid; w < nst; w += NTH) {
-      const int q = w / A, i = w - q * A;
-      if (T.s_valid[q]) stage[w] = __ldcg(base_scr + (size_t)q * DS_MAX_ATOMS + i);
-    }
-    __syncthreads();
-    const int nvp = T.nvp;
-    staged = (size_t)nst * sizeof(float4) + (size_t)nvp * A * sizeof(double) <= (size_t)stage_bytes;
-    if (staged) {
-      double *terms = reinterpret_cast<double *>(stage + nst);  // [atom][pair]
-      for (int w = tid; w < nvp * A; w += NTH) {
-        const int i = w / nvp, k = w - i * nvp;
-        const int p = T.vp[k] & 0xFF, q = T.vp[k] >> 8;
-        terms[w] = rmsd_term(stage[p * A + i], stage[q * A + i]);
-      }
-      __syncthreads();
-      for (int k = tid; k < nvp; k += NTH) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(kFull, part, o));
+      bool dis;
+      if (__dmul_rn(part, 1.0 - 1e-12) >= lim) {
+        dis = true;
+      } else if (__dmul_rn(part, 1.0 + 1e-12) < lim) {
+        dis = false;
+      } else {
         double sum = 0.0;
-        for (int i = 0; i < A; ++i) sum = __dadd_rn(sum, terms[i * nvp + k]);
-        const int p = T.vp[k] & 0xFF, q = T.vp[k] >> 8;
-        if (heavy > 0 && sum >= __dmul_rn(dp.thr2, (double)heavy)) {
-          atomicOr(&T.dis[p], 1u << q);
-          atomicOr(&T.dis[q], 1u << p);
-        }
+#pragma unroll
+        for (int c = 0; c < (DS_MAX_ATOMS + 31) / 32; ++c)
+          if (32 * c < A)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sum = __dadd_rn(sum, __shfl_sync(kFull, t[c], j));
+        dis = sum >= lim;
+      }
+      if (lane == 0 && heavy > 0 && dis) {
+        atomicOr(&T.dis[p], 1u << q);
+        atomicOr(&T.dis[q], 1u << p);
       }
     }
   }
-  const int warp = tid >> 5;
-  for (int pidx = staged ? npairs : warp; pidx < npairs; pidx += NTH / 32) {
-    int p = 0, rem = pidx;
-    while (rem >= dp.N - 1 - p) {
-      rem -= dp.N - 1 - p;
-      ++p;
-    }
-    const int q = p + 1 + rem;
-    if (!T.s_valid[p] || !T.s_valid[q]) continue;
-    const float4 *up = base_scr + (size_t)p * DS_MAX_ATOMS, *uq = base_scr + (size_t)q * DS_MAX_ATOMS;
-    double t[(DS_MAX_ATOMS + 31) / 32];
-#pragma unroll
-    for (int k = 0; k < (DS_MAX_ATOMS + 31) / 32; ++k) {
-      const int i = 32 * k + lane;
-      t[k] = 0.0;
-      if (i < A) t[k] = rmsd_term(__ldcg(up + i), __ldcg(uq + i));
-    }
-    double sum = 0.0;
-#pragma unroll
-    for (int k = 0; k < (DS_MAX_ATOMS + 31) / 32; ++k)
-      if (32 * k < A)
-#pragma unroll
-        for (int j = 0; j < 32; ++j) sum = __dadd_rn(sum, __shfl_sync(kFull, t[k], j));
-    if (lane == 0 && heavy > 0 && sum >= __dmul_rn(dp.thr2, (double)heavy)) {
-      atomicOr(&T.dis[p], 1u << q);
-      atomicOr(&T.dis[q], 1u << p);
-    }
-  }
   __syncthreads();
-  if (tid == 0) {
+  MARK2(3, lig * dp.N + r);
+  // warp 0: the greedy keep in rank order (a candidate is kept when it is dissimilar to every pose
+  // kept so far), then the best rescored kept pose (ties -> smallest restart)
+  if (tid < 32) {
+    const int oc = tid < nvalid ? T.ord[tid] : 0;
+    const unsigned od = tid < nvalid ? T.dis[oc] : 0u;
+    unsigned km = 0u;
     int nk = 0;
     for (int o = 0; o < nvalid && nk < dp.K; ++o) {
-      const int c = T.ord[o];
-      bool ok = true;
-      for (int t = 0; t < nk; ++t) ok = ok && ((T.dis[c] >> T.kept[t]) & 1u);
-      if (ok) T.kept[nk++] = c;
+      const int c = __shfl_sync(kFull, oc, o);
+      const unsigned d = __shfl_sync(kFull, od, o);
+      if ((d & km) == km) {
+        if (tid == nk) T.kept[nk] = c;
+        km |= 1u << c;
+        ++nk;
+      }
     }
-    T.nkept = nk;
+    __syncwarp();
+    const int rr = tid < nk ? T.kept[tid] : 0x7FFFFFFF;
+    long long ch = tid < nk ? lr[rr].chem : LLONG_MIN;
+    long long bc = ch;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bc = max(bc, __shfl_xor_sync(kFull, bc, o));
+    const int br = __reduce_min_sync(kFull, (unsigned)(ch == bc ? rr : 0x7FFFFFFF));
+    if (tid < nk && out.rrec) out.rrec[(size_t)lig * N + rr].kept = (uint8_t)(tid + 1);
+    if (tid == 0) {
+      T.nkept = nk;
+      T.s_cnt[0] = (unsigned)br;
+      T.chem = (unsigned long long)bc;
+    }
   }
   __syncthreads();
-  const int nk = T.nkept;
-  long long best_chem = 0;
-  int best_r = -1;
-  for (int t = 0; t < nk; ++t) {
-    const int rr = T.kept[t];
-    const long long chem = lr[rr].chem;
-    if (best_r < 0 || chem > best_chem || (chem == best_chem && rr < best_r)) {
-      best_chem = chem;
-      best_r = rr;
-    }
-    if (tid == 0 && out.rrec) out.rrec[(size_t)lig * dp.N + rr].kept = (uint8_t)(t + 1);
-  }
+  MARK2(4, lig * dp.N + r);
+  const int nk = T.nkept, best_r = (int)T.s_cnt[0];
+  const long long best_chem = (long long)T.chem;
   const int brot = (int)lr[best_r].rot;
   res.status = DS_STATUS_OK;
-  res.geom_score = T.s_geom[best_r];
+  res.geom_score = lr[best_r].geom;
   res.chem_fx = best_chem;
   res.best_restart = (uint8_t)best_r;
   res.best_ax = (uint8_t)(brot / dp.n_a);
@@ -468,10 +483,10 @@ __device__ __forceinline__ void lat_tail(LatTail &T, const float4 *U, int degen,
     }
   if (out.best_tors)
     for (int f = tid; f < F; f += NTH)
-      out.best_tors[f0 + f] = __ldcg(out.rtors + (size_t)(f0 + f) * dp.N + best_r);
+      out.best_tors[f0 + f] = posed ? srt[f * N + best_r] : __ldcg(out.rtors + (size_t)(f0 + f) * N + best_r);
   if (out.rtors_host)  // zero-copy outputs: every restart's torsion indices, straight to the host
-    for (int q = tid; q < F * dp.N; q += NTH)
-      out.rtors_host[(size_t)f0 * dp.N + q] = __ldcg(out.rtors + (size_t)f0 * dp.N + q);
+    for (int q = tid; q < nrt; q += NTH)
+      out.rtors_host[(size_t)f0 * N + q] = posed ? srt[q] : __ldcg(out.rtors + (size_t)f0 * N + q);
   MARK(4, lig * dp.N + r);
 }
 
@@ -758,17 +773,25 @@ __global__ void __launch_bounds__(kLatThreads, 1)
 // The fragment chain is the latency family's critical path (~2.4 us per fragment of dependent,
 // barrier-separated phases on one SM).  Fragment f + 1 depends on f only through the angle f
 // commits, and there are n_t of those (every angle bumped = no commit = angle 0's positions), so
-// a cluster of n_t CTAs evaluates fragments in pairs: in every CTA, thread group 0 sweeps f on the
-// current pose (the same bits in every CTA), while group 1 of CTA h commits angle h of f on a copy
-// and sweeps f + 1 on it.  As soon as group 0 has a_f, group 1 of CTA a_f (CTA 0 when every angle
-// of f bumped) pushes its pose (f and f + 1 committed) and its outcome for f + 1 into every CTA's
-// shared memory through DSMEM stores; one cluster barrier later every CTA moves on to f + 2 with
-// only local reads: half the chain length, on n_t x N SMs instead of N.  Results are
-// bit-identical to the sequential chain (the pose is CTA a_f's, computed by the same operations).
-constexpr int kSpecH = 10;        // hypotheses per fragment = torsion angles = cluster size
-constexpr int kGrpThreads = 256;  // threads per group (two groups per CTA)
+// a cluster evaluates fragments in pairs.  The lead (thread group 0 of CTA 0) sweeps f on the
+// current pose; thread group 1 of CTA h commits angle h of f on a copy of the pose and sweeps
+// f + 1 on it, concurrently.  The lead publishes its outcome for f into every CTA's shared memory
+// (DSMEM stores, each followed by a release arrive on that CTA's mbarrier); group 1 of CTA a_f
+// (CTA 0 when every angle of f bumped), the winner, then pushes its pose — f and f + 1 committed
+// — and its outcome for f + 1 the same way, and every CTA moves on to f + 2 as soon as that one
+// push has landed: the losing hypotheses are never waited for.  Half the chain length, on
+// n_t x N SMs instead of N; bit-identical to the sequential chain (the pose is the winner's,
+// computed by the same operations).  Ordering: the pose is double-buffered, and the lead
+// publishes a_f only after every hypothesis group has signalled (rbar) that it has read the
+// step's pose, so a push never overwrites a buffer that is still being read.  (Group 0 of
+// CTAs 1 .. n_t - 1 idles: 1 + n_t single-group CTAs would not all be resident — one GPC of the
+// B200 holds fewer than 11 CTAs of this size, so only 7 such clusters fit.)
+constexpr int kSpecH = 10;             // hypotheses per fragment = torsion angles = cluster size
+constexpr int kSpecT = 256;            // threads per group (two groups per CTA)
+constexpr int kAlignR = 900 / kSpecH;  // alignment rotations per CTA (n_a = 30): 3 ax x 30 ay
+constexpr int kAlignG = 11;            // atom groups per (ax, ay pair) (3 x 15 x kAlignG <= 2 kSpecT)
 
-struct LatGrp {                   // one thread group's per-fragment scratch
+struct LatGrp {                        // a CTA's per-fragment scratch
   float2 chr[DS_MAX_ATOMS];
   float2 chm[DS_MAX_ATOMS];
   uint8_t mlist[DS_MAX_ATOMS];
@@ -780,20 +803,57 @@ struct LatGrp {                   // one thread group's per-fragment scratch
   unsigned abump;
 };
 
-struct SpecRec {                  // one fragment's outcome (the group's thread 0 writes it)
-  int best_k;                     // committed angle, -1: every angle bumped
-  int delta;                      // grid-score change of the committed angle: ascore[k] - ascore[0]
+// one fragment's outcome packed into 64 bits, so that a single (single-copy atomic) DSMEM store
+// carries it together with its validity tag:
+//   [0, 8) tag = step + 1   [8] degenerate axis   [9, 13) committed angle + 1 (0: every angle bumped)
+//   [13, 18) early exits    [18, 36) score change of the committed angle + 2^17   [36, 64) P14 pairs
+struct SpecRec {
+  int best_k, delta, degen;
   unsigned pairs, exits;
-  int degen;
 };
+__device__ __forceinline__ unsigned long long spec_pack(unsigned tag, int degen, int best_k, int delta, unsigned pairs,
+                                                        unsigned exits) {
+  return (unsigned long long)tag | (unsigned long long)degen << 8 | (unsigned long long)(best_k + 1) << 9 |
+         (unsigned long long)exits << 13 | (unsigned long long)(delta + 131072) << 18 | (unsigned long long)pairs << 36;
+}
+__device__ __forceinline__ SpecRec spec_unpack(unsigned long long v) {
+  SpecRec r;
+  r.degen = (int)((v >> 8) & 1u);
+  r.best_k = (int)((v >> 9) & 15u) - 1;
+  r.exits = (unsigned)((v >> 13) & 31u);
+  r.delta = (int)((v >> 18) & 0x3FFFFu) - 131072;
+  r.pairs = (unsigned)(v >> 36);
+  return r;
+}
 
 __device__ __forceinline__ void grp_sync(int id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kGrpThreads) : "memory");
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kSpecT) : "memory");
 }
-// named barrier across both groups: the producer arrives (its prior shared-memory writes become
-// visible to the waiters), the consumer waits
-__device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// the shared::cluster address of p in CTA rank
+__device__ __forceinline__ unsigned dsmem(const void *p, unsigned rank) {
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(p)), "r"(rank));
+  return ra;
+}
+// publish a tagged 64-bit record into CTA rank's slot; wait for this CTA's slot to carry tag
+__device__ __forceinline__ void slot_put(unsigned long long *slot, unsigned rank, unsigned long long v) {
+  asm volatile("st.relaxed.cluster.shared::cluster.u64 [%0], %1;" ::"r"(dsmem(slot, rank)), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long slot_get(const unsigned long long *slot, unsigned tag) {
+  unsigned long long v;
+  do {
+    asm volatile("ld.relaxed.cluster.shared::cta.u64 %0, [%1];" : "=l"(v) : "r"(smem_addr(slot)) : "memory");
+  } while ((unsigned)(v & 0xFFu) != tag);
+  return v;
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long *bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tLAB_WAITC:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONEC;\n\tbra LAB_WAITC;\n\tDONEC:\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
 
 // the torsion axis of a fragment from the positions U (the recipe of the sequential kernel);
 // false when it is degenerate
@@ -833,19 +893,21 @@ __device__ __forceinline__ float grp_min_d2(const float4 *U, const LatGrp &S, in
 }
 
 // one fragment's phases (A) compaction + cylindrical coordinates, (C) bump candidates, (D) the
-// angle sweep, (E) best clean angle, by one group of kGrpThreads threads (gt = thread in group,
+// angle sweep, (E) best clean angle, by the kSpecT threads of a CTA (gt = thread index,
 // barrier id bar) on the positions U, which it does not modify.  Returns the committed angle
 // (-1: all bumped, -2: degenerate axis), the same in every thread of the group; the group's
-// thread 0 writes rec.  The axis and the moving count are left for the caller's commit.
+// lanes of warp 0 get the packed outcome (spec_pack; the tag is the caller's).  The axis and the
+// moving count are left for the caller's commit.
 template <bool kSmemGrid>
 __device__ __forceinline__ int lat_frag(const float4 *U, LatGrp &S, uint4 fa, uint4 fb, int A, const GridGeom &g,
                                         const uint8_t *grid, const float2 *strig, const DockParams &dp, int gt,
-                                        int bar, SpecRec &rec, float3 &a3, float &kx, float &ky, float &kz, int &nMo) {
+                                        int bar, unsigned long long &rec, float3 &a3, float &kx, float &ky, float &kz,
+                                        int &nMo) {
   constexpr int kNT = kSpecH;
   const int lane = gt & 31, warp = gt >> 5;
   const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
   if (!lat_axis(U, ab, ae, dp.eps_axis, a3, kx, ky, kz)) {
-    if (gt == 0) rec.degen = 1;
+    rec = spec_pack(0, 1, -1, 0, 0u, 0u);
     return -2;
   }
   // ---- (A) ----
@@ -897,8 +959,8 @@ __device__ __forceinline__ int lat_frag(const float4 *U, LatGrp &S, uint4 fa, ui
   if (nC > 0) {
     const int total = nM * nC;
     int pm = small_div(gt, nC), pc = gt - pm * nC;
-    const int dm = small_div(kGrpThreads, nC), dc = kGrpThreads - dm * nC;
-    for (int p0 = 0; p0 < total; p0 += kGrpThreads) {
+    const int dm = small_div(kSpecT, nC), dc = kSpecT - dm * nC;
+    for (int p0 = 0; p0 < total; p0 += kSpecT) {
       if (p0 + gt < total) {
         const float2 hm = S.chm[pm], hc = S.chr[pc];
         const float dh = hm.x - hc.x, dr = hm.y - hc.y;
@@ -918,7 +980,7 @@ __device__ __forceinline__ int lat_frag(const float4 *U, LatGrp &S, uint4 fa, ui
   grp_sync(bar);
   // ---- (D) thread = (angle a, moving-atom group mg), as in k_optimize_latency ----
   {
-    constexpr int G = kGrpThreads / kNT;
+    constexpr int G = kSpecT / kNT;
     const int mg = gt / kNT, a = gt - mg * kNT;
     if (mg < G) {
       float R[9];
@@ -965,13 +1027,7 @@ __device__ __forceinline__ int lat_frag(const float4 *U, LatGrp &S, uint4 fa, ui
       np = (dp.early_exit && mb != 0x7FFFFFFF) ? (unsigned)((mb + 1) * nC) : (unsigned)(nM * nC);
     }
     np = __reduce_add_sync(kFull, np);
-    if (lane == 0) {
-      rec.best_k = best_k;
-      rec.delta = best ? (int)(best >> 8) - 65536 : 0;
-      rec.pairs = np;
-      rec.exits = dp.early_exit ? (unsigned)__popc(abump) : 0u;
-      rec.degen = 0;
-    }
+    rec = spec_pack(0, 0, best_k, best ? (int)(best >> 8) - 65536 : 0, np, dp.early_exit ? (unsigned)__popc(abump) : 0u);
   }
   nMo = nM;
   return best_k;
@@ -989,24 +1045,26 @@ __device__ __forceinline__ void lat_commit(float4 *U, const LatGrp &S, int nM, c
 }
 
 template <bool kSmemGrid>
-__global__ void __launch_bounds__(2 * kGrpThreads, 1)
-    k_optimize_latency_spec(PocketView pk, BatchView bt, DockParams dp, const unsigned *keys, OptOut out,
-                            LatRec *recs, int *done) {
-  constexpr int NTH = 2 * kGrpThreads;
-  // P[cur]: the committed pose; P[cur ^ 1]: the next one, written by the winning CTA of the step
-  __shared__ __align__(16) float4 P[2][DS_MAX_ATOMS];
-  __shared__ __align__(16) float4 Q[DS_MAX_ATOMS];      // group 1's hypothesis pose
-  __shared__ LatGrp GS[2];
-  __shared__ SpecRec R0[2];                             // group 0's outcome for f (by step parity)
-  __shared__ SpecRec R1loc;                             // group 1's outcome for f + 1
-  __shared__ SpecRec R1in[2];                           // the winner's outcome for f + 1 (pushed)
+__global__ void __launch_bounds__(2 * kSpecT, 1)
+    k_optimize_latency_spec(PocketView pk, BatchView bt, DockParams dp, OptOut out, LatRec *recs, int *done) {
+  constexpr int NTH = 2 * kSpecT;
+  constexpr int kSteps = (DS_MAX_ATOMS - 2 + 1) / 2;
+  __shared__ __align__(16) float4 P[DS_MAX_ATOMS];  // the committed pose (every CTA its own copy)
+  __shared__ __align__(16) float4 Q[DS_MAX_ATOMS];  // the hypothesis group's pose
+  __shared__ LatGrp GS[2];                          // [0]: the lead (CTA 0), [1]: the hypothesis group
+  // published outcomes, one slot per step (written once, so never overwritten while unread):
+  // slot0: the lead's for f, slot1: the winner's for f + 1
+  __shared__ unsigned long long slot0[kSteps], slot1[kSteps];
+  __shared__ unsigned long long kslot[kSpecH];      // every CTA's best alignment key
+  __shared__ int apart[kAlignG][kAlignR];           // alignment partial scores (atom group, rotation)
   __shared__ LatTail T;
   __shared__ unsigned s_key;
   __shared__ __align__(8) unsigned long long bar[2];
   extern __shared__ __align__(16) unsigned char dsm[];
   cg::cluster_group cl = cg::this_cluster();
   const int h = (int)cl.block_rank();
-  const int tid = threadIdx.x, grp = tid / kGrpThreads, gt = tid - grp * kGrpThreads;
+  const int tid = threadIdx.x, grp = tid / kSpecT, gt = tid - grp * kSpecT;
+  const bool lead = h == 0 && grp == 0, hyp = grp == 1;
   const int lr = blockIdx.x / kSpecH;
   const int lig = lr / dp.N, r = lr - lig * dp.N;
   if (h == 0) MARK(0, lr);
@@ -1026,69 +1084,131 @@ __global__ void __launch_bounds__(2 * kGrpThreads, 1)
     mbar_fence_init();
     mbar_expect_tx(&bar[0], 360 * sizeof(float2));
     bulk_g2s(strig, pk.trig, 360 * sizeof(float2), &bar[0]);
-    mbar_expect_tx(&bar[1], 32u * F + wbytes + lut_bulk + (kSmemGrid ? pk.grid_bytes : 0));
+    mbar_expect_tx(&bar[1], 32u * F + wbytes + lut_bulk + pk.grid_bytes);
     if (F) bulk_g2s(sfrag, bt.frags + 2 * (size_t)f0, 32u * F, &bar[1]);
     bulk_g2s(sw, pk.wfx, wbytes, &bar[1]);
     if (lut_bulk) bulk_g2s(slut, pk.bin_lut, lut_bulk, &bar[1]);
-    if (kSmemGrid) bulk_g2s(const_cast<uint8_t *>(grid), pk.grid, pk.grid_bytes, &bar[1]);
     T.geom = 0;
     T.heavy = 0;
     T.chem = 0ull;
   }
+  for (int i = tid; i < kSteps; i += NTH) {
+    slot0[i] = 0ull;
+    slot1[i] = 0ull;
+  }
+  if (tid < kSpecH) kslot[tid] = 0ull;
+  if (tid == 0) s_key = 0u;
   for (int i = lut_bulk + tid; i < lut_n; i += NTH) slut[i] = __ldg(pk.bin_lut + i);
-  __syncthreads();
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (tid == 0) s_key = __ldcg(keys + (size_t)lig * dp.N + r);
-  __syncthreads();
+  cl.sync();  // every CTA's barriers are initialised and slots cleared before any remote write
+  if (h == 0) MARK2(5, lr);
+  // the pocket grid: CTA h fetches slice h once and the TMA engine multicasts it into all the
+  // cluster's CTAs (each CTA's bar[1] counts the whole grid): 1/10 of the L2 reads
+  if (tid == 0) {
+    const unsigned sl = ((unsigned)pk.grid_bytes / kSpecH + 15u) & ~15u;
+    const unsigned lo = min((unsigned)pk.grid_bytes, h * sl), hi = min((unsigned)pk.grid_bytes, lo + sl);
+    if (hi > lo)
+      bulk_g2s_multicast(const_cast<uint8_t *>(grid) + lo, pk.grid + lo, hi - lo, &bar[1], (1u << kSpecH) - 1u);
+  }
+  if (tid < A) Q[tid] = __ldg(bt.atoms + a0 + tid);  // the ligand's atoms (for the alignment)
   mbar_wait(&bar[0], 0);
-  const unsigned key = s_key;
+  // ---- alignment (Alg. 1 lines 4-7, P6) spread over the cluster: CTA h scores the 90 rotations
+  // of ax in [3 h, 3 h + 3); a thread takes one ax, a pair of ay (v = R' d shared, the two angles'
+  // x / z coordinates in packed f32x2 arithmetic, each lane bit-identical to the scalar recipe)
+  // and every kAlignG-th atom; integer sums, so the split does not change them.  Every CTA
+  // publishes its best key into every CTA and all take the maximum: the cluster alignment
+  // kernel's key. ----
+  float R0s[9], Tt[3];
+  start_params(bt.idh[lig], dp.seed, r, strig, pk.inv_s, g.nx, g.ny, g.nz, R0s, Tt);
+  mbar_wait(&bar[1], 0);
+  __syncthreads();  // the atoms in Q
+  if (h == 0) MARK2(6, lr);
+  if (tid < kAlignG * (kAlignR / 2)) {
+    const int j = tid / (kAlignR / 2), pr = tid - j * (kAlignR / 2);  // pr = ax_local * 15 + ay pair
+    const int axl = pr / 15, ay = 2 * (pr - axl * 15);
+    float Rp[9];
+    align_rx(strig[(3 * h + axl) * dp.step_a], R0s, Rp);
+    const float2 c0 = strig[ay * dp.step_a], c1 = strig[(ay + 1) * dp.step_a];
+    const f2_t C = f2_pack(c0.x, c1.x), S = f2_pack(c0.y, c1.y), NS = f2_pack(-c0.y, -c1.y);
+    const f2_t TX = f2_pack(Tt[0], Tt[0]), TZ = f2_pack(Tt[2], Tt[2]), MM = f2_pack(kMagic, kMagic);
+    const unsigned K = (unsigned)(kMagicBits - 1);
+    int s0 = 0, s1 = 0;
+#pragma unroll 4
+    for (int i = j; i < A; i += kAlignG) {
+      const float4 d = Q[i];
+      const float3 v = align_v(Rp, d.x, d.y, d.z);
+      const unsigned yk = g.NX * clamp_bits(__fadd_rn(v.y, Tt[1]), g.by);
+      const f2_t VX = f2_pack(v.x, v.x), VZ = f2_pack(v.z, v.z);
+      float mx0, mx1, mz0, mz1;
+      f2_unpack(f2_add(f2_fma(S, VZ, f2_fma(C, VX, TX)), MM), mx0, mx1);
+      f2_unpack(f2_add(f2_fma(C, VZ, f2_fma(NS, VX, TZ)), MM), mz0, mz1);
+      const unsigned i0 = min((unsigned)__float_as_int(mx0) - K, g.bx) + g.NXY * min((unsigned)__float_as_int(mz0) - K, g.bz) + yk;
+      const unsigned i1 = min((unsigned)__float_as_int(mx1) - K, g.bx) + g.NXY * min((unsigned)__float_as_int(mz1) - K, g.bz) + yk;
+      s0 += lat_grid_val<true>(grid, (int)i0);
+      s1 += lat_grid_val<true>(grid, (int)i1);
+    }
+    apart[j][axl * 30 + ay] = s0;
+    apart[j][axl * 30 + ay + 1] = s1;
+  }
+  __syncthreads();
+  if (tid < 32 * ((kAlignR + 31) / 32)) {
+    unsigned best = 0u;
+    if (tid < kAlignR) {
+      int sc = 0;
+#pragma unroll
+      for (int j = 0; j < kAlignG; ++j) sc += apart[j][tid];
+      best = ((unsigned)(sc + 32768) << 16) | (unsigned)(65535 - (h * kAlignR + tid));
+    }
+    best = __reduce_max_sync(kFull, best);
+    if ((tid & 31) == 0) atomicMax(&s_key, best);
+  }
+  __syncthreads();
+  if (h == 0) MARK2(7, lr);
+  if (tid < kSpecH) slot_put(&kslot[h], tid, (unsigned long long)s_key << 32 | 0xA5u);
+  unsigned key = 0u;
+  for (int c = 0; c < kSpecH; ++c) key = max(key, (unsigned)(slot_get(&kslot[c], 0xA5u) >> 32));
   int total = (int)(key >> 16) - 32768;
   const int rot = 65535 - (int)(key & 0xFFFFu);
   const int ix = rot / dp.n_a, iy = rot - ix * dp.n_a;
   if (tid < A) {
-    float R0s[9], Tt[3], Rp[9];
-    start_params(bt.idh[lig], dp.seed, r, strig, pk.inv_s, g.nx, g.ny, g.nz, R0s, Tt);
+    float Rp[9];
     align_rx(strig[ix * dp.step_a], R0s, Rp);
     const float2 cy = strig[iy * dp.step_a];
-    const float4 d = __ldg(bt.atoms + a0 + tid);
+    const float4 d = Q[tid];
     const float3 u = align_u(align_v(Rp, d.x, d.y, d.z), cy.x, cy.y, Tt);
-    P[0][tid] = make_float4(u.x, u.y, u.z, d.w);
+    P[tid] = make_float4(u.x, u.y, u.z, d.w);
   }
   __syncthreads();
-  mbar_wait(&bar[1], 0);
   if (h == 0) MARK(1, lr);
   unsigned evals = 0, exits = 0, pairs = 0;
-  int all_bumped = 0, degen = 0, degen_f = 0, cur = 0;
+  int all_bumped = 0, degen = 0, degen_f = 0;
 #ifdef DS_SPEC_PROBE
   long long t_step = clock64();
 #endif
-  for (int f = 0; f < F; f += 2) {
-    const int par = (f >> 1) & 1;
+  for (int f = 0, st = 0; (lead || hyp) && f < F; f += 2, ++st) {
+    const unsigned tag = (unsigned)st + 1u;
     const bool two = f + 1 < F;  // uniform over the cluster
     const uint4 fa = sfrag[2 * f], fb = sfrag[2 * f + 1];
-    float4 *Pc = P[cur];
-    if (grp == 0) {
-      float3 a3;
-      float kx = 0.f, ky = 0.f, kz = 0.f;
-      int nM = 0;
-      const int k = lat_frag<kSmemGrid>(Pc, GS[0], fa, fb, A, g, grid, strig, dp, gt, 1, R0[par], a3, kx, ky, kz, nM);
-      if (gt == 0) SPROBE(0);
-      if (two)
-        nb_arrive(3, NTH);  // a_f is known: group 1 may decide whether it won
-      else if (k > 0)       // the chain's last, unpaired fragment: commit here (group 1 is idle)
-        lat_commit(Pc, GS[0], nM, strig, dp.step_t, k, a3, kx, ky, kz, gt, kGrpThreads);
-    } else if (two) {
-      // commit hypothesis h of fragment f on a copy of the pose, then sweep f + 1 on it
+    float3 fa3;                   // fragment f's axis (hypothesis group)
+    float fkx = 0.f, fky = 0.f, fkz = 0.f;
+    if (lead) {
       float3 a3;
       float kx, ky, kz;
+      int nM = 0;
+      unsigned long long rec = 0ull;
+      lat_frag<kSmemGrid>(P, GS[0], fa, fb, A, g, grid, strig, dp, gt, 1, rec, a3, kx, ky, kz, nM);
+      if (gt < kSpecH) slot_put(&slot0[st], gt, rec | tag);  // lane c publishes into CTA c
+      if (gt == 0) SPROBE(0);
+    } else {
+      // commit hypothesis h of fragment f on a copy of the pose, then sweep f + 1 on it
       const int ab = (int)(fb.y & 0xFFu), ae = (int)((fb.y >> 8) & 0xFFu);
-      const bool ok = lat_axis(Pc, ab, ae, dp.eps_axis, a3, kx, ky, kz);  // else group 0 reports the break
-      if (ok) {
+      const bool ok = lat_axis(P, ab, ae, dp.eps_axis, fa3, fkx, fky, fkz);  // else the lead reports the break
+      if (!two) grp_sync(2);  // every thread has read the axis atoms before the commit below
+      if (two && ok) {
         if (gt < A) {
-          const float4 p = Pc[gt];
+          const float4 p = P[gt];
           const bool mv = (frag_word(fa, fb, gt >> 5) >> (gt & 31)) & 1u;
           if (mv && h > 0) {
-            const float3 q = lat_torsion_pos(strig, dp.step_t, h, kx, ky, kz, a3, p);
+            const float3 q = lat_torsion_pos(strig, dp.step_t, h, fkx, fky, fkz, fa3, p);
             Q[gt] = make_float4(q.x, q.y, q.z, p.w);
           } else {
             Q[gt] = p;
@@ -1096,49 +1216,68 @@ __global__ void __launch_bounds__(2 * kGrpThreads, 1)
         }
         grp_sync(2);
         if (gt == 0) SPROBE(1);
+        float3 a3;
+        float kx, ky, kz;
         int nM = 0;
-        const int k = lat_frag<kSmemGrid>(Q, GS[1], sfrag[2 * f + 2], sfrag[2 * f + 3], A, g, grid, strig, dp, gt, 2,
-                                          R1loc, a3, kx, ky, kz, nM);
-        if (k > 0) lat_commit(Q, GS[1], nM, strig, dp.step_t, k, a3, kx, ky, kz, gt, kGrpThreads);
+        unsigned long long rec = 0ull;
+        lat_frag<kSmemGrid>(Q, GS[1], sfrag[2 * f + 2], sfrag[2 * f + 3], A, g, grid, strig, dp, gt, 2, rec, a3, kx, ky,
+                            kz, nM);
         if (gt == 0) SPROBE(2);
+        // the winner (CTA 0 when every angle of f bumped) publishes its outcome for f + 1
+        const SpecRec r0 = spec_unpack(slot_get(&slot0[st], tag));
+        if (gt == 0) SPROBE(3);
+        if (!r0.degen && h == (r0.best_k < 0 ? 0 : r0.best_k) && gt < kSpecH) slot_put(&slot1[st], gt, rec | tag);
       }
-      nb_sync(3, NTH);  // also orders every group-1 thread's commit before the push reads Q
-      if (gt == 0) SPROBE(3);
-      const SpecRec r0 = R0[par];
-      // the winning hypothesis (CTA 0's when every angle of f bumped) pushes its pose after f and
-      // f + 1 and its outcome for f + 1 into every CTA's shared memory, before the cluster barrier
-      if (ok && !r0.degen && h == (r0.best_k < 0 ? 0 : r0.best_k)) {
-        for (int u = gt; u < kSpecH * A; u += kGrpThreads) {
-          const int c = u / A, i = u - c * A;
-          cl.map_shared_rank(&P[cur ^ 1][0], c)[i] = Q[i];
-        }
-        if (gt < kSpecH) *cl.map_shared_rank(&R1in[par], gt) = R1loc;
-      }
-      if (gt == 0) SPROBE(4);
     }
-    if (two)
-      cl.sync();
-    else
-      __syncthreads();
-    if (tid == 0) SPROBE(5);
-#ifdef DS_SPEC_PROBE
-    t_step = clock64();
-#endif
-    const SpecRec r0 = R0[par];
-    if (r0.degen) {
+    const SpecRec r0 = spec_unpack(slot_get(&slot0[st], tag));
+    if (r0.degen) {  // a degenerate axis at f: the chain stops (every group alike)
       degen = 1;
       degen_f = f;
       break;
     }
+    SpecRec r1;
+    if (two) {
+      r1 = spec_unpack(slot_get(&slot1[st], tag));
+      if (gt == 0) SPROBE(4);
+    }
+    // every CTA commits a_f and a_{f+1} on its own pose, with the operations the lead and the
+    // winner used (so the bits are theirs); in CTA 0 the hypothesis group does it for both groups
+    if (hyp) {
+      if (r0.best_k > 0 && gt < A && ((frag_word(fa, fb, gt >> 5) >> (gt & 31)) & 1u)) {
+        const float4 p = P[gt];
+        const float3 q = lat_torsion_pos(strig, dp.step_t, r0.best_k, fkx, fky, fkz, fa3, p);
+        P[gt] = make_float4(q.x, q.y, q.z, p.w);
+      }
+      if (two && !r1.degen && r1.best_k > 0) {
+        grp_sync(2);
+        const uint4 ga = sfrag[2 * f + 2], gb = sfrag[2 * f + 3];
+        float3 b3;
+        float bkx, bky, bkz;
+        lat_axis(P, (int)(gb.y & 0xFFu), (int)((gb.y >> 8) & 0xFFu), dp.eps_axis, b3, bkx, bky, bkz);
+        grp_sync(2);  // every thread has read the axis atoms before they may move
+        if (gt < A && ((frag_word(ga, gb, gt >> 5) >> (gt & 31)) & 1u)) {
+          const float4 p = P[gt];
+          const float3 q = lat_torsion_pos(strig, dp.step_t, r1.best_k, bkx, bky, bkz, b3, p);
+          P[gt] = make_float4(q.x, q.y, q.z, p.w);
+        }
+      }
+    }
+    if (h == 0)
+      __syncthreads();  // CTA 0: the lead reads the committed pose next
+    else
+      grp_sync(2);
+    if (gt == 0) SPROBE(5);
+#ifdef DS_SPEC_PROBE
+    t_step = clock64();
+#endif
     evals += kSpecH;
     pairs += r0.pairs;
     exits += r0.exits;
     all_bumped += r0.best_k < 0;
     if (r0.best_k >= 0) total += r0.delta;
-    if (h == 0 && tid == 0)
+    if (lead && gt == 0)
       out.rtors[(size_t)(f0 + f) * dp.N + r] = r0.best_k < 0 ? (uint8_t)DS_TORSION_NONE : (uint8_t)r0.best_k;
     if (two) {
-      const SpecRec r1 = R1in[par];
       if (r1.degen) {
         degen = 1;
         degen_f = f + 1;
@@ -1149,17 +1288,15 @@ __global__ void __launch_bounds__(2 * kGrpThreads, 1)
       exits += r1.exits;
       all_bumped += r1.best_k < 0;
       if (r1.best_k >= 0) total += r1.delta;
-      if (h == 0 && tid == 0)
+      if (lead && gt == 0)
         out.rtors[(size_t)(f0 + f + 1) * dp.N + r] = r1.best_k < 0 ? (uint8_t)DS_TORSION_NONE : (uint8_t)r1.best_k;
-      cur ^= 1;
     }
   }
-  const float4 *Pf = P[cur];
-  // every CTA holds the final pose: the rescore (P11) is split over the cluster and summed into
-  // CTA 0 (exact 64-bit integer sum, so the split does not change it)
+  // every hypothesis group holds the final pose: the rescore (P11) is split over them and summed
+  // into CTA 0 (exact 64-bit integer sum, so the split does not change it)
   const int valid = !(F >= 1 && all_bumped == F);
-  if (!degen && valid) {
-    long long acc = lat_rescore_acc(Pf, A, pk, sw, slut, h * NTH + tid, kSpecH * NTH);
+  if (hyp && !degen && valid) {
+    long long acc = lat_rescore_acc(P, A, pk, sw, slut, h * kSpecT + gt, kSpecH * kSpecT);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
     if ((tid & 31) == 0 && acc) atomicAdd(cl.map_shared_rank(&T.chem, 0), (unsigned long long)acc);
@@ -1167,7 +1304,7 @@ __global__ void __launch_bounds__(2 * kGrpThreads, 1)
   cl.sync();  // no CTA leaves while another may still access its shared memory
   if (h != 0) return;
   MARK(2, lr);
-  lat_tail<NTH, false>(T, Pf, degen, degen_f, total, valid, key, ix, iy, rot, evals, pairs, exits, pk, dp, sw, slut,
+  lat_tail<NTH, false>(T, P, degen, degen_f, total, valid, key, ix, iy, rot, evals, pairs, exits, pk, dp, sw, slut,
                        out, recs, done, lig, r, a0, A, f0, F,
                        reinterpret_cast<float4 *>(const_cast<uint8_t *>(grid)), pk.grid_bytes);
 }
@@ -1181,65 +1318,68 @@ static int spec_mode() {
   return e ? atoi(e) : -1;
 }
 
-// returns the CTAs per (ligand, restart): kSpecH for the cluster-speculative kernel, else 1
-int launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
-                            const unsigned *keys, OptOut out, void *recs, int *done, bool pdl, cudaStream_t st) {
-  const size_t base = lat_base_bytes(pk.nb, pk.lut_cap);
-  static const int optin = [] {
-    int dev = 0, v = 0;
+static int smem_optin() {
+  static const int v = [] {
+    int dev = 0, x = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return v;
+    cudaDeviceGetAttribute(&x, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return x;
   }();
-  const size_t with_grid = base + (size_t)pk.grid_bytes;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  return v;
+}
+
+// The cluster-speculative kernel with its own alignment (one launch per call) when it applies:
+// the default 12-degree alignment step and 10 torsion angles, the grid in shared memory, and (unless
+// forced) every cluster of the call resident at once.  Returns false when the caller must run the
+// alignment kernel and the one-CTA chain instead.
+bool launch_spread_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, OptOut out, void *recs,
+                           int *done, cudaStream_t st) {
   const int mode = spec_mode();
-  if (keys && dp.n_t == kSpecH && mode != 0) {
-    auto kern = k_optimize_latency_spec<true>;
-    static const size_t spec_static = [] {
-      cudaFuncAttributes fa;
-      cudaFuncGetAttributes(&fa, (const void *)k_optimize_latency_spec<true>);
-      cudaFuncSetAttribute((const void *)k_optimize_latency_spec<true>,
-                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      return (size_t)fa.sharedSizeBytes;
-    }();
-    if (with_grid + spec_static + 1024 <= (size_t)optin) {
-      allow_max_smem((const void *)kern);
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(bt.L * dp.N * kSpecH);
-      cfg.blockDim = dim3(2 * kGrpThreads);
-      cfg.dynamicSmemBytes = with_grid;
-      cfg.stream = st;
-      attr[1].id = cudaLaunchAttributeClusterDimension;
-      attr[1].val.clusterDim.x = kSpecH;
-      attr[1].val.clusterDim.y = 1;
-      attr[1].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 2;
-      bool use = mode == 1;
-      if (!use) {  // resident clusters at this shared-memory size (cached per size)
-        static std::mutex mu;
-        static std::map<size_t, int> resident;
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = resident.find(with_grid);
-        if (it == resident.end()) {
-          int n = 0;
-          cudaLaunchConfig_t q = cfg;
-          q.numAttrs = 2;
-          if (cudaOccupancyMaxActiveClusters(&n, (const void *)kern, &q) != cudaSuccess) n = 0;
-          it = resident.emplace(with_grid, n).first;
-        }
-        use = bt.L * dp.N <= it->second;
-      }
-      if (use) {
-        cudaLaunchKernelEx(&cfg, kern, pk, bt, dp, keys, out, (LatRec *)recs, done);
-        return kSpecH;
-      }
+  if (mode == 0 || dp.n_t != kSpecH || dp.n_a != 30 || dp.step_a <= 0) return false;
+  auto kern = k_optimize_latency_spec<true>;
+  static const size_t spec_static = [] {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void *)k_optimize_latency_spec<true>);
+    cudaFuncSetAttribute((const void *)k_optimize_latency_spec<true>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                         1);
+    return (size_t)fa.sharedSizeBytes;
+  }();
+  const size_t with_grid = lat_base_bytes(pk.nb, pk.lut_cap) + (size_t)pk.grid_bytes;
+  if (with_grid + spec_static + 1024 > (size_t)smem_optin()) return false;
+  allow_max_smem((const void *)kern);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(bt.L * dp.N * kSpecH);
+  cfg.blockDim = dim3(2 * kSpecT);
+  cfg.dynamicSmemBytes = with_grid;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kSpecH;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (mode != 1) {  // resident clusters at this shared-memory size (cached per size)
+    static std::mutex mu;
+    static std::map<size_t, int> resident;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = resident.find(with_grid);
+    if (it == resident.end()) {
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, (const void *)kern, &cfg) != cudaSuccess) n = 0;
+      it = resident.emplace(with_grid, n).first;
     }
+    if (bt.L * dp.N > it->second) return false;
   }
-  const bool fits = with_grid + sizeof(LatSmem) + 1024 <= (size_t)optin;
+  cudaLaunchKernelEx(&cfg, kern, pk, bt, dp, out, (LatRec *)recs, done);
+  return true;
+}
+
+void launch_optimize_latency(const PocketView &pk, const BatchView &bt, const DockParams &dp, int *scores,
+                             const unsigned *keys, OptOut out, void *recs, int *done, bool pdl, cudaStream_t st) {
+  const size_t base = lat_base_bytes(pk.nb, pk.lut_cap);
+  const size_t with_grid = base + (size_t)pk.grid_bytes;
+  const bool fits = with_grid + sizeof(LatSmem) + 1024 <= (size_t)smem_optin();
   const bool nt10 = dp.n_t == 10;
   auto kern = fits ? (nt10 ? k_optimize_latency<true, 10> : k_optimize_latency<true, 0>)
                    : (nt10 ? k_optimize_latency<false, 10> : k_optimize_latency<false, 0>);
@@ -1250,10 +1390,12 @@ int launch_optimize_latency(const PocketView &pk, const BatchView &bt, const Doc
   cfg.blockDim = dim3(kLatThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kern, pk, bt, dp, scores, keys, out, (LatRec *)recs, done);
-  return 1;
 }
 
 }  // namespace ds
@@ -1261,6 +1403,9 @@ int launch_optimize_latency(const PocketView &pk, const BatchView &bt, const Doc
 #ifdef DS_SPEC_PROBE
 extern "C" int ds_probe_marks(unsigned long long *out) {
   return (int)cudaMemcpyFromSymbol(out, ds::g_marks, sizeof(ds::g_marks));
+}
+extern "C" int ds_probe_marks2(unsigned long long *out) {
+  return (int)cudaMemcpyFromSymbol(out, ds::g_marks2, sizeof(ds::g_marks2));
 }
 extern "C" int ds_probe_steps(long long *out) {
   return (int)cudaMemcpyFromSymbol(out, ds::g_steps, sizeof(ds::g_steps));

@@ -1,6 +1,6 @@
 """The latency family's cluster-speculative optimisation kernel: one (ligand,
-restart) over a cluster of n_t CTAs that evaluates fragment pairs (f on the current pose, f + 1
-under each of f's n_t possible commits).  Its results must be bit-identical to the oracle and to
+restart) over a cluster of n_t CTAs that evaluates fragment pairs (a lead thread group sweeps f on
+the current pose, a thread group of CTA h sweeps f + 1 under f's commit of angle h).  Its results must be bit-identical to the oracle and to
 the sequential one-CTA fragment chain, for every shape the chain has: no fragments, one, odd and
 even fragment counts, all-bumped fragments, degenerate axes at even and odd positions, early exit
 off, maximum ligands, restart counts that run the clusters in several waves.
@@ -41,7 +41,8 @@ def _same(s, q, batch):
         f0, f1 = batch.frag_off[i], batch.frag_off[i + 1]
         assert np.array_equal(s.best_coords[a0:a1], q.best_coords[a0:a1])
         assert np.array_equal(s.best_torsion[f0:f1], q.best_torsion[f0:f1])
-    assert np.array_equal(s.restarts, q.restarts)
+    for f in s.restarts.dtype.names:
+        assert np.array_equal(s.restarts[f], q.restarts[f]), (f, s.restarts[f], q.restarts[f])
     assert np.array_equal(s.restart_torsion, q.restart_torsion)
 
 
