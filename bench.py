@@ -294,7 +294,9 @@ def roofline_block(cal, kms, n, ms_step, peak_winst, work, peaks):
 def config2_leg(ctx, dp, pocket, table, cfg, local, reps=30):
     """BASELINE config 2: one ~90-atom, 20-bond ligand, time to result (H2D + kernels + D2H) of the
     latency vs the batched family, the CPU oracle on one core and the latency engine's CPU shape on
-    all cores; parity of both families against the oracle."""
+    all cores; parity of both families against the oracle.  "latency" is the library's own choice
+    for a single ligand (the cluster-speculative kernel, 10 CTAs per restart); "latency_chain"
+    forces the one-CTA-per-restart chain (DS_LATENCY_SPEC=0) for comparison."""
     from paper_2209_05069_b200 import io, native
     import oracle.oracle as orc
     cands = io.generate_dataset_batch(36, 20, 64, seed=2)
@@ -306,7 +308,13 @@ def config2_leg(ctx, dp, pocket, table, cfg, local, reps=30):
            "atoms": int(A[pick]), "fragments": 20}
     o = orc.dock_batch(lig, pocket, table, cfg, seed=0, threads=1)
     with ClockSampler(local) as clk:
-        for name, fam in (("latency", native.FAMILY_LATENCY), ("batched", native.FAMILY_BATCHED)):
+        for name, fam, spec in (("latency", native.FAMILY_LATENCY, None),
+                                ("latency_chain", native.FAMILY_LATENCY, "0"),
+                                ("batched", native.FAMILY_BATCHED, None)):
+            if spec is None:
+                os.environ.pop("DS_LATENCY_SPEC", None)
+            else:
+                os.environ["DS_LATENCY_SPEC"] = spec
             for _ in range(5):
                 g = ctx.dock(dp, packed, cfg, 0, fam, coords=True)
             dev, wall = [], []
@@ -319,7 +327,9 @@ def config2_leg(ctx, dp, pocket, table, cfg, local, reps=30):
                                       o.results["bump_checks_rows" if f == "bump_checks" else f].astype(np.int64))
                        for f in PARITY_FIELDS) and np.array_equal(g.best_coords, o.best_coords)
             out[name] = {"device_ms_median": float(np.median(dev)), "device_ms_min": float(np.min(dev)),
-                         "wall_ms_median": 1e3 * float(np.median(wall)), "parity_ok": bool(same)}
+                         "wall_ms_median": 1e3 * float(np.median(wall)), "parity_ok": bool(same),
+                         "ctas_per_restart": int(g.stats.lat_spread) if fam == native.FAMILY_LATENCY else None}
+        os.environ.pop("DS_LATENCY_SPEC", None)
     out["clocks"] = clk.summary()
     t0 = time.perf_counter()
     orc.dock_batch(lig, pocket, table, cfg, seed=0, threads=1)

@@ -235,13 +235,22 @@ __device__ __forceinline__ void bulk_g2s_multicast(void *dst, const void *src, u
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "h"((unsigned short)mask)
       : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+// the spin loop is C++ around one try_wait, so the compiler sees the loop
+__device__ __forceinline__ bool mbar_try(unsigned long long *bar, unsigned parity) {
+  unsigned ok;
   asm volatile(
-      "{\n\t.reg .pred P1;\n\tLAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_addr(bar)),
-      "r"(parity)
+      "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
       : "memory");
+  return ok != 0u;
 }
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+// CTA barrier without the .aligned requirement (threads of a warp may arrive from divergent
+// paths, e.g. right after an mbarrier spin loop)
+__device__ __forceinline__ void cta_sync_unaligned() { asm volatile("barrier.sync 0;" ::: "memory"); }
 
 }  // namespace ds

@@ -835,11 +835,15 @@ __device__ __forceinline__ unsigned dsmem(const void *p, unsigned rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(p)), "r"(rank));
   return ra;
 }
-// publish a tagged 64-bit record into CTA rank's slot; wait for this CTA's slot to carry tag
+// publish a tagged 64-bit record into CTA rank's slot, and wait for this CTA's slot to carry tag.
+// A slot is zeroed at kernel start (before a cluster barrier) and written once; the record
+// travels in the same single-copy-atomic word as its validity tag, so relaxed cluster-scope
+// (strong) accesses suffice and no fence is needed.  compute-sanitizer racecheck reports these
+// pairs (it orders cross-CTA shared-memory accesses by cluster barriers only); DESIGN.md §8.
 __device__ __forceinline__ void slot_put(unsigned long long *slot, unsigned rank, unsigned long long v) {
   asm volatile("st.relaxed.cluster.shared::cluster.u64 [%0], %1;" ::"r"(dsmem(slot, rank)), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long slot_get(const unsigned long long *slot, unsigned tag) {
+__device__ __forceinline__ unsigned long long slot_get(unsigned long long *slot, unsigned tag) {
   unsigned long long v;
   do {
     asm volatile("ld.relaxed.cluster.shared::cta.u64 %0, [%1];" : "=l"(v) : "r"(smem_addr(slot)) : "memory");
@@ -1120,7 +1124,7 @@ __global__ void __launch_bounds__(2 * kSpecT, 1)
   float R0s[9], Tt[3];
   start_params(bt.idh[lig], dp.seed, r, strig, pk.inv_s, g.nx, g.ny, g.nz, R0s, Tt);
   mbar_wait(&bar[1], 0);
-  __syncthreads();  // the atoms in Q
+  cta_sync_unaligned();  // the atoms in Q
   if (h == 0) MARK2(6, lr);
   if (tid < kAlignG * (kAlignR / 2)) {
     const int j = tid / (kAlignR / 2), pr = tid - j * (kAlignR / 2);  // pr = ax_local * 15 + ay pair
