@@ -389,8 +389,11 @@ def api_leg(batch, pocket, table, cfg, steps):
     """e2e through the reference-facing entry point: engines.batched_engine.run on a LigandBatch
     stream (bucketizer + dispatchers + result table), results compared with ds_dock's."""
     from paper_2209_05069_b200 import engines
-    kw = dict(table=table, capacities="device", workers=4, dispatchers_per_device=4)
-    engines.batched_engine.run(batch, pocket, cfg, **kw)   # warm-up: dispatcher contexts, pinned stream arena
+    kw = dict(table=table, capacities="device", workers=4, dispatchers_per_device=2)
+    # warm-up: dispatcher contexts, device streams, the pinned stream arena and two sets of pooled
+    # pinned outputs (a run overlaps the previous report, which the loop below still holds)
+    for _ in range(2):
+        rep = engines.batched_engine.run(batch, pocket, cfg, **kw)
     times, rep = [], None
     for _ in range(steps):
         t0 = time.perf_counter()
@@ -399,7 +402,7 @@ def api_leg(batch, pocket, table, cfg, steps):
     dt = float(np.mean(times))
     c = rep.counters
     return rep, {"value": batch.n / dt, "unit": "ligands/s", "ms_per_step": 1e3 * dt,
-                 "path": "engines.batched_engine.run(LigandBatch) -> bucketizer -> dispatchers -> ds_dock",
+                 "path": "engines.batched_engine.run(LigandBatch) -> producers (pack + ds_stream_upload) -> bucketizer -> dispatchers (ds_stream_dock) -> ds_stream_download",
                  "capacity": rep.dispatch_log[0]["capacity"] if rep.dispatch_log else None,
                  "batches_dispatched": c.batches_dispatched, "batch_fill_ratio_mean":
                      c.batch_fill_ratio_sum / c.batches_dispatched if c.batches_dispatched else None,

@@ -202,6 +202,27 @@ int ds_dock_resident(ds_ctx *ctx, const ds_pocket *pocket, ds_dev_batch *batch,
 int ds_batch_download(ds_ctx *ctx, ds_dev_batch *batch, const ds_outputs *out);
 void ds_batch_destroy(ds_dev_batch *batch);
 
+/* Engine stream (batched_engine.run; replaces the per-batch ds_dock of the
+ * reference's dispatcher): the packed ligand stream of one engine run is kept on the
+ * device.  ds_stream_begin sizes it for n_ligands (CSR offsets as in ds_batch_desc, kept by the
+ * stream) and zeroes the result records; producers call ds_stream_upload for the ranges [lo, hi)
+ * they have packed (base pointers of the WHOLE stream's arrays, ds_pack_ligands layout; pinned
+ * memory is DMA'd directly; synchronous, thread-safe for disjoint ranges); a dispatcher docks each
+ * batch the bucketizer detaches as a list of stream ligand numbers with ds_stream_dock (its own
+ * ctx: stream + scratch; batched family; each ligand at most once per run), and one
+ * ds_stream_download returns the records, best poses and best torsion indices of the whole stream
+ * (ds_outputs.restarts / restart_torsion must be NULL).  Buffers grow and are kept across runs. */
+typedef struct ds_stream ds_stream;
+int ds_stream_create(ds_ctx *ctx, ds_stream **out);
+void ds_stream_destroy(ds_stream *stream);
+int ds_stream_begin(ds_stream *stream, int32_t n_ligands, const int32_t *atom_off, const int32_t *frag_off,
+                    int32_t restarts);
+int ds_stream_upload(ds_stream *stream, int32_t lo, int32_t hi, const float *atom_xyzt, const uint32_t *frag_desc,
+                     const uint64_t *id_hash);
+int ds_stream_dock(ds_ctx *ctx, const ds_pocket *pocket, ds_stream *stream, const int32_t *sel, int32_t n_sel,
+                   const ds_dock_config *cfg, ds_stats *stats);
+int ds_stream_download(ds_ctx *ctx, ds_stream *stream, const ds_outputs *out);
+
 /* Device-side ingest: generate ligands first_index .. first_index +
  * count - 1 of a synthetic dataset (the same ligands as ds_generate_ligands with these shapes,
  * SPEC.md:443 generate_dataset) directly into the ctx's device buffers, packed as ds_pack_ligands

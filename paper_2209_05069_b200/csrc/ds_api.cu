@@ -128,6 +128,11 @@ struct ds_ctx {
   // no D2H); x_rtors_host is where the last CTA copies the per-restart torsion indices
   bool x_zero_copy = false;
   uint8_t *x_rtors_host = nullptr;
+  // during ds_stream_dock only: the engine stream's per-(ligand, restart) keys and (geom, valid)
+  // words (indexed by the stream's ligand numbers) and the batch's select order; null otherwise
+  uint32_t *sv_keys = nullptr;
+  int *sv_rgv = nullptr;
+  const int *sv_sel = nullptr;
   // pinned host staging
   void *h_stage = nullptr;
   size_t h_cap = 0;
@@ -801,7 +806,7 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t at
   int in_smem = gb + fixed + per_warp * 8 <= c->smem_optin;
   if (in_smem) warps_a = (int)std::min<size_t>(DS_ALIGN_WARPS, (c->smem_optin - gb - fixed) / per_warp);
   const size_t smem_a = (in_smem ? gb : 0) + fixed + per_warp * warps_a;
-  AlignOut ao{(uint32_t *)c->b_keys.p + (size_t)L0 * dp.N};
+  AlignOut ao{c->sv_keys ? c->sv_keys : (uint32_t *)c->b_keys.p + (size_t)L0 * dp.N};
   cudaEventRecord(e0, c->stream);
   launch_align_batched(pk->view, bt, dp, c->io.order_a + L0, ao, queue, in_smem, c->sm_count, warps_a,
                        smem_a, c->stream);
@@ -809,14 +814,15 @@ int run_batched_range(ds_ctx *c, const ds_pocket *pk, int L0, int L1, int64_t at
   // --- torsion optimisation, then select + rescore: warp per ligand, persistent, occupancy-sized ---
   const int blocks_t = c->sm_count * std::max(1, torsion_blocks_per_sm());
   int rc;
-  if ((rc = c->ensure(c->b_rgv, sizeof(int) * (size_t)dp.N * (size_t)(L1 - L0))))
+  if (!c->sv_rgv && (rc = c->ensure(c->b_rgv, sizeof(int) * (size_t)dp.N * (size_t)(L1 - L0))))
     return rc;
   OptOut oo = {};
   oo.res = c->io.res + L0;
   oo.rrec = want_rrec ? c->io.rrec + (size_t)L0 * dp.N : nullptr;
   oo.rtors = c->io.rtors;
   oo.final_u = nullptr;
-  oo.rgv = (int *)c->b_rgv.p;
+  oo.rgv = c->sv_rgv ? c->sv_rgv : (int *)c->b_rgv.p;
+  oo.sel_order = c->sv_sel;
   oo.atom_base = atom_base;
   oo.best_coords = want_coords ? c->io.coords : nullptr;
   oo.best_tors = want_btors ? c->io.btors : nullptr;
@@ -1225,6 +1231,188 @@ int ds_batch_download(ds_ctx *c, ds_dev_batch *d, const ds_outputs *out) {
 
 void ds_batch_destroy(ds_dev_batch *d) { delete d; }
 
+// ---- engine stream (batched_engine.run) ---------------------------------------
+// The whole packed ligand stream of one engine run lives on the device: producers upload the
+// ranges they have packed, each batch the bucketizer detaches is docked as a list of stream ligand
+// numbers (the kernels take queue item -> ligand orders), outputs stay at the stream's ligand /
+// atom / fragment offsets and come back with one download — no per-batch gather, H2D, D2H or
+// scatter on the host.  Buffers grow geometrically and are kept across runs.
+}  // extern "C"
+
+struct ds_stream {
+  int device = 0;
+  int L = 0, NA = 0, NF = 0, N = 0;
+  std::vector<int> atom_off, frag_off;  // host copies: LPT keys and the batch's largest ligand
+  DevBuf atom_off_d, atoms, frag_off_d, frags, idh, keys, rgv, res, rtors, coords, btors;
+  int64_t allocs = 0;
+  int grow(DevBuf &b, size_t bytes) {
+    bytes = std::max<size_t>(bytes, 256);
+    if (bytes <= b.cap) return DS_OK;
+    size_t nc = std::max(bytes, b.cap * 3 / 2);
+    nc = (nc + 255) & ~(size_t)255;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+    cudaError_t e = cudaMalloc(&b.p, nc);
+    if (e != cudaSuccess) return fail(DS_ERR_OOM, "cudaMalloc(%zu): %s", nc, cudaGetErrorString(e));
+    b.cap = nc;
+    ++allocs;
+    return DS_OK;
+  }
+  ~ds_stream() {
+    cudaSetDevice(device);
+    for (DevBuf *b : {&atom_off_d, &atoms, &frag_off_d, &frags, &idh, &keys, &rgv, &res, &rtors, &coords, &btors})
+      if (b->p) cudaFree(b->p);
+  }
+};
+
+extern "C" {
+
+int ds_stream_create(ds_ctx *c, ds_stream **out) {
+  if (!c || !out) return fail(DS_ERR_INVALID_ARG, "NULL argument");
+  *out = new ds_stream();
+  (*out)->device = c->device;
+  return DS_OK;
+}
+
+void ds_stream_destroy(ds_stream *s) { delete s; }
+
+int ds_stream_begin(ds_stream *s, int32_t n_ligands, const int32_t *atom_off, const int32_t *frag_off,
+                    int32_t restarts) {
+  if (!s || n_ligands < 0 || (n_ligands > 0 && (!atom_off || !frag_off)) || restarts < 1 ||
+      restarts > DS_MAX_RESTARTS)
+    return fail(DS_ERR_INVALID_ARG, "bad argument");
+  const int L = n_ligands;
+  const int NA = L ? atom_off[L] : 0, NF = L ? frag_off[L] : 0;
+  if (L && (atom_off[0] != 0 || frag_off[0] != 0)) return fail(DS_ERR_INVALID_ARG, "offsets must start at 0");
+  for (int i = 0; i < L; ++i) {
+    const int A = atom_off[i + 1] - atom_off[i];
+    if (A < 1 || A > DS_MAX_ATOMS) return fail(DS_ERR_TOO_MANY_ATOMS, "ligand %d has %d atoms", i, A);
+    if (frag_off[i + 1] < frag_off[i]) return fail(DS_ERR_INVALID_ARG, "frag_off not monotone");
+  }
+  DS_CUDA(enter_device(s->device));
+  int rc;
+  if ((rc = s->grow(s->atom_off_d, 4ull * (L + 1))) || (rc = s->grow(s->atoms, 16ull * NA)) ||
+      (rc = s->grow(s->frag_off_d, 4ull * (L + 1))) || (rc = s->grow(s->frags, 32ull * NF)) ||
+      (rc = s->grow(s->idh, 8ull * L)) || (rc = s->grow(s->keys, 4ull * L * restarts)) ||
+      (rc = s->grow(s->rgv, 4ull * L * restarts)) || (rc = s->grow(s->res, sizeof(ds_result) * (size_t)L)) ||
+      (rc = s->grow(s->rtors, (size_t)NF * restarts)) || (rc = s->grow(s->coords, 12ull * NA)) ||
+      (rc = s->grow(s->btors, (size_t)NF)))
+    return rc;
+  s->L = L;
+  s->NA = NA;
+  s->NF = NF;
+  s->N = restarts;
+  s->atom_off.assign(atom_off, atom_off + L + 1);
+  s->frag_off.assign(frag_off, frag_off + L + 1);
+  if (!L) {
+    s->atom_off.assign(1, 0);
+    s->frag_off.assign(1, 0);
+  }
+  // records of ligands no batch docks (invalid ones) read back as zeros
+  DS_CUDA(cudaMemcpy(s->atom_off_d.p, s->atom_off.data(), 4ull * (L + 1), cudaMemcpyHostToDevice));
+  DS_CUDA(cudaMemcpy(s->frag_off_d.p, s->frag_off.data(), 4ull * (L + 1), cudaMemcpyHostToDevice));
+  DS_CUDA(cudaMemset(s->res.p, 0, sizeof(ds_result) * (size_t)std::max(L, 1)));
+  return DS_OK;
+}
+
+int ds_stream_upload(ds_stream *s, int32_t lo, int32_t hi, const float *atom_xyzt, const uint32_t *frag_desc,
+                     const uint64_t *id_hash) {
+  if (!s || lo < 0 || hi < lo || hi > s->L || !atom_xyzt || !id_hash || (!frag_desc && s->NF))
+    return fail(DS_ERR_INVALID_ARG, "bad argument");
+  if (lo == hi) return DS_OK;
+  DS_CUDA(enter_device(s->device));
+  // the calling thread's own stream: producers upload disjoint ranges concurrently
+  cudaStream_t st = cudaStreamPerThread;
+  const size_t a0 = s->atom_off[lo], a1 = s->atom_off[hi], f0 = s->frag_off[lo], f1 = s->frag_off[hi];
+  DS_CUDA(cudaMemcpyAsync((float4 *)s->atoms.p + a0, atom_xyzt + 4 * a0, 16 * (a1 - a0), cudaMemcpyHostToDevice, st));
+  if (f1 > f0)
+    DS_CUDA(cudaMemcpyAsync((char *)s->frags.p + 32 * f0, (const char *)frag_desc + 32 * f0, 32 * (f1 - f0),
+                            cudaMemcpyHostToDevice, st));
+  DS_CUDA(cudaMemcpyAsync((uint64_t *)s->idh.p + lo, id_hash + lo, 8ull * (hi - lo), cudaMemcpyHostToDevice, st));
+  DS_CUDA(cudaStreamSynchronize(st));
+  return DS_OK;
+}
+
+int ds_stream_dock(ds_ctx *c, const ds_pocket *pk, ds_stream *s, const int32_t *sel, int32_t n_sel,
+                   const ds_dock_config *cfg, ds_stats *st) {
+  if (!c || !pk || !s || !cfg || n_sel < 0 || (n_sel && !sel)) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  if (c->device != s->device) return fail(DS_ERR_INVALID_ARG, "stream and context on different devices");
+  DockParams dp;
+  int rc;
+  if ((rc = check_config(cfg, pk, &dp))) return rc;
+  if (dp.N != s->N) return fail(DS_ERR_INVALID_ARG, "restarts %d != the stream's %d", dp.N, s->N);
+  if (st) memset(st, 0, sizeof *st);
+  if (!n_sel) return DS_OK;
+  // LPT orders of the batch (stream ligand numbers): alignment ~ A, optimisation ~ (F + 2) * A,
+  // descending, stable counting sorts
+  int max_atoms = 0;
+  for (int k = 0; k < n_sel; ++k) {
+    const int i = sel[k];
+    if (i < 0 || i >= s->L) return fail(DS_ERR_INVALID_ARG, "ligand %d outside the stream", i);
+    max_atoms = std::max(max_atoms, s->atom_off[i + 1] - s->atom_off[i]);
+  }
+  DS_CUDA(enter_device(c->device));
+  if ((rc = c->ensure(c->b_order_a, 4ull * n_sel)) || (rc = c->ensure(c->b_order_o, 4ull * n_sel)) ||
+      (rc = c->ensure(c->b_queue, 256)) || (rc = c->ensure_host(8ull * n_sel)))
+    return rc;
+  int *oa = (int *)c->h_stage, *oo = oa + n_sel;
+  auto csort = [&](int *out, int nkeys, auto key) {
+    std::vector<int> cnt(nkeys + 1, 0);
+    for (int k = 0; k < n_sel; ++k) cnt[nkeys - 1 - key(sel[k])]++;
+    int run = 0;
+    for (int q = 0; q < nkeys; ++q) {
+      const int t = cnt[q];
+      cnt[q] = run;
+      run += t;
+    }
+    for (int k = 0; k < n_sel; ++k) out[cnt[nkeys - 1 - key(sel[k])]++] = sel[k];
+  };
+  const int *ao = s->atom_off.data(), *fo = s->frag_off.data();
+  csort(oa, DS_MAX_ATOMS + 1, [&](int i) { return ao[i + 1] - ao[i]; });
+  csort(oo, 4096, [&](int i) { return std::min(4095, ((fo[i + 1] - fo[i] + 2) * (ao[i + 1] - ao[i])) >> 3); });
+  cudaEventRecord(c->ev[0], c->stream);
+  DS_CUDA(cudaMemcpyAsync(c->b_order_a.p, oa, 4ull * n_sel, cudaMemcpyHostToDevice, c->stream));
+  DS_CUDA(cudaMemcpyAsync(c->b_order_o.p, oo, 4ull * n_sel, cudaMemcpyHostToDevice, c->stream));
+  DS_CUDA(cudaMemsetAsync(c->b_queue.p, 0, 256, c->stream));
+  c->io = {(int *)s->atom_off_d.p, (float4 *)s->atoms.p, (int *)s->frag_off_d.p, (uint4 *)s->frags.p,
+           (uint64_t *)s->idh.p,   (int *)c->b_order_a.p, (int *)c->b_order_o.p, (ds_result *)s->res.p,
+           nullptr,               (uint8_t *)s->rtors.p, (float *)s->coords.p,  (uint8_t *)s->btors.p};
+  c->x_zero_copy = false;
+  c->sv_keys = (uint32_t *)s->keys.p;
+  c->sv_rgv = (int *)s->rgv.p;
+  c->sv_sel = (const int *)c->b_order_o.p;
+  ++c->gen;  // the per-array views no longer describe a resident batch
+  rc = run_batched_range(c, pk, 0, n_sel, 0, max_atoms, dp, true, true, false, st, c->ev[1], c->ev[2], c->ev[3],
+                         (int *)c->b_queue.p);
+  c->sv_keys = nullptr;
+  c->sv_rgv = nullptr;
+  c->sv_sel = nullptr;
+  io_from_buffers(c);
+  if (rc) return rc;
+  cudaEventRecord(c->ev[4], c->stream);
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  fill_times(c, st, false, true);
+  if (st) st->h2d_bytes = 8ll * n_sel;
+  return DS_OK;
+}
+
+int ds_stream_download(ds_ctx *c, ds_stream *s, const ds_outputs *out) {
+  if (!c || !s || !out || out->restarts || out->restart_torsion) return fail(DS_ERR_INVALID_ARG, "bad argument");
+  if (c->device != s->device) return fail(DS_ERR_INVALID_ARG, "stream and context on different devices");
+  if (!s->L) return DS_OK;
+  DS_CUDA(enter_device(c->device));
+  if (out->results)
+    DS_CUDA(cudaMemcpyAsync(out->results, s->res.p, sizeof(ds_result) * (size_t)s->L, cudaMemcpyDeviceToHost,
+                            c->stream));
+  if (out->best_coords && s->NA)
+    DS_CUDA(cudaMemcpyAsync(out->best_coords, s->coords.p, 12ull * s->NA, cudaMemcpyDeviceToHost, c->stream));
+  if (out->best_torsion && s->NF)
+    DS_CUDA(cudaMemcpyAsync(out->best_torsion, s->btors.p, (size_t)s->NF, cudaMemcpyDeviceToHost, c->stream));
+  DS_CUDA(cudaStreamSynchronize(c->stream));
+  return DS_OK;
+}
+
 int ds_generate_resident(ds_ctx *c, int64_t seed, int64_t first_index, int32_t count, const int32_t *shapes,
                          ds_dev_batch **out, float *device_ms) {
   if (!c || !out || !shapes || count < 0) return fail(DS_ERR_INVALID_ARG, "bad argument");
@@ -1328,8 +1516,9 @@ int ds_query_capacity(ds_ctx *c, int range_idx, int *ligands) {
   // (synthetic-pocket grid in shared memory) and torsion kernels, ~90 % of the step; the select
   // kernel's residency is set by its per-warp pose slots (top-K x the batch's largest ligand),
   // which a batch does not know before it is filled.  A batch is `waves` such launches' worth
-  // (DS_CAPACITY_WAVES, default 2): persistent CTAs drain an LPT queue, so more than one wave
-  // amortises the tail of the slowest ligands.
+  // (DS_CAPACITY_WAVES, default 1 = the paper's one resident launch): the batched engine docks the
+  // batches already waiting in one launch, so small batches cost no extra kernel tails, and the
+  // first one fills (and the GPU starts) earliest with one wave.
   const int N = 8;
   const size_t per_warp = (size_t)align_warp_smem_bytes_host(N);
   const size_t grid_bytes = 181888, fixed = 30 * 16;
@@ -1343,7 +1532,7 @@ int ds_query_capacity(ds_ctx *c, int range_idx, int *ligands) {
   if (per_sm <= 0) return fail(DS_ERR_CUDA, "occupancy query returned 0 resident warps");
   static const int waves = [] {
     const char *e = getenv("DS_CAPACITY_WAVES");
-    const int w = e ? atoi(e) : 2;
+    const int w = e ? atoi(e) : 1;
     return w < 1 ? 1 : w;
   }();
   *ligands = c->sm_count * per_sm * waves;

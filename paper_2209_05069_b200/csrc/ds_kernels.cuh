@@ -69,6 +69,7 @@ struct OptOut {
   float *best_coords;        // atom_total*3 (may be null)
   uint8_t *best_tors;        // frag_total (may be null)
   uint8_t *rtors_host;       // latency, zero-copy outputs: the last CTA copies its ligand's rtors here
+  const int *sel_order;      // batched select: queue item -> ligand (an engine stream's batch), null = identity
 };
 
 }  // namespace ds

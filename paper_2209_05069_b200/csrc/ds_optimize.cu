@@ -730,10 +730,11 @@ __global__ void __launch_bounds__(kOptWarps * 32)
   __syncthreads();
 
   for (;;) {
-    int lig = 0;
-    if (lane == 0) lig = atomicAdd(queue, 1);
-    lig = __shfl_sync(kFull, lig, 0);
-    if (lig >= bt.L) break;
+    int item = 0;
+    if (lane == 0) item = atomicAdd(queue, 1);
+    item = __shfl_sync(kFull, item, 0);
+    if (item >= bt.L) break;
+    const int lig = out.sel_order ? out.sel_order[item] : item;
     ds_result res = out.res[lig];
     if (res.status != DS_STATUS_OK) continue;  // DegenerateAxis: already final
     const int a0 = bt.atom_off[lig];

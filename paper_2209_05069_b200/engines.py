@@ -4,13 +4,17 @@ latency_engine.run  — PAPER.md:287-348: every ligand is one synchronous dock c
                       thread owns one ds_ctx (a CUDA stream + a worst-case workspace allocated once,
                       PAPER.md:310-313) and the ligand's restarts/rotations are spread across the GPU.
 batched_engine.run  — PAPER.md:349-426: producer threads pack + validate chunks of
-                      the stream natively and push the ligands into the bucketizer (bulk push per
-                      bucket key, linearizable per bucket); every batch the bucketizer detaches when
-                      full — and, at end of stream, every flushed partial one — goes to a dispatcher
-                      thread (four per device, each with its own ds_ctx and stream, so the tail of
-                      one batch overlaps the next) that cuts it out of the packed stream and docks it
-                      with the batched kernels (one warp per ligand).  The dispatch log records when
-                      each batch was detached, started and finished.
+                      the stream natively, upload each packed chunk into the device-resident stream
+                      (ds_stream) and push its ligands into the bucketizer (bulk push per bucket
+                      key, linearizable per bucket); every batch the bucketizer detaches when full
+                      — and, at end of stream, every flushed partial one — goes to a dispatcher
+                      thread (two per device, each with its own ds_ctx and CUDA stream) that docks
+                      it as an index list over the resident stream with the batched kernels (one
+                      warp per ligand); batches already waiting when a dispatcher picks one up go
+                      into the same launch (each is still its own dispatch in the log).  The
+                      outputs stay on the device at the stream's offsets and come back with one
+                      download into pooled pinned memory.  The dispatch log records when each
+                      batch was detached, started and finished.
 
 Both accept the reference's stream of Ligand objects, or a LigandBatch (io.parse_ligand_batch, the
 generators) — the zero-object fast path — and return an EngineReport whose results are ordered by
@@ -35,7 +39,8 @@ from .bucketizer import Batch, BucketKey, Bucketizer, bucket_capacity, device_ca
 from .docking import _pockets, thread_context
 from .native import (CHEM_SCALE, DS_OK, ERRORS, FAMILY_BATCHED, FAMILY_LATENCY, FRAG_WORDS, MASK_WORDS,
                      RESULT_DTYPE, STATUS_DEGENERATE_AXIS, STATUS_NO_VALID_POSE, Context, DsError,
-                     InteractionTable, LigandBatch, PackedBatch, _p, check, lib, pack, pinned_empty)
+                     EngineStream, GeneratedIds, InteractionTable, LigandBatch, PackedBatch, _p, check, lib, pack,
+                     pinned_empty, pooled_pinned_empty)
 
 Stream = Union[LigandBatch, Iterable[model.Ligand]]
 
@@ -205,26 +210,48 @@ class latency_engine:  # noqa: N801  (module-like namespace mirroring `dockscree
 # ---- batched engine ----------------------------------------------------------------------------
 _POOL_LOCK = threading.Lock()
 _DISPATCH_POOL: Dict[Tuple[int, int], "_Dispatcher"] = {}
+_STREAM_POOL: Dict[int, List["_DeviceStream"]] = {}
 
 
 class _Dispatcher:
-    """One dispatcher slot: a ds_ctx (own CUDA stream + workspaces) on one device and pinned staging
-    for the batches it cuts out of the packed stream.  Kept across runs (allocate once
-    in the lifetime of the thread); a run holds the slot's lock while it uses it."""
+    """One dispatcher slot: a ds_ctx (own CUDA stream + workspaces) on one device.  Kept across runs
+    (allocate once in the lifetime of the thread); a run holds the slot's lock while
+    it uses it."""
 
     def __init__(self, device: int):
         self.device = device
         self.ctx = Context(device)
         self.lock = threading.Lock()
-        self.bufs: Dict[str, np.ndarray] = {}
 
-    def buf(self, name: str, shape, dtype) -> np.ndarray:
-        count = int(np.prod(shape))
-        b = self.bufs.get(name)
-        if b is None or b.size < count or b.dtype != np.dtype(dtype):
-            b = pinned_empty(max(count * 3 // 2, 1), dtype)
-            self.bufs[name] = b
-        return b[:count].reshape(shape)
+
+def _dispatcher(device: int, slot: int) -> _Dispatcher:
+    with _POOL_LOCK:
+        d = _DISPATCH_POOL.get((device, slot))
+        if d is None:
+            d = _DISPATCH_POOL[(device, slot)] = _Dispatcher(device)
+        return d
+
+
+class _DeviceStream:
+    """A device's EngineStream (the packed ligand stream of a run on the device) with the context
+    that downloads it; kept across runs (its buffers only grow), held by one run at a time."""
+
+    def __init__(self, device: int):
+        self.ctx = Context(device)
+        self.stream = EngineStream(self.ctx)
+        self.lock = threading.Lock()
+
+
+def _acquire_stream(device: int) -> _DeviceStream:
+    with _POOL_LOCK:
+        pool = _STREAM_POOL.setdefault(device, [])
+        for ds in pool:
+            if ds.lock.acquire(blocking=False):
+                return ds
+        ds = _DeviceStream(device)
+        ds.lock.acquire()
+        pool.append(ds)
+        return ds
 
 
 class _StreamArena:
@@ -248,37 +275,34 @@ class _StreamArena:
 _ARENA = _StreamArena()
 
 
-def _dispatcher(device: int, slot: int) -> _Dispatcher:
-    with _POOL_LOCK:
-        d = _DISPATCH_POOL.get((device, slot))
-        if d is None:
-            d = _DISPATCH_POOL[(device, slot)] = _Dispatcher(device)
-        return d
-
-
-def _csr_gather(sel: np.ndarray, src_off: np.ndarray, src: np.ndarray, elem: int, disp: _Dispatcher, name: str,
-                row_shape: tuple, dtype):
-    L = lib()
-    off = disp.buf(name + "_off", (len(sel) + 1,), np.int32)
-    check(L.ds_csr_gather(len(sel), _p(sel), _p(src_off), None, elem, _p(off), None))
-    total = int(off[-1])
-    dst = disp.buf(name, (max(total, 1),) + row_shape, dtype)
-    if total:
-        check(L.ds_csr_gather(len(sel), _p(sel), _p(src_off), _p(src), elem, _p(off), _p(dst)))
-    return off, dst[:total]
+def _id_chunk(batch: LigandBatch, lo: int, hi: int):
+    """Packed id bytes of ligands [lo, hi) and their offsets (relative to the chunk)."""
+    ids = batch.ids[lo:hi]
+    if isinstance(ids, GeneratedIds):
+        blob, off = ids.id_blob()
+    else:
+        enc = [x.encode() for x in ids]
+        off = np.zeros(len(enc) + 1, np.int64)
+        off[1:] = np.cumsum([len(e) for e in enc])
+        blob = b"".join(enc)
+    return C.create_string_buffer(blob, max(len(blob), 1)), np.ascontiguousarray(off, np.int64)
 
 
 class batched_engine:  # noqa: N801
     @staticmethod
     def run(stream: Stream, pocket: model.Pocket, cfg: model.DockConfig = model.DockConfig(),
-            workers: int = 1, seed: int = 0, table: Optional[InteractionTable] = None,
+            workers: int = 4, seed: int = 0, table: Optional[InteractionTable] = None,
             capacities: Union[None, str, Mapping[int, int]] = None, devices: Sequence[int] = (0,),
-            dispatchers_per_device: int = 4, chunk: int = 8192) -> EngineReport:
+            dispatchers_per_device: int = 2, chunk: int = 8192, merge_ligands: int = 1 << 16) -> EngineReport:
         """producers -> bucketizer -> dispatchers; flush at end of stream.
 
         capacities: None = SPEC.md:332's fixed per-range capacities; "device" = the occupancy-derived
         capacities of this B200 (ds_query_capacity); or a {range: capacity} map.
-        workers = producer threads (validation, packing, classification, push)."""
+        workers = producer threads (validation, packing, upload, classification, push).  The packed
+        stream lives on each device (ds_stream): a producer uploads every chunk it has packed before
+        pushing its ligands, a dispatcher docks each detached batch as an index list over it — the
+        batches already waiting when it picks one up (up to merge_ligands ligands) in the same
+        launch, each still logged as its own dispatch — and the outputs come back once at the end."""
         if workers < 1 or dispatchers_per_device < 1:
             raise ValueError("workers must be positive")
         t0 = time.perf_counter()
@@ -290,140 +314,168 @@ class batched_engine:  # noqa: N801
         if capacities == "device":
             capacities = device_capacities(slots[0].ctx)
         bucketizer = Bucketizer(capacities)
-        # the packed stream (pinned: batches are cut out of it natively) and the result arrays
         ao = np.ascontiguousarray(batch.atom_off, np.int32)
         fo = np.ascontiguousarray(batch.frag_off, np.int32)
+        dstreams = {d: _acquire_stream(d) for d in devices}
         arena = _ARENA if _ARENA.lock.acquire(blocking=False) else _StreamArena()
-        xyzt = arena.get("xyzt", (max(na, 1), 4), np.float32)
-        fdesc = arena.get("fdesc", (max(nf, 1), FRAG_WORDS), np.uint32)
-        idh = np.empty(max(n, 1), np.uint64)
-        cen = np.empty((max(n, 1), 3), np.float32)
-        res = np.zeros(max(n, 1), RESULT_DTYPE)[:n]
-        coords = np.empty((max(na, 1), 3), np.float32)     # every row is written by its batch
-        tors = np.empty(max(nf, 1), np.uint8)
-        xyz = np.ascontiguousarray(batch.atom_xyz, np.float32)
-        typ = np.ascontiguousarray(batch.atom_type, np.uint8)
-        fax = np.ascontiguousarray(batch.frag_axis, np.int32) if nf else np.zeros((1, 2), np.int32)
-        fm = np.ascontiguousarray(batch.frag_mask, np.uint32) if nf else np.zeros((1, MASK_WORDS), np.uint32)
-        ids_blob, id_off = batch.id_bytes() if n else (b"", np.zeros(1, np.int64))
-        idbuf = C.create_string_buffer(ids_blob, max(len(ids_blob), 1))
-        id_off = np.ascontiguousarray(id_off, np.int64)
-        tm["allocated"] = time.perf_counter() - t0
-        rng_key = ((np.diff(ao) - 1) // 32).astype(np.int64) * 1_000_000 + np.diff(fo).astype(np.int64) // 4
-        valid = np.ones(max(n, 1), bool)[:n]
+        try:
+            for ds in dstreams.values():
+                ds.stream.begin(ao, fo, cfg.restarts_n)
+            # the packed stream (pinned: uploaded by DMA) and the host copies of the outputs
+            xyzt = arena.get("xyzt", (max(na, 1), 4), np.float32)
+            fdesc = arena.get("fdesc", (max(nf, 1), FRAG_WORDS), np.uint32)
+            idh = arena.get("idh", (max(n, 1),), np.uint64)
+            cen = arena.get("cen", (max(n, 1), 3), np.float32)
+            xyz = np.ascontiguousarray(batch.atom_xyz, np.float32)
+            typ = np.ascontiguousarray(batch.atom_type, np.uint8)
+            fax = np.ascontiguousarray(batch.frag_axis, np.int32) if nf else np.zeros((1, 2), np.int32)
+            fm = np.ascontiguousarray(batch.frag_mask, np.uint32) if nf else np.zeros((1, MASK_WORDS), np.uint32)
+            tm["allocated"] = time.perf_counter() - t0
+            rng_key = ((np.diff(ao) - 1) // 32).astype(np.int64) * 1_000_000 + np.diff(fo).astype(np.int64) // 4
+            valid = np.ones(max(n, 1), bool)[:n]
+            dev_of_row = np.full(max(n, 1), -1, np.int16)[:n]
 
-        dq: "queue.Queue" = queue.Queue()
-        lock = threading.Lock()
-        log: List[dict] = []
-        dev_ms = [0.0]
-        fatal: list = []
-        nxt = [0]
-        L = lib()
+            dq: "queue.Queue" = queue.Queue()
+            lock = threading.Lock()
+            log: List[dict] = []
+            dev_ms = [0.0]
+            fatal: list = []
+            nxt = [0]
+            L = lib()
 
-        def pack_range(lo: int, hi: int) -> None:
-            """Validate + pack ligands [lo, hi) in place into the stream arrays; a bad ligand is
-            recorded and left out of the buckets."""
-            bad = C.c_int32(-1)
-            rc = L.ds_pack_ligands(hi - lo, _p(ao[lo:]), _p(xyz), _p(typ), _p(fo[lo:]), _p(fax), _p(fm),
-                                   C.cast(idbuf, C.c_void_p), _p(id_off[lo:]), _p(xyzt), _p(fdesc), _p(idh[lo:]),
-                                   _p(cen[lo:]), C.byref(bad))
-            if rc == DS_OK:
-                return
-            for i in range(lo, hi):   # cold path: find every bad ligand of the chunk
-                rc = L.ds_pack_ligands(1, _p(ao[i:]), _p(xyz), _p(typ), _p(fo[i:]), _p(fax), _p(fm),
-                                       C.cast(idbuf, C.c_void_p), _p(id_off[i:]), _p(xyzt), _p(fdesc), _p(idh[i:]),
-                                       _p(cen[i:]), C.byref(bad))
-                if rc != DS_OK:
-                    valid[i] = False
-                    res[i]["status"] = NOT_DOCKED
-                    exc = ERRORS.get(rc, DsError)
-                    with lock:
-                        errors.append((int(seq_of_row[i]), batch.ids[i], f"{exc.__name__}: {batch.ids[i]}: invalid"))
-
-        def producer() -> None:
-            try:
-                while not fatal:
-                    with lock:
-                        lo = nxt[0]
-                        nxt[0] += chunk
-                    if lo >= n:
-                        return
-                    hi = min(n, lo + chunk)
-                    pack_range(lo, hi)
-                    idx = np.arange(lo, hi, dtype=np.int32)
-                    keys = rng_key[lo:hi]
-                    if not valid[lo:hi].all():
-                        idx, keys = idx[valid[lo:hi]], keys[valid[lo:hi]]
-                    order = np.argsort(keys, kind="stable")
-                    uk, start = np.unique(keys[order], return_index=True)
-                    bounds = list(start) + [len(order)]
-                    for k, key in enumerate(uk.tolist()):
-                        bk = BucketKey(key // 1_000_000, key % 1_000_000)
-                        for b in bucketizer.push_many(bk, idx[order[bounds[k]:bounds[k + 1]]]):
-                            dq.put(("full", b, time.perf_counter()))
-            except BaseException as e:
-                with lock:
-                    fatal.append(e)
-
-        def dispatch(slot: _Dispatcher) -> None:
-            with slot.lock:
-                try:
-                    ctx = slot.ctx
-                    dp = _pockets.get(ctx, pocket, table)
-                    while True:
-                        item = dq.get()
-                        if item is None:
-                            return
-                        if fatal:
-                            continue
-                        kind, b, t_detached = item
-                        t_start = time.perf_counter()
-                        sel = np.ascontiguousarray(b.seqs, np.int32)
-                        s_ao, s_xyzt = _csr_gather(sel, ao, xyzt, 16, slot, "xyzt", (4,), np.float32)
-                        s_fo, s_fd = _csr_gather(sel, fo, fdesc, 32, slot, "frag", (FRAG_WORDS,), np.uint32)
-                        s_idh = slot.buf("idh", (len(sel),), np.uint64)
-                        np.take(idh, sel, out=s_idh)
-                        sub = PackedBatch(len(sel), s_ao, s_xyzt, s_fo, s_fd, s_idh, None)
-                        out = ctx.dock(dp, sub, cfg, seed, FAMILY_BATCHED, coords=True)
-                        res[sel] = out.results
-                        if int(s_ao[-1]):
-                            check(L.ds_csr_scatter(len(sel), _p(sel), _p(s_ao), _p(out.best_coords), 12, _p(ao),
-                                                   _p(coords)))
-                        if int(s_fo[-1]):
-                            check(L.ds_csr_scatter(len(sel), _p(sel), _p(s_fo), _p(out.best_torsion), 1, _p(fo),
-                                                   _p(tors)))
-                        t_end = time.perf_counter()
+            def pack_range(lo: int, hi: int) -> None:
+                """Validate + pack ligands [lo, hi) into the stream arrays; a bad ligand is recorded
+                 and left out of the buckets."""
+                bad = C.c_int32(-1)
+                idbuf, id_off = _id_chunk(batch, lo, hi)
+                pid = C.cast(idbuf, C.c_void_p)
+                rc = L.ds_pack_ligands(hi - lo, _p(ao[lo:]), _p(xyz), _p(typ), _p(fo[lo:]), _p(fax), _p(fm), pid,
+                                       _p(id_off), _p(xyzt), _p(fdesc), _p(idh[lo:]), _p(cen[lo:]), C.byref(bad))
+                if rc == DS_OK:
+                    return
+                for i in range(lo, hi):   # cold path: find every bad ligand of the chunk
+                    rc = L.ds_pack_ligands(1, _p(ao[i:]), _p(xyz), _p(typ), _p(fo[i:]), _p(fax), _p(fm), pid,
+                                           _p(id_off[i - lo:]), _p(xyzt), _p(fdesc), _p(idh[i:]), _p(cen[i:]),
+                                           C.byref(bad))
+                    if rc != DS_OK:
+                        valid[i] = False
+                        exc = ERRORS.get(rc, DsError)
                         with lock:
-                            dev_ms[0] += out.stats.total_ms
-                            log.append({"key": (b.key.atom_range_index, b.key.fragment_group_index), "kind": kind,
-                                        "size": len(sel), "capacity": b.capacity, "detached": t_detached - t0,
-                                        "started": t_start - t0, "finished": t_end - t0, "device": slot.device,
-                                        "device_ms": out.stats.total_ms})
-                except BaseException as e:  # configuration / device errors end the run (re-raised below)
+                            errors.append((int(seq_of_row[i]), batch.ids[i], f"{exc.__name__}: {batch.ids[i]}: invalid"))
+
+            def producer() -> None:
+                try:
+                    while not fatal:
+                        with lock:
+                            lo = nxt[0]
+                            nxt[0] += chunk
+                        if lo >= n:
+                            return
+                        hi = min(n, lo + chunk)
+                        pack_range(lo, hi)
+                        for ds in dstreams.values():   # on the device before any of its ligands is pushed
+                            ds.stream.upload(lo, hi, xyzt, fdesc, idh)
+                        idx = np.arange(lo, hi, dtype=np.int32)
+                        keys = rng_key[lo:hi]
+                        if not valid[lo:hi].all():
+                            idx, keys = idx[valid[lo:hi]], keys[valid[lo:hi]]
+                        order = np.argsort(keys, kind="stable")
+                        uk, start = np.unique(keys[order], return_index=True)
+                        bounds = list(start) + [len(order)]
+                        for k, key in enumerate(uk.tolist()):
+                            bk = BucketKey(key // 1_000_000, key % 1_000_000)
+                            for b in bucketizer.push_many(bk, idx[order[bounds[k]:bounds[k + 1]]]):
+                                dq.put(("full", b, time.perf_counter()))
+                except BaseException as e:
                     with lock:
                         fatal.append(e)
 
-        disp = [threading.Thread(target=dispatch, args=(s,)) for s in slots]
-        for t in disp:
-            t.start()
-        prod = [threading.Thread(target=producer) for _ in range(workers)]
-        for t in prod:
-            t.start()
-        for t in prod:
-            t.join()
-        t_flush = time.perf_counter()
-        tm["produced"] = t_flush - t0
-        for b in bucketizer.flush():           # end of stream: partial batches (SPEC.md:352)
-            dq.put(("flush", b, t_flush))
-        for _ in disp:
-            dq.put(None)
-        for t in disp:
-            t.join()
-        if arena is _ARENA:
-            _ARENA.lock.release()
-        tm["docked"] = time.perf_counter() - t0
-        if fatal:
-            raise fatal[0]
+            def dispatch(slot: _Dispatcher) -> None:
+                with slot.lock:
+                    try:
+                        ctx = slot.ctx
+                        dp = _pockets.get(ctx, pocket, table)
+                        es = dstreams[slot.device].stream
+                        done = False
+                        while not done:
+                            item = dq.get()
+                            if item is None:
+                                return
+                            items, size = [item], len(item[1].seqs)
+                            while size < merge_ligands:     # batches already waiting: same launch
+                                try:
+                                    more = dq.get_nowait()
+                                except queue.Empty:
+                                    break
+                                if more is None:
+                                    done = True
+                                    break
+                                items.append(more)
+                                size += len(more[1].seqs)
+                            if fatal:
+                                continue
+                            t_start = time.perf_counter()
+                            sel = np.concatenate([np.asarray(it[1].seqs, np.int32) for it in items])
+                            st = es.dock(ctx, dp, sel, cfg, seed)
+                            dev_of_row[sel] = slot.device
+                            t_end = time.perf_counter()
+                            with lock:
+                                dev_ms[0] += st.total_ms
+                                for kind, b, t_detached in items:
+                                    log.append({"key": (b.key.atom_range_index, b.key.fragment_group_index),
+                                                "kind": kind, "size": len(b.seqs), "capacity": b.capacity,
+                                                "detached": t_detached - t0, "started": t_start - t0,
+                                                "finished": t_end - t0, "device": slot.device,
+                                                "device_ms": st.total_ms, "launch_ligands": len(sel)})
+                    except BaseException as e:  # configuration / device errors end the run (re-raised below)
+                        with lock:
+                            fatal.append(e)
+
+            disp = [threading.Thread(target=dispatch, args=(s,)) for s in slots]
+            for t in disp:
+                t.start()
+            prod = [threading.Thread(target=producer) for _ in range(workers)]
+            for t in prod:
+                t.start()
+            for t in prod:
+                t.join()
+            t_flush = time.perf_counter()
+            tm["produced"] = t_flush - t0
+            for b in bucketizer.flush():           # end of stream: partial batches (SPEC.md:352)
+                dq.put(("flush", b, t_flush))
+            for _ in disp:
+                dq.put(None)
+            for t in disp:
+                t.join()
+            tm["docked"] = time.perf_counter() - t0
+            if fatal:
+                raise fatal[0]
+            # page-locked (DMA at full PCIe speed, no page faults), reused once a report is dropped
+            res = pooled_pinned_empty(max(n, 1), RESULT_DTYPE)
+            coords = pooled_pinned_empty((max(na, 1), 3), np.float32)
+            tors = pooled_pinned_empty(max(nf, 1), np.uint8)
+            for d, ds in dstreams.items():
+                if len(dstreams) == 1:
+                    ds.stream.download(ds.ctx, res, coords, tors)
+                    continue
+                r1, c1, t1 = np.empty_like(res), np.empty_like(coords), np.empty_like(tors)
+                ds.stream.download(ds.ctx, r1, c1, t1)
+                rows = np.nonzero(dev_of_row == d)[0]
+                res[rows] = r1[rows]
+                for r in rows:
+                    a0, a1, f0, f1 = ao[r], ao[r + 1], fo[r], fo[r + 1]
+                    coords[a0:a1] = c1[a0:a1]
+                    tors[f0:f1] = t1[f0:f1]
+            res = res[:n]
+            if not valid.all():
+                res[~valid] = np.zeros(1, RESULT_DTYPE)
+                res["status"][~valid] = NOT_DOCKED
+            tm["downloaded"] = time.perf_counter() - t0
+        finally:
+            if arena is _ARENA:
+                _ARENA.lock.release()
+            for ds in dstreams.values():
+                ds.lock.release()
         log.sort(key=lambda e: e["started"])
         rep = _finish_arrays(n_in, seq_of_row, batch.ids, res, coords, ao, tors, fo, errors, bucketizer.counters, t0,
                              dev_ms[0])

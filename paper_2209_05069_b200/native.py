@@ -139,6 +139,11 @@ def lib():
             "ds_op_apply_torsion": (C.c_int, [vp, vp, i32, i32, i32, i32, vp, i32, vp, vp]),
             "ds_op_bump_check": (C.c_int, [vp, vp, i32, i32, i32, i32, vp, C.c_float, i32, vp, vp]),
             "ds_csr_scatter": (C.c_int, [i32, vp, vp, vp, i32, vp, vp]),
+            "ds_stream_create": (C.c_int, [vp, vp]), "ds_stream_destroy": (None, [vp]),
+            "ds_stream_begin": (C.c_int, [vp, i32, vp, vp, i32]),
+            "ds_stream_upload": (C.c_int, [vp, i32, i32, vp, vp, vp]),
+            "ds_stream_dock": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
+            "ds_stream_download": (C.c_int, [vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -161,6 +166,54 @@ def pinned_empty(shape, dtype) -> np.ndarray:
     buf = (C.c_char * nbytes).from_address(ptr)
     weakref.finalize(buf, lib().ds_host_free, ptr)
     return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
+
+
+class _PinnedPool:
+    """Reusable page-locked blocks for per-call outputs (the batched engine's result arrays): an
+    array from take() returns its block to the pool when the last view of it is gone, so a run
+    whose previous report has been dropped reuses that report's pinned memory instead of page-
+    locking (or page-faulting) hundreds of MB again.  At most keep_bytes stay pooled."""
+
+    def __init__(self, keep_bytes: int = 2 << 30):
+        self.keep = keep_bytes
+        self.free: list = []      # (capacity, ptr), most recently returned last
+        self.lock = threading.Lock()
+
+    def take(self, shape, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        count = int(np.prod(shape))
+        nbytes = max(count * dtype.itemsize, 1)
+        ptr = cap = None
+        with self.lock:
+            fits = [k for k, (c, _) in enumerate(self.free) if nbytes <= c <= 2 * nbytes + (1 << 20)]
+            if fits:
+                k = min(fits, key=lambda k: self.free[k][0])
+                cap, ptr = self.free.pop(k)
+        if ptr is None:
+            cap = nbytes + nbytes // 4
+            ptr = lib().ds_host_alloc(cap)
+            if not ptr:
+                raise MemoryError(f"ds_host_alloc({cap}) failed")
+        buf = (C.c_char * nbytes).from_address(ptr)
+        weakref.finalize(buf, self._give_back, cap, ptr)
+        return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
+
+    def _give_back(self, cap: int, ptr: int):
+        with self.lock:
+            self.free.append((cap, ptr))
+            drop = []
+            while sum(c for c, _ in self.free) > self.keep:
+                drop.append(self.free.pop(0))
+        for _, p in drop:
+            lib().ds_host_free(p)
+
+
+_OUT_POOL = _PinnedPool()
+
+
+def pooled_pinned_empty(shape, dtype) -> np.ndarray:
+    """pinned_empty from the reusable output pool (see _PinnedPool)."""
+    return _OUT_POOL.take(shape, dtype)
 
 
 def pinned_copy(a: np.ndarray) -> np.ndarray:
@@ -629,6 +682,52 @@ class Context:
 
     def __exit__(self, *a):
         self.close()
+
+
+class EngineStream:
+    """ds_stream: the packed ligand stream of a batched-engine run kept on one device.
+    begin() sizes it, producers upload() the ranges they packed, dispatchers dock() index lists of
+    stream ligands on their own contexts, download() returns every ligand's outputs."""
+
+    def __init__(self, ctx: Context):
+        h = C.c_void_p()
+        check(lib().ds_stream_create(ctx.handle, C.byref(h)))
+        self.handle, self.device = h, ctx.device
+        self._atom_off = self._frag_off = None
+
+    def begin(self, atom_off: np.ndarray, frag_off: np.ndarray, restarts: int):
+        self._atom_off = np.ascontiguousarray(atom_off, np.int32)
+        self._frag_off = np.ascontiguousarray(frag_off, np.int32)
+        check(lib().ds_stream_begin(self.handle, len(self._atom_off) - 1, _p(self._atom_off), _p(self._frag_off),
+                                    int(restarts)))
+
+    def upload(self, lo: int, hi: int, xyzt: np.ndarray, fdesc: np.ndarray, idh: np.ndarray):
+        check(lib().ds_stream_upload(self.handle, int(lo), int(hi), _p(xyzt), _p(fdesc), _p(idh)))
+
+    def dock(self, ctx: Context, dpocket: "DevicePocket", sel: np.ndarray, cfg: model.DockConfig,
+             seed: int = 0) -> Stats:
+        sel = np.ascontiguousarray(sel, np.int32)
+        st = Stats()
+        ccfg = config_c(cfg, seed)
+        check(lib().ds_stream_dock(ctx.handle, dpocket.handle, self.handle, _p(sel), len(sel), C.byref(ccfg),
+                                   C.byref(st)))
+        return st
+
+    def download(self, ctx: Context, results: np.ndarray, best_coords: Optional[np.ndarray],
+                 best_torsion: Optional[np.ndarray]):
+        out = Outputs(_p(results), _p(best_coords), _p(best_torsion), None, None)
+        check(lib().ds_stream_download(ctx.handle, self.handle, C.byref(out)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().ds_stream_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class ResidentBatch:

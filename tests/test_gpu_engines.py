@@ -158,3 +158,56 @@ def test_engine_fatal_config_error_raises(synth_pocket, table):
     for run in (engines.batched_engine.run, engines.latency_engine.run):
         with pytest.raises(DsError):
             run(ligs, synth_pocket, cfg, workers=2, table=table)
+
+
+def test_engine_stream_index_lists_equal_ds_dock(synth_pocket, table):
+    """ds_stream (the batched engine's device-resident stream): the ligands docked as shuffled index
+    lists on two contexts, uploaded in ranges, give ds_dock's records, poses and torsions; ligands no
+    list names read back as zero records; a config with other restarts is refused."""
+    from paper_2209_05069_b200.native import Context, EngineStream, RESULT_DTYPE, pack, pinned_copy
+    b = io.generate_mixed_batch(3000, seed=23)
+    cfg = model.DockConfig()
+    p = pack(b)
+    ctx0, ctx1 = Context(0), Context(0)
+    ref = ctx0.dock(ctx0.pocket(synth_pocket, table), p, cfg, seed=4)
+    es = EngineStream(ctx0)
+    es.begin(p.atom_off, p.frag_off, cfg.restarts_n)
+    xyzt, fdesc, idh = pinned_copy(p.atom_xyzt), pinned_copy(p.frag_desc), pinned_copy(p.id_hash)
+    for lo in range(0, b.n, 700):
+        es.upload(lo, min(b.n, lo + 700), xyzt, fdesc, idh)
+    perm = np.random.default_rng(0).permutation(b.n - 10).astype(np.int32)   # the last 10: never docked
+    es.dock(ctx0, ctx0.pocket(synth_pocket, table), perm[:1234], cfg, seed=4)
+    es.dock(ctx1, ctx1.pocket(synth_pocket, table), perm[1234:], cfg, seed=4)
+    res = np.empty(b.n, RESULT_DTYPE)
+    co = np.empty((int(p.atom_off[-1]), 3), np.float32)
+    to = np.empty(int(p.frag_off[-1]), np.uint8)
+    es.download(ctx0, res, co, to)
+    n = b.n - 10
+    assert np.array_equal(res[:n], ref.results[:n])
+    a_n, f_n = int(p.atom_off[n]), int(p.frag_off[n])
+    assert np.array_equal(co[:a_n], ref.best_coords[:a_n]) and np.array_equal(to[:f_n], ref.best_torsion[:f_n])
+    assert not res[n:].view(np.uint8).any()
+    with pytest.raises(ValueError):   # DS_ERR_INVALID_ARG
+        es.dock(ctx0, ctx0.pocket(synth_pocket, table), perm[:5], model.DockConfig(restarts_n=4), seed=4)
+    es.close()
+
+
+def test_batched_engine_concurrent_runs(synth_pocket, table):
+    """Two batched_engine.run calls at once (each takes its own device stream and arena from the
+    pools) give the same results as one at a time."""
+    import threading
+    b1, b2 = io.generate_mixed_batch(2500, seed=24), io.generate_mixed_batch(1800, seed=25)
+    cfg = model.DockConfig()
+    solo = [engines.batched_engine.run(b, synth_pocket, cfg, table=table).records["results"] for b in (b1, b2)]
+    out = [None, None]
+
+    def go(k, b):
+        out[k] = engines.batched_engine.run(b, synth_pocket, cfg, table=table, capacities={0: 200, 1: 150, 2: 100,
+                                                                                          3: 50, 4: 20})
+    ts = [threading.Thread(target=go, args=(k, b)) for k, b in enumerate((b1, b2))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for k in range(2):
+        assert np.array_equal(out[k].records["results"], solo[k])
