@@ -147,10 +147,13 @@ def ncu_calibration(sha: str):
             docs.append((path, doc))
     if not docs:
         return {}
-    match = [d for d in docs if d[1].get("lib_sha16") == sha]
+    from paper_2209_05069_b200.native import source_sha16
+    src = source_sha16()
+    match = [d for d in docs if d[1].get("src_sha16") == src or d[1].get("lib_sha16") == sha]
     path, doc = (match or docs)[-1]
     nlig = doc["ligands"]
-    out = {"source": os.path.relpath(path, ROOT), "matches_build": bool(match), "lib_sha16": doc.get("lib_sha16")}
+    out = {"source": os.path.relpath(path, ROOT), "matches_build": bool(match), "lib_sha16": doc.get("lib_sha16"),
+           "src_sha16": src, "profiled_src_sha16": doc.get("src_sha16")}
     for k in doc.get("kernels", []):
         name = k["kernel"].split("(")[0].split("<")[0].replace("void ", "").strip().split("::")[-1]
         out[name] = {"inst_per_ligand": k.get("warp_inst_executed", 0) / nlig,

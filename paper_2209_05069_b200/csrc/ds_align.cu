@@ -16,7 +16,12 @@
 // biased 16-bit sums (9 SASS instructions per (atom, ay), 13.3 before f32x2).  The binding unit is
 // the FMA-heavy pipe (FFMA2, FADD2 and IMAD all issue there; ncu: 82 % of its peak, shared-memory
 // wavefronts 82 %), not issue.  Every lane is busy whatever the atom count (the paper's
-// lanes-over-atoms mapping idles lanes when A % 32 != 0).  Output: one packed
+// lanes-over-atoms mapping idles lanes when A % 32 != 0).  A round of the warp is
+// one restart (lane = ax), so whether an atom's every pose of that restart stays within one node
+// of the grid (|d| against the restart's translation, a bound with half a node of margin) is
+// warp-uniform; such atoms (~70 % of the config-3 work) skip the two clamps and take both magic
+// offsets out of the per-angle index: 262 instead of 322 SASS instructions per atom (-3.5 % align
+// time measured: the shared-memory wavefronts of the random grid gathers bind next).  Output: one packed
 // argmax key per (ligand, restart): (score + 32768) << 16 | (65535 - (ix * n_a + iy)).
 #include <string.h>
 
@@ -39,13 +44,18 @@ __constant__ float4 c_trig_ay[360];  // (cos, sin, -sin, 0) of iy * step_a
 // the same angles as packed pairs for the f32x2 path: [k/2] = {(c_k, c_k+1), (s_k, s_k+1), (-s_k, -s_k+1)}
 __constant__ unsigned long long c_pair_ay[180][3];
 
+#ifndef DS_ALIGN_INSIDE
+#define DS_ALIGN_INSIDE 1  // unclamped node indices for atoms whose poses all stay in the grid
+#endif
 #ifndef DS_ALIGN_F32X2
 #define DS_ALIGN_F32X2 2   // 0 scalar, 1 all packed, 2 packed x + scalar z (fastest), 3 packed FMAs + scalar rounding adds
 #endif
 
 // dynamic smem layout: [grid bytes (16-aligned)] [trig_a float4[n_a]] [per warp: stage float4[32],
-// params float[N*12], keys u32[N]]
-__host__ __device__ inline int align_warp_smem_bytes(int N) { return 32 * 16 + ((N * 12 * 4 + N * 4 + 15) & ~15); }
+// params float[N*kPrm], keys u32[N]]
+// params per restart: R0s (9), t (3), the unclamped-path radius limit (1)
+constexpr int kPrm = 13;
+__host__ __device__ inline int align_warp_smem_bytes(int N) { return 32 * 16 + ((N * kPrm * 4 + N * 4 + 15) & ~15); }
 
 __device__ __forceinline__ unsigned grid_u8(const uint8_t *grid, int idx, bool smem) {
   return smem ? (unsigned)grid[idx] : (unsigned)__ldg(grid + idx);
@@ -94,6 +104,35 @@ __device__ __forceinline__ void unit_atom_x2(const float3 v, f2_t TX, f2_t TZ, u
     const unsigned cz1 = min((unsigned)__float_as_int(mz1) - K, (unsigned)(g.nz + 1));
     const int i0 = (int)((cx0 + g.NXY * cz0) + yk);
     const int i1 = (int)((cx1 + g.NXY * cz1) + yk);
+    acc[k >> 1] += grid_u8(grid, i0, kSmemGrid) + (grid_u8(grid, i1, kSmemGrid) << 16);
+  }
+}
+
+// The same scores for an atom whose every alignment pose stays within one node of the grid (the
+// caller's radius test): no clamp can bind, so the node index is bits(mx) + NXY bits(mz) + ykf with
+// both magic offsets folded into the per-atom ykf — one IADD + one IMAD per angle instead of two
+// unsigned clamps + IMAD + IADD; identical indices (the clamps are identities here).
+template <int G, bool kSmemGrid>
+__device__ __forceinline__ void unit_atom_x2_inside(const float3 v, f2_t TX, f2_t TZ, unsigned ykf, const GridGeom &g,
+                                                    const uint8_t *grid, unsigned *acc) {
+  const f2_t VX = f2_pack(v.x, v.x), VZ = f2_pack(v.z, v.z);
+  const f2_t MM = f2_pack(kMagic, kMagic);
+#pragma unroll
+  for (int k = 0; k < G; k += 2) {
+    const f2_t C = c_pair_ay[k >> 1][0], S = c_pair_ay[k >> 1][1];
+    float mx0, mx1;
+    f2_unpack(f2_add(f2_fma(S, VZ, f2_fma(C, VX, TX)), MM), mx0, mx1);
+    float c0, c1, s0, s1;
+    f2_unpack(C, c0, c1);
+    f2_unpack(S, s0, s1);
+    float vx, vz, tz, tz1;
+    f2_unpack(VX, vx, tz1);
+    f2_unpack(VZ, vz, tz1);
+    f2_unpack(TZ, tz, tz1);
+    const float mz0 = __fadd_rn(__fmaf_rn(c0, vz, __fmaf_rn(-s0, vx, tz)), kMagic);
+    const float mz1 = __fadd_rn(__fmaf_rn(c1, vz, __fmaf_rn(-s1, vx, tz)), kMagic);
+    const int i0 = (int)(g.NXY * (unsigned)__float_as_int(mz0) + ((unsigned)__float_as_int(mx0) + ykf));
+    const int i1 = (int)(g.NXY * (unsigned)__float_as_int(mz1) + ((unsigned)__float_as_int(mx1) + ykf));
     acc[k >> 1] += grid_u8(grid, i0, kSmemGrid) + (grid_u8(grid, i1, kSmemGrid) << 16);
   }
 }
@@ -153,7 +192,7 @@ __global__ void __launch_bounds__(DS_ALIGN_WARPS * 32, 1)
   unsigned char *wbase = smem + gbytes + n_a * 16 + warp * align_warp_smem_bytes(dp.N);
   float4 *stage = reinterpret_cast<float4 *>(wbase);
   float *prm = reinterpret_cast<float *>(wbase + 32 * 16);
-  unsigned *keys = reinterpret_cast<unsigned *>(prm + dp.N * 12);
+  unsigned *keys = reinterpret_cast<unsigned *>(prm + dp.N * kPrm);
   __syncthreads();
 
   const GridGeom g = pk.g;
@@ -170,22 +209,42 @@ __global__ void __launch_bounds__(DS_ALIGN_WARPS * 32, 1)
     const int A = bt.atom_off[lig + 1] - a0;
     const uint64_t idh = bt.idh[lig];
     for (int r = lane; r < dp.N; r += 32) {
-      start_params(idh, dp.seed, r, pk.trig, pk.inv_s, g.nx, g.ny, g.nz, prm + r * 12, prm + r * 12 + 9);
+      float *P = prm + r * kPrm;
+      start_params(idh, dp.seed, r, pk.trig, pk.inv_s, g.nx, g.ny, g.nz, P, P + 9);
+      // unclamped path (kConst): an atom with |d|^2 < P[12] has every pose of this restart within
+      // one node of the grid in x and z — |u - t| <= |v| (1 + 1e-5) + 1e-5 and |v| <= |d| inv_s
+      // (1 + 1e-5), so |d| inv_s <= rs = min(t + 1, n - t) with the 0.9996 factor keeps u in
+      // [-1.5, n + 0.5], i.e. rint(u) + 1 in [0, n + 1] (the halo planes included)
+      const float rs = fminf(fminf(__fadd_rn(P[9], 1.f), __fsub_rn((float)g.nx, P[9])),
+                             fminf(__fadd_rn(P[11], 1.f), __fsub_rn((float)g.nz, P[11])));
+      const float ra = __fmul_rn(rs, pk.spacing);  // spacing * inv_s = 1 within 2^-23
+      P[12] = __fmul_rn(__fmul_rn(ra, ra), 0.9996f);
       keys[r] = 0u;
     }
     const int nchunk = (A + 31) >> 5;
-    if (nchunk == 1) stage[lane] = lane < A ? __ldg(bt.atoms + a0 + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+    // staged atoms carry |d|^2 in .w (the alignment does not read the type)
+    auto stage_atom = [&](int ai) {
+      if (ai >= A) return make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 d = __ldg(bt.atoms + a0 + ai);
+      return make_float4(d.x, d.y, d.z, __fmaf_rn(d.z, d.z, __fmaf_rn(d.y, d.y, __fmul_rn(d.x, d.x))));
+    };
+    if (nchunk == 1) stage[lane] = stage_atom(lane);
     __syncwarp();
 
-    for (int base = 0; base < total; base += 32) {
-      const bool uvalid = base + lane < total;
-      const int unit = min(base + lane, total - 1);
+    // kConst: one restart per round (units padded to 32 per restart, unit = 32 r + ax), so the
+    // restart's parameters and the unclamped-path test are warp-uniform; else 32 (chunk, restart,
+    // ax) units per round.  (The opaque XOR hides that r is warp-uniform: uniform r moves the
+    // restart's values into uniform registers and evicts the ay constants from them.)
+    const int total_u = kConst ? dp.N * 32 : total;
+    for (int base = 0; base < total_u; base += 32) {
+      const int unit = kConst ? base + (lane ^ (int)dp.opaque0) : min(base + lane, total - 1);
+      const bool uvalid = kConst ? (unit & 31) < n_a : base + lane < total;
       const int h = kConst ? 0 : unit / per_h;
       const int q = unit - h * per_h;
-      const int r = q / n_a;
-      const int ix = q - r * n_a;
+      const int r = kConst ? unit >> 5 : q / n_a;
+      const int ix = kConst ? min(unit & 31, n_a - 1) : q - r * n_a;
       const int iy0 = h * G;
-      const float *P = prm + r * 12;
+      const float *P = prm + r * kPrm;
       float Rp[9], t[3];
       {
         float R0s[9];
@@ -197,14 +256,14 @@ __global__ void __launch_bounds__(DS_ALIGN_WARPS * 32, 1)
         t[1] = P[10];
         t[2] = P[11];
       }
+      const float lim = P[12];  // the unclamped path's |d|^2 limit of this round's restart
       unsigned acc[G / 2];
 #pragma unroll
       for (int k = 0; k < G / 2; ++k) acc[k] = 0u;
       for (int c = 0; c < nchunk; ++c) {
         if (nchunk > 1) {
           __syncwarp();
-          const int ai = c * 32 + lane;
-          stage[lane] = ai < A ? __ldg(bt.atoms + a0 + ai) : make_float4(0.f, 0.f, 0.f, 0.f);
+          stage[lane] = stage_atom(c * 32 + lane);
           __syncwarp();
         }
         const int n = min(32, A - c * 32);
@@ -213,6 +272,16 @@ __global__ void __launch_bounds__(DS_ALIGN_WARPS * 32, 1)
           const float3 v = align_v(Rp, d.x, d.y, d.z);
           // u_y is shared by all ay; the opaque XOR keeps the row offset an ALU add per angle
           const unsigned yk = (g.NX * clamp_bits(__fadd_rn(v.y, t[1]), g.ny + 1)) ^ dp.opaque0;
+#if DS_ALIGN_F32X2 == 2 && DS_ALIGN_INSIDE
+          if (kConst && d.w < lim) {  // the restart keeps every pose of the atom inside (warp-uniform)
+            const unsigned K = (unsigned)(kMagicBits - 1);
+            // opaque: no constant folded out of ykf into the shared-memory address (it would need the
+            // window base in a vector register and an extra add per load)
+            unit_atom_x2_inside<G, kSmemGrid>(v, f2_pack(t[0], t[0]), f2_pack(t[2], t[2]),
+                                              (yk - K - g.NXY * K) ^ dp.opaque0, g, grid, acc);
+            continue;
+          }
+#endif
           unit_atom<G, kConst, kSmemGrid>(v, t, yk, g, grid, strig, iy0, n_a, acc);
         }
       }

@@ -23,6 +23,21 @@ from . import model
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DOCKSCREEN_LIB") or os.path.join(_HERE, "libdockscreen.so")  # override: A/B builds
 
+
+def source_sha16() -> str:
+    """sha256[:16] over the native sources and build recipe of libdockscreen.so (csrc/*, the C-ABI
+    header): the identity of the kernels a build contains.  nvcc's output is not byte-reproducible
+    (host object paths / temporaries), so profiles are tied to builds by this, not the .so bytes."""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(_HERE, "csrc")
+    files = sorted(f for f in os.listdir(csrc) if f.endswith((".cu", ".cuh", ".cpp", ".h")) or f == "Makefile")
+    for f in files + [os.path.join("..", "..", "include", "dockscreen.h")]:
+        h.update(f.encode())
+        with open(os.path.join(csrc, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
 DS_OK = 0
 ERRORS = {
     -1: ValueError, -2: model.TooManyAtoms, -3: model.MalformedFragment, -4: model.IndexOutOfRange,

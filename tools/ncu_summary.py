@@ -5,6 +5,7 @@ CSV.
     python tools/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01/ncu_kernels [launches.csv]
 """
 import csv
+import os
 import io
 import json
 import subprocess
@@ -103,6 +104,9 @@ def main():
     a = ap.parse_args()
     rep, out = a.report, a.out
     doc = {"report": rep, "kernels": raw(rep), "ligands": a.ligands, "workload": a.workload}
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2209_05069_b200.native import source_sha16
+    doc["src_sha16"] = source_sha16()   # the tree this summary is made from = the profiled build's
     if a.lib:
         import hashlib
         with open(a.lib, "rb") as fh:
