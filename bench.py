@@ -267,7 +267,9 @@ def roofline_block(cal, kms, n, ms_step, peak_winst, work, peaks):
                          "model_frac": (work[k] / (t / 1e3)) / peak_winst if t > 0 else None,
                          "ncu_inst_per_ligand": inst, "dram_bytes_per_ligand": kc.get("dram_bytes_per_ligand"),
                          "l2_hit_pct": kc.get("l2_hit_pct"), "ncu_issue_active_pct": kc.get("issue_active_pct"),
-                         "active_threads_per_inst": kc.get("active_threads_per_inst")}
+                         "active_threads_per_inst": kc.get("active_threads_per_inst"),
+                         "ncu_smem_wavefront_pct": kc.get("smem_wavefront_pct"),
+                         "ncu_fmaheavy_pipe_pct": kc.get("pipe_fmaheavy_pct")}
     dom = max(kms, key=kms.get)
     d = per_kernel[dom]
     kc = cal.get(dom, {})
@@ -276,7 +278,14 @@ def roofline_block(cal, kms, n, ms_step, peak_winst, work, peaks):
             "unit": "Gwarp-inst/s", "frac": d["executed_issue_frac"],
             "traffic": kc["dram_bytes_per_ligand"] * n if "dram_bytes_per_ligand" in kc else None,
             "l2_hit_pct": kc.get("l2_hit_pct"), "model_frac": d["model_frac"],
-            "calibration": {k: cal.get(k) for k in ("source", "matches_build", "lib_sha16")},
+            "calibration": {k: cal.get(k) for k in ("source", "matches_build", "lib_sha16", "src_sha16",
+                                                    "profiled_src_sha16")},
+            # the unit that binds the kernel in the capture (ncu % of its peak): for the alignment it
+            # is the shared-memory wavefronts of the random grid gathers, not instruction issue
+            "binding_unit": max(((u, kc.get(m)) for u, m in (("instruction issue", "issue_active_pct"),
+                                                             ("shared-memory wavefronts", "smem_wavefront_pct"),
+                                                             ("FMA-heavy pipe", "pipe_fmaheavy_pct"))
+                                 if kc.get(m) is not None), key=lambda x: x[1], default=(None, None)),
             "note": "achieved = ncu-counted warp-instructions per ligand of this kernel (committed capture of this "
                     "library build, 20k ligands of the same generator) x ligands / live CUDA-event kernel time; peak = "
                     "SMs x 4 issue/clk x sm_max_mhz (MEASURED_PEAKS.json); traffic = ncu dram__bytes read+write per "

@@ -105,15 +105,17 @@ def _finish_arrays(n_in: int, seq_of_row: np.ndarray, ids, res, coords, atom_off
                    errors: list, counters: model.Counters, t0: float, dev_ms: float) -> EngineReport:
     """Report from the per-row result arrays (row = valid ligand, seq_of_row = its input sequence);
     rows with status NOT_DOCKED did no work and are already in `errors`."""
-    st = res["status"]
+    st = np.ascontiguousarray(res["status"])
     docked = st != NOT_DOCKED
-    counters.poses_scored += int(res["poses_scored"][docked].astype(np.int64).sum())
-    counters.bump_checks += int(res["bump_checks"][docked].astype(np.int64).sum())
-    counters.bump_early_exits += int(res["bump_early_exits"][docked].astype(np.int64).sum())
-    for i in np.nonzero(docked & (st != 0))[0]:
+    every = bool(docked.all())
+    for name in ("poses_scored", "bump_checks", "bump_early_exits"):
+        col = res[name]
+        setattr(counters, name, getattr(counters, name) + int((col if every else col[docked]).sum(dtype=np.int64)))
+    bad = np.nonzero(st != 0)[0]
+    for i in bad[docked[bad]]:
         errors.append((int(seq_of_row[i]), ids[int(i)], _status_error(int(st[i]))))
     errors.sort()
-    rows = np.nonzero(st == 0)[0]
+    rows = np.nonzero(st == 0)[0] if len(bad) else np.arange(len(st), dtype=np.int64)
     table = ResultTable(ids, seq_of_row[rows], rows, res, coords, atom_off, tors, frag_off)
     rep = EngineReport(table, time.perf_counter() - t0, counters, errors, dev_ms)
     rep.records = {"results": res, "best_coords": coords, "best_torsion": tors, "atom_off": atom_off,
