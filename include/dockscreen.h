@@ -339,6 +339,10 @@ int ds_csr_gather(int32_t n_sel, const int32_t *sel, const int32_t *src_off, con
 int ds_csr_scatter(int32_t n_sel, const int32_t *sel, const int32_t *src_off, const void *src, int32_t elem_bytes,
                    const int32_t *dst_off, void *dst);
 /* Seeded symmetric 16x16 interaction table in [-1, 1]. */
+/* Threads of the host-side parallel loops (packing, validation, generation) run by the CALLING
+ * thread from now on; concurrent producer threads split the host cores instead of each spawning a
+ * team of all of them. */
+int ds_set_host_threads(int32_t n);
 int ds_default_table(int64_t seed, float *table /* 256 */);
 
 #ifdef __cplusplus

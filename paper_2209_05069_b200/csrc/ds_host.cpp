@@ -397,6 +397,12 @@ int ds_csr_scatter(int32_t n_sel, const int32_t *sel, const int32_t *src_off, co
   return DS_OK;
 }
 
+int ds_set_host_threads(int32_t n) {
+  if (n < 1) return DS_ERR_INVALID_ARG;
+  omp_set_num_threads(n);  // the calling thread's parallel regions (OpenMP nthreads-var is per thread)
+  return DS_OK;
+}
+
 int ds_default_table(int64_t seed, float *table) {
   if (!table) return DS_ERR_INVALID_ARG;
   Rng r((uint64_t)seed, kStreamTable, 0);

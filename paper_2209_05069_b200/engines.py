@@ -25,6 +25,7 @@ are fatal and re-raised from run().  There is no CPU execution path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import queue
 import threading
 import time
@@ -365,8 +366,12 @@ class batched_engine:  # noqa: N801
                         with lock:
                             errors.append((int(seq_of_row[i]), batch.ids[i], f"{exc.__name__}: {batch.ids[i]}: invalid"))
 
+            host_threads = max(1, (os.cpu_count() or 1) // workers)
+            ptime = [0.0, 0.0]   # producer seconds packing, uploading (summed over producers)
+
             def producer() -> None:
                 try:
+                    L.ds_set_host_threads(host_threads)   # the producers split the host cores
                     while not fatal:
                         with lock:
                             lo = nxt[0]
@@ -374,9 +379,15 @@ class batched_engine:  # noqa: N801
                         if lo >= n:
                             return
                         hi = min(n, lo + chunk)
+                        t_a = time.perf_counter()
                         pack_range(lo, hi)
+                        t_b = time.perf_counter()
                         for ds in dstreams.values():   # on the device before any of its ligands is pushed
                             ds.stream.upload(lo, hi, xyzt, fdesc, idh)
+                        t_c = time.perf_counter()
+                        with lock:
+                            ptime[0] += t_b - t_a
+                            ptime[1] += t_c - t_b
                         idx = np.arange(lo, hi, dtype=np.int32)
                         keys = rng_key[lo:hi]
                         if not valid[lo:hi].all():
@@ -443,6 +454,7 @@ class batched_engine:  # noqa: N801
                 t.join()
             t_flush = time.perf_counter()
             tm["produced"] = t_flush - t0
+            tm["producers_packing"], tm["producers_uploading"] = ptime
             for b in bucketizer.flush():           # end of stream: partial batches
                 dq.put(("flush", b, t_flush))
             for _ in disp:

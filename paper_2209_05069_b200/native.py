@@ -159,6 +159,7 @@ def lib():
             "ds_stream_upload": (C.c_int, [vp, i32, i32, vp, vp, vp]),
             "ds_stream_dock": (C.c_int, [vp, vp, vp, vp, i32, vp, vp]),
             "ds_stream_download": (C.c_int, [vp, vp, vp]),
+            "ds_set_host_threads": (C.c_int, [i32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

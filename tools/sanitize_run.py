@@ -38,3 +38,11 @@ kernels.apply_rigid(x, kernels.rot_x(30), np.zeros(3, np.float32))
 kernels.apply_torsion(x, frag, 72)
 kernels.bump_check(x, frag)
 print("sanitize run ok")
+
+# the batched engine's device-resident stream (ds_stream_*): producers, merged dispatches, download
+from paper_2209_05069_b200 import engines  # noqa: E402
+eb = io.generate_mixed_batch(600, seed=9)
+rep = engines.batched_engine.run(eb, io.synthetic_pocket(), model.DockConfig(), workers=2, table=table,
+                                 capacities={0: 64, 1: 48, 2: 32, 3: 16, 4: 8}, chunk=128)
+assert len(rep.results) + len(rep.errors) == eb.n
+print("engine stream ok")
