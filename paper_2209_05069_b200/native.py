@@ -25,14 +25,16 @@ LIB_PATH = os.environ.get("DOCKSCREEN_LIB") or os.path.join(_HERE, "libdockscree
 
 
 def source_sha16() -> str:
-    """sha256[:16] over the native sources and build recipe of libdockscreen.so (csrc/*, the C-ABI
-    header): the identity of the kernels a build contains.  nvcc's output is not byte-reproducible
-    (host object paths / temporaries), so profiles are tied to builds by this, not the .so bytes."""
+    """sha256[:16] over the CUDA sources and build recipe of libdockscreen.so (csrc/*.cu, *.cuh — the
+    kernels and their launch code — and the Makefile's flags; not the host-only helpers in
+    ds_host.cpp): the identity of the kernels a build contains.  nvcc's output is not
+    byte-reproducible (host object paths / temporaries), so profiles are tied to builds by this,
+    not by the .so bytes."""
     import hashlib
     h = hashlib.sha256()
     csrc = os.path.join(_HERE, "csrc")
-    files = sorted(f for f in os.listdir(csrc) if f.endswith((".cu", ".cuh", ".cpp", ".h")) or f == "Makefile")
-    for f in files + [os.path.join("..", "..", "include", "dockscreen.h")]:
+    files = sorted(f for f in os.listdir(csrc) if f.endswith((".cu", ".cuh")) or f == "Makefile")
+    for f in files:
         h.update(f.encode())
         with open(os.path.join(csrc, f), "rb") as fh:
             h.update(fh.read())
