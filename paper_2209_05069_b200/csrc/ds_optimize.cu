@@ -34,6 +34,9 @@ constexpr int kInline = 3;           // bump candidates kept inline per moving a
 constexpr int kOvf = 32;             // per-fragment overflow list of further (moving, candidate) pairs
 constexpr int kOptWarps = 8;         // warps per CTA of the select kernel (one ligand each)
 constexpr int kTorWarps = 8;         // warps per CTA of the torsion kernel (1-warp CTAs measured slower)
+#ifndef DS_SEL_MIN_BLOCKS
+#define DS_SEL_MIN_BLOCKS 4          // select: 4 x 8 warps resident (<= 64 registers)
+#endif
 #ifndef DS_OPT_MIN_BLOCKS
 #define DS_OPT_MIN_BLOCKS 4          // resident CTAs per SM the register budget is sized for
 #endif
@@ -55,8 +58,9 @@ struct TorWarpSmem {
   int mhit[32];             // early exit: per sweep lane, the moving slot of its bump (P14 row count)
 };
 
-// Per-warp header of the select/rescore kernel's scratch; K pose slots of slot_atoms float4 follow
-// (the kept poses and the candidate being replayed; .w = the atom's weight-table row offset)
+// Per-warp header of the select/rescore kernel's scratch; two pose slots of slot_atoms float4 follow
+// (the candidate being replayed and a kept pose replayed for an exact RMSD; .w = the atom's
+// weight-table row offset); cen[DS_MAX_RESTARTS] is the second slot's centroid scratch
 struct SelHdr {
   double cen[DS_MAX_RESTARTS + 1][3];  // heavy-atom coordinate sums of the slots (RMSD lower bound)
   int geom[DS_MAX_RESTARTS];
@@ -688,7 +692,11 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
 // pairs take the oracle's sequential f64 sum (one lane per kept pose).  The kept poses are then
 // rescored from their slots.  Nothing is read back from device memory but the inputs, the keys,
 // the torsion indices and the per-restart (geom, valid) words.
-__global__ void __launch_bounds__(kOptWarps * 32)
+// kMode: the rescore's binning / accumulator (one instantiation each, chosen at launch from the
+// pocket): 0 full-range bin table + int32 partials, 1 clamped table + int32, 2 compares + int32,
+// 3 compares + int64 (tables whose weights do not fit two terms in an int32)
+template <int kMode>
+__global__ void __launch_bounds__(kOptWarps * 32, DS_SEL_MIN_BLOCKS)
     k_select_batched(PocketView pk, BatchView bt, DockParams dp, const uint32_t *keys, OptOut out, int *queue,
                      int tables_bytes, int warp_bytes) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -768,12 +776,17 @@ __global__ void __launch_bounds__(kOptWarps * 32)
       }
     }
     __syncwarp();
-    // greedy keep (warp-uniform): replay each candidate into the next free slot
+    // greedy keep (warp-uniform): each candidate is replayed into the candidate slot; a kept pose
+    // is rescored at once (and its coordinates written out while it is the best so far), so only
+    // the kept poses' heavy-atom centroids stay — a kept pose the centroid bound cannot separate
+    // from a later candidate (rare) is replayed again into the second slot for the exact sum
     const double hh = (double)heavy * (double)heavy;
+    float4 *cand = slots, *xs = slots + dp.slot_atoms;
     int nk = 0;
+    long long best_chem = 0;
+    int best_r = -1;
     for (int o = 0; o < nvalid && nk < dp.K; ++o) {
       const int c = S.ord[o];
-      float4 *cand = slots + (size_t)nk * dp.slot_atoms;
       replay_pose(cand, S.cen[nk], pk, bt, dp, keys, out, lig, c, a0, A, f0, F, rowmul);
       bool close = false;  // kept poses the bound cannot separate from the candidate
       if (lane < nk) {
@@ -781,40 +794,49 @@ __global__ void __launch_bounds__(kOptWarps * 32)
                      dz = S.cen[nk][2] - S.cen[lane][2];
         close = !(heavy > 0 && dx * dx + dy * dy + dz * dz >= thr2_margin * hh);
       }
+      unsigned cm = __ballot_sync(kFull, close);
       bool dis = true;
-      if (close) dis = pose_pair_dissimilar(cand, slots + (size_t)lane * dp.slot_atoms, A, heavy, dp.thr2);
-      if (__all_sync(kFull, dis)) {
-        if (lane == 0) S.kept[nk] = (uint8_t)c;
-        ++nk;
+      while (cm && dis) {
+        const int k = __ffs(cm) - 1;
+        cm &= cm - 1;
+        replay_pose(xs, S.cen[DS_MAX_RESTARTS], pk, bt, dp, keys, out, lig, S.kept[k], a0, A, f0, F, rowmul);
+        int d = 1;
+        if (lane == 0) d = pose_pair_dissimilar(cand, xs, A, heavy, dp.thr2);
+        dis = __shfl_sync(kFull, d, 0) != 0;
       }
-      __syncwarp();
-    }
-    // ---- rescore kept poses (P11): exact fixed-point sum over (ligand atom, pocket atom) ----
-    long long best_chem = 0;
-    int best_r = -1, best_t = 0;
-    for (int t = 0; t < nk; ++t) {
-      const int r = S.kept[t];
-      const float4 *su = slots + (size_t)t * dp.slot_atoms;
+      if (!dis) continue;
+      if (lane == 0) S.kept[nk] = (uint8_t)c;
+      // ---- rescore the kept pose (P11): exact fixed-point sum over (ligand atom, pocket atom) ----
       // int32 partials when two weight terms fit (every default-like table), int64 otherwise
       long long acc;
-      if (pk.part_terms >= 2 && pk.lut_cap >= 0 && pk.lut_full)
-        acc = rescore_pose_x2<2, int>(su, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, pk.lut_shift,
-                                      pk.lut_cap, pk.part_terms / 2);
-      else if (pk.part_terms >= 2 && pk.lut_cap >= 0)
-        acc = rescore_pose_x2<1, int>(su, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, pk.lut_shift,
-                                      pk.lut_cap, pk.part_terms / 2);
-      else if (pk.part_terms >= 2)
-        acc = rescore_pose_x2<0, int>(su, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0, 0,
+      if (kMode == 0)
+        acc = rescore_pose_x2<2, int>(cand, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut,
+                                      pk.lut_shift, pk.lut_cap, pk.part_terms / 2);
+      else if (kMode == 1)
+        acc = rescore_pose_x2<1, int>(cand, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut,
+                                      pk.lut_shift, pk.lut_cap, pk.part_terms / 2);
+      else if (kMode == 2)
+        acc = rescore_pose_x2<0, int>(cand, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0, 0,
                                       pk.part_terms / 2);
       else
-        acc = rescore_pose_x2<0, long long>(su, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0, 0, A);
+        acc = rescore_pose_x2<0, long long>(cand, A, s_nx, s_ny, s_nz, s_col, nrounds, s_w, pk.nb, s_ub2, s_lut, 0,
+                                            0, A);
       acc = warp_sum64(acc);
-      if (best_r < 0 || acc > best_chem || (acc == best_chem && r < best_r)) {
+      if (best_r < 0 || acc > best_chem || (acc == best_chem && c < best_r)) {
         best_chem = acc;
-        best_r = r;
-        best_t = t;
+        best_r = c;
+        if (out.best_coords)
+          for (int i = lane; i < A; i += 32) {  // back to Å: q = fma(u, s, o)   (P2)
+            const float4 x = cand[i];
+            float *q = out.best_coords + 3 * (size_t)(a0 + i);
+            q[0] = __fmaf_rn(x.x, pk.spacing, pk.ox);
+            q[1] = __fmaf_rn(x.y, pk.spacing, pk.oy);
+            q[2] = __fmaf_rn(x.z, pk.spacing, pk.oz);
+          }
       }
-      if (lane == 0 && out.rrec) out.rrec[(size_t)lig * dp.N + r].kept = (uint8_t)(t + 1);
+      if (lane == 0 && out.rrec) out.rrec[(size_t)lig * dp.N + c].kept = (uint8_t)(nk + 1);
+      ++nk;
+      __syncwarp();
     }
     const unsigned bkey = keys[(size_t)lig * dp.N + best_r];
     const int brot = 65535 - (int)(bkey & 0xFFFFu);
@@ -826,16 +848,6 @@ __global__ void __launch_bounds__(kOptWarps * 32)
     res.best_ay = (uint8_t)(brot - (brot / dp.n_a) * dp.n_a);
     res.n_kept = (uint8_t)nk;
     if (lane == 0) out.res[lig] = res;
-    if (out.best_coords) {
-      const float4 *ub = slots + (size_t)best_t * dp.slot_atoms;
-      for (int i = lane; i < A; i += 32) {  // back to Å: q = fma(u, s, o)   (P2)
-        const float4 x = ub[i];
-        float *o = out.best_coords + 3 * (size_t)(a0 + i);
-        o[0] = __fmaf_rn(x.x, pk.spacing, pk.ox);
-        o[1] = __fmaf_rn(x.y, pk.spacing, pk.oy);
-        o[2] = __fmaf_rn(x.z, pk.spacing, pk.oz);
-      }
-    }
     if (out.best_tors)
       for (int f = lane; f < F; f += 32) out.best_tors[f0 + f] = out.rtors[(size_t)(f0 + f) * dp.N + best_r];
     __syncwarp();
@@ -848,8 +860,10 @@ static size_t select_tables_bytes(int n_patoms, int nb, int lut_cap) {
   return (fixed + 15) & ~(size_t)15;
 }
 static size_t select_warp_bytes(int K, int slot_atoms) {
-  // the candidate is replayed into slot nk < K, so K slots hold the kept poses and the candidate
-  return ((sizeof(SelHdr) + 15) & ~(size_t)15) + (size_t)K * slot_atoms * sizeof(float4);
+  // two pose slots: the candidate and the on-demand replay of a kept pose (kept poses are rescored
+  // when kept, so only their centroids stay)
+  (void)K;
+  return ((sizeof(SelHdr) + 15) & ~(size_t)15) + (size_t)2 * slot_atoms * sizeof(float4);
 }
 // dynamic shared memory of a k_select_batched CTA (kOptWarps warps) for top-K K and ligands of at
 // most slot_atoms atoms
@@ -881,16 +895,32 @@ void launch_torsion_batched(const PocketView &pk, const BatchView &bt, const Doc
 // warps per CTA (1..kOptWarps) chosen for the most resident warps per SM: every CTA carries its
 // own rescore tables beside its warps' pose slots (one warp always fits: 32 slots x 160 atoms x
 // 16 B + the tables)
+static int select_mode(const PocketView &pk) {
+  if (pk.part_terms >= 2 && pk.lut_cap >= 0 && pk.lut_full) return 0;
+  if (pk.part_terms >= 2 && pk.lut_cap >= 0) return 1;
+  return pk.part_terms >= 2 ? 2 : 3;
+}
+static const void *select_kernel(int mode) {
+  switch (mode) {
+    case 0: return (const void *)k_select_batched<0>;
+    case 1: return (const void *)k_select_batched<1>;
+    case 2: return (const void *)k_select_batched<2>;
+    default: return (const void *)k_select_batched<3>;
+  }
+}
+
 void launch_select_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const uint32_t *keys,
                            OptOut out, int *queue, int sm_count, size_t smem_optin, cudaStream_t st) {
+  const int mode = select_mode(pk);
+  const void *kern = select_kernel(mode);
   const size_t tb = select_tables_bytes(pk.n_atoms, pk.nb, pk.lut_cap), wb = select_warp_bytes(dp.K, dp.slot_atoms);
   int best_w = 1, best_res = 0, best_per_sm = 1;
   for (int w = 1; w <= kOptWarps; ++w) {
     const size_t smem = tb + w * wb;
     if (smem > smem_optin) break;
-    allow_max_smem((const void *)k_select_batched);
+    allow_max_smem(kern);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_batched, w * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, w * 32, smem);
     if (per_sm * w >= best_res) {
       best_res = per_sm * w;
       best_w = w;
@@ -898,8 +928,11 @@ void launch_select_batched(const PocketView &pk, const BatchView &bt, const Dock
     }
   }
   const size_t smem = tb + best_w * wb;
-  allow_max_smem((const void *)k_select_batched);
-  k_select_batched<<<sm_count * best_per_sm, best_w * 32, smem, st>>>(pk, bt, dp, keys, out, queue, (int)tb, (int)wb);
+  allow_max_smem(kern);
+  const int itb = (int)tb, iwb = (int)wb;
+  void *args[] = {(void *)&pk, (void *)&bt, (void *)&dp, (void *)&keys, (void *)&out, (void *)&queue, (void *)&itb,
+                  (void *)&iwb};
+  cudaLaunchKernel(kern, dim3(sm_count * best_per_sm), dim3(best_w * 32), args, smem, st);
 }
 
 int torsion_blocks_per_sm() {
@@ -911,8 +944,8 @@ int torsion_blocks_per_sm() {
 
 int select_blocks_per_sm(size_t smem) {
   int n = 0;
-  allow_max_smem((const void *)k_select_batched);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_select_batched, kOptWarps * 32, smem);
+  allow_max_smem((const void *)k_select_batched<0>);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_select_batched<0>, kOptWarps * 32, smem);
   return n;
 }
 
