@@ -249,3 +249,18 @@ def test_degenerate_axis_both_families(gpu_ctx, synth_pocket, table):
         g, o = _run(gpu_ctx, bad, synth_pocket, table, cfg, seed=1, family=fam)
         assert (o.results["status"][[1, 4, 6]] == native.STATUS_DEGENERATE_AXIS).all()
         compare(bad, g, o, cfg)
+
+
+@pytest.mark.parametrize("rmsd,k", [(4.0, 4), (15.0, 8), (40.0, 3), (15.0, 1)])
+def test_select_exact_rmsd_path(gpu_ctx, synth_pocket, table, rmsd, k):
+    """Large similarity thresholds: the centroid bound rarely separates poses, so most pairs take
+    the exact sequential RMSD (the kept pose replayed into the second slot) and many candidates are
+    rejected — both families against the oracle, every field."""
+    batch = io.generate_mixed_batch(80, seed=31)
+    cfg = model.DockConfig(restarts_n=8, rescore_top_k=k, similarity_rmsd=rmsd)
+    for fam in (FAMILY_BATCHED, FAMILY_LATENCY):
+        g, o = _run(gpu_ctx, batch, synth_pocket, table, cfg, seed=7, family=fam)
+        compare(batch, g, o, cfg)
+    kept = o.results["n_kept"][o.results["status"] == 0]
+    if rmsd >= 15.0 and k > 1:
+        assert (kept < k).any()   # the threshold rejects candidates: the exact path decided some
