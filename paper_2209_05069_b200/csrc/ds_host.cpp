@@ -100,21 +100,42 @@ int ds_generated_id(int64_t seed, int64_t index, char *buf, size_t cap) {
 
 // ids first_index .. first_index + count - 1 as one byte blob + offsets (off[count] = total):
 // with buf == NULL only the offsets are filled (size query); both passes OpenMP-parallel
+// "%lld" of v into out (no terminator); returns the length
+static int fmt_i64(int64_t v, char *out) {
+  char tmp[24];
+  int n = 0;
+  uint64_t u = v < 0 ? (uint64_t)0 - (uint64_t)v : (uint64_t)v;
+  do {
+    tmp[n++] = (char)('0' + u % 10u);
+    u /= 10u;
+  } while (u);
+  int k = 0;
+  if (v < 0) out[k++] = '-';
+  while (n) out[k++] = tmp[--n];
+  return k;
+}
+
+// "lig_<seed>_<index>" (the snprintf format of ds_generated_id) into out; returns the length
+static int fmt_generated_id(int64_t seed, int64_t index, char *out) {
+  memcpy(out, "lig_", 4);
+  int k = 4 + fmt_i64(seed, out + 4);
+  out[k++] = '_';
+  return k + fmt_i64(index, out + k);
+}
+
 int ds_generated_ids(int64_t seed, int64_t first_index, int32_t count, char *buf, int64_t *off) {
   if (count < 0 || !off) return DS_ERR_INVALID_ARG;
   std::vector<int32_t> len((size_t)count);
 #pragma omp parallel for schedule(static)
-  for (int32_t i = 0; i < count; ++i)
-    len[i] = snprintf(nullptr, 0, "lig_%lld_%lld", (long long)seed, (long long)(first_index + i));
+  for (int32_t i = 0; i < count; ++i) {
+    char tmp[64];
+    len[i] = fmt_generated_id(seed, first_index + i, tmp);
+  }
   off[0] = 0;
   for (int32_t i = 0; i < count; ++i) off[i + 1] = off[i] + len[i];
   if (buf) {
 #pragma omp parallel for schedule(static)
-    for (int32_t i = 0; i < count; ++i) {
-      char tmp[64];
-      snprintf(tmp, sizeof tmp, "lig_%lld_%lld", (long long)seed, (long long)(first_index + i));
-      memcpy(buf + off[i], tmp, (size_t)len[i]);
-    }
+    for (int32_t i = 0; i < count; ++i) fmt_generated_id(seed, first_index + i, buf + off[i]);
   }
   return DS_OK;
 }
