@@ -211,3 +211,20 @@ def test_batched_engine_concurrent_runs(synth_pocket, table):
         t.join()
     for k in range(2):
         assert np.array_equal(out[k].records["results"], solo[k])
+
+
+def test_batched_engine_nondefault_config_equals_ds_dock(synth_pocket, table):
+    """The engine stream with another restart count, top-K, angle steps and no early exit: the
+    records, poses and torsions equal one ds_dock of the whole batch."""
+    from paper_2209_05069_b200.native import Context, pack
+    b = io.generate_mixed_batch(2500, seed=26)
+    cfg = model.DockConfig(restarts_n=12, rescore_top_k=6, alignment_step_deg=10, torsion_step_deg=30,
+                           early_exit=False)
+    ctx = Context(0)
+    ref = ctx.dock(ctx.pocket(synth_pocket, table), pack(b), cfg, seed=3)
+    rep = engines.batched_engine.run(b, synth_pocket, cfg, seed=3, table=table, workers=3,
+                                     capacities={0: 300, 1: 200, 2: 100, 3: 60, 4: 20}, chunk=400)
+    rec = rep.records
+    assert np.array_equal(rec["results"], ref.results)
+    assert np.array_equal(rec["best_coords"][:len(ref.best_coords)], ref.best_coords)
+    assert np.array_equal(rec["best_torsion"][:len(ref.best_torsion)], ref.best_torsion)
