@@ -319,9 +319,11 @@ class batched_engine:  # noqa: N801
         bucketizer = Bucketizer(capacities)
         ao = np.ascontiguousarray(batch.atom_off, np.int32)
         fo = np.ascontiguousarray(batch.frag_off, np.int32)
-        dstreams = {d: _acquire_stream(d) for d in devices}
+        dstreams: Dict[int, _DeviceStream] = {}
         arena = _ARENA if _ARENA.lock.acquire(blocking=False) else _StreamArena()
         try:
+            for d in devices:   # inside the try: every stream taken is released below
+                dstreams[d] = _acquire_stream(d)
             for ds in dstreams.values():
                 ds.stream.begin(ao, fo, cfg.restarts_n)
             # the packed stream (pinned: uploaded by DMA) and the host copies of the outputs

@@ -148,3 +148,10 @@ def test_engine_ligandbatch_bad_rows_found_at_pack_time(fake_device):
     assert len(rep.results) == 297
     fs = fake_device.stream
     assert fs.docked.sum() == 297 and fs.docked[[0, 77, 299]].sum() == 0
+
+
+def test_engine_empty_stream(fake_device):
+    b = io.generate_mixed_batch(5, seed=2).slice(0, 0)
+    rep = engines.batched_engine.run(b, model.Pocket.__new__(model.Pocket), model.DockConfig(), workers=2)
+    assert len(rep.results) == 0 and rep.errors == [] and rep.dispatch_log == []
+    assert rep.counters.batches_dispatched == 0
