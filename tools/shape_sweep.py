@@ -20,6 +20,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2209_05069_b200 import io, model, native  # noqa: E402
+from bench import ClockSampler  # noqa: E402  (NVML clocks and throttle reasons while timing)
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--count", type=int, default=4096, help="ligands per shape cell")
@@ -49,6 +50,8 @@ def device_rate(batch, reps):
 
 
 os.makedirs(a.out, exist_ok=True)
+clk = ClockSampler(0)
+clk.__enter__()
 cells = [(h, f) for h in range(8, 41, 4) for f in (0, 1, 2, 4, 8, 12, 16, 20) if f < h - 1]
 classes = {"Small": (20, 1), "Medium": (35, 12), "Large": (50, 20)}
 rows = []
@@ -79,7 +82,9 @@ with open(os.path.join(a.out, "size_ladder.csv"), "w", newline="") as fh:
     w.writerow(["ligands", "batched_ligands_per_s", "latency_ligands_per_s", "batched_ms", "latency_ms"])
     w.writerows(lrows)
 
+clk.__exit__(None, None, None)
 summary = {"workload": "config4 shape sweep + size ladder, synthetic pocket, DockConfig defaults, device-timed",
+           "clocks": clk.summary(), "lib_src_sha16": native.source_sha16(),
            "count_per_cell": a.count,
            "classes": {r[2]: {"batched": r[4], "latency": r[5]} for r in rows if r[2]},
            "batched_over_latency_range": [min(r[6] for r in rows), max(r[6] for r in rows)],
