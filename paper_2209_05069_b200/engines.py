@@ -36,12 +36,11 @@ from typing import Dict, Iterable, List, Mapping, Optional, Sequence, Tuple, Uni
 import numpy as np
 
 from . import model
-from .bucketizer import Batch, BucketKey, Bucketizer, bucket_capacity, device_capacities
+from .bucketizer import BucketKey, Bucketizer, device_capacities
 from .docking import _pockets, thread_context
-from .native import (CHEM_SCALE, DS_OK, ERRORS, FAMILY_BATCHED, FAMILY_LATENCY, FRAG_WORDS, MASK_WORDS,
-                     RESULT_DTYPE, STATUS_DEGENERATE_AXIS, STATUS_NO_VALID_POSE, Context, DsError,
-                     EngineStream, GeneratedIds, InteractionTable, LigandBatch, PackedBatch, _p, check, lib, pack,
-                     pinned_empty, pooled_pinned_empty)
+from .native import (CHEM_SCALE, DS_OK, ERRORS, FAMILY_LATENCY, FRAG_WORDS, MASK_WORDS, RESULT_DTYPE,
+                     STATUS_DEGENERATE_AXIS, STATUS_NO_VALID_POSE, Context, DsError, EngineStream, GeneratedIds,
+                     InteractionTable, LigandBatch, _p, lib, pack, pinned_empty, pooled_pinned_empty)
 
 Stream = Union[LigandBatch, Iterable[model.Ligand]]
 
