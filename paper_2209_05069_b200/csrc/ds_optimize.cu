@@ -41,13 +41,14 @@ constexpr int kTorWarps = 8;         // warps per CTA of the torsion kernel (1-w
 #define DS_OPT_MIN_BLOCKS 4          // resident CTAs per SM the register budget is sized for
 #endif
 
-// Per-warp shared scratch of the torsion kernel (53 KB per 8-warp CTA: 4 CTAs per SM).
+// Per-warp shared scratch of the torsion kernel (39 KB per 8-warp CTA: 4 CTAs per SM, registers
+// bind; the rest of the SM's L1/shared array caches grid gathers).
 struct TorWarpSmem {
   float4 u[kMaxA];          // committed pose of the current restart (grid frame), .w = type
-  // moving atoms of the current fragment, ascending, as structure-of-arrays so that the two atoms a
-  // sweep lane takes per round (slots 2j, 2j+1) load as one f32x2 pair per coordinate; info word:
+  // moving atoms of the current fragment, ascending: their indices into u (a sweep lane takes slots
+  // 2j, 2j+1 and packs their coordinates into f32x2 pairs) and their info words (pairs):
   //   bits 0-7 bump-candidate count, 8-15 / 16-23 / 24-31 the first three candidates
-  f2_t mxp[kMaxA / 2 + 1], myp[kMaxA / 2 + 1], mzp[kMaxA / 2 + 1];
+  uint8_t mlist[kMaxA];
   uint2 mip[kMaxA / 2 + 1];
   // cylindrical (h, r) as two arrays (C' pairs load as f32x2): C' atoms in [0, nCf) (+ one far pad
   // entry), moving atom m at kMaxA-1-m
@@ -372,9 +373,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
             const float4 p = S.u[i];
             if (mv) {
               const int m = nM + __popc(bm & lt);
-              reinterpret_cast<float *>(S.mxp)[m] = p.x;
-              reinterpret_cast<float *>(S.myp)[m] = p.y;
-              reinterpret_cast<float *>(S.mzp)[m] = p.z;
+              S.mlist[m] = (uint8_t)i;
               reinterpret_cast<unsigned *>(S.mip)[m] = 0u;  // info word
             }
           }
@@ -411,8 +410,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         int hlo = 0x7FFFFFFF, hhi = (int)0x80000000, rhi = 0;
         if (lane == 0) S.n_ovf = 0;
         for (int m = lane; m < nM; m += 32) {
-          const float4 pm = make_float4(reinterpret_cast<const float *>(S.mxp)[m], reinterpret_cast<const float *>(S.myp)[m],
-                                        reinterpret_cast<const float *>(S.mzp)[m], 0.f);
+          const float4 pm = S.u[S.mlist[m]];
           const float2 hr = cyl_coords(pm, a3, kx, ky, kz);
           reinterpret_cast<float *>(S.chh2)[kMaxA - 1 - m] = hr.x;
           reinterpret_cast<float *>(S.chr2)[kMaxA - 1 - m] = hr.y;
@@ -550,7 +548,9 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
             if (act1) {
               const int j = m1 >> 1;
               // w = p - a (as p + (-a): exact negation), p' = R w + a (P8), then + magic (P4)
-              const f2_t WX = f2_add(S.mxp[j], NAX), WY = f2_add(S.myp[j], NAY), WZ = f2_add(S.mzp[j], NAZ);
+              const float4 p1 = S.u[S.mlist[m1]], p2 = S.u[S.mlist[act2 ? m2 : m1]];
+              const f2_t WX = f2_add(f2_pack(p1.x, p2.x), NAX), WY = f2_add(f2_pack(p1.y, p2.y), NAY),
+                         WZ = f2_add(f2_pack(p1.z, p2.z), NAZ);
               const f2_t QX = f2_fma(R2, WZ, f2_fma(R1, WY, f2_fma(R0, WX, AX)));
               const f2_t QY = f2_fma(R5, WZ, f2_fma(R4, WY, f2_fma(R3, WX, AY)));
               const f2_t QZ = f2_fma(R8, WZ, f2_fma(R7, WY, f2_fma(R6, WX, AZ)));
@@ -626,9 +626,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
             const unsigned bm = __ballot_sync(kFull, mv);
             if (mv) {
               const int m = mr + __popc(bm & lt);
-              const float4 W = make_float4(reinterpret_cast<const float *>(S.mxp)[m],
-                                           reinterpret_cast<const float *>(S.myp)[m],
-                                           reinterpret_cast<const float *>(S.mzp)[m], 0.f);
+              const float4 W = S.u[i];  // not yet moved: the committed pose's position
               const float3 q = torsion_pos(pk, kNT ? 360 / kNT : dp.step_t, best_k, kx, ky, kz, a3, W);
               S.u[i] = make_float4(q.x, q.y, q.z, S.u[i].w);
             }
