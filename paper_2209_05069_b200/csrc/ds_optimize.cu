@@ -41,15 +41,15 @@ constexpr int kTorWarps = 8;         // warps per CTA of the torsion kernel (1-w
 #define DS_OPT_MIN_BLOCKS 4          // resident CTAs per SM the register budget is sized for
 #endif
 
-// Per-warp shared scratch of the torsion kernel (39 KB per 8-warp CTA: 4 CTAs per SM, registers
+// Per-warp shared scratch of the torsion kernel (34 KB per 8-warp CTA: 4 CTAs per SM, registers
 // bind; the rest of the SM's L1/shared array caches grid gathers).
 struct TorWarpSmem {
-  float4 u[kMaxA];          // committed pose of the current restart (grid frame), .w = type
+  float4 u[kMaxA];          // committed pose of the current restart (grid frame), .w: see mlist
   // moving atoms of the current fragment, ascending: their indices into u (a sweep lane takes slots
-  // 2j, 2j+1 and packs their coordinates into f32x2 pairs) and their info words (pairs):
-  //   bits 0-7 bump-candidate count, 8-15 / 16-23 / 24-31 the first three candidates
+  // 2j, 2j+1 and packs their coordinates into f32x2 pairs); a moving atom's u[i].w holds its info
+  // word for the fragment: bits 0-7 bump-candidate count, 8-15 / 16-23 / 24-31 the first three
+  // candidates
   uint8_t mlist[kMaxA];
-  uint2 mip[kMaxA / 2 + 1];
   // cylindrical (h, r) as two arrays (C' pairs load as f32x2): C' atoms in [0, nCf) (+ one far pad
   // entry), moving atom m at kMaxA-1-m
   f2_t chh2[kMaxA / 2], chr2[kMaxA / 2];
@@ -369,14 +369,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           const bool mv = in && ((mw5[s] >> lane) & 1u);
           const bool cp = in && !mv && i != ab && i != ae;
           const unsigned bm = __ballot_sync(kFull, mv), bc = __ballot_sync(kFull, cp);
-          if (in) {
-            const float4 p = S.u[i];
-            if (mv) {
-              const int m = nM + __popc(bm & lt);
-              S.mlist[m] = (uint8_t)i;
-              reinterpret_cast<unsigned *>(S.mip)[m] = 0u;  // info word
-            }
-          }
+          if (mv) S.mlist[nM + __popc(bm & lt)] = (uint8_t)i;
           if (cp) S.clist[nC + __popc(bc & lt)] = (uint8_t)i;
           nM += __popc(bm);
           nC += __popc(bc);
@@ -481,7 +474,9 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
               }
             }
           }
-          if (ok) reinterpret_cast<unsigned *>(S.mip)[m] = cnt | inl;  // cnt <= nCf < 256
+          // the info word rides in the moving atom's .w (unused by the torsion kernel otherwise), so
+          // the sweep gets it with the atom's position load
+          if (ok) reinterpret_cast<unsigned *>(&S.u[S.mlist[m]])[3] = cnt | inl;  // cnt <= nCf < 256
         }
         unsigned best_key = 0;  // (score + 32768) << 16 | (65535 - angle); 0 = no clean angle
         __syncwarp();
@@ -565,7 +560,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
               f2_unpack(QX, q1.x, q2.x);
               f2_unpack(QY, q1.y, q2.y);
               f2_unpack(QZ, q1.z, q2.z);
-              const uint2 info = S.mip[j];
+              const uint2 info = make_uint2(__float_as_uint(p1.w), __float_as_uint(p2.w));
               const bool h1 = bump_hit(S, info.x, q1, m1, n_ovf, nCf, dp.bd2);
               const bool h2 = act2 && bump_hit(S, info.y, q2, m2, n_ovf, nCf, dp.bd2);
               part += gv1 + (act2 ? gv2 : 0);  // a bumped angle's sum is never used
