@@ -41,19 +41,21 @@ constexpr int kTorWarps = 8;         // warps per CTA of the torsion kernel (1-w
 #define DS_OPT_MIN_BLOCKS 4          // resident CTAs per SM the register budget is sized for
 #endif
 
-// Per-warp shared scratch of the torsion kernel (34 KB per 8-warp CTA: 4 CTAs per SM, registers
-// bind; the rest of the SM's L1/shared array caches grid gathers).
+// Per-warp shared scratch of the torsion kernel (34 KB per 8-warp CTA at MA = 160, 28 KB at 128,
+// 15 KB at 64: 4 CTAs per SM, registers bind; the rest of the SM's L1/shared array caches the grid
+// gathers, so the launch takes the smallest MA that holds its largest ligand).
+template <int MA>  // MA: the largest ligand the launch may hold (a multiple of 32, <= kMaxA)
 struct TorWarpSmem {
-  float4 u[kMaxA];          // committed pose of the current restart (grid frame), .w: see mlist
+  float4 u[MA];          // committed pose of the current restart (grid frame), .w: see mlist
   // moving atoms of the current fragment, ascending: their indices into u (a sweep lane takes slots
   // 2j, 2j+1 and packs their coordinates into f32x2 pairs); a moving atom's u[i].w holds its info
   // word for the fragment: bits 0-7 bump-candidate count, 8-15 / 16-23 / 24-31 the first three
   // candidates
-  uint8_t mlist[kMaxA];
+  uint8_t mlist[MA];
   // cylindrical (h, r) as two arrays (C' pairs load as f32x2): C' atoms in [0, nCf) (+ one far pad
-  // entry), moving atom m at kMaxA-1-m
-  f2_t chh2[kMaxA / 2], chr2[kMaxA / 2];
-  uint8_t clist[kMaxA];     // complement atom indices, ascending
+  // entry), moving atom m at MA-1-m
+  f2_t chh2[MA / 2], chr2[MA / 2];
+  uint8_t clist[MA];     // complement atom indices, ascending
   uint16_t ovf[kOvf];       // candidates beyond kInline: moving slot << 8 | atom index
   int n_ovf;                // entries appended (> kOvf: the list overflowed, scan C')
   int mhit[32];             // early exit: per sweep lane, the moving slot of its bump (P14 row count)
@@ -240,7 +242,8 @@ __device__ __noinline__ bool pose_pair_dissimilar(const float4 *up, const float4
 
 // minimum squared distance from q to the bump candidates of moving slot m beyond the inline ones:
 // the fragment's overflow list, or every prefiltered C' atom when that list overflowed (cold path)
-__device__ __forceinline__ float overflow_min(const TorWarpSmem &S, int m, int n_ovf, int nCf, float3 q) {
+template <typename SM>
+__device__ __forceinline__ float overflow_min(const SM &S, int m, int n_ovf, int nCf, float3 q) {
   float mind = __int_as_float(0x7f800000);
   if (n_ovf <= kOvf) {
 #pragma unroll 1
@@ -263,7 +266,8 @@ __device__ __forceinline__ float overflow_min(const TorWarpSmem &S, int m, int n
 
 // P9 bump test of a rotated moving atom q against its candidates (info word of its record):
 // true iff some candidate lies strictly closer than the bump distance
-__device__ __forceinline__ bool bump_hit(const TorWarpSmem &S, unsigned info, float3 q, int m, int n_ovf, int nCf,
+template <typename SM>
+__device__ __forceinline__ bool bump_hit(const SM &S, unsigned info, float3 q, int m, int n_ovf, int nCf,
                                          float bd2) {
   const unsigned cnt = info & 0xFFu;
   if (cnt == 0u) return false;
@@ -300,15 +304,15 @@ __device__ __noinline__ void clear_unreached(const OptOut &out, int N, int f0, i
 
 // kEarly: DockConfig.early_exit; kNT: the torsion angle count when it is the default
 // 10 (torsion_step_deg = 36: the sweep's lane layout and loops become constants), 0 = runtime
-template <bool kEarly, int kNT>
+template <bool kEarly, int kNT, int MA>
 __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
     k_torsion_batched(PocketView pk, BatchView bt, DockParams dp, const int *order, const uint32_t *keys,
                       OptOut out, int *queue) {
   // per-warp scratch at a compile-time offset of the shared window (nothing to rematerialise from
   // launch parameters); dynamic because it exceeds the 48 KB static limit
-  extern __shared__ __align__(16) TorWarpSmem s_warp[];
+  extern __shared__ __align__(16) unsigned char s_tor[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  TorWarpSmem &S = s_warp[warp];
+  TorWarpSmem<MA> &S = reinterpret_cast<TorWarpSmem<MA> *>(s_tor)[warp];
   const GridGeom g = pk.g;
   const unsigned lt = lanemask_lt();
 
@@ -392,7 +396,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         }
         __syncwarp();
         // ---- bump candidates per moving atom: cylindrical coordinates of C' in chr[0, nC) and of M
-        // in chr[kMaxA-1-m] (nM + nC <= A - 2), then every (m, c) pair tested by a flat lane loop;
+        // in chr[MA-1-m] (nM + nC <= A - 2), then every (m, c) pair tested by a flat lane loop;
         // survivors are counted into the moving atom's info word, the first kInline of them are kept
         // inline and the rest go to a short per-fragment overflow list (their order is irrelevant:
         // only the minimum distance is used).
@@ -405,8 +409,8 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         for (int m = lane; m < nM; m += 32) {
           const float4 pm = S.u[S.mlist[m]];
           const float2 hr = cyl_coords(pm, a3, kx, ky, kz);
-          reinterpret_cast<float *>(S.chh2)[kMaxA - 1 - m] = hr.x;
-          reinterpret_cast<float *>(S.chr2)[kMaxA - 1 - m] = hr.y;
+          reinterpret_cast<float *>(S.chh2)[MA - 1 - m] = hr.x;
+          reinterpret_cast<float *>(S.chr2)[MA - 1 - m] = hr.y;
           hlo = min(hlo, ordered_bits(hr.x));
           hhi = max(hhi, ordered_bits(hr.x));
           rhi = max(rhi, __float_as_int(hr.y));  // r >= +0: bit order is float order
@@ -436,7 +440,7 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
           }
           nCf += __popc(bk);
         }
-        // far pad after the last C' entry (slot nCf < kMaxA - nM since nCf + nM <= A - 2): an odd
+        // far pad after the last C' entry (slot nCf < MA - nM since nCf + nM <= A - 2): an odd
         // nCf still tests whole f32x2 pairs and the pad never passes the bound
         if (lane == 0) {
           reinterpret_cast<float *>(S.chh2)[nCf] = 3.0e38f;
@@ -448,8 +452,8 @@ __global__ void __launch_bounds__(kTorWarps * 32, DS_OPT_MIN_BLOCKS)
         for (int m0 = 0; m0 < nM; m0 += 32) {
           const int m = m0 + lane;
           const bool ok = m < nM;
-          const float hmh = ok ? reinterpret_cast<const float *>(S.chh2)[kMaxA - 1 - m] : 3.0e38f;
-          const float hmr = ok ? reinterpret_cast<const float *>(S.chr2)[kMaxA - 1 - m] : 3.0e38f;
+          const float hmh = ok ? reinterpret_cast<const float *>(S.chh2)[MA - 1 - m] : 3.0e38f;
+          const float hmr = ok ? reinterpret_cast<const float *>(S.chr2)[MA - 1 - m] : 3.0e38f;
           const f2_t HM = f2_pack(hmh, hmh), RM = f2_pack(hmr, hmr);
           unsigned cnt = 0, inl = 0;
           // two C' atoms per iteration with packed f32x2 (the bound is conservative, so any rounding
@@ -864,24 +868,34 @@ size_t select_cta_smem_bytes(int n_patoms, int nb, int lut_cap, int K, int slot_
   return select_tables_bytes(n_patoms, nb, lut_cap) + kOptWarps * select_warp_bytes(K, slot_atoms);
 }
 
-constexpr size_t kTorSmem = kTorWarps * sizeof(TorWarpSmem);
+template <int MA>
+constexpr size_t tor_smem() { return kTorWarps * sizeof(TorWarpSmem<MA>); }
 
-template <bool E, int NT>
+template <bool E, int NT, int MA>
 static void launch_tors(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                         const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st) {
-  allow_max_smem((const void *)k_torsion_batched<E, NT>);
-  k_torsion_batched<E, NT><<<blocks, kTorWarps * 32, kTorSmem, st>>>(pk, bt, dp, order, keys, out, queue);
+  allow_max_smem((const void *)k_torsion_batched<E, NT, MA>);
+  k_torsion_batched<E, NT, MA><<<blocks, kTorWarps * 32, tor_smem<MA>(), st>>>(pk, bt, dp, order, keys, out, queue);
+}
+
+// the scratch class of the launch: the smallest MA holding its largest ligand (dp.slot_atoms)
+template <bool E, int NT>
+static void launch_tors_ma(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
+                           const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st) {
+  if (NT && dp.slot_atoms <= 64) launch_tors<E, NT, 64>(pk, bt, dp, order, keys, out, queue, blocks, st);
+  else if (NT && dp.slot_atoms <= 128) launch_tors<E, NT, 128>(pk, bt, dp, order, keys, out, queue, blocks, st);
+  else launch_tors<E, NT, kMaxA>(pk, bt, dp, order, keys, out, queue, blocks, st);
 }
 
 void launch_torsion_batched(const PocketView &pk, const BatchView &bt, const DockParams &dp, const int *order,
                             const uint32_t *keys, OptOut out, int *queue, int blocks, cudaStream_t st) {
   const bool nt10 = dp.n_t == 10;
   if (dp.early_exit) {
-    if (nt10) launch_tors<true, 10>(pk, bt, dp, order, keys, out, queue, blocks, st);
-    else launch_tors<true, 0>(pk, bt, dp, order, keys, out, queue, blocks, st);
+    if (nt10) launch_tors_ma<true, 10>(pk, bt, dp, order, keys, out, queue, blocks, st);
+    else launch_tors_ma<true, 0>(pk, bt, dp, order, keys, out, queue, blocks, st);
   } else {
-    if (nt10) launch_tors<false, 10>(pk, bt, dp, order, keys, out, queue, blocks, st);
-    else launch_tors<false, 0>(pk, bt, dp, order, keys, out, queue, blocks, st);
+    if (nt10) launch_tors_ma<false, 10>(pk, bt, dp, order, keys, out, queue, blocks, st);
+    else launch_tors_ma<false, 0>(pk, bt, dp, order, keys, out, queue, blocks, st);
   }
 }
 
@@ -930,8 +944,9 @@ void launch_select_batched(const PocketView &pk, const BatchView &bt, const Dock
 
 int torsion_blocks_per_sm() {
   int n = 0;
-  allow_max_smem((const void *)k_torsion_batched<true, 10>);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_torsion_batched<true, 10>, kTorWarps * 32, kTorSmem);
+  allow_max_smem((const void *)k_torsion_batched<true, 10, kMaxA>);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_torsion_batched<true, 10, kMaxA>, kTorWarps * 32,
+                                                tor_smem<kMaxA>());
   return n;
 }
 
