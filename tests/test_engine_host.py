@@ -65,8 +65,11 @@ class FakeDispatcher:
 @pytest.fixture
 def fake_device(monkeypatch):
     dev = FakeDevStream()
-    dev.lock.acquire()
-    monkeypatch.setattr(engines, "_acquire_stream", lambda d: dev)
+
+    def acquire(d):   # as engines._acquire_stream: the run holds the stream's lock until it ends
+        dev.lock.acquire()
+        return dev
+    monkeypatch.setattr(engines, "_acquire_stream", acquire)
     slots = {}
     monkeypatch.setattr(engines, "_dispatcher", lambda d, k: slots.setdefault((d, k), FakeDispatcher(d)))
     monkeypatch.setattr(engines._pockets, "get", lambda ctx, pocket, table: None)
@@ -155,3 +158,30 @@ def test_engine_empty_stream(fake_device):
     rep = engines.batched_engine.run(b, model.Pocket.__new__(model.Pocket), model.DockConfig(), workers=2)
     assert len(rep.results) == 0 and rep.errors == [] and rep.dispatch_log == []
     assert rep.counters.batches_dispatched == 0
+
+
+def test_engine_dispatch_invariants_random_configs(fake_device):
+    """Random capacities, chunk sizes, worker / dispatcher counts and merge limits: every ligand is
+    docked exactly once, full batches have exactly their capacity, at most one flushed partial per
+    bucket comes last, and the observed counters match the log."""
+    rng = np.random.default_rng(5)
+    b = io.generate_mixed_batch(1500, seed=19)
+    for _ in range(6):
+        caps = {r: int(rng.integers(1, 120)) for r in range(5)}
+        rep = engines.batched_engine.run(b, model.Pocket.__new__(model.Pocket), model.DockConfig(),
+                                         workers=int(rng.integers(1, 5)), capacities=caps,
+                                         dispatchers_per_device=int(rng.integers(1, 4)),
+                                         chunk=int(rng.integers(16, 700)), merge_ligands=int(rng.integers(1, 800)))
+        fs = fake_device.stream
+        assert (fs.docked == 1).all()
+        per = {}
+        for e in rep.dispatch_log:
+            per.setdefault(e["key"], []).append(e)
+        for key, es in per.items():
+            es.sort(key=lambda e: e["detached"])
+            kinds = [e["kind"] for e in es]
+            assert kinds.count("flush") <= 1 and (kinds[-1] == "flush" or "flush" not in kinds)
+            assert all(e["size"] == caps[key[0]] for e in es if e["kind"] == "full")
+            assert all(0 < e["size"] <= caps[key[0]] for e in es)
+        assert rep.counters.batches_dispatched == len(rep.dispatch_log)
+        assert abs(rep.counters.batch_fill_ratio_sum - sum(e["size"] / e["capacity"] for e in rep.dispatch_log)) < 1e-9
